@@ -1,0 +1,222 @@
+/*
+ * superneuro_mat.h -- C ABI of the B200-native MAT-mode simulation engine.
+ *
+ * Drop-in boundary for the reference's MAT path (SuperNeuro MAT mode as
+ * implemented by spikeforge, /root/reference/proj).  Plain pointers and sizes
+ * only; no exceptions cross this boundary.  Each entry point names the
+ * reference interface it replaces.
+ *
+ *   reference (C++, proj/include/spikeforge/...)         this ABI
+ *   ---------------------------------------------------  ----------------------------
+ *   NeuronParams push (model.hpp:20-29)                   sn_add_neurons
+ *   SynapseDef push (model.hpp:31-39)                     sn_add_synapses
+ *   StimulusEntry push (model.hpp:53-63)                  sn_add_stimulus
+ *   StdpConfig (model.hpp:67-78), defaults (model.cpp:10-22)
+ *                                                         sn_set_stdp, sn_stdp_defaults
+ *   WeightStorage Auto/Dense/Sparse (mat_engine.hpp:16)   sn_options.storage
+ *   mat_init (mat_engine.hpp:89-90, mat_engine.cpp:109-166)
+ *                                                         sn_setup
+ *   mat_step + apply_stdp loop of mat_run
+ *     (mat_engine.hpp:92-103, mat_engine.cpp:168-287)     sn_simulate
+ *   RunResult.raster (model.hpp:87-104)                   sn_raster_size / sn_get_raster
+ *   RunResult.membrane_trace                              sn_get_membrane_trace
+ *   MatState.membrane (mat_engine.hpp:56-58)              sn_get_membrane
+ *   WeightMatrix::slot_get(slot(s)) (mat_engine.hpp:37-39)
+ *                                                         sn_get_synapse_weights
+ *   erdos_renyi (netgen.hpp:31-34, netgen.cpp:19-54)      sn_generate_erdos_renyi
+ *   std::invalid_argument / std::logic_error messages     sn_status + sn_last_error()
+ *
+ * Unlike mat_init (mat_engine.cpp:114-131), delays > 1 and axonal delays are
+ * accepted and simulated natively (ring of spike-history bits) with the
+ * timing of lower_delays + mat_run (lowering.cpp:22-59, oracle.cpp:91-95).
+ *
+ * Threading: one host thread drives one engine (MatState is not thread-safe
+ * either); distinct engines are independent.
+ */
+#ifndef SUPERNEURO_MAT_H
+#define SUPERNEURO_MAT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SN_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SN_API __attribute__((visibility("default")))
+#else
+#define SN_API
+#endif
+
+typedef struct sn_engine sn_engine;
+
+typedef enum sn_status {
+    SN_OK = 0,
+    SN_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+    SN_ERR_LOGIC = 2,            /* reference: std::logic_error (misuse/order) */
+    SN_ERR_CUDA = 3,
+    SN_ERR_NCCL = 4,
+    SN_ERR_OOM = 5,
+    SN_ERR_UNSUPPORTED = 6
+} sn_status;
+
+typedef enum sn_storage {
+    SN_STORAGE_AUTO = 0,   /* dense when the N x N_local fp32 matrix is small or dense enough */
+    SN_STORAGE_DENSE = 1,  /* row-major W[pre][post], pre-major like mat_engine.cpp:34-38 */
+    SN_STORAGE_SPARSE = 2  /* post-major blocked CSC, spike-history pull */
+} sn_storage;
+
+typedef enum sn_precision {
+    SN_WEIGHTS_F32 = 0,    /* fp32 weight storage (HBM traffic 4 B/synapse) */
+    SN_WEIGHTS_F64 = 1     /* fp64 storage + fp64 STDP arithmetic (bit-exact weights) */
+} sn_precision;
+
+typedef struct sn_options {
+    int32_t abi_version;     /* = SN_ABI_VERSION */
+    int32_t device;          /* CUDA ordinal */
+    int32_t storage;         /* sn_storage */
+    int32_t precision;       /* sn_precision */
+    int32_t exact_order;     /* 1: each post accumulates its inputs sequentially in
+                                ascending pre order starting from leak(v), as
+                                mat_engine.cpp:173-180 does (bit-exact membranes on
+                                float nets; slower).  0: fixed-order parallel
+                                reduction (deterministic; exact on integer nets). */
+    int32_t record_membrane; /* SimulationConfig::record_membrane */
+    int32_t stream_io;       /* 1: per-step H2D of the step's stimulus and D2H of the
+                                step's spike bits through pinned host buffers (the
+                                end-to-end path).  0: stimulus table resident in HBM,
+                                raster kept in HBM until sn_get_raster. */
+    int32_t use_graphs;      /* 1: replay the per-step kernels as a CUDA graph */
+    int32_t rank;            /* post-neuron partition index (0 when world == 1) */
+    int32_t world;           /* number of partitions / GPUs (1 = single GPU) */
+    int32_t profile;         /* 1: time every kernel with CUDA events (sn_get_stats) */
+    int32_t reserved[5];
+} sn_options;
+
+typedef struct sn_stats {
+    int64_t steps_done;
+    int64_t spike_count;        /* spikes of this partition since setup */
+    int64_t kernel_launches;    /* kernels launched by the engine since setup */
+    int64_t synapses_local;     /* synapses stored on this partition */
+    int32_t dense;              /* 1 dense storage, 0 sparse */
+    int32_t n_local;            /* posts owned by this partition */
+    int32_t first_local;        /* first owned global id */
+    int32_t max_delay;
+    /* profile (opts.profile == 1): accumulated device time per kernel class */
+    double sweep_ms;            /* propagation (+ STDP) sweep over the weights */
+    int64_t sweep_launches;
+    double neuron_ms;           /* LIF update (+ history/traces) */
+    int64_t neuron_launches;
+    double exchange_ms;         /* spike-bit all-gather */
+    double last_simulate_ms;    /* device time of the last sn_simulate (events) */
+    double sweep_bytes_per_launch_last; /* algorithmic bytes of the last sweep */
+    double sweep_bytes_total;   /* algorithmic bytes of all sweeps since reset */
+} sn_stats;
+
+/* ---- lifecycle ---------------------------------------------------------- */
+SN_API sn_status sn_options_init(sn_options* opts);
+SN_API sn_status sn_engine_create(const sn_options* opts, sn_engine** out);
+SN_API void sn_engine_destroy(sn_engine* e);
+/* Thread-local message of the last failing call on this thread ("" if none). */
+SN_API const char* sn_last_error(void);
+SN_API int32_t sn_abi_version(void);
+SN_API int32_t sn_device_count(void);
+
+/* ---- model building (before sn_setup) ----------------------------------- */
+/* Appends `count` neurons; ids continue from the current count.  axonal_delay
+ * may be NULL (all 0).  first_id may be NULL. */
+SN_API sn_status sn_add_neurons(sn_engine* e, int64_t count, const double* threshold,
+                         const double* leak, const double* reset,
+                         const int32_t* refractory, const int32_t* axonal_delay,
+                         int64_t* first_id);
+/* Appends synapses in list order (the order sn_get_synapse_weights reports).
+ * delay and stdp_enabled may be NULL (1 / not plastic). */
+SN_API sn_status sn_add_synapses(sn_engine* e, int64_t count, const int32_t* pre,
+                          const int32_t* post, const double* weight,
+                          const int32_t* delay, const uint8_t* stdp_enabled);
+/* Appends stimulus entries (any order; list order matters for float sums). */
+SN_API sn_status sn_add_stimulus(sn_engine* e, int64_t count, const int32_t* step,
+                          const int32_t* neuron, const double* amplitude);
+/* Replaces the stimulus schedule (allowed after setup, between simulate calls). */
+SN_API sn_status sn_clear_stimulus(sn_engine* e);
+/* Enables windowed pairwise STDP (mat_engine.cpp:210-250). */
+SN_API sn_status sn_set_stdp(sn_engine* e, int32_t window, const double* a_plus,
+                      const double* a_minus, double w_min, double w_max);
+/* StdpConfig::defaults() (model.cpp:10-22); a_plus/a_minus need `*window`
+ * (20) slots; pass NULL to query the window only. */
+SN_API sn_status sn_stdp_defaults(int32_t* window, double* a_plus, double* a_minus,
+                           double* w_min, double* w_max);
+
+/* On-device Erdos-Renyi network, bit-identical to erdos_renyi(n, p, seed)
+ * (netgen.cpp:19-54: pair (i,j), i != j, exists iff unit_at(i*n+j) < p on
+ * stream 1; thr 1, leak 0, reset 0, refr 0, weight 1, delay 1).  Replaces any
+ * neurons/synapses added so far.  Optional variations:
+ *   weight            weight of every synapse
+ *   delay_max > 1     delay = 1 + RandomStream(seed, delay_stream).below_at(key, delay_max)
+ *                     key = synapse list index when delay_by_synapse_index
+ *                     (only for p == 1) else pair index i*n + j
+ *   stdp_enabled      all synapses plastic
+ * Synapse list order = the reference's (i ascending, j ascending). */
+SN_API sn_status sn_generate_erdos_renyi(sn_engine* e, int32_t n, double p, uint64_t seed,
+                                  double weight, int32_t delay_max,
+                                  uint64_t delay_stream, int32_t delay_by_synapse_index,
+                                  int32_t stdp_enabled);
+
+/* ---- mat_init / mat_run ------------------------------------------------- */
+/* Validates (reference messages, model.cpp:34-117) and builds device state. */
+SN_API sn_status sn_setup(sn_engine* e);
+/* Advances `steps` steps (continuing from the current step). */
+SN_API sn_status sn_simulate(sn_engine* e, int32_t steps);
+/* Blocks until all queued device work of the engine is done. */
+SN_API sn_status sn_synchronize(sn_engine* e);
+
+/* ---- results ------------------------------------------------------------ */
+/* Spike events of this partition since setup, (step, neuron) ascending. */
+SN_API sn_status sn_raster_size(sn_engine* e, int64_t* events);
+SN_API sn_status sn_get_raster(sn_engine* e, int32_t* steps, int32_t* neurons, int64_t capacity);
+/* Drops the host raster accumulated so far (long runs). */
+SN_API sn_status sn_clear_raster(sn_engine* e);
+/* Final membrane of this partition's neurons (n_local doubles, fp64). */
+SN_API sn_status sn_get_membrane(sn_engine* e, double* out, int64_t count);
+/* membrane_trace rows (one per simulated step) x n_local. */
+SN_API sn_status sn_membrane_trace_rows(sn_engine* e, int64_t* rows);
+SN_API sn_status sn_get_membrane_trace(sn_engine* e, double* out, int64_t count);
+/* Current weight of every synapse added with sn_add_synapses, in list order
+ * (fp64; fp32 storage is widened).  Partitioned engines report 0 for
+ * synapses whose post they do not own. */
+SN_API sn_status sn_get_synapse_weights(sn_engine* e, double* out, int64_t count);
+/* Dense export of this partition's weight block W[pre][post_local]
+ * (n x n_local doubles) -- absent synapses read 0 (test/debug helper). */
+SN_API sn_status sn_get_weight_matrix(sn_engine* e, double* out, int64_t count);
+SN_API sn_status sn_get_stats(sn_engine* e, sn_stats* out);
+SN_API sn_status sn_reset_stats(sn_engine* e);
+
+/* ---- multi-GPU (post-neuron partitioning) -------------------------------- */
+/* Size of an NCCL unique id (128). */
+SN_API int32_t sn_comm_id_size(void);
+/* rank 0 creates the id; the host broadcasts it (e.g. torch.distributed). */
+SN_API sn_status sn_comm_create_id(uint8_t* id_out);
+/* Joins the NCCL communicator; sn_simulate then all-gathers the spike
+ * bitmask once per step (in-place ncclAllGather of n/8 bytes). */
+SN_API sn_status sn_comm_init(sn_engine* e, const uint8_t* id, int32_t rank, int32_t world);
+/* Host-driven exchange (used to emulate partitions on one GPU and by tests):
+ * sn_step_local runs the LIF update of one step and leaves this partition's
+ * spike words in its bitmask slice; the host copies every partition's slice
+ * into every other partition's full bitmask with sn_put_spike_words, then
+ * sn_step_finish runs history/traces and the sweep. */
+SN_API sn_status sn_partition_range(int32_t n, int32_t rank, int32_t world, int32_t* first,
+                             int32_t* count);
+SN_API sn_status sn_step_local(sn_engine* e);
+SN_API sn_status sn_get_spike_words(sn_engine* e, uint32_t* out, int64_t words);
+SN_API sn_status sn_put_spike_words(sn_engine* e, int32_t first_word, const uint32_t* words,
+                             int64_t count);
+SN_API sn_status sn_step_finish(sn_engine* e);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SUPERNEURO_MAT_H */

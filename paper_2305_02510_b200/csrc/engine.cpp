@@ -1,0 +1,1113 @@
+// Host side of the B200 MAT engine: validation with the reference's messages,
+// device layout construction, the per-step launch sequence, results.
+//
+// Reference anchors:
+//   validate_network / validate_stimulus / validate_stdp   proj/src/model.cpp:34-117
+//   mat_init (SoA fill, weight build, stdp list)           proj/src/mat_engine.cpp:109-166
+//   mat_run loop (stimulus, step, stdp, raster)            proj/src/mat_engine.cpp:252-287
+#include "engine.hpp"
+
+#include "nccl_dl.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <sstream>
+#include <unordered_set>
+
+namespace snb {
+
+void cuda_check(cudaError_t err, const char* what) {
+    if (err == cudaSuccess) return;
+    if (err == cudaErrorMemoryAllocation)
+        throw OutOfMemory(std::string("out of device memory in ") + what);
+    throw CudaError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(err));
+}
+
+void DevBuf::alloc(size_t b) {
+    release();
+    if (b == 0) b = 16;
+    cuda_check(cudaMalloc(&p, b), "cudaMalloc");
+    bytes = b;
+}
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+}
+void HostBuf::reserve(size_t b) {
+    if (b <= bytes) return;
+    release();
+    cuda_check(cudaMallocHost(&p, b), "cudaMallocHost");
+    bytes = b;
+}
+void HostBuf::release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+}
+
+namespace {
+
+std::string fmt_double(double v) {  // model.cpp:26-30
+    std::ostringstream os;
+    os << v;
+    return os.str();
+}
+
+void throw_first(const char* where, const std::vector<std::string>& v) {  // mat_engine.cpp:15-21
+    if (v.empty()) return;
+    std::string msg = std::string(where) + ": " + v.front();
+    if (v.size() > 1) msg += " (+" + std::to_string(v.size() - 1) + " more)";
+    throw InvalidArgument(msg);
+}
+
+template <typename T>
+void upload(DevBuf& d, const std::vector<T>& h) {
+    d.alloc(h.size() * sizeof(T));
+    if (!h.empty()) cuda_check(cudaMemcpy(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+}
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+Engine::Engine(const sn_options& opt) : opt_(opt) {
+    if (opt_.world < 1) throw InvalidArgument("sn_engine_create: world must be >= 1");
+    if (opt_.rank < 0 || opt_.rank >= opt_.world) throw InvalidArgument("sn_engine_create: rank out of range");
+    if (opt_.storage < 0 || opt_.storage > 2) throw InvalidArgument("sn_engine_create: unknown storage");
+    int count = 0;
+    cuda_check(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    if (opt_.device < 0 || opt_.device >= count)
+        throw InvalidArgument("sn_engine_create: CUDA device " + std::to_string(opt_.device) +
+                              " not present (" + std::to_string(count) + " visible)");
+    cuda_check(cudaSetDevice(opt_.device), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    f64_ = opt_.precision == SN_WEIGHTS_F64;
+    exact_ = opt_.exact_order != 0;
+}
+
+Engine::~Engine() {
+    cudaSetDevice(opt_.device);
+    if (stream_) cudaStreamSynchronize(stream_);
+    delete comm_;
+    for (auto e : ev_pool_) cudaEventDestroy(e);
+    for (auto& p : pending_) {
+        (void)p;
+    }
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::require_not_setup(const char* what) const {
+    if (setup_done_) throw LogicError(std::string(what) + ": the network is fixed after sn_setup");
+}
+void Engine::require_setup(const char* what) const {
+    if (!setup_done_) throw LogicError(std::string(what) + ": call sn_setup first");
+}
+
+void Engine::partition(int32_t n, int32_t rank, int32_t world, int32_t* first, int32_t* count) {
+    // contiguous post ranges, each a multiple of 32 ids so spike words never straddle ranks
+    const int64_t words = (static_cast<int64_t>(n) + 31) / 32;
+    const int64_t per = (words + world - 1) / world * 32;
+    const int64_t f = per * rank;
+    const int64_t c = std::max<int64_t>(0, std::min<int64_t>(n - f, per));
+    *first = static_cast<int32_t>(std::min<int64_t>(f, n));
+    *count = static_cast<int32_t>(c);
+}
+
+// ---- model building --------------------------------------------------------
+void Engine::add_neurons(int64_t count, const double* thr, const double* leak, const double* reset,
+                         const int32_t* refr, const int32_t* axonal, int64_t* first_id) {
+    require_not_setup("sn_add_neurons");
+    if (count < 0) throw InvalidArgument("sn_add_neurons: count must be >= 0");
+    if (count > 0 && (!thr || !leak || !reset || !refr))
+        throw InvalidArgument("sn_add_neurons: null parameter array");
+    if (generated_) throw LogicError("sn_add_neurons: network was generated with sn_generate_erdos_renyi");
+    if (first_id) *first_id = static_cast<int64_t>(thr_.size());
+    if (static_cast<int64_t>(thr_.size()) + count > INT32_MAX)
+        throw InvalidArgument("sn_add_neurons: neuron ids must fit int32");
+    thr_.insert(thr_.end(), thr, thr + count);
+    leak_.insert(leak_.end(), leak, leak + count);
+    reset_.insert(reset_.end(), reset, reset + count);
+    refr_.insert(refr_.end(), refr, refr + count);
+    if (axonal) axonal_.insert(axonal_.end(), axonal, axonal + count);
+    else axonal_.insert(axonal_.end(), static_cast<size_t>(count), 0);
+}
+
+void Engine::add_synapses(int64_t count, const int32_t* pre, const int32_t* post, const double* w,
+                          const int32_t* delay, const uint8_t* stdp) {
+    require_not_setup("sn_add_synapses");
+    if (count < 0) throw InvalidArgument("sn_add_synapses: count must be >= 0");
+    if (count > 0 && (!pre || !post || !w)) throw InvalidArgument("sn_add_synapses: null parameter array");
+    if (generated_) throw LogicError("sn_add_synapses: network was generated with sn_generate_erdos_renyi");
+    pre_.insert(pre_.end(), pre, pre + count);
+    post_.insert(post_.end(), post, post + count);
+    weight_.insert(weight_.end(), w, w + count);
+    if (delay) delay_.insert(delay_.end(), delay, delay + count);
+    else delay_.insert(delay_.end(), static_cast<size_t>(count), 1);
+    if (stdp) plastic_.insert(plastic_.end(), stdp, stdp + count);
+    else plastic_.insert(plastic_.end(), static_cast<size_t>(count), 0);
+}
+
+void Engine::add_stimulus(int64_t count, const int32_t* step, const int32_t* neuron, const double* amp) {
+    if (count < 0) throw InvalidArgument("sn_add_stimulus: count must be >= 0");
+    if (count > 0 && (!step || !neuron || !amp)) throw InvalidArgument("sn_add_stimulus: null parameter array");
+    const size_t base = st_step_.size();
+    for (int64_t i = 0; i < count; ++i) {
+        const std::string who = "stimulus[" + std::to_string(base + i) + "]";
+        if (step[i] < 0)
+            throw InvalidArgument("mat_run: " + who + ": step " + std::to_string(step[i]) + " is negative");
+        if (!std::isfinite(amp[i])) throw InvalidArgument("mat_run: " + who + ": amplitude must be finite");
+        if (setup_done_ && (neuron[i] < 0 || neuron[i] >= n_))
+            throw InvalidArgument("mat_run: " + who + ": neuron id " + std::to_string(neuron[i]) +
+                                  " out of range (" + std::to_string(n_) + " neurons)");
+    }
+    st_step_.insert(st_step_.end(), step, step + count);
+    st_neuron_.insert(st_neuron_.end(), neuron, neuron + count);
+    st_amp_.insert(st_amp_.end(), amp, amp + count);
+    stim_dirty_ = true;
+}
+
+void Engine::clear_stimulus() {
+    st_step_.clear();
+    st_neuron_.clear();
+    st_amp_.clear();
+    stim_dirty_ = true;
+}
+
+void Engine::set_stdp(int32_t window, const double* ap, const double* am, double wmin, double wmax) {
+    require_not_setup("sn_set_stdp");
+    std::vector<std::string> bad;  // validate_stdp (model.cpp:104-117)
+    if (window < 1) bad.push_back("stdp: window must be >= 1");
+    if (window >= 1 && (!ap || !am)) throw InvalidArgument("sn_set_stdp: null kernel array");
+    if (window >= 1) {
+        for (int k = 0; k < window; ++k)
+            if (!(ap[k] >= 0.0)) { bad.push_back("stdp: a_plus entries must be >= 0"); break; }
+        for (int k = 0; k < window; ++k)
+            if (!(am[k] >= 0.0)) { bad.push_back("stdp: a_minus entries must be >= 0"); break; }
+    }
+    if (!(wmin <= wmax)) bad.push_back("stdp: w_min must be <= w_max");
+    throw_first("mat_init", bad);
+    stdp_on_ = true;
+    window_ = window;
+    a_plus_.assign(ap, ap + window);
+    a_minus_.assign(am, am + window);
+    w_min_ = wmin;
+    w_max_ = wmax;
+}
+
+void Engine::generate_er(int32_t n, double p, uint64_t seed, double weight, int32_t delay_max,
+                         uint64_t delay_stream, int32_t by_syn, int32_t stdp) {
+    require_not_setup("sn_generate_erdos_renyi");
+    if (n < 1) throw InvalidArgument("erdos_renyi: n must be >= 1");           // netgen.cpp:20
+    if (!(p >= 0.0 && p <= 1.0)) throw InvalidArgument("erdos_renyi: p must be in [0, 1]");
+    if (!std::isfinite(weight)) throw InvalidArgument("erdos_renyi: weight must be finite");
+    if (delay_max < 1) throw InvalidArgument("erdos_renyi: delay_max must be >= 1");
+    if (by_syn && delay_max > 1 && p < 1.0)
+        throw InvalidArgument("erdos_renyi: synapse-index keyed delays need p == 1");
+    if (!pre_.empty()) throw LogicError("sn_generate_erdos_renyi: synapses were already added");
+    generated_ = true;
+    thr_.assign(n, 1.0);
+    leak_.assign(n, 0.0);
+    reset_.assign(n, 0.0);
+    refr_.assign(n, 0);
+    axonal_.assign(n, 0);
+    er_.n = n;
+    er_.p = p;
+    er_.edge_key = stream_key(seed, 1);  // kEdgeStream (netgen.cpp:15)
+    er_.delay_key = stream_key(seed, delay_stream);
+    er_.delay_max = delay_max;
+    er_.delay_by_synapse_index = by_syn;
+    er_.weight_f = static_cast<float>(weight);
+    er_.weight_d = weight;
+    er_.stdp = stdp ? 1 : 0;
+    er_delay_max_ = delay_max;
+}
+
+void Engine::validate() const {
+    std::vector<std::string> out;  // validate_network (model.cpp:34-84)
+    const int n = static_cast<int>(thr_.size());
+    for (int i = 0; i < n; ++i) {
+        const std::string who = "neurons[" + std::to_string(i) + "]";
+        if (!std::isfinite(thr_[i])) out.push_back(who + ": threshold must be finite");
+        if (std::isnan(leak_[i]) || leak_[i] < 0.0)
+            out.push_back(who + ": leak must be >= 0 or infinite (got " + fmt_double(leak_[i]) + ")");
+        if (!std::isfinite(reset_[i])) out.push_back(who + ": reset must be finite");
+        if (refr_[i] < 0)
+            out.push_back(who + ": refractory_period must be >= 0 (got " + std::to_string(refr_[i]) + ")");
+        if (axonal_[i] < 0)
+            out.push_back(who + ": axonal_delay must be >= 0 (got " + std::to_string(axonal_[i]) + ")");
+    }
+    if (!generated_) {
+        std::unordered_set<uint64_t> seen;
+        seen.reserve(pre_.size());
+        for (size_t s = 0; s < pre_.size(); ++s) {
+            const std::string who = "synapses[" + std::to_string(s) + "]";
+            const bool pre_ok = pre_[s] >= 0 && pre_[s] < n;
+            const bool post_ok = post_[s] >= 0 && post_[s] < n;
+            if (!pre_ok)
+                out.push_back(who + ": pre id " + std::to_string(pre_[s]) + " out of range (" +
+                              std::to_string(n) + " neurons)");
+            if (!post_ok)
+                out.push_back(who + ": post id " + std::to_string(post_[s]) + " out of range (" +
+                              std::to_string(n) + " neurons)");
+            if (!std::isfinite(weight_[s])) out.push_back(who + ": weight must be finite");
+            if (delay_[s] < 1) out.push_back(who + ": delay must be >= 1 (got " + std::to_string(delay_[s]) + ")");
+            if (pre_ok && post_ok) {
+                const uint64_t key = (static_cast<uint64_t>(static_cast<uint32_t>(pre_[s])) << 32) |
+                                     static_cast<uint32_t>(post_[s]);
+                if (!seen.insert(key).second)
+                    out.push_back(who + ": duplicate synapse (" + std::to_string(pre_[s]) + ", " +
+                                  std::to_string(post_[s]) + ")");
+            }
+        }
+    }
+    throw_first("mat_init", out);
+    for (size_t i = 0; i < st_neuron_.size(); ++i)
+        if (st_neuron_[i] < 0 || st_neuron_[i] >= n)
+            throw InvalidArgument("mat_run: stimulus[" + std::to_string(i) + "]: neuron id " +
+                                  std::to_string(st_neuron_[i]) + " out of range (" + std::to_string(n) +
+                                  " neurons)");
+}
+
+// ---- setup -------------------------------------------------------------------
+void Engine::setup() {
+    require_not_setup("sn_setup");
+    cuda_check(cudaSetDevice(opt_.device), "cudaSetDevice");
+    validate();
+    n_ = static_cast<int32_t>(thr_.size());
+    if (n_ < 1) throw InvalidArgument("mat_init: the network has no neurons");
+    partition(n_, opt_.rank, opt_.world, &first_, &nl_);
+    {
+        int32_t f0, c0;
+        partition(n_, 0, opt_.world, &f0, &c0);
+        part_ = std::max(c0, 32);
+    }
+    nl_words_ = (nl_ + 31) / 32;
+    words_ = opt_.world * (part_ / 32);
+
+    // effective delays (delay + axonal of the pre), spans
+    dmax_ = 1;
+    dp_ = 1;
+    if (generated_) {
+        dmax_ = er_delay_max_;
+        if (er_.stdp) dp_ = er_delay_max_;
+    } else {
+        for (size_t s = 0; s < pre_.size(); ++s) {
+            const int64_t d = static_cast<int64_t>(delay_[s]) + axonal_[pre_[s]];
+            if (d > 64)
+                throw Unsupported("mat_init: synapses[" + std::to_string(s) + "] has effective delay " +
+                                  std::to_string(d) + "; this engine supports delays up to 64 steps");
+            dmax_ = std::max<int32_t>(dmax_, static_cast<int32_t>(d));
+            if (stdp_on_ && plastic_[s]) dp_ = std::max<int32_t>(dp_, static_cast<int32_t>(d));
+        }
+    }
+    has_delay_ = dmax_ > 1;
+    hw_ = stdp_on_ ? static_cast<int32_t>((window_ + dp_ + 63) / 64) : 1;
+    hw_ = std::max(hw_, 1);
+    if (hw_ > 8)
+        throw Unsupported("mat_init: STDP window + delay span exceeds the 512-step history of this engine");
+    hbits_ = dmax_ == 1 ? 1 : dmax_ <= 16 ? 16 : dmax_ <= 32 ? 32 : 64;
+
+    // storage choice (mat_engine.cpp:27-30 switches at n > 12000; here the
+    // choice follows bytes per step instead)
+    const int64_t m = generated_ ? -1 : static_cast<int64_t>(pre_.size());
+    double density;
+    if (generated_) density = er_.p;
+    else density = n_ > 0 ? static_cast<double>(m) / (static_cast<double>(n_) * n_) : 0.0;
+    const size_t esz = f64_ ? 8 : 4;
+    const double dense_bytes = static_cast<double>(n_) * round_up(std::max(nl_, 1), 32) * esz;
+    size_t free_b = 0, total_b = 0;
+    cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    if (opt_.storage == SN_STORAGE_DENSE) dense_ = true;
+    else if (opt_.storage == SN_STORAGE_SPARSE) dense_ = false;
+    else dense_ = (density >= 0.1 || n_ <= 4096) && dense_bytes < 0.85 * static_cast<double>(free_b);
+
+    if (generated_) build_generated();
+    else if (dense_) build_dense_from_lists();
+    else build_sparse_from_lists();
+
+    alloc_state();
+    stim_dirty_ = true;
+    build_stimulus_table();
+    plan_launches();
+    cuda_check(cudaStreamSynchronize(stream_), "setup sync");
+    setup_done_ = true;
+    stats_.synapses_local = syn_local_;
+    stats_.dense = dense_ ? 1 : 0;
+    stats_.n_local = nl_;
+    stats_.first_local = first_;
+    stats_.max_delay = dmax_;
+}
+
+void Engine::build_dense_from_lists() {
+    pitch_ = round_up(std::max(nl_, 1), 32);
+    const int64_t elems = static_cast<int64_t>(n_) * pitch_;
+    std::vector<float> wf;
+    std::vector<double> wd;
+    if (f64_) wd.assign(static_cast<size_t>(elems), 0.0);
+    else wf.assign(static_cast<size_t>(elems), 0.0f);
+    std::vector<uint8_t> dl;
+    if (has_delay_) dl.assign(static_cast<size_t>(elems), 1);
+    std::vector<int64_t> pl_count(n_, 0);
+    std::vector<uint8_t> self_present(n_, 0);
+    slot_.assign(pre_.size(), -1);
+    syn_local_ = 0;
+    for (size_t s = 0; s < pre_.size(); ++s) {
+        const int j = post_[s];
+        if (j < first_ || j >= first_ + nl_) continue;
+        const int i = pre_[s];
+        const int64_t off = static_cast<int64_t>(i) * pitch_ + (j - first_);
+        if (f64_) wd[off] = weight_[s];
+        else wf[off] = static_cast<float>(weight_[s]);
+        if (has_delay_) dl[off] = static_cast<uint8_t>(delay_[s] + axonal_[i]);
+        slot_[s] = off;
+        ++syn_local_;
+        if (stdp_on_ && plastic_[s]) ++pl_count[i];
+        if (i == j) self_present[i] = 1;
+    }
+    std::vector<uint8_t> kind(n_, kRowNone), row_pl(n_, 0);
+    any_mixed_ = false;
+    for (int i = 0; i < n_; ++i) {
+        const bool self_local = i >= first_ && i < first_ + nl_;
+        if (pl_count[i] == 0) kind[i] = kRowNone;
+        else if (pl_count[i] == nl_) kind[i] = kRowAll;
+        else if (self_local && pl_count[i] == nl_ - 1 && !self_present[i]) kind[i] = kRowAllButSelf;
+        else { kind[i] = kRowMixed; any_mixed_ = true; }
+        row_pl[i] = kind[i] != kRowNone;
+    }
+    if (f64_) upload(d_w_, wd);
+    else upload(d_w_, wf);
+    if (has_delay_) upload(d_delay_, dl);
+    if (any_mixed_) {
+        std::vector<uint32_t> mask(static_cast<size_t>(n_) * (pitch_ / 32), 0u);
+        for (size_t s = 0; s < pre_.size(); ++s) {
+            if (slot_[s] < 0 || !plastic_[s]) continue;
+            const int64_t off = slot_[s];
+            const int64_t row = off / pitch_, c = off % pitch_;
+            mask[row * (pitch_ / 32) + c / 32] |= 1u << (c % 32);
+        }
+        upload(d_mask_, mask);
+    }
+    upload(d_kind_, kind);
+    upload(d_row_plastic_, row_pl);
+    sweep_bytes_full_ = static_cast<double>(n_) * nl_ * ((stdp_on_ ? 2.0 : 1.0) * (f64_ ? 8 : 4) + (has_delay_ ? 1 : 0));
+}
+
+void Engine::build_sparse_from_lists() {
+    pb_ = sparse_block_pres(hbits_);
+    nblocks_ = (n_ + pb_ - 1) / pb_;
+    const int64_t nseg = static_cast<int64_t>(nblocks_) * nl_;
+    std::vector<int64_t> cnt(static_cast<size_t>(nseg) + 1, 0);
+    std::vector<int64_t> local;
+    local.reserve(pre_.size());
+    for (size_t s = 0; s < pre_.size(); ++s) {
+        const int j = post_[s];
+        if (j < first_ || j >= first_ + nl_) continue;
+        local.push_back(static_cast<int64_t>(s));
+        ++cnt[static_cast<int64_t>(pre_[s] / pb_) * nl_ + (j - first_)];
+    }
+    syn_local_ = static_cast<int64_t>(local.size());
+    std::vector<int64_t> off(static_cast<size_t>(nseg) + 1, 0);
+    for (int64_t g = 0; g < nseg; ++g) off[g + 1] = off[g] + round_up(cnt[g], 4);
+    sparse_elems_ = off[nseg];
+    // order within a segment: pre ascending (matches the CSR propagate order)
+    std::sort(local.begin(), local.end(), [&](int64_t a, int64_t b) {
+        const int64_t ga = static_cast<int64_t>(pre_[a] / pb_) * nl_ + (post_[a] - first_);
+        const int64_t gb = static_cast<int64_t>(pre_[b] / pb_) * nl_ + (post_[b] - first_);
+        if (ga != gb) return ga < gb;
+        return pre_[a] < pre_[b];
+    });
+    std::vector<uint32_t> meta(static_cast<size_t>(sparse_elems_), 0u);
+    std::vector<float> wf;
+    std::vector<double> wd;
+    if (f64_) wd.assign(static_cast<size_t>(sparse_elems_), 0.0);
+    else wf.assign(static_cast<size_t>(sparse_elems_), 0.0f);
+    std::vector<int64_t> cur(off.begin(), off.end() - 1);
+    slot_.assign(pre_.size(), -1);
+    std::vector<uint8_t> row_pl(n_, 0);
+    for (int64_t s : local) {
+        const int i = pre_[s];
+        const int64_t g = static_cast<int64_t>(i / pb_) * nl_ + (post_[s] - first_);
+        const int64_t q = cur[g]++;
+        const int d = delay_[s] + axonal_[i];
+        const bool pl = stdp_on_ && plastic_[s];
+        meta[q] = static_cast<uint32_t>(i % pb_) | (static_cast<uint32_t>(d - 1) << 16) | (pl ? (1u << 22) : 0u);
+        if (f64_) wd[q] = weight_[s];
+        else wf[q] = static_cast<float>(weight_[s]);
+        slot_[s] = q;
+        if (pl) row_pl[i] = 1;
+    }
+    upload(d_off_, off);
+    upload(d_meta_, meta);
+    if (f64_) upload(d_w_, wd);
+    else upload(d_w_, wf);
+    upload(d_row_plastic_, row_pl);
+    sweep_bytes_full_ = static_cast<double>(syn_local_) * ((stdp_on_ ? 2.0 : 1.0) * (f64_ ? 8 : 4) + 4.0);
+}
+
+void Engine::build_generated() {
+    const size_t esz = f64_ ? 8 : 4;
+    slot_.clear();
+    std::vector<uint8_t> row_pl(n_, 0);
+    if (dense_) {
+        pitch_ = round_up(std::max(nl_, 1), 32);
+        const int64_t elems = static_cast<int64_t>(n_) * pitch_;
+        d_w_.alloc(static_cast<size_t>(elems) * esz);
+        if (has_delay_) d_delay_.alloc(static_cast<size_t>(elems));
+        std::vector<uint8_t> kind(n_, kRowNone);
+        any_mixed_ = false;
+        if (er_.stdp) {
+            for (int i = 0; i < n_; ++i) {
+                const bool self_local = i >= first_ && i < first_ + nl_;
+                if (er_.p >= 1.0) kind[i] = self_local ? kRowAllButSelf : kRowAll;
+                else { kind[i] = kRowMixed; any_mixed_ = true; }
+                row_pl[i] = 1;
+            }
+            if (nl_ == 0) std::fill(kind.begin(), kind.end(), kRowNone);
+        }
+        if (any_mixed_) d_mask_.alloc(static_cast<size_t>(n_) * (pitch_ / 32) * 4);
+        launch_er_dense(er_, d_w_.p, f64_, has_delay_ ? d_delay_.as<uint8_t>() : nullptr,
+                        any_mixed_ ? d_mask_.as<uint32_t>() : nullptr, first_, nl_, pitch_, stream_);
+        stats_.kernel_launches += 1;
+        upload(d_kind_, kind);
+        if (er_.p >= 1.0) {
+            const int64_t self_local = std::max(0, std::min(nl_, n_ - first_));
+            syn_local_ = static_cast<int64_t>(n_) * nl_ - self_local;
+        } else {
+            syn_local_ = static_cast<int64_t>(er_.p * static_cast<double>(n_) * nl_);  // expectation
+        }
+        sweep_bytes_full_ = static_cast<double>(n_) * nl_ * ((stdp_on_ ? 2.0 : 1.0) * esz + (has_delay_ ? 1 : 0));
+    } else {
+        pb_ = sparse_block_pres(hbits_);
+        nblocks_ = (n_ + pb_ - 1) / pb_;
+        const int64_t nseg = static_cast<int64_t>(nblocks_) * nl_;
+        DevBuf d_counts;
+        d_counts.alloc(static_cast<size_t>(nseg) * 8);
+        launch_er_sparse_count(er_, first_, nl_, pb_, nblocks_, d_counts.as<int64_t>(), stream_);
+        std::vector<int64_t> cnt(static_cast<size_t>(nseg));
+        cuda_check(cudaMemcpyAsync(cnt.data(), d_counts.p, static_cast<size_t>(nseg) * 8, cudaMemcpyDeviceToHost, stream_), "counts D2H");
+        cuda_check(cudaStreamSynchronize(stream_), "counts sync");
+        std::vector<int64_t> off(static_cast<size_t>(nseg) + 1, 0);
+        syn_local_ = 0;
+        for (int64_t g = 0; g < nseg; ++g) {
+            off[g + 1] = off[g] + round_up(cnt[g], 4);
+            syn_local_ += cnt[g];
+        }
+        sparse_elems_ = off[nseg];
+        upload(d_off_, off);
+        d_meta_.alloc(static_cast<size_t>(sparse_elems_) * 4);
+        d_w_.alloc(static_cast<size_t>(sparse_elems_) * esz);
+        launch_er_sparse_fill(er_, first_, nl_, pb_, nblocks_, d_off_.as<int64_t>(), d_meta_.as<uint32_t>(),
+                              d_w_.p, f64_, stream_);
+        stats_.kernel_launches += 2;
+        if (er_.stdp) std::fill(row_pl.begin(), row_pl.end(), 1);
+        sweep_bytes_full_ = static_cast<double>(syn_local_) * ((stdp_on_ ? 2.0 : 1.0) * esz + 4.0);
+    }
+    upload(d_row_plastic_, row_pl);
+    if (er_.stdp && !stdp_on_)
+        throw InvalidArgument("mat_init: plastic synapses were generated but no STDP config was set (sn_set_stdp)");
+}
+
+void Engine::alloc_state() {
+    std::vector<double> v(reset_.begin() + first_, reset_.begin() + first_ + nl_);
+    upload(d_v_, v);  // membrane = reset (mat_engine.cpp:143)
+    upload(d_thr_, std::vector<double>(thr_.begin() + first_, thr_.begin() + first_ + nl_));
+    upload(d_leak_, std::vector<double>(leak_.begin() + first_, leak_.begin() + first_ + nl_));
+    upload(d_reset_, std::vector<double>(reset_.begin() + first_, reset_.begin() + first_ + nl_));
+    upload(d_refr_, std::vector<int32_t>(refr_.begin() + first_, refr_.begin() + first_ + nl_));
+    d_cnt_.alloc(static_cast<size_t>(std::max(nl_, 1)) * 4);
+    cuda_check(cudaMemsetAsync(d_cnt_.p, 0, d_cnt_.bytes, stream_), "memset");
+    const size_t wbytes = static_cast<size_t>(std::max(words_, (n_ + 31) / 32)) * 4;
+    d_bits_.alloc(wbytes);
+    d_active_.alloc(wbytes);
+    cuda_check(cudaMemsetAsync(d_bits_.p, 0, wbytes, stream_), "memset");
+    cuda_check(cudaMemsetAsync(d_active_.p, 0, wbytes, stream_), "memset");
+    d_hist_.alloc(static_cast<size_t>(hw_) * n_ * 8);
+    cuda_check(cudaMemsetAsync(d_hist_.p, 0, d_hist_.bytes, stream_), "memset");
+    d_hist_lo_.alloc(static_cast<size_t>(n_) * 4);
+    cuda_check(cudaMemsetAsync(d_hist_lo_.p, 0, d_hist_lo_.bytes, stream_), "memset");
+    const size_t np = static_cast<size_t>(n_) * (stdp_on_ ? dp_ : 1);
+    d_pot64_.alloc(np * 8);
+    d_pot32_.alloc(np * 4);
+    d_dep64_.alloc(static_cast<size_t>(n_) * 8);
+    d_dep32_.alloc(static_cast<size_t>(n_) * 4);
+    for (DevBuf* b : {&d_pot64_, &d_pot32_, &d_dep64_, &d_dep32_})
+        cuda_check(cudaMemsetAsync(b->p, 0, b->bytes, stream_), "memset");
+    if (stdp_on_) {
+        upload(d_ap_, a_plus_);
+        upload(d_am_, a_minus_);
+    } else {
+        d_ap_.alloc(8);
+        d_am_.alloc(8);
+    }
+    d_step_.alloc(8);
+    d_spikes_.alloc(16);
+    cuda_check(cudaMemsetAsync(d_step_.p, 0, 8, stream_), "memset");
+    cuda_check(cudaMemsetAsync(d_spikes_.p, 0, 16, stream_), "memset");
+    d_uexact_.alloc(static_cast<size_t>(std::max(nl_, 1)) * 8);
+    launch_prologue(d_uexact_.as<double>(), d_v_.as<double>(), d_leak_.as<double>(), d_reset_.as<double>(), nl_, stream_);
+}
+
+void Engine::plan_launches() {
+    int sms = 148;
+    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt_.device), "attr");
+    if (dense_) {
+        const int vec = dense_vec(f64_);
+        const int span = dense_threads() * vec;
+        const int ntiles = std::max(1, (nl_ + span - 1) / span);
+        tile_w_ = static_cast<int32_t>(round_up((nl_ + ntiles - 1) / ntiles, vec));
+        tile_w_ = std::max(tile_w_, vec);
+        if (exact_) {
+            nchunks_ = 1;
+            rows_per_chunk_ = static_cast<int32_t>(round_up(n_, 32));
+        } else {
+            // ~8 resident CTAs per SM; one wave of equal items
+            const int resident = sms * 8;
+            int nch = std::max(1, resident / ntiles);
+            int rpc = static_cast<int>(round_up((n_ + nch - 1) / nch, 32));
+            rpc = std::max(rpc, 32);
+            nch = (n_ + rpc - 1) / rpc;
+            rows_per_chunk_ = rpc;
+            nchunks_ = nch;
+        }
+        const int items = ntiles * nchunks_;
+        dense_grid_ = std::min(items, sms * 8);
+        d_partial_.alloc(static_cast<size_t>(nchunks_) * std::max(nl_, 1) * 8);
+        cuda_check(cudaMemsetAsync(d_partial_.p, 0, d_partial_.bytes, stream_), "memset");
+    } else {
+        const double avg = nl_ > 0 ? static_cast<double>(sparse_elems_) / (static_cast<double>(nblocks_) * nl_) : 0.0;
+        sub_ = avg >= 256 ? 32 : avg >= 96 ? 16 : avg >= 40 ? 8 : 4;
+        const int target = sms * 8;
+        int gx = std::max(1, target / std::max(1, nblocks_));
+        const int unit = 8 * (32 / sub_);
+        posts_per_cta_ = static_cast<int32_t>(round_up((nl_ + gx - 1) / gx, unit));
+        posts_per_cta_ = std::max(posts_per_cta_, unit);
+        sparse_gx_ = std::max(1, (nl_ + posts_per_cta_ - 1) / posts_per_cta_);
+        nchunks_ = nblocks_;
+        d_partial_.alloc(static_cast<size_t>(nblocks_) * std::max(nl_, 1) * 8);
+        cuda_check(cudaMemsetAsync(d_partial_.p, 0, d_partial_.bytes, stream_), "memset");
+    }
+}
+
+void Engine::build_stimulus_table() {
+    if (!stim_dirty_) return;
+    // stable by step; per step sum amplitudes per neuron in list order from 0.0
+    // (mat_engine.cpp:258-275), keep local neurons, neuron ascending
+    std::vector<size_t> ord(st_step_.size());
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return st_step_[a] < st_step_[b]; });
+    int32_t steps = 0;
+    for (int32_t s : st_step_) steps = std::max(steps, s + 1);
+    hs_off_.assign(static_cast<size_t>(steps) + 1, 0);
+    hs_neuron_.clear();
+    hs_amp_.clear();
+    size_t k = 0;
+    for (int32_t t = 0; t < steps; ++t) {
+        std::vector<std::pair<int32_t, double>> acc;  // neuron -> sum, first-appearance order
+        std::vector<int32_t> seen_idx;
+        while (k < ord.size() && st_step_[ord[k]] == t) {
+            const size_t e = ord[k++];
+            const int32_t j = st_neuron_[e];
+            if (j < first_ || j >= first_ + nl_) continue;
+            bool found = false;
+            for (auto& pr : acc)
+                if (pr.first == j) { pr.second += st_amp_[e]; found = true; break; }
+            if (!found) acc.emplace_back(j, 0.0 + st_amp_[e]);
+        }
+        std::sort(acc.begin(), acc.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (auto& pr : acc) {
+            hs_neuron_.push_back(pr.first);
+            hs_amp_.push_back(pr.second);
+        }
+        hs_off_[t + 1] = static_cast<int64_t>(hs_neuron_.size());
+    }
+    if (!opt_.stream_io) {
+        upload(d_st_off_, hs_off_);
+        upload(d_st_neuron_, hs_neuron_);
+        upload(d_st_amp_, hs_amp_);
+        st_steps_dev_ = steps;
+    }
+    stim_dirty_ = false;
+}
+
+// ---- per-step launch sequence ----------------------------------------------
+NeuronArgs Engine::neuron_args(int t_base, int rows, uint32_t* raster, double* trace, const int64_t* st_off,
+                               const int32_t* st_neuron, const double* st_amp, int32_t st_steps,
+                               int32_t st_stream) {
+    NeuronArgs a{};
+    a.n = n_;
+    a.first = first_;
+    a.nl = nl_;
+    a.v = d_v_.as<double>();
+    a.thr = d_thr_.as<double>();
+    a.leak = d_leak_.as<double>();
+    a.reset = d_reset_.as<double>();
+    a.refr = d_refr_.as<int32_t>();
+    a.cnt = d_cnt_.as<int32_t>();
+    a.partial = d_partial_.as<double>();
+    a.nchunks = nchunks_;
+    a.u_exact = d_uexact_.as<double>();
+    a.st_off = st_off;
+    a.st_neuron = st_neuron;
+    a.st_amp = st_amp;
+    a.st_steps = st_steps;
+    a.st_stream = st_stream;
+    a.d_step = d_step_.as<int32_t>();
+    a.t_base = t_base;
+    a.bits = d_bits_.as<uint32_t>();
+    a.raster = raster;
+    a.nl_words = nl_words_;
+    a.raster_rows = rows;
+    a.trace = trace;
+    a.spike_count = d_spikes_.as<unsigned long long>();
+    return a;
+}
+
+HistArgs Engine::hist_args() {
+    HistArgs h{};
+    h.n = n_;
+    h.bits = d_bits_.as<uint32_t>();
+    h.hist = d_hist_.as<uint64_t>();
+    h.hw = hw_;
+    h.dmax = dmax_;
+    h.stdp = stdp_on_ ? 1 : 0;
+    h.window = window_;
+    h.dp = stdp_on_ ? dp_ : 1;
+    h.a_plus = d_ap_.as<double>();
+    h.a_minus = d_am_.as<double>();
+    h.pot64 = d_pot64_.as<double>();
+    h.pot32 = d_pot32_.as<float>();
+    h.dep64 = d_dep64_.as<double>();
+    h.dep32 = d_dep32_.as<float>();
+    h.row_plastic = d_row_plastic_.as<uint8_t>();
+    h.active = d_active_.as<uint32_t>();
+    h.d_step = d_step_.as<int32_t>();
+    h.hist_lo = (!dense_ && (hbits_ == 16 || hbits_ == 32)) ? d_hist_lo_.as<uint32_t>() : nullptr;
+    h.active_count = d_spikes_.as<unsigned long long>() + 1;
+    return h;
+}
+
+void Engine::launch_sweep() {
+    if (dense_) {
+        DenseArgs a{};
+        a.n = n_;
+        a.first = first_;
+        a.nl = nl_;
+        a.pitch = pitch_;
+        a.w = d_w_.p;
+        a.delay = has_delay_ ? d_delay_.as<uint8_t>() : nullptr;
+        a.mask = any_mixed_ ? d_mask_.as<uint32_t>() : nullptr;
+        a.kind = d_kind_.as<uint8_t>();
+        a.active = d_active_.as<uint32_t>();
+        a.hist = d_hist_.as<uint64_t>();
+        a.bits = d_bits_.as<uint32_t>();
+        a.pot = f64_ ? static_cast<const void*>(d_pot64_.p) : static_cast<const void*>(d_pot32_.p);
+        a.dep = f64_ ? static_cast<const void*>(d_dep64_.p) : static_cast<const void*>(d_dep32_.p);
+        a.dp = stdp_on_ ? dp_ : 1;
+        a.w_min = w_min_;
+        a.w_max = w_max_;
+        a.tile_w = tile_w_;
+        a.rows_per_chunk = rows_per_chunk_;
+        a.nchunks = nchunks_;
+        a.partial = d_partial_.as<double>();
+        a.v = d_v_.as<double>();
+        a.leak = d_leak_.as<double>();
+        a.reset = d_reset_.as<double>();
+        a.u_exact = d_uexact_.as<double>();
+        a.d_step = d_step_.as<int32_t>();
+        launch_dense(a, f64_, stdp_on_, has_delay_, exact_, dense_grid_, stream_);
+    } else {
+        SparseArgs a{};
+        a.n = n_;
+        a.first = first_;
+        a.nl = nl_;
+        a.pb = pb_;
+        a.nblocks = nblocks_;
+        a.off = d_off_.as<int64_t>();
+        a.meta = d_meta_.as<uint32_t>();
+        a.w = d_w_.p;
+        a.bits = d_bits_.as<uint32_t>();
+        a.hist_lo = d_hist_lo_.as<uint32_t>();
+        a.hist = d_hist_.as<uint64_t>();
+        a.pot = f64_ ? static_cast<const void*>(d_pot64_.p) : static_cast<const void*>(d_pot32_.p);
+        a.dep = f64_ ? static_cast<const void*>(d_dep64_.p) : static_cast<const void*>(d_dep32_.p);
+        a.dp = stdp_on_ ? dp_ : 1;
+        a.w_min = w_min_;
+        a.w_max = w_max_;
+        a.posts_per_cta = posts_per_cta_;
+        a.partial = d_partial_.as<double>();
+        a.v = d_v_.as<double>();
+        a.leak = d_leak_.as<double>();
+        a.reset = d_reset_.as<double>();
+        a.u_exact = d_uexact_.as<double>();
+        a.d_step = d_step_.as<int32_t>();
+        if (nl_ == 0) launch_step_bump(a.d_step, stream_);
+        else launch_sparse(a, f64_, stdp_on_, hbits_, sub_, exact_, sparse_gx_, stream_);
+    }
+    stats_.kernel_launches += 1;
+}
+
+cudaEvent_t Engine::get_event() {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+}
+
+void Engine::enqueue_step(const NeuronArgs& na, bool exchange) {
+    const bool prof = opt_.profile != 0;
+    const bool fused = opt_.world == 1;
+    const HistArgs h = hist_args();
+    cudaEvent_t e0{}, e1{}, e2{}, e3{};
+    if (prof) { e0 = get_event(); cuda_check(cudaEventRecord(e0, stream_), "rec"); }
+    launch_neuron(na, exact_, fused, h, stream_);
+    stats_.kernel_launches += 1;
+    if (prof) { e1 = get_event(); cuda_check(cudaEventRecord(e1, stream_), "rec"); pending_.push_back({e0, e1, 0, 0.0}); }
+    if (!fused && exchange) {
+        if (prof) { e0 = get_event(); cuda_check(cudaEventRecord(e0, stream_), "rec"); }
+        if (comm_) comm_->all_gather_inplace(d_bits_.as<uint32_t>(), static_cast<size_t>(part_ / 32), stream_);
+        launch_hist(h, stream_);
+        stats_.kernel_launches += 1;
+        if (prof) { e1 = get_event(); cuda_check(cudaEventRecord(e1, stream_), "rec"); pending_.push_back({e0, e1, 2, 0.0}); }
+    }
+    if (prof) { e2 = get_event(); cuda_check(cudaEventRecord(e2, stream_), "rec"); }
+    launch_sweep();
+    if (prof) { e3 = get_event(); cuda_check(cudaEventRecord(e3, stream_), "rec"); pending_.push_back({e2, e3, 1, 0.0}); }
+}
+
+void Engine::flush_pending() {
+    if (pending_.empty()) return;
+    cuda_check(cudaStreamSynchronize(stream_), "profile sync");
+    for (auto& p : pending_) {
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, p.a, p.b), "elapsed");
+        if (p.kind == 0) { stats_.neuron_ms += ms; stats_.neuron_launches += 1; }
+        else if (p.kind == 1) { stats_.sweep_ms += ms; stats_.sweep_launches += 1; }
+        else if (p.kind == 2) { stats_.exchange_ms += ms; }
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    pending_.clear();
+}
+
+void Engine::simulate(int32_t steps) {
+    require_setup("sn_simulate");
+    if (steps < 1) throw InvalidArgument("mat_run: steps must be >= 1");
+    if (opt_.world > 1 && !comm_)
+        throw LogicError("sn_simulate: partitioned engine needs sn_comm_init (or use sn_step_local/sn_step_finish)");
+    cuda_check(cudaSetDevice(opt_.device), "cudaSetDevice");
+    build_stimulus_table();
+    const int t0 = t_;
+    double* trace = nullptr;
+    if (opt_.record_membrane) {
+        d_trace_.alloc(static_cast<size_t>(steps) * std::max(nl_, 1) * 8);
+        trace = d_trace_.as<double>();
+    }
+    cudaEvent_t eb = get_event(), ee = get_event();
+    if (opt_.stream_io) {
+        // pack each step's stimulus rows into pinned memory; copy per step
+        std::vector<size_t> pos(static_cast<size_t>(steps) + 1, 0);
+        size_t total = 0;
+        for (int s = 0; s < steps; ++s) {
+            const int t = t0 + s;
+            int64_t k = 0;
+            if (t + 1 < static_cast<int>(hs_off_.size())) k = hs_off_[t + 1] - hs_off_[t];
+            pos[s] = total;
+            if (k > 0) total += 16 + static_cast<size_t>(k) * 8 + round_up(static_cast<size_t>(k) * 4, 8);
+        }
+        pos[steps] = total;
+        h_stage_.reserve(std::max<size_t>(total, 64));
+        size_t max_chunk = 64;
+        for (int s = 0; s < steps; ++s) {
+            const int t = t0 + s;
+            const size_t sz = pos[s + 1] - pos[s];
+            if (!sz) continue;
+            max_chunk = std::max(max_chunk, sz);
+            const int64_t lo = hs_off_[t], k = hs_off_[t + 1] - lo;
+            uint8_t* base = h_stage_.as<uint8_t>() + pos[s];
+            int64_t* off = reinterpret_cast<int64_t*>(base);
+            off[0] = 0;
+            off[1] = k;
+            std::memcpy(base + 16, hs_amp_.data() + lo, static_cast<size_t>(k) * 8);
+            std::memcpy(base + 16 + k * 8, hs_neuron_.data() + lo, static_cast<size_t>(k) * 4);
+        }
+        if (d_stage_.bytes < max_chunk) d_stage_.alloc(max_chunk);
+        h_raster_.reserve(static_cast<size_t>(steps) * std::max(nl_words_, 1) * 4);
+        cuda_check(cudaEventRecord(eb, stream_), "rec");
+        for (int s = 0; s < steps; ++s) {
+            const size_t sz = pos[s + 1] - pos[s];
+            const int64_t* st_off = nullptr;
+            const int32_t* st_neuron = nullptr;
+            const double* st_amp = nullptr;
+            int32_t st_steps = 0;
+            if (sz) {
+                cuda_check(cudaMemcpyAsync(d_stage_.p, h_stage_.as<uint8_t>() + pos[s], sz, cudaMemcpyHostToDevice, stream_), "stim H2D");
+                const int64_t k = reinterpret_cast<const int64_t*>(h_stage_.as<uint8_t>() + pos[s])[1];
+                st_off = d_stage_.as<int64_t>();
+                st_amp = reinterpret_cast<const double*>(d_stage_.as<uint8_t>() + 16);
+                st_neuron = reinterpret_cast<const int32_t*>(d_stage_.as<uint8_t>() + 16 + k * 8);
+                st_steps = 1;
+            }
+            NeuronArgs na = neuron_args(t0, steps, nullptr, trace, st_off, st_neuron, st_amp, st_steps, 1);
+            enqueue_step(na, true);
+            if (nl_words_ > 0)
+                cuda_check(cudaMemcpyAsync(h_raster_.as<uint32_t>() + static_cast<size_t>(s) * nl_words_,
+                                           d_bits_.as<uint32_t>() + first_ / 32, static_cast<size_t>(nl_words_) * 4,
+                                           cudaMemcpyDeviceToHost, stream_), "raster D2H");
+        }
+        cuda_check(cudaEventRecord(ee, stream_), "rec");
+        cuda_check(cudaStreamSynchronize(stream_), "simulate sync");
+        RasterChunk ch;
+        ch.t0 = t0;
+        ch.rows = steps;
+        ch.words.assign(h_raster_.as<uint32_t>(), h_raster_.as<uint32_t>() + static_cast<size_t>(steps) * nl_words_);
+        raster_.push_back(std::move(ch));
+    } else {
+        const size_t rbytes = static_cast<size_t>(steps) * std::max(nl_words_, 1) * 4;
+        if (d_raster_.bytes < rbytes) d_raster_.alloc(rbytes);
+        NeuronArgs na = neuron_args(t0, steps, d_raster_.as<uint32_t>(), trace, d_st_off_.as<int64_t>(),
+                                    d_st_neuron_.as<int32_t>(), d_st_amp_.as<double>(), st_steps_dev_, 0);
+        cuda_check(cudaEventRecord(eb, stream_), "rec");
+        if (opt_.use_graphs && !opt_.profile) {
+            cudaGraph_t g;
+            cudaGraphExec_t ge;
+            cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
+            const int64_t launches0 = stats_.kernel_launches;
+            enqueue_step(na, true);
+            const int64_t per_step = stats_.kernel_launches - launches0;
+            cuda_check(cudaStreamEndCapture(stream_, &g), "end capture");
+            cuda_check(cudaGraphInstantiate(&ge, g, 0), "instantiate");
+            for (int s = 0; s < steps; ++s) cuda_check(cudaGraphLaunch(ge, stream_), "graph launch");
+            stats_.kernel_launches += per_step * (steps - 1);
+            cuda_check(cudaEventRecord(ee, stream_), "rec");
+            cuda_check(cudaStreamSynchronize(stream_), "simulate sync");
+            cudaGraphExecDestroy(ge);
+            cudaGraphDestroy(g);
+        } else {
+            for (int s = 0; s < steps; ++s) enqueue_step(na, true);
+            cuda_check(cudaEventRecord(ee, stream_), "rec");
+        }
+        RasterChunk ch;
+        ch.t0 = t0;
+        ch.rows = steps;
+        ch.words.resize(static_cast<size_t>(steps) * nl_words_);
+        if (!ch.words.empty())
+            cuda_check(cudaMemcpyAsync(ch.words.data(), d_raster_.p, ch.words.size() * 4, cudaMemcpyDeviceToHost, stream_), "raster D2H");
+        cuda_check(cudaStreamSynchronize(stream_), "simulate sync");
+        raster_.push_back(std::move(ch));
+    }
+    float ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&ms, eb, ee), "elapsed");
+    cudaEventDestroy(eb);
+    cudaEventDestroy(ee);
+    stats_.last_simulate_ms = ms;
+    flush_pending();
+    if (opt_.record_membrane) {
+        const size_t cnt = static_cast<size_t>(steps) * nl_;
+        const size_t old = trace_.size();
+        trace_.resize(old + cnt);
+        if (cnt) cuda_check(cudaMemcpy(trace_.data() + old, d_trace_.p, cnt * 8, cudaMemcpyDeviceToHost), "trace D2H");
+        trace_rows_ += steps;
+    }
+    t_ += steps;
+    stats_.steps_done = t_;
+    events_valid_ = false;
+}
+
+void Engine::synchronize() { cuda_check(cudaStreamSynchronize(stream_), "sn_synchronize"); }
+
+// ---- host-driven exchange (partition emulation / custom transports) ---------
+void Engine::step_local() {
+    require_setup("sn_step_local");
+    host_exchange_ = true;
+    build_stimulus_table();
+    if (d_raster_.bytes < static_cast<size_t>(std::max(nl_words_, 1)) * 4)
+        d_raster_.alloc(static_cast<size_t>(std::max(nl_words_, 1)) * 4);
+    double* trace = nullptr;
+    if (opt_.record_membrane) {
+        d_trace_.alloc(static_cast<size_t>(std::max(nl_, 1)) * 8);
+        trace = d_trace_.as<double>();
+    }
+    if (opt_.stream_io) throw Unsupported("sn_step_local: stream_io engines use sn_simulate");
+    NeuronArgs na = neuron_args(t_, 1, d_raster_.as<uint32_t>(), trace, d_st_off_.as<int64_t>(),
+                                d_st_neuron_.as<int32_t>(), d_st_amp_.as<double>(), st_steps_dev_, 0);
+    launch_neuron(na, exact_, opt_.world == 1, hist_args(), stream_);
+    stats_.kernel_launches += 1;
+    cuda_check(cudaStreamSynchronize(stream_), "step_local sync");
+}
+
+void Engine::get_spike_words(uint32_t* out, int64_t words) {
+    require_setup("sn_get_spike_words");
+    if (words > words_) throw InvalidArgument("sn_get_spike_words: more words than the bitmask holds");
+    cuda_check(cudaMemcpy(out, d_bits_.p, static_cast<size_t>(words) * 4, cudaMemcpyDeviceToHost), "bits D2H");
+}
+
+void Engine::put_spike_words(int32_t first_word, const uint32_t* w, int64_t count) {
+    require_setup("sn_put_spike_words");
+    if (first_word < 0 || first_word + count > words_) throw InvalidArgument("sn_put_spike_words: range outside the bitmask");
+    cuda_check(cudaMemcpy(d_bits_.as<uint32_t>() + first_word, w, static_cast<size_t>(count) * 4, cudaMemcpyHostToDevice), "bits H2D");
+}
+
+void Engine::step_finish() {
+    require_setup("sn_step_finish");
+    if (opt_.world > 1) {
+        launch_hist(hist_args(), stream_);
+        stats_.kernel_launches += 1;
+    }
+    launch_sweep();
+    RasterChunk ch;
+    ch.t0 = t_;
+    ch.rows = 1;
+    ch.words.resize(static_cast<size_t>(nl_words_));
+    if (nl_words_) cuda_check(cudaMemcpyAsync(ch.words.data(), d_raster_.p, ch.words.size() * 4, cudaMemcpyDeviceToHost, stream_), "raster D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "step_finish sync");
+    raster_.push_back(std::move(ch));
+    if (opt_.record_membrane) {
+        const size_t old = trace_.size();
+        trace_.resize(old + nl_);
+        if (nl_) cuda_check(cudaMemcpy(trace_.data() + old, d_trace_.p, static_cast<size_t>(nl_) * 8, cudaMemcpyDeviceToHost), "trace D2H");
+        trace_rows_ += 1;
+    }
+    t_ += 1;
+    stats_.steps_done = t_;
+    events_valid_ = false;
+}
+
+void Engine::comm_init(const uint8_t* id, int32_t rank, int32_t world) {
+    if (world != opt_.world || rank != opt_.rank)
+        throw InvalidArgument("sn_comm_init: rank/world differ from the engine options");
+    cuda_check(cudaSetDevice(opt_.device), "cudaSetDevice");
+    delete comm_;
+    comm_ = nullptr;
+    if (world > 1) comm_ = new NcclComm(id, rank, world);
+}
+
+// ---- results -------------------------------------------------------------------
+void Engine::decode_raster() {
+    if (events_valid_) return;
+    events_.clear();
+    for (const RasterChunk& ch : raster_) {
+        for (int r = 0; r < ch.rows; ++r) {
+            const uint32_t* row = ch.words.data() + static_cast<size_t>(r) * nl_words_;
+            for (int w = 0; w < nl_words_; ++w) {
+                uint32_t x = row[w];
+                while (x) {
+                    const int b = __builtin_ctz(x);
+                    x &= x - 1;
+                    events_.emplace_back(ch.t0 + r, first_ + w * 32 + b);
+                }
+            }
+        }
+    }
+    events_valid_ = true;
+}
+
+int64_t Engine::raster_size() {
+    require_setup("sn_raster_size");
+    decode_raster();
+    return static_cast<int64_t>(events_.size());
+}
+
+void Engine::get_raster(int32_t* steps, int32_t* neurons, int64_t cap) {
+    require_setup("sn_get_raster");
+    decode_raster();
+    if (cap < static_cast<int64_t>(events_.size()))
+        throw InvalidArgument("sn_get_raster: capacity " + std::to_string(cap) + " < " + std::to_string(events_.size()) + " events");
+    for (size_t i = 0; i < events_.size(); ++i) {
+        steps[i] = events_[i].first;
+        neurons[i] = events_[i].second;
+    }
+}
+
+void Engine::clear_raster() {
+    raster_.clear();
+    events_.clear();
+    events_valid_ = true;
+}
+
+void Engine::get_membrane(double* out, int64_t count) {
+    require_setup("sn_get_membrane");
+    if (count < nl_) throw InvalidArgument("sn_get_membrane: buffer smaller than the local neuron count");
+    if (nl_) cuda_check(cudaMemcpy(out, d_v_.p, static_cast<size_t>(nl_) * 8, cudaMemcpyDeviceToHost), "membrane D2H");
+}
+
+int64_t Engine::trace_rows() { return trace_rows_; }
+
+void Engine::get_trace(double* out, int64_t count) {
+    if (count < static_cast<int64_t>(trace_.size())) throw InvalidArgument("sn_get_membrane_trace: buffer too small");
+    std::memcpy(out, trace_.data(), trace_.size() * 8);
+}
+
+void Engine::get_synapse_weights(double* out, int64_t count) {
+    require_setup("sn_get_synapse_weights");
+    if (generated_) throw Unsupported("sn_get_synapse_weights: generated networks have no synapse list; use sn_get_weight_matrix");
+    if (count < static_cast<int64_t>(pre_.size())) throw InvalidArgument("sn_get_synapse_weights: buffer too small");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    const size_t esz = f64_ ? 8 : 4;
+    std::vector<uint8_t> host(d_w_.bytes);
+    cuda_check(cudaMemcpy(host.data(), d_w_.p, d_w_.bytes, cudaMemcpyDeviceToHost), "weights D2H");
+    for (size_t s = 0; s < pre_.size(); ++s) {
+        if (slot_[s] < 0) { out[s] = 0.0; continue; }
+        if (esz == 8) out[s] = reinterpret_cast<const double*>(host.data())[slot_[s]];
+        else out[s] = static_cast<double>(reinterpret_cast<const float*>(host.data())[slot_[s]]);
+    }
+}
+
+void Engine::get_weight_matrix(double* out, int64_t count) {
+    require_setup("sn_get_weight_matrix");
+    if (count < static_cast<int64_t>(n_) * nl_) throw InvalidArgument("sn_get_weight_matrix: buffer too small");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    std::fill(out, out + static_cast<int64_t>(n_) * nl_, 0.0);
+    const size_t esz = f64_ ? 8 : 4;
+    std::vector<uint8_t> host(d_w_.bytes);
+    cuda_check(cudaMemcpy(host.data(), d_w_.p, d_w_.bytes, cudaMemcpyDeviceToHost), "weights D2H");
+    auto get = [&](int64_t q) {
+        return esz == 8 ? reinterpret_cast<const double*>(host.data())[q]
+                        : static_cast<double>(reinterpret_cast<const float*>(host.data())[q]);
+    };
+    if (dense_) {
+        for (int i = 0; i < n_; ++i)
+            for (int c = 0; c < nl_; ++c) out[static_cast<int64_t>(i) * nl_ + c] = get(static_cast<int64_t>(i) * pitch_ + c);
+    } else {
+        std::vector<int64_t> off(static_cast<size_t>(nblocks_) * nl_ + 1);
+        std::vector<uint32_t> meta(static_cast<size_t>(sparse_elems_));
+        cuda_check(cudaMemcpy(off.data(), d_off_.p, off.size() * 8, cudaMemcpyDeviceToHost), "off D2H");
+        if (!meta.empty()) cuda_check(cudaMemcpy(meta.data(), d_meta_.p, meta.size() * 4, cudaMemcpyDeviceToHost), "meta D2H");
+        for (int b = 0; b < nblocks_; ++b)
+            for (int p = 0; p < nl_; ++p)
+                for (int64_t q = off[static_cast<size_t>(b) * nl_ + p]; q < off[static_cast<size_t>(b) * nl_ + p + 1]; ++q) {
+                    const double w = get(q);
+                    const int i = b * pb_ + static_cast<int>(meta[q] & 0xffffu);
+                    if (w != 0.0) out[static_cast<int64_t>(i) * nl_ + p] = w;
+                }
+    }
+}
+
+void Engine::get_stats(sn_stats* out) {
+    if (setup_done_) {
+        unsigned long long c[2] = {0, 0};
+        cuda_check(cudaMemcpy(c, d_spikes_.p, 16, cudaMemcpyDeviceToHost), "stats D2H");
+        stats_.spike_count = static_cast<int64_t>(c[0]);
+        // algorithmic bytes: every visited row (dense) or every stored synapse (sparse pull)
+        if (dense_) {
+            const double per_row = static_cast<double>(nl_) * ((stdp_on_ ? 2.0 : 1.0) * (f64_ ? 8 : 4) + (has_delay_ ? 1 : 0));
+            stats_.sweep_bytes_total = static_cast<double>(c[1]) * per_row;
+        } else {
+            stats_.sweep_bytes_total = sweep_bytes_full_ * static_cast<double>(t_);
+        }
+        stats_.sweep_bytes_per_launch_last = sweep_bytes_full_;
+    }
+    *out = stats_;
+}
+
+void Engine::reset_stats() {
+    stats_.sweep_ms = stats_.neuron_ms = stats_.exchange_ms = 0.0;
+    stats_.sweep_launches = stats_.neuron_launches = 0;
+    stats_.kernel_launches = 0;
+    stats_.sweep_bytes_total = 0.0;
+    if (setup_done_) cuda_check(cudaMemset(d_spikes_.as<unsigned long long>() + 1, 0, 8), "reset");
+}
+
+}  // namespace snb

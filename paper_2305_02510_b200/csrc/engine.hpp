@@ -1,0 +1,209 @@
+// Host engine behind the C ABI (include/superneuro_mat.h).
+//
+// Mirrors the state the reference keeps in MatState (mat_engine.hpp:56-80)
+// but lays it out for HBM: SoA neuron state for the local post partition,
+// spike history as bit words, weights dense pre-major or blocked CSC.
+#pragma once
+
+#include "../../include/superneuro_mat.h"
+#include "kernels.cuh"
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace snb {
+
+struct InvalidArgument : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct LogicError : std::logic_error {
+    using std::logic_error::logic_error;
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct NcclError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct Unsupported : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct OutOfMemory : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t err, const char* what);
+
+// Owning device allocation.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void alloc(size_t b);
+    void release();
+    template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+// Owning pinned host allocation.
+struct HostBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    HostBuf() = default;
+    HostBuf(const HostBuf&) = delete;
+    HostBuf& operator=(const HostBuf&) = delete;
+    ~HostBuf() { release(); }
+    void reserve(size_t b);
+    void release();
+    template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct RasterChunk {
+    int32_t t0 = 0;
+    int32_t rows = 0;
+    std::vector<uint32_t> words;  // rows x nl_words
+};
+
+struct NcclComm;  // nccl_dl.cpp
+
+class Engine {
+public:
+    explicit Engine(const sn_options& opt);
+    ~Engine();
+
+    void add_neurons(int64_t count, const double* thr, const double* leak, const double* reset,
+                     const int32_t* refr, const int32_t* axonal, int64_t* first_id);
+    void add_synapses(int64_t count, const int32_t* pre, const int32_t* post, const double* w,
+                      const int32_t* delay, const uint8_t* stdp);
+    void add_stimulus(int64_t count, const int32_t* step, const int32_t* neuron, const double* amp);
+    void clear_stimulus();
+    void set_stdp(int32_t window, const double* ap, const double* am, double wmin, double wmax);
+    void generate_er(int32_t n, double p, uint64_t seed, double weight, int32_t delay_max,
+                     uint64_t delay_stream, int32_t by_syn, int32_t stdp);
+    void setup();
+    void simulate(int32_t steps);
+    void synchronize();
+
+    int64_t raster_size();
+    void get_raster(int32_t* steps, int32_t* neurons, int64_t cap);
+    void clear_raster();
+    void get_membrane(double* out, int64_t count);
+    int64_t trace_rows();
+    void get_trace(double* out, int64_t count);
+    void get_synapse_weights(double* out, int64_t count);
+    void get_weight_matrix(double* out, int64_t count);
+    void get_stats(sn_stats* out);
+    void reset_stats();
+
+    void comm_init(const uint8_t* id, int32_t rank, int32_t world);
+    void step_local();
+    void get_spike_words(uint32_t* out, int64_t words);
+    void put_spike_words(int32_t first_word, const uint32_t* w, int64_t count);
+    void step_finish();
+
+    static void partition(int32_t n, int32_t rank, int32_t world, int32_t* first, int32_t* count);
+
+private:
+    void require_not_setup(const char* what) const;
+    void require_setup(const char* what) const;
+    void validate() const;
+    void build_dense_from_lists();
+    void build_sparse_from_lists();
+    void build_generated();
+    void alloc_state();
+    void build_stimulus_table();
+    void plan_launches();
+    NeuronArgs neuron_args(int t_base, int rows, uint32_t* raster, double* trace,
+                           const int64_t* st_off, const int32_t* st_neuron, const double* st_amp,
+                           int32_t st_steps, int32_t st_stream);
+    HistArgs hist_args();
+    void launch_sweep();
+    void enqueue_step(const NeuronArgs& na, bool exchange);
+    void flush_pending();
+    void decode_raster();
+
+    sn_options opt_;
+    cudaStream_t stream_ = nullptr;
+    bool setup_done_ = false;
+
+    // ---- model (host, as given) ----
+    std::vector<double> thr_, leak_, reset_;
+    std::vector<int32_t> refr_, axonal_;
+    std::vector<int32_t> pre_, post_, delay_;
+    std::vector<double> weight_;
+    std::vector<uint8_t> plastic_;
+    std::vector<int32_t> st_step_, st_neuron_;
+    std::vector<double> st_amp_;
+    bool stdp_on_ = false;
+    int32_t window_ = 0;
+    std::vector<double> a_plus_, a_minus_;
+    double w_min_ = 0.0, w_max_ = 1.0;
+    bool generated_ = false;
+    ErArgs er_{};
+    int32_t er_delay_max_ = 1;
+
+    // ---- derived layout ----
+    int32_t n_ = 0, first_ = 0, nl_ = 0, part_ = 0;
+    int32_t words_ = 0, nl_words_ = 0;  // full bitmask words (world * part/32), local words
+    bool dense_ = true, f64_ = false, exact_ = false, has_delay_ = false;
+    int32_t dmax_ = 1, dp_ = 1, hw_ = 1, hbits_ = 1;
+    int64_t pitch_ = 0;
+    bool any_mixed_ = false;
+    int64_t syn_local_ = 0;
+    std::vector<int64_t> slot_;  // synapse list index -> storage element (-1 if not local)
+    // sparse
+    int32_t pb_ = 0, nblocks_ = 0, sub_ = 32, posts_per_cta_ = 0, sparse_gx_ = 1;
+    int64_t sparse_elems_ = 0;
+    // dense plan
+    int32_t tile_w_ = 0, rows_per_chunk_ = 0, nchunks_ = 1, dense_grid_ = 1;
+    double sweep_bytes_full_ = 0.0;  // algorithmic bytes of a sweep over every active row
+
+    // ---- device ----
+    DevBuf d_w_, d_delay_, d_mask_, d_kind_, d_row_plastic_;
+    DevBuf d_off_, d_meta_;
+    DevBuf d_v_, d_thr_, d_leak_, d_reset_, d_refr_, d_cnt_;
+    DevBuf d_bits_, d_hist_, d_hist_lo_, d_active_;
+    DevBuf d_pot64_, d_pot32_, d_dep64_, d_dep32_, d_ap_, d_am_;
+    DevBuf d_partial_, d_uexact_;
+    DevBuf d_step_, d_spikes_;
+    DevBuf d_st_off_, d_st_neuron_, d_st_amp_;
+    int32_t st_steps_dev_ = 0;
+    DevBuf d_stage_;
+    DevBuf d_raster_, d_trace_;
+
+    // ---- host results ----
+    HostBuf h_stage_, h_raster_;
+    std::vector<RasterChunk> raster_;
+    std::vector<std::pair<int32_t, int32_t>> events_;
+    bool events_valid_ = true;
+    std::vector<double> trace_;
+    int64_t trace_rows_ = 0;
+    int32_t t_ = 0;  // host mirror of the device step counter
+
+    // host stimulus CSR (per step, local neurons, summed in list order)
+    std::vector<int64_t> hs_off_;
+    std::vector<int32_t> hs_neuron_;
+    std::vector<double> hs_amp_;
+    bool stim_dirty_ = true;
+
+    // ---- stats / profiling ----
+    sn_stats stats_{};
+    std::vector<cudaEvent_t> ev_pool_;
+    struct Pending {
+        cudaEvent_t a, b;
+        int kind;  // 0 neuron, 1 sweep, 2 exchange, 3 whole
+        double bytes;
+    };
+    std::vector<Pending> pending_;
+    cudaEvent_t get_event();
+    void record_begin(cudaEvent_t& e);
+
+    NcclComm* comm_ = nullptr;
+    bool host_exchange_ = false;
+};
+
+}  // namespace snb

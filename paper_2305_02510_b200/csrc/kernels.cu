@@ -1,0 +1,814 @@
+// sm_100a kernels for the MAT-mode step (SuperNeuro MAT / spikeforge mat_engine).
+//
+// Per simulated step t the engine runs:
+//   k_neuron   LIF update of the local posts          mat_engine.cpp:173-198, model.hpp:127-138
+//              (+ history shift, STDP traces, active-row bitmask when single-partition)
+//   [ncclAllGather of the spike bitmask, then k_hist over all N, when partitioned]
+//   k_dense_sweep / k_sparse_pull
+//              one pass over the weights: STDP update (mat_engine.cpp:242-249) fused
+//              with the spike-gated propagation of step t+1 (mat_engine.cpp:79-93),
+//              so every plastic weight is read and written exactly once per step.
+//
+// All kernels are HBM-streaming integer/fp32 work; no tensor cores (a batch-1
+// binary-spike GEMV is not a dense contraction).
+#include "kernels.cuh"
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace snb {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kSubRows = 1024;   // rows per active-list build in the dense sweep
+constexpr int kHistWordsMax = 8; // history bits <= 512
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+// RandomStream::u64_at / unit_at / below_at (rng.hpp:28-41)
+__device__ __forceinline__ uint64_t u64_at(uint64_t key, uint64_t idx) {
+    return mix64(key + idx * 0x9e3779b97f4a7c15ULL);
+}
+__device__ __forceinline__ double unit_at(uint64_t key, uint64_t idx) {
+    return static_cast<double>(u64_at(key, idx) >> 11) * 0x1.0p-53;
+}
+__device__ __forceinline__ uint64_t below_at(uint64_t key, uint64_t idx, uint64_t n) {
+    return __umul64hi(u64_at(key, idx), n);
+}
+
+// leak_toward (model.hpp:127-138), literally.
+__device__ __forceinline__ double leak_toward(double v, double leak, double reset) {
+    const double d = v - reset;
+    if (d > 0.0) {
+        const double stepped = d - leak;
+        return reset + (stepped > 0.0 ? stepped : 0.0);
+    }
+    if (d < 0.0) {
+        const double stepped = d + leak;
+        return reset + (stepped < 0.0 ? stepped : 0.0);
+    }
+    return v;
+}
+
+// std::clamp(v, lo, hi) (mat_engine.cpp:247) for both precisions.
+template <typename T>
+__device__ __forceinline__ T clamp_ref(T v, T lo, T hi) {
+    return v < lo ? lo : (hi < v ? hi : v);
+}
+
+__device__ __forceinline__ uint32_t bit_of(const uint32_t* bits, int i) {
+    return (__ldg(bits + (i >> 5)) >> (i & 31)) & 1u;
+}
+
+// ---------------------------------------------------------------------------
+// History shift + windowed STDP traces for neuron i (mat_engine.cpp:200-240).
+// hist bit k (across words) = s_i[t-k]; history before step 0 is zero, so the
+// reference's `k > t` break (mat_engine.cpp:230) needs no special casing.
+//   dep_i      = sum_{k=1..W} a_minus[k-1] s_i[t-k]           (k ascending, fp64)
+//   pot_i^(d)  = sum_{k=1..W} a_plus[k-1]  s_i[t-k-d+1]       (lowered-net shift)
+// Returns whether row i must be visited by the sweep this step.
+__device__ __forceinline__ bool hist_update(const HistArgs& h, int i, bool s, int t) {
+    uint64_t words[kHistWordsMax];
+    uint64_t carry = s ? 1ull : 0ull;
+#pragma unroll
+    for (int k = 0; k < kHistWordsMax; ++k) {
+        if (k < h.hw) {
+            const uint64_t x = h.hist[static_cast<int64_t>(k) * h.n + i];
+            const uint64_t nx = (x << 1) | carry;
+            carry = x >> 63;
+            h.hist[static_cast<int64_t>(k) * h.n + i] = nx;
+            words[k] = nx;
+        } else {
+            words[k] = 0;
+        }
+    }
+    if (h.hist_lo) h.hist_lo[i] = static_cast<uint32_t>(words[0]);
+    const uint64_t dmask = h.dmax >= 64 ? ~0ull : ((1ull << h.dmax) - 1ull);
+    bool act = (words[0] & dmask) != 0;
+    if (h.stdp) {
+        // dep: bits 1..W
+        double dep = 0.0;
+        for (int k = 1; k <= h.window; ++k) {
+            const int b = k;
+            if ((words[b >> 6] >> (b & 63)) & 1ull) dep += h.a_minus[k - 1];
+        }
+        h.dep64[i] = dep;
+        h.dep32[i] = static_cast<float>(dep);
+        bool any_pot = false;
+        for (int d = 1; d <= h.dp; ++d) {
+            double pot = 0.0;
+            for (int k = 1; k <= h.window; ++k) {
+                const int b = k + d - 1;
+                if ((words[b >> 6] >> (b & 63)) & 1ull) pot += h.a_plus[k - 1];
+            }
+            h.pot64[static_cast<int64_t>(i) * h.dp + (d - 1)] = pot;
+            h.pot32[static_cast<int64_t>(i) * h.dp + (d - 1)] = static_cast<float>(pot);
+            any_pot |= (pot != 0.0);
+        }
+        // t == 0: apply_stdp clamps every plastic weight even when dw == 0
+        // (mat_engine.cpp:243-249); afterwards weights stay inside the bounds,
+        // so rows with no pairing and no delivery are provably unchanged.
+        if (h.row_plastic[i] && (any_pot || t == 0)) act = true;
+    }
+    return act;
+}
+
+// ---------------------------------------------------------------------------
+// K1: LIF update of the local posts for step t (mat_engine.cpp:168-198).
+template <bool EXACT, bool FUSED>
+__global__ void __launch_bounds__(kThreads) k_neuron(NeuronArgs a, HistArgs h) {
+    const int j = blockIdx.x * kThreads + threadIdx.x;
+    const int t = *a.d_step;
+    const bool valid = j < a.nl;
+    bool s = false;
+    if (valid) {
+        double v = a.v[j];
+        const double reset = a.reset[j];
+        double u;
+        if (EXACT) {
+            u = a.u_exact[j];  // leak(v) + sum in ascending pre order, from the sweep
+        } else {
+            double in = 0.0;
+            for (int c = 0; c < a.nchunks; ++c) in += a.partial[static_cast<int64_t>(c) * a.nl + j];
+            u = leak_toward(v, a.leak[j], reset) + in;
+        }
+        // external stimulus: the step's entries pre-summed in list order
+        // (mat_engine.cpp:271-275); u += ext only when the step has any (179-180)
+        const int row = a.st_stream ? 0 : t;
+        if (row < a.st_steps) {
+            int64_t lo = a.st_off[row], hi = a.st_off[row + 1];
+            if (hi > lo) {
+                const int gj = a.first + j;
+                double ext = 0.0;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    const int nid = a.st_neuron[mid];
+                    if (nid == gj) { ext = a.st_amp[mid]; break; }
+                    if (nid < gj) lo = mid + 1; else hi = mid;
+                }
+                u += ext;
+            }
+        }
+        s = u > a.thr[j];
+        const int c = a.cnt[j];
+        if (c > 0) {  // refractory: silent, held at reset (185-189)
+            s = false;
+            a.cnt[j] = c - 1;
+            u = reset;
+        }
+        if (s) {
+            v = reset;
+            a.cnt[j] = a.refr[j];
+        } else {
+            v = u;
+        }
+        a.v[j] = v;
+        if (a.trace && (t - a.t_base) < a.raster_rows)
+            a.trace[static_cast<int64_t>(t - a.t_base) * a.nl + j] = v;
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, s);
+    const int lane = threadIdx.x & 31;
+    const int wi = j >> 5;
+    if (lane == 0 && wi < a.nl_words) {
+        a.bits[(a.first >> 5) + wi] = word;
+        if (a.raster && (t - a.t_base) < a.raster_rows)
+            a.raster[static_cast<int64_t>(t - a.t_base) * a.nl_words + wi] = word;
+        if (word) atomicAdd(a.spike_count, static_cast<unsigned long long>(__popc(word)));
+    }
+    if (FUSED) {
+        bool act = false;
+        if (valid) act = hist_update(h, j, s, t);
+        const uint32_t aw = __ballot_sync(0xffffffffu, act);
+        if (lane == 0 && wi < a.nl_words) {
+            h.active[wi] = aw;
+            if (aw) atomicAdd(h.active_count, static_cast<unsigned long long>(__popc(aw)));
+        }
+    }
+}
+
+// Partitioned runs: history/traces for all N from the all-gathered bitmask.
+__global__ void __launch_bounds__(kThreads) k_hist(HistArgs h) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    const int t = *h.d_step;
+    bool act = false;
+    if (i < h.n) {
+        const bool s = (h.bits[i >> 5] >> (i & 31)) & 1u;
+        act = hist_update(h, i, s, t);
+    }
+    const uint32_t aw = __ballot_sync(0xffffffffu, act);
+    if ((threadIdx.x & 31) == 0 && (i >> 5) < ((h.n + 31) >> 5)) {
+        h.active[i >> 5] = aw;
+        if (aw) atomicAdd(h.active_count, static_cast<unsigned long long>(__popc(aw)));
+    }
+}
+
+__global__ void k_prologue(double* u, const double* v, const double* leak, const double* reset,
+                           int nl) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < nl) u[j] = leak_toward(v[j], leak[j], reset[j]);
+}
+
+__global__ void k_step_bump(int32_t* d_step) { *d_step += 1; }
+
+// ---------------------------------------------------------------------------
+// Dense sweep: W[pre][post] row-major (pre-major like mat_engine.cpp:34-38),
+// column tiles x row chunks.  For each active row i (ascending) and each of the
+// thread's VEC local columns j:
+//   plastic: w' = clamp(w + s_j[t] pot_i^(d) - e_ij dep_j, w_min, w_max)
+//   e_ij = s_i[t+1-d_ij] (history bit d-1): input to post j at step t+1
+//   acc_j += e_ij * w'
+// Non-exact: per-thread fp32 group sums of U rows promoted to fp64, partials
+// per row chunk summed by k_neuron in chunk order (deterministic; exact for
+// integer nets).  Exact: one chunk, fp64 accumulator seeded with leak(v_j)
+// and rows added in ascending order exactly as mat_step does.
+template <typename WT> struct VecT;
+template <> struct VecT<float> {
+    using V = float4;
+    static constexpr int N = 4;
+    __device__ static V load(const float* p) { return __ldcs(reinterpret_cast<const float4*>(p)); }
+    __device__ static void store(float* p, const V& v) { __stcs(reinterpret_cast<float4*>(p), v); }
+    __device__ static float get(const V& v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
+    __device__ static void set(V& v, int k, float x) {
+        if (k == 0) v.x = x; else if (k == 1) v.y = x; else if (k == 2) v.z = x; else v.w = x;
+    }
+};
+template <> struct VecT<double> {
+    using V = double2;
+    static constexpr int N = 2;
+    __device__ static V load(const double* p) { return __ldcs(reinterpret_cast<const double2*>(p)); }
+    __device__ static void store(double* p, const V& v) { __stcs(reinterpret_cast<double2*>(p), v); }
+    __device__ static double get(const V& v, int k) { return k == 0 ? v.x : v.y; }
+    __device__ static void set(V& v, int k, double x) { if (k == 0) v.x = x; else v.y = x; }
+};
+
+template <typename WT, bool STDP, bool DELAY, bool EXACT>
+__global__ void __launch_bounds__(kThreads) k_dense_sweep(DenseArgs a) {
+    using VT = VecT<WT>;
+    using V = typename VT::V;
+    constexpr int VEC = VT::N;
+    constexpr int U = 8;  // rows in flight per thread
+
+    __shared__ int32_t s_rows[kSubRows];
+    __shared__ uint64_t s_e[kSubRows];
+    __shared__ WT s_pot[STDP && !DELAY ? kSubRows : 1];
+    __shared__ uint8_t s_kind[kSubRows];
+    __shared__ uint32_t s_word[32];
+    __shared__ int32_t s_wpref[33];
+
+    const int tid = threadIdx.x;
+    const int ntiles = (a.nl + a.tile_w - 1) / a.tile_w;
+    const int items = ntiles * a.nchunks;
+    const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
+    const WT* pot = static_cast<const WT*>(a.pot);
+    const WT* dep = static_cast<const WT*>(a.dep);
+    WT* W = static_cast<WT*>(a.w);
+    const uint64_t dmask = DELAY ? ~0ull : 1ull;
+
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int chunk = item / ntiles;
+        const int tile = item - chunk * ntiles;
+        const int tcol = tid * VEC;
+        const int c0 = tile * a.tile_w + tcol;
+        const bool in_tile = tcol < a.tile_w && c0 < a.nl;
+        const int r0 = chunk * a.rows_per_chunk;
+        const int r1 = min(a.n, r0 + a.rows_per_chunk);
+
+        bool sj[VEC];
+        WT depj[VEC];
+        int gc[VEC];
+        double acc[VEC];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+            gc[k] = a.first + c0 + k;
+            const bool ok = in_tile && (c0 + k) < a.nl;
+            sj[k] = ok && STDP ? bit_of(a.bits, gc[k]) : false;
+            depj[k] = ok && STDP ? dep[gc[k]] : WT(0);
+            acc[k] = (EXACT && ok) ? leak_toward(a.v[c0 + k], a.leak[c0 + k], a.reset[c0 + k]) : 0.0;
+        }
+
+        for (int sa = r0; sa < r1; sa += kSubRows) {
+            const int sb = min(r1, sa + kSubRows);
+            const int nwords = (sb - sa + 31) >> 5;
+            __syncthreads();  // previous sub-chunk fully consumed
+            if (tid < 32) {
+                uint32_t wd = 0;
+                if (tid < nwords) {
+                    wd = a.active[(sa >> 5) + tid];
+                    const int rem = sb - (sa + tid * 32);
+                    if (rem < 32) wd &= (rem <= 0) ? 0u : ((1u << rem) - 1u);
+                }
+                const int c = __popc(wd);
+                int incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int x = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (tid >= o) incl += x;
+                }
+                s_word[tid] = wd;
+                s_wpref[tid] = incl - c;
+                if (tid == 31) s_wpref[32] = incl;
+            }
+            __syncthreads();
+            for (int r = sa + tid; r < sb; r += kThreads) {
+                const int l = (r - sa) >> 5, b = (r - sa) & 31;
+                const uint32_t wd = s_word[l];
+                if ((wd >> b) & 1u) {
+                    const int pos = s_wpref[l] + __popc(wd & ((1u << b) - 1u));
+                    s_rows[pos] = r;
+                    s_e[pos] = __ldg(a.hist + r) & dmask;
+                    if (STDP) s_kind[pos] = __ldg(a.kind + r);
+                    if (STDP && !DELAY) s_pot[pos] = pot[r];
+                }
+            }
+            __syncthreads();
+            const int cnt = s_wpref[32];
+
+            for (int base = 0; base < cnt; base += U) {
+                V wv[U];
+                uint32_t dv[U];
+                uint32_t mv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int idx = base + u;
+                    dv[u] = 0x01010101u;
+                    mv[u] = 0;
+                    if (idx < cnt && in_tile) {
+                        const int row = s_rows[idx];
+                        const int64_t off = static_cast<int64_t>(row) * a.pitch + c0;
+                        wv[u] = VT::load(W + off);
+                        if (DELAY) {
+                            if (VEC == 4) dv[u] = __ldg(reinterpret_cast<const uint32_t*>(a.delay + off));
+                            else dv[u] = __ldg(reinterpret_cast<const uint16_t*>(a.delay + off));
+                        }
+                        if (STDP && s_kind[idx] == kRowMixed)
+                            mv[u] = __ldg(a.mask + static_cast<int64_t>(row) * (a.pitch >> 5) + (c0 >> 5)) >> (c0 & 31);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < VEC; ++k) VT::set(wv[u], k, WT(0));
+                    }
+                }
+                WT grp[VEC];
+#pragma unroll
+                for (int k = 0; k < VEC; ++k) grp[k] = WT(0);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int idx = base + u;
+                    if (idx >= cnt || !in_tile) continue;
+                    const int row = s_rows[idx];
+                    const uint64_t ebits = s_e[idx];
+                    bool changed = false;
+                    uint8_t kind = STDP ? s_kind[idx] : uint8_t(kRowNone);
+#pragma unroll
+                    for (int k = 0; k < VEC; ++k) {
+                        WT w = VT::get(wv[u], k);
+                        const int d1 = DELAY ? static_cast<int>((dv[u] >> (8 * k)) & 0xffu) - 1 : 0;
+                        const bool e = (ebits >> d1) & 1ull;
+                        if (STDP && kind != kRowNone) {
+                            const bool pl = kind == kRowAll || (kind == kRowAllButSelf && gc[k] != row) ||
+                                            (kind == kRowMixed && ((mv[u] >> k) & 1u));
+                            if (pl) {
+                                const WT p = DELAY ? pot[static_cast<int64_t>(row) * a.dp + d1] : s_pot[idx];
+                                // dw = 0; if s_post: dw += pot; if s_pre: dw -= dep (243-246)
+                                WT dw = WT(0);
+                                if (sj[k]) dw += p;
+                                if (e) dw -= depj[k];
+                                const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
+                                changed |= (nw != w);
+                                w = nw;
+                                VT::set(wv[u], k, nw);
+                            }
+                        }
+                        if (e) {
+                            if (EXACT) acc[k] += static_cast<double>(w);
+                            else grp[k] += w;
+                        }
+                    }
+                    if (STDP && changed) {
+                        VT::store(W + static_cast<int64_t>(row) * a.pitch + c0, wv[u]);
+                    }
+                }
+                if (!EXACT) {
+#pragma unroll
+                    for (int k = 0; k < VEC; ++k) acc[k] += static_cast<double>(grp[k]);
+                }
+            }
+        }
+        if (in_tile) {
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) {
+                if (c0 + k < a.nl) {
+                    if (EXACT) a.u_exact[c0 + k] = acc[k];
+                    else a.partial[static_cast<int64_t>(chunk) * a.nl + c0 + k] = acc[k];
+                }
+            }
+        }
+    }
+    if (blockIdx.x == 0 && tid == 0) *a.d_step += 1;  // no other CTA reads it
+}
+
+// ---------------------------------------------------------------------------
+// Sparse pull: blocked CSC.  CTA (post group, pre block b) stages the spike
+// history of the block's pres in shared memory, then SUB lanes per post walk
+// the post's incoming list (pre ascending, padded to 4) with 128-bit loads:
+//   e = s_pre[t+1-d]  (history bit d-1)    acc += e * w'
+// Replaces the CSR branch of WeightMatrix::propagate (mat_engine.cpp:88-92)
+// and the oracle's delivery queue (oracle.cpp:91-95) without atomics.
+template <int HB> struct HistT { using T = uint64_t; };
+template <> struct HistT<16> { using T = uint16_t; };
+template <> struct HistT<32> { using T = uint32_t; };
+
+template <typename WT, bool STDP, int HB, int SUB>
+__global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    using HT = typename HistT<HB>::T;
+    const int b = blockIdx.y;
+    const int pre0 = b * a.pb;
+    const int pcount = min(a.pb, a.n - pre0);
+    const int tid = threadIdx.x;
+    // stage history of this pre block
+    if (HB == 1) {
+        uint32_t* sb = reinterpret_cast<uint32_t*>(smem_raw);
+        const int nw = (pcount + 31) >> 5;
+        for (int k = tid; k < nw; k += kThreads) sb[k] = __ldg(a.bits + (pre0 >> 5) + k);
+    } else {
+        HT* sh = reinterpret_cast<HT*>(smem_raw);
+        for (int k = tid; k < pcount; k += kThreads) {
+            if (HB == 64) sh[k] = static_cast<HT>(__ldg(a.hist + pre0 + k));
+            else sh[k] = static_cast<HT>(__ldg(a.hist_lo + pre0 + k));
+        }
+    }
+    __syncthreads();
+    const uint32_t* sbits = reinterpret_cast<const uint32_t*>(smem_raw);
+    const HT* shist = reinterpret_cast<const HT*>(smem_raw);
+
+    const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
+    const WT* pot = static_cast<const WT*>(a.pot);
+    const WT* dep = static_cast<const WT*>(a.dep);
+    WT* W = static_cast<WT*>(a.w);
+
+    const int p0 = blockIdx.x * a.posts_per_cta;
+    const int p1 = min(a.nl, p0 + a.posts_per_cta);
+    constexpr int PER_WARP = 32 / SUB;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int sg = lane / SUB, sl = lane % SUB;
+    for (int pb = p0 + warp * PER_WARP; pb < p1; pb += (kThreads / 32) * PER_WARP) {
+        const int p = pb + sg;
+        const bool valid = p < p1;
+        WT sum = WT(0);
+        if (valid) {
+            const int64_t beg = a.off[static_cast<int64_t>(b) * a.nl + p];
+            const int64_t end = a.off[static_cast<int64_t>(b) * a.nl + p + 1];
+            const int gp = a.first + p;
+            bool sp = false;
+            WT depp = WT(0);
+            if (STDP) {
+                sp = bit_of(a.bits, gp);
+                depp = dep[gp];
+            }
+#pragma unroll 2
+            for (int64_t q = beg + sl * 4; q < end; q += SUB * 4) {
+                const uint4 m4 = __ldcs(reinterpret_cast<const uint4*>(a.meta + q));
+                WT wv[4];
+                if (sizeof(WT) == 4) {
+                    const float4 f = __ldcs(reinterpret_cast<const float4*>(W + q));
+                    wv[0] = f.x; wv[1] = f.y; wv[2] = f.z; wv[3] = f.w;
+                } else {
+                    const double2 f0 = __ldcs(reinterpret_cast<const double2*>(W + q));
+                    const double2 f1 = __ldcs(reinterpret_cast<const double2*>(W + q + 2));
+                    wv[0] = f0.x; wv[1] = f0.y; wv[2] = f1.x; wv[3] = f1.y;
+                }
+                const uint32_t ms[4] = {m4.x, m4.y, m4.z, m4.w};
+                bool changed = false;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t m = ms[k];
+                    const int pl = static_cast<int>(m & 0xffffu);
+                    const int d1 = static_cast<int>((m >> 16) & 63u);
+                    uint32_t e;
+                    if (HB == 1) e = (sbits[pl >> 5] >> (pl & 31)) & 1u;
+                    else e = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
+                    WT w = wv[k];
+                    if (STDP && ((m >> 22) & 1u)) {
+                        const WT pt = pot[static_cast<int64_t>(pre0 + pl) * a.dp + d1];
+                        WT dw = WT(0);
+                        if (sp) dw += pt;
+                        if (e) dw -= depp;
+                        const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
+                        changed |= (nw != w);
+                        w = nw;
+                        wv[k] = nw;
+                    }
+                    if (e) sum += w;
+                }
+                if (STDP && changed) {
+                    if (sizeof(WT) == 4) {
+                        __stcs(reinterpret_cast<float4*>(W + q),
+                               make_float4(float(wv[0]), float(wv[1]), float(wv[2]), float(wv[3])));
+                    } else {
+                        __stcs(reinterpret_cast<double2*>(W + q), make_double2(double(wv[0]), double(wv[1])));
+                        __stcs(reinterpret_cast<double2*>(W + q + 2), make_double2(double(wv[2]), double(wv[3])));
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int o = SUB / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (valid && sl == 0) a.partial[static_cast<int64_t>(b) * a.nl + p] = static_cast<double>(sum);
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *a.d_step += 1;
+}
+
+// Sparse exact: one thread per post, ascending pre, fp64 seeded with leak(v).
+template <typename WT, bool STDP>
+__global__ void __launch_bounds__(kThreads) k_sparse_exact(SparseArgs a) {
+    const int p = blockIdx.x * kThreads + threadIdx.x;
+    if (p < a.nl) {
+        const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
+        const WT* pot = static_cast<const WT*>(a.pot);
+        const WT* dep = static_cast<const WT*>(a.dep);
+        WT* W = static_cast<WT*>(a.w);
+        const int gp = a.first + p;
+        const bool sp = STDP ? bit_of(a.bits, gp) : false;
+        const WT depp = STDP ? dep[gp] : WT(0);
+        double acc = leak_toward(a.v[p], a.leak[p], a.reset[p]);
+        for (int b = 0; b < a.nblocks; ++b) {
+            const int64_t beg = a.off[static_cast<int64_t>(b) * a.nl + p];
+            const int64_t end = a.off[static_cast<int64_t>(b) * a.nl + p + 1];
+            for (int64_t q = beg; q < end; ++q) {
+                const uint32_t m = a.meta[q];
+                const int pre = b * a.pb + static_cast<int>(m & 0xffffu);
+                const int d1 = static_cast<int>((m >> 16) & 63u);
+                const bool e = (a.hist[pre] >> d1) & 1ull;
+                WT w = W[q];
+                if (STDP && ((m >> 22) & 1u)) {
+                    const WT pt = pot[static_cast<int64_t>(pre) * a.dp + d1];
+                    WT dw = WT(0);
+                    if (sp) dw += pt;
+                    if (e) dw -= depp;
+                    w = clamp_ref<WT>(w + dw, wmin, wmax);
+                    W[q] = w;
+                }
+                if (e) acc += static_cast<double>(w);
+            }
+        }
+        a.u_exact[p] = acc;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.d_step += 1;
+}
+
+// ---------------------------------------------------------------------------
+// On-device erdos_renyi (netgen.cpp:36-51): pair (i, j), i != j, exists iff
+// unit_at(i*n + j) < p on stream 1 -- bit-identical draws.
+__device__ __forceinline__ bool er_edge(const ErArgs& e, int i, int j) {
+    if (i == j || !(e.p > 0.0)) return false;
+    if (e.p >= 1.0) return true;  // unit_at < 1 always
+    const uint64_t pair = static_cast<uint64_t>(i) * static_cast<uint64_t>(e.n) + static_cast<uint64_t>(j);
+    return unit_at(e.edge_key, pair) < e.p;
+}
+__device__ __forceinline__ int er_delay(const ErArgs& e, int i, int j) {
+    if (e.delay_max <= 1) return 1;
+    uint64_t key;
+    if (e.delay_by_synapse_index)  // p == 1: synapse index of (i, j) in list order
+        key = static_cast<uint64_t>(i) * static_cast<uint64_t>(e.n - 1) + static_cast<uint64_t>(j - (j > i ? 1 : 0));
+    else
+        key = static_cast<uint64_t>(i) * static_cast<uint64_t>(e.n) + static_cast<uint64_t>(j);
+    return 1 + static_cast<int>(below_at(e.delay_key, key, static_cast<uint64_t>(e.delay_max)));
+}
+
+template <typename WT>
+__global__ void k_er_dense(ErArgs e, WT* w, uint8_t* delay, uint32_t* mask, int first, int nl,
+                           int64_t pitch) {
+    const int i = blockIdx.y;
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // < pitch
+    if (c >= pitch) return;
+    const int j = first + static_cast<int>(c);
+    const bool present = c < nl && er_edge(e, i, j);
+    const int64_t off = static_cast<int64_t>(i) * pitch + c;
+    w[off] = present ? (sizeof(WT) == 4 ? WT(e.weight_f) : WT(e.weight_d)) : WT(0);
+    if (delay) delay[off] = static_cast<uint8_t>(present ? er_delay(e, i, j) : 1);
+    if (mask) {
+        const uint32_t word = __ballot_sync(0xffffffffu, present && e.stdp);
+        if ((threadIdx.x & 31) == 0) mask[static_cast<int64_t>(i) * (pitch >> 5) + (c >> 5)] = word;
+    }
+}
+
+__global__ void k_er_sparse_count(ErArgs e, int first, int nl, int pb, int nblocks, int64_t* counts) {
+    const int64_t tidg = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tidg >= static_cast<int64_t>(nl) * nblocks) return;
+    const int b = static_cast<int>(tidg / nl);
+    const int p = static_cast<int>(tidg - static_cast<int64_t>(b) * nl);
+    const int j = first + p;
+    const int i0 = b * pb, i1 = min(e.n, i0 + pb);
+    int64_t cnt = 0;
+    for (int i = i0; i < i1; ++i) cnt += er_edge(e, i, j) ? 1 : 0;
+    counts[tidg] = cnt;
+}
+
+template <typename WT>
+__global__ void k_er_sparse_fill(ErArgs e, int first, int nl, int pb, int nblocks, const int64_t* off,
+                                 uint32_t* meta, WT* w) {
+    const int64_t tidg = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tidg >= static_cast<int64_t>(nl) * nblocks) return;
+    const int b = static_cast<int>(tidg / nl);
+    const int p = static_cast<int>(tidg - static_cast<int64_t>(b) * nl);
+    const int j = first + p;
+    const int i0 = b * pb, i1 = min(e.n, i0 + pb);
+    int64_t q = off[tidg];
+    const int64_t end = off[tidg + 1];
+    const WT wt = sizeof(WT) == 4 ? WT(e.weight_f) : WT(e.weight_d);
+    for (int i = i0; i < i1; ++i) {
+        if (!er_edge(e, i, j)) continue;
+        const int d = er_delay(e, i, j);
+        meta[q] = static_cast<uint32_t>(i - i0) | (static_cast<uint32_t>(d - 1) << 16) |
+                  (e.stdp ? (1u << 22) : 0u);
+        w[q] = wt;
+        ++q;
+    }
+    for (; q < end; ++q) {  // padding: never delivers, never plastic
+        meta[q] = 0;
+        w[q] = WT(0);
+    }
+}
+
+void check(cudaError_t err, const char* what) {
+    if (err != cudaSuccess)
+        throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(err));
+}
+
+}  // namespace
+
+uint64_t stream_key(uint64_t seed, uint64_t stream) {
+    // RandomStream(seed, stream, 0, 0) key derivation (rng.hpp:19-24)
+    uint64_t k = mix64(seed + 0x9e3779b97f4a7c15ULL);
+    k = mix64(k ^ stream);
+    k = mix64(k ^ 0ull);
+    return mix64(k ^ 0ull);
+}
+
+int dense_vec(bool f64) { return f64 ? 2 : 4; }
+int dense_threads() { return kThreads; }
+int sparse_block_pres(int hbits) {
+    // 32 KB of staged history per CTA (pre ids are 16-bit block-local)
+    switch (hbits) {
+        case 1: return 65536;
+        case 16: return 16384;
+        case 32: return 8192;
+        default: return 4096;
+    }
+}
+
+void launch_neuron(const NeuronArgs& a, bool exact, bool fused, const HistArgs& h, cudaStream_t s) {
+    const int grid = (a.nl + kThreads - 1) / kThreads;
+    if (grid == 0) return;
+    if (exact) {
+        if (fused) k_neuron<true, true><<<grid, kThreads, 0, s>>>(a, h);
+        else k_neuron<true, false><<<grid, kThreads, 0, s>>>(a, h);
+    } else {
+        if (fused) k_neuron<false, true><<<grid, kThreads, 0, s>>>(a, h);
+        else k_neuron<false, false><<<grid, kThreads, 0, s>>>(a, h);
+    }
+    check(cudaGetLastError(), "k_neuron");
+}
+
+void launch_hist(const HistArgs& h, cudaStream_t s) {
+    const int grid = (h.n + kThreads - 1) / kThreads;
+    k_hist<<<grid, kThreads, 0, s>>>(h);
+    check(cudaGetLastError(), "k_hist");
+}
+
+void launch_prologue(double* u, const double* v, const double* leak, const double* reset, int nl,
+                     cudaStream_t s) {
+    if (nl <= 0) return;
+    k_prologue<<<(nl + 255) / 256, 256, 0, s>>>(u, v, leak, reset, nl);
+    check(cudaGetLastError(), "k_prologue");
+}
+
+void launch_step_bump(int32_t* d_step, cudaStream_t s) {
+    k_step_bump<<<1, 1, 0, s>>>(d_step);
+    check(cudaGetLastError(), "k_step_bump");
+}
+
+template <typename WT, bool STDP, bool DELAY, bool EXACT>
+static void dense_go(const DenseArgs& a, int grid, cudaStream_t s) {
+    k_dense_sweep<WT, STDP, DELAY, EXACT><<<grid, kThreads, 0, s>>>(a);
+}
+
+void launch_dense(const DenseArgs& a, bool f64, bool stdp, bool delay, bool exact, int grid,
+                  cudaStream_t s) {
+#define SNB_DENSE(WT)                                                            \
+    do {                                                                         \
+        if (stdp) {                                                              \
+            if (delay) {                                                         \
+                if (exact) dense_go<WT, true, true, true>(a, grid, s);           \
+                else dense_go<WT, true, true, false>(a, grid, s);                \
+            } else {                                                             \
+                if (exact) dense_go<WT, true, false, true>(a, grid, s);          \
+                else dense_go<WT, true, false, false>(a, grid, s);               \
+            }                                                                    \
+        } else {                                                                 \
+            if (delay) {                                                         \
+                if (exact) dense_go<WT, false, true, true>(a, grid, s);          \
+                else dense_go<WT, false, true, false>(a, grid, s);               \
+            } else {                                                             \
+                if (exact) dense_go<WT, false, false, true>(a, grid, s);         \
+                else dense_go<WT, false, false, false>(a, grid, s);              \
+            }                                                                    \
+        }                                                                        \
+    } while (0)
+    if (f64) SNB_DENSE(double);
+    else SNB_DENSE(float);
+#undef SNB_DENSE
+    check(cudaGetLastError(), "k_dense_sweep");
+}
+
+template <typename WT, bool STDP, int HB>
+static void sparse_go_sub(const SparseArgs& a, int sub, int gx, size_t smem, cudaStream_t s) {
+    dim3 grid(gx, a.nblocks);
+    switch (sub) {
+        case 4: k_sparse_pull<WT, STDP, HB, 4><<<grid, kThreads, smem, s>>>(a); break;
+        case 8: k_sparse_pull<WT, STDP, HB, 8><<<grid, kThreads, smem, s>>>(a); break;
+        case 16: k_sparse_pull<WT, STDP, HB, 16><<<grid, kThreads, smem, s>>>(a); break;
+        default: k_sparse_pull<WT, STDP, HB, 32><<<grid, kThreads, smem, s>>>(a); break;
+    }
+}
+
+template <typename WT, bool STDP>
+static void sparse_go(const SparseArgs& a, int hbits, int sub, int gx, cudaStream_t s) {
+    size_t smem;
+    switch (hbits) {
+        case 1:
+            smem = static_cast<size_t>((a.pb + 31) / 32) * 4;
+            sparse_go_sub<WT, STDP, 1>(a, sub, gx, smem, s);
+            break;
+        case 16:
+            smem = static_cast<size_t>(a.pb) * 2;
+            sparse_go_sub<WT, STDP, 16>(a, sub, gx, smem, s);
+            break;
+        case 32:
+            smem = static_cast<size_t>(a.pb) * 4;
+            sparse_go_sub<WT, STDP, 32>(a, sub, gx, smem, s);
+            break;
+        default:
+            smem = static_cast<size_t>(a.pb) * 8;
+            sparse_go_sub<WT, STDP, 64>(a, sub, gx, smem, s);
+            break;
+    }
+}
+
+void launch_sparse(const SparseArgs& a, bool f64, bool stdp, int hbits, int sub, bool exact, int gx,
+                   cudaStream_t s) {
+    if (exact) {
+        const int grid = (a.nl + kThreads - 1) / kThreads;
+        if (grid == 0) {
+            launch_step_bump(a.d_step, s);
+            return;
+        }
+        if (f64) {
+            if (stdp) k_sparse_exact<double, true><<<grid, kThreads, 0, s>>>(a);
+            else k_sparse_exact<double, false><<<grid, kThreads, 0, s>>>(a);
+        } else {
+            if (stdp) k_sparse_exact<float, true><<<grid, kThreads, 0, s>>>(a);
+            else k_sparse_exact<float, false><<<grid, kThreads, 0, s>>>(a);
+        }
+    } else {
+        if (f64) {
+            if (stdp) sparse_go<double, true>(a, hbits, sub, gx, s);
+            else sparse_go<double, false>(a, hbits, sub, gx, s);
+        } else {
+            if (stdp) sparse_go<float, true>(a, hbits, sub, gx, s);
+            else sparse_go<float, false>(a, hbits, sub, gx, s);
+        }
+    }
+    check(cudaGetLastError(), "k_sparse");
+}
+
+void launch_er_dense(const ErArgs& e, void* w, bool f64, uint8_t* delay, uint32_t* mask, int first,
+                     int nl, int64_t pitch, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>((pitch + 255) / 256), static_cast<unsigned>(e.n));
+    if (f64) k_er_dense<double><<<grid, 256, 0, s>>>(e, static_cast<double*>(w), delay, mask, first, nl, pitch);
+    else k_er_dense<float><<<grid, 256, 0, s>>>(e, static_cast<float*>(w), delay, mask, first, nl, pitch);
+    check(cudaGetLastError(), "k_er_dense");
+}
+
+void launch_er_sparse_count(const ErArgs& e, int first, int nl, int pb, int nblocks, int64_t* counts,
+                            cudaStream_t s) {
+    const int64_t tot = static_cast<int64_t>(nl) * nblocks;
+    k_er_sparse_count<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(e, first, nl, pb, nblocks, counts);
+    check(cudaGetLastError(), "k_er_sparse_count");
+}
+
+void launch_er_sparse_fill(const ErArgs& e, int first, int nl, int pb, int nblocks, const int64_t* off,
+                           uint32_t* meta, void* w, bool f64, cudaStream_t s) {
+    const int64_t tot = static_cast<int64_t>(nl) * nblocks;
+    const unsigned g = static_cast<unsigned>((tot + 255) / 256);
+    if (f64) k_er_sparse_fill<double><<<g, 256, 0, s>>>(e, first, nl, pb, nblocks, off, meta, static_cast<double*>(w));
+    else k_er_sparse_fill<float><<<g, 256, 0, s>>>(e, first, nl, pb, nblocks, off, meta, static_cast<float*>(w));
+    check(cudaGetLastError(), "k_er_sparse_fill");
+}
+
+}  // namespace snb

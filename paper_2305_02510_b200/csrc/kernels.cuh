@@ -1,0 +1,167 @@
+// Device-side parameter blocks and launcher declarations for the MAT step.
+// Reference semantics: see DESIGN.md and the per-kernel comments in kernels.cu.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace snb {
+
+// Row (pre-neuron) plasticity classes for dense storage; computed per
+// partition at setup so the sweep needs no mask loads for the common shapes.
+enum RowKind : uint8_t {
+    kRowNone = 0,     // no plastic synapse in this row's local columns
+    kRowAll = 1,      // every local column is a plastic synapse
+    kRowAllButSelf = 2,  // every local column but j == i plastic, (i,i) absent
+    kRowMixed = 3     // consult the plastic bitmask
+};
+
+struct NeuronArgs {
+    // local partition [first, first + nl)
+    int32_t n;            // global neuron count
+    int32_t first;
+    int32_t nl;
+    double* v;
+    const double* thr;
+    const double* leak;
+    const double* reset;
+    const int32_t* refr;
+    int32_t* cnt;
+    // synaptic input
+    const double* partial;     // [nchunks][nl] (non-exact)
+    int32_t nchunks;
+    const double* u_exact;     // [nl] (exact mode)
+    // stimulus: per-step CSR over (neuron asc, amp)
+    const int64_t* st_off;     // [st_steps + 1]
+    const int32_t* st_neuron;
+    const double* st_amp;
+    int32_t st_steps;          // number of steps covered by the table
+    int32_t st_stream;         // 1: table has one row (index 0) for the current step
+    // time
+    int32_t* d_step;           // device step counter (read here; sweep increments)
+    int32_t t_base;            // raster/trace row = t - t_base
+    // outputs
+    uint32_t* bits;            // full bitmask [words]; this kernel writes local words
+    uint32_t* raster;          // [rows][nl_words] or null
+    int32_t nl_words;
+    int32_t raster_rows;
+    double* trace;             // [rows][nl] or null
+    unsigned long long* spike_count;
+};
+
+struct HistArgs {
+    int32_t n;
+    const uint32_t* bits;      // full spike bitmask of step t
+    uint64_t* hist;            // [hw][n]; bit k of the concatenation = s[t-k]
+    int32_t hw;
+    int32_t dmax;              // propagation delay span (bits 0..dmax-1)
+    // STDP traces
+    int32_t stdp;
+    int32_t window;
+    int32_t dp;                // plastic delay span (pot per d = 1..dp)
+    const double* a_plus;
+    const double* a_minus;
+    double* pot64;             // [n][dp]
+    float* pot32;
+    double* dep64;             // [n]
+    float* dep32;
+    const uint8_t* row_plastic;  // [n]
+    uint32_t* active;          // [words] rows that the sweep must visit
+    int32_t* d_step;
+    uint32_t* hist_lo;         // [n] low 32 history bits (sparse pull staging)
+    unsigned long long* active_count;  // running sum of active rows (algorithmic bytes)
+};
+
+struct DenseArgs {
+    int32_t n;                 // rows
+    int32_t first;             // global id of local column 0
+    int32_t nl;                // local columns
+    int64_t pitch;             // elements per row
+    void* w;                   // WT[n][pitch]
+    const uint8_t* delay;      // [n][pitch] or null
+    const uint32_t* mask;      // [n][pitch/32] plastic bits or null
+    const uint8_t* kind;       // [n] RowKind
+    const uint32_t* active;    // [words]
+    const uint64_t* hist;      // word 0 of the history
+    const uint32_t* bits;      // spike bitmask (column spikes s_j[t])
+    const void* pot;           // WT [n][dp]
+    const void* dep;           // WT [n]
+    int32_t dp;
+    double w_min, w_max;
+    int32_t tile_w;            // columns per CTA tile (multiple of VEC)
+    int32_t rows_per_chunk;
+    int32_t nchunks;
+    double* partial;           // [nchunks][nl]
+    // exact mode
+    const double* v;           // local membrane (after this step)
+    const double* leak;
+    const double* reset;
+    double* u_exact;           // [nl]
+    int32_t* d_step;
+};
+
+struct SparseArgs {
+    int32_t n;
+    int32_t first;
+    int32_t nl;
+    int32_t pb;                // pres per block
+    int32_t nblocks;
+    const int64_t* off;        // [nblocks * nl + 1], lists padded to 4
+    const uint32_t* meta;      // pre_local | (d-1) << 16 | plastic << 22
+    void* w;                   // WT[]
+    const uint32_t* bits;
+    const uint32_t* hist_lo;
+    const uint64_t* hist;
+    const void* pot;
+    const void* dep;
+    int32_t dp;
+    double w_min, w_max;
+    int32_t posts_per_cta;
+    double* partial;           // [nblocks][nl]
+    const double* v;
+    const double* leak;
+    const double* reset;
+    double* u_exact;
+    int32_t* d_step;
+};
+
+// ---- launchers (kernels.cu) ----
+void launch_neuron(const NeuronArgs& a, bool exact, bool fused_hist, const HistArgs& h,
+                   cudaStream_t s);
+void launch_hist(const HistArgs& h, cudaStream_t s);
+void launch_dense(const DenseArgs& a, bool f64, bool stdp, bool delay, bool exact, int grid_ctas,
+                  cudaStream_t s);
+int dense_vec(bool f64);
+int dense_threads();
+void launch_sparse(const SparseArgs& a, bool f64, bool stdp, int hbits, int sub, bool exact,
+                   int grid_x, cudaStream_t s);
+void launch_prologue(double* u_exact, const double* v, const double* leak, const double* reset,
+                     int nl, cudaStream_t s);
+void launch_step_bump(int32_t* d_step, cudaStream_t s);
+int sparse_block_pres(int hbits);
+
+// ---- on-device Erdos-Renyi generation (netgen.cpp:36-51 semantics) ----
+struct ErArgs {
+    int32_t n;
+    double p;
+    uint64_t edge_key;         // RandomStream(seed, 1) key
+    uint64_t delay_key;        // RandomStream(seed, delay_stream) key
+    int32_t delay_max;         // <= 1: unit delays
+    int32_t delay_by_synapse_index;
+    float weight_f;
+    double weight_d;
+    int32_t stdp;
+};
+// dense: fills W[n][pitch] for local columns [first, first+nl), delays, mask bits
+void launch_er_dense(const ErArgs& e, void* w, bool f64, uint8_t* delay, uint32_t* mask,
+                     int first, int nl, int64_t pitch, cudaStream_t s);
+// sparse: pass 1 counts per (block, local post); pass 2 fills
+void launch_er_sparse_count(const ErArgs& e, int first, int nl, int pb, int nblocks,
+                            int64_t* counts, cudaStream_t s);
+void launch_er_sparse_fill(const ErArgs& e, int first, int nl, int pb, int nblocks,
+                           const int64_t* off, uint32_t* meta, void* w, bool f64,
+                           cudaStream_t s);
+
+uint64_t stream_key(uint64_t seed, uint64_t stream);
+
+}  // namespace snb

@@ -1,0 +1,130 @@
+"""Regenerates tests/golden/*.npz / scale.json from the REFERENCE's own code
+(oracle/_ref/libspikeforge_ref.so, built by `make -C oracle ref` from
+/root/reference/proj/src).  Run in the build container (the reference tree
+does not exist on the GPU box):
+
+    python tests/golden/make_golden.py
+
+Each case records the reference MAT path's raster, final membrane, final
+synapse weights (list order) and, when asked, the membrane trace.  Delayed
+cases use the reference MAT path for delays: lower_delays -> mat_run ->
+restrict_raster (spikeforge_main.cpp:44-64).
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(HERE))
+
+from oracle import bridge as B  # noqa: E402
+import cases as CS  # noqa: E402
+from paper_2305_02510_b200.model import StdpConfig  # noqa: E402
+from paper_2305_02510_b200.netgen import (DELAY_STREAM, RandomStream, erdos_renyi_arrays,  # noqa: E402
+                                          scenario_stimulus)
+
+
+def raster_digest(steps, neurons) -> str:
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(steps, np.int32).tobytes())
+    h.update(np.ascontiguousarray(neurons, np.int32).tobytes())
+    return h.hexdigest()
+
+
+def run_case(c):
+    return B.run_ref_mat(c.arrays(), c.steps, c.stim_arrays(), c.stdp_tuple(), c.record, lower=c.lower)
+
+
+def dump_suite(fname, cases):
+    out = {}
+    for c in cases:
+        r = run_case(c)
+        out[f"{c.name}/steps"] = r["steps"]
+        out[f"{c.name}/neurons"] = r["neurons"]
+        out[f"{c.name}/membrane"] = r["membrane"]
+        out[f"{c.name}/weights"] = r.get("weights", np.zeros(0))
+        if "membrane_trace" in r:
+            out[f"{c.name}/trace"] = r["membrane_trace"]
+    np.savez_compressed(os.path.join(HERE, fname), **out)
+    print(f"{fname}: {len(cases)} cases")
+
+
+def scenario(n, p, seed, steps, delay_max=1):
+    pre, post = erdos_renyi_arrays(n, p, seed)
+    arrays = {"threshold": np.ones(n), "leak": np.zeros(n), "reset": np.zeros(n),
+              "refractory": np.zeros(n, np.int32), "axonal": np.zeros(n, np.int32),
+              "pre": pre, "post": post, "weight": np.ones(len(pre)),
+              "delay": np.ones(len(pre), np.int32), "stdp": np.zeros(len(pre), np.uint8)}
+    if delay_max > 1:
+        arrays["delay"] = (1 + RandomStream(seed, DELAY_STREAM).below_np(
+            np.arange(len(pre), dtype=np.uint64), delay_max)).astype(np.int32)
+    return arrays, scenario_stimulus(n, steps, seed).to_arrays()
+
+
+def main():
+    B.build(ref=True)
+    dump_suite("kat.npz", CS.kat_cases())
+    dump_suite("rand_unit.npz", CS.random_unit_cases())
+    dump_suite("rand_delay.npz", CS.random_delay_cases())
+    dump_suite("rand_stdp.npz", CS.random_stdp_cases())
+    dump_suite("crit1.npz", CS.crit1_cases())
+    dump_suite("crit7.npz", CS.crit7_cases())
+
+    scale = {"generator": "tests/golden/make_golden.py", "source": "oracle/_ref/libspikeforge_ref.so"}
+    # netgen goldens (test_netgen.cpp:65-69, 124-134)
+    scale["er100_025_counts"] = {str(s): int(len(B.ref_erdos_renyi(100, 0.25, s)[0])) for s in (0, 1, 42)}
+    # scenario rasters (paper protocol, BASELINE cfg1 and the N=1000 p=1 row)
+    for tag, (n, p, seed, steps, dmax) in {
+        "cfg1_seed0": (100, 0.05, 0, 1000, 1),
+        "cfg1_seed1": (100, 0.05, 1, 1000, 1),
+        "cfg1_seed42": (100, 0.05, 42, 1000, 1),
+        "n1000_p1_seed0": (1000, 1.0, 0, 1000, 1),
+    }.items():
+        arrays, stim = scenario(n, p, seed, steps, dmax)
+        t0 = time.time()
+        r = B.run_ref_mat_raster(arrays, steps, stim)
+        scale[tag] = {"n": n, "p": p, "seed": seed, "steps": steps, "spikes": int(len(r["steps"])),
+                      "digest": raster_digest(r["steps"], r["neurons"]), "ref_path": "mat_run",
+                      "ref_seconds": round(time.time() - t0, 3)}
+        print(tag, scale[tag])
+    # cfg2: 1k all-to-all, delays 1..8 keyed by synapse index (acceptance_main.cpp:98-100)
+    arrays, stim = scenario(1000, 1.0, 0, 1000, 8)
+    t0 = time.time()
+    r = B.run_ref_abm(arrays, 1000, stim)
+    scale["cfg2_seed0"] = {"n": 1000, "p": 1.0, "seed": 0, "steps": 1000, "delay_max": 8,
+                           "spikes": int(len(r["steps"])), "digest": raster_digest(r["steps"], r["neurons"]),
+                           "ref_path": "abm_run (== oracle_run == mat_run(lower_delays))",
+                           "ref_seconds": round(time.time() - t0, 3)}
+    print("cfg2", scale["cfg2_seed0"])
+    # dense STDP, defaults, N=1024, T=100
+    n = 1024
+    arrays, stim = scenario(n, 1.0, 0, 100)
+    arrays["stdp"][:] = 1
+    d = StdpConfig.defaults()
+    sd = (d.window, np.array(d.a_plus), np.array(d.a_minus), d.w_min, d.w_max)
+    t0 = time.time()
+    r = B.run_ref_mat(arrays, 100, stim, sd)
+    w = r["weights"]
+    scale["stdp_n1024_seed0"] = {"n": n, "steps": 100, "spikes": int(len(r["steps"])),
+                                 "digest": raster_digest(r["steps"], r["neurons"]),
+                                 "weight_sum": float(np.sum(w)), "weight_min": float(w.min()),
+                                 "weight_max": float(w.max()),
+                                 "membrane_sum": float(np.sum(r["membrane"])),
+                                 "ref_seconds": round(time.time() - t0, 3)}
+    np.savez_compressed(os.path.join(HERE, "stdp_n1024.npz"), weights=w.astype(np.float64),
+                        membrane=r["membrane"])
+    print("stdp", scale["stdp_n1024_seed0"])
+    with open(os.path.join(HERE, "scale.json"), "w") as f:
+        json.dump(scale, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
