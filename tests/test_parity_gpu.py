@@ -64,7 +64,15 @@ def run_engine(c, chunks=None, **cfg):
 
 
 def is_float_case(c):
-    return c.stdp is not None
+    """Exactness needs integer-valued inputs: STDP makes weights fractional,
+    and non-integer weights/amplitudes round differently in fp32 storage or
+    in a different summation order."""
+    if c.stdp is not None:
+        return True
+    a = c.arrays()
+    vals = [a["weight"], a["threshold"], a["reset"], c.stim_arrays()[2]]
+    lk = a["leak"][np.isfinite(a["leak"])]
+    return any(np.any(v != np.round(v)) for v in vals + [lk])
 
 
 SUITES = [
