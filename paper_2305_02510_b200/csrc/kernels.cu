@@ -412,6 +412,192 @@ __global__ void __launch_bounds__(kThreads) k_dense_sweep(DenseArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Streaming variant of the dense sweep (non-exact order), the hot kernel of
+// the STDP configs.  Same arithmetic as k_dense_sweep but shaped for issue
+// efficiency: one 16-byte shared record per active row (row|kind, history
+// bits, pot), the active list padded to a multiple of U with inert rows so
+// the U-row load batch has no bounds checks, 0/1 spike factors folded into
+// FFMA (exact: the factors are 0 or 1), plasticity class dispatched once per
+// row (warp-uniform), unconditional 128-bit streaming stores on plastic rows.
+template <typename WT> struct RowRec;
+template <> struct alignas(16) RowRec<float> {
+    int32_t rowk;      // row | kind << 28
+    uint32_t e_lo, e_hi;
+    float pot;
+};
+template <> struct alignas(16) RowRec<double> {
+    int32_t rowk;
+    uint32_t e_lo, e_hi, pad;
+    double pot;
+    double pad2;
+};
+
+template <typename WT, bool STDP, bool DELAY>
+__global__ void __launch_bounds__(kThreads, 2) k_dense_stream(DenseArgs a) {
+    using VT = VecT<WT>;
+    using V = typename VT::V;
+    constexpr int VEC = VT::N;
+    constexpr int U = 8;
+    __shared__ RowRec<WT> s_rec[kSubRows + U];
+    __shared__ uint32_t s_word[32];
+    __shared__ int32_t s_wpref[33];
+
+    const int tid = threadIdx.x;
+    const int ntiles = (a.nl + a.tile_w - 1) / a.tile_w;
+    const int items = ntiles * a.nchunks;
+    const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
+    const WT* pot = static_cast<const WT*>(a.pot);
+    const WT* dep = static_cast<const WT*>(a.dep);
+    WT* W = static_cast<WT*>(a.w);
+    const int64_t mpitch = a.pitch >> 5;
+
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int chunk = item / ntiles;
+        const int tile = item - chunk * ntiles;
+        const int tcol = tid * VEC;
+        const int c0 = tile * a.tile_w + tcol;
+        const bool in_tile = tcol < a.tile_w && c0 < a.nl;
+        const int gc0 = a.first + c0;
+        const int r0 = chunk * a.rows_per_chunk;
+        const int r1 = min(a.n, r0 + a.rows_per_chunk);
+
+        WT sjf[VEC], depj[VEC];
+        double acc[VEC];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+            const bool ok = in_tile && (c0 + k) < a.nl;
+            sjf[k] = (ok && STDP && bit_of(a.bits, gc0 + k)) ? WT(1) : WT(0);
+            depj[k] = (ok && STDP) ? dep[gc0 + k] : WT(0);
+            acc[k] = 0.0;
+        }
+
+        for (int sa = r0; sa < r1; sa += kSubRows) {
+            const int sb = min(r1, sa + kSubRows);
+            const int nwords = (sb - sa + 31) >> 5;
+            __syncthreads();
+            if (tid < 32) {
+                uint32_t wd = 0;
+                if (tid < nwords) {
+                    wd = a.active[(sa >> 5) + tid];
+                    const int rem = sb - (sa + tid * 32);
+                    if (rem < 32) wd &= (rem <= 0) ? 0u : ((1u << rem) - 1u);
+                }
+                const int c = __popc(wd);
+                int incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int x = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (tid >= o) incl += x;
+                }
+                s_word[tid] = wd;
+                s_wpref[tid] = incl - c;
+                if (tid == 31) s_wpref[32] = incl;
+            }
+            __syncthreads();
+            for (int r = sa + tid; r < sb; r += kThreads) {
+                const int l = (r - sa) >> 5, b = (r - sa) & 31;
+                const uint32_t wd = s_word[l];
+                if ((wd >> b) & 1u) {
+                    const int pos = s_wpref[l] + __popc(wd & ((1u << b) - 1u));
+                    const uint64_t h = __ldg(a.hist + r);
+                    RowRec<WT> rec;
+                    const int kind = STDP ? static_cast<int>(__ldg(a.kind + r)) : 0;
+                    rec.rowk = r | (kind << 28);
+                    rec.e_lo = static_cast<uint32_t>(h);
+                    rec.e_hi = static_cast<uint32_t>(h >> 32);
+                    rec.pot = (STDP && !DELAY) ? pot[r] : WT(0);
+                    s_rec[pos] = rec;
+                }
+            }
+            const int cnt = s_wpref[32];
+            if (tid < U && cnt > 0) {  // inert padding: re-reads row sa, no spike, no store
+                RowRec<WT> rec;
+                rec.rowk = sa;
+                rec.e_lo = rec.e_hi = 0;
+                rec.pot = WT(0);
+                s_rec[cnt + tid] = rec;
+            }
+            __syncthreads();
+            if (!in_tile) continue;
+
+            for (int base = 0; base < cnt; base += U) {
+                V wv[U];
+                uint32_t dv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int row = s_rec[base + u].rowk & 0x0fffffff;
+                    const int64_t off = static_cast<int64_t>(row) * a.pitch + c0;
+                    wv[u] = VT::load(W + off);
+                    if (DELAY) {
+                        if (VEC == 4) dv[u] = __ldg(reinterpret_cast<const uint32_t*>(a.delay + off));
+                        else dv[u] = __ldg(reinterpret_cast<const uint16_t*>(a.delay + off));
+                    }
+                }
+                WT grp[VEC];
+#pragma unroll
+                for (int k = 0; k < VEC; ++k) grp[k] = WT(0);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const RowRec<WT> rec = s_rec[base + u];
+                    const int row = rec.rowk & 0x0fffffff;
+                    const int kind = rec.rowk >> 28;
+                    const uint64_t ebits = (static_cast<uint64_t>(rec.e_hi) << 32) | rec.e_lo;
+                    WT w[VEC], ef[VEC];
+#pragma unroll
+                    for (int k = 0; k < VEC; ++k) {
+                        w[k] = VT::get(wv[u], k);
+                        const int d1 = DELAY ? static_cast<int>((dv[u] >> (8 * k)) & 0xffu) - 1 : 0;
+                        ef[k] = ((ebits >> d1) & 1ull) ? WT(1) : WT(0);
+                    }
+                    if (STDP && kind != kRowNone) {
+                        WT nw[VEC];
+#pragma unroll
+                        for (int k = 0; k < VEC; ++k) {
+                            WT p;
+                            if (DELAY) {
+                                const int d1 = static_cast<int>((dv[u] >> (8 * k)) & 0xffu) - 1;
+                                p = pot[static_cast<int64_t>(row) * a.dp + d1];
+                            } else {
+                                p = rec.pot;
+                            }
+                            // dw = s_post*pot - s_pre*dep (mat_engine.cpp:243-246); 0/1 factors are exact
+                            const WT dw = fma(sjf[k], p, -(ef[k] * depj[k]));
+                            nw[k] = clamp_ref<WT>(w[k] + dw, wmin, wmax);
+                        }
+                        if (kind == kRowAllButSelf) {
+                            const int selfk = row - gc0;   // (i, i) is absent: keep it exactly
+#pragma unroll
+                            for (int k = 0; k < VEC; ++k) nw[k] = (selfk == k) ? w[k] : nw[k];
+                        } else if (kind == kRowMixed) {
+                            const uint32_t mv = __ldg(a.mask + static_cast<int64_t>(row) * mpitch + (c0 >> 5)) >> (c0 & 31);
+#pragma unroll
+                            for (int k = 0; k < VEC; ++k) nw[k] = ((mv >> k) & 1u) ? nw[k] : w[k];
+                        }
+                        V out;
+#pragma unroll
+                        for (int k = 0; k < VEC; ++k) {
+                            VT::set(out, k, nw[k]);
+                            w[k] = nw[k];
+                        }
+                        VT::store(W + static_cast<int64_t>(row) * a.pitch + c0, out);
+                    }
+#pragma unroll
+                    for (int k = 0; k < VEC; ++k) grp[k] = fma(ef[k], w[k], grp[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < VEC; ++k) acc[k] += static_cast<double>(grp[k]);
+            }
+        }
+        if (in_tile) {
+#pragma unroll
+            for (int k = 0; k < VEC; ++k)
+                if (c0 + k < a.nl) a.partial[static_cast<int64_t>(chunk) * a.nl + c0 + k] = acc[k];
+        }
+    }
+    if (blockIdx.x == 0 && tid == 0) *a.d_step += 1;
+}
+
+// ---------------------------------------------------------------------------
 // Sparse pull: blocked CSC.  CTA (post group, pre block b) stages the spike
 // history of the block's pres in shared memory, then SUB lanes per post walk
 // the post's incoming list (pre ascending, padded to 4) with 128-bit loads:
@@ -695,7 +881,8 @@ void launch_step_bump(int32_t* d_step, cudaStream_t s) {
 
 template <typename WT, bool STDP, bool DELAY, bool EXACT>
 static void dense_go(const DenseArgs& a, int grid, cudaStream_t s) {
-    k_dense_sweep<WT, STDP, DELAY, EXACT><<<grid, kThreads, 0, s>>>(a);
+    if (EXACT) k_dense_sweep<WT, STDP, DELAY, true><<<grid, kThreads, 0, s>>>(a);
+    else k_dense_stream<WT, STDP, DELAY><<<grid, kThreads, 0, s>>>(a);
 }
 
 void launch_dense(const DenseArgs& a, bool f64, bool stdp, bool delay, bool exact, int grid,
