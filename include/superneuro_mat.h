@@ -93,7 +93,9 @@ typedef struct sn_options {
     int32_t rank;            /* post-neuron partition index (0 when world == 1) */
     int32_t world;           /* number of partitions / GPUs (1 = single GPU) */
     int32_t profile;         /* 1: time every kernel with CUDA events (sn_get_stats) */
-    int32_t reserved[5];
+    int32_t persistent;      /* 0: auto (one cooperative launch per sn_simulate for small
+                                dense single-GPU nets), -1: never */
+    int32_t reserved[4];
 } sn_options;
 
 typedef struct sn_stats {

@@ -38,7 +38,8 @@ class Options(C.Structure):
         ("rank", C.c_int32),
         ("world", C.c_int32),
         ("profile", C.c_int32),
-        ("reserved", C.c_int32 * 5),
+        ("persistent", C.c_int32),
+        ("reserved", C.c_int32 * 4),
     ]
 
 

@@ -554,7 +554,28 @@ void Engine::alloc_state() {
 void Engine::plan_launches() {
     int sms = 148;
     cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt_.device), "attr");
-    if (dense_) {
+    const size_t esz = f64_ ? 8 : 4;
+    persistent_ = opt_.persistent >= 0 && dense_ && !exact_ && opt_.world == 1 && !opt_.stream_io && nl_ > 0 &&
+                  static_cast<double>(n_) * pitch_ * esz <= 64.0 * 1024 * 1024;  // L2-resident
+    if (persistent_) {
+        // 32-row chunks; split columns until the items fill the co-resident CTAs
+        const int vec = dense_vec(f64_);
+        const int resident = persistent_max_ctas(f64_, stdp_on_, has_delay_);
+        rows_per_chunk_ = 32;
+        nchunks_ = (n_ + 31) / 32;
+        const int max_tiles = std::max(1, (nl_ + 32 * vec - 1) / (32 * vec));
+        int ntiles = std::min(max_tiles, std::max(1, (resident + nchunks_ - 1) / nchunks_));
+        ntiles = std::min(ntiles, std::max(1, (nl_ + dense_threads() * vec - 1) / (dense_threads() * vec) * 8));
+        tile_w_ = static_cast<int32_t>(round_up((nl_ + ntiles - 1) / ntiles, vec));
+        tile_w_ = std::min<int32_t>(std::max(tile_w_, vec), dense_threads() * vec);
+        ntiles = (nl_ + tile_w_ - 1) / tile_w_;
+        const int items = ntiles * nchunks_;
+        const bool tiny = static_cast<double>(n_) * pitch_ * esz <= 256.0 * 1024;
+        persist_grid_ = tiny ? 1 : std::max(1, std::min(items, resident));
+        dense_grid_ = std::min(items, sms * 8);
+        d_partial_.alloc(static_cast<size_t>(nchunks_) * std::max(nl_, 1) * 8);
+        cuda_check(cudaMemsetAsync(d_partial_.p, 0, d_partial_.bytes, stream_), "memset");
+    } else if (dense_) {
         const int vec = dense_vec(f64_);
         const int span = dense_threads() * vec;
         const int ntiles = std::max(1, (nl_ + span - 1) / span);
@@ -690,34 +711,39 @@ HistArgs Engine::hist_args() {
     return h;
 }
 
+DenseArgs Engine::dense_args() {
+    DenseArgs a{};
+    a.n = n_;
+    a.first = first_;
+    a.nl = nl_;
+    a.pitch = pitch_;
+    a.w = d_w_.p;
+    a.delay = has_delay_ ? d_delay_.as<uint8_t>() : nullptr;
+    a.mask = any_mixed_ ? d_mask_.as<uint32_t>() : nullptr;
+    a.kind = d_kind_.as<uint8_t>();
+    a.active = d_active_.as<uint32_t>();
+    a.hist = d_hist_.as<uint64_t>();
+    a.bits = d_bits_.as<uint32_t>();
+    a.pot = f64_ ? static_cast<const void*>(d_pot64_.p) : static_cast<const void*>(d_pot32_.p);
+    a.dep = f64_ ? static_cast<const void*>(d_dep64_.p) : static_cast<const void*>(d_dep32_.p);
+    a.dp = stdp_on_ ? dp_ : 1;
+    a.w_min = w_min_;
+    a.w_max = w_max_;
+    a.tile_w = tile_w_;
+    a.rows_per_chunk = rows_per_chunk_;
+    a.nchunks = nchunks_;
+    a.partial = d_partial_.as<double>();
+    a.v = d_v_.as<double>();
+    a.leak = d_leak_.as<double>();
+    a.reset = d_reset_.as<double>();
+    a.u_exact = d_uexact_.as<double>();
+    a.d_step = d_step_.as<int32_t>();
+    return a;
+}
+
 void Engine::launch_sweep() {
     if (dense_) {
-        DenseArgs a{};
-        a.n = n_;
-        a.first = first_;
-        a.nl = nl_;
-        a.pitch = pitch_;
-        a.w = d_w_.p;
-        a.delay = has_delay_ ? d_delay_.as<uint8_t>() : nullptr;
-        a.mask = any_mixed_ ? d_mask_.as<uint32_t>() : nullptr;
-        a.kind = d_kind_.as<uint8_t>();
-        a.active = d_active_.as<uint32_t>();
-        a.hist = d_hist_.as<uint64_t>();
-        a.bits = d_bits_.as<uint32_t>();
-        a.pot = f64_ ? static_cast<const void*>(d_pot64_.p) : static_cast<const void*>(d_pot32_.p);
-        a.dep = f64_ ? static_cast<const void*>(d_dep64_.p) : static_cast<const void*>(d_dep32_.p);
-        a.dp = stdp_on_ ? dp_ : 1;
-        a.w_min = w_min_;
-        a.w_max = w_max_;
-        a.tile_w = tile_w_;
-        a.rows_per_chunk = rows_per_chunk_;
-        a.nchunks = nchunks_;
-        a.partial = d_partial_.as<double>();
-        a.v = d_v_.as<double>();
-        a.leak = d_leak_.as<double>();
-        a.reset = d_reset_.as<double>();
-        a.u_exact = d_uexact_.as<double>();
-        a.d_step = d_step_.as<int32_t>();
+        DenseArgs a = dense_args();
         launch_dense(a, f64_, stdp_on_, has_delay_, exact_, dense_grid_, stream_);
     } else {
         SparseArgs a{};
@@ -870,7 +896,19 @@ void Engine::simulate(int32_t steps) {
         NeuronArgs na = neuron_args(t0, steps, d_raster_.as<uint32_t>(), trace, d_st_off_.as<int64_t>(),
                                     d_st_neuron_.as<int32_t>(), d_st_amp_.as<double>(), st_steps_dev_, 0);
         cuda_check(cudaEventRecord(eb, stream_), "rec");
-        if (opt_.use_graphs && !opt_.profile) {
+        if (persistent_) {
+            cudaEvent_t p0{}, p1{};
+            if (opt_.profile) { p0 = get_event(); cuda_check(cudaEventRecord(p0, stream_), "rec"); }
+            launch_persistent_dense(na, hist_args(), dense_args(), f64_, stdp_on_, has_delay_, persist_grid_, steps,
+                                    stream_);
+            stats_.kernel_launches += 1;
+            if (opt_.profile) {
+                p1 = get_event();
+                cuda_check(cudaEventRecord(p1, stream_), "rec");
+                pending_.push_back({p0, p1, 1, 0.0});
+            }
+            cuda_check(cudaEventRecord(ee, stream_), "rec");
+        } else if (opt_.use_graphs && !opt_.profile) {
             cudaGraph_t g;
             cudaGraphExec_t ge;
             cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");

@@ -122,6 +122,7 @@ private:
                            int32_t st_steps, int32_t st_stream);
     HistArgs hist_args();
     void launch_sweep();
+    DenseArgs dense_args();
     void enqueue_step(const NeuronArgs& na, bool exchange);
     void flush_pending();
     void decode_raster();
@@ -160,6 +161,8 @@ private:
     int64_t sparse_elems_ = 0;
     // dense plan
     int32_t tile_w_ = 0, rows_per_chunk_ = 0, nchunks_ = 1, dense_grid_ = 1;
+    bool persistent_ = false;     // small dense nets: one cooperative launch per simulate
+    int32_t persist_grid_ = 1;
     double sweep_bytes_full_ = 0.0;  // algorithmic bytes of a sweep over every active row
 
     // ---- device ----

@@ -13,11 +13,14 @@
 // binary-spike GEMV is not a dense contraction).
 #include "kernels.cuh"
 
+#include <cooperative_groups.h>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
 
 namespace snb {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -62,7 +65,7 @@ __device__ __forceinline__ T clamp_ref(T v, T lo, T hi) {
 }
 
 __device__ __forceinline__ uint32_t bit_of(const uint32_t* bits, int i) {
-    return (__ldg(bits + (i >> 5)) >> (i & 31)) & 1u;
+    return (__ldcg(bits + (i >> 5)) >> (i & 31)) & 1u;
 }
 
 // ---------------------------------------------------------------------------
@@ -120,10 +123,9 @@ __device__ __forceinline__ bool hist_update(const HistArgs& h, int i, bool s, in
 
 // ---------------------------------------------------------------------------
 // K1: LIF update of the local posts for step t (mat_engine.cpp:168-198).
+// Called by full warps (j covers a multiple of 32); one neuron per thread.
 template <bool EXACT, bool FUSED>
-__global__ void __launch_bounds__(kThreads) k_neuron(NeuronArgs a, HistArgs h) {
-    const int j = blockIdx.x * kThreads + threadIdx.x;
-    const int t = *a.d_step;
+__device__ __forceinline__ void neuron_step(const NeuronArgs& a, const HistArgs& h, int j, int t) {
     const bool valid = j < a.nl;
     bool s = false;
     if (valid) {
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(kThreads) k_neuron(NeuronArgs a, HistArgs h) {
             u = a.u_exact[j];  // leak(v) + sum in ascending pre order, from the sweep
         } else {
             double in = 0.0;
-            for (int c = 0; c < a.nchunks; ++c) in += a.partial[static_cast<int64_t>(c) * a.nl + j];
+            for (int c = 0; c < a.nchunks; ++c) in += __ldcg(a.partial + static_cast<int64_t>(c) * a.nl + j);
             u = leak_toward(v, a.leak[j], reset) + in;
         }
         // external stimulus: the step's entries pre-summed in list order
@@ -189,6 +191,11 @@ __global__ void __launch_bounds__(kThreads) k_neuron(NeuronArgs a, HistArgs h) {
             if (aw) atomicAdd(h.active_count, static_cast<unsigned long long>(__popc(aw)));
         }
     }
+}
+
+template <bool EXACT, bool FUSED>
+__global__ void __launch_bounds__(kThreads) k_neuron(NeuronArgs a, HistArgs h) {
+    neuron_step<EXACT, FUSED>(a, h, blockIdx.x * kThreads + threadIdx.x, *a.d_step);
 }
 
 // Partitioned runs: history/traces for all N from the all-gathered bitmask.
@@ -298,7 +305,7 @@ __global__ void __launch_bounds__(kThreads) k_dense_sweep(DenseArgs a) {
             if (tid < 32) {
                 uint32_t wd = 0;
                 if (tid < nwords) {
-                    wd = a.active[(sa >> 5) + tid];
+                    wd = __ldcg(a.active + (sa >> 5) + tid);
                     const int rem = sb - (sa + tid * 32);
                     if (rem < 32) wd &= (rem <= 0) ? 0u : ((1u << rem) - 1u);
                 }
@@ -433,7 +440,7 @@ template <> struct alignas(16) RowRec<double> {
 };
 
 template <typename WT, bool STDP, bool DELAY>
-__global__ void __launch_bounds__(kThreads, 2) k_dense_stream(DenseArgs a) {
+__device__ __forceinline__ void dense_stream_body(const DenseArgs& a, int cta, int ncta) {
     using VT = VecT<WT>;
     using V = typename VT::V;
     constexpr int VEC = VT::N;
@@ -451,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_dense_stream(DenseArgs a) {
     WT* W = static_cast<WT*>(a.w);
     const int64_t mpitch = a.pitch >> 5;
 
-    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    for (int item = cta; item < items; item += ncta) {
         const int chunk = item / ntiles;
         const int tile = item - chunk * ntiles;
         const int tcol = tid * VEC;
@@ -467,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_dense_stream(DenseArgs a) {
         for (int k = 0; k < VEC; ++k) {
             const bool ok = in_tile && (c0 + k) < a.nl;
             sjf[k] = (ok && STDP && bit_of(a.bits, gc0 + k)) ? WT(1) : WT(0);
-            depj[k] = (ok && STDP) ? dep[gc0 + k] : WT(0);
+            depj[k] = (ok && STDP) ? __ldcg(dep + gc0 + k) : WT(0);
             acc[k] = 0.0;
         }
 
@@ -478,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_dense_stream(DenseArgs a) {
             if (tid < 32) {
                 uint32_t wd = 0;
                 if (tid < nwords) {
-                    wd = a.active[(sa >> 5) + tid];
+                    wd = __ldcg(a.active + (sa >> 5) + tid);
                     const int rem = sb - (sa + tid * 32);
                     if (rem < 32) wd &= (rem <= 0) ? 0u : ((1u << rem) - 1u);
                 }
@@ -499,13 +506,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_dense_stream(DenseArgs a) {
                 const uint32_t wd = s_word[l];
                 if ((wd >> b) & 1u) {
                     const int pos = s_wpref[l] + __popc(wd & ((1u << b) - 1u));
-                    const uint64_t h = __ldg(a.hist + r);
+                    const uint64_t h = __ldcg(a.hist + r);
                     RowRec<WT> rec;
                     const int kind = STDP ? static_cast<int>(__ldg(a.kind + r)) : 0;
                     rec.rowk = r | (kind << 28);
                     rec.e_lo = static_cast<uint32_t>(h);
                     rec.e_hi = static_cast<uint32_t>(h >> 32);
-                    rec.pot = (STDP && !DELAY) ? pot[r] : WT(0);
+                    rec.pot = (STDP && !DELAY) ? __ldcg(pot + r) : WT(0);
                     s_rec[pos] = rec;
                 }
             }
@@ -556,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_dense_stream(DenseArgs a) {
                             WT p;
                             if (DELAY) {
                                 const int d1 = static_cast<int>((dv[u] >> (8 * k)) & 0xffu) - 1;
-                                p = pot[static_cast<int64_t>(row) * a.dp + d1];
+                                p = __ldcg(pot + static_cast<int64_t>(row) * a.dp + d1);
                             } else {
                                 p = rec.pot;
                             }
@@ -594,7 +601,33 @@ __global__ void __launch_bounds__(kThreads, 2) k_dense_stream(DenseArgs a) {
                 if (c0 + k < a.nl) a.partial[static_cast<int64_t>(chunk) * a.nl + c0 + k] = acc[k];
         }
     }
-    if (blockIdx.x == 0 && tid == 0) *a.d_step += 1;
+}
+
+template <typename WT, bool STDP, bool DELAY>
+__global__ void __launch_bounds__(kThreads, 2) k_dense_stream(DenseArgs a) {
+    dense_stream_body<WT, STDP, DELAY>(a, blockIdx.x, gridDim.x);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.d_step += 1;  // no other CTA reads it
+}
+
+// Persistent single-GPU step loop for small dense nets (launch-latency bound
+// otherwise): one cooperative launch runs `steps` steps; neuron phase and
+// sweep phase are separated by grid-wide barriers (cooperative groups).
+template <typename WT, bool STDP, bool DELAY>
+__global__ void __launch_bounds__(kThreads, 2) k_persistent_dense(NeuronArgs na, HistArgs h, DenseArgs da,
+                                                                 int steps) {
+    cg::grid_group grid = cg::this_grid();
+    const bool single = gridDim.x == 1;
+    int t = *na.d_step;
+    const int span = ((na.nl + 31) / 32) * 32;
+    for (int s = 0; s < steps; ++s, ++t) {
+        for (int j = blockIdx.x * kThreads + threadIdx.x; j - static_cast<int>(threadIdx.x & 31) < span;
+             j += gridDim.x * kThreads)
+            neuron_step<false, true>(na, h, j, t);
+        if (single) __syncthreads(); else grid.sync();
+        dense_stream_body<WT, STDP, DELAY>(da, blockIdx.x, gridDim.x);
+        if (single) __syncthreads(); else grid.sync();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *na.d_step = t;
 }
 
 // ---------------------------------------------------------------------------
@@ -769,8 +802,8 @@ __device__ __forceinline__ int er_delay(const ErArgs& e, int i, int j) {
 template <typename WT>
 __global__ void k_er_dense(ErArgs e, WT* w, uint8_t* delay, uint32_t* mask, int first, int nl,
                            int64_t pitch) {
-    const int i = blockIdx.y;
-    const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // < pitch
+    const int i = blockIdx.x;
+    const int64_t c = static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x;  // < pitch
     if (c >= pitch) return;
     const int j = first + static_cast<int>(c);
     const bool present = c < nl && er_edge(e, i, j);
@@ -885,6 +918,51 @@ static void dense_go(const DenseArgs& a, int grid, cudaStream_t s) {
     else k_dense_stream<WT, STDP, DELAY><<<grid, kThreads, 0, s>>>(a);
 }
 
+template <typename WT, bool STDP, bool DELAY>
+static void persistent_go(NeuronArgs na, HistArgs h, DenseArgs da, int grid, int steps, cudaStream_t s,
+                          int* max_ctas) {
+    auto kern = k_persistent_dense<WT, STDP, DELAY>;
+    if (max_ctas) {
+        int dev = 0, sms = 0, occ = 0;
+        check(cudaGetDevice(&dev), "cudaGetDevice");
+        check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+        check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0), "occupancy");
+        *max_ctas = occ * sms;
+        return;
+    }
+    void* args[] = {&na, &h, &da, &steps};
+    check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kThreads), args, 0, s),
+          "k_persistent_dense");
+}
+
+static void persistent_dispatch(const NeuronArgs& na, const HistArgs& h, const DenseArgs& da, bool f64,
+                                bool stdp, bool delay, int grid, int steps, cudaStream_t s, int* max_ctas) {
+#define SNB_P(WT)                                                                         \
+    do {                                                                                  \
+        if (stdp) {                                                                       \
+            if (delay) persistent_go<WT, true, true>(na, h, da, grid, steps, s, max_ctas);   \
+            else persistent_go<WT, true, false>(na, h, da, grid, steps, s, max_ctas);        \
+        } else {                                                                          \
+            if (delay) persistent_go<WT, false, true>(na, h, da, grid, steps, s, max_ctas);  \
+            else persistent_go<WT, false, false>(na, h, da, grid, steps, s, max_ctas);       \
+        }                                                                                 \
+    } while (0)
+    if (f64) SNB_P(double);
+    else SNB_P(float);
+#undef SNB_P
+}
+
+int persistent_max_ctas(bool f64, bool stdp, bool delay) {
+    int m = 0;
+    persistent_dispatch(NeuronArgs{}, HistArgs{}, DenseArgs{}, f64, stdp, delay, 0, 0, nullptr, &m);
+    return m;
+}
+
+void launch_persistent_dense(const NeuronArgs& na, const HistArgs& h, const DenseArgs& da, bool f64,
+                             bool stdp, bool delay, int grid, int steps, cudaStream_t s) {
+    persistent_dispatch(na, h, da, f64, stdp, delay, grid, steps, s, nullptr);
+}
+
 void launch_dense(const DenseArgs& a, bool f64, bool stdp, bool delay, bool exact, int grid,
                   cudaStream_t s) {
 #define SNB_DENSE(WT)                                                            \
@@ -976,7 +1054,7 @@ void launch_sparse(const SparseArgs& a, bool f64, bool stdp, int hbits, int sub,
 
 void launch_er_dense(const ErArgs& e, void* w, bool f64, uint8_t* delay, uint32_t* mask, int first,
                      int nl, int64_t pitch, cudaStream_t s) {
-    dim3 grid(static_cast<unsigned>((pitch + 255) / 256), static_cast<unsigned>(e.n));
+    dim3 grid(static_cast<unsigned>(e.n), static_cast<unsigned>((pitch + 255) / 256));
     if (f64) k_er_dense<double><<<grid, 256, 0, s>>>(e, static_cast<double*>(w), delay, mask, first, nl, pitch);
     else k_er_dense<float><<<grid, 256, 0, s>>>(e, static_cast<float*>(w), delay, mask, first, nl, pitch);
     check(cudaGetLastError(), "k_er_dense");

@@ -139,6 +139,10 @@ void launch_prologue(double* u_exact, const double* v, const double* leak, const
                      int nl, cudaStream_t s);
 void launch_step_bump(int32_t* d_step, cudaStream_t s);
 int sparse_block_pres(int hbits);
+// persistent cooperative step loop for small dense nets (single partition)
+int persistent_max_ctas(bool f64, bool stdp, bool delay);
+void launch_persistent_dense(const NeuronArgs& na, const HistArgs& h, const DenseArgs& da, bool f64,
+                             bool stdp, bool delay, int grid, int steps, cudaStream_t s);
 
 // ---- on-device Erdos-Renyi generation (netgen.cpp:36-51 semantics) ----
 struct ErArgs {

@@ -25,7 +25,7 @@ class MatEngine:
                  precision: str = "f32", exact_order: bool = False,
                  record_membrane: bool = False, stream_io: bool = False,
                  use_graphs: bool = True, rank: int = 0, world: int = 1,
-                 profile: bool = False):
+                 profile: bool = False, persistent: bool = True):
         o = _capi.Options()
         check(lib.sn_options_init(C.byref(o)))
         o.device = device
@@ -38,6 +38,7 @@ class MatEngine:
         o.rank = rank
         o.world = world
         o.profile = 1 if profile else 0
+        o.persistent = 0 if persistent else -1
         h = C.c_void_p()
         check(lib.sn_engine_create(C.byref(o), C.byref(h)))
         self._h = h

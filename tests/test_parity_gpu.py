@@ -25,7 +25,9 @@ CONFIGS = {
     "dense_f64_exact": dict(storage=1, precision="f64", exact_order=True),
     "sparse_f64_exact": dict(storage=2, precision="f64", exact_order=True),
     "dense_f32_stream": dict(storage=1, stream_io=True),
-    "dense_f32_nograph": dict(storage=1, use_graphs=False),
+    "dense_f32_nograph": dict(storage=1, use_graphs=False, persistent=False),
+    "dense_f32_graph": dict(storage=1, persistent=False),
+    "dense_f64": dict(storage=1, precision="f64"),
 }
 
 
@@ -282,7 +284,7 @@ def test_neuromorphic_model_api():
 
 def test_profile_stats_and_launch_count():
     from paper_2305_02510_b200.engine import MatEngine
-    eng = MatEngine(profile=True)
+    eng = MatEngine(profile=True, persistent=False)
     eng.generate_erdos_renyi(2048, 1.0, 0, stdp=True)
     from paper_2305_02510_b200.model import StdpConfig
     d = StdpConfig.defaults()
