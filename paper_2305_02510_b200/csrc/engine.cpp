@@ -544,6 +544,8 @@ void Engine::alloc_state() {
         d_am_.alloc(8);
     }
     d_step_.alloc(8);
+    d_work_.alloc(8);
+    cuda_check(cudaMemsetAsync(d_work_.p, 0, 8, stream_), "memset");
     d_spikes_.alloc(16);
     cuda_check(cudaMemsetAsync(d_step_.p, 0, 8, stream_), "memset");
     cuda_check(cudaMemsetAsync(d_spikes_.p, 0, 16, stream_), "memset");
@@ -585,17 +587,17 @@ void Engine::plan_launches() {
             nchunks_ = 1;
             rows_per_chunk_ = static_cast<int32_t>(round_up(n_, 32));
         } else {
-            // ~8 resident CTAs per SM; one wave of equal items
-            const int resident = sms * 8;
-            int nch = std::max(1, resident / ntiles);
-            int rpc = static_cast<int>(round_up((n_ + nch - 1) / nch, 32));
-            rpc = std::max(rpc, 32);
+            // one wave of co-resident CTAs claiming ~4 items each dynamically
+            const int resident = dense_stream_max_ctas(f64_, stdp_on_, has_delay_);
+            int nch = std::max(1, static_cast<int>(std::lround(4.0 * resident / ntiles)));
+            int rpc = std::max(32, (n_ + nch - 1) / nch);
             nch = (n_ + rpc - 1) / rpc;
             rows_per_chunk_ = rpc;
             nchunks_ = nch;
+            dense_grid_ = std::min(ntiles * nchunks_, resident);
         }
         const int items = ntiles * nchunks_;
-        dense_grid_ = std::min(items, sms * 8);
+        if (exact_) dense_grid_ = std::min(items, sms * 8);
         d_partial_.alloc(static_cast<size_t>(nchunks_) * std::max(nl_, 1) * 8);
         cuda_check(cudaMemsetAsync(d_partial_.p, 0, d_partial_.bytes, stream_), "memset");
     } else {
@@ -677,6 +679,7 @@ NeuronArgs Engine::neuron_args(int t_base, int rows, uint32_t* raster, double* t
     a.st_steps = st_steps;
     a.st_stream = st_stream;
     a.d_step = d_step_.as<int32_t>();
+    a.work = (dense_ && !exact_) ? d_work_.as<int32_t>() : nullptr;
     a.t_base = t_base;
     a.bits = d_bits_.as<uint32_t>();
     a.raster = raster;
@@ -738,6 +741,7 @@ DenseArgs Engine::dense_args() {
     a.reset = d_reset_.as<double>();
     a.u_exact = d_uexact_.as<double>();
     a.d_step = d_step_.as<int32_t>();
+    a.work = exact_ ? nullptr : d_work_.as<int32_t>();
     return a;
 }
 

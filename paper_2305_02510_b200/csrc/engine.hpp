@@ -172,7 +172,7 @@ private:
     DevBuf d_bits_, d_hist_, d_hist_lo_, d_active_;
     DevBuf d_pot64_, d_pot32_, d_dep64_, d_dep32_, d_ap_, d_am_;
     DevBuf d_partial_, d_uexact_;
-    DevBuf d_step_, d_spikes_;
+    DevBuf d_step_, d_spikes_, d_work_;
     DevBuf d_st_off_, d_st_neuron_, d_st_amp_;
     int32_t st_steps_dev_ = 0;
     DevBuf d_stage_;

@@ -127,6 +127,7 @@ __device__ __forceinline__ bool hist_update(const HistArgs& h, int i, bool s, in
 template <bool EXACT, bool FUSED>
 __device__ __forceinline__ void neuron_step(const NeuronArgs& a, const HistArgs& h, int j, int t) {
     const bool valid = j < a.nl;
+    if (a.work && j == 0) *a.work = 0;  // the previous sweep has finished (stream / grid order)
     bool s = false;
     if (valid) {
         double v = a.v[j];
@@ -335,13 +336,13 @@ __global__ void __launch_bounds__(kThreads) k_dense_sweep(DenseArgs a) {
             __syncthreads();
             const int cnt = s_wpref[32];
 
-            for (int base = 0; base < cnt; base += U) {
+            for (int gb = 0; gb < cnt; gb += U) {
                 V wv[U];
                 uint32_t dv[U];
                 uint32_t mv[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int idx = base + u;
+                    const int idx = gb + u;
                     dv[u] = 0x01010101u;
                     mv[u] = 0;
                     if (idx < cnt && in_tile) {
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(kThreads) k_dense_sweep(DenseArgs a) {
                 for (int k = 0; k < VEC; ++k) grp[k] = WT(0);
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int idx = base + u;
+                    const int idx = gb + u;
                     if (idx >= cnt || !in_tile) continue;
                     const int row = s_rows[idx];
                     const uint64_t ebits = s_e[idx];
@@ -458,7 +459,17 @@ __device__ __forceinline__ void dense_stream_body(const DenseArgs& a, int cta, i
     WT* W = static_cast<WT*>(a.w);
     const int64_t mpitch = a.pitch >> 5;
 
-    for (int item = cta; item < items; item += ncta) {
+    // Items are claimed dynamically (a.work, reset by the neuron phase) so the
+    // CTAs of a one-wave grid finish together; static striding otherwise.
+    __shared__ int s_item;
+    int item = cta;
+    if (a.work) {
+        __syncthreads();
+        if (tid == 0) s_item = atomicAdd(a.work, 1);
+        __syncthreads();
+        item = s_item;
+    }
+    while (item < items) {
         const int chunk = item / ntiles;
         const int tile = item - chunk * ntiles;
         const int tcol = tid * VEC;
@@ -478,15 +489,20 @@ __device__ __forceinline__ void dense_stream_body(const DenseArgs& a, int cta, i
             acc[k] = 0.0;
         }
 
-        for (int sa = r0; sa < r1; sa += kSubRows) {
-            const int sb = min(r1, sa + kSubRows);
-            const int nwords = (sb - sa + 31) >> 5;
+        // sub-chunks start at a 32-aligned base so <= 32 active words cover them
+        for (int sa = r0, sb_next = r0; sa < r1; sa = sb_next) {
+            const int base = sa & ~31;
+            const int sb = min(r1, base + kSubRows);
+            sb_next = sb;
+            const int nwords = (sb - base + 31) >> 5;
             __syncthreads();
             if (tid < 32) {
                 uint32_t wd = 0;
                 if (tid < nwords) {
-                    wd = __ldcg(a.active + (sa >> 5) + tid);
-                    const int rem = sb - (sa + tid * 32);
+                    wd = __ldcg(a.active + (base >> 5) + tid);
+                    const int lo = sa - (base + tid * 32);  // bits below sa
+                    if (lo > 0) wd &= (lo >= 32) ? 0u : ~((1u << lo) - 1u);
+                    const int rem = sb - (base + tid * 32);
                     if (rem < 32) wd &= (rem <= 0) ? 0u : ((1u << rem) - 1u);
                 }
                 const int c = __popc(wd);
@@ -502,7 +518,7 @@ __device__ __forceinline__ void dense_stream_body(const DenseArgs& a, int cta, i
             }
             __syncthreads();
             for (int r = sa + tid; r < sb; r += kThreads) {
-                const int l = (r - sa) >> 5, b = (r - sa) & 31;
+                const int l = (r - base) >> 5, b = (r - base) & 31;
                 const uint32_t wd = s_word[l];
                 if ((wd >> b) & 1u) {
                     const int pos = s_wpref[l] + __popc(wd & ((1u << b) - 1u));
@@ -527,12 +543,12 @@ __device__ __forceinline__ void dense_stream_body(const DenseArgs& a, int cta, i
             __syncthreads();
             if (!in_tile) continue;
 
-            for (int base = 0; base < cnt; base += U) {
+            for (int gb = 0; gb < cnt; gb += U) {
                 V wv[U];
                 uint32_t dv[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int row = s_rec[base + u].rowk & 0x0fffffff;
+                    const int row = s_rec[gb + u].rowk & 0x0fffffff;
                     const int64_t off = static_cast<int64_t>(row) * a.pitch + c0;
                     wv[u] = VT::load(W + off);
                     if (DELAY) {
@@ -545,7 +561,7 @@ __device__ __forceinline__ void dense_stream_body(const DenseArgs& a, int cta, i
                 for (int k = 0; k < VEC; ++k) grp[k] = WT(0);
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const RowRec<WT> rec = s_rec[base + u];
+                    const RowRec<WT> rec = s_rec[gb + u];
                     const int row = rec.rowk & 0x0fffffff;
                     const int kind = rec.rowk >> 28;
                     const uint64_t ebits = (static_cast<uint64_t>(rec.e_hi) << 32) | rec.e_lo;
@@ -599,6 +615,14 @@ __device__ __forceinline__ void dense_stream_body(const DenseArgs& a, int cta, i
 #pragma unroll
             for (int k = 0; k < VEC; ++k)
                 if (c0 + k < a.nl) a.partial[static_cast<int64_t>(chunk) * a.nl + c0 + k] = acc[k];
+        }
+        if (a.work) {
+            __syncthreads();
+            if (tid == 0) s_item = atomicAdd(a.work, 1);
+            __syncthreads();
+            item = s_item;
+        } else {
+            item += ncta;
         }
     }
 }
@@ -950,6 +974,25 @@ static void persistent_dispatch(const NeuronArgs& na, const HistArgs& h, const D
     if (f64) SNB_P(double);
     else SNB_P(float);
 #undef SNB_P
+}
+
+template <typename WT, bool STDP, bool DELAY>
+static int stream_occ() {
+    int dev = 0, sms = 0, occ = 0;
+    check(cudaGetDevice(&dev), "cudaGetDevice");
+    check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dense_stream<WT, STDP, DELAY>, kThreads, 0),
+          "occupancy");
+    return occ * sms;
+}
+
+int dense_stream_max_ctas(bool f64, bool stdp, bool delay) {
+    if (f64) {
+        if (stdp) return delay ? stream_occ<double, true, true>() : stream_occ<double, true, false>();
+        return delay ? stream_occ<double, false, true>() : stream_occ<double, false, false>();
+    }
+    if (stdp) return delay ? stream_occ<float, true, true>() : stream_occ<float, true, false>();
+    return delay ? stream_occ<float, false, true>() : stream_occ<float, false, false>();
 }
 
 int persistent_max_ctas(bool f64, bool stdp, bool delay) {

@@ -39,6 +39,7 @@ struct NeuronArgs {
     int32_t st_stream;         // 1: table has one row (index 0) for the current step
     // time
     int32_t* d_step;           // device step counter (read here; sweep increments)
+    int32_t* work;             // sweep work counter, reset here (null: static schedule)
     int32_t t_base;            // raster/trace row = t - t_base
     // outputs
     uint32_t* bits;            // full bitmask [words]; this kernel writes local words
@@ -98,6 +99,7 @@ struct DenseArgs {
     const double* reset;
     double* u_exact;           // [nl]
     int32_t* d_step;
+    int32_t* work;             // dynamic item counter (null: static striding)
 };
 
 struct SparseArgs {
@@ -133,6 +135,7 @@ void launch_dense(const DenseArgs& a, bool f64, bool stdp, bool delay, bool exac
                   cudaStream_t s);
 int dense_vec(bool f64);
 int dense_threads();
+int dense_stream_max_ctas(bool f64, bool stdp, bool delay);  // occupancy x SMs
 void launch_sparse(const SparseArgs& a, bool f64, bool stdp, int hbits, int sub, bool exact,
                    int grid_x, cudaStream_t s);
 void launch_prologue(double* u_exact, const double* v, const double* leak, const double* reset,
