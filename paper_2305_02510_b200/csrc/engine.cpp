@@ -615,9 +615,13 @@ void Engine::plan_launches() {
     } else {
         const double avg = nl_ > 0 ? static_cast<double>(sparse_elems_) / (static_cast<double>(nblocks_) * nl_) : 0.0;
         sub_ = avg >= 256 ? 32 : avg >= 96 ? 16 : avg >= 40 ? 8 : 4;
+        // default: flat per-warp stream over 4-entry chunks (k_sparse_stream);
+        // SNB_SPARSE_KERNEL=pull keeps the lanes-per-post variant for A/B runs
+        const char* sk = std::getenv("SNB_SPARSE_KERNEL");
+        if (!(sk && std::string(sk) == "pull")) sub_ = 0;
         const int target = sms * 8;
         int gx = std::max(1, target / std::max(1, nblocks_));
-        const int unit = 8 * (32 / sub_);
+        const int unit = sub_ == 0 ? 8 : 8 * (32 / sub_);
         posts_per_cta_ = static_cast<int32_t>(round_up((nl_ + gx - 1) / gx, unit));
         posts_per_cta_ = std::max(posts_per_cta_, unit);
         sparse_gx_ = std::max(1, (nl_ + posts_per_cta_ - 1) / posts_per_cta_);

@@ -766,6 +766,166 @@ __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *a.d_step += 1;
 }
 
+// Sparse stream: the same blocked-CSC pull, but each warp streams a contiguous
+// run of its CTA's posts as one flat array of 4-entry chunks (lists are padded
+// to 4, so a chunk never straddles two posts): every lane issues U 128-bit
+// meta + weight loads back to back (no per-post tail waste), a fixed
+// segmented suffix-reduction over lanes folds chunks into per-post sums, and
+// the last segment's sum is carried into the next iteration.  The order of
+// additions is fixed by the data layout, so results are deterministic.
+template <typename WT, bool STDP, int HB>
+__global__ void __launch_bounds__(kThreads) k_sparse_stream(SparseArgs a) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    using HT = typename HistT<HB>::T;
+    constexpr int U = 4;
+    const int b = blockIdx.y;
+    const int pre0 = b * a.pb;
+    const int pcount = min(a.pb, a.n - pre0);
+    const int tid = threadIdx.x;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *a.d_step += 1;  // nobody reads it here
+    if (HB == 1) {
+        uint32_t* sb = reinterpret_cast<uint32_t*>(smem_raw);
+        const int nw = (pcount + 31) >> 5;
+        for (int k = tid; k < nw; k += kThreads) sb[k] = __ldcg(a.bits + (pre0 >> 5) + k);
+    } else {
+        HT* sh = reinterpret_cast<HT*>(smem_raw);
+        for (int k = tid; k < pcount; k += kThreads) {
+            if (HB == 64) sh[k] = static_cast<HT>(__ldcg(a.hist + pre0 + k));
+            else sh[k] = static_cast<HT>(__ldcg(a.hist_lo + pre0 + k));
+        }
+    }
+    __syncthreads();
+    const uint32_t* sbits = reinterpret_cast<const uint32_t*>(smem_raw);
+    const HT* shist = reinterpret_cast<const HT*>(smem_raw);
+    const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
+    const WT* pot = static_cast<const WT*>(a.pot);
+    const WT* dep = static_cast<const WT*>(a.dep);
+    WT* W = static_cast<WT*>(a.w);
+    const int64_t* off = a.off + static_cast<int64_t>(b) * a.nl;  // off[p], p in [0, nl]
+    double* part = a.partial + static_cast<int64_t>(b) * a.nl;
+
+    const int warp = tid >> 5, lane = tid & 31;
+    const int p0 = blockIdx.x * a.posts_per_cta;
+    const int p1 = min(a.nl, p0 + a.posts_per_cta);
+    if (p0 >= p1) return;
+    // split [p0, p1) among the 8 warps by entry count (boundaries at post starts)
+    const int64_t e0 = __ldg(off + p0), e1 = __ldg(off + p1);
+    auto lower_post = [&](int64_t target) {  // first p in [p0, p1] with off[p] >= target
+        int lo = p0, hi = p1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(off + mid) < target) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+    };
+    const int nwarps = kThreads / 32;
+    const int pa = lower_post(e0 + (e1 - e0) * warp / nwarps);
+    const int pb = warp == nwarps - 1 ? p1 : lower_post(e0 + (e1 - e0) * (warp + 1) / nwarps);
+    if (pa >= pb) return;
+    // empty lists never appear in the stream: their partial is 0
+    for (int q = pa + lane; q < pb; q += 32)
+        if (__ldg(off + q) == __ldg(off + q + 1)) part[q] = 0.0;
+
+    int64_t e = __ldg(off + pa);
+    const int64_t end = __ldg(off + pb);
+    int carry_post = pa;
+    WT carry = WT(0);
+    int lp = pa;  // this lane's current post (monotone)
+    while (e < end) {
+        uint4 m4[U];
+        WT wv[U][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t q = e + static_cast<int64_t>(u * 32 + lane) * 4;
+            if (q < end) {
+                m4[u] = __ldcs(reinterpret_cast<const uint4*>(a.meta + q));
+                if (sizeof(WT) == 4) {
+                    const float4 f = __ldcs(reinterpret_cast<const float4*>(W + q));
+                    wv[u][0] = f.x; wv[u][1] = f.y; wv[u][2] = f.z; wv[u][3] = f.w;
+                } else {
+                    const double2 f0 = __ldcs(reinterpret_cast<const double2*>(W + q));
+                    const double2 f1 = __ldcs(reinterpret_cast<const double2*>(W + q + 2));
+                    wv[u][0] = f0.x; wv[u][1] = f0.y; wv[u][2] = f1.x; wv[u][3] = f1.y;
+                }
+            } else {
+                m4[u] = make_uint4(0, 0, 0, 0);
+                wv[u][0] = wv[u][1] = wv[u][2] = wv[u][3] = WT(0);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t q = e + static_cast<int64_t>(u * 32 + lane) * 4;
+            const bool valid = q < end;
+            int p = pb;  // sentinel for lanes past the end
+            if (valid) {
+                while (__ldg(off + lp + 1) <= q) ++lp;
+                p = lp;
+            }
+            WT csum = WT(0);
+            if (valid) {
+                const uint32_t ms[4] = {m4[u].x, m4[u].y, m4[u].z, m4[u].w};
+                bool sp = false;
+                WT depp = WT(0);
+                if (STDP) {
+                    sp = bit_of(a.bits, a.first + p);
+                    depp = __ldcg(dep + a.first + p);
+                }
+                bool changed = false;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t m = ms[k];
+                    const int pl = static_cast<int>(m & 0xffffu);
+                    const int d1 = static_cast<int>((m >> 16) & 63u);
+                    uint32_t ev;
+                    if (HB == 1) ev = (sbits[pl >> 5] >> (pl & 31)) & 1u;
+                    else ev = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
+                    WT w = wv[u][k];
+                    if (STDP && ((m >> 22) & 1u)) {
+                        const WT pt = __ldcg(pot + static_cast<int64_t>(pre0 + pl) * a.dp + d1);
+                        const WT dw = fma(sp ? WT(1) : WT(0), pt, -((ev ? WT(1) : WT(0)) * depp));
+                        const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
+                        changed |= (nw != w);
+                        w = nw;
+                        wv[u][k] = nw;
+                    }
+                    csum = fma(ev ? WT(1) : WT(0), w, csum);
+                }
+                if (STDP && changed) {
+                    if (sizeof(WT) == 4) {
+                        __stcs(reinterpret_cast<float4*>(W + q),
+                               make_float4(float(wv[u][0]), float(wv[u][1]), float(wv[u][2]), float(wv[u][3])));
+                    } else {
+                        __stcs(reinterpret_cast<double2*>(W + q), make_double2(double(wv[u][0]), double(wv[u][1])));
+                        __stcs(reinterpret_cast<double2*>(W + q + 2), make_double2(double(wv[u][2]), double(wv[u][3])));
+                    }
+                }
+            }
+            // segmented suffix sum over lanes (posts are non-decreasing in lane)
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const WT x = __shfl_down_sync(0xffffffffu, csum, o);
+                const int px = __shfl_down_sync(0xffffffffu, p, o);
+                if (lane + o < 32 && px == p) csum += x;
+            }
+            const int pprev = __shfl_up_sync(0xffffffffu, p, 1);
+            const bool head = lane == 0 || pprev != p;
+            const int plast = __shfl_sync(0xffffffffu, p, 31);
+            const int first_post = __shfl_sync(0xffffffffu, p, 0);
+            if (first_post != carry_post && lane == 0 && carry_post < pb) part[carry_post] = static_cast<double>(carry);
+            WT total = csum;
+            if (head && lane == 0 && p == carry_post) total += carry;
+            if (head && p != plast && p < pb) part[p] = static_cast<double>(total);
+            // the segment holding lane 31 continues into the next iteration;
+            // its head total already includes the old carry when it began at lane 0
+            const int head_last = __ffs(__ballot_sync(0xffffffffu, p == plast)) - 1;
+            carry = __shfl_sync(0xffffffffu, total, head_last);
+            carry_post = plast;
+        }
+        e += static_cast<int64_t>(U * 32) * 4;
+    }
+    if (lane == 0 && carry_post < pb) part[carry_post] = static_cast<double>(carry);
+}
+
 // Sparse exact: one thread per post, ascending pre, fp64 seeded with leak(v).
 template <typename WT, bool STDP>
 __global__ void __launch_bounds__(kThreads) k_sparse_exact(SparseArgs a) {
@@ -1038,6 +1198,7 @@ template <typename WT, bool STDP, int HB>
 static void sparse_go_sub(const SparseArgs& a, int sub, int gx, size_t smem, cudaStream_t s) {
     dim3 grid(gx, a.nblocks);
     switch (sub) {
+        case 0: k_sparse_stream<WT, STDP, HB><<<grid, kThreads, smem, s>>>(a); break;
         case 4: k_sparse_pull<WT, STDP, HB, 4><<<grid, kThreads, smem, s>>>(a); break;
         case 8: k_sparse_pull<WT, STDP, HB, 8><<<grid, kThreads, smem, s>>>(a); break;
         case 16: k_sparse_pull<WT, STDP, HB, 16><<<grid, kThreads, smem, s>>>(a); break;
