@@ -15,6 +15,7 @@
 #include <numeric>
 #include <sstream>
 #include <cstdlib>
+#include <unordered_map>
 #include <unordered_set>
 
 namespace snb {
@@ -421,11 +422,37 @@ void Engine::build_sparse_from_lists() {
         if (ga != gb) return ga < gb;
         return pre_[a] < pre_[b];
     });
-    std::vector<uint32_t> meta(static_cast<size_t>(sparse_elems_), 0u);
+    // weight dictionary: a static (non-plastic) net with <= 511 distinct weights
+    // keeps only the 4-byte meta word per synapse (index in bits 23..31)
+    dict_.clear();
+    if (!stdp_on_ && !exact_) {
+        std::unordered_map<uint64_t, int> idx;
+        bool fits = true;
+        for (int64_t s : local) {
+            uint64_t key;
+            const double w = f64_ ? weight_[s] : static_cast<double>(static_cast<float>(weight_[s]));
+            std::memcpy(&key, &w, 8);
+            if (idx.emplace(key, static_cast<int>(dict_.size())).second) dict_.push_back(w);
+            if (dict_.size() > 511) { fits = false; break; }
+        }
+        if (!fits) dict_.clear();
+        else dict_.push_back(0.0);  // padding entry
+    }
+    const bool dict = !dict_.empty();
+    std::unordered_map<uint64_t, int> dict_idx;
+    for (size_t k = 0; k < dict_.size(); ++k) {
+        uint64_t key;
+        std::memcpy(&key, &dict_[k], 8);
+        dict_idx.emplace(key, static_cast<int>(k));
+    }
+    const uint32_t pad_meta = dict ? (static_cast<uint32_t>(dict_.size() - 1) << 23) : 0u;
+    std::vector<uint32_t> meta(static_cast<size_t>(sparse_elems_), pad_meta);
     std::vector<float> wf;
     std::vector<double> wd;
-    if (f64_) wd.assign(static_cast<size_t>(sparse_elems_), 0.0);
-    else wf.assign(static_cast<size_t>(sparse_elems_), 0.0f);
+    if (!dict) {
+        if (f64_) wd.assign(static_cast<size_t>(sparse_elems_), 0.0);
+        else wf.assign(static_cast<size_t>(sparse_elems_), 0.0f);
+    }
     std::vector<int64_t> cur(off.begin(), off.end() - 1);
     slot_.assign(pre_.size(), -1);
     std::vector<uint8_t> row_pl(n_, 0);
@@ -436,17 +463,47 @@ void Engine::build_sparse_from_lists() {
         const int d = delay_[s] + axonal_[i];
         const bool pl = stdp_on_ && plastic_[s];
         meta[q] = static_cast<uint32_t>(i % pb_) | (static_cast<uint32_t>(d - 1) << 16) | (pl ? (1u << 22) : 0u);
-        if (f64_) wd[q] = weight_[s];
-        else wf[q] = static_cast<float>(weight_[s]);
+        if (dict) {
+            const double w = f64_ ? weight_[s] : static_cast<double>(static_cast<float>(weight_[s]));
+            uint64_t key;
+            std::memcpy(&key, &w, 8);
+            meta[q] |= static_cast<uint32_t>(dict_idx.at(key)) << 23;
+        } else if (f64_) {
+            wd[q] = weight_[s];
+        } else {
+            wf[q] = static_cast<float>(weight_[s]);
+        }
         slot_[s] = q;
         if (pl) row_pl[i] = 1;
     }
     upload(d_off_, off);
     upload(d_meta_, meta);
-    if (f64_) upload(d_w_, wd);
+    if (dict) d_w_.alloc(16);
+    else if (f64_) upload(d_w_, wd);
     else upload(d_w_, wf);
+    upload_dict();
     upload(d_row_plastic_, row_pl);
-    sweep_bytes_full_ = static_cast<double>(syn_local_) * ((stdp_on_ ? 2.0 : 1.0) * (f64_ ? 8 : 4) + 4.0);
+    sweep_bytes_full_ = static_cast<double>(syn_local_) *
+                        (dict ? 4.0 : (stdp_on_ ? 2.0 : 1.0) * (f64_ ? 8 : 4) + 4.0);
+}
+
+void Engine::upload_dict() {
+    if (dict_.empty()) {
+        d_wdict_.release();
+        return;
+    }
+    if (f64_) {
+        upload(d_wdict_, dict_);
+    } else {
+        std::vector<float> f(dict_.begin(), dict_.end());
+        upload(d_wdict_, f);
+    }
+}
+
+double Engine::sparse_weight(const std::vector<uint8_t>& host_w, const std::vector<uint32_t>& meta, int64_t q) const {
+    if (!dict_.empty()) return dict_[meta[q] >> 23];
+    return f64_ ? reinterpret_cast<const double*>(host_w.data())[q]
+                : static_cast<double>(reinterpret_cast<const float*>(host_w.data())[q]);
 }
 
 void Engine::build_generated() {
@@ -500,12 +557,17 @@ void Engine::build_generated() {
         sparse_elems_ = off[nseg];
         upload(d_off_, off);
         d_meta_.alloc(static_cast<size_t>(sparse_elems_) * 4);
-        d_w_.alloc(static_cast<size_t>(sparse_elems_) * esz);
+        // static nets use the weight dictionary {weight, 0.0 (padding)}: 4 B/synapse
+        dict_.clear();
+        if (!er_.stdp && !exact_) dict_ = {f64_ ? er_.weight_d : static_cast<double>(er_.weight_f), 0.0};
+        const bool dict = !dict_.empty();
+        d_w_.alloc(dict ? 16 : static_cast<size_t>(sparse_elems_) * esz);
         launch_er_sparse_fill(er_, first_, nl_, pb_, nblocks_, d_off_.as<int64_t>(), d_meta_.as<uint32_t>(),
-                              d_w_.p, f64_, stream_);
+                              dict ? nullptr : d_w_.p, f64_, stream_);
+        upload_dict();
         stats_.kernel_launches += 2;
         if (er_.stdp) std::fill(row_pl.begin(), row_pl.end(), 1);
-        sweep_bytes_full_ = static_cast<double>(syn_local_) * ((stdp_on_ ? 2.0 : 1.0) * esz + 4.0);
+        sweep_bytes_full_ = static_cast<double>(syn_local_) * (dict ? 4.0 : (stdp_on_ ? 2.0 : 1.0) * esz + 4.0);
     }
     upload(d_row_plastic_, row_pl);
     if (er_.stdp && !stdp_on_)
@@ -615,10 +677,11 @@ void Engine::plan_launches() {
     } else {
         const double avg = nl_ > 0 ? static_cast<double>(sparse_elems_) / (static_cast<double>(nblocks_) * nl_) : 0.0;
         sub_ = avg >= 256 ? 32 : avg >= 96 ? 16 : avg >= 40 ? 8 : 4;
-        // default: flat per-warp stream over 4-entry chunks (k_sparse_stream);
-        // SNB_SPARSE_KERNEL=pull keeps the lanes-per-post variant for A/B runs
+        // default: SUB lanes per post (k_sparse_pull, 1.058 ms on cfg4); the flat
+        // per-warp chunk stream (k_sparse_stream, 1.115 ms) stays selectable for
+        // A/B runs with SNB_SPARSE_KERNEL=stream (tools/ab_sparse.sh)
         const char* sk = std::getenv("SNB_SPARSE_KERNEL");
-        if (!(sk && std::string(sk) == "pull")) sub_ = 0;
+        if (sk && std::string(sk) == "stream" && dict_.empty()) sub_ = 0;
         const int target = sms * 8;
         int gx = std::max(1, target / std::max(1, nblocks_));
         const int unit = sub_ == 0 ? 8 : 8 * (32 / sub_);
@@ -784,6 +847,8 @@ void Engine::launch_sweep() {
         a.w_min = w_min_;
         a.w_max = w_max_;
         a.posts_per_cta = posts_per_cta_;
+        a.wdict = dict_.empty() ? nullptr : d_wdict_.p;
+        a.dict_size = static_cast<int32_t>(dict_.size());
         a.partial = d_partial_.as<double>();
         a.v = d_v_.as<double>();
         a.leak = d_leak_.as<double>();
@@ -1106,9 +1171,15 @@ void Engine::get_synapse_weights(double* out, int64_t count) {
     const size_t esz = f64_ ? 8 : 4;
     std::vector<uint8_t> host(d_w_.bytes);
     cuda_check(cudaMemcpy(host.data(), d_w_.p, d_w_.bytes, cudaMemcpyDeviceToHost), "weights D2H");
+    std::vector<uint32_t> meta;
+    if (!dense_ && !dict_.empty()) {
+        meta.resize(static_cast<size_t>(sparse_elems_));
+        if (!meta.empty()) cuda_check(cudaMemcpy(meta.data(), d_meta_.p, meta.size() * 4, cudaMemcpyDeviceToHost), "meta D2H");
+    }
     for (size_t s = 0; s < pre_.size(); ++s) {
         if (slot_[s] < 0) { out[s] = 0.0; continue; }
-        if (esz == 8) out[s] = reinterpret_cast<const double*>(host.data())[slot_[s]];
+        if (!meta.empty()) out[s] = dict_[meta[slot_[s]] >> 23];
+        else if (esz == 8) out[s] = reinterpret_cast<const double*>(host.data())[slot_[s]];
         else out[s] = static_cast<double>(reinterpret_cast<const float*>(host.data())[slot_[s]]);
     }
 }
@@ -1136,7 +1207,7 @@ void Engine::get_weight_matrix(double* out, int64_t count) {
         for (int b = 0; b < nblocks_; ++b)
             for (int p = 0; p < nl_; ++p)
                 for (int64_t q = off[static_cast<size_t>(b) * nl_ + p]; q < off[static_cast<size_t>(b) * nl_ + p + 1]; ++q) {
-                    const double w = get(q);
+                    const double w = sparse_weight(host, meta, q);
                     const int i = b * pb_ + static_cast<int>(meta[q] & 0xffffu);
                     if (w != 0.0) out[static_cast<int64_t>(i) * nl_ + p] = w;
                 }

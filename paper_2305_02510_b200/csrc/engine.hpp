@@ -159,6 +159,10 @@ private:
     // sparse
     int32_t pb_ = 0, nblocks_ = 0, sub_ = 32, posts_per_cta_ = 0, sparse_gx_ = 1;
     int64_t sparse_elems_ = 0;
+    std::vector<double> dict_;   // sparse weight dictionary (empty: weights stored per synapse)
+    DevBuf d_wdict_;
+    void upload_dict();
+    double sparse_weight(const std::vector<uint8_t>& host_w, const std::vector<uint32_t>& meta, int64_t q) const;
     // dense plan
     int32_t tile_w_ = 0, rows_per_chunk_ = 0, nchunks_ = 1, dense_grid_ = 1;
     bool persistent_ = false;     // small dense nets: one cooperative launch per simulate

@@ -665,7 +665,7 @@ template <int HB> struct HistT { using T = uint64_t; };
 template <> struct HistT<16> { using T = uint16_t; };
 template <> struct HistT<32> { using T = uint32_t; };
 
-template <typename WT, bool STDP, int HB, int SUB>
+template <typename WT, bool STDP, int HB, int SUB, bool DICT>
 __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     using HT = typename HistT<HB>::T;
@@ -685,6 +685,11 @@ __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
             else sh[k] = static_cast<HT>(__ldg(a.hist_lo + pre0 + k));
         }
     }
+    // weight dictionary (non-plastic nets with <= 512 distinct weights): the
+    // meta word carries the index, so the weight stream disappears (4 B/synapse)
+    WT* s_wd = reinterpret_cast<WT*>(smem_raw + (((HB == 1 ? ((a.pb + 31) / 32) * 4 : a.pb * (HB / 8)) + 15) & ~15));
+    if (DICT)
+        for (int k = tid; k < a.dict_size; k += kThreads) s_wd[k] = static_cast<const WT*>(a.wdict)[k];
     __syncthreads();
     const uint32_t* sbits = reinterpret_cast<const uint32_t*>(smem_raw);
     const HT* shist = reinterpret_cast<const HT*>(smem_raw);
@@ -717,7 +722,10 @@ __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
             for (int64_t q = beg + sl * 4; q < end; q += SUB * 4) {
                 const uint4 m4 = __ldcs(reinterpret_cast<const uint4*>(a.meta + q));
                 WT wv[4];
-                if (sizeof(WT) == 4) {
+                if (DICT) {
+                    wv[0] = s_wd[m4.x >> 23]; wv[1] = s_wd[m4.y >> 23];
+                    wv[2] = s_wd[m4.z >> 23]; wv[3] = s_wd[m4.w >> 23];
+                } else if (sizeof(WT) == 4) {
                     const float4 f = __ldcs(reinterpret_cast<const float4*>(W + q));
                     wv[0] = f.x; wv[1] = f.y; wv[2] = f.z; wv[3] = f.w;
                 } else {
@@ -736,7 +744,7 @@ __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
                     if (HB == 1) e = (sbits[pl >> 5] >> (pl & 31)) & 1u;
                     else e = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
                     WT w = wv[k];
-                    if (STDP && ((m >> 22) & 1u)) {
+                    if (!DICT && STDP && ((m >> 22) & 1u)) {
                         const WT pt = pot[static_cast<int64_t>(pre0 + pl) * a.dp + d1];
                         WT dw = WT(0);
                         if (sp) dw += pt;
@@ -748,7 +756,7 @@ __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
                     }
                     if (e) sum += w;
                 }
-                if (STDP && changed) {
+                if (!DICT && STDP && changed) {
                     if (sizeof(WT) == 4) {
                         __stcs(reinterpret_cast<float4*>(W + q),
                                make_float4(float(wv[0]), float(wv[1]), float(wv[2]), float(wv[3])));
@@ -1028,13 +1036,13 @@ __global__ void k_er_sparse_fill(ErArgs e, int first, int nl, int pb, int nblock
         if (!er_edge(e, i, j)) continue;
         const int d = er_delay(e, i, j);
         meta[q] = static_cast<uint32_t>(i - i0) | (static_cast<uint32_t>(d - 1) << 16) |
-                  (e.stdp ? (1u << 22) : 0u);
-        w[q] = wt;
+                  (e.stdp ? (1u << 22) : 0u);   // dictionary index 0 (bits 23..31) = e.weight
+        if (w) w[q] = wt;
         ++q;
     }
     for (; q < end; ++q) {  // padding: never delivers, never plastic
-        meta[q] = 0;
-        w[q] = WT(0);
+        meta[q] = w ? 0u : (1u << 23);      // dictionary entry 1 = 0.0
+        if (w) w[q] = WT(0);
     }
 }
 
@@ -1196,13 +1204,24 @@ void launch_dense(const DenseArgs& a, bool f64, bool stdp, bool delay, bool exac
 
 template <typename WT, bool STDP, int HB>
 static void sparse_go_sub(const SparseArgs& a, int sub, int gx, size_t smem, cudaStream_t s) {
+    if (a.dict_size > 0 && sub == 0) sub = 16;  // the dictionary path lives in the pull kernel
     dim3 grid(gx, a.nblocks);
+    if (a.dict_size > 0) smem = ((smem + 15) & ~static_cast<size_t>(15)) + static_cast<size_t>(a.dict_size) * sizeof(WT);
+    if (a.dict_size > 0 && !STDP) {
+        switch (sub) {
+            case 4: k_sparse_pull<WT, false, HB, 4, true><<<grid, kThreads, smem, s>>>(a); break;
+            case 8: k_sparse_pull<WT, false, HB, 8, true><<<grid, kThreads, smem, s>>>(a); break;
+            case 16: k_sparse_pull<WT, false, HB, 16, true><<<grid, kThreads, smem, s>>>(a); break;
+            default: k_sparse_pull<WT, false, HB, 32, true><<<grid, kThreads, smem, s>>>(a); break;
+        }
+        return;
+    }
     switch (sub) {
         case 0: k_sparse_stream<WT, STDP, HB><<<grid, kThreads, smem, s>>>(a); break;
-        case 4: k_sparse_pull<WT, STDP, HB, 4><<<grid, kThreads, smem, s>>>(a); break;
-        case 8: k_sparse_pull<WT, STDP, HB, 8><<<grid, kThreads, smem, s>>>(a); break;
-        case 16: k_sparse_pull<WT, STDP, HB, 16><<<grid, kThreads, smem, s>>>(a); break;
-        default: k_sparse_pull<WT, STDP, HB, 32><<<grid, kThreads, smem, s>>>(a); break;
+        case 4: k_sparse_pull<WT, STDP, HB, 4, false><<<grid, kThreads, smem, s>>>(a); break;
+        case 8: k_sparse_pull<WT, STDP, HB, 8, false><<<grid, kThreads, smem, s>>>(a); break;
+        case 16: k_sparse_pull<WT, STDP, HB, 16, false><<<grid, kThreads, smem, s>>>(a); break;
+        default: k_sparse_pull<WT, STDP, HB, 32, false><<<grid, kThreads, smem, s>>>(a); break;
     }
 }
 

@@ -119,6 +119,8 @@ struct SparseArgs {
     int32_t dp;
     double w_min, w_max;
     int32_t posts_per_cta;
+    const void* wdict;         // WT[dict_size] weight dictionary (meta bits 23..31) or null
+    int32_t dict_size;         // 0: weights stream from w[]
     double* partial;           // [nblocks][nl]
     const double* v;
     const double* leak;
