@@ -681,7 +681,7 @@ void Engine::plan_launches() {
         // per-warp chunk stream (k_sparse_stream, 1.115 ms) stays selectable for
         // A/B runs with SNB_SPARSE_KERNEL=stream (tools/ab_sparse.sh)
         const char* sk = std::getenv("SNB_SPARSE_KERNEL");
-        if (sk && std::string(sk) == "stream" && dict_.empty()) sub_ = 0;
+        if (sk && std::string(sk) == "stream") sub_ = 0;
         const int target = sms * 8;
         int gx = std::max(1, target / std::max(1, nblocks_));
         const int unit = sub_ == 0 ? 8 : 8 * (32 / sub_);

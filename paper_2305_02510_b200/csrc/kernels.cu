@@ -781,11 +781,11 @@ __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
 // segmented suffix-reduction over lanes folds chunks into per-post sums, and
 // the last segment's sum is carried into the next iteration.  The order of
 // additions is fixed by the data layout, so results are deterministic.
-template <typename WT, bool STDP, int HB>
+template <typename WT, bool STDP, int HB, bool DICT>
 __global__ void __launch_bounds__(kThreads) k_sparse_stream(SparseArgs a) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     using HT = typename HistT<HB>::T;
-    constexpr int U = 4;
+    constexpr int U = DICT ? 8 : 4;
     const int b = blockIdx.y;
     const int pre0 = b * a.pb;
     const int pcount = min(a.pb, a.n - pre0);
@@ -802,6 +802,9 @@ __global__ void __launch_bounds__(kThreads) k_sparse_stream(SparseArgs a) {
             else sh[k] = static_cast<HT>(__ldcg(a.hist_lo + pre0 + k));
         }
     }
+    WT* s_wd = reinterpret_cast<WT*>(smem_raw + (((HB == 1 ? ((a.pb + 31) / 32) * 4 : a.pb * (HB / 8)) + 15) & ~15));
+    if (DICT)
+        for (int k = tid; k < a.dict_size; k += kThreads) s_wd[k] = static_cast<const WT*>(a.wdict)[k];
     __syncthreads();
     const uint32_t* sbits = reinterpret_cast<const uint32_t*>(smem_raw);
     const HT* shist = reinterpret_cast<const HT*>(smem_raw);
@@ -847,7 +850,9 @@ __global__ void __launch_bounds__(kThreads) k_sparse_stream(SparseArgs a) {
             const int64_t q = e + static_cast<int64_t>(u * 32 + lane) * 4;
             if (q < end) {
                 m4[u] = __ldcs(reinterpret_cast<const uint4*>(a.meta + q));
-                if (sizeof(WT) == 4) {
+                if (DICT) {
+                    // resolved after the loads (smem), see below
+                } else if (sizeof(WT) == 4) {
                     const float4 f = __ldcs(reinterpret_cast<const float4*>(W + q));
                     wv[u][0] = f.x; wv[u][1] = f.y; wv[u][2] = f.z; wv[u][3] = f.w;
                 } else {
@@ -864,6 +869,11 @@ __global__ void __launch_bounds__(kThreads) k_sparse_stream(SparseArgs a) {
         for (int u = 0; u < U; ++u) {
             const int64_t q = e + static_cast<int64_t>(u * 32 + lane) * 4;
             const bool valid = q < end;
+            if (DICT) {
+                wv[u][0] = s_wd[m4[u].x >> 23]; wv[u][1] = s_wd[m4[u].y >> 23];
+                wv[u][2] = s_wd[m4[u].z >> 23]; wv[u][3] = s_wd[m4[u].w >> 23];
+                if (!valid) wv[u][0] = wv[u][1] = wv[u][2] = wv[u][3] = WT(0);
+            }
             int p = pb;  // sentinel for lanes past the end
             if (valid) {
                 while (__ldg(off + lp + 1) <= q) ++lp;
@@ -1204,11 +1214,11 @@ void launch_dense(const DenseArgs& a, bool f64, bool stdp, bool delay, bool exac
 
 template <typename WT, bool STDP, int HB>
 static void sparse_go_sub(const SparseArgs& a, int sub, int gx, size_t smem, cudaStream_t s) {
-    if (a.dict_size > 0 && sub == 0) sub = 16;  // the dictionary path lives in the pull kernel
     dim3 grid(gx, a.nblocks);
     if (a.dict_size > 0) smem = ((smem + 15) & ~static_cast<size_t>(15)) + static_cast<size_t>(a.dict_size) * sizeof(WT);
     if (a.dict_size > 0 && !STDP) {
         switch (sub) {
+            case 0: k_sparse_stream<WT, false, HB, true><<<grid, kThreads, smem, s>>>(a); break;
             case 4: k_sparse_pull<WT, false, HB, 4, true><<<grid, kThreads, smem, s>>>(a); break;
             case 8: k_sparse_pull<WT, false, HB, 8, true><<<grid, kThreads, smem, s>>>(a); break;
             case 16: k_sparse_pull<WT, false, HB, 16, true><<<grid, kThreads, smem, s>>>(a); break;
@@ -1217,7 +1227,7 @@ static void sparse_go_sub(const SparseArgs& a, int sub, int gx, size_t smem, cud
         return;
     }
     switch (sub) {
-        case 0: k_sparse_stream<WT, STDP, HB><<<grid, kThreads, smem, s>>>(a); break;
+        case 0: k_sparse_stream<WT, STDP, HB, false><<<grid, kThreads, smem, s>>>(a); break;
         case 4: k_sparse_pull<WT, STDP, HB, 4, false><<<grid, kThreads, smem, s>>>(a); break;
         case 8: k_sparse_pull<WT, STDP, HB, 8, false><<<grid, kThreads, smem, s>>>(a); break;
         case 16: k_sparse_pull<WT, STDP, HB, 16, false><<<grid, kThreads, smem, s>>>(a); break;
