@@ -704,13 +704,28 @@ __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
     constexpr int PER_WARP = 32 / SUB;
     const int warp = tid >> 5, lane = tid & 31;
     const int sg = lane / SUB, sl = lane % SUB;
-    for (int pb = p0 + warp * PER_WARP; pb < p1; pb += (kThreads / 32) * PER_WARP) {
-        const int p = pb + sg;
+    // Software pipeline: the next post's list bounds are loaded while the
+    // current post streams, and each post's chunks are fetched UL at a time
+    // (all loads issued before any use) -- one memory round trip per post.
+    constexpr int UL = DICT ? 4 : 2;
+    const int stride = (kThreads / 32) * PER_WARP;
+    const int64_t* offb = a.off + static_cast<int64_t>(b) * a.nl;
+    int p = p0 + warp * PER_WARP + sg;
+    int64_t beg = 0, end = 0;
+    if (p < p1) {
+        beg = __ldg(offb + p);
+        end = __ldg(offb + p + 1);
+    }
+    for (int pbase = p0 + warp * PER_WARP; pbase < p1; pbase += stride) {  // warp-uniform trip count
         const bool valid = p < p1;
+        const int pn = p + stride;
+        int64_t nbeg = 0, nend = 0;
+        if (pn < p1) {
+            nbeg = __ldg(offb + pn);
+            nend = __ldg(offb + pn + 1);
+        }
         WT sum = WT(0);
         if (valid) {
-            const int64_t beg = a.off[static_cast<int64_t>(b) * a.nl + p];
-            const int64_t end = a.off[static_cast<int64_t>(b) * a.nl + p + 1];
             const int gp = a.first + p;
             bool sp = false;
             WT depp = WT(0);
@@ -718,51 +733,65 @@ __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
                 sp = bit_of(a.bits, gp);
                 depp = dep[gp];
             }
-#pragma unroll 2
-            for (int64_t q = beg + sl * 4; q < end; q += SUB * 4) {
-                const uint4 m4 = __ldcs(reinterpret_cast<const uint4*>(a.meta + q));
-                WT wv[4];
-                if (DICT) {
-                    wv[0] = s_wd[m4.x >> 23]; wv[1] = s_wd[m4.y >> 23];
-                    wv[2] = s_wd[m4.z >> 23]; wv[3] = s_wd[m4.w >> 23];
-                } else if (sizeof(WT) == 4) {
-                    const float4 f = __ldcs(reinterpret_cast<const float4*>(W + q));
-                    wv[0] = f.x; wv[1] = f.y; wv[2] = f.z; wv[3] = f.w;
-                } else {
-                    const double2 f0 = __ldcs(reinterpret_cast<const double2*>(W + q));
-                    const double2 f1 = __ldcs(reinterpret_cast<const double2*>(W + q + 2));
-                    wv[0] = f0.x; wv[1] = f0.y; wv[2] = f1.x; wv[3] = f1.y;
-                }
-                const uint32_t ms[4] = {m4.x, m4.y, m4.z, m4.w};
-                bool changed = false;
+            for (int64_t q0 = beg + sl * 4; q0 < end; q0 += SUB * 4 * UL) {
+                uint4 m4[UL];
+                WT wv[UL][4];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t m = ms[k];
-                    const int pl = static_cast<int>(m & 0xffffu);
-                    const int d1 = static_cast<int>((m >> 16) & 63u);
-                    uint32_t e;
-                    if (HB == 1) e = (sbits[pl >> 5] >> (pl & 31)) & 1u;
-                    else e = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
-                    WT w = wv[k];
-                    if (!DICT && STDP && ((m >> 22) & 1u)) {
-                        const WT pt = pot[static_cast<int64_t>(pre0 + pl) * a.dp + d1];
-                        WT dw = WT(0);
-                        if (sp) dw += pt;
-                        if (e) dw -= depp;
-                        const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
-                        changed |= (nw != w);
-                        w = nw;
-                        wv[k] = nw;
+                for (int u = 0; u < UL; ++u) {
+                    const int64_t q = q0 + static_cast<int64_t>(u) * SUB * 4;
+                    if (q < end) {
+                        m4[u] = __ldcs(reinterpret_cast<const uint4*>(a.meta + q));
+                        if (!DICT) {
+                            if (sizeof(WT) == 4) {
+                                const float4 f = __ldcs(reinterpret_cast<const float4*>(W + q));
+                                wv[u][0] = f.x; wv[u][1] = f.y; wv[u][2] = f.z; wv[u][3] = f.w;
+                            } else {
+                                const double2 f0 = __ldcs(reinterpret_cast<const double2*>(W + q));
+                                const double2 f1 = __ldcs(reinterpret_cast<const double2*>(W + q + 2));
+                                wv[u][0] = f0.x; wv[u][1] = f0.y; wv[u][2] = f1.x; wv[u][3] = f1.y;
+                            }
+                        }
                     }
-                    if (e) sum += w;
                 }
-                if (!DICT && STDP && changed) {
-                    if (sizeof(WT) == 4) {
-                        __stcs(reinterpret_cast<float4*>(W + q),
-                               make_float4(float(wv[0]), float(wv[1]), float(wv[2]), float(wv[3])));
-                    } else {
-                        __stcs(reinterpret_cast<double2*>(W + q), make_double2(double(wv[0]), double(wv[1])));
-                        __stcs(reinterpret_cast<double2*>(W + q + 2), make_double2(double(wv[2]), double(wv[3])));
+#pragma unroll
+                for (int u = 0; u < UL; ++u) {
+                    const int64_t q = q0 + static_cast<int64_t>(u) * SUB * 4;
+                    if (q >= end) continue;
+                    if (DICT) {
+                        wv[u][0] = s_wd[m4[u].x >> 23]; wv[u][1] = s_wd[m4[u].y >> 23];
+                        wv[u][2] = s_wd[m4[u].z >> 23]; wv[u][3] = s_wd[m4[u].w >> 23];
+                    }
+                    const uint32_t ms[4] = {m4[u].x, m4[u].y, m4[u].z, m4[u].w};
+                    bool changed = false;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t m = ms[k];
+                        const int pl = static_cast<int>(m & 0xffffu);
+                        const int d1 = static_cast<int>((m >> 16) & 63u);
+                        uint32_t e;
+                        if (HB == 1) e = (sbits[pl >> 5] >> (pl & 31)) & 1u;
+                        else e = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
+                        WT w = wv[u][k];
+                        if (!DICT && STDP && ((m >> 22) & 1u)) {
+                            const WT pt = pot[static_cast<int64_t>(pre0 + pl) * a.dp + d1];
+                            WT dw = WT(0);
+                            if (sp) dw += pt;
+                            if (e) dw -= depp;
+                            const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
+                            changed |= (nw != w);
+                            w = nw;
+                            wv[u][k] = nw;
+                        }
+                        if (e) sum += w;
+                    }
+                    if (!DICT && STDP && changed) {
+                        if (sizeof(WT) == 4) {
+                            __stcs(reinterpret_cast<float4*>(W + q),
+                                   make_float4(float(wv[u][0]), float(wv[u][1]), float(wv[u][2]), float(wv[u][3])));
+                        } else {
+                            __stcs(reinterpret_cast<double2*>(W + q), make_double2(double(wv[u][0]), double(wv[u][1])));
+                            __stcs(reinterpret_cast<double2*>(W + q + 2), make_double2(double(wv[u][2]), double(wv[u][3])));
+                        }
                     }
                 }
             }
@@ -770,6 +799,9 @@ __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
 #pragma unroll
         for (int o = SUB / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
         if (valid && sl == 0) a.partial[static_cast<int64_t>(b) * a.nl + p] = static_cast<double>(sum);
+        p = pn;
+        beg = nbeg;
+        end = nend;
     }
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *a.d_step += 1;
 }
