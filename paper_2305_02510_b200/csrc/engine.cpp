@@ -669,6 +669,19 @@ void Engine::plan_launches() {
             rows_per_chunk_ = rpc;
             nchunks_ = nch;
             dense_grid_ = dynamic_sched_ ? std::min(ntiles * nchunks_, resident) : ntiles * nchunks_;
+            // TMA-staged variant (fp32, unit delays): one CTA per SM claiming items
+            const char* dk = std::getenv("SNB_DENSE_KERNEL");
+            tma_ = !f64_ && !has_delay_ && dk && std::string(dk) == "tma";
+            if (tma_) {
+                const char* tw = std::getenv("SNB_TMA_WAVES");
+                const double tw_waves = tw ? std::atof(tw) : 6.0;
+                int tn = std::max(1, static_cast<int>(std::lround(tw_waves * sms / ntiles)));
+                int trpc = static_cast<int>(round_up(std::max(32, (n_ + tn - 1) / tn), 32));
+                trpc = std::min(trpc, dense_tma_max_rows());
+                rows_per_chunk_ = trpc;
+                nchunks_ = (n_ + trpc - 1) / trpc;
+                dense_grid_ = std::min(sms, ntiles * nchunks_);
+            }
         }
         const int items = ntiles * nchunks_;
         if (exact_) dense_grid_ = std::min(items, sms * 8);
@@ -820,14 +833,15 @@ DenseArgs Engine::dense_args() {
     a.reset = d_reset_.as<double>();
     a.u_exact = d_uexact_.as<double>();
     a.d_step = d_step_.as<int32_t>();
-    a.work = (dynamic_sched_ && !exact_ && !persistent_) ? d_work_.as<int32_t>() : nullptr;
+    a.work = ((dynamic_sched_ || tma_) && !exact_ && !persistent_) ? d_work_.as<int32_t>() : nullptr;
     return a;
 }
 
 void Engine::launch_sweep() {
     if (dense_) {
         DenseArgs a = dense_args();
-        launch_dense(a, f64_, stdp_on_, has_delay_, exact_, dense_grid_, stream_);
+        if (tma_) launch_dense_tma(a, stdp_on_, dense_grid_, stream_);
+        else launch_dense(a, f64_, stdp_on_, has_delay_, exact_, dense_grid_, stream_);
     } else {
         SparseArgs a{};
         a.n = n_;

@@ -167,6 +167,7 @@ private:
     int32_t tile_w_ = 0, rows_per_chunk_ = 0, nchunks_ = 1, dense_grid_ = 1;
     bool persistent_ = false;     // small dense nets: one cooperative launch per simulate
     bool dynamic_sched_ = false;  // dense sweep items claimed through an atomic counter
+    bool tma_ = false;            // k_dense_tma (cp.async.bulk ring) instead of k_dense_stream
     int32_t persist_grid_ = 1;
     double sweep_bytes_full_ = 0.0;  // algorithmic bytes of a sweep over every active row
 

@@ -633,6 +633,251 @@ __global__ void __launch_bounds__(kThreads, 2) k_dense_stream(DenseArgs a) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.d_step += 1;  // no other CTA reads it
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged dense sweep (fp32, unit delays): one CTA per SM, a producer warp
+// streams the active rows' tile segments into a kTmaStages-deep shared-memory
+// ring with cp.async.bulk (completion on mbarriers), 8 consumer warps apply
+// the same per-element update as k_dense_stream from shared memory and write
+// the new weights with 128-bit streaming stores.  Loads never occupy
+// registers, so the in-flight window per SM is the whole ring.
+constexpr int kTmaRows = 4;        // rows per stage
+constexpr int kTmaStages = 8;      // ring depth
+constexpr int kTmaListMax = 2048;  // rows per item (one list build per item)
+constexpr int kTmaThreads = 288;   // 8 consumer warps + 1 producer warp
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <bool STDP>
+__global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const bool producer = warp == 8;
+    const int ntiles = (a.nl + a.tile_w - 1) / a.tile_w;
+    const int items = ntiles * a.nchunks;
+    const uint32_t row_bytes = static_cast<uint32_t>(a.tile_w) * 4u;
+    const size_t stage_bytes = static_cast<size_t>(kTmaRows) * row_bytes;
+    float* ring = reinterpret_cast<float*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * stage_bytes);
+    uint64_t* empty = full + kTmaStages;
+    RowRec<float>* s_rec = reinterpret_cast<RowRec<float>*>(empty + kTmaStages);
+    __shared__ uint32_t s_word[32];
+    __shared__ int32_t s_wpref[33];
+    __shared__ int32_t s_cnt;
+    __shared__ int s_item;
+
+    const float wmin = static_cast<float>(a.w_min), wmax = static_cast<float>(a.w_max);
+    const float* dep = static_cast<const float*>(a.dep);
+    const float* pot = static_cast<const float*>(a.pot);
+    float* W = static_cast<float*>(a.w);
+
+    if (tid == 0) {
+        for (int s = 0; s < kTmaStages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    uint32_t it = 0;  // ring position, advanced identically by producer and consumers
+    int item = blockIdx.x;
+    if (a.work) {
+        if (tid == 0) s_item = atomicAdd(a.work, 1);
+        __syncthreads();
+        item = s_item;
+    }
+    while (item < items) {
+        const int chunk = item / ntiles;
+        const int tile = item - chunk * ntiles;
+        const int col0 = tile * a.tile_w;
+        const int width = static_cast<int>(min(static_cast<int64_t>(a.tile_w), a.pitch - col0));
+        const uint32_t copy_bytes = static_cast<uint32_t>(width) * 4u;
+        const int r0 = chunk * a.rows_per_chunk;
+        const int r1 = min(a.n, r0 + a.rows_per_chunk);
+
+        // active-row list of [r0, r1) in <= 1024-row pieces (32-aligned bases)
+        if (tid == 0) s_cnt = 0;
+        __syncthreads();
+        for (int sa = r0, sb_next = r0; sa < r1; sa = sb_next) {
+            const int base = sa & ~31;
+            const int sb = min(r1, base + kSubRows);
+            sb_next = sb;
+            const int nwords = (sb - base + 31) >> 5;
+            const int cnt0 = s_cnt;
+            if (tid < 32) {
+                uint32_t wd = 0;
+                if (tid < nwords) {
+                    wd = __ldcg(a.active + (base >> 5) + tid);
+                    const int lo = sa - (base + tid * 32);
+                    if (lo > 0) wd &= (lo >= 32) ? 0u : ~((1u << lo) - 1u);
+                    const int rem = sb - (base + tid * 32);
+                    if (rem < 32) wd &= (rem <= 0) ? 0u : ((1u << rem) - 1u);
+                }
+                const int c = __popc(wd);
+                int incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int x = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (tid >= o) incl += x;
+                }
+                s_word[tid] = wd;
+                s_wpref[tid] = cnt0 + incl - c;
+                if (tid == 31) s_wpref[32] = cnt0 + incl;
+            }
+            __syncthreads();
+            for (int r = sa + tid; r < sb; r += kTmaThreads) {
+                const int l = (r - base) >> 5, b = (r - base) & 31;
+                const uint32_t wd = s_word[l];
+                if ((wd >> b) & 1u) {
+                    const int pos = s_wpref[l] + __popc(wd & ((1u << b) - 1u));
+                    const uint64_t h = __ldcg(a.hist + r);
+                    RowRec<float> rec;
+                    const int kind = STDP ? static_cast<int>(__ldg(a.kind + r)) : 0;
+                    rec.rowk = r | (kind << 28);
+                    rec.e_lo = static_cast<uint32_t>(h);
+                    rec.e_hi = static_cast<uint32_t>(h >> 32);
+                    rec.pot = STDP ? __ldcg(pot + r) : 0.f;
+                    s_rec[pos] = rec;
+                }
+            }
+            __syncthreads();
+            if (tid == 0) s_cnt = s_wpref[32];
+            __syncthreads();
+        }
+        const int cnt = s_cnt;
+        const int ngroups = (cnt + kTmaRows - 1) / kTmaRows;
+
+        if (producer) {
+            if (lane == 0) {
+                for (int g = 0; g < ngroups; ++g, ++it) {
+                    const int s = it % kTmaStages;
+                    const uint32_t ph = (it / kTmaStages) & 1u;
+                    mbar_wait(empty + s, ph ^ 1u);
+                    const int nr = min(kTmaRows, cnt - g * kTmaRows);
+                    mbar_arrive_expect_tx(full + s, static_cast<uint32_t>(nr) * copy_bytes);
+                    for (int r = 0; r < nr; ++r) {
+                        const int row = s_rec[g * kTmaRows + r].rowk & 0x0fffffff;
+                        bulk_g2s(reinterpret_cast<uint8_t*>(ring) + s * stage_bytes + static_cast<size_t>(r) * row_bytes,
+                                 W + static_cast<int64_t>(row) * a.pitch + col0, copy_bytes, full + s);
+                    }
+                }
+            } else {
+                it += ngroups;
+            }
+        } else {
+            const int tcol = tid * 4;
+            const int c0 = col0 + tcol;
+            const bool in_tile = tcol < width && c0 < a.nl;
+            const int gc0 = a.first + c0;
+            float sjf[4], depj[4];
+            double acc[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const bool ok = in_tile && (c0 + k) < a.nl;
+                sjf[k] = (ok && STDP && bit_of(a.bits, gc0 + k)) ? 1.f : 0.f;
+                depj[k] = (ok && STDP) ? __ldcg(dep + gc0 + k) : 0.f;
+                acc[k] = 0.0;
+            }
+            for (int g = 0; g < ngroups; ++g, ++it) {
+                const int s = it % kTmaStages;
+                const uint32_t ph = (it / kTmaStages) & 1u;
+                mbar_wait(full + s, ph);
+                const int nr = min(kTmaRows, cnt - g * kTmaRows);
+                float grp[4] = {0.f, 0.f, 0.f, 0.f};
+                if (in_tile) {
+#pragma unroll
+                    for (int r = 0; r < kTmaRows; ++r) {
+                        if (r >= nr) break;
+                        const RowRec<float> rec = s_rec[g * kTmaRows + r];
+                        const int row = rec.rowk & 0x0fffffff;
+                        const int kind = rec.rowk >> 28;
+                        const float4 wv = *reinterpret_cast<const float4*>(
+                            reinterpret_cast<const uint8_t*>(ring) + s * stage_bytes + static_cast<size_t>(r) * row_bytes + tcol * 4);
+                        float w[4] = {wv.x, wv.y, wv.z, wv.w};
+                        const float ef = (rec.e_lo & 1u) ? 1.f : 0.f;
+                        if (STDP && kind != kRowNone) {
+                            float nw[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const float dw = fmaf(sjf[k], rec.pot, -(ef * depj[k]));
+                                nw[k] = clamp_ref<float>(w[k] + dw, wmin, wmax);
+                            }
+                            if (kind == kRowAllButSelf) {
+                                const int selfk = row - gc0;
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) nw[k] = (selfk == k) ? w[k] : nw[k];
+                            } else if (kind == kRowMixed) {
+                                const uint32_t mv =
+                                    __ldg(a.mask + static_cast<int64_t>(row) * (a.pitch >> 5) + (c0 >> 5)) >> (c0 & 31);
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) nw[k] = ((mv >> k) & 1u) ? nw[k] : w[k];
+                            }
+                            __stcs(reinterpret_cast<float4*>(W + static_cast<int64_t>(row) * a.pitch + c0),
+                                   make_float4(nw[0], nw[1], nw[2], nw[3]));
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) w[k] = nw[k];
+                        }
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) grp[k] = fmaf(ef, w[k], grp[k]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + s);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc[k] += static_cast<double>(grp[k]);
+            }
+            if (in_tile) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (c0 + k < a.nl) a.partial[static_cast<int64_t>(chunk) * a.nl + c0 + k] = acc[k];
+            }
+        }
+        __syncthreads();  // ring drained for this item's rows; list may be rebuilt
+        if (a.work) {
+            if (tid == 0) s_item = atomicAdd(a.work, 1);
+            __syncthreads();
+            item = s_item;
+        } else {
+            item += gridDim.x;
+        }
+    }
+    if (blockIdx.x == 0 && tid == 0) *a.d_step += 1;
+}
+
+size_t dense_tma_smem(int tile_w) {
+    return static_cast<size_t>(kTmaStages) * kTmaRows * tile_w * 4 + 2 * kTmaStages * 8 +
+           static_cast<size_t>(kTmaListMax + kTmaRows) * sizeof(RowRec<float>);
+}
+
 // Persistent single-GPU step loop for small dense nets (launch-latency bound
 // otherwise): one cooperative launch runs `steps` steps; neuron phase and
 // sweep phase are separated by grid-wide barriers (cooperative groups).
@@ -1104,6 +1349,21 @@ uint64_t stream_key(uint64_t seed, uint64_t stream) {
 }
 
 int dense_vec(bool f64) { return f64 ? 2 : 4; }
+
+int dense_tma_max_rows() { return kTmaListMax; }
+
+void launch_dense_tma(const DenseArgs& a, bool stdp, int grid, cudaStream_t s) {
+    const size_t smem = dense_tma_smem(a.tile_w);
+    static size_t configured[2] = {0, 0};
+    auto kern = stdp ? k_dense_tma<true> : k_dense_tma<false>;
+    if (configured[stdp ? 1 : 0] < smem) {
+        check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+              "k_dense_tma smem attribute");
+        configured[stdp ? 1 : 0] = smem;
+    }
+    kern<<<grid, kTmaThreads, smem, s>>>(a);
+    check(cudaGetLastError(), "k_dense_tma");
+}
 int dense_threads() { return kThreads; }
 int sparse_block_pres(int hbits) {
     // 32 KB of staged history per CTA (pre ids are 16-bit block-local)
