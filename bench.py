@@ -260,7 +260,8 @@ def run_ours(args):
         "spikes_timed": timed_spikes,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "k_dense_sweep (fused STDP + propagation)" if st["dense"] else "k_sparse_pull",
+                     "kernel": sn._capi.Stats.KERNEL_NAMES.get(st["sweep_kernel"], "?"),
+                     "kernel_ctas": st["sweep_ctas"],
                      "bytes_per_launch": bytes_per_sweep, "avg_launch_ms": sweep_avg_ms,
                      "peak_source": peak_src},
         "cpu_baseline": cpu,

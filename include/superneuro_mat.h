@@ -116,7 +116,20 @@ typedef struct sn_stats {
     double last_simulate_ms;    /* device time of the last sn_simulate (events) */
     double sweep_bytes_per_launch_last; /* algorithmic bytes of the last sweep */
     double sweep_bytes_total;   /* algorithmic bytes of all sweeps since reset */
+    int32_t sweep_kernel;       /* sn_sweep_kernel of the plan chosen at sn_setup */
+    int32_t sweep_ctas;         /* grid size of that kernel */
 } sn_stats;
+
+typedef enum sn_sweep_kernel {
+    SN_SWEEP_DENSE_STREAM = 1,  /* k_dense_stream: 128-bit LDG/STG streaming sweep */
+    SN_SWEEP_DENSE_TMA = 2,     /* k_dense_tma: cp.async.bulk ring, one CTA per SM */
+    SN_SWEEP_DENSE_EXACT = 3,   /* k_dense_sweep<EXACT>: ascending-pre fp64 order */
+    SN_SWEEP_PERSISTENT = 4,    /* k_persistent_dense: whole step loop in one launch */
+    SN_SWEEP_SPARSE_PULL = 5,   /* k_sparse_pull: SUB lanes per post, weights streamed */
+    SN_SWEEP_SPARSE_DICT = 6,   /* k_sparse_pull with the weight dictionary (4 B/synapse) */
+    SN_SWEEP_SPARSE_STREAM = 7, /* k_sparse_stream: flat chunk stream per warp */
+    SN_SWEEP_SPARSE_EXACT = 8   /* k_sparse_exact: one thread per post, ascending pre */
+} sn_sweep_kernel;
 
 /* ---- lifecycle ---------------------------------------------------------- */
 SN_API sn_status sn_options_init(sn_options* opts);

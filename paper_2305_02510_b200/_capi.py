@@ -61,7 +61,13 @@ class Stats(C.Structure):
         ("last_simulate_ms", C.c_double),
         ("sweep_bytes_per_launch_last", C.c_double),
         ("sweep_bytes_total", C.c_double),
+        ("sweep_kernel", C.c_int32),
+        ("sweep_ctas", C.c_int32),
     ]
+
+    KERNEL_NAMES = {1: "k_dense_stream", 2: "k_dense_tma", 3: "k_dense_sweep<exact>",
+                    4: "k_persistent_dense", 5: "k_sparse_pull", 6: "k_sparse_pull<dict>",
+                    7: "k_sparse_stream", 8: "k_sparse_exact"}
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <numeric>
 #include <sstream>
+#include <thread>
 #include <cstdlib>
 #include <unordered_map>
 #include <unordered_set>
@@ -1123,45 +1124,78 @@ void Engine::comm_init(const uint8_t* id, int32_t rank, int32_t world) {
 }
 
 // ---- results -------------------------------------------------------------------
+// Bitmask raster -> (step, neuron) events, ascending: per-row popcounts, a
+// prefix sum, then rows decoded in parallel straight into the two arrays.
 void Engine::decode_raster() {
     if (events_valid_) return;
-    events_.clear();
-    for (const RasterChunk& ch : raster_) {
-        for (int r = 0; r < ch.rows; ++r) {
-            const uint32_t* row = ch.words.data() + static_cast<size_t>(r) * nl_words_;
+    std::vector<std::pair<const uint32_t*, int32_t>> rows;  // (words, step)
+    for (const RasterChunk& ch : raster_)
+        for (int r = 0; r < ch.rows; ++r)
+            rows.emplace_back(ch.words.data() + static_cast<size_t>(r) * nl_words_, ch.t0 + r);
+    std::vector<int64_t> start(rows.size() + 1, 0);
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const size_t nthreads = std::max<size_t>(1, std::min<size_t>(hw, rows.size() / 8 + 1));
+    auto parallel = [&](auto&& fn) {
+        std::vector<std::thread> pool;
+        const size_t per = (rows.size() + nthreads - 1) / nthreads;
+        for (size_t t = 0; t < nthreads; ++t) {
+            const size_t a = t * per, b = std::min(rows.size(), a + per);
+            if (a >= b) break;
+            pool.emplace_back([&fn, a, b] { fn(a, b); });
+        }
+        for (auto& th : pool) th.join();
+    };
+    parallel([&](size_t a, size_t b) {
+        for (size_t r = a; r < b; ++r) {
+            int64_t c = 0;
+            for (int w = 0; w < nl_words_; ++w) c += __builtin_popcount(rows[r].first[w]);
+            start[r + 1] = c;
+        }
+    });
+    for (size_t r = 0; r < rows.size(); ++r) start[r + 1] += start[r];
+    ev_steps_.resize(static_cast<size_t>(start.back()));
+    ev_neurons_.resize(static_cast<size_t>(start.back()));
+    parallel([&](size_t a, size_t b) {
+        for (size_t r = a; r < b; ++r) {
+            int64_t o = start[r];
+            const uint32_t* row = rows[r].first;
             for (int w = 0; w < nl_words_; ++w) {
                 uint32_t x = row[w];
                 while (x) {
-                    const int b = __builtin_ctz(x);
+                    const int bit = __builtin_ctz(x);
                     x &= x - 1;
-                    events_.emplace_back(ch.t0 + r, first_ + w * 32 + b);
+                    ev_steps_[o] = rows[r].second;
+                    ev_neurons_[o] = first_ + w * 32 + bit;
+                    ++o;
                 }
             }
         }
-    }
+    });
     events_valid_ = true;
 }
 
 int64_t Engine::raster_size() {
     require_setup("sn_raster_size");
     decode_raster();
-    return static_cast<int64_t>(events_.size());
+    return static_cast<int64_t>(ev_steps_.size());
 }
 
 void Engine::get_raster(int32_t* steps, int32_t* neurons, int64_t cap) {
     require_setup("sn_get_raster");
     decode_raster();
-    if (cap < static_cast<int64_t>(events_.size()))
-        throw InvalidArgument("sn_get_raster: capacity " + std::to_string(cap) + " < " + std::to_string(events_.size()) + " events");
-    for (size_t i = 0; i < events_.size(); ++i) {
-        steps[i] = events_[i].first;
-        neurons[i] = events_[i].second;
+    const int64_t ne = static_cast<int64_t>(ev_steps_.size());
+    if (cap < ne)
+        throw InvalidArgument("sn_get_raster: capacity " + std::to_string(cap) + " < " + std::to_string(ne) + " events");
+    if (ne) {
+        std::memcpy(steps, ev_steps_.data(), static_cast<size_t>(ne) * 4);
+        std::memcpy(neurons, ev_neurons_.data(), static_cast<size_t>(ne) * 4);
     }
 }
 
 void Engine::clear_raster() {
     raster_.clear();
-    events_.clear();
+    ev_steps_.clear();
+    ev_neurons_.clear();
     events_valid_ = true;
 }
 
@@ -1242,6 +1276,19 @@ void Engine::get_stats(sn_stats* out) {
             stats_.sweep_bytes_total = sweep_bytes_full_ * static_cast<double>(t_);
         }
         stats_.sweep_bytes_per_launch_last = sweep_bytes_full_;
+        if (dense_) {
+            stats_.sweep_kernel = persistent_ ? SN_SWEEP_PERSISTENT
+                                  : exact_    ? SN_SWEEP_DENSE_EXACT
+                                  : tma_      ? SN_SWEEP_DENSE_TMA
+                                              : SN_SWEEP_DENSE_STREAM;
+            stats_.sweep_ctas = persistent_ ? persist_grid_ : dense_grid_;
+        } else {
+            stats_.sweep_kernel = exact_ ? SN_SWEEP_SPARSE_EXACT
+                                  : sub_ == 0 ? SN_SWEEP_SPARSE_STREAM
+                                  : !dict_.empty() ? SN_SWEEP_SPARSE_DICT
+                                                   : SN_SWEEP_SPARSE_PULL;
+            stats_.sweep_ctas = sparse_gx_ * nblocks_;
+        }
     }
     *out = stats_;
 }

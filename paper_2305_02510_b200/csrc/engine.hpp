@@ -187,7 +187,7 @@ private:
     // ---- host results ----
     HostBuf h_stage_, h_raster_;
     std::vector<RasterChunk> raster_;
-    std::vector<std::pair<int32_t, int32_t>> events_;
+    std::vector<int32_t> ev_steps_, ev_neurons_;
     bool events_valid_ = true;
     std::vector<double> trace_;
     int64_t trace_rows_ = 0;

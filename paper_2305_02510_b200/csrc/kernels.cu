@@ -136,8 +136,15 @@ __device__ __forceinline__ void neuron_step(const NeuronArgs& a, const HistArgs&
         if (EXACT) {
             u = a.u_exact[j];  // leak(v) + sum in ascending pre order, from the sweep
         } else {
-            double in = 0.0;
-            for (int c = 0; c < a.nchunks; ++c) in += __ldcg(a.partial + static_cast<int64_t>(c) * a.nl + j);
+            // chunk partials: 8 independent loads in flight, fixed-order combine
+            double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            int c = 0;
+            for (; c + 8 <= a.nchunks; c += 8) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc[k] += __ldcg(a.partial + static_cast<int64_t>(c + k) * a.nl + j);
+            }
+            for (int k = 0; c < a.nchunks; ++c, ++k) acc[k] += __ldcg(a.partial + static_cast<int64_t>(c) * a.nl + j);
+            const double in = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
             u = leak_toward(v, a.leak[j], reset) + in;
         }
         // external stimulus: the step's entries pre-summed in list order
