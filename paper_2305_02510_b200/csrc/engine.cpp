@@ -635,8 +635,15 @@ void Engine::plan_launches() {
         tile_w_ = static_cast<int32_t>(round_up((nl_ + ntiles - 1) / ntiles, vec));
         tile_w_ = std::min<int32_t>(std::max(tile_w_, vec), dense_threads() * vec);
         ntiles = (nl_ + tile_w_ - 1) / tile_w_;
+        const bool tiny = static_cast<double>(n_) * pitch_ * esz <= 256.0 * 1024 &&
+                          nl_ <= dense_threads() * vec;
+        if (tiny) {  // one CTA: a single item avoids serial per-item round trips
+            rows_per_chunk_ = static_cast<int32_t>(round_up(n_, 32));
+            nchunks_ = 1;
+            tile_w_ = static_cast<int32_t>(round_up(nl_, vec));
+            ntiles = 1;
+        }
         const int items = ntiles * nchunks_;
-        const bool tiny = static_cast<double>(n_) * pitch_ * esz <= 256.0 * 1024;
         persist_grid_ = tiny ? 1 : std::max(1, std::min(items, resident));
         dense_grid_ = std::min(items, sms * 8);
         d_partial_.alloc(static_cast<size_t>(nchunks_) * std::max(nl_, 1) * 8);
