@@ -446,7 +446,8 @@ void Engine::build_sparse_from_lists() {
         std::memcpy(&key, &dict_[k], 8);
         dict_idx.emplace(key, static_cast<int>(k));
     }
-    const uint32_t pad_meta = dict ? (static_cast<uint32_t>(dict_.size() - 1) << 23) : 0u;
+    // dictionary padding: value 0.0 and the inert pre slot pb (zero history)
+    const uint32_t pad_meta = dict ? ((static_cast<uint32_t>(dict_.size() - 1) << 23) | static_cast<uint32_t>(pb_)) : 0u;
     std::vector<uint32_t> meta(static_cast<size_t>(sparse_elems_), pad_meta);
     std::vector<float> wf;
     std::vector<double> wd;

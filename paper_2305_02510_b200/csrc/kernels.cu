@@ -917,6 +917,29 @@ template <int HB> struct HistT { using T = uint64_t; };
 template <> struct HistT<16> { using T = uint16_t; };
 template <> struct HistT<32> { using T = uint32_t; };
 
+// Shared-memory image of a pre block's spike history: pcount entries from
+// global memory, then zeros up to and including slot pb (the inert padding
+// pre of dictionary-encoded lists).  Returns the 16-aligned byte size.
+template <int HB>
+__device__ __forceinline__ size_t stage_history(const SparseArgs& a, int pre0, int pcount, uint8_t* smem) {
+    using HT = typename HistT<HB>::T;
+    const int tid = threadIdx.x;
+    if (HB == 1) {
+        uint32_t* sb = reinterpret_cast<uint32_t*>(smem);
+        const int nw = (pcount + 31) >> 5;
+        const int nw_all = a.pb / 32 + 1;
+        for (int k = tid; k < nw_all; k += blockDim.x) sb[k] = k < nw ? __ldcg(a.bits + (pre0 >> 5) + k) : 0u;
+        return (static_cast<size_t>(nw_all) * 4 + 15) & ~static_cast<size_t>(15);
+    }
+    HT* sh = reinterpret_cast<HT*>(smem);
+    for (int k = tid; k <= a.pb; k += blockDim.x) {
+        HT v = 0;
+        if (k < pcount) v = static_cast<HT>(HB == 64 ? __ldcg(a.hist + pre0 + k) : __ldcg(a.hist_lo + pre0 + k));
+        sh[k] = v;
+    }
+    return (static_cast<size_t>(a.pb + 1) * sizeof(HT) + 15) & ~static_cast<size_t>(15);
+}
+
 template <typename WT, bool STDP, int HB, int SUB, bool DICT>
 __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -925,26 +948,16 @@ __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
     const int pre0 = b * a.pb;
     const int pcount = min(a.pb, a.n - pre0);
     const int tid = threadIdx.x;
-    // stage history of this pre block
-    if (HB == 1) {
-        uint32_t* sb = reinterpret_cast<uint32_t*>(smem_raw);
-        const int nw = (pcount + 31) >> 5;
-        for (int k = tid; k < nw; k += kThreads) sb[k] = __ldg(a.bits + (pre0 >> 5) + k);
-    } else {
-        HT* sh = reinterpret_cast<HT*>(smem_raw);
-        for (int k = tid; k < pcount; k += kThreads) {
-            if (HB == 64) sh[k] = static_cast<HT>(__ldg(a.hist + pre0 + k));
-            else sh[k] = static_cast<HT>(__ldg(a.hist_lo + pre0 + k));
-        }
-    }
-    // weight dictionary (non-plastic nets with <= 512 distinct weights): the
+    const size_t hbytes = stage_history<HB>(a, pre0, pcount, smem_raw);
+    // weight dictionary (non-plastic nets with <= 511 distinct weights): the
     // meta word carries the index, so the weight stream disappears (4 B/synapse)
-    WT* s_wd = reinterpret_cast<WT*>(smem_raw + (((HB == 1 ? ((a.pb + 31) / 32) * 4 : a.pb * (HB / 8)) + 15) & ~15));
+    WT* s_wd = reinterpret_cast<WT*>(smem_raw + hbytes);
     if (DICT)
         for (int k = tid; k < a.dict_size; k += kThreads) s_wd[k] = static_cast<const WT*>(a.wdict)[k];
     __syncthreads();
     const uint32_t* sbits = reinterpret_cast<const uint32_t*>(smem_raw);
     const HT* shist = reinterpret_cast<const HT*>(smem_raw);
+    const bool uniform = DICT && a.dict_size == 2;  // {w, 0.0 padding}: every synapse carries w
 
     const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
     const WT* pot = static_cast<const WT*>(a.pot);
@@ -977,6 +990,7 @@ __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
             nend = __ldg(offb + pn + 1);
         }
         WT sum = WT(0);
+        int cnt = 0;
         if (valid) {
             const int gp = a.first + p;
             bool sp = false;
@@ -1009,6 +1023,18 @@ __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
                 for (int u = 0; u < UL; ++u) {
                     const int64_t q = q0 + static_cast<int64_t>(u) * SUB * 4;
                     if (q >= end) continue;
+                    if (DICT && uniform) {
+                        // one weight for every synapse: count the delivering pres
+                        // (padding points at the zero-history slot pb)
+                        const uint32_t ms[4] = {m4[u].x, m4[u].y, m4[u].z, m4[u].w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const int pl = static_cast<int>(ms[k] & 0xffffu);
+                            if (HB == 1) cnt += static_cast<int>((sbits[pl >> 5] >> (pl & 31)) & 1u);
+                            else cnt += static_cast<int>((shist[pl] >> ((ms[k] >> 16) & 63u)) & 1u);
+                        }
+                        continue;
+                    }
                     if (DICT) {
                         wv[u][0] = s_wd[m4[u].x >> 23]; wv[u][1] = s_wd[m4[u].y >> 23];
                         wv[u][2] = s_wd[m4[u].z >> 23]; wv[u][3] = s_wd[m4[u].w >> 23];
@@ -1048,8 +1074,14 @@ __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
                 }
             }
         }
+        if (DICT && uniform) {
 #pragma unroll
-        for (int o = SUB / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            for (int o = SUB / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            sum = static_cast<WT>(cnt) * s_wd[0];
+        } else {
+#pragma unroll
+            for (int o = SUB / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        }
         if (valid && sl == 0) a.partial[static_cast<int64_t>(b) * a.nl + p] = static_cast<double>(sum);
         p = pn;
         beg = nbeg;
@@ -1075,18 +1107,8 @@ __global__ void __launch_bounds__(kThreads) k_sparse_stream(SparseArgs a) {
     const int pcount = min(a.pb, a.n - pre0);
     const int tid = threadIdx.x;
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *a.d_step += 1;  // nobody reads it here
-    if (HB == 1) {
-        uint32_t* sb = reinterpret_cast<uint32_t*>(smem_raw);
-        const int nw = (pcount + 31) >> 5;
-        for (int k = tid; k < nw; k += kThreads) sb[k] = __ldcg(a.bits + (pre0 >> 5) + k);
-    } else {
-        HT* sh = reinterpret_cast<HT*>(smem_raw);
-        for (int k = tid; k < pcount; k += kThreads) {
-            if (HB == 64) sh[k] = static_cast<HT>(__ldcg(a.hist + pre0 + k));
-            else sh[k] = static_cast<HT>(__ldcg(a.hist_lo + pre0 + k));
-        }
-    }
-    WT* s_wd = reinterpret_cast<WT*>(smem_raw + (((HB == 1 ? ((a.pb + 31) / 32) * 4 : a.pb * (HB / 8)) + 15) & ~15));
+    const size_t hbytes = stage_history<HB>(a, pre0, pcount, smem_raw);
+    WT* s_wd = reinterpret_cast<WT*>(smem_raw + hbytes);
     if (DICT)
         for (int k = tid; k < a.dict_size; k += kThreads) s_wd[k] = static_cast<const WT*>(a.wdict)[k];
     __syncthreads();
@@ -1335,7 +1357,8 @@ __global__ void k_er_sparse_fill(ErArgs e, int first, int nl, int pb, int nblock
         ++q;
     }
     for (; q < end; ++q) {  // padding: never delivers, never plastic
-        meta[q] = w ? 0u : (1u << 23);      // dictionary entry 1 = 0.0
+        // dictionary mode: entry 1 (= 0.0) and pre slot pb, whose staged history is zero
+        meta[q] = w ? 0u : ((1u << 23) | static_cast<uint32_t>(pb));
         if (w) w[q] = WT(0);
     }
 }
@@ -1375,7 +1398,7 @@ int dense_threads() { return kThreads; }
 int sparse_block_pres(int hbits) {
     // 32 KB of staged history per CTA (pre ids are 16-bit block-local)
     switch (hbits) {
-        case 1: return 65536;
+        case 1: return 32768;   // pre_local == pb is the inert padding slot (16-bit field)
         case 16: return 16384;
         case 32: return 8192;
         default: return 4096;
@@ -1534,26 +1557,19 @@ static void sparse_go_sub(const SparseArgs& a, int sub, int gx, size_t smem, cud
     }
 }
 
+static size_t hist_smem_bytes(int pb, int hbits) {
+    if (hbits == 1) return (static_cast<size_t>(pb / 32 + 1) * 4 + 15) & ~static_cast<size_t>(15);
+    return (static_cast<size_t>(pb + 1) * (hbits / 8) + 15) & ~static_cast<size_t>(15);
+}
+
 template <typename WT, bool STDP>
 static void sparse_go(const SparseArgs& a, int hbits, int sub, int gx, cudaStream_t s) {
-    size_t smem;
+    const size_t smem = hist_smem_bytes(a.pb, hbits);
     switch (hbits) {
-        case 1:
-            smem = static_cast<size_t>((a.pb + 31) / 32) * 4;
-            sparse_go_sub<WT, STDP, 1>(a, sub, gx, smem, s);
-            break;
-        case 16:
-            smem = static_cast<size_t>(a.pb) * 2;
-            sparse_go_sub<WT, STDP, 16>(a, sub, gx, smem, s);
-            break;
-        case 32:
-            smem = static_cast<size_t>(a.pb) * 4;
-            sparse_go_sub<WT, STDP, 32>(a, sub, gx, smem, s);
-            break;
-        default:
-            smem = static_cast<size_t>(a.pb) * 8;
-            sparse_go_sub<WT, STDP, 64>(a, sub, gx, smem, s);
-            break;
+        case 1: sparse_go_sub<WT, STDP, 1>(a, sub, gx, smem, s); break;
+        case 16: sparse_go_sub<WT, STDP, 16>(a, sub, gx, smem, s); break;
+        case 32: sparse_go_sub<WT, STDP, 32>(a, sub, gx, smem, s); break;
+        default: sparse_go_sub<WT, STDP, 64>(a, sub, gx, smem, s); break;
     }
 }
 
