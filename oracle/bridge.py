@@ -266,6 +266,57 @@ def ref_erdos_renyi(n, p, seed):
     return pre[:m].copy(), post[:m].copy()
 
 
+def ref_has_io() -> bool:
+    return ref_available() and hasattr(ref_lib(), "ref_write_raster")
+
+
+def _ref_str(fn, *args) -> str:
+    lib = ref_lib()
+    f = getattr(lib, fn)
+    f.restype = C.c_void_p
+    ptr = f(*args)
+    try:
+        return C.string_at(ptr).decode()
+    finally:
+        lib.ref_free_str.argtypes = [C.c_void_p]
+        lib.ref_free_str(ptr)
+
+
+def ref_serialize_network(arrays) -> str:
+    p, keep = make_problem(arrays, 1)
+    ref_lib().ref_serialize_network.argtypes = [C.POINTER(Problem)]
+    return _ref_str("ref_serialize_network", C.byref(p))
+
+
+def ref_write_raster(steps, neurons) -> str:
+    s = np.ascontiguousarray(steps, np.int32)
+    n = np.ascontiguousarray(neurons, np.int32)
+    ref_lib().ref_write_raster.argtypes = [C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int64]
+    return _ref_str("ref_write_raster", s.ctypes.data_as(C.POINTER(C.c_int32)),
+                    n.ctypes.data_as(C.POINTER(C.c_int32)), len(s))
+
+
+def ref_write_stimulus(stim) -> str:
+    arrays = {"threshold": np.ones(1), "leak": np.zeros(1), "reset": np.zeros(1),
+              "refractory": np.zeros(1, np.int32), "pre": [], "post": [], "weight": []}
+    p, keep = make_problem(arrays, 1, stim)
+    ref_lib().ref_write_stimulus.argtypes = [C.POINTER(Problem)]
+    return _ref_str("ref_write_stimulus", C.byref(p))
+
+
+def ref_serialize_stdp(stdp) -> str:
+    arrays = {"threshold": np.ones(1), "leak": np.zeros(1), "reset": np.zeros(1),
+              "refractory": np.zeros(1, np.int32), "pre": [], "post": [], "weight": []}
+    p, keep = make_problem(arrays, 1, None, stdp)
+    ref_lib().ref_serialize_stdp.argtypes = [C.POINTER(Problem)]
+    return _ref_str("ref_serialize_stdp", C.byref(p))
+
+
+def ref_roundtrip_network(text: str) -> str:
+    ref_lib().ref_roundtrip_network.argtypes = [C.c_char_p]
+    return _ref_str("ref_roundtrip_network", text.encode())
+
+
 def ref_bench_scenario(n, p, seed, steps, stdp_on, storage=0) -> dict:
     """Reference CPU path timed like bench.cpp:24-50 (mat_init outside the clock)."""
     lib = ref_lib()

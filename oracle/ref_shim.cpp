@@ -371,3 +371,43 @@ int ref_bench_scenario(int n, double p, uint64_t seed, int steps, int stdp_on, i
 }
 
 }  // extern "C"
+
+// ---- wire formats (proj/src/io.cpp), for byte-identity tests of the Python io mirror ----
+#ifdef SPIKEFORGE_WITH_IO
+#include "spikeforge/io.hpp"
+
+namespace {
+char* dup_str(const std::string& s) {
+    char* out = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return out;
+}
+}  // namespace
+
+extern "C" {
+
+void ref_free_str(char* s) { std::free(s); }
+
+char* ref_serialize_network(const orc_problem* p) { return dup_str(serialize_network(to_net(p))); }
+
+char* ref_write_raster(const int32_t* steps, const int32_t* neurons, int64_t n) {
+    SpikeRaster r;
+    for (int64_t i = 0; i < n; ++i) r.events.push_back({steps[i], neurons[i]});
+    return dup_str(write_raster(r));
+}
+
+char* ref_write_stimulus(const orc_problem* p) { return dup_str(write_stimulus(to_stim(p))); }
+
+char* ref_serialize_stdp(const orc_problem* p) { return dup_str(serialize_stdp(*to_cfg(p).stdp)); }
+
+// parse_network -> serialize_network round trip of a text (empty string on FormatError)
+char* ref_roundtrip_network(const char* text) {
+    try {
+        return dup_str(serialize_network(parse_network(text)));
+    } catch (const std::exception& e) {
+        return dup_str(std::string("ERROR ") + e.what());
+    }
+}
+
+}  // extern "C"
+#endif

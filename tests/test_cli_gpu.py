@@ -1,0 +1,66 @@
+"""CLI front end: `gen` → `run --backend gpu` writes a raster
+CSV byte-identical to the reference's write_raster of its own mat/oracle run,
+and `compare` reports identical / the first divergence with the reference's
+exit codes (spikeforge_main.cpp:26-27)."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from oracle import bridge as B
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def cli(*args):
+    return subprocess.run([sys.executable, "-m", "paper_2305_02510_b200", *args], cwd=ROOT,
+                          capture_output=True, text=True, timeout=300)
+
+
+def test_gen_run_compare(tmp_path):
+    from paper_2305_02510_b200 import io as fio
+    net_p, stim_p, out_p = (str(tmp_path / f) for f in ("net.json", "stim.csv", "raster.csv"))
+    r = cli("gen", "--neurons", "60", "--prob", "0.3", "--seed", "4", "--steps", "300",
+            "--out", net_p, "--stimulus-out", stim_p)
+    assert r.returncode == 0, r.stderr
+    for backend in ("gpu", "gpu-sparse", "gpu-exact"):
+        r = cli("run", "--network", net_p, "--stimulus", stim_p, "--steps", "300", "--backend", backend,
+                "--out", out_p)
+        assert r.returncode == 0, r.stderr
+        assert "spikes=" in r.stdout
+        mine = open(out_p).read()
+        net = fio.parse_network(open(net_p).read())
+        stim = fio.parse_stimulus(open(stim_p).read())
+        o = B.run_oracle(net.to_arrays(), 300, stim.to_arrays())
+        assert len(o["steps"]) > 0
+        expect = fio.write_raster(fio.SpikeRaster(steps_array=o["steps"], neurons_array=o["neurons"]))
+        assert mine == expect
+        if B.ref_has_io():
+            assert mine == B.ref_write_raster(o["steps"], o["neurons"])
+    r = cli("compare", "--network", net_p, "--stimulus", stim_p, "--steps", "300",
+            "--backends", "gpu,gpu-sparse,gpu-exact", "--against", out_p)
+    assert r.returncode == 0 and r.stdout.strip() == "identical", r.stdout + r.stderr
+    # a raster with one spike removed diverges: exit code 1
+    lines = open(out_p).read().splitlines()
+    bad = str(tmp_path / "bad.csv")
+    open(bad, "w").write("\n".join(lines[:5] + lines[6:]) + "\n")
+    r = cli("compare", "--network", net_p, "--stimulus", stim_p, "--steps", "300", "--backends", "gpu",
+            "--against", bad)
+    assert r.returncode == 1 and r.stdout.startswith("divergence: step")
+    # errors: exit code 2 with the reference's "error: " prefix
+    r = cli("run", "--network", str(tmp_path / "missing.json"))
+    assert r.returncode == 2 and r.stderr.startswith("error: ")
+
+
+def test_bench_rows(tmp_path):
+    from paper_2305_02510_b200 import io as fio
+    out = str(tmp_path / "bench.csv")
+    r = cli("bench", "--sizes", "100,1000", "--probs", "0.25,1.0", "--steps", "200", "--out", out)
+    assert r.returncode == 0, r.stderr
+    rows = fio.parse_bench(open(out).read())
+    assert len(rows) == 4 and all(row.spike_count > 0 and row.steps == 200 for row in rows)
