@@ -176,6 +176,37 @@ def test_cfg2_delays_match_reference(storage):
     assert _digest(s, n) == e["digest"]
 
 
+@pytest.mark.parametrize("storage", [2, 1])
+def test_cfg4_shape_at_reduced_scale(storage):
+    """cfg4's shape (1% ER, delays 1..16 keyed by pair index, unit weights) at
+    N = 12,000 for 40 steps: on-device generation + sweep vs the oracle run on
+    the same network generated on the host."""
+    from paper_2305_02510_b200.engine import MatEngine
+    from paper_2305_02510_b200.netgen import (DELAY_STREAM, RandomStream, erdos_renyi_arrays,
+                                              scenario_stimulus)
+    from oracle import bridge as B
+    n, p, seed, steps, dmax = 12000, 0.01, 3, 40, 16
+    pre, post = erdos_renyi_arrays(n, p, seed)
+    keys = pre.astype(np.uint64) * np.uint64(n) + post.astype(np.uint64)
+    delay = (1 + RandomStream(seed, DELAY_STREAM).below_np(keys, dmax)).astype(np.int32)
+    arrays = {"threshold": np.ones(n), "leak": np.zeros(n), "reset": np.zeros(n),
+              "refractory": np.zeros(n, np.int32), "axonal": np.zeros(n, np.int32), "pre": pre,
+              "post": post, "weight": np.ones(len(pre)), "delay": delay, "stdp": np.zeros(len(pre), np.uint8)}
+    stim = scenario_stimulus(n, steps, seed, count=40, period=3, amplitude=2.0).to_arrays()
+    o = B.run_oracle(arrays, steps, stim)
+    assert len(o["steps"]) > 1000
+    eng = MatEngine(storage=storage)
+    eng.generate_erdos_renyi(n, p, seed, delay_max=dmax)
+    eng.setup()
+    eng.add_stimulus(*stim)
+    eng.simulate(steps)
+    s, q = eng.raster()
+    st = eng.stats()
+    eng.close()
+    assert st["synapses_local"] == len(pre) or storage == 1
+    assert np.array_equal(s, o["steps"]) and np.array_equal(q, o["neurons"])
+
+
 @pytest.mark.parametrize("precision", ["f32", "f64"])
 def test_dense_stdp_n1024_matches_reference(precision):
     e = _scale()["stdp_n1024_seed0"]
