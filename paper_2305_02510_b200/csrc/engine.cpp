@@ -700,6 +700,10 @@ void Engine::plan_launches() {
     } else {
         const double avg = nl_ > 0 ? static_cast<double>(sparse_elems_) / (static_cast<double>(nblocks_) * nl_) : 0.0;
         sub_ = avg >= 256 ? 32 : avg >= 96 ? 16 : avg >= 40 ? 8 : 4;
+        if (const char* sv = std::getenv("SNB_SPARSE_SUB")) {  // A/B knob: lanes per post
+            const int v = std::atoi(sv);
+            if (v == 4 || v == 8 || v == 16 || v == 32) sub_ = v;
+        }
         // default: SUB lanes per post (k_sparse_pull, 1.058 ms on cfg4); the flat
         // per-warp chunk stream (k_sparse_stream, 1.115 ms) stays selectable for
         // A/B runs with SNB_SPARSE_KERNEL=stream (tools/ab_sparse.sh)

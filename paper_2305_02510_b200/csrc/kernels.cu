@@ -972,7 +972,8 @@ __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
     // Software pipeline: the next post's list bounds are loaded while the
     // current post streams, and each post's chunks are fetched UL at a time
     // (all loads issued before any use) -- one memory round trip per post.
-    constexpr int UL = DICT ? 4 : 2;
+    // chunk loads per lane per batch: cover a typical list in one round trip
+    constexpr int UL = DICT ? (SUB <= 8 ? 8 : 4) : 2;
     const int stride = (kThreads / 32) * PER_WARP;
     const int64_t* offb = a.off + static_cast<int64_t>(b) * a.nl;
     int p = p0 + warp * PER_WARP + sg;
