@@ -700,9 +700,12 @@ void Engine::plan_launches() {
     } else {
         const double avg = nl_ > 0 ? static_cast<double>(sparse_elems_) / (static_cast<double>(nblocks_) * nl_) : 0.0;
         sub_ = avg >= 256 ? 32 : avg >= 96 ? 16 : avg >= 40 ? 8 : 4;
+        // dictionary lists are half as long in bytes; more posts per warp hide
+        // more latency (cfg4, 160 entries/list: SUB 16 0.720 ms, 8 0.682, 4 0.652)
+        if (!dict_.empty()) sub_ = avg >= 1024 ? 16 : avg >= 384 ? 8 : 4;
         if (const char* sv = std::getenv("SNB_SPARSE_SUB")) {  // A/B knob: lanes per post
             const int v = std::atoi(sv);
-            if (v == 4 || v == 8 || v == 16 || v == 32) sub_ = v;
+            if (v == 4 || v == 8 || v == 16 || v == 32 || (!dict_.empty() && (v == 1 || v == 2))) sub_ = v;
         }
         // default: SUB lanes per post (k_sparse_pull, 1.058 ms on cfg4); the flat
         // per-warp chunk stream (k_sparse_stream, 1.115 ms) stays selectable for

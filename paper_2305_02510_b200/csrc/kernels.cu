@@ -1542,6 +1542,8 @@ static void sparse_go_sub(const SparseArgs& a, int sub, int gx, size_t smem, cud
     if (a.dict_size > 0 && !STDP) {
         switch (sub) {
             case 0: k_sparse_stream<WT, false, HB, true><<<grid, kThreads, smem, s>>>(a); break;
+            case 1: k_sparse_pull<WT, false, HB, 1, true><<<grid, kThreads, smem, s>>>(a); break;
+            case 2: k_sparse_pull<WT, false, HB, 2, true><<<grid, kThreads, smem, s>>>(a); break;
             case 4: k_sparse_pull<WT, false, HB, 4, true><<<grid, kThreads, smem, s>>>(a); break;
             case 8: k_sparse_pull<WT, false, HB, 8, true><<<grid, kThreads, smem, s>>>(a); break;
             case 16: k_sparse_pull<WT, false, HB, 16, true><<<grid, kThreads, smem, s>>>(a); break;
