@@ -230,6 +230,20 @@ SN_API sn_status sn_put_spike_words(sn_engine* e, int32_t first_word, const uint
                              int64_t count);
 SN_API sn_status sn_step_finish(sn_engine* e);
 
+/* Peer-to-peer exchange fused into the neuron kernel (alternative to NCCL):
+ * every rank exports 128 bytes of CUDA IPC handles (its spike bitmask and its
+ * per-rank flag array), the host all-gathers them (rank-major), each rank
+ * opens its peers'; from then on the neuron kernel stores its spike words
+ * directly into every peer's bitmask over NVLink and releases a step flag,
+ * and the history kernel acquires all flags before reading.  One process per
+ * GPU, all GPUs peer-capable (NVSwitch). */
+SN_API int32_t sn_p2p_handle_size(void);
+SN_API sn_status sn_p2p_get_handles(sn_engine* e, uint8_t* out, int64_t capacity);
+SN_API sn_status sn_p2p_open(sn_engine* e, const uint8_t* all_handles, int32_t world);
+/* Same protocol for `world` engines of ONE process on ONE device (partition
+ * emulation; drive them with sn_step_local on all, then sn_step_finish). */
+SN_API sn_status sn_p2p_connect_local(sn_engine* const* engines, int32_t world);
+
 #ifdef __cplusplus
 }
 #endif

@@ -124,6 +124,10 @@ SIGNATURES = {
     "sn_get_spike_words": (_i32, [_P, _pu32, _i64]),
     "sn_put_spike_words": (_i32, [_P, _i32, _pu32, _i64]),
     "sn_step_finish": (_i32, [_P]),
+    "sn_p2p_handle_size": (_i32, []),
+    "sn_p2p_get_handles": (_i32, [_P, _pu8, _i64]),
+    "sn_p2p_open": (_i32, [_P, _pu8, _i32]),
+    "sn_p2p_connect_local": (_i32, [C.POINTER(_P), _i32]),
 }
 
 

@@ -302,6 +302,36 @@ sn_status sn_put_spike_words(sn_engine* e, int32_t first_word, const uint32_t* w
     });
 }
 
+int32_t sn_p2p_handle_size(void) { return 2 * Engine::kIpcHandleBytes; }
+
+sn_status sn_p2p_get_handles(sn_engine* e, uint8_t* out, int64_t capacity) {
+    return guard([&] {
+        SN_NEED(e);
+        if (!out) throw InvalidArgument("sn_p2p_get_handles: null output");
+        e->impl.p2p_get_handles(out, capacity);
+    });
+}
+
+sn_status sn_p2p_open(sn_engine* e, const uint8_t* all_handles, int32_t world) {
+    return guard([&] {
+        SN_NEED(e);
+        if (!all_handles) throw InvalidArgument("sn_p2p_open: null handles");
+        e->impl.p2p_open(all_handles, world);
+    });
+}
+
+sn_status sn_p2p_connect_local(sn_engine* const* engines, int32_t world) {
+    return guard([&] {
+        if (!engines || world < 1) throw InvalidArgument("sn_p2p_connect_local: bad arguments");
+        std::vector<Engine*> impls(static_cast<size_t>(world));
+        for (int q = 0; q < world; ++q) {
+            SN_NEED(engines[q]);
+            impls[q] = &engines[q]->impl;
+        }
+        Engine::p2p_connect_local(impls.data(), world);
+    });
+}
+
 sn_status sn_step_finish(sn_engine* e) {
     return guard([&] {
         SN_NEED(e);

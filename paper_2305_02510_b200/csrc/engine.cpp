@@ -96,6 +96,7 @@ Engine::~Engine() {
     cudaSetDevice(opt_.device);
     if (stream_) cudaStreamSynchronize(stream_);
     delete comm_;
+    for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
     for (auto e : ev_pool_) cudaEventDestroy(e);
     for (auto& p : pending_) {
         (void)p;
@@ -610,6 +611,11 @@ void Engine::alloc_state() {
     }
     d_step_.alloc(8);
     d_work_.alloc(8);
+    d_flags_.alloc(static_cast<size_t>(opt_.world) * 4);
+    d_done_.alloc(8);
+    d_err_.alloc(8);
+    for (DevBuf* b : {&d_flags_, &d_done_, &d_err_})
+        cuda_check(cudaMemsetAsync(b->p, 0, b->bytes, stream_), "memset");
     cuda_check(cudaMemsetAsync(d_work_.p, 0, 8, stream_), "memset");
     d_spikes_.alloc(16);
     cuda_check(cudaMemsetAsync(d_step_.p, 0, 8, stream_), "memset");
@@ -796,6 +802,13 @@ NeuronArgs Engine::neuron_args(int t_base, int rows, uint32_t* raster, double* t
     a.raster_rows = rows;
     a.trace = trace;
     a.spike_count = d_spikes_.as<unsigned long long>();
+    if (p2p_) {
+        a.peer_bits = d_peer_bits_.as<uint32_t* const>();
+        a.peer_flags = d_peer_flags_.as<int32_t* const>();
+        a.done = d_done_.as<uint32_t>();
+        a.rank = opt_.rank;
+        a.world = opt_.world;
+    }
     return a;
 }
 
@@ -820,6 +833,11 @@ HistArgs Engine::hist_args() {
     h.d_step = d_step_.as<int32_t>();
     h.hist_lo = (!dense_ && (hbits_ == 16 || hbits_ == 32)) ? d_hist_lo_.as<uint32_t>() : nullptr;
     h.active_count = d_spikes_.as<unsigned long long>() + 1;
+    if (p2p_) {
+        h.flags = d_flags_.as<int32_t>();
+        h.world = opt_.world;
+        h.error = d_err_.as<int32_t>();
+    }
     return h;
 }
 
@@ -909,7 +927,7 @@ void Engine::enqueue_step(const NeuronArgs& na, bool exchange) {
     if (prof) { e1 = get_event(); cuda_check(cudaEventRecord(e1, stream_), "rec"); pending_.push_back({e0, e1, 0, 0.0}); }
     if (!fused && exchange) {
         if (prof) { e0 = get_event(); cuda_check(cudaEventRecord(e0, stream_), "rec"); }
-        if (comm_) comm_->all_gather_inplace(d_bits_.as<uint32_t>(), static_cast<size_t>(part_ / 32), stream_);
+        if (comm_ && !p2p_) comm_->all_gather_inplace(d_bits_.as<uint32_t>(), static_cast<size_t>(part_ / 32), stream_);
         launch_hist(h, stream_);
         stats_.kernel_launches += 1;
         if (prof) { e1 = get_event(); cuda_check(cudaEventRecord(e1, stream_), "rec"); pending_.push_back({e0, e1, 2, 0.0}); }
@@ -937,8 +955,9 @@ void Engine::flush_pending() {
 void Engine::simulate(int32_t steps) {
     require_setup("sn_simulate");
     if (steps < 1) throw InvalidArgument("mat_run: steps must be >= 1");
-    if (opt_.world > 1 && !comm_)
-        throw LogicError("sn_simulate: partitioned engine needs sn_comm_init (or use sn_step_local/sn_step_finish)");
+    if (opt_.world > 1 && !comm_ && !p2p_)
+        throw LogicError("sn_simulate: partitioned engine needs sn_comm_init or sn_p2p_open "
+                         "(or use sn_step_local/sn_step_finish)");
     cuda_check(cudaSetDevice(opt_.device), "cudaSetDevice");
     build_stimulus_table();
     const int t0 = t_;
@@ -1058,6 +1077,7 @@ void Engine::simulate(int32_t steps) {
     cudaEventDestroy(ee);
     stats_.last_simulate_ms = ms;
     flush_pending();
+    check_exchange_error();
     if (opt_.record_membrane) {
         const size_t cnt = static_cast<size_t>(steps) * nl_;
         const size_t old = trace_.size();
@@ -1117,6 +1137,7 @@ void Engine::step_finish() {
     ch.words.resize(static_cast<size_t>(nl_words_));
     if (nl_words_) cuda_check(cudaMemcpyAsync(ch.words.data(), d_raster_.p, ch.words.size() * 4, cudaMemcpyDeviceToHost, stream_), "raster D2H");
     cuda_check(cudaStreamSynchronize(stream_), "step_finish sync");
+    check_exchange_error();
     raster_.push_back(std::move(ch));
     if (opt_.record_membrane) {
         const size_t old = trace_.size();
@@ -1136,6 +1157,83 @@ void Engine::comm_init(const uint8_t* id, int32_t rank, int32_t world) {
     delete comm_;
     comm_ = nullptr;
     if (world > 1) comm_ = new NcclComm(id, rank, world);
+}
+
+// ---- peer-to-peer exchange ---------------------------------------------------
+// Each rank exports (cudaIpcGetMemHandle) its full spike bitmask and its
+// flag array; after opening every peer's pair, the neuron kernel stores its
+// spike words straight into all peers' bitmasks over NVLink and releases
+// flag[rank] = t + 1 in each of them; k_hist acquires all flags before
+// reading the bitmask.  No NCCL call remains on the step path.
+void Engine::p2p_get_handles(uint8_t* out, int64_t cap) {
+    require_setup("sn_p2p_get_handles");
+    if (cap < 2 * kIpcHandleBytes) throw InvalidArgument("sn_p2p_get_handles: buffer smaller than 128 bytes");
+    cudaIpcMemHandle_t hb, hf;
+    cuda_check(cudaIpcGetMemHandle(&hb, d_bits_.p), "cudaIpcGetMemHandle(bits)");
+    cuda_check(cudaIpcGetMemHandle(&hf, d_flags_.p), "cudaIpcGetMemHandle(flags)");
+    std::memcpy(out, &hb, kIpcHandleBytes);
+    std::memcpy(out + kIpcHandleBytes, &hf, kIpcHandleBytes);
+}
+
+void Engine::set_peer_tables(const std::vector<uint32_t*>& bits, const std::vector<int32_t*>& flags) {
+    d_peer_bits_.alloc(bits.size() * sizeof(uint32_t*));
+    d_peer_flags_.alloc(flags.size() * sizeof(int32_t*));
+    cuda_check(cudaMemcpy(d_peer_bits_.p, bits.data(), bits.size() * sizeof(uint32_t*), cudaMemcpyHostToDevice), "peer table");
+    cuda_check(cudaMemcpy(d_peer_flags_.p, flags.data(), flags.size() * sizeof(int32_t*), cudaMemcpyHostToDevice), "peer table");
+    p2p_ = true;
+}
+
+void Engine::p2p_open(const uint8_t* all, int32_t world) {
+    require_setup("sn_p2p_open");
+    if (world != opt_.world) throw InvalidArgument("sn_p2p_open: world differs from the engine options");
+    cuda_check(cudaSetDevice(opt_.device), "cudaSetDevice");
+    std::vector<uint32_t*> bits(world);
+    std::vector<int32_t*> flags(world);
+    for (int q = 0; q < world; ++q) {
+        if (q == opt_.rank) {
+            bits[q] = d_bits_.as<uint32_t>();
+            flags[q] = d_flags_.as<int32_t>();
+            continue;
+        }
+        cudaIpcMemHandle_t hb, hf;
+        std::memcpy(&hb, all + static_cast<size_t>(q) * 2 * kIpcHandleBytes, kIpcHandleBytes);
+        std::memcpy(&hf, all + static_cast<size_t>(q) * 2 * kIpcHandleBytes + kIpcHandleBytes, kIpcHandleBytes);
+        void* pb = nullptr;
+        void* pf = nullptr;
+        cuda_check(cudaIpcOpenMemHandle(&pb, hb, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(bits)");
+        ipc_opened_.push_back(pb);
+        cuda_check(cudaIpcOpenMemHandle(&pf, hf, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(flags)");
+        ipc_opened_.push_back(pf);
+        bits[q] = static_cast<uint32_t*>(pb);
+        flags[q] = static_cast<int32_t*>(pf);
+    }
+    set_peer_tables(bits, flags);
+}
+
+void Engine::p2p_connect_local(Engine* const* engines, int32_t world) {
+    std::vector<uint32_t*> bits(world);
+    std::vector<int32_t*> flags(world);
+    for (int q = 0; q < world; ++q) {
+        Engine* e = engines[q];
+        if (!e || !e->setup_done_) throw LogicError("sn_p2p_connect_local: every engine must be set up");
+        if (e->opt_.world != world || e->opt_.rank != q)
+            throw InvalidArgument("sn_p2p_connect_local: engines must be ranks 0..world-1 in order");
+        if (e->opt_.device != engines[0]->opt_.device)
+            throw InvalidArgument("sn_p2p_connect_local: engines must share one device (use sn_p2p_open across GPUs)");
+        bits[q] = e->d_bits_.as<uint32_t>();
+        flags[q] = e->d_flags_.as<int32_t>();
+    }
+    for (int q = 0; q < world; ++q) {
+        cuda_check(cudaSetDevice(engines[q]->opt_.device), "cudaSetDevice");
+        engines[q]->set_peer_tables(bits, flags);
+    }
+}
+
+void Engine::check_exchange_error() {
+    if (!p2p_) return;
+    int32_t err = 0;
+    cuda_check(cudaMemcpy(&err, d_err_.p, 4, cudaMemcpyDeviceToHost), "exchange error D2H");
+    if (err) throw NcclError("peer-to-peer spike exchange timed out (a peer rank stopped publishing)");
 }
 
 // ---- results -------------------------------------------------------------------

@@ -100,6 +100,11 @@ public:
     void reset_stats();
 
     void comm_init(const uint8_t* id, int32_t rank, int32_t world);
+    // peer-to-peer spike exchange fused into the neuron kernel (NVLink stores)
+    static constexpr int kIpcHandleBytes = 64;
+    void p2p_get_handles(uint8_t* out, int64_t cap);
+    void p2p_open(const uint8_t* all_handles, int32_t world);
+    static void p2p_connect_local(Engine* const* engines, int32_t world);
     void step_local();
     void get_spike_words(uint32_t* out, int64_t words);
     void put_spike_words(int32_t first_word, const uint32_t* w, int64_t count);
@@ -212,6 +217,11 @@ private:
     void record_begin(cudaEvent_t& e);
 
     NcclComm* comm_ = nullptr;
+    bool p2p_ = false;
+    DevBuf d_flags_, d_done_, d_err_, d_peer_bits_, d_peer_flags_;
+    std::vector<void*> ipc_opened_;  // peer allocations mapped with cudaIpcOpenMemHandle
+    void set_peer_tables(const std::vector<uint32_t*>& bits, const std::vector<int32_t*>& flags);
+    void check_exchange_error();
     bool host_exchange_ = false;
 };
 

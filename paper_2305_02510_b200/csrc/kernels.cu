@@ -186,6 +186,9 @@ __device__ __forceinline__ void neuron_step(const NeuronArgs& a, const HistArgs&
     const int wi = j >> 5;
     if (lane == 0 && wi < a.nl_words) {
         a.bits[(a.first >> 5) + wi] = word;
+        if (a.peer_bits)  // fused all-gather: store the word into every peer's bitmask (NVLink)
+            for (int q = 0; q < a.world; ++q)
+                if (q != a.rank) a.peer_bits[q][(a.first >> 5) + wi] = word;
         if (a.raster && (t - a.t_base) < a.raster_rows)
             a.raster[static_cast<int64_t>(t - a.t_base) * a.nl_words + wi] = word;
         if (word) atomicAdd(a.spike_count, static_cast<unsigned long long>(__popc(word)));
@@ -201,15 +204,60 @@ __device__ __forceinline__ void neuron_step(const NeuronArgs& a, const HistArgs&
     }
 }
 
+__device__ __forceinline__ void st_release_sys(int32_t* p, int32_t v) {
+    asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int32_t ld_acquire_sys(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 template <bool EXACT, bool FUSED>
 __global__ void __launch_bounds__(kThreads) k_neuron(NeuronArgs a, HistArgs h) {
-    neuron_step<EXACT, FUSED>(a, h, blockIdx.x * kThreads + threadIdx.x, *a.d_step);
+    const int t = *a.d_step;
+    neuron_step<EXACT, FUSED>(a, h, blockIdx.x * kThreads + threadIdx.x, t);
+    if (a.peer_bits) {
+        // publish step t to every rank once all CTAs' words are out: each CTA
+        // fences its peer stores system-wide and counts itself; the last CTA
+        // releases flag[rank] = t + 1 in every rank's flag array
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t prev = atomicAdd(a.done, 1u);
+            if (prev == gridDim.x - 1) {
+                __threadfence_system();
+                for (int q = 0; q < a.world; ++q) st_release_sys(a.peer_flags[q] + a.rank, t + 1);
+                *a.done = 0;
+            }
+        }
+    }
 }
 
 // Partitioned runs: history/traces for all N from the all-gathered bitmask.
 __global__ void __launch_bounds__(kThreads) k_hist(HistArgs h) {
     const int i = blockIdx.x * kThreads + threadIdx.x;
     const int t = *h.d_step;
+    if (h.flags) {  // peer-to-peer exchange: wait for every rank's words of step t
+        if (threadIdx.x == 0) {
+            const uint64_t t0 = globaltimer_ns();
+            for (int q = 0; q < h.world; ++q) {
+                while (ld_acquire_sys(h.flags + q) <= t) {
+                    if (globaltimer_ns() - t0 > 30ull * 1000000000ull) {  // 30 s: a peer died
+                        atomicExch(h.error, 1);
+                        break;
+                    }
+                    __nanosleep(200);
+                }
+            }
+        }
+        __syncthreads();
+    }
     bool act = false;
     if (i < h.n) {
         const bool s = (h.bits[i >> 5] >> (i & 31)) & 1u;
@@ -1407,7 +1455,8 @@ int sparse_block_pres(int hbits) {
 }
 
 void launch_neuron(const NeuronArgs& a, bool exact, bool fused, const HistArgs& h, cudaStream_t s) {
-    const int grid = (a.nl + kThreads - 1) / kThreads;
+    int grid = (a.nl + kThreads - 1) / kThreads;
+    if (a.peer_bits && grid == 0) grid = 1;  // an empty partition still publishes its step
     if (grid == 0) return;
     if (exact) {
         if (fused) k_neuron<true, true><<<grid, kThreads, 0, s>>>(a, h);

@@ -48,6 +48,13 @@ struct NeuronArgs {
     int32_t raster_rows;
     double* trace;             // [rows][nl] or null
     unsigned long long* spike_count;
+    // peer-to-peer spike exchange (fused into this kernel; null when unused):
+    // every rank's full bitmask and flag array, reachable over NVLink
+    uint32_t* const* peer_bits;   // [world] device pointers (peer or local)
+    int32_t* const* peer_flags;   // [world] -> int32[world]; flag[src] = last step src published
+    uint32_t* done;               // CTA completion counter of this launch
+    int32_t rank;
+    int32_t world;
 };
 
 struct HistArgs {
@@ -71,6 +78,10 @@ struct HistArgs {
     int32_t* d_step;
     uint32_t* hist_lo;         // [n] low 32 history bits (sparse pull staging)
     unsigned long long* active_count;  // running sum of active rows (algorithmic bytes)
+    // peer-to-peer exchange: wait until every rank published step t (flags[q] > t)
+    const int32_t* flags;              // this rank's int32[world] (written by peers) or null
+    int32_t world;
+    int32_t* error;                    // set to 1 when the wait times out
 };
 
 struct DenseArgs {

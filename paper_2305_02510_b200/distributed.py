@@ -60,6 +60,17 @@ def broadcast_uid(uid: Optional[bytes], src: int = 0, group=None) -> bytes:
     return box[0]
 
 
+def exchange_p2p_handles(mine: bytes, group=None) -> bytes:
+    """All-gather every rank's 128-byte IPC handle block, rank-major, for sn_p2p_open."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    parts = [None] * world
+    dist.all_gather_object(parts, mine, group=group)
+    if any(len(p) != len(mine) for p in parts):
+        raise RuntimeError("p2p handle blocks differ in size across ranks")
+    return b"".join(parts)
+
+
 def merge_rasters(parts: Sequence[Tuple[np.ndarray, np.ndarray]]) -> Tuple[np.ndarray, np.ndarray]:
     """Per-rank (steps, neurons) rasters -> one raster ascending by (step, neuron)."""
     if not parts:
@@ -102,6 +113,9 @@ def run_partitioned(net: NetworkDef, cfg: SimulationConfig, stim: Optional[Stimu
     if transport == "nccl":
         uid = broadcast_uid(comm_unique_id() if rank == 0 else None, group=group)
         eng.comm_init(uid, rank, world)
+        eng.simulate(cfg.steps)
+    elif transport == "p2p":
+        eng.p2p_open(exchange_p2p_handles(eng.p2p_handles(), group), world)
         eng.simulate(cfg.steps)
     elif transport == "host":
         wpr = words_per_rank(n, world)

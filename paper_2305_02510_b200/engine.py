@@ -186,6 +186,24 @@ class MatEngine:
     def step_finish(self):
         check(lib.sn_step_finish(self._h))
 
+    # ---- peer-to-peer exchange (fused into the neuron kernel) ----
+    def p2p_handles(self) -> bytes:
+        size = lib.sn_p2p_handle_size()
+        buf = (C.c_uint8 * size)()
+        check(lib.sn_p2p_get_handles(self._h, buf, size))
+        return bytes(buf)
+
+    def p2p_open(self, all_handles: bytes, world: int):
+        buf = (C.c_uint8 * len(all_handles)).from_buffer_copy(all_handles)
+        check(lib.sn_p2p_open(self._h, buf, int(world)))
+
+
+def p2p_connect_local(engines) -> None:
+    """Wire `engines` (ranks 0..G-1 of one process, one device) for the
+    peer-to-peer exchange protocol (partition emulation)."""
+    arr = (C.c_void_p * len(engines))(*[e._h.value for e in engines])
+    check(lib.sn_p2p_connect_local(arr, len(engines)))
+
 
 def comm_unique_id() -> bytes:
     size = lib.sn_comm_id_size()

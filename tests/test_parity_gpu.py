@@ -274,6 +274,47 @@ def test_partitions_emulated_on_one_gpu(world, storage):
             e.close()
 
 
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("storage", [1, 2])
+def test_p2p_exchange_emulated_on_one_gpu(world, storage):
+    """The fused peer-to-peer exchange (the neuron kernel stores its spike
+    words into every partition's bitmask and releases a step flag; the
+    history kernel acquires all flags) with G partitions on one device: all
+    step_local launches complete before any step_finish, so no kernel ever
+    waits on one that has not run.  Raster and weights equal the single engine."""
+    from paper_2305_02510_b200.engine import MatEngine, p2p_connect_local
+    g = np.load(os.path.join(GOLD, "rand_stdp.npz"))
+    for c in CS.random_stdp_cases()[:3] + CS.random_stdp_cases()[20:22]:
+        a = c.arrays()
+        engines = []
+        for r in range(world):
+            e = MatEngine(storage=storage, precision="f64", rank=r, world=world)
+            e.add_neurons(a["threshold"], a["leak"], a["reset"], a["refractory"], a["axonal"])
+            if len(a["pre"]):
+                e.add_synapses(a["pre"], a["post"], a["weight"], a["delay"], a["stdp"])
+            s = c.stdp
+            e.set_stdp(s.window, s.a_plus, s.a_minus, s.w_min, s.w_max)
+            e.setup()
+            e.add_stimulus(*c.stim_arrays())
+            engines.append(e)
+        p2p_connect_local(engines)
+        for _ in range(c.steps):
+            for e in engines:
+                e.step_local()
+            for e in engines:
+                e.step_finish()
+        steps = np.concatenate([e.raster()[0] for e in engines])
+        neurons = np.concatenate([e.raster()[1] for e in engines])
+        order = np.lexsort((neurons, steps))
+        assert np.array_equal(steps[order], g[f"{c.name}/steps"]), c.name
+        assert np.array_equal(neurons[order], g[f"{c.name}/neurons"]), c.name
+        if len(a["pre"]):
+            w = sum(e.synapse_weights() for e in engines)
+            assert np.array_equal(w, g[f"{c.name}/weights"]), c.name
+        for e in engines:
+            e.close()
+
+
 def test_mat_run_api_and_errors():
     import paper_2305_02510_b200 as sn
     from support import kick, two_neuron_chain
