@@ -123,6 +123,18 @@ def build_engine(sn, wl, device, rank, world, stream_io=False, profile=False):
     return eng
 
 
+def connect(sn, eng, rank, world, transport):
+    """Join the per-step spike exchange of a partitioned run: one in-place
+    ncclAllGather (nccl) or stores fused into the neuron kernel (p2p)."""
+    if world == 1:
+        return
+    from paper_2305_02510_b200 import distributed as D
+    if transport == "p2p":
+        eng.p2p_open(D.exchange_p2p_handles(eng.p2p_handles()), world)
+    else:
+        eng.comm_init(D.broadcast_uid(sn.comm_unique_id() if rank == 0 else None), rank, world)
+
+
 def add_protocol_stimulus(sn, eng, n, horizon):
     st = sn.netgen.scenario_stimulus(n, horizon, 0)
     arr = st.to_arrays()
@@ -146,16 +158,9 @@ def run_ours(args):
     horizon = W + K
 
     eng = build_engine(sn, wl, device, rank, world, profile=True)
-    if world > 1:
-        import torch
-        uid = [sn.comm_unique_id() if rank == 0 else None]
-        torch_dist.broadcast_object_list(uid, src=0)
-        eng.setup()
-        eng.comm_init(uid[0], rank, world)
-    else:
-        eng.setup()
+    eng.setup()
+    connect(sn, eng, rank, world, args.transport)
     stim = add_protocol_stimulus(sn, eng, n, horizon)
-    st0 = eng.stats()
     eng.simulate(W)                       # warm-up
     eng.synchronize()
     eng.reset_stats()
@@ -211,13 +216,8 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         eng2 = build_engine(sn, wl, device, rank, world, stream_io=True)
-        if world > 1:
-            uid = [sn.comm_unique_id() if rank == 0 else None]
-            torch_dist.broadcast_object_list(uid, src=0)
-            eng2.setup()
-            eng2.comm_init(uid[0], rank, world)
-        else:
-            eng2.setup()
+        eng2.setup()
+        connect(sn, eng2, rank, world, args.transport)
         add_protocol_stimulus(sn, eng2, n, horizon)
         eng2.simulate(W)
         eng2.synchronize()
@@ -254,7 +254,8 @@ def run_ours(args):
         "data": "synthetic (on-device erdos_renyi, bit-identical to netgen.cpp; paper stimulus)",
         "config": {"workload": f"{wl}: {desc}", "n": n, "p": p, "stdp": stdp, "delay_max": dmax,
                    "storage": "dense" if st["dense"] else "sparse",
-                   "parallelism": f"post-partition x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"post-partition x{world} ({args.transport} spike exchange)"
+                                   if world > 1 else "single GPU"),
                    "l2": "inputs larger than L2" if n * n * p * 4 > 126e6 else "working set L2-resident"},
         "syn_events_per_s": syn_events / (ms / 1e3),
         "spikes_timed": timed_spikes,
@@ -382,6 +383,8 @@ def main():
     ap.add_argument("--workload", choices=list(WORKLOADS), default="cfg3")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg")
+    ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
+                    help="per-step spike exchange when N > 1")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: the timing contract wants >= 3 warm-up steps", file=sys.stderr)
