@@ -872,7 +872,7 @@ DenseArgs Engine::dense_args() {
     return a;
 }
 
-void Engine::launch_sweep() {
+void Engine::launch_sweep_only() {
     if (dense_) {
         DenseArgs a = dense_args();
         if (tma_) launch_dense_tma(a, stdp_on_, dense_grid_, stream_);
@@ -907,6 +907,10 @@ void Engine::launch_sweep() {
         if (nl_ == 0) launch_step_bump(a.d_step, stream_);
         else launch_sparse(a, f64_, stdp_on_, hbits_, sub_, exact_, sparse_gx_, stream_);
     }
+}
+
+void Engine::launch_sweep() {
+    launch_sweep_only();
     stats_.kernel_launches += 1;
 }
 
@@ -935,6 +939,88 @@ void Engine::enqueue_step(const NeuronArgs& na, bool exchange) {
     if (prof) { e2 = get_event(); cuda_check(cudaEventRecord(e2, stream_), "rec"); }
     launch_sweep();
     if (prof) { e3 = get_event(); cuda_check(cudaEventRecord(e3, stream_), "rec"); pending_.push_back({e2, e3, 1, 0.0}); }
+}
+
+// The step loop as CUDA graphs of up to 64 steps (kernels read the step from
+// d_step, so one graph serves every chunk of a simulate call).  With
+// profiling, per-kernel CUDA events are captured into the graph (event record
+// nodes) and read after each replay, so the timed loop keeps graph launch
+// costs while reporting per-kernel device time.  Returns the summed device
+// time of the chunks.
+double Engine::run_graph_chunks(const NeuronArgs& na, int steps) {
+    const int chunk = std::min(steps, 64);
+    const bool prof = opt_.profile != 0;
+    const bool fused = opt_.world == 1;
+    const int per = 6;
+    std::vector<cudaEvent_t> ev(prof ? static_cast<size_t>(chunk) * per : 0);
+    for (auto& e : ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    const HistArgs h = hist_args();
+    auto capture = [&](int k) {
+        cudaGraph_t g;
+        cudaGraphExec_t ge;
+        cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
+        for (int s = 0; s < k; ++s) {
+            cudaEvent_t* e = prof ? &ev[static_cast<size_t>(s) * per] : nullptr;
+            if (e) cuda_check(cudaEventRecord(e[0], stream_), "rec");
+            launch_neuron(na, exact_, fused, h, stream_);
+            if (e) cuda_check(cudaEventRecord(e[1], stream_), "rec");
+            if (!fused) {
+                if (e) cuda_check(cudaEventRecord(e[2], stream_), "rec");
+                if (comm_ && !p2p_) comm_->all_gather_inplace(d_bits_.as<uint32_t>(), static_cast<size_t>(part_ / 32), stream_);
+                launch_hist(h, stream_);
+                if (e) cuda_check(cudaEventRecord(e[3], stream_), "rec");
+            }
+            if (e) cuda_check(cudaEventRecord(e[4], stream_), "rec");
+            launch_sweep_only();
+            if (e) cuda_check(cudaEventRecord(e[5], stream_), "rec");
+        }
+        cuda_check(cudaStreamEndCapture(stream_, &g), "end capture");
+        cuda_check(cudaGraphInstantiate(&ge, g, 0), "instantiate");
+        cudaGraphDestroy(g);
+        return ge;
+    };
+    cudaGraphExec_t full = capture(chunk);
+    cudaGraphExec_t tail = (steps % chunk) ? capture(steps % chunk) : nullptr;
+    const int per_step_kernels = fused ? 2 : 3;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spans;
+    double total = 0.0;
+    for (int done = 0; done < steps;) {
+        const int k = std::min(chunk, steps - done);
+        cudaEvent_t c0 = get_event(), c1 = get_event();
+        cuda_check(cudaEventRecord(c0, stream_), "rec");
+        cuda_check(cudaGraphLaunch(k == chunk ? full : tail, stream_), "graph launch");
+        cuda_check(cudaEventRecord(c1, stream_), "rec");
+        spans.emplace_back(c0, c1);
+        stats_.kernel_launches += static_cast<int64_t>(per_step_kernels) * k;
+        if (prof) {
+            cuda_check(cudaStreamSynchronize(stream_), "profile sync");
+            for (int s = 0; s < k; ++s) {
+                const cudaEvent_t* e = &ev[static_cast<size_t>(s) * per];
+                float a = 0.f, b = 0.f, c = 0.f;
+                cuda_check(cudaEventElapsedTime(&a, e[0], e[1]), "elapsed");
+                cuda_check(cudaEventElapsedTime(&c, e[4], e[5]), "elapsed");
+                if (!fused) cuda_check(cudaEventElapsedTime(&b, e[2], e[3]), "elapsed");
+                stats_.neuron_ms += a;
+                stats_.neuron_launches += 1;
+                stats_.exchange_ms += b;
+                stats_.sweep_ms += c;
+                stats_.sweep_launches += 1;
+            }
+        }
+        done += k;
+    }
+    cuda_check(cudaStreamSynchronize(stream_), "simulate sync");
+    for (auto& sp : spans) {
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, sp.first, sp.second), "elapsed");
+        total += ms;
+        cudaEventDestroy(sp.first);
+        cudaEventDestroy(sp.second);
+    }
+    cudaGraphExecDestroy(full);
+    if (tail) cudaGraphExecDestroy(tail);
+    for (auto& e : ev) cudaEventDestroy(e);
+    return total;
 }
 
 void Engine::flush_pending() {
@@ -967,6 +1053,7 @@ void Engine::simulate(int32_t steps) {
         trace = d_trace_.as<double>();
     }
     cudaEvent_t eb = get_event(), ee = get_event();
+    double graph_ms = -1.0;  // device time summed over graph chunks (excludes host syncs)
     if (opt_.stream_io) {
         // pack each step's stimulus rows into pinned memory; copy per step
         std::vector<size_t> pos(static_cast<size_t>(steps) + 1, 0);
@@ -1043,21 +1130,9 @@ void Engine::simulate(int32_t steps) {
                 pending_.push_back({p0, p1, 1, 0.0});
             }
             cuda_check(cudaEventRecord(ee, stream_), "rec");
-        } else if (opt_.use_graphs && !opt_.profile) {
-            cudaGraph_t g;
-            cudaGraphExec_t ge;
-            cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
-            const int64_t launches0 = stats_.kernel_launches;
-            enqueue_step(na, true);
-            const int64_t per_step = stats_.kernel_launches - launches0;
-            cuda_check(cudaStreamEndCapture(stream_, &g), "end capture");
-            cuda_check(cudaGraphInstantiate(&ge, g, 0), "instantiate");
-            for (int s = 0; s < steps; ++s) cuda_check(cudaGraphLaunch(ge, stream_), "graph launch");
-            stats_.kernel_launches += per_step * (steps - 1);
+        } else if (opt_.use_graphs) {
+            graph_ms = run_graph_chunks(na, steps);
             cuda_check(cudaEventRecord(ee, stream_), "rec");
-            cuda_check(cudaStreamSynchronize(stream_), "simulate sync");
-            cudaGraphExecDestroy(ge);
-            cudaGraphDestroy(g);
         } else {
             for (int s = 0; s < steps; ++s) enqueue_step(na, true);
             cuda_check(cudaEventRecord(ee, stream_), "rec");
@@ -1075,7 +1150,7 @@ void Engine::simulate(int32_t steps) {
     cuda_check(cudaEventElapsedTime(&ms, eb, ee), "elapsed");
     cudaEventDestroy(eb);
     cudaEventDestroy(ee);
-    stats_.last_simulate_ms = ms;
+    stats_.last_simulate_ms = graph_ms >= 0.0 ? graph_ms : ms;
     flush_pending();
     check_exchange_error();
     if (opt_.record_membrane) {

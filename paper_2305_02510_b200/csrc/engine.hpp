@@ -127,6 +127,8 @@ private:
                            int32_t st_steps, int32_t st_stream);
     HistArgs hist_args();
     void launch_sweep();
+    void launch_sweep_only();  // no launch accounting (graph capture counts in bulk)
+    double run_graph_chunks(const NeuronArgs& na, int steps);
     DenseArgs dense_args();
     void enqueue_step(const NeuronArgs& na, bool exchange);
     void flush_pending();
