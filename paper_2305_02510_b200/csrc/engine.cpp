@@ -961,18 +961,18 @@ double Engine::run_graph_chunks(const NeuronArgs& na, int steps) {
         cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
         for (int s = 0; s < k; ++s) {
             cudaEvent_t* e = prof ? &ev[static_cast<size_t>(s) * per] : nullptr;
-            if (e) cuda_check(cudaEventRecord(e[0], stream_), "rec");
+            if (e) cuda_check(cudaEventRecordWithFlags(e[0], stream_, cudaEventRecordExternal), "rec");
             launch_neuron(na, exact_, fused, h, stream_);
-            if (e) cuda_check(cudaEventRecord(e[1], stream_), "rec");
+            if (e) cuda_check(cudaEventRecordWithFlags(e[1], stream_, cudaEventRecordExternal), "rec");
             if (!fused) {
-                if (e) cuda_check(cudaEventRecord(e[2], stream_), "rec");
+                if (e) cuda_check(cudaEventRecordWithFlags(e[2], stream_, cudaEventRecordExternal), "rec");
                 if (comm_ && !p2p_) comm_->all_gather_inplace(d_bits_.as<uint32_t>(), static_cast<size_t>(part_ / 32), stream_);
                 launch_hist(h, stream_);
-                if (e) cuda_check(cudaEventRecord(e[3], stream_), "rec");
+                if (e) cuda_check(cudaEventRecordWithFlags(e[3], stream_, cudaEventRecordExternal), "rec");
             }
-            if (e) cuda_check(cudaEventRecord(e[4], stream_), "rec");
+            if (e) cuda_check(cudaEventRecordWithFlags(e[4], stream_, cudaEventRecordExternal), "rec");
             launch_sweep_only();
-            if (e) cuda_check(cudaEventRecord(e[5], stream_), "rec");
+            if (e) cuda_check(cudaEventRecordWithFlags(e[5], stream_, cudaEventRecordExternal), "rec");
         }
         cuda_check(cudaStreamEndCapture(stream_, &g), "end capture");
         cuda_check(cudaGraphInstantiate(&ge, g, 0), "instantiate");
