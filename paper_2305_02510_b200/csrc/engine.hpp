@@ -129,6 +129,8 @@ private:
     void launch_sweep();
     void launch_sweep_only();  // no launch accounting (graph capture counts in bulk)
     double run_graph_chunks(const NeuronArgs& na, int steps);
+    static constexpr int kProfStride = 8;  // graph mode: time every 8th step's kernels
+    int64_t steps_at_reset_ = 0;
     DenseArgs dense_args();
     void enqueue_step(const NeuronArgs& na, bool exchange);
     void flush_pending();
