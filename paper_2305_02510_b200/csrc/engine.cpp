@@ -42,6 +42,7 @@ void DevBuf::release() {
 void HostBuf::reserve(size_t b) {
     if (b <= bytes) return;
     release();
+    b = std::max(b, 2 * bytes);  // geometric growth: pinned allocation is slow and synchronising
     cuda_check(cudaMallocHost(&p, b), "cudaMallocHost");
     bytes = b;
 }
@@ -337,6 +338,10 @@ void Engine::setup() {
     stim_dirty_ = true;
     build_stimulus_table();
     plan_launches();
+    if (opt_.stream_io) {  // pinned staging sized up front (1024 steps of spike words)
+        h_raster_.reserve(static_cast<size_t>(1024) * std::max(nl_words_, 1) * 4);
+        h_stage_.reserve(64 * 1024);
+    }
     cuda_check(cudaStreamSynchronize(stream_), "setup sync");
     setup_done_ = true;
     stats_.synapses_local = syn_local_;
