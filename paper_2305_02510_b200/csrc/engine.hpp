@@ -196,7 +196,8 @@ private:
     // ---- host results ----
     HostBuf h_stage_, h_raster_;
     std::vector<RasterChunk> raster_;
-    std::vector<int32_t> ev_steps_, ev_neurons_;
+    std::vector<std::pair<const uint32_t*, int32_t>> dec_rows_;  // raster rows (words, step)
+    std::vector<int64_t> dec_start_;                            // first event of each row
     bool events_valid_ = true;
     std::vector<double> trace_;
     int64_t trace_rows_ = 0;
