@@ -657,6 +657,8 @@ void Engine::plan_launches() {
         }
         const int items = ntiles * nchunks_;
         persist_grid_ = tiny ? 1 : std::max(1, std::min(items, resident));
+        if (const char* pc = std::getenv("SNB_PERSIST_CTAS"))  // A/B knob
+            persist_grid_ = std::max(1, std::min(std::atoi(pc), resident));
         dense_grid_ = std::min(items, sms * 8);
         d_partial_.alloc(static_cast<size_t>(nchunks_) * std::max(nl_, 1) * 8);
         cuda_check(cudaMemsetAsync(d_partial_.p, 0, d_partial_.bytes, stream_), "memset");

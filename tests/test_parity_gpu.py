@@ -176,6 +176,29 @@ def test_cfg2_delays_match_reference(storage):
     assert _digest(s, n) == e["digest"]
 
 
+@pytest.mark.parametrize("storage", [1, 2])
+def test_long_stdp_window_multiword_history(storage):
+    """StdpConfig windows are arbitrary (model.cpp:104-117): window 70 with
+    delays up to 6 needs two 64-bit history words per neuron."""
+    from oracle import bridge as B
+    from support import random_net, random_stim
+    from paper_2305_02510_b200.model import StdpConfig
+    w = 70
+    cfg = StdpConfig(window=w, a_plus=[0.02 * 0.97 ** k for k in range(w)],
+                     a_minus=[0.025 * 0.96 ** k for k in range(w)], w_min=0.0, w_max=1.0)
+    for seed in (400, 401, 402):
+        net = random_net(seed, max_neurons=30, edge_prob=0.3, max_delay=4, max_axonal=2)
+        for s in net.synapses:
+            s.stdp_enabled = True
+        steps = 150
+        stim = random_stim(seed, net.neuron_count(), steps, 120)
+        c = CS.Case(f"long_window_{seed}", net, steps, stim, stdp=cfg)
+        o = B.run_oracle(c.arrays(), steps, c.stim_arrays(), c.stdp_tuple())
+        r = run_engine(c, storage=storage, precision="f64")
+        assert np.array_equal(r["steps"], o["steps"]) and np.array_equal(r["neurons"], o["neurons"])
+        assert np.array_equal(r["weights"], o["weights"])
+
+
 @pytest.mark.parametrize("storage", [2, 1])
 def test_cfg4_shape_at_reduced_scale(storage):
     """cfg4's shape (1% ER, delays 1..16 keyed by pair index, unit weights) at
