@@ -152,6 +152,25 @@ def test_oracle_matches_live_reference_random():
 
 
 @pytest.mark.skipif(not B.ref_available(), reason="oracle/_ref not built")
+def test_oracle_long_window_matches_reference():
+    """window 70 (> 64 history bits), delays up to 6: weights bit-exact vs the
+    reference MAT path (lower_delays + mat_run)."""
+    from support import random_net, random_stim
+    w = 70
+    sd = (w, np.array([0.02 * 0.97 ** k for k in range(w)]), np.array([0.025 * 0.96 ** k for k in range(w)]),
+          0.0, 1.0)
+    for seed in (400, 401, 402):
+        net = random_net(seed, max_neurons=30, edge_prob=0.3, max_delay=4, max_axonal=2)
+        a = net.to_arrays()
+        a["stdp"][:] = 1
+        st = random_stim(seed, net.neuron_count(), 150, 120).to_arrays()
+        r = B.run_ref_mat(a, 150, st, sd, lower=True)
+        o = B.run_oracle(a, 150, st, sd)
+        assert np.array_equal(r["steps"], o["steps"]) and np.array_equal(r["neurons"], o["neurons"])
+        assert np.array_equal(r["weights"], o["weights"])
+
+
+@pytest.mark.skipif(not B.ref_available(), reason="oracle/_ref not built")
 def test_shim_loop_equals_mat_run():
     """ref_shim's spelled-out mat_run loop == the reference's mat_run."""
     from support import random_net, random_stim
