@@ -12,6 +12,9 @@ from .netgen import (BenchScenario, RandomStream, ScenarioBundle, SequentialRng,
                      erdos_renyi, mix64)
 from .engine import MatEngine, comm_unique_id, device_count, partition_range, stdp_defaults
 from .api import NeuromorphicModel, mat_run
+from .lowering import LoweredNetwork, ProxyInfo, annotate_proxy_metadata, lower_delays, proxy_count
+from .io import (FormatError, parse_network, parse_raster, parse_stdp, parse_stimulus,
+                 serialize_network, serialize_stdp, write_raster, write_stimulus)
 
 __all__ = [
     "INFINITE_LEAK", "NetworkDef", "NeuronParams", "RunResult", "SimulationConfig", "SpikeEvent",
@@ -20,7 +23,9 @@ __all__ = [
     "validate_network", "validate_stdp", "validate_stimulus", "BenchScenario", "RandomStream",
     "ScenarioBundle", "SequentialRng", "build_scenario", "erdos_renyi", "mix64", "MatEngine",
     "comm_unique_id", "device_count", "partition_range", "stdp_defaults", "NeuromorphicModel",
-    "mat_run",
+    "mat_run", "LoweredNetwork", "ProxyInfo", "annotate_proxy_metadata", "lower_delays",
+    "proxy_count", "FormatError", "parse_network", "parse_raster", "parse_stdp", "parse_stimulus",
+    "serialize_network", "serialize_stdp", "write_raster", "write_stimulus",
 ]
 
 __version__ = "0.1.0"
