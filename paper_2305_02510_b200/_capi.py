@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsnmat.so")
+LIB_PATH = os.environ.get("SNB_LIB") or os.path.join(_HERE, "libsnmat.so")  # SNB_LIB: A/B builds
 
 SN_OK = 0
 SN_ERR_INVALID_ARGUMENT = 1

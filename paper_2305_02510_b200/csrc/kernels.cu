@@ -989,7 +989,10 @@ __device__ __forceinline__ size_t stage_history(const SparseArgs& a, int pre0, i
 }
 
 template <typename WT, bool STDP, int HB, int SUB, bool DICT>
-__global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
+#ifndef SNB_SPARSE_MINB
+#define SNB_SPARSE_MINB 4  // <= 64 regs: 4 CTAs/SM (5 spills; cfg4 0.562 ms vs 0.652 unbounded)
+#endif
+__global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(SparseArgs a) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     using HT = typename HistT<HB>::T;
     const int b = blockIdx.y;
@@ -1021,7 +1024,10 @@ __global__ void __launch_bounds__(kThreads) k_sparse_pull(SparseArgs a) {
     // current post streams, and each post's chunks are fetched UL at a time
     // (all loads issued before any use) -- one memory round trip per post.
     // chunk loads per lane per batch: cover a typical list in one round trip
-    constexpr int UL = DICT ? (SUB <= 8 ? 8 : 4) : 2;
+#ifndef SNB_SPARSE_UL
+#define SNB_SPARSE_UL 8
+#endif
+    constexpr int UL = DICT ? (SUB <= 8 ? SNB_SPARSE_UL : 4) : 2;
     const int stride = (kThreads / 32) * PER_WARP;
     const int64_t* offb = a.off + static_cast<int64_t>(b) * a.nl;
     int p = p0 + warp * PER_WARP + sg;
