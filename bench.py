@@ -236,7 +236,8 @@ def run_ours(args):
     # one sweep per step; the engine times a sample of the timed region's sweeps
     # (every 8th step's kernels carry CUDA event nodes), the persistent kernel
     # covers all K steps in one launch
-    persistent = sn._capi.Stats.KERNEL_NAMES.get(st["sweep_kernel"]) == "k_persistent_dense"
+    kname = sn._capi.Stats.KERNEL_NAMES.get(st["sweep_kernel"], "?")
+    persistent = kname in ("k_persistent_dense", "k_tiny")
     sweep_avg_ms = st["sweep_ms"] / (K if persistent else max(1, st["sweep_launches"]))
     bytes_per_sweep = st["sweep_bytes_total"] / K
     peak, peak_src = load_peaks()
@@ -294,7 +295,8 @@ def run_ours(args):
         "dtype": "fp32 weights, fp64 membrane/traces" if stdp else "fp32 weights, fp64 membrane",
         "data": "synthetic (on-device erdos_renyi, bit-identical to netgen.cpp; paper stimulus)",
         "config": {"workload": f"{wl}: {desc}", "n": n, "p": p, "stdp": stdp, "delay_max": dmax,
-                   "storage": "dense" if st["dense"] else "sparse",
+                   "storage": ("shared-memory in-lists" if kname == "k_tiny"
+                               else "dense" if st["dense"] else "sparse"),
                    "parallelism": (f"post-partition x{world} ({args.transport} spike exchange)"
                                    if world > 1 else "single GPU"),
                    "l2": "inputs larger than L2" if n * n * p * 4 > 126e6 else "working set L2-resident"},
@@ -302,7 +304,7 @@ def run_ours(args):
         "spikes_timed": timed_spikes,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": sn._capi.Stats.KERNEL_NAMES.get(st["sweep_kernel"], "?"),
+                     "kernel": kname,
                      "kernel_ctas": st["sweep_ctas"],
                      "bytes_per_launch": bytes_per_sweep, "avg_launch_ms": sweep_avg_ms,
                      "peak_source": peak_src},

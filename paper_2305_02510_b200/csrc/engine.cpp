@@ -229,6 +229,175 @@ void Engine::generate_er(int32_t n, double p, uint64_t seed, double weight, int3
     er_.weight_d = weight;
     er_.stdp = stdp ? 1 : 0;
     er_delay_max_ = delay_max;
+    if (n <= kTinyMaxNeurons) materialize_er();
+}
+
+// Small generated nets become ordinary synapse lists (host draws identical to
+// the device generator and to netgen.cpp:36-51), so every list-based path --
+// including the shared-memory step loop -- applies to them.
+void Engine::materialize_er() {
+    const int n = er_.n;
+    auto mix = [](uint64_t z) {
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        return z ^ (z >> 31);
+    };
+    auto u64_at = [&](uint64_t key, uint64_t idx) { return mix(key + idx * 0x9e3779b97f4a7c15ULL); };
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            if (i == j || !(er_.p > 0.0)) continue;
+            const uint64_t pair = static_cast<uint64_t>(i) * static_cast<uint64_t>(n) + static_cast<uint64_t>(j);
+            if (er_.p < 1.0 && static_cast<double>(u64_at(er_.edge_key, pair) >> 11) * 0x1.0p-53 >= er_.p) continue;
+            int d = 1;
+            if (er_.delay_max > 1) {
+                const uint64_t key = er_.delay_by_synapse_index
+                                         ? static_cast<uint64_t>(i) * static_cast<uint64_t>(n - 1) +
+                                               static_cast<uint64_t>(j - (j > i ? 1 : 0))
+                                         : pair;
+                const unsigned __int128 prod = static_cast<unsigned __int128>(u64_at(er_.delay_key, key)) *
+                                               static_cast<unsigned __int128>(er_.delay_max);
+                d = 1 + static_cast<int>(static_cast<uint64_t>(prod >> 64));
+            }
+            pre_.push_back(i);
+            post_.push_back(j);
+            weight_.push_back(er_.weight_d);
+            delay_.push_back(d);
+            plastic_.push_back(static_cast<uint8_t>(er_.stdp));
+        }
+    generated_ = false;
+}
+
+// In-lists for k_tiny: post-major, pre ascending.  Returns false when the
+// state and the lists would not leave room for a step's stimulus in shared memory.
+bool Engine::build_tiny() {
+    TinyArgs probe{};  // state + lists + one step with every neuron stimulated
+    probe.n = n_;
+    probe.steps = 1;
+    probe.hw = hw_;
+    probe.f64 = f64_ ? 1 : 0;
+    probe.m = static_cast<int32_t>(pre_.size());
+    probe.st_count = n_;
+    probe.stdp = stdp_on_ ? 1 : 0;
+    probe.window = window_;
+    probe.dp = dp_;
+    if (tiny_smem_bytes(probe) + 4096 > static_cast<size_t>(tiny_max_smem())) return false;
+
+    std::vector<uint32_t> off(static_cast<size_t>(n_) + 1, 0);
+    for (size_t s = 0; s < pre_.size(); ++s) ++off[post_[s] + 1];
+    for (int j = 0; j < n_; ++j) off[j + 1] += off[j];
+    std::vector<size_t> ord(pre_.size());
+    std::iota(ord.begin(), ord.end(), 0);
+    std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+        return post_[a] != post_[b] ? post_[a] < post_[b] : pre_[a] < pre_[b];
+    });
+    // meta: (32-bit history word index << 5 | bit) with the word of delay bit
+    // d-1 of pre at (d-1)/32 * np + pre; plastic flag in bit 31
+    const uint32_t np = static_cast<uint32_t>(round_up(n_, 32));
+    std::vector<uint32_t> meta(pre_.size());
+    std::vector<uint16_t> pidx(stdp_on_ ? pre_.size() : 0);
+    std::vector<float> wf;
+    std::vector<double> wd;
+    if (f64_) wd.resize(pre_.size());
+    else wf.resize(pre_.size());
+    slot_.assign(pre_.size(), -1);
+    for (size_t q = 0; q < ord.size(); ++q) {
+        const size_t s = ord[q];
+        const uint32_t d1 = static_cast<uint32_t>(delay_[s] + axonal_[pre_[s]] - 1);
+        const uint32_t pre = static_cast<uint32_t>(pre_[s]);
+        const bool pl = stdp_on_ && plastic_[s];
+        meta[q] = (((d1 >> 5) * np + pre) << 5) | (d1 & 31u) | (pl ? (1u << 31) : 0u);
+        if (stdp_on_) pidx[q] = static_cast<uint16_t>(pre * static_cast<uint32_t>(dp_) + d1);
+        if (f64_) wd[q] = weight_[s];
+        else wf[q] = static_cast<float>(weight_[s]);
+        slot_[s] = static_cast<int64_t>(q);
+    }
+    upload(d_toff_, off);
+    upload(d_meta_, meta);
+    upload(d_tpidx_, pidx);
+    if (f64_) upload(d_w_, wd);
+    else upload(d_w_, wf);
+    syn_local_ = static_cast<int64_t>(pre_.size());
+    sweep_bytes_full_ = static_cast<double>(pre_.size()) * ((stdp_on_ ? 2.0 : 1.0) * (f64_ ? 8 : 4) + 4.0);
+    return true;
+}
+
+// One k_tiny launch per chunk of steps whose stimulus fits next to the state.
+void Engine::run_tiny(int t0, int steps, uint32_t* raster, double* trace, bool host_io) {
+    TinyArgs a{};
+    a.n = n_;
+    a.hw = hw_;
+    a.dmax = dmax_;
+    a.f64 = f64_ ? 1 : 0;
+    a.v = d_v_.as<double>();
+    a.cnt = d_cnt_.as<int32_t>();
+    a.hist = d_hist_.as<uint64_t>();
+    a.thr = d_thr_.as<double>();
+    a.leak = d_leak_.as<double>();
+    a.reset = d_reset_.as<double>();
+    a.refr = d_refr_.as<int32_t>();
+    a.off = d_toff_.as<uint32_t>();
+    a.meta = d_meta_.as<uint32_t>();
+    a.pidx = d_tpidx_.as<uint16_t>();
+    a.w = d_w_.p;
+    a.m = static_cast<int32_t>(pre_.size());
+    a.stdp = stdp_on_ ? 1 : 0;
+    a.window = window_;
+    a.dp = dp_;
+    a.a_plus = d_ap_.as<double>();
+    a.a_minus = d_am_.as<double>();
+    a.w_min = w_min_;
+    a.w_max = w_max_;
+    a.spike_count = d_spikes_.as<unsigned long long>();
+    a.d_step = d_step_.as<int32_t>();
+    const size_t limit = static_cast<size_t>(tiny_max_smem());
+    const int words = std::max(nl_words_, 1);
+    const int table = static_cast<int>(hs_off_.size()) - 1;  // steps covered by the stimulus CSR
+    for (int done = 0; done < steps;) {
+        const int tt = t0 + done;
+        int k = steps - done, rows = 0;
+        int64_t lo = 0, hi = 0;
+        for (;;) {  // shrink the launch until its stimulus fits next to the state
+            rows = std::max(0, std::min(table - tt, k));
+            lo = rows > 0 ? hs_off_[tt] : 0;
+            hi = rows > 0 ? hs_off_[tt + rows] : 0;
+            a.steps = k;
+            a.st_rows = rows;
+            a.st_count = static_cast<int32_t>(hi - lo);
+            if (tiny_smem_bytes(a) <= limit || k == 1) break;
+            k = std::max(1, k / 2);
+        }
+        if (rows == 0) {
+            a.st_off = nullptr;
+            a.st_neuron = nullptr;
+            a.st_amp = nullptr;
+        } else if (host_io) {
+            // the kernel reads this launch's rows straight from pinned host memory
+            const size_t cnt = static_cast<size_t>(hi - lo);
+            const size_t ob = round_up((static_cast<int64_t>(rows) + 1) * 8, 16);
+            h_stage_.reserve(ob + cnt * 12 + 16);
+            uint8_t* base = h_stage_.as<uint8_t>();
+            int64_t* soff = reinterpret_cast<int64_t*>(base);
+            double* samp = reinterpret_cast<double*>(base + ob);
+            int32_t* sneu = reinterpret_cast<int32_t*>(base + ob + cnt * 8);
+            for (int s = 0; s <= rows; ++s) soff[s] = hs_off_[tt + s] - lo;
+            std::memcpy(samp, hs_amp_.data() + lo, cnt * 8);
+            std::memcpy(sneu, hs_neuron_.data() + lo, cnt * 4);
+            a.st_off = soff;
+            a.st_amp = samp;
+            a.st_neuron = sneu;
+        } else {  // device-resident table from build_stimulus_table
+            a.st_off = d_st_off_.as<int64_t>() + tt;
+            a.st_neuron = d_st_neuron_.as<int32_t>();
+            a.st_amp = d_st_amp_.as<double>();
+        }
+        a.raster = raster + static_cast<size_t>(done) * words;
+        a.trace = trace ? trace + static_cast<size_t>(done) * n_ : nullptr;
+        launch_tiny(a, stream_);
+        stats_.kernel_launches += 1;
+        done += k;
+        if (host_io && rows > 0 && done < steps)
+            cuda_check(cudaStreamSynchronize(stream_), "tiny sync");  // staging is reused
+    }
 }
 
 void Engine::validate() const {
@@ -330,14 +499,22 @@ void Engine::setup() {
     else if (opt_.storage == SN_STORAGE_SPARSE) dense_ = false;
     else dense_ = (density >= 0.1 || n_ <= 4096) && dense_bytes < 0.85 * static_cast<double>(free_b);
 
-    if (generated_) build_generated();
-    else if (dense_) build_dense_from_lists();
-    else build_sparse_from_lists();
+    tiny_ = !generated_ && opt_.world == 1 && opt_.persistent >= 0 && opt_.storage == SN_STORAGE_AUTO &&
+            n_ <= kTinyMaxNeurons && build_tiny();
+    if (tiny_) {
+        dense_ = false;  // the shared-memory step loop owns the weights; no dense/sparse copy
+    } else if (generated_) {
+        build_generated();
+    } else if (dense_) {
+        build_dense_from_lists();
+    } else {
+        build_sparse_from_lists();
+    }
 
     alloc_state();
     stim_dirty_ = true;
     build_stimulus_table();
-    plan_launches();
+    if (!tiny_) plan_launches();
     if (opt_.stream_io) {  // pinned staging sized up front (1024 steps of spike words)
         h_raster_.reserve(static_cast<size_t>(1024) * std::max(nl_words_, 1) * 4);
         h_stage_.reserve(64 * 1024);
@@ -1063,7 +1240,39 @@ void Engine::simulate(int32_t steps) {
     }
     cudaEvent_t eb = get_event(), ee = get_event();
     double graph_ms = -1.0;  // device time summed over graph chunks (excludes host syncs)
-    if (opt_.stream_io) {
+    if (tiny_) {
+        // one CTA runs the call; stream_io: stimulus read from and raster
+        // written to pinned host memory by the kernel itself
+        const size_t rwords = static_cast<size_t>(steps) * std::max(nl_words_, 1);
+        uint32_t* raster;
+        if (opt_.stream_io) {
+            h_raster_.reserve(rwords * 4);
+            raster = h_raster_.as<uint32_t>();
+        } else {
+            if (d_raster_.bytes < rwords * 4) d_raster_.alloc(rwords * 4);
+            raster = d_raster_.as<uint32_t>();
+        }
+        cuda_check(cudaEventRecord(eb, stream_), "rec");
+        cudaEvent_t p0{}, p1{};
+        if (opt_.profile) { p0 = get_event(); cuda_check(cudaEventRecord(p0, stream_), "rec"); }
+        run_tiny(t0, steps, raster, trace, opt_.stream_io != 0);
+        if (opt_.profile) {  // the call is one fused launch: accounted as the sweep
+            p1 = get_event();
+            cuda_check(cudaEventRecord(p1, stream_), "rec");
+            pending_.push_back({p0, p1, 1, 0.0});
+        }
+        cuda_check(cudaEventRecord(ee, stream_), "rec");
+        RasterChunk ch;
+        ch.t0 = t0;
+        ch.rows = steps;
+        ch.words.resize(static_cast<size_t>(steps) * nl_words_);
+        if (!opt_.stream_io && !ch.words.empty())
+            cuda_check(cudaMemcpyAsync(ch.words.data(), raster, ch.words.size() * 4, cudaMemcpyDeviceToHost, stream_),
+                       "raster D2H");
+        cuda_check(cudaStreamSynchronize(stream_), "simulate sync");
+        if (opt_.stream_io && !ch.words.empty()) std::memcpy(ch.words.data(), raster, ch.words.size() * 4);
+        raster_.push_back(std::move(ch));
+    } else if (opt_.stream_io) {
         // pack each step's stimulus rows into pinned memory; copy per step
         std::vector<size_t> pos(static_cast<size_t>(steps) + 1, 0);
         size_t total = 0;
@@ -1179,6 +1388,7 @@ void Engine::synchronize() { cuda_check(cudaStreamSynchronize(stream_), "sn_sync
 // ---- host-driven exchange (partition emulation / custom transports) ---------
 void Engine::step_local() {
     require_setup("sn_step_local");
+    if (tiny_) throw LogicError("sn_step_local: single-partition engines run through sn_simulate");
     host_exchange_ = true;
     build_stimulus_table();
     if (d_raster_.bytes < static_cast<size_t>(std::max(nl_words_, 1)) * 4)
@@ -1210,6 +1420,7 @@ void Engine::put_spike_words(int32_t first_word, const uint32_t* w, int64_t coun
 
 void Engine::step_finish() {
     require_setup("sn_step_finish");
+    if (tiny_) throw LogicError("sn_step_finish: single-partition engines run through sn_simulate");
     if (opt_.world > 1) {
         launch_hist(hist_args(), stream_);
         stats_.kernel_launches += 1;
@@ -1331,8 +1542,10 @@ void Engine::decode_raster() {
             rows.emplace_back(ch.words.data() + static_cast<size_t>(r) * nl_words_, ch.t0 + r);
     std::vector<int64_t> start(rows.size() + 1, 0);
     const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    const size_t nthreads = std::max<size_t>(1, std::min<size_t>(hw, rows.size() / 8 + 1));
+    // a thread per ~64k words: spawning costs tens of microseconds
+    const size_t nthreads = std::max<size_t>(1, std::min<size_t>(hw, rows.size() * nl_words_ / 65536));
     auto parallel = [&](auto&& fn) {
+        if (nthreads == 1) return fn(size_t{0}, rows.size());
         std::vector<std::thread> pool;
         const size_t per = (rows.size() + nthreads - 1) / nthreads;
         for (size_t t = 0; t < nthreads; ++t) {
@@ -1371,29 +1584,31 @@ void Engine::get_raster(int32_t* steps, int32_t* neurons, int64_t cap) {
         throw InvalidArgument("sn_get_raster: capacity " + std::to_string(cap) + " < " + std::to_string(ne) + " events");
     const size_t nrows = dec_rows_.size();
     const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    const size_t nthreads = std::max<size_t>(1, std::min<size_t>(hw, nrows / 4 + 1));
+    const size_t nthreads = std::max<size_t>(1, std::min<size_t>(hw, static_cast<size_t>(ne / 131072)));
     const size_t per = (nrows + nthreads - 1) / std::max<size_t>(nthreads, 1);
+    auto expand = [this, steps, neurons](size_t a, size_t b) {
+        for (size_t r = a; r < b; ++r) {
+            int64_t o = dec_start_[r];
+            const uint32_t* row = dec_rows_[r].first;
+            const int32_t step = dec_rows_[r].second;
+            for (int w = 0; w < nl_words_; ++w) {
+                uint32_t x = row[w];
+                while (x) {
+                    const int bit = __builtin_ctz(x);
+                    x &= x - 1;
+                    steps[o] = step;
+                    neurons[o] = first_ + w * 32 + bit;
+                    ++o;
+                }
+            }
+        }
+    };
+    if (nthreads == 1) return expand(0, nrows);
     std::vector<std::thread> pool;
     for (size_t t = 0; t < nthreads; ++t) {
         const size_t a = t * per, b = std::min(nrows, a + per);
         if (a >= b) break;
-        pool.emplace_back([this, steps, neurons, a, b] {
-            for (size_t r = a; r < b; ++r) {
-                int64_t o = dec_start_[r];
-                const uint32_t* row = dec_rows_[r].first;
-                const int32_t step = dec_rows_[r].second;
-                for (int w = 0; w < nl_words_; ++w) {
-                    uint32_t x = row[w];
-                    while (x) {
-                        const int bit = __builtin_ctz(x);
-                        x &= x - 1;
-                        steps[o] = step;
-                        neurons[o] = first_ + w * 32 + bit;
-                        ++o;
-                    }
-                }
-            }
-        });
+        pool.emplace_back(expand, a, b);
     }
     for (auto& th : pool) th.join();
 }
@@ -1451,7 +1666,9 @@ void Engine::get_weight_matrix(double* out, int64_t count) {
         return esz == 8 ? reinterpret_cast<const double*>(host.data())[q]
                         : static_cast<double>(reinterpret_cast<const float*>(host.data())[q]);
     };
-    if (dense_) {
+    if (tiny_) {
+        for (size_t s = 0; s < pre_.size(); ++s) out[static_cast<int64_t>(pre_[s]) * nl_ + post_[s]] = get(slot_[s]);
+    } else if (dense_) {
         for (int i = 0; i < n_; ++i)
             for (int c = 0; c < nl_; ++c) out[static_cast<int64_t>(i) * nl_ + c] = get(static_cast<int64_t>(i) * pitch_ + c);
     } else {
@@ -1482,7 +1699,10 @@ void Engine::get_stats(sn_stats* out) {
             stats_.sweep_bytes_total = sweep_bytes_full_ * static_cast<double>(t_ - steps_at_reset_);
         }
         stats_.sweep_bytes_per_launch_last = sweep_bytes_full_;
-        if (dense_) {
+        if (tiny_) {
+            stats_.sweep_kernel = SN_SWEEP_TINY;
+            stats_.sweep_ctas = 1;
+        } else if (dense_) {
             stats_.sweep_kernel = persistent_ ? SN_SWEEP_PERSISTENT
                                   : exact_    ? SN_SWEEP_DENSE_EXACT
                                   : tma_      ? SN_SWEEP_DENSE_TMA

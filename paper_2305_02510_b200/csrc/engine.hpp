@@ -177,6 +177,13 @@ private:
     bool persistent_ = false;     // small dense nets: one cooperative launch per simulate
     bool dynamic_sched_ = false;  // dense sweep items claimed through an atomic counter
     bool tma_ = false;            // k_dense_tma (cp.async.bulk ring) instead of k_dense_stream
+    // tiny nets: the whole call in one CTA with shared-memory state (k_tiny)
+    static constexpr int kTinyMaxNeurons = 1024;
+    bool tiny_ = false;
+    DevBuf d_toff_, d_tpidx_;
+    void materialize_er();
+    bool build_tiny();
+    void run_tiny(int t0, int steps, uint32_t* raster, double* trace, bool host_io);
     int32_t persist_grid_ = 1;
     double sweep_bytes_full_ = 0.0;  // algorithmic bytes of a sweep over every active row
 

@@ -933,6 +933,214 @@ size_t dense_tma_smem(int tile_w) {
            static_cast<size_t>(kTmaListMax + kTmaRows) * sizeof(RowRec<float>);
 }
 
+// ---------------------------------------------------------------------------
+// Tiny nets: one CTA runs the whole call with every array in shared memory.
+// Per step: (1) thread j integrates post j -- leak, its incoming list in
+// ascending pre order (history bit d-1 of the pre = s_pre[t-d]), the step's
+// stimulus, threshold/refractory/reset; (2) history shift, raster word (warp
+// ballot), STDP traces; (3) thread j applies STDP to its own plastic synapses
+// (mat_engine.cpp:242-249, every plastic synapse every step).  One CTA barrier
+// per step (double-buffered history), no global memory on the critical path.
+struct TinyLayout {
+    size_t hist, pot, dep, off, meta, pidx, w, st_off, st_neuron, st_amp, ap, am, total;
+};
+
+__host__ __device__ inline size_t tiny_align(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
+
+// Shared memory: history as 32-bit words, double-buffered (buffer b, word k,
+// neuron j at [(b * 2hw + k) * np + j]) so one barrier per step separates the
+// readers of step t from the writers of step t+1; STDP traces double-buffered
+// the same way.  Per-neuron LIF state lives in the owning thread's registers.
+__host__ __device__ inline TinyLayout tiny_layout(const TinyArgs& a) {
+    TinyLayout L{};
+    const size_t np = static_cast<size_t>((a.n + 31) / 32 * 32);
+    size_t o = 0;
+    L.hist = o; o = tiny_align(o + 2 * np * 8 * a.hw);
+    L.pot = o; o = tiny_align(o + (a.stdp ? 2 * np * 8 * a.dp : 0));
+    L.dep = o; o = tiny_align(o + (a.stdp ? 2 * np * 8 : 0));
+    L.off = o; o = tiny_align(o + (static_cast<size_t>(a.n) + 1) * 4);
+    L.meta = o; o = tiny_align(o + static_cast<size_t>(a.m) * 4);
+    L.pidx = o; o = tiny_align(o + (a.stdp ? static_cast<size_t>(a.m) * 2 : 0));
+    L.w = o; o = tiny_align(o + static_cast<size_t>(a.m) * (a.f64 ? 8 : 4));
+    L.st_off = o; o = tiny_align(o + (static_cast<size_t>(a.steps) + 1) * 4);
+    L.st_neuron = o; o = tiny_align(o + static_cast<size_t>(a.st_count) * 4);
+    L.st_amp = o; o = tiny_align(o + static_cast<size_t>(a.st_count) * 8);
+    L.ap = o; o = tiny_align(o + (a.stdp ? static_cast<size_t>(a.window) * 8 : 0));
+    L.am = o; o = tiny_align(o + (a.stdp ? static_cast<size_t>(a.window) * 8 : 0));
+    L.total = o;
+    return L;
+}
+
+// Bit test of one incoming synapse: meta = byte offset of the 32-bit history
+// word within a buffer << 3 | bit (plastic flag in bit 31, masked off here).
+__device__ __forceinline__ bool tiny_bit(const uint8_t* buf, uint32_t mq) {
+    const uint32_t word = *reinterpret_cast<const uint32_t*>(buf + ((mq >> 3) & 0x3fffcu));
+    return __funnelshift_r(word, word, mq) & 1u;
+}
+
+template <typename WT, bool STDP>
+__global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    const TinyLayout L = tiny_layout(a);
+    const int tid = threadIdx.x;
+    const int n = a.n;
+    const int np = (n + 31) / 32 * 32;
+    const int hw2 = 2 * a.hw;
+    const size_t hbuf = static_cast<size_t>(hw2) * np * 4;  // bytes per history buffer
+    uint32_t* hist = reinterpret_cast<uint32_t*>(sm + L.hist);
+    double* pot = reinterpret_cast<double*>(sm + L.pot);
+    double* dep = reinterpret_cast<double*>(sm + L.dep);
+    uint32_t* off = reinterpret_cast<uint32_t*>(sm + L.off);
+    uint32_t* meta = reinterpret_cast<uint32_t*>(sm + L.meta);
+    uint16_t* pidx = reinterpret_cast<uint16_t*>(sm + L.pidx);
+    WT* w = reinterpret_cast<WT*>(sm + L.w);
+    int32_t* st_off = reinterpret_cast<int32_t*>(sm + L.st_off);
+    int32_t* st_neuron = reinterpret_cast<int32_t*>(sm + L.st_neuron);
+    double* st_amp = reinterpret_cast<double*>(sm + L.st_amp);
+    double* ap = reinterpret_cast<double*>(sm + L.ap);
+    double* am = reinterpret_cast<double*>(sm + L.am);
+    // ---- load: owned neuron state into registers, shared arrays ----
+    const int j = tid;
+    const bool own = j < n;
+    double v = own ? a.v[j] : 0.0;
+    const double thr = own ? a.thr[j] : 0.0;
+    const double leak = own ? a.leak[j] : 0.0;
+    const double rst = own ? a.reset[j] : 0.0;
+    const int32_t refr = own ? a.refr[j] : 0;
+    int32_t cnt = own ? a.cnt[j] : 0;
+    for (int k = 0; k < a.hw; ++k) {
+        const uint64_t x = own ? a.hist[static_cast<int64_t>(k) * n + j] : 0ull;
+        hist[(2 * k) * np + j] = static_cast<uint32_t>(x);
+        hist[(2 * k + 1) * np + j] = static_cast<uint32_t>(x >> 32);
+    }
+    const int nt = blockDim.x;
+    for (int i = tid; i <= n; i += nt) off[i] = a.off[i];
+    for (int q = tid; q < a.m; q += nt) {
+        meta[q] = a.meta[q];
+        w[q] = static_cast<const WT*>(a.w)[q];
+        if (STDP) pidx[q] = a.pidx[q];
+    }
+    const int64_t sbase = a.st_rows > 0 ? a.st_off[0] : 0;
+    for (int s = tid; s <= a.steps; s += nt)
+        st_off[s] = a.st_rows > 0 ? static_cast<int32_t>(a.st_off[min(s, a.st_rows)] - sbase) : 0;
+    for (int e = tid; e < a.st_count; e += nt) {
+        st_neuron[e] = a.st_neuron[sbase + e];
+        st_amp[e] = a.st_amp[sbase + e];
+    }
+    if (STDP)
+        for (int k = tid; k < a.window; k += nt) {
+            ap[k] = a.a_plus[k];
+            am[k] = a.a_minus[k];
+        }
+    __syncthreads();
+    const int t0 = *a.d_step;
+    const int words = (n + 31) / 32;
+    const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
+    const uint32_t q0 = own ? off[j] : 0u, q1 = own ? off[j + 1] : 0u;
+    unsigned long long spikes = 0;
+    for (int s = 0; s < a.steps; ++s) {
+        const int cur = s & 1;
+        const uint8_t* hc = sm + L.hist + cur * hbuf;        // history through t-1
+        uint32_t* hn = reinterpret_cast<uint32_t*>(sm + L.hist + (cur ^ 1) * hbuf);  // through t
+        bool fired = false;
+        if (own) {
+            // (1) leak, incoming list in ascending pre order (bit d-1 = s_pre[t-d]),
+            // the step's stimulus, threshold, refractory (mat_engine.cpp:160-198)
+            double u = leak_toward(v, leak, rst);
+#pragma unroll 4
+            for (uint32_t q = q0; q < q1; ++q) {
+                const uint32_t mq = meta[q];
+                if (tiny_bit(hc, mq)) u += static_cast<double>(w[q]);
+            }
+            int lo = st_off[s], hi = st_off[s + 1];
+            if (hi > lo) {
+                double ext = 0.0;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    const int nm = st_neuron[mid];
+                    if (nm == j) { ext = st_amp[mid]; break; }
+                    if (nm < j) lo = mid + 1; else hi = mid;
+                }
+                u += ext;
+            }
+            fired = u > thr;
+            if (cnt > 0) {
+                fired = false;
+                cnt -= 1;
+                u = rst;
+            }
+            if (fired) {
+                v = rst;
+                cnt = refr;
+            } else {
+                v = u;
+            }
+            if (a.trace) a.trace[static_cast<int64_t>(s) * n + j] = v;
+        }
+        const uint32_t word = __ballot_sync(0xffffffffu, fired);
+        if ((tid & 31) == 0 && (tid >> 5) < words) {
+            a.raster[static_cast<int64_t>(s) * words + (tid >> 5)] = word;
+            spikes += __popc(word);
+        }
+        // (2) own history row into the other buffer (+ own STDP traces)
+        if (j < np) {
+            const uint32_t* hcw = reinterpret_cast<const uint32_t*>(hc);
+            uint32_t carry = fired ? 1u : 0u;
+            for (int k = 0; k < hw2; ++k) {
+                const uint32_t x = hcw[k * np + j];
+                hn[k * np + j] = (x << 1) | carry;
+                carry = x >> 31;
+            }
+            if (STDP && own) {
+                double* potn = pot + (cur ^ 1) * np * a.dp;
+                double dsum = 0.0;
+                for (int k = 1; k <= a.window; ++k)
+                    if ((hn[(k >> 5) * np + j] >> (k & 31)) & 1u) dsum += am[k - 1];
+                dep[(cur ^ 1) * np + j] = dsum;
+                for (int d = 1; d <= a.dp; ++d) {
+                    double psum = 0.0;
+                    for (int k = 1; k <= a.window; ++k) {
+                        const int b = k + d - 1;
+                        if ((hn[(b >> 5) * np + j] >> (b & 31)) & 1u) psum += ap[k - 1];
+                    }
+                    potn[j * a.dp + (d - 1)] = psum;
+                }
+            }
+        }
+        __syncthreads();  // the new history (and traces) of step t are complete
+        if (STDP && own) {
+            // (3) STDP on post j's plastic synapses: dw = 0; if s_post dw += pot^(d)_pre;
+            // if s_pre[t-d+1] dw -= dep_post; clamp (mat_engine.cpp:242-249)
+            const uint8_t* hnb = reinterpret_cast<const uint8_t*>(hn);
+            const double* potn = pot + (cur ^ 1) * np * a.dp;
+            const double depj = dep[(cur ^ 1) * np + j];
+            for (uint32_t q = q0; q < q1; ++q) {
+                const uint32_t mq = meta[q];
+                if (!(mq >> 31)) continue;
+                WT dw = WT(0);
+                if (fired) dw += static_cast<WT>(potn[pidx[q]]);
+                if (tiny_bit(hnb, mq)) dw -= static_cast<WT>(depj);
+                w[q] = clamp_ref<WT>(w[q] + dw, wmin, wmax);
+            }
+        }
+    }
+    // ---- write back (the last step's history is in buffer steps & 1) ----
+    const uint32_t* hl = reinterpret_cast<const uint32_t*>(sm + L.hist + (a.steps & 1) * hbuf);
+    if (own) {
+        a.v[j] = v;
+        a.cnt[j] = cnt;
+        for (int k = 0; k < a.hw; ++k)
+            a.hist[static_cast<int64_t>(k) * n + j] =
+                static_cast<uint64_t>(hl[(2 * k) * np + j]) | (static_cast<uint64_t>(hl[(2 * k + 1) * np + j]) << 32);
+    }
+    if (STDP) {
+        __syncthreads();  // every owner's last-step weight update is done
+        for (int q = tid; q < a.m; q += nt) static_cast<WT*>(a.w)[q] = w[q];
+    }
+    if (spikes) atomicAdd(a.spike_count, spikes);
+    if (tid == 0) *a.d_step = t0 + a.steps;
+}
+
 // Persistent single-GPU step loop for small dense nets (launch-latency bound
 // otherwise): one cooperative launch runs `steps` steps; neuron phase and
 // sweep phase are separated by grid-wide barriers (cooperative groups).
@@ -1436,6 +1644,33 @@ uint64_t stream_key(uint64_t seed, uint64_t stream) {
 int dense_vec(bool f64) { return f64 ? 2 : 4; }
 
 int dense_tma_max_rows() { return kTmaListMax; }
+
+size_t tiny_smem_bytes(const TinyArgs& a) { return tiny_layout(a).total; }
+
+int tiny_max_smem() {
+    int dev = 0, v = 0;
+    check(cudaGetDevice(&dev), "cudaGetDevice");
+    check(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
+    return v;
+}
+
+void launch_tiny(const TinyArgs& a, cudaStream_t s) {
+    const size_t smem = tiny_smem_bytes(a);
+    const int threads = (a.n + 31) / 32 * 32;
+    auto go = [&](auto kern) {
+        check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+              "k_tiny smem attribute");
+        kern<<<1, threads, smem, s>>>(a);
+    };
+    if (a.f64) {
+        if (a.stdp) go(k_tiny<double, true>);
+        else go(k_tiny<double, false>);
+    } else {
+        if (a.stdp) go(k_tiny<float, true>);
+        else go(k_tiny<float, false>);
+    }
+    check(cudaGetLastError(), "k_tiny");
+}
 
 void launch_dense_tma(const DenseArgs& a, bool stdp, int grid, cudaStream_t s) {
     const size_t smem = dense_tma_smem(a.tile_w);

@@ -163,6 +163,57 @@ int persistent_max_ctas(bool f64, bool stdp, bool delay);
 void launch_persistent_dense(const NeuronArgs& na, const HistArgs& h, const DenseArgs& da, bool f64,
                              bool stdp, bool delay, int grid, int steps, cudaStream_t s);
 
+// ---- tiny nets: the whole T-step loop in one CTA, all state in shared memory ----
+// Eligible when N <= 1024 and the incoming lists, the per-neuron state and the
+// call's stimulus fit in shared memory.  Thread j owns post j: it sums its
+// incoming list in ascending pre order starting from leak(v) (the order of
+// mat_engine.cpp:173-180, so fp64 membranes are bit-exact) and applies STDP
+// to its own plastic synapses.
+struct TinyArgs {
+    int32_t n;
+    int32_t steps;
+    int32_t hw;                // history words per neuron
+    int32_t dmax;
+    int32_t f64;               // weight precision of w
+    // state (global, loaded at start and written back at the end)
+    double* v;
+    int32_t* cnt;
+    uint64_t* hist;            // [hw][n]
+    const double* thr;
+    const double* leak;
+    const double* reset;
+    const int32_t* refr;
+    // incoming lists, post-major, pre ascending
+    const uint32_t* off;       // [n+1]
+    const uint32_t* meta;      // history word byte offset << 3 | (d-1) & 31, plastic << 31
+    const uint16_t* pidx;      // STDP: pre * dp + (d-1), the pot^(d) trace of the pre
+    void* w;                   // float or double [m]
+    int32_t m;
+    // stimulus of this launch: rows of the per-step CSR (neuron ascending).
+    // st_off points at the row of the launch's first step; entries are
+    // st_neuron/st_amp[st_off[s]]; only the first st_rows rows exist.
+    const int64_t* st_off;     // [st_rows + 1]
+    const int32_t* st_neuron;
+    const double* st_amp;
+    int32_t st_rows;
+    int32_t st_count;          // st_off[st_rows] - st_off[0]
+    // STDP
+    int32_t stdp;
+    int32_t window;
+    int32_t dp;
+    const double* a_plus;
+    const double* a_minus;
+    double w_min, w_max;
+    // outputs (device or host-mapped pinned memory)
+    uint32_t* raster;          // [steps][words]
+    double* trace;             // [steps][n] or null
+    unsigned long long* spike_count;
+    int32_t* d_step;
+};
+size_t tiny_smem_bytes(const TinyArgs& a);
+int tiny_max_smem();
+void launch_tiny(const TinyArgs& a, cudaStream_t s);
+
 // ---- on-device Erdos-Renyi generation (netgen.cpp:36-51 semantics) ----
 struct ErArgs {
     int32_t n;

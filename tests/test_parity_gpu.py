@@ -28,7 +28,13 @@ CONFIGS = {
     "dense_f32_nograph": dict(storage=1, use_graphs=False, persistent=False),
     "dense_f32_graph": dict(storage=1, persistent=False),
     "dense_f64": dict(storage=1, precision="f64"),
+    # automatic storage: nets that fit in shared memory run k_tiny (ascending-pre
+    # order, so fp64 is bit-exact like the exact sweeps)
+    "tiny_f32": dict(storage=0),
+    "tiny_f64": dict(storage=0, precision="f64", exact_order=True),
+    "tiny_f32_stream": dict(storage=0, stream_io=True),
 }
+TINY_KERNEL = 9
 
 
 def run_engine(c, chunks=None, **cfg):
@@ -94,8 +100,10 @@ def test_engine_matches_reference_goldens(fname, factory, cfg_name):
     g = np.load(os.path.join(GOLD, fname))
     f64 = cfg.get("precision") == "f64"
     exact = cfg.get("exact_order", False)
+    tiny_runs = 0
     for c in factory():
         r = run_engine(c, **cfg)
+        tiny_runs += r["stats"]["sweep_kernel"] == TINY_KERNEL
         assert np.array_equal(r["steps"], g[f"{c.name}/steps"]), (c.name, cfg_name)
         assert np.array_equal(r["neurons"], g[f"{c.name}/neurons"]), (c.name, cfg_name)
         gm = g[f"{c.name}/membrane"]
@@ -113,6 +121,32 @@ def test_engine_matches_reference_goldens(fname, factory, cfg_name):
                 assert close_rel(r["weights"], gw), (c.name, cfg_name)
         if c.record:
             assert np.array_equal(r["trace"], g[f"{c.name}/trace"]), (c.name, cfg_name)
+    if cfg_name.startswith("tiny"):
+        assert tiny_runs > 0, "no case took the shared-memory path"
+
+
+def test_tiny_chunked_and_stimulus_overflow():
+    """k_tiny across several simulate calls, and a stimulus table too large for
+    one launch's shared memory (the engine splits the call), equal the oracle."""
+    from oracle import bridge as B
+    from support import random_net, random_stim
+    from paper_2305_02510_b200.model import StdpConfig
+    d = StdpConfig.defaults()
+    for seed in (510, 511):
+        net = random_net(seed, min_neurons=600, max_neurons=900, edge_prob=0.006, max_delay=5, max_axonal=1)
+        for i, s in enumerate(net.synapses):
+            s.stdp_enabled = i % 2 == 0
+        n = net.neuron_count()
+        steps = 400
+        stim = random_stim(seed, n, steps, 40 * steps)   # ~40 kicks per step: > smem for 400 steps
+        c = CS.Case(f"tiny_overflow_{seed}", net, steps, stim, stdp=d)
+        o = B.run_oracle(c.arrays(), steps, c.stim_arrays(), c.stdp_tuple())
+        for chunks in (None, [3, 150, steps - 153]):
+            r = run_engine(c, chunks=chunks, storage=0, precision="f64")
+            assert r["stats"]["sweep_kernel"] == TINY_KERNEL
+            assert np.array_equal(r["steps"], o["steps"]) and np.array_equal(r["neurons"], o["neurons"])
+            assert np.array_equal(r["weights"], o["weights"])
+            assert np.array_equal(r["membrane"], o["membrane"])
 
 
 def test_chunked_simulate_equals_single_call():
@@ -153,7 +187,7 @@ def _generated(entry, storage, stdp=False, by_syn=False, precision="f32"):
     return eng
 
 
-@pytest.mark.parametrize("storage", [1, 2])
+@pytest.mark.parametrize("storage", [0, 1, 2])
 @pytest.mark.parametrize("tag", ["cfg1_seed0", "cfg1_seed1", "cfg1_seed42", "n1000_p1_seed0"])
 def test_generated_scenarios_match_reference(tag, storage):
     """On-device erdos_renyi + paper protocol == reference mat_run raster."""
