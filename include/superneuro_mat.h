@@ -24,6 +24,9 @@
  *   WeightMatrix::slot_get(slot(s)) (mat_engine.hpp:37-39)
  *                                                         sn_get_synapse_weights
  *   erdos_renyi (netgen.hpp:31-34, netgen.cpp:19-54)      sn_generate_erdos_renyi
+ *   AbmWorld / abm_run (abm_engine.hpp:70-121)            sn_options.mode = SN_MODE_ABM
+ *   SimulationConfig::seed, StochasticLifBehavior
+ *     (abm_engine.hpp:43-52, bindings.cpp:180-186)        sn_set_seed, sn_set_fire_probability
  *   std::invalid_argument / std::logic_error messages     sn_status + sn_last_error()
  *
  * Unlike mat_init (mat_engine.cpp:114-131), delays > 1 and axonal delays are
@@ -74,6 +77,12 @@ typedef enum sn_precision {
     SN_WEIGHTS_F64 = 1     /* fp64 storage + fp64 STDP arithmetic (bit-exact weights) */
 } sn_precision;
 
+typedef enum sn_mode {
+    SN_MODE_MAT = 0,  /* mat_run (mat_engine.cpp:168-287): u = leak(v) + W-sum [+ ext]; "lif" only */
+    SN_MODE_ABM = 1   /* abm_run (abm_engine.cpp:146-243): u = leak(v) + (W-sum + ext), per-neuron
+                         stochastic firing (sn_set_fire_probability), no plasticity */
+} sn_mode;
+
 typedef struct sn_options {
     int32_t abi_version;     /* = SN_ABI_VERSION */
     int32_t device;          /* CUDA ordinal */
@@ -95,7 +104,8 @@ typedef struct sn_options {
     int32_t profile;         /* 1: time every kernel with CUDA events (sn_get_stats) */
     int32_t persistent;      /* 0: auto (one cooperative launch per sn_simulate for small
                                 dense single-GPU nets), -1: never */
-    int32_t reserved[4];
+    int32_t mode;            /* sn_mode: MAT (mat_run) or agent-based (abm_run) semantics */
+    int32_t reserved[3];
 } sn_options;
 
 typedef struct sn_stats {
@@ -181,6 +191,22 @@ SN_API sn_status sn_generate_erdos_renyi(sn_engine* e, int32_t n, double p, uint
                                   double weight, int32_t delay_max,
                                   uint64_t delay_stream, int32_t delay_by_synapse_index,
                                   int32_t stdp_enabled);
+
+/* ---- agent-based mode (sn_options.mode = SN_MODE_ABM) -------------------- */
+/* SimulationConfig::seed (model.hpp:80-85): keys the per-(agent, step) random
+ * streams of stochastic behaviours (abm_engine.cpp:163-164).  Before sn_setup. */
+SN_API sn_status sn_set_seed(sn_engine* e, uint64_t seed);
+/* Behaviour of neurons [first, first + count): the fire probability p of
+ * StochasticLifBehavior (abm_engine.cpp:28-39) -- above threshold, the neuron
+ * fires iff the first unit draw of RandomStream(seed, "abm-agen", id, step)
+ * is < p.  p = 1 is "lif" (BehaviorRegistry's built-in, abm_engine.cpp:40),
+ * 0.5 is "stochastic_lif" (:41), any p in [0, 1] is what
+ * register_stochastic_lif(name, p) registers (bindings.cpp:180-186).
+ * Neurons must already be added; p outside [0, 1] is SN_ERR_INVALID_ARGUMENT
+ * ("stochastic lif: fire probability must be in [0, 1]").  In MAT mode any
+ * p != 1 makes sn_setup fail like mat_init (mat_engine.cpp:116-119). */
+SN_API sn_status sn_set_fire_probability(sn_engine* e, int64_t first, int64_t count,
+                                         const double* fire_probability);
 
 /* ---- mat_init / mat_run ------------------------------------------------- */
 /* Validates (reference messages, model.cpp:34-117) and builds device state. */

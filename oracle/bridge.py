@@ -47,6 +47,8 @@ class Problem(C.Structure):
         ("w_min", C.c_double),
         ("w_max", C.c_double),
         ("record_membrane", C.c_int32),
+        ("seed", C.c_uint64),
+        ("fire_p", C.POINTER(C.c_double)),
     ]
 
 
@@ -87,6 +89,8 @@ def oracle_lib():
         lib = C.CDLL(ORACLE_SO)
         lib.mat_oracle_run.argtypes = [C.POINTER(Problem), C.POINTER(Result)]
         lib.mat_oracle_run.restype = C.c_int
+        lib.abm_oracle_run.argtypes = [C.POINTER(Problem), C.POINTER(Result)]
+        lib.abm_oracle_run.restype = C.c_int
         lib.orc_result_free.argtypes = [C.POINTER(Result)]
         _oracle = lib
     return _oracle
@@ -107,6 +111,7 @@ def ref_lib():
         lib.ref_mat_run_raster.argtypes = [P, C.c_int, R]
         lib.ref_oracle_run.argtypes = [P, R]
         lib.ref_abm_run.argtypes = [P, R]
+        lib.ref_abm_run_full.argtypes = [P, R]
         lib.ref_validate.argtypes = [P, C.c_char_p, C.c_int]
         lib.ref_mat_init_error.argtypes = [P, C.c_char_p, C.c_int]
         lib.ref_erdos_renyi.argtypes = [C.c_int, C.c_double, C.c_uint64, C.POINTER(C.c_int32),
@@ -137,7 +142,8 @@ class _Keep:
     """Holds the numpy buffers a Problem points into."""
 
 
-def make_problem(arrays: dict, steps: int, stim=None, stdp=None, record_membrane=False):
+def make_problem(arrays: dict, steps: int, stim=None, stdp=None, record_membrane=False,
+                 seed: int = 0, fire_p=None):
     """arrays: NetworkDef.to_arrays() layout; stim: (step, neuron, amp) arrays;
     stdp: (window, a_plus, a_minus, w_min, w_max) or None."""
     keep = _Keep()
@@ -178,6 +184,9 @@ def make_problem(arrays: dict, steps: int, stim=None, stdp=None, record_membrane
         p.w_min = wmin
         p.w_max = wmax
     p.record_membrane = 1 if record_membrane else 0
+    p.seed = int(seed) & ((1 << 64) - 1)
+    if fire_p is not None:
+        p.fire_p = arr("fp", fire_p, np.float64, C.c_double)
     return p, keep
 
 
@@ -245,6 +254,24 @@ def run_ref_abm(arrays, steps, stim=None) -> dict:
     r = Result()
     lib.ref_abm_run(C.byref(p), C.byref(r))
     return _collect(lib, r, steps, with_state=False)
+
+
+def run_abm_oracle(arrays, steps, stim=None, seed=0, fire_p=None, record_membrane=False) -> dict:
+    """abm_oracle.c: the plain-C restatement of abm_run."""
+    lib = oracle_lib()
+    p, keep = make_problem(arrays, steps, stim, None, record_membrane, seed, fire_p)
+    r = Result()
+    lib.abm_oracle_run(C.byref(p), C.byref(r))
+    return _collect(lib, r, steps)
+
+
+def run_ref_abm_full(arrays, steps, stim=None, seed=0, fire_p=None, record_membrane=False) -> dict:
+    """The reference's abm_run with stochastic behaviours and the run seed."""
+    lib = ref_lib()
+    p, keep = make_problem(arrays, steps, stim, None, record_membrane, seed, fire_p)
+    r = Result()
+    lib.ref_abm_run_full(C.byref(p), C.byref(r))
+    return _collect(lib, r, steps)
 
 
 def ref_validate(arrays, steps, stim=None, stdp=None):

@@ -52,6 +52,11 @@ typedef struct orc_problem {
     double w_min;
     double w_max;
     int32_t record_membrane;
+    /* agent-based mode (abm_engine.hpp:70-121): SimulationConfig::seed and one
+       fire probability per neuron (NULL = all "lif"; p < 1 = a StochasticLif
+       behaviour with that probability, abm_engine.cpp:28-39) */
+    uint64_t seed;
+    const double* fire_p;
 } orc_problem;
 
 typedef struct orc_result {

@@ -25,10 +25,12 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <limits>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -253,6 +255,50 @@ int ref_abm_run(const orc_problem* p, orc_result* out) {
         SimulationConfig cfg = to_cfg(p);
         cfg.stdp.reset();
         put_raster(abm_run(to_net(p), cfg, to_stim(p)).raster, out);
+    });
+}
+
+// abm_run with heterogeneous behaviours: fire_p[i] < 1 runs neuron i under a
+// StochasticLifBehavior(fire_p[i]) registered through the reference's own
+// registry (the register_stochastic_lif binding, bindings.cpp:180-186);
+// "stochastic_lif" is used for 0.5 and "lif" for 1.  Always records the
+// membrane trace: its last row is the final membrane.
+int ref_abm_run_full(const orc_problem* p, orc_result* out) {
+    return guarded(out, [&] {
+        NetworkDef net = to_net(p);
+        if (p->fire_p) {
+            for (int i = 0; i < p->n; ++i) {
+                const double fp = p->fire_p[i];
+                if (fp == 1.0) continue;
+                if (fp == 0.5) {
+                    net.neurons[i].behavior = "stochastic_lif";
+                    continue;
+                }
+                char name[64];
+                std::snprintf(name, sizeof(name), "shim_stochastic_%a", fp);
+                if (!BehaviorRegistry::global().find(name))
+                    BehaviorRegistry::global().register_behavior(
+                        name, std::make_shared<StochasticLifBehavior>(fp));
+                net.neurons[i].behavior = name;
+            }
+        }
+        SimulationConfig cfg = to_cfg(p);
+        cfg.stdp.reset();
+        cfg.seed = p->seed;
+        cfg.record_membrane = true;
+        const RunResult r = abm_run(net, cfg, to_stim(p));
+        put_raster(r.raster, out);
+        out->n = p->n;
+        out->membrane = static_cast<double*>(std::malloc(sizeof(double) * std::max(1, p->n)));
+        const auto& last = r.membrane_trace.back();
+        std::copy(last.begin(), last.end(), out->membrane);
+        if (p->record_membrane) {
+            out->membrane_trace = static_cast<double*>(
+                std::malloc(sizeof(double) * static_cast<std::size_t>(p->steps) * std::max(1, p->n)));
+            for (int t = 0; t < p->steps; ++t)
+                std::copy(r.membrane_trace[t].begin(), r.membrane_trace[t].end(),
+                          out->membrane_trace + static_cast<std::size_t>(t) * p->n);
+        }
     });
 }
 

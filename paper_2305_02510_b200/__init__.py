@@ -1,4 +1,5 @@
-"""B200-native engine for SuperNeuro's MAT-mode simulation step.
+"""B200-native engine for SuperNeuro's MAT-mode simulation step (and the
+agent-based mode, ``abm_run``, on the same kernels).
 
 The API mirrors the reference's ``spikeforge`` module (proj/python/spikeforge/
 __init__.py) for the MAT path; compute runs in hand-written sm_100a kernels
@@ -12,6 +13,7 @@ from .netgen import (BenchScenario, RandomStream, ScenarioBundle, SequentialRng,
                      erdos_renyi, mix64)
 from .engine import MatEngine, comm_unique_id, device_count, partition_range, stdp_defaults
 from .api import NeuromorphicModel, mat_run
+from .abm import abm_run, behavior_names, register_stochastic_lif
 from .lowering import LoweredNetwork, ProxyInfo, annotate_proxy_metadata, lower_delays, proxy_count
 from .io import (FormatError, parse_network, parse_raster, parse_stdp, parse_stimulus,
                  serialize_network, serialize_stdp, write_raster, write_stimulus)
@@ -23,8 +25,8 @@ __all__ = [
     "validate_network", "validate_stdp", "validate_stimulus", "BenchScenario", "RandomStream",
     "ScenarioBundle", "SequentialRng", "build_scenario", "erdos_renyi", "mix64", "MatEngine",
     "comm_unique_id", "device_count", "partition_range", "stdp_defaults", "NeuromorphicModel",
-    "mat_run", "LoweredNetwork", "ProxyInfo", "annotate_proxy_metadata", "lower_delays",
-    "proxy_count", "FormatError", "parse_network", "parse_raster", "parse_stdp", "parse_stimulus",
+    "mat_run", "abm_run", "behavior_names", "register_stochastic_lif", "LoweredNetwork",
+    "ProxyInfo", "annotate_proxy_metadata", "lower_delays", "proxy_count", "FormatError", "parse_network", "parse_raster", "parse_stdp", "parse_stimulus",
     "serialize_network", "serialize_stdp", "write_raster", "write_stimulus",
 ]
 

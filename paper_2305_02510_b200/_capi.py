@@ -22,6 +22,7 @@ SN_ERR_UNSUPPORTED = 6
 
 SN_STORAGE_AUTO, SN_STORAGE_DENSE, SN_STORAGE_SPARSE = 0, 1, 2
 SN_WEIGHTS_F32, SN_WEIGHTS_F64 = 0, 1
+SN_MODE_MAT, SN_MODE_ABM = 0, 1
 SN_ABI_VERSION = 1
 
 
@@ -39,7 +40,8 @@ class Options(C.Structure):
         ("world", C.c_int32),
         ("profile", C.c_int32),
         ("persistent", C.c_int32),
-        ("reserved", C.c_int32 * 4),
+        ("mode", C.c_int32),
+        ("reserved", C.c_int32 * 3),
     ]
 
 
@@ -103,6 +105,8 @@ SIGNATURES = {
     "sn_set_stdp": (_i32, [_P, _i32, _pdbl, _pdbl, _dbl, _dbl]),
     "sn_stdp_defaults": (_i32, [_pi32, _pdbl, _pdbl, _pdbl, _pdbl]),
     "sn_generate_erdos_renyi": (_i32, [_P, _i32, _dbl, _u64, _dbl, _i32, _u64, _i32, _i32]),
+    "sn_set_seed": (_i32, [_P, _u64]),
+    "sn_set_fire_probability": (_i32, [_P, _i64, _i64, _pdbl]),
     "sn_setup": (_i32, [_P]),
     "sn_simulate": (_i32, [_P, _i32]),
     "sn_synchronize": (_i32, [_P]),

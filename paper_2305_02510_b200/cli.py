@@ -4,12 +4,16 @@ with GPU backends.  Exit codes as the reference: 0 ok, 1 diverged, 2 error
 (spikeforge_main.cpp:26-27, 319-328).
 
   python -m paper_2305_02510_b200 run --network net.json --stimulus stim.csv \\
-         --steps 1000 [--backend gpu|gpu-sparse|gpu-exact] [--stdp stdp.json] [--out raster.csv]
+         --steps 1000 [--backend gpu|gpu-sparse|gpu-exact|gpu-abm] [--stdp stdp.json] [--out raster.csv]
 
 Backends: ``gpu`` (Auto storage, fp32 weights), ``gpu-dense`` / ``gpu-sparse``
 (forced storage), ``gpu-exact`` (fp64 weights + ascending-pre order: bit-exact
 with the reference mat path on float nets).  ``mat`` is accepted as an alias of
-``gpu``.  Delays need no lowering on any backend.  ``compare --against FILE``
+``gpu``.  ``gpu-abm`` (alias ``abm``) runs the agent-based mode (abm_run
+semantics: heterogeneous/stochastic behaviours, the run seed, no plasticity;
+fp64 + ascending order, bit-exact with the reference abm backend) and
+``gpu-abm-fast`` the same with fp32 weights and the parallel sum.
+Delays need no lowering on any backend.  ``compare --against FILE``
 checks a run against a raster CSV produced by the reference CLI.
 """
 from __future__ import annotations
@@ -23,6 +27,7 @@ from typing import List, Optional
 import numpy as np
 
 from . import io as fio
+from .abm import abm_run
 from .api import mat_run
 from .model import SimulationConfig, SpikeRaster, StimulusSchedule, WeightStorage
 from .netgen import BenchScenario, build_scenario, erdos_renyi
@@ -36,6 +41,9 @@ BACKENDS = {
     "gpu-dense": dict(storage=WeightStorage.Dense),
     "gpu-sparse": dict(storage=WeightStorage.Sparse),
     "gpu-exact": dict(storage=WeightStorage.Auto, precision="f64", exact_order=True),
+    "gpu-abm": dict(storage=WeightStorage.Auto, precision="f64", exact_order=True, abm=True),
+    "abm": dict(storage=WeightStorage.Auto, precision="f64", exact_order=True, abm=True),
+    "gpu-abm-fast": dict(storage=WeightStorage.Auto, precision="f32", exact_order=False, abm=True),
 }
 
 
@@ -45,7 +53,10 @@ def run_backend(backend: str, net, cfg, stim, device: int = 0):
     opts = dict(BACKENDS[backend])
     storage = opts.pop("storage")
     t0 = time.perf_counter()
-    res = mat_run(net, cfg, stim, storage, device=device, **opts)
+    if opts.pop("abm", False):
+        res = abm_run(net, cfg, stim, device=device, storage=int(storage), **opts)
+    else:
+        res = mat_run(net, cfg, stim, storage, device=device, **opts)
     return res.raster, time.perf_counter() - t0
 
 
@@ -120,10 +131,13 @@ def cmd_bench(a) -> int:
     for backend in a.backends.split(","):
         opts = dict(BACKENDS[backend])
         storage = int(opts.pop("storage"))
+        mode = "abm" if opts.pop("abm", False) else "mat"
         for n in sizes:
             for p in probs:
-                eng = MatEngine(device=a.device, storage=storage, **opts)
+                eng = MatEngine(device=a.device, storage=storage, mode=mode, **opts)
                 eng.generate_erdos_renyi(n, p, a.seed)
+                if mode == "abm":
+                    eng.set_seed(a.seed)
                 eng.setup()
                 from .netgen import scenario_stimulus
                 eng.add_stimulus(*scenario_stimulus(n, a.steps, a.seed, amplitude=a.amplitude).to_arrays())

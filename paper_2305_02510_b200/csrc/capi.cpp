@@ -154,6 +154,20 @@ sn_status sn_stdp_defaults(int32_t* window, double* a_plus, double* a_minus, dou
     });
 }
 
+sn_status sn_set_seed(sn_engine* e, uint64_t seed) {
+    return guard([&] {
+        SN_NEED(e);
+        e->impl.set_seed(seed);
+    });
+}
+
+sn_status sn_set_fire_probability(sn_engine* e, int64_t first, int64_t count, const double* p) {
+    return guard([&] {
+        SN_NEED(e);
+        e->impl.set_fire_probability(first, count, p);
+    });
+}
+
 sn_status sn_generate_erdos_renyi(sn_engine* e, int32_t n, double p, uint64_t seed, double weight,
                                   int32_t delay_max, uint64_t delay_stream, int32_t by_syn,
                                   int32_t stdp_enabled) {

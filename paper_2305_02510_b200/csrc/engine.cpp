@@ -75,6 +75,12 @@ void upload(DevBuf& d, const std::vector<T>& h) {
 
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+uint64_t host_mix64(uint64_t z) {  // rng.hpp:8-12
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -82,6 +88,7 @@ Engine::Engine(const sn_options& opt) : opt_(opt) {
     if (opt_.world < 1) throw InvalidArgument("sn_engine_create: world must be >= 1");
     if (opt_.rank < 0 || opt_.rank >= opt_.world) throw InvalidArgument("sn_engine_create: rank out of range");
     if (opt_.storage < 0 || opt_.storage > 2) throw InvalidArgument("sn_engine_create: unknown storage");
+    if (opt_.mode != SN_MODE_MAT && opt_.mode != SN_MODE_ABM) throw InvalidArgument("sn_engine_create: unknown mode");
     int count = 0;
     cuda_check(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
     if (opt_.device < 0 || opt_.device >= count)
@@ -91,6 +98,40 @@ Engine::Engine(const sn_options& opt) : opt_(opt) {
     cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     f64_ = opt_.precision == SN_WEIGHTS_F64;
     exact_ = opt_.exact_order != 0;
+    abm_ = opt_.mode == SN_MODE_ABM;
+}
+
+// ---- agent-based mode ----------------------------------------------------------
+// SimulationConfig::seed (model.hpp:80-85): keys the per-(agent, step) streams
+// of the stochastic behaviours (abm_engine.cpp:163-164).
+void Engine::set_seed(uint64_t seed) {
+    require_not_setup("sn_set_seed");
+    seed_ = seed;
+}
+
+// Behaviour of neurons [first, first + count) as the fire probability of
+// StochasticLifBehavior (abm_engine.cpp:28-39); 1 = "lif".
+void Engine::set_fire_probability(int64_t first, int64_t count, const double* p) {
+    require_not_setup("sn_set_fire_probability");
+    const int64_t n = static_cast<int64_t>(thr_.size());
+    if (count < 0 || first < 0 || first + count > n)
+        throw InvalidArgument("sn_set_fire_probability: neuron range [" + std::to_string(first) + ", " +
+                              std::to_string(first + count) + ") outside the " + std::to_string(n) +
+                              " neurons added");
+    if (count > 0 && !p) throw InvalidArgument("sn_set_fire_probability: null array");
+    for (int64_t i = 0; i < count; ++i)
+        if (!(p[i] >= 0.0 && p[i] <= 1.0))  // abm_engine.cpp:30-32
+            throw InvalidArgument("stochastic lif: fire probability must be in [0, 1]");
+    if (fire_p_.size() < static_cast<size_t>(n)) fire_p_.resize(static_cast<size_t>(n), 1.0);
+    std::copy(p, p + count, fire_p_.begin() + first);
+}
+
+uint64_t Engine::agent_stream_key(uint64_t seed, uint64_t agent) {
+    // RandomStream(seed, 0x61626d2d6167656e, agent, step) keys (rng.hpp:19-24,
+    // abm_engine.cpp:12); the final mix with the step happens on the device
+    uint64_t k = host_mix64(seed + 0x9e3779b97f4a7c15ULL);
+    k = host_mix64(k ^ 0x61626d2d6167656eULL);
+    return host_mix64(k ^ agent);
 }
 
 Engine::~Engine() {
@@ -163,10 +204,10 @@ void Engine::add_stimulus(int64_t count, const int32_t* step, const int32_t* neu
     for (int64_t i = 0; i < count; ++i) {
         const std::string who = "stimulus[" + std::to_string(base + i) + "]";
         if (step[i] < 0)
-            throw InvalidArgument("mat_run: " + who + ": step " + std::to_string(step[i]) + " is negative");
-        if (!std::isfinite(amp[i])) throw InvalidArgument("mat_run: " + who + ": amplitude must be finite");
+            throw InvalidArgument(run_name() + ": " + who + ": step " + std::to_string(step[i]) + " is negative");
+        if (!std::isfinite(amp[i])) throw InvalidArgument(run_name() + ": " + who + ": amplitude must be finite");
         if (setup_done_ && (neuron[i] < 0 || neuron[i] >= n_))
-            throw InvalidArgument("mat_run: " + who + ": neuron id " + std::to_string(neuron[i]) +
+            throw InvalidArgument(run_name() + ": " + who + ": neuron id " + std::to_string(neuron[i]) +
                                   " out of range (" + std::to_string(n_) + " neurons)");
     }
     st_step_.insert(st_step_.end(), step, step + count);
@@ -237,12 +278,7 @@ void Engine::generate_er(int32_t n, double p, uint64_t seed, double weight, int3
 // including the shared-memory step loop -- applies to them.
 void Engine::materialize_er() {
     const int n = er_.n;
-    auto mix = [](uint64_t z) {
-        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-        return z ^ (z >> 31);
-    };
-    auto u64_at = [&](uint64_t key, uint64_t idx) { return mix(key + idx * 0x9e3779b97f4a7c15ULL); };
+    auto u64_at = [](uint64_t key, uint64_t idx) { return host_mix64(key + idx * 0x9e3779b97f4a7c15ULL); };
     for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j) {
             if (i == j || !(er_.p > 0.0)) continue;
@@ -349,6 +385,9 @@ void Engine::run_tiny(int t0, int steps, uint32_t* raster, double* trace, bool h
     a.w_max = w_max_;
     a.spike_count = d_spikes_.as<unsigned long long>();
     a.d_step = d_step_.as<int32_t>();
+    a.abm = abm_ ? 1 : 0;
+    a.fire_p = any_stochastic_ ? d_firep_.as<double>() : nullptr;
+    a.agent_key = any_stochastic_ ? d_akey_.as<uint64_t>() : nullptr;
     const size_t limit = static_cast<size_t>(tiny_max_smem());
     const int words = std::max(nl_words_, 1);
     const int table = static_cast<int>(hs_off_.size()) - 1;  // steps covered by the stimulus CSR
@@ -438,10 +477,21 @@ void Engine::validate() const {
             }
         }
     }
-    throw_first("mat_init", out);
+    if (abm_) {  // AbmWorld reports the first violation only (abm_engine.cpp:14-17, 79)
+        if (!out.empty()) throw InvalidArgument("abm world: " + out.front());
+    } else {
+        throw_first("mat_init", out);
+    }
+    if (!abm_)
+        for (size_t i = 0; i < fire_p_.size(); ++i)
+            if (fire_p_[i] != 1.0)
+                throw InvalidArgument("mat_init: homogeneous backend supports \"lif\" only; neuron " +
+                                      std::to_string(i) + " has a stochastic behavior (fire probability " +
+                                      fmt_double(fire_p_[i]) + ")");
+    if (abm_ && stdp_on_) throw LogicError("abm world: the agent-based engine has no plasticity");
     for (size_t i = 0; i < st_neuron_.size(); ++i)
         if (st_neuron_[i] < 0 || st_neuron_[i] >= n)
-            throw InvalidArgument("mat_run: stimulus[" + std::to_string(i) + "]: neuron id " +
+            throw InvalidArgument(run_name() + ": stimulus[" + std::to_string(i) + "]: neuron id " +
                                   std::to_string(st_neuron_[i]) + " out of range (" + std::to_string(n) +
                                   " neurons)");
 }
@@ -452,7 +502,9 @@ void Engine::setup() {
     cuda_check(cudaSetDevice(opt_.device), "cudaSetDevice");
     validate();
     n_ = static_cast<int32_t>(thr_.size());
-    if (n_ < 1) throw InvalidArgument("mat_init: the network has no neurons");
+    if (n_ < 1) throw InvalidArgument(std::string(abm_ ? "abm world" : "mat_init") + ": the network has no neurons");
+    if (!fire_p_.empty()) fire_p_.resize(static_cast<size_t>(n_), 1.0);
+    any_stochastic_ = abm_ && std::any_of(fire_p_.begin(), fire_p_.end(), [](double p) { return p < 1.0; });
     partition(n_, opt_.rank, opt_.world, &first_, &nl_);
     {
         int32_t f0, c0;
@@ -803,7 +855,15 @@ void Engine::alloc_state() {
     cuda_check(cudaMemsetAsync(d_step_.p, 0, 8, stream_), "memset");
     cuda_check(cudaMemsetAsync(d_spikes_.p, 0, 16, stream_), "memset");
     d_uexact_.alloc(static_cast<size_t>(std::max(nl_, 1)) * 8);
-    launch_prologue(d_uexact_.as<double>(), d_v_.as<double>(), d_leak_.as<double>(), d_reset_.as<double>(), nl_, stream_);
+    launch_prologue(d_uexact_.as<double>(), d_v_.as<double>(), d_leak_.as<double>(), d_reset_.as<double>(), nl_, abm_,
+                    stream_);
+    if (any_stochastic_) {  // per-neuron fire probabilities and agent stream keys of this partition
+        std::vector<double> fp(fire_p_.begin() + first_, fire_p_.begin() + first_ + nl_);
+        std::vector<uint64_t> key(static_cast<size_t>(nl_));
+        for (int j = 0; j < nl_; ++j) key[j] = agent_stream_key(seed_, static_cast<uint64_t>(first_ + j));
+        upload(d_firep_, fp);
+        upload(d_akey_, key);
+    }
 }
 
 void Engine::plan_launches() {
@@ -986,6 +1046,9 @@ NeuronArgs Engine::neuron_args(int t_base, int rows, uint32_t* raster, double* t
     a.raster_rows = rows;
     a.trace = trace;
     a.spike_count = d_spikes_.as<unsigned long long>();
+    a.abm = abm_ ? 1 : 0;
+    a.fire_p = any_stochastic_ ? d_firep_.as<double>() : nullptr;
+    a.agent_key = any_stochastic_ ? d_akey_.as<uint64_t>() : nullptr;
     if (p2p_) {
         a.peer_bits = d_peer_bits_.as<uint32_t* const>();
         a.peer_flags = d_peer_flags_.as<int32_t* const>();
@@ -1053,6 +1116,7 @@ DenseArgs Engine::dense_args() {
     a.u_exact = d_uexact_.as<double>();
     a.d_step = d_step_.as<int32_t>();
     a.work = ((dynamic_sched_ || tma_) && !exact_ && !persistent_) ? d_work_.as<int32_t>() : nullptr;
+    a.abm = abm_ ? 1 : 0;
     return a;
 }
 
@@ -1088,6 +1152,7 @@ void Engine::launch_sweep_only() {
         a.reset = d_reset_.as<double>();
         a.u_exact = d_uexact_.as<double>();
         a.d_step = d_step_.as<int32_t>();
+        a.abm = abm_ ? 1 : 0;
         if (nl_ == 0) launch_step_bump(a.d_step, stream_);
         else launch_sparse(a, f64_, stdp_on_, hbits_, sub_, exact_, sparse_gx_, stream_);
     }
@@ -1226,7 +1291,7 @@ void Engine::flush_pending() {
 
 void Engine::simulate(int32_t steps) {
     require_setup("sn_simulate");
-    if (steps < 1) throw InvalidArgument("mat_run: steps must be >= 1");
+    if (steps < 1) throw InvalidArgument(run_name() + ": steps must be >= 1");
     if (opt_.world > 1 && !comm_ && !p2p_)
         throw LogicError("sn_simulate: partitioned engine needs sn_comm_init or sn_p2p_open "
                          "(or use sn_step_local/sn_step_finish)");

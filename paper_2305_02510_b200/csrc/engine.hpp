@@ -84,6 +84,8 @@ public:
     void set_stdp(int32_t window, const double* ap, const double* am, double wmin, double wmax);
     void generate_er(int32_t n, double p, uint64_t seed, double weight, int32_t delay_max,
                      uint64_t delay_stream, int32_t by_syn, int32_t stdp);
+    void set_seed(uint64_t seed);
+    void set_fire_probability(int64_t first, int64_t count, const double* p);
     void setup();
     void simulate(int32_t steps);
     void synchronize();
@@ -155,6 +157,15 @@ private:
     bool generated_ = false;
     ErArgs er_{};
     int32_t er_delay_max_ = 1;
+
+    // agent-based mode (sn_options.mode == SN_MODE_ABM)
+    bool abm_ = false;
+    uint64_t seed_ = 0;
+    std::vector<double> fire_p_;  // per neuron; empty = all "lif"
+    bool any_stochastic_ = false;
+    DevBuf d_firep_, d_akey_;
+    static uint64_t agent_stream_key(uint64_t seed, uint64_t agent);
+    std::string run_name() const { return abm_ ? "abm_run" : "mat_run"; }
 
     // ---- derived layout ----
     int32_t n_ = 0, first_ = 0, nl_ = 0, part_ = 0;

@@ -44,6 +44,14 @@ __device__ __forceinline__ uint64_t below_at(uint64_t key, uint64_t idx, uint64_
     return __umul64hi(u64_at(key, idx), n);
 }
 
+// StochasticLifBehavior gate (abm_engine.cpp:34-39): the first unit draw of
+// RandomStream(seed, agent stream, id, step); `key` = the stream key before
+// the step mix (rng.hpp:19-24), precomputed per neuron on the host.
+__device__ __forceinline__ bool agent_fires(uint64_t key, int t, double p) {
+    const uint64_t k = mix64(key ^ static_cast<uint64_t>(t));
+    return static_cast<double>(mix64(k) >> 11) * 0x1.0p-53 < p;
+}
+
 // leak_toward (model.hpp:127-138), literally.
 __device__ __forceinline__ double leak_toward(double v, double leak, double reset) {
     const double d = v - reset;
@@ -132,9 +140,9 @@ __device__ __forceinline__ void neuron_step(const NeuronArgs& a, const HistArgs&
     if (valid) {
         double v = a.v[j];
         const double reset = a.reset[j];
-        double u;
+        double u;  // MAT: leak(v) + input; ABM: the synaptic input alone
         if (EXACT) {
-            u = a.u_exact[j];  // leak(v) + sum in ascending pre order, from the sweep
+            u = a.u_exact[j];  // (leak(v) +) sum in ascending pre order, from the sweep
         } else {
             // chunk partials: 8 independent loads in flight, fixed-order combine
             double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -145,7 +153,7 @@ __device__ __forceinline__ void neuron_step(const NeuronArgs& a, const HistArgs&
             }
             for (int k = 0; c < a.nchunks; ++c, ++k) acc[k] += __ldcg(a.partial + static_cast<int64_t>(c) * a.nl + j);
             const double in = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-            u = leak_toward(v, a.leak[j], reset) + in;
+            u = a.abm ? in : leak_toward(v, a.leak[j], reset) + in;
         }
         // external stimulus: the step's entries pre-summed in list order
         // (mat_engine.cpp:271-275); u += ext only when the step has any (179-180)
@@ -164,7 +172,13 @@ __device__ __forceinline__ void neuron_step(const NeuronArgs& a, const HistArgs&
                 u += ext;
             }
         }
+        // ABM: input = pending + ext, u = leak(v) + input (abm_engine.cpp:150-154, 24)
+        if (a.abm) u = leak_toward(v, a.leak[j], reset) + u;
         s = u > a.thr[j];
+        if (s && a.fire_p) {
+            const double p = a.fire_p[j];
+            if (p < 1.0) s = agent_fires(a.agent_key[j], t, p);
+        }
         const int c = a.cnt[j];
         if (c > 0) {  // refractory: silent, held at reset (185-189)
             s = false;
@@ -271,9 +285,9 @@ __global__ void __launch_bounds__(kThreads) k_hist(HistArgs h) {
 }
 
 __global__ void k_prologue(double* u, const double* v, const double* leak, const double* reset,
-                           int nl) {
+                           int nl, int abm) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < nl) u[j] = leak_toward(v[j], leak[j], reset[j]);
+    if (j < nl) u[j] = abm ? 0.0 : leak_toward(v[j], leak[j], reset[j]);
 }
 
 __global__ void k_step_bump(int32_t* d_step) { *d_step += 1; }
@@ -351,7 +365,7 @@ __global__ void __launch_bounds__(kThreads) k_dense_sweep(DenseArgs a) {
             const bool ok = in_tile && (c0 + k) < a.nl;
             sj[k] = ok && STDP ? bit_of(a.bits, gc[k]) : false;
             depj[k] = ok && STDP ? dep[gc[k]] : WT(0);
-            acc[k] = (EXACT && ok) ? leak_toward(a.v[c0 + k], a.leak[c0 + k], a.reset[c0 + k]) : 0.0;
+            acc[k] = (EXACT && ok && !a.abm) ? leak_toward(a.v[c0 + k], a.leak[c0 + k], a.reset[c0 + k]) : 0.0;
         }
 
         for (int sa = r0; sa < r1; sa += kSubRows) {
@@ -1008,6 +1022,8 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
     const double rst = own ? a.reset[j] : 0.0;
     const int32_t refr = own ? a.refr[j] : 0;
     int32_t cnt = own ? a.cnt[j] : 0;
+    const double fire_p = (own && a.fire_p) ? a.fire_p[j] : 1.0;
+    const uint64_t akey = fire_p < 1.0 ? a.agent_key[j] : 0ull;
     for (int k = 0; k < a.hw; ++k) {
         const uint64_t x = own ? a.hist[static_cast<int64_t>(k) * n + j] : 0ull;
         hist[(2 * k) * np + j] = static_cast<uint32_t>(x);
@@ -1046,7 +1062,8 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
         if (own) {
             // (1) leak, incoming list in ascending pre order (bit d-1 = s_pre[t-d]),
             // the step's stimulus, threshold, refractory (mat_engine.cpp:160-198)
-            double u = leak_toward(v, leak, rst);
+            // MAT: u = leak(v) + w...; ABM: pending = 0.0 + w..., u = leak(v) + (pending + ext)
+            double u = a.abm ? 0.0 : leak_toward(v, leak, rst);
 #pragma unroll 4
             for (uint32_t q = q0; q < q1; ++q) {
                 const uint32_t mq = meta[q];
@@ -1063,7 +1080,9 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
                 }
                 u += ext;
             }
+            if (a.abm) u = leak_toward(v, leak, rst) + u;
             fired = u > thr;
+            if (fired && fire_p < 1.0) fired = agent_fires(akey, t0 + s, fire_p);
             if (cnt > 0) {
                 fired = false;
                 cnt -= 1;
@@ -1525,7 +1544,7 @@ __global__ void __launch_bounds__(kThreads) k_sparse_exact(SparseArgs a) {
         const int gp = a.first + p;
         const bool sp = STDP ? bit_of(a.bits, gp) : false;
         const WT depp = STDP ? dep[gp] : WT(0);
-        double acc = leak_toward(a.v[p], a.leak[p], a.reset[p]);
+        double acc = a.abm ? 0.0 : leak_toward(a.v[p], a.leak[p], a.reset[p]);
         for (int b = 0; b < a.nblocks; ++b) {
             const int64_t beg = a.off[static_cast<int64_t>(b) * a.nl + p];
             const int64_t end = a.off[static_cast<int64_t>(b) * a.nl + p + 1];
@@ -1716,9 +1735,9 @@ void launch_hist(const HistArgs& h, cudaStream_t s) {
 }
 
 void launch_prologue(double* u, const double* v, const double* leak, const double* reset, int nl,
-                     cudaStream_t s) {
+                     bool abm, cudaStream_t s) {
     if (nl <= 0) return;
-    k_prologue<<<(nl + 255) / 256, 256, 0, s>>>(u, v, leak, reset, nl);
+    k_prologue<<<(nl + 255) / 256, 256, 0, s>>>(u, v, leak, reset, nl, abm ? 1 : 0);
     check(cudaGetLastError(), "k_prologue");
 }
 

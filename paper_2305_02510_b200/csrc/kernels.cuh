@@ -55,6 +55,12 @@ struct NeuronArgs {
     uint32_t* done;               // CTA completion counter of this launch
     int32_t rank;
     int32_t world;
+    // agent-based mode (abm_engine.cpp:146-189): u = leak(v) + (pending + ext),
+    // where pending is the synaptic input summed from 0.0; stochastic firing
+    // gate unit(seed, agent, step) < fire_p for fire_p < 1 (null: all "lif")
+    int32_t abm;
+    const double* fire_p;         // [nl] or null
+    const uint64_t* agent_key;    // [nl] RandomStream(seed, agent stream, id) key before the step mix
 };
 
 struct HistArgs {
@@ -111,6 +117,7 @@ struct DenseArgs {
     double* u_exact;           // [nl]
     int32_t* d_step;
     int32_t* work;             // dynamic item counter (null: static striding)
+    int32_t abm;               // exact mode seeds the accumulator with 0.0 instead of leak(v)
 };
 
 struct SparseArgs {
@@ -138,6 +145,7 @@ struct SparseArgs {
     const double* reset;
     double* u_exact;
     int32_t* d_step;
+    int32_t abm;               // exact mode seeds the accumulator with 0.0 instead of leak(v)
 };
 
 // ---- launchers (kernels.cu) ----
@@ -155,7 +163,7 @@ void launch_dense_tma(const DenseArgs& a, bool stdp, int grid, cudaStream_t s);
 void launch_sparse(const SparseArgs& a, bool f64, bool stdp, int hbits, int sub, bool exact,
                    int grid_x, cudaStream_t s);
 void launch_prologue(double* u_exact, const double* v, const double* leak, const double* reset,
-                     int nl, cudaStream_t s);
+                     int nl, bool abm, cudaStream_t s);
 void launch_step_bump(int32_t* d_step, cudaStream_t s);
 int sparse_block_pres(int hbits);
 // persistent cooperative step loop for small dense nets (single partition)
@@ -209,6 +217,10 @@ struct TinyArgs {
     double* trace;             // [steps][n] or null
     unsigned long long* spike_count;
     int32_t* d_step;
+    // agent-based mode (see NeuronArgs)
+    int32_t abm;
+    const double* fire_p;      // [n] or null
+    const uint64_t* agent_key; // [n]
 };
 size_t tiny_smem_bytes(const TinyArgs& a);
 int tiny_max_smem();

@@ -25,7 +25,7 @@ class MatEngine:
                  precision: str = "f32", exact_order: bool = False,
                  record_membrane: bool = False, stream_io: bool = False,
                  use_graphs: bool = True, rank: int = 0, world: int = 1,
-                 profile: bool = False, persistent: bool = True):
+                 profile: bool = False, persistent: bool = True, mode: str = "mat"):
         o = _capi.Options()
         check(lib.sn_options_init(C.byref(o)))
         o.device = device
@@ -39,6 +39,9 @@ class MatEngine:
         o.world = world
         o.profile = 1 if profile else 0
         o.persistent = 0 if persistent else -1
+        if mode not in ("mat", "abm"):
+            raise ValueError(f'unknown engine mode "{mode}" (expected "mat" or "abm")')
+        o.mode = _capi.SN_MODE_ABM if mode == "abm" else _capi.SN_MODE_MAT
         h = C.c_void_p()
         check(lib.sn_engine_create(C.byref(o), C.byref(h)))
         self._h = h
@@ -111,6 +114,14 @@ class MatEngine:
         check(lib.sn_generate_erdos_renyi(self._h, int(n), float(p), int(seed) & ((1 << 64) - 1),
                                           float(weight), int(delay_max), int(delay_stream),
                                           1 if delay_by_synapse_index else 0, 1 if stdp else 0))
+
+    # ---- agent-based mode ----
+    def set_seed(self, seed: int):
+        check(lib.sn_set_seed(self._h, int(seed) & ((1 << 64) - 1)))
+
+    def set_fire_probability(self, fire_probability, first: int = 0):
+        fp = _c(fire_probability, np.float64)
+        check(lib.sn_set_fire_probability(self._h, int(first), len(fp), ptr(fp, C.c_double)))
 
     def setup(self):
         check(lib.sn_setup(self._h))

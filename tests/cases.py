@@ -13,7 +13,9 @@ from paper_2305_02510_b200.netgen import RandomStream, erdos_renyi_arrays
 
 class Case:
     def __init__(self, name, net, steps, stim=None, stdp=None, record=False, lower=False,
-                 cite=""):
+                 cite="", seed=0, fire_p=None):
+        self.seed = seed        # SimulationConfig::seed (agent-based cases)
+        self.fire_p = fire_p    # per-neuron fire probability (agent-based cases), None = all lif
         self.name = name
         self.net = net
         self.steps = steps
@@ -203,4 +205,87 @@ def crit7_cases():
         refr = RandomStream(seed, 0x72656672).below_np(np.arange(20, dtype=np.uint64), 5).astype(np.int32)
         net = NetworkDef.from_arrays(np.ones(20), np.zeros(20), np.zeros(20), refr, pre, post, np.ones(len(pre)))
         out.append(Case(f"crit7_seed{seed}", net, 400, periodic_drive(20, 400, 3, 5, 2.0, seed)))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Agent-based (abm_run) cases: each restates a test of
+# proj/tests/test_abm_engine.cpp, plus float-weight nets (where the ABM
+# summation order, leak(v) + (pending + ext), differs from MAT's) and
+# heterogeneous stochastic behaviours.
+def _fire_mix(n, seed, choices=(0.0, 0.25, 0.5, 0.8, 1.0), frac=0.5):
+    rng = np.random.default_rng(seed)
+    fp = np.where(rng.random(n) < frac, rng.choice(np.array(choices), n), 1.0)
+    return fp.astype(np.float64)
+
+
+def float_abm_net(n, p, seed, max_delay=4, max_axonal=1):
+    """Float weights/thresholds/leaks so the summation order is observable."""
+    rs = RandomStream(seed, 0x61626D666C74)
+    pre, post = erdos_renyi_arrays(n, p, seed)
+    m = len(pre)
+    k = np.arange(m, dtype=np.uint64)
+    w = -0.15 + 0.75 * rs.unit_np(k)
+    d = (1 + rs.below_np(k + np.uint64(m), max_delay)).astype(np.int32)
+    kn = np.arange(n, dtype=np.uint64) + np.uint64(3 * m)
+    thr = 0.6 + 0.5 * rs.unit_np(kn)
+    leak = 0.01 + 0.1 * rs.unit_np(kn + np.uint64(n))
+    reset = -0.1 + 0.2 * rs.unit_np(kn + np.uint64(2 * n))
+    refr = rs.below_np(kn + np.uint64(3 * n), 3).astype(np.int32)
+    ax = rs.below_np(kn + np.uint64(4 * n), max_axonal + 1).astype(np.int32)
+    return NetworkDef.from_arrays(threshold=thr, leak=leak, reset=reset, refractory=refr, pre=pre,
+                                  post=post, weight=w, delay=d, axonal_delay=ax)
+
+
+def float_stim(n, steps, count, seed):
+    rs = RandomStream(seed, 0x61626D7374)
+    k = np.arange(count, dtype=np.uint64)
+    st = rs.below_np(k, steps).astype(np.int32)
+    nr = rs.below_np(k + np.uint64(count), n).astype(np.int32)
+    am = 0.2 + 1.3 * rs.unit_np(k + np.uint64(2 * count))
+    return _sched([(int(a), int(b), float(c)) for a, b, c in zip(st, nr, am)])
+
+
+def abm_cases():
+    out = []
+    c = "test_abm_engine.cpp"
+    out.append(Case("abm_chain", two_neuron_chain(2.0), 5, kick(), cite=f"{c}:38-42"))
+    out.append(Case("abm_delay3", two_neuron_chain(2.0, 3), 8, kick(), cite=f"{c}:44-48"))
+    net = two_neuron_chain(2.0, 1)
+    net.neurons[0].axonal_delay = 2
+    out.append(Case("abm_axonal2", net, 8, kick(), cite=f"{c}:50-55"))
+    out.append(Case("abm_same_step", two_neuron_chain(5.0), 3, kick(), cite=f"{c}:57-63"))
+    net = NetworkDef()
+    net.neurons = [NeuronParams() for _ in range(5)]
+    out.append(Case("abm_two_phase", net, 1, _sched([(0, j, 2.0) for j in (0, 1, 3, 4)]),
+                    cite=f"{c}:65-73"))
+    for seed in range(500, 540, 3):
+        net = random_net(seed)
+        out.append(Case(f"abm_rand_{seed}", net, 150, random_stim(seed, net.neuron_count(), 150, 50),
+                        cite=f"{c}:75-85"))
+    for seed in range(600, 630, 3):
+        net = random_net(seed, max_neurons=15, edge_prob=0.35, max_delay=5, max_axonal=2)
+        out.append(Case(f"abm_delay_{seed}", net, 120, random_stim(seed, net.neuron_count(), 120, 50),
+                        cite=f"{c}:87-98"))
+    net = random_net(900)
+    fp = np.ones(net.neuron_count())
+    fp[::2] = 1.0  # "always_fires_when_above" = StochasticLif(1.0): identical to lif
+    out.append(Case("abm_p1_degenerate", net, 100, random_stim(900, net.neuron_count(), 100, 40),
+                    fire_p=fp, cite=f"{c}:100-111"))
+    out.append(Case("abm_p0_never", two_neuron_chain(5.0), 10, kick(), fire_p=np.array([1.0, 0.0]),
+                    cite=f"{c}:113-120"))
+    drive = _sched([(t, 0, 2.0) for t in range(100)])
+    for seed in (9, 10):
+        out.append(Case(f"abm_seeded_{seed}", two_neuron_chain(2.0), 100, drive, seed=seed,
+                        fire_p=np.array([1.0, 0.5]), cite=f"{c}:122-141"))
+    for seed in range(40, 46):
+        net = random_net(seed, max_neurons=30, edge_prob=0.3, max_delay=4, max_axonal=2)
+        out.append(Case(f"abm_stoch_{seed}", net, 200, random_stim(seed, net.neuron_count(), 200, 150),
+                        seed=seed * 1000 + 7, fire_p=_fire_mix(net.neuron_count(), seed),
+                        record=True, cite="heterogeneous stochastic behaviours"))
+    for seed, n, p in ((1, 40, 0.3), (2, 64, 0.2), (3, 100, 0.1), (4, 33, 1.0)):
+        net = float_abm_net(n, p, seed)
+        out.append(Case(f"abm_float_{seed}", net, 200, float_stim(n, 200, 6 * n, seed), seed=seed,
+                        fire_p=_fire_mix(n, seed + 100, frac=0.3), record=True,
+                        cite="float nets: leak(v) + (pending + ext) order"))
     return out

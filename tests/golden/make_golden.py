@@ -57,6 +57,51 @@ def dump_suite(fname, cases):
     print(f"{fname}: {len(cases)} cases")
 
 
+def dump_abm_suite(fname, cases):
+    """abm_run of the reference (stochastic behaviours registered through its
+    own registry): raster, final membrane and, when asked, the trace."""
+    out = {}
+    for c in cases:
+        r = B.run_ref_abm_full(c.arrays(), c.steps, c.stim_arrays(), seed=c.seed, fire_p=c.fire_p,
+                               record_membrane=c.record)
+        out[f"{c.name}/steps"] = r["steps"]
+        out[f"{c.name}/neurons"] = r["neurons"]
+        out[f"{c.name}/membrane"] = r["membrane"]
+        if "membrane_trace" in r:
+            out[f"{c.name}/trace"] = r["membrane_trace"]
+    np.savez_compressed(os.path.join(HERE, fname), **out)
+    print(f"{fname}: {len(cases)} cases")
+
+
+def abm_scale_case():
+    """ER(1000, 0.1, seed 3), delays 1..8 (synapse-index keyed), every other
+    neuron "stochastic_lif", paper stimulus, 500 steps, run seed 77."""
+    n, steps = 1000, 500
+    arrays, stim = scenario(n, 0.1, 3, steps, 8)
+    fp = np.ones(n)
+    fp[1::2] = 0.5
+    return arrays, stim, fp, steps, 77
+
+
+def main_abm():
+    B.build(ref=True)
+    dump_abm_suite("abm.npz", CS.abm_cases())
+    path = os.path.join(HERE, "scale.json")
+    with open(path) as f:
+        scale = json.load(f)
+    arrays, stim, fp, steps, seed = abm_scale_case()
+    t0 = time.time()
+    r = B.run_ref_abm_full(arrays, steps, stim, seed=seed, fire_p=fp)
+    scale["abm_er1000_stoch"] = {"n": 1000, "p": 0.1, "net_seed": 3, "delay_max": 8, "steps": steps,
+                                 "run_seed": seed, "spikes": int(len(r["steps"])),
+                                 "digest": raster_digest(r["steps"], r["neurons"]),
+                                 "membrane_sum": float(np.sum(r["membrane"])), "ref_path": "abm_run",
+                                 "ref_seconds": round(time.time() - t0, 3)}
+    print("abm scale", scale["abm_er1000_stoch"])
+    with open(path, "w") as f:
+        json.dump(scale, f, indent=1)
+
+
 def scenario(n, p, seed, steps, delay_max=1):
     pre, post = erdos_renyi_arrays(n, p, seed)
     arrays = {"threshold": np.ones(n), "leak": np.zeros(n), "reset": np.zeros(n),
@@ -127,4 +172,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--abm" in sys.argv:   # agent-based fixtures only (abm.npz + scale.json abm entries)
+        main_abm()
+    else:
+        main()
+        main_abm()

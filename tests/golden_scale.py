@@ -29,3 +29,14 @@ def scenario_problem(entry: dict):
         stdp = (d.window, np.array(d.a_plus), np.array(d.a_minus), d.w_min, d.w_max)
     stim = scenario_stimulus(n, steps, seed).to_arrays()
     return arrays, stim, stdp, steps
+
+
+def abm_scale_problem(entry: dict):
+    """scale.json "abm_er1000_stoch" (tests/golden/make_golden.py abm_scale_case):
+    ER(n, p, net_seed) with synapse-index keyed delays, every other neuron
+    "stochastic_lif" (p = 0.5), paper stimulus, run seed `run_seed`."""
+    arrays, stim, _, steps = scenario_problem({"n": entry["n"], "p": entry["p"], "seed": entry["net_seed"],
+                                               "steps": entry["steps"], "delay_max": entry["delay_max"]})
+    fp = np.ones(entry["n"])
+    fp[1::2] = 0.5
+    return arrays, stim, fp, steps, entry["run_seed"]

@@ -28,7 +28,9 @@ def test_gen_run_compare(tmp_path):
     r = cli("gen", "--neurons", "60", "--prob", "0.3", "--seed", "4", "--steps", "300",
             "--out", net_p, "--stimulus-out", stim_p)
     assert r.returncode == 0, r.stderr
-    for backend in ("gpu", "gpu-sparse", "gpu-exact"):
+    # gpu-abm: the agent-based mode agrees with the matrix backends on lif nets
+    # (test_abm_engine.cpp:75-85)
+    for backend in ("gpu", "gpu-sparse", "gpu-exact", "gpu-abm"):
         r = cli("run", "--network", net_p, "--stimulus", stim_p, "--steps", "300", "--backend", backend,
                 "--out", out_p)
         assert r.returncode == 0, r.stderr
@@ -43,7 +45,7 @@ def test_gen_run_compare(tmp_path):
         if B.ref_has_io():
             assert mine == B.ref_write_raster(o["steps"], o["neurons"])
     r = cli("compare", "--network", net_p, "--stimulus", stim_p, "--steps", "300",
-            "--backends", "gpu,gpu-sparse,gpu-exact", "--against", out_p)
+            "--backends", "gpu,gpu-sparse,gpu-exact,gpu-abm,gpu-abm-fast", "--against", out_p)
     assert r.returncode == 0 and r.stdout.strip() == "identical", r.stdout + r.stderr
     # a raster with one spike removed diverges: exit code 1
     lines = open(out_p).read().splitlines()

@@ -182,3 +182,78 @@ def test_shim_loop_equals_mat_run():
             r = B.run_ref_mat(a, 100, st, storage=storage)
             q = B.run_ref_mat_raster(a, 100, st, storage=storage)
             assert np.array_equal(r["steps"], q["steps"]) and np.array_equal(r["neurons"], q["neurons"])
+
+
+# ---------------------------------------------------------------------------
+# agent-based mode: oracle/abm_oracle.c vs the reference's abm_run
+def test_abm_oracle_matches_reference_goldens():
+    """abm.npz: the reference's abm_run (stochastic behaviours registered in
+    its own registry) on every case of cases.abm_cases(); the C restatement
+    must reproduce rasters, final membranes and traces bit for bit."""
+    g = _gold("abm.npz")
+    for c in CS.abm_cases():
+        o = B.run_abm_oracle(c.arrays(), c.steps, c.stim_arrays(), seed=c.seed, fire_p=c.fire_p,
+                             record_membrane=c.record)
+        assert np.array_equal(o["steps"], g[f"{c.name}/steps"]), c.name
+        assert np.array_equal(o["neurons"], g[f"{c.name}/neurons"]), c.name
+        assert np.array_equal(o["membrane"], g[f"{c.name}/membrane"]), c.name
+        if c.record:
+            assert np.array_equal(o["membrane_trace"], g[f"{c.name}/trace"]), c.name
+
+
+def test_abm_kat_literal_values():
+    """The literal expectations of test_abm_engine.cpp, from the goldens."""
+    g = _gold("abm.npz")
+
+    def pairs(name):
+        return list(zip(g[f"{name}/steps"].tolist(), g[f"{name}/neurons"].tolist()))
+
+    assert pairs("abm_chain") == [(0, 0), (1, 1)]                      # :38-42
+    assert pairs("abm_delay3") == [(0, 0), (3, 1)]                     # :44-48
+    assert pairs("abm_axonal2") == [(0, 0), (3, 1)]                    # :50-55
+    assert pairs("abm_same_step") == [(0, 0), (1, 1)]                  # :57-63
+    assert pairs("abm_two_phase") == [(0, 0), (0, 1), (0, 3), (0, 4)]  # :65-73
+    assert pairs("abm_p0_never") == [(0, 0)]                           # :113-120
+    a, b = pairs("abm_seeded_9"), pairs("abm_seeded_10")               # :122-141
+    assert a != b
+    fires = sum(1 for _, j in a if j == 1)
+    assert 20 < fires < 80
+
+
+def test_abm_float_order_differs_from_mat():
+    """On float nets the agent step sums leak(v) + (pending + ext) while MAT
+    sums ((leak(v) + w...) + ext): the two modes are distinguishable, so the
+    ABM parity tests do check the ABM order."""
+    c = [c for c in CS.abm_cases() if c.name == "abm_float_1"][0]
+    a = c.arrays()
+    abm = B.run_abm_oracle(a, c.steps, c.stim_arrays(), record_membrane=True)
+    mat = B.run_oracle(a, c.steps, c.stim_arrays(), None, True)
+    assert not np.array_equal(abm["membrane_trace"], mat["membrane_trace"])
+    assert np.allclose(abm["membrane_trace"], mat["membrane_trace"], rtol=0, atol=1e-9)
+
+
+def test_abm_scale_golden():
+    """ER(1000, 0.1), delays 1..8, half the neurons stochastic_lif, 500 steps."""
+    with open(os.path.join(GOLD, "scale.json")) as f:
+        sc = json.load(f)["abm_er1000_stoch"]
+    from golden_scale import abm_scale_problem
+    arrays, stim, fp, steps, seed = abm_scale_problem(sc)
+    o = B.run_abm_oracle(arrays, steps, stim, seed=seed, fire_p=fp)
+    assert len(o["steps"]) == sc["spikes"]
+    assert digest(o["steps"], o["neurons"]) == sc["digest"]
+    assert float(np.sum(o["membrane"])) == sc["membrane_sum"]
+
+
+@pytest.mark.skipif(not B.ref_available(), reason="oracle/_ref not built")
+def test_abm_oracle_matches_live_reference_random():
+    """Fresh seeds and probabilities outside the golden set."""
+    from support import random_net, random_stim
+    for seed in range(2000, 2010):
+        net = random_net(seed, max_neurons=40, edge_prob=0.3, max_delay=6, max_axonal=3)
+        n = net.neuron_count()
+        fp = CS._fire_mix(n, seed, choices=(0.1, 0.33, 0.5, 0.9), frac=0.6)
+        st = random_stim(seed, n, 160, 120).to_arrays()
+        o = B.run_abm_oracle(net.to_arrays(), 160, st, seed=seed, fire_p=fp, record_membrane=True)
+        r = B.run_ref_abm_full(net.to_arrays(), 160, st, seed=seed, fire_p=fp, record_membrane=True)
+        assert np.array_equal(o["steps"], r["steps"]) and np.array_equal(o["neurons"], r["neurons"])
+        assert np.array_equal(o["membrane_trace"], r["membrane_trace"])
