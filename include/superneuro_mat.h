@@ -94,10 +94,12 @@ typedef struct sn_options {
                                 float nets; slower).  0: fixed-order parallel
                                 reduction (deterministic; exact on integer nets). */
     int32_t record_membrane; /* SimulationConfig::record_membrane */
-    int32_t stream_io;       /* 1: per-step H2D of the step's stimulus and D2H of the
-                                step's spike bits through pinned host buffers (the
-                                end-to-end path).  0: stimulus table resident in HBM,
-                                raster kept in HBM until sn_get_raster. */
+    int32_t stream_io;       /* 1 (the end-to-end path): each sn_simulate copies its
+                                steps' stimulus rows H2D from pinned memory in one
+                                transfer, and the kernels store every step's spike
+                                words straight into pinned (mapped) host memory.
+                                0: stimulus table resident in HBM, raster staged in
+                                HBM and copied once per call. */
     int32_t use_graphs;      /* 1: replay the per-step kernels as a CUDA graph */
     int32_t rank;            /* post-neuron partition index (0 when world == 1) */
     int32_t world;           /* number of partitions / GPUs (1 = single GPU) */
@@ -128,6 +130,10 @@ typedef struct sn_stats {
     double sweep_bytes_total;   /* algorithmic bytes of all sweeps since reset */
     int32_t sweep_kernel;       /* sn_sweep_kernel of the plan chosen at sn_setup */
     int32_t sweep_ctas;         /* grid size of that kernel */
+    /* stream_io: host<->device bytes of the last sn_simulate (stimulus rows
+       H2D, spike words D2H; 0 when the inputs are resident) */
+    double h2d_bytes_last;
+    double d2h_bytes_last;
 } sn_stats;
 
 typedef enum sn_sweep_kernel {

@@ -65,6 +65,8 @@ class Stats(C.Structure):
         ("sweep_bytes_total", C.c_double),
         ("sweep_kernel", C.c_int32),
         ("sweep_ctas", C.c_int32),
+        ("h2d_bytes_last", C.c_double),
+        ("d2h_bytes_last", C.c_double),
     ]
 
     KERNEL_NAMES = {1: "k_dense_stream", 2: "k_dense_tma", 3: "k_dense_sweep<exact>",

@@ -424,6 +424,7 @@ void Engine::run_tiny(int t0, int steps, uint32_t* raster, double* trace, bool h
             a.st_off = soff;
             a.st_amp = samp;
             a.st_neuron = sneu;
+            stats_.h2d_bytes_last += static_cast<double>(ob + cnt * 12);
         } else {  // device-resident table from build_stimulus_table
             a.st_off = d_st_off_.as<int64_t>() + tt;
             a.st_neuron = d_st_neuron_.as<int32_t>();
@@ -870,7 +871,7 @@ void Engine::plan_launches() {
     int sms = 148;
     cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt_.device), "attr");
     const size_t esz = f64_ ? 8 : 4;
-    persistent_ = opt_.persistent >= 0 && dense_ && !exact_ && opt_.world == 1 && !opt_.stream_io && nl_ > 0 &&
+    persistent_ = opt_.persistent >= 0 && dense_ && !exact_ && opt_.world == 1 && nl_ > 0 &&
                   static_cast<double>(n_) * pitch_ * esz <= 64.0 * 1024 * 1024;  // L2-resident
     if (persistent_) {
         // 32-row chunks; split columns until the items fill the co-resident CTAs
@@ -1018,7 +1019,7 @@ void Engine::build_stimulus_table() {
 // ---- per-step launch sequence ----------------------------------------------
 NeuronArgs Engine::neuron_args(int t_base, int rows, uint32_t* raster, double* trace, const int64_t* st_off,
                                const int32_t* st_neuron, const double* st_amp, int32_t st_steps,
-                               int32_t st_stream) {
+                               int32_t st_base) {
     NeuronArgs a{};
     a.n = n_;
     a.first = first_;
@@ -1036,7 +1037,7 @@ NeuronArgs Engine::neuron_args(int t_base, int rows, uint32_t* raster, double* t
     a.st_neuron = st_neuron;
     a.st_amp = st_amp;
     a.st_steps = st_steps;
-    a.st_stream = st_stream;
+    a.st_base = st_base;
     a.d_step = d_step_.as<int32_t>();
     a.work = (dense_ && !exact_) ? d_work_.as<int32_t>() : nullptr;
     a.t_base = t_base;
@@ -1310,6 +1311,7 @@ void Engine::simulate(int32_t steps) {
         // written to pinned host memory by the kernel itself
         const size_t rwords = static_cast<size_t>(steps) * std::max(nl_words_, 1);
         uint32_t* raster;
+        stats_.h2d_bytes_last = 0.0;
         if (opt_.stream_io) {
             h_raster_.reserve(rwords * 4);
             raster = h_raster_.as<uint32_t>();
@@ -1336,71 +1338,50 @@ void Engine::simulate(int32_t steps) {
                        "raster D2H");
         cuda_check(cudaStreamSynchronize(stream_), "simulate sync");
         if (opt_.stream_io && !ch.words.empty()) std::memcpy(ch.words.data(), raster, ch.words.size() * 4);
-        raster_.push_back(std::move(ch));
-    } else if (opt_.stream_io) {
-        // pack each step's stimulus rows into pinned memory; copy per step
-        std::vector<size_t> pos(static_cast<size_t>(steps) + 1, 0);
-        size_t total = 0;
-        for (int s = 0; s < steps; ++s) {
-            const int t = t0 + s;
-            int64_t k = 0;
-            if (t + 1 < static_cast<int>(hs_off_.size())) k = hs_off_[t + 1] - hs_off_[t];
-            pos[s] = total;
-            if (k > 0) total += 16 + static_cast<size_t>(k) * 8 + round_up(static_cast<size_t>(k) * 4, 8);
-        }
-        pos[steps] = total;
-        h_stage_.reserve(std::max<size_t>(total, 64));
-        size_t max_chunk = 64;
-        for (int s = 0; s < steps; ++s) {
-            const int t = t0 + s;
-            const size_t sz = pos[s + 1] - pos[s];
-            if (!sz) continue;
-            max_chunk = std::max(max_chunk, sz);
-            const int64_t lo = hs_off_[t], k = hs_off_[t + 1] - lo;
-            uint8_t* base = h_stage_.as<uint8_t>() + pos[s];
-            int64_t* off = reinterpret_cast<int64_t*>(base);
-            off[0] = 0;
-            off[1] = k;
-            std::memcpy(base + 16, hs_amp_.data() + lo, static_cast<size_t>(k) * 8);
-            std::memcpy(base + 16 + k * 8, hs_neuron_.data() + lo, static_cast<size_t>(k) * 4);
-        }
-        if (d_stage_.bytes < max_chunk) d_stage_.alloc(max_chunk);
-        h_raster_.reserve(static_cast<size_t>(steps) * std::max(nl_words_, 1) * 4);
-        cuda_check(cudaEventRecord(eb, stream_), "rec");
-        for (int s = 0; s < steps; ++s) {
-            const size_t sz = pos[s + 1] - pos[s];
-            const int64_t* st_off = nullptr;
-            const int32_t* st_neuron = nullptr;
-            const double* st_amp = nullptr;
-            int32_t st_steps = 0;
-            if (sz) {
-                cuda_check(cudaMemcpyAsync(d_stage_.p, h_stage_.as<uint8_t>() + pos[s], sz, cudaMemcpyHostToDevice, stream_), "stim H2D");
-                const int64_t k = reinterpret_cast<const int64_t*>(h_stage_.as<uint8_t>() + pos[s])[1];
-                st_off = d_stage_.as<int64_t>();
-                st_amp = reinterpret_cast<const double*>(d_stage_.as<uint8_t>() + 16);
-                st_neuron = reinterpret_cast<const int32_t*>(d_stage_.as<uint8_t>() + 16 + k * 8);
-                st_steps = 1;
-            }
-            NeuronArgs na = neuron_args(t0, steps, nullptr, trace, st_off, st_neuron, st_amp, st_steps, 1);
-            enqueue_step(na, true);
-            if (nl_words_ > 0)
-                cuda_check(cudaMemcpyAsync(h_raster_.as<uint32_t>() + static_cast<size_t>(s) * nl_words_,
-                                           d_bits_.as<uint32_t>() + first_ / 32, static_cast<size_t>(nl_words_) * 4,
-                                           cudaMemcpyDeviceToHost, stream_), "raster D2H");
-        }
-        cuda_check(cudaEventRecord(ee, stream_), "rec");
-        cuda_check(cudaStreamSynchronize(stream_), "simulate sync");
-        RasterChunk ch;
-        ch.t0 = t0;
-        ch.rows = steps;
-        ch.words.assign(h_raster_.as<uint32_t>(), h_raster_.as<uint32_t>() + static_cast<size_t>(steps) * nl_words_);
+        if (opt_.stream_io) stats_.d2h_bytes_last = static_cast<double>(ch.words.size()) * 4;
         raster_.push_back(std::move(ch));
     } else {
-        const size_t rbytes = static_cast<size_t>(steps) * std::max(nl_words_, 1) * 4;
-        if (d_raster_.bytes < rbytes) d_raster_.alloc(rbytes);
-        NeuronArgs na = neuron_args(t0, steps, d_raster_.as<uint32_t>(), trace, d_st_off_.as<int64_t>(),
-                                    d_st_neuron_.as<int32_t>(), d_st_amp_.as<double>(), st_steps_dev_, 0);
+        // stream_io (the end-to-end path): this call's stimulus rows go H2D from
+        // pinned memory in one copy inside the timed region, and the kernels
+        // store every step's spike words straight into pinned host memory
+        // (mapped), so each step's result crosses to the host as it is made.
+        const size_t rwords = static_cast<size_t>(steps) * std::max(nl_words_, 1);
+        uint32_t* raster = nullptr;
+        const int64_t* st_off = d_st_off_.as<int64_t>();
+        const int32_t* st_neuron = d_st_neuron_.as<int32_t>();
+        const double* st_amp = d_st_amp_.as<double>();
+        int32_t st_rows = st_steps_dev_, st_base = 0;
         cuda_check(cudaEventRecord(eb, stream_), "rec");
+        if (opt_.stream_io) {
+            h_raster_.reserve(rwords * 4);
+            raster = h_raster_.as<uint32_t>();
+            const int table = static_cast<int>(hs_off_.size()) - 1;
+            st_rows = std::max(0, std::min(table - t0, steps));
+            st_base = t0;
+            const int64_t lo = st_rows > 0 ? hs_off_[t0] : 0, hi = st_rows > 0 ? hs_off_[t0 + st_rows] : 0;
+            const size_t cnt = static_cast<size_t>(hi - lo);
+            const size_t ob = round_up((static_cast<int64_t>(st_rows) + 1) * 8, 16);
+            const size_t bytes = ob + cnt * 12 + 16;
+            h_stage_.reserve(bytes);
+            uint8_t* hb = h_stage_.as<uint8_t>();
+            int64_t* soff = reinterpret_cast<int64_t*>(hb);
+            for (int r = 0; r <= st_rows; ++r) soff[r] = (st_rows > 0 ? hs_off_[t0 + r] : 0) - lo;
+            if (cnt) {
+                std::memcpy(hb + ob, hs_amp_.data() + lo, cnt * 8);
+                std::memcpy(hb + ob + cnt * 8, hs_neuron_.data() + lo, cnt * 4);
+            }
+            if (d_stage_.bytes < bytes) d_stage_.alloc(std::max(bytes, 2 * d_stage_.bytes));
+            cuda_check(cudaMemcpyAsync(d_stage_.p, hb, bytes, cudaMemcpyHostToDevice, stream_), "stim H2D");
+            uint8_t* db = d_stage_.as<uint8_t>();
+            st_off = reinterpret_cast<const int64_t*>(db);
+            st_amp = reinterpret_cast<const double*>(db + ob);
+            st_neuron = reinterpret_cast<const int32_t*>(db + ob + cnt * 8);
+            stats_.h2d_bytes_last = static_cast<double>(bytes);
+        } else {
+            if (d_raster_.bytes < rwords * 4) d_raster_.alloc(rwords * 4);
+            raster = d_raster_.as<uint32_t>();
+        }
+        NeuronArgs na = neuron_args(t0, steps, raster, trace, st_off, st_neuron, st_amp, st_rows, st_base);
         if (persistent_) {
             cudaEvent_t p0{}, p1{};
             if (opt_.profile) { p0 = get_event(); cuda_check(cudaEventRecord(p0, stream_), "rec"); }
@@ -1424,9 +1405,11 @@ void Engine::simulate(int32_t steps) {
         ch.t0 = t0;
         ch.rows = steps;
         ch.words.resize(static_cast<size_t>(steps) * nl_words_);
-        if (!ch.words.empty())
+        if (!opt_.stream_io && !ch.words.empty())
             cuda_check(cudaMemcpyAsync(ch.words.data(), d_raster_.p, ch.words.size() * 4, cudaMemcpyDeviceToHost, stream_), "raster D2H");
         cuda_check(cudaStreamSynchronize(stream_), "simulate sync");
+        if (opt_.stream_io && !ch.words.empty()) std::memcpy(ch.words.data(), raster, ch.words.size() * 4);
+        if (opt_.stream_io) stats_.d2h_bytes_last = static_cast<double>(ch.words.size()) * 4;
         raster_.push_back(std::move(ch));
     }
     float ms = 0.f;

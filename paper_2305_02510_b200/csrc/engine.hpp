@@ -126,7 +126,7 @@ private:
     void plan_launches();
     NeuronArgs neuron_args(int t_base, int rows, uint32_t* raster, double* trace,
                            const int64_t* st_off, const int32_t* st_neuron, const double* st_amp,
-                           int32_t st_steps, int32_t st_stream);
+                           int32_t st_steps, int32_t st_base);
     HistArgs hist_args();
     void launch_sweep();
     void launch_sweep_only();  // no launch accounting (graph capture counts in bulk)

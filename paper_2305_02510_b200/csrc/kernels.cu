@@ -157,8 +157,8 @@ __device__ __forceinline__ void neuron_step(const NeuronArgs& a, const HistArgs&
         }
         // external stimulus: the step's entries pre-summed in list order
         // (mat_engine.cpp:271-275); u += ext only when the step has any (179-180)
-        const int row = a.st_stream ? 0 : t;
-        if (row < a.st_steps) {
+        const int row = t - a.st_base;
+        if (row >= 0 && row < a.st_steps) {
             int64_t lo = a.st_off[row], hi = a.st_off[row + 1];
             if (hi > lo) {
                 const int gj = a.first + j;

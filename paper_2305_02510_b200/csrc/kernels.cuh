@@ -36,7 +36,7 @@ struct NeuronArgs {
     const int32_t* st_neuron;
     const double* st_amp;
     int32_t st_steps;          // number of steps covered by the table
-    int32_t st_stream;         // 1: table has one row (index 0) for the current step
+    int32_t st_base;           // step of table row 0 (row = t - st_base)
     // time
     int32_t* d_step;           // device step counter (read here; sweep increments)
     int32_t* work;             // sweep work counter, reset here (null: static schedule)
