@@ -145,8 +145,10 @@ typedef enum sn_sweep_kernel {
     SN_SWEEP_SPARSE_DICT = 6,   /* k_sparse_pull with the weight dictionary (4 B/synapse) */
     SN_SWEEP_SPARSE_STREAM = 7, /* k_sparse_stream: flat chunk stream per warp */
     SN_SWEEP_SPARSE_EXACT = 8,  /* k_sparse_exact: one thread per post, ascending pre */
-    SN_SWEEP_TINY = 9           /* k_tiny: whole call in one CTA, state in shared memory
+    SN_SWEEP_TINY = 9,          /* k_tiny: whole call in one CTA, state in shared memory
                                    (single partition, N <= 1024, lists fit in smem) */
+    SN_SWEEP_SPARSE_TMA = 10    /* k_sparse_tma: cp.async.bulk stream of uniform-weight
+                                   lists, hit bits + per-post prefix counts */
 } sn_sweep_kernel;
 
 /* ---- lifecycle ---------------------------------------------------------- */

@@ -182,6 +182,10 @@ private:
     std::vector<double> dict_;   // sparse weight dictionary (empty: weights stored per synapse)
     DevBuf d_wdict_;
     void upload_dict();
+    bool sparse_tma_ = false;  // k_sparse_tma stage plan (static uniform-weight lists)
+    DevBuf d_sp_stages_, d_sp_first_, d_sp_block_, d_sp_bnd_;
+    int32_t sp_ctas_ = 0;
+    bool build_sparse_tma_plan(int ctas);
     double sparse_weight(const std::vector<uint8_t>& host_w, const std::vector<uint32_t>& meta, int64_t q) const;
     // dense plan
     int32_t tile_w_ = 0, rows_per_chunk_ = 0, nchunks_ = 1, dense_grid_ = 1;

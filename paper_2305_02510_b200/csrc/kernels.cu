@@ -1192,6 +1192,11 @@ template <int HB> struct HistT { using T = uint64_t; };
 template <> struct HistT<16> { using T = uint16_t; };
 template <> struct HistT<32> { using T = uint32_t; };
 
+__host__ __device__ inline size_t sp_hist_bytes(int pb, int hbits) {
+    return hbits == 1 ? ((static_cast<size_t>(pb) / 32 + 1) * 4 + 15) & ~static_cast<size_t>(15)
+                      : ((static_cast<size_t>(pb) + 1) * (hbits / 8) + 15) & ~static_cast<size_t>(15);
+}
+
 // Shared-memory image of a pre block's spike history: pcount entries from
 // global memory, then zeros up to and including slot pb (the inert padding
 // pre of dictionary-encoded lists).  Returns the 16-aligned byte size.
@@ -1370,6 +1375,144 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(Spars
         end = nend;
     }
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *a.d_step += 1;
+}
+
+// ---------------------------------------------------------------------------
+// Sparse TMA stream (static nets whose lists carry one weight w: the ER
+// generator's networks, cfg4).  The blocked-CSC meta array is one contiguous
+// stream in (block, post) order.  The host cuts it into stages of whole posts
+// (<= kSpE entries, one pre block, <= kSpNbMax posts) and gives each CTA a
+// contiguous run of stages inside one pre block (CTAs per block in proportion
+// to its entries).  A producer warp
+// streams every stage's meta words plus the stage-relative end position of each
+// of its posts (uint16) into a kSpStages-deep ring with cp.async.bulk; each
+// consumer warp takes whole stages (warp w: stages w, w + kSpConsumers, ...) and
+// counts, 4 lanes per post, the entries whose pre delivers (e = s_pre[t+1-d])
+// -> partial[b][p] = count * w, the value k_sparse_pull's uniform path writes.
+// The loads never occupy registers; no CTA barrier per stage.
+constexpr int kSpE = 2048;        // entries per stage (8 KB of meta)
+constexpr int kSpStages = 20;     // ring depth: ~12 stages in flight beyond the ones being counted
+constexpr int kSpNbMax = 256;     // posts per stage
+constexpr int kSpConsumers = 8;   // consumer warps
+constexpr int kSpThreads = 32 * (kSpConsumers + 1);
+
+template <int HB>
+__device__ __forceinline__ void sp_stage_history(const SparseArgs& a, int b, uint8_t* smem, int tid, int nt) {
+    using HT = typename HistT<HB>::T;
+    const int pre0 = b * a.pb;
+    const int pcount = max(0, min(a.pb, a.n - pre0));
+    if (HB == 1) {
+        uint32_t* sb = reinterpret_cast<uint32_t*>(smem);
+        const int nw = (pcount + 31) >> 5;
+        const int nw_all = a.pb / 32 + 1;
+        for (int k = tid; k < nw_all; k += nt) sb[k] = k < nw ? __ldcg(a.bits + (pre0 >> 5) + k) : 0u;
+        return;
+    }
+    HT* sh = reinterpret_cast<HT*>(smem);
+    for (int k = tid; k <= a.pb; k += nt) {
+        HT v = 0;
+        if (k < pcount) v = static_cast<HT>(HB == 64 ? __ldcg(a.hist + pre0 + k) : __ldcg(a.hist_lo + pre0 + k));
+        sh[k] = v;
+    }
+}
+
+template <int HB>
+__device__ __forceinline__ uint32_t sp_hit(const uint8_t* hist, uint32_t m) {
+    using HT = typename HistT<HB>::T;
+    const int pl = static_cast<int>(m & 0xffffu);
+    if (HB == 1) return (reinterpret_cast<const uint32_t*>(hist)[pl >> 5] >> (pl & 31)) & 1u;
+    return static_cast<uint32_t>((reinterpret_cast<const HT*>(hist)[pl] >> ((m >> 16) & 63u)) & 1u);
+}
+
+template <typename WT, int HB>
+__global__ void __launch_bounds__(kSpThreads, 1) k_sparse_tma(SparseArgs a, SpStagePlan plan) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    uint32_t* r_meta = reinterpret_cast<uint32_t*>(smem);
+    uint16_t* r_bnd = reinterpret_cast<uint16_t*>(smem + kSpStages * kSpE * 4);
+    uint8_t* s_hist = smem + kSpStages * (kSpE * 4 + kSpNbMax * 2);
+    const size_t hist_bytes = sp_hist_bytes(a.pb, HB);
+    int4* s_hdr = reinterpret_cast<int4*>(s_hist + hist_bytes);  // [stages] {entries, k0, nb, block}
+    uint64_t* full = reinterpret_cast<uint64_t*>(s_hdr + kSpStages);
+    uint64_t* empty = full + kSpStages;
+    const int s0 = plan.cta_first[blockIdx.x], s1 = plan.cta_first[blockIdx.x + 1];
+    const int blk0 = plan.cta_block[blockIdx.x];
+    if (tid == 0) {
+        for (int s = 0; s < kSpStages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // the one pre block of this CTA's stages
+    if (warp < kSpConsumers) sp_stage_history<HB>(a, blk0, s_hist, tid, 32 * kSpConsumers);
+    __syncthreads();
+    if (warp == kSpConsumers) {
+        // ---- producer: stage records read 32 at a time (one per lane) ----
+        SpStage cur{}, nxt{};
+        if (s0 + lane < s1) cur = plan.stages[s0 + lane];
+        if (s0 + 32 + lane < s1) nxt = plan.stages[s0 + 32 + lane];
+        for (int s = s0, i = 0; s < s1; ++s, ++i) {
+            const int w = (s - s0) & 31;
+            if (w == 0 && s != s0) {
+                cur = nxt;
+                if (s + 32 + lane < s1) nxt = plan.stages[s + 32 + lane];
+            }
+            const int64_t q = __shfl_sync(0xffffffffu, cur.q, w);
+            const int64_t bo = __shfl_sync(0xffffffffu, cur.bnd_off, w);
+            const int entries = __shfl_sync(0xffffffffu, cur.entries, w);
+            const int k0 = __shfl_sync(0xffffffffu, cur.k0, w);
+            const int nb = __shfl_sync(0xffffffffu, cur.nb, w);
+            const int blk = __shfl_sync(0xffffffffu, cur.block, w);
+            const int slot = i % kSpStages;
+            if (lane == 0) {
+                mbar_wait(empty + slot, ((i / kSpStages) & 1u) ^ 1u);
+                s_hdr[slot] = make_int4(entries, k0, nb, blk);
+                const uint32_t mbytes = static_cast<uint32_t>(entries) * 4u;
+                const uint32_t bbytes = static_cast<uint32_t>((nb * 2 + 15) & ~15);
+                mbar_arrive_expect_tx(full + slot, mbytes + bbytes);
+                if (mbytes) bulk_g2s(r_meta + slot * kSpE, a.meta + q, mbytes, full + slot);
+                if (bbytes) bulk_g2s(r_bnd + slot * kSpNbMax, plan.bnd + bo, bbytes, full + slot);
+            }
+            __syncwarp();
+        }
+        return;
+    }
+    // ---- consumer warp: stages warp, warp + kSpConsumers, ... of the CTA's run;
+    // 4 lanes per post count the delivering entries of its list (16 B per lane-step) ----
+    const WT w0 = static_cast<const WT*>(a.wdict)[0];
+    const int sg = lane >> 2, sl = lane & 3;
+    for (int i = warp; s0 + i < s1; i += kSpConsumers) {
+        const int slot = i % kSpStages;
+        mbar_wait(full + slot, (i / kSpStages) & 1u);
+        const int4 hdr = s_hdr[slot];
+        const int k0 = hdr.y, nb = hdr.z;
+        const uint8_t* hist = s_hist;
+        const uint32_t* m = r_meta + slot * kSpE;
+        const uint16_t* bp = r_bnd + slot * kSpNbMax;
+        for (int j0 = 0; j0 < nb; j0 += 8) {
+            const int j = j0 + sg;
+            int beg = 0, end = 0;
+            if (j < nb) {
+                end = bp[j];
+                beg = j > 0 ? bp[j - 1] : 0;
+            }
+            int cnt = 0;
+#pragma unroll 4
+            for (int q = beg + sl * 4; q < end; q += 16) {
+                const uint4 mm = *reinterpret_cast<const uint4*>(m + q);
+                cnt += static_cast<int>(sp_hit<HB>(hist, mm.x) + sp_hit<HB>(hist, mm.y) + sp_hit<HB>(hist, mm.z) +
+                                        sp_hit<HB>(hist, mm.w));
+            }
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+            if (sl == 0 && j < nb) a.partial[k0 + j - 1] = static_cast<double>(static_cast<WT>(cnt) * w0);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + slot);
+    }
+    if (blockIdx.x == 0 && tid == 0) *a.d_step += 1;
 }
 
 // Sparse stream: the same blocked-CSC pull, but each warp streams a contiguous
@@ -1910,6 +2053,39 @@ void launch_sparse(const SparseArgs& a, bool f64, bool stdp, int hbits, int sub,
         }
     }
     check(cudaGetLastError(), "k_sparse");
+}
+
+size_t sparse_tma_smem(const SparseArgs& a, int hbits) {
+    return static_cast<size_t>(kSpStages) * (kSpE * 4 + kSpNbMax * 2) + sp_hist_bytes(a.pb, hbits) +
+           kSpStages * 16 + 2 * kSpStages * 8;
+}
+
+int sparse_tma_stage_entries() { return kSpE; }
+int sparse_tma_max_boundaries() { return kSpNbMax; }
+
+void launch_sparse_tma(const SparseArgs& a, const SpStagePlan& plan, int ctas, bool f64, int hbits, cudaStream_t s) {
+    const size_t smem = sparse_tma_smem(a, hbits);
+    auto go = [&](auto kern) {
+        check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+              "k_sparse_tma smem attribute");
+        kern<<<ctas, kSpThreads, smem, s>>>(a, plan);
+    };
+    if (f64) {
+        switch (hbits) {
+            case 1: go(k_sparse_tma<double, 1>); break;
+            case 16: go(k_sparse_tma<double, 16>); break;
+            case 32: go(k_sparse_tma<double, 32>); break;
+            default: go(k_sparse_tma<double, 64>); break;
+        }
+    } else {
+        switch (hbits) {
+            case 1: go(k_sparse_tma<float, 1>); break;
+            case 16: go(k_sparse_tma<float, 16>); break;
+            case 32: go(k_sparse_tma<float, 32>); break;
+            default: go(k_sparse_tma<float, 64>); break;
+        }
+    }
+    check(cudaGetLastError(), "k_sparse_tma");
 }
 
 void launch_er_dense(const ErArgs& e, void* w, bool f64, uint8_t* delay, uint32_t* mask, int first,

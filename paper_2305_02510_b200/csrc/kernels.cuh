@@ -148,6 +148,24 @@ struct SparseArgs {
     int32_t abm;               // exact mode seeds the accumulator with 0.0 instead of leak(v)
 };
 
+// Stage plan of k_sparse_tma (built on the host at setup from the CSC offsets):
+// stage = <= sparse_tma_stage_entries() consecutive meta entries of one pre
+// block plus the stage-relative positions of the post boundaries inside it.
+struct SpStage {
+    int64_t q;          // first meta entry
+    int64_t bnd_off;    // first position in bnd (multiple of 8)
+    int32_t entries;    // meta entries (multiple of 4)
+    int32_t k0;         // 1 + the stage's first linear post b * nl + p (= partial row + 1)
+    int32_t nb;         // whole posts in the stage (their end positions are in bnd)
+    int32_t block;      // pre block of every entry of the stage
+};
+struct SpStagePlan {
+    const SpStage* stages;
+    const int32_t* cta_first;  // [ctas + 1] stage range per CTA
+    const int32_t* cta_block;  // [ctas] first pre block of the CTA (its stages use it and the next)
+    const uint16_t* bnd;       // end position of each post of a stage, stage-relative
+};
+
 // ---- launchers (kernels.cu) ----
 void launch_neuron(const NeuronArgs& a, bool exact, bool fused_hist, const HistArgs& h,
                    cudaStream_t s);
@@ -166,6 +184,11 @@ void launch_prologue(double* u_exact, const double* v, const double* leak, const
                      int nl, bool abm, cudaStream_t s);
 void launch_step_bump(int32_t* d_step, cudaStream_t s);
 int sparse_block_pres(int hbits);
+// TMA-fed stream for static uniform-weight lists (dictionary {w, 0}), no exact order
+size_t sparse_tma_smem(const SparseArgs& a, int hbits);
+int sparse_tma_stage_entries();
+int sparse_tma_max_boundaries();
+void launch_sparse_tma(const SparseArgs& a, const SpStagePlan& plan, int ctas, bool f64, int hbits, cudaStream_t s);
 // persistent cooperative step loop for small dense nets (single partition)
 int persistent_max_ctas(bool f64, bool stdp, bool delay);
 void launch_persistent_dense(const NeuronArgs& na, const HistArgs& h, const DenseArgs& da, bool f64,

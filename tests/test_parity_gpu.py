@@ -428,3 +428,17 @@ def test_profile_stats_and_launch_count():
     assert st["sweep_launches"] == 2 and st["neuron_launches"] == 2
     assert st["kernel_launches"] == 20
     assert st["sweep_ms"] > 0 and st["dense"] == 1
+
+
+def test_sparse_tma_stream_opt_in(monkeypatch):
+    """The opt-in TMA-fed uniform-weight stream (SNB_SPARSE_KERNEL=tma) gives
+    the reference rasters (cfg1 / cfg2 goldens, delays 1..8)."""
+    monkeypatch.setenv("SNB_SPARSE_KERNEL", "tma")
+    for tag, by_syn in (("cfg1_seed0", False), ("cfg1_seed42", False), ("cfg2_seed0", True)):
+        e = _scale()[tag]
+        eng = _generated(e, 2, by_syn=by_syn)
+        s, n = eng.raster()
+        st = eng.stats()
+        eng.close()
+        assert st["sweep_kernel"] == 10, tag
+        assert _digest(s, n) == e["digest"], tag
