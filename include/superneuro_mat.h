@@ -147,8 +147,10 @@ typedef enum sn_sweep_kernel {
     SN_SWEEP_SPARSE_EXACT = 8,  /* k_sparse_exact: one thread per post, ascending pre */
     SN_SWEEP_TINY = 9,          /* k_tiny: whole call in one CTA, state in shared memory
                                    (single partition, N <= 1024, lists fit in smem) */
-    SN_SWEEP_SPARSE_TMA = 10    /* k_sparse_tma: cp.async.bulk stream of uniform-weight
-                                   lists, hit bits + per-post prefix counts */
+    SN_SWEEP_SPARSE_TMA = 10,   /* k_sparse_tma: cp.async.bulk-fed stream of uniform-weight
+                                   lists (opt-in, SNB_SPARSE_KERNEL=tma) */
+    SN_SWEEP_SPARSE_COUNT = 11  /* k_sparse_count: k_sparse_pull specialised for one-weight
+                                   static lists (counts the delivering pres) */
 } sn_sweep_kernel;
 
 /* ---- lifecycle ---------------------------------------------------------- */

@@ -1377,6 +1377,88 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(Spars
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *a.d_step += 1;
 }
 
+// Sparse count: k_sparse_pull specialised for static lists that carry one
+// weight w (dictionary {w, 0}: the ER generator's nets, cfg4).  Same CTA
+// tiling and pipelining; per post the lanes count the delivering entries and
+// one lane writes count * w.  Loads are predicated on the 32-bit number of
+// remaining entries and the bit test is one funnel shift, so an entry costs
+// address + LDS + SHF.W + AND (padding entries point at the zero-history slot pb).
+template <typename WT, int HB, int SUB>
+__global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_count(SparseArgs a) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    using HT = typename HistT<HB>::T;
+    static_assert(HB != 64, "64-step histories use k_sparse_pull");
+    const int b = blockIdx.y;
+    const int pre0 = b * a.pb;
+    const int pcount = min(a.pb, a.n - pre0);
+    const int tid = threadIdx.x;
+    stage_history<HB>(a, pre0, pcount, smem_raw);
+    __syncthreads();
+    const uint32_t* sbits = reinterpret_cast<const uint32_t*>(smem_raw);
+    const HT* shist = reinterpret_cast<const HT*>(smem_raw);
+    const WT w0 = static_cast<const WT*>(a.wdict)[0];
+    const int p0 = blockIdx.x * a.posts_per_cta;
+    const int p1 = min(a.nl, p0 + a.posts_per_cta);
+    constexpr int PER_WARP = 32 / SUB;
+    constexpr int UL = SUB <= 8 ? SNB_SPARSE_UL : 4;
+    constexpr int STEP = SUB * 4 * UL;  // entries one lane group covers per batch
+    const int warp = tid >> 5, lane = tid & 31;
+    const int sg = lane / SUB, sl = lane % SUB;
+    const int stride = (kThreads / 32) * PER_WARP;
+    const int64_t* offb = a.off + static_cast<int64_t>(b) * a.nl;
+    int p = p0 + warp * PER_WARP + sg;
+    int64_t beg = 0, end = 0;
+    if (p < p1) {
+        beg = __ldg(offb + p);
+        end = __ldg(offb + p + 1);
+    }
+    for (int pbase = p0 + warp * PER_WARP; pbase < p1; pbase += stride) {  // warp-uniform trip count
+        const bool valid = p < p1;
+        const int pn = p + stride;
+        int64_t nbeg = 0, nend = 0;
+        if (pn < p1) {
+            nbeg = __ldg(offb + pn);
+            nend = __ldg(offb + pn + 1);
+        }
+        int cnt = 0;
+        if (valid) {
+            for (int64_t q0 = beg + sl * 4; q0 < end; q0 += STEP) {
+                const int rem = static_cast<int>(min(end - q0, static_cast<int64_t>(STEP)));
+                const uint4* src = reinterpret_cast<const uint4*>(a.meta + q0);
+                uint4 m4[UL];
+#pragma unroll
+                for (int u = 0; u < UL; ++u)
+                    if (u * SUB * 4 < rem) m4[u] = __ldcs(src + u * SUB);
+#pragma unroll
+                for (int u = 0; u < UL; ++u) {
+                    if (u * SUB * 4 < rem) {
+                        const uint32_t ms[4] = {m4[u].x, m4[u].y, m4[u].z, m4[u].w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint32_t mk = ms[k];
+                            if (HB == 1) {
+                                const uint32_t h = sbits[(mk & 0xffffu) >> 5];
+                                cnt += static_cast<int>(__funnelshift_r(h, h, mk) & 1u);  // bit pl & 31
+                            } else {
+                                const uint32_t h = static_cast<uint32_t>(shist[mk & 0xffffu]);
+                                cnt += static_cast<int>(__funnelshift_r(h, h, mk >> 16) & 1u);  // bit d-1 < 32
+                            }
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int o = SUB / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (valid && sl == 0)
+            a.partial[static_cast<int64_t>(b) * a.nl + p] = static_cast<double>(static_cast<WT>(cnt) * w0);
+        p = pn;
+        beg = nbeg;
+        end = nend;
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *a.d_step += 1;
+}
+
 // ---------------------------------------------------------------------------
 // Sparse TMA stream (static nets whose lists carry one weight w: the ER
 // generator's networks, cfg4).  The blocked-CSC meta array is one contiguous
@@ -1991,6 +2073,18 @@ template <typename WT, bool STDP, int HB>
 static void sparse_go_sub(const SparseArgs& a, int sub, int gx, size_t smem, cudaStream_t s) {
     dim3 grid(gx, a.nblocks);
     if (a.dict_size > 0) smem = ((smem + 15) & ~static_cast<size_t>(15)) + static_cast<size_t>(a.dict_size) * sizeof(WT);
+    if (a.dict_size == 2 && !STDP && sub != 0 && HB != 64) {  // one weight: count the delivering pres
+        constexpr int HC = HB == 64 ? 32 : HB;  // (64 never reaches the launch)
+        switch (sub) {
+            case 1: k_sparse_count<WT, HC, 1><<<grid, kThreads, smem, s>>>(a); break;
+            case 2: k_sparse_count<WT, HC, 2><<<grid, kThreads, smem, s>>>(a); break;
+            case 4: k_sparse_count<WT, HC, 4><<<grid, kThreads, smem, s>>>(a); break;
+            case 8: k_sparse_count<WT, HC, 8><<<grid, kThreads, smem, s>>>(a); break;
+            case 16: k_sparse_count<WT, HC, 16><<<grid, kThreads, smem, s>>>(a); break;
+            default: k_sparse_count<WT, HC, 32><<<grid, kThreads, smem, s>>>(a); break;
+        }
+        return;
+    }
     if (a.dict_size > 0 && !STDP) {
         switch (sub) {
             case 0: k_sparse_stream<WT, false, HB, true><<<grid, kThreads, smem, s>>>(a); break;
