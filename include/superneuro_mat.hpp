@@ -11,6 +11,15 @@
 //   m.setup();
 //   auto r = m.simulate(10);                         // r.events: (step, neuron) ascending
 //
+// Agent-based runs (abm_run, abm_engine.cpp:218-243): construct with
+// SN_MODE_ABM, give stochastic neurons a fire probability (1 = "lif",
+// 0.5 = "stochastic_lif") and set the run seed:
+//
+//   superneuro::Model m(0, SN_STORAGE_AUTO, SN_WEIGHTS_F64, SN_MODE_ABM);
+//   m.set_exact_order(true);                        // bit-exact with the reference
+//   int c = m.create_neuron(1.0, 0.0, 0.0, 0, 0, 0.5);
+//   m.set_seed(9);
+//
 // Errors surface as std::invalid_argument / std::logic_error / std::runtime_error
 // with the engine's message, the same exception types the reference throws.
 #pragma once
@@ -65,12 +74,17 @@ struct StdpParams {                     // StdpConfig (model.hpp:67-78)
 class Model {
 public:
     explicit Model(int device = 0, sn_storage storage = SN_STORAGE_AUTO,
-                   sn_precision precision = SN_WEIGHTS_F32) {
+                   sn_precision precision = SN_WEIGHTS_F32, sn_mode mode = SN_MODE_MAT) {
         check(sn_options_init(&opts_));
         opts_.device = device;
         opts_.storage = storage;
         opts_.precision = precision;
+        opts_.mode = mode;
     }
+    // sequential ascending-pre accumulation (bit-exact membranes on float nets)
+    void set_exact_order(bool on) { opts_.exact_order = on ? 1 : 0; }
+    // SimulationConfig::seed: keys the stochastic behaviours of SN_MODE_ABM
+    void set_seed(uint64_t seed) { seed_ = seed; }
     ~Model() {
         if (e_) sn_engine_destroy(e_);
     }
@@ -78,7 +92,8 @@ public:
     Model& operator=(const Model&) = delete;
 
     int create_neuron(double threshold = 1.0, double leak = 0.0, double reset_state = 0.0,
-                      int refractory_period = 0, int axonal_delay = 0) {
+                      int refractory_period = 0, int axonal_delay = 0, double fire_probability = 1.0) {
+        fire_p_.push_back(fire_probability);
         thr_.push_back(threshold);
         leak_.push_back(leak);
         reset_.push_back(reset_state);
@@ -109,6 +124,12 @@ public:
         if (stdp)
             check(sn_set_stdp(e_, stdp->window, stdp->a_plus.data(), stdp->a_minus.data(),
                               stdp->w_min, stdp->w_max));
+        check(sn_set_seed(e_, seed_));
+        for (double p : fire_p_)
+            if (p != 1.0) {
+                check(sn_set_fire_probability(e_, 0, n, fire_p_.data()));
+                break;
+            }
         check(sn_setup(e_));
     }
     Result simulate(int time_steps) {
@@ -138,7 +159,8 @@ public:
 private:
     sn_options opts_{};
     sn_engine* e_ = nullptr;
-    std::vector<double> thr_, leak_, reset_, w_, sa_;
+    std::vector<double> thr_, leak_, reset_, w_, sa_, fire_p_;
+    uint64_t seed_ = 0;
     std::vector<int32_t> refr_, axonal_, pre_, post_, d_, st_, sn_;
     std::vector<uint8_t> stdp_;
     size_t pushed_ = 0;

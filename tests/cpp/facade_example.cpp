@@ -1,6 +1,7 @@
 // Drop-in use of the C++ facade: the two-neuron delay-3 chain of the
 // reference tests (test_oracle.cpp:47-51) -> {(0,0),(3,1)}; plus an STDP pair
-// (test_stdp.cpp:46-57) -> weight 0.5 + 0.1 within fp32 storage tolerance.
+// (test_stdp.cpp:46-57) -> weight 0.5 + 0.1 within fp32 storage tolerance;
+// plus a seeded stochastic agent-based run.
 #include "superneuro_mat.hpp"
 
 #include <cmath>
@@ -34,6 +35,27 @@ int main() {
         const auto q = p.simulate(3);
         if (q.weights.size() != 1 || q.weights[0] != 0.5 + 0.1) {
             std::printf("FAIL stdp %.17g\n", q.weights.empty() ? -1.0 : q.weights[0]);
+            return 1;
+        }
+        // agent-based mode: stochastic_lif (p = 0.5) post, seeded -- deterministic
+        // per seed, fires on some but not all of its above-threshold steps
+        // (test_abm_engine.cpp:122-141)
+        auto run_abm = [](uint64_t seed) {
+            superneuro::Model g(0, SN_STORAGE_AUTO, SN_WEIGHTS_F64, SN_MODE_ABM);
+            g.set_exact_order(true);
+            g.create_neuron();
+            g.create_neuron(1.0, 0.0, 0.0, 0, 0, 0.5);
+            g.create_synapse(0, 1, 2.0, 1, false);
+            for (int t = 0; t < 100; ++t) g.add_spike(t, 0, 2.0);
+            g.set_seed(seed);
+            g.setup();
+            int fires = 0;
+            for (const auto& ev : g.simulate(100).events) fires += ev.neuron == 1;
+            return fires;
+        };
+        const int f9 = run_abm(9), f9b = run_abm(9);
+        if (f9 != f9b || f9 <= 20 || f9 >= 80) {
+            std::printf("FAIL abm %d %d\n", f9, f9b);
             return 1;
         }
         std::printf("facade ok\n");
