@@ -210,7 +210,7 @@ def test_cfg2_delays_match_reference(storage):
     assert _digest(s, n) == e["digest"]
 
 
-@pytest.mark.parametrize("storage", [1, 2])
+@pytest.mark.parametrize("storage", [0, 1, 2])
 def test_long_stdp_window_multiword_history(storage):
     """StdpConfig windows are arbitrary (model.cpp:104-117): window 70 with
     delays up to 6 needs two 64-bit history words per neuron."""
@@ -231,6 +231,41 @@ def test_long_stdp_window_multiword_history(storage):
         r = run_engine(c, storage=storage, precision="f64")
         assert np.array_equal(r["steps"], o["steps"]) and np.array_equal(r["neurons"], o["neurons"])
         assert np.array_equal(r["weights"], o["weights"])
+        if storage == 0:
+            assert r["stats"]["sweep_kernel"] == TINY_KERNEL
+
+
+def test_tiny_long_delays_and_edge_sizes():
+    """k_tiny with effective delays up to 48 (history bits past the first
+    32-bit word), a window-70 STDP span across three words, a single-neuron
+    net and a net without synapses, each against the oracle."""
+    from oracle import bridge as B
+    from support import random_net, random_stim
+    from paper_2305_02510_b200.model import NetworkDef, NeuronParams, StdpConfig
+    w = 70
+    cfg = StdpConfig(window=w, a_plus=[0.02 * 0.97 ** k for k in range(w)],
+                     a_minus=[0.025 * 0.96 ** k for k in range(w)], w_min=0.0, w_max=1.0)
+    cases = []
+    for seed in (700, 701):
+        net = random_net(seed, min_neurons=40, max_neurons=80, edge_prob=0.1, max_delay=40, max_axonal=8)
+        for i, s in enumerate(net.synapses):
+            s.stdp_enabled = i % 3 != 0
+        cases.append(CS.Case(f"tiny_delay_{seed}", net, 200, random_stim(seed, net.neuron_count(), 200, 300),
+                             stdp=cfg if seed == 701 else None))
+    one = NetworkDef()
+    one.neurons = [NeuronParams(threshold=1.0, leak=0.5, reset=0.0, refractory=2)]
+    cases.append(CS.Case("tiny_one", one, 30, random_stim(3, 1, 30, 20)))
+    bare = NetworkDef()
+    bare.neurons = [NeuronParams(threshold=1.5) for _ in range(37)]
+    cases.append(CS.Case("tiny_bare", bare, 30, random_stim(4, 37, 30, 60)))
+    for c in cases:
+        o = B.run_oracle(c.arrays(), c.steps, c.stim_arrays(), c.stdp_tuple())
+        r = run_engine(c, storage=0, precision="f64")
+        assert r["stats"]["sweep_kernel"] == TINY_KERNEL, c.name
+        assert np.array_equal(r["steps"], o["steps"]) and np.array_equal(r["neurons"], o["neurons"]), c.name
+        assert np.array_equal(r["membrane"], o["membrane"]), c.name
+        if "weights" in r:
+            assert np.array_equal(r["weights"], o["weights"]), c.name
 
 
 @pytest.mark.parametrize("storage", [2, 1])
