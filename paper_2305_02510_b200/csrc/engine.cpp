@@ -954,6 +954,10 @@ void Engine::plan_launches() {
         // dictionary lists are half as long in bytes; more posts per warp hide
         // more latency (cfg4, 160 entries/list: SUB 16 0.720 ms, 8 0.682, 4 0.652)
         if (!dict_.empty()) sub_ = avg >= 1024 ? 16 : avg >= 384 ? 8 : 4;
+        // one-weight lists (k_sparse_count): 8 lanes per post read whole 128-byte
+        // lines (4 posts per warp-wide LDG.128); cfg4, 160 entries per list:
+        // SUB 8 0.514 ms vs SUB 4 0.529 ms, 16 0.678
+        if (dict_.size() == 2 && !stdp_on_) sub_ = avg >= 1024 ? 16 : avg >= 96 ? 8 : 4;
         if (const char* sv = std::getenv("SNB_SPARSE_SUB")) {  // A/B knob: lanes per post
             const int v = std::atoi(sv);
             if (v == 4 || v == 8 || v == 16 || v == 32 || (!dict_.empty() && (v == 1 || v == 2))) sub_ = v;

@@ -1400,7 +1400,10 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_count(Spar
     const int p0 = blockIdx.x * a.posts_per_cta;
     const int p1 = min(a.nl, p0 + a.posts_per_cta);
     constexpr int PER_WARP = 32 / SUB;
-    constexpr int UL = SUB <= 8 ? SNB_SPARSE_UL : 4;
+#ifndef SNB_SPARSE_COUNT_UL
+#define SNB_SPARSE_COUNT_UL 6  // cfg4 (tools/ab_sparse.sh): UL 4 0.579, 5 0.561, 6 0.514, 7 0.532, 8 0.541, 12 0.689 ms at SUB 8
+#endif
+    constexpr int UL = SUB <= 8 ? SNB_SPARSE_COUNT_UL : 4;
     constexpr int STEP = SUB * 4 * UL;  // entries one lane group covers per batch
     const int warp = tid >> 5, lane = tid & 31;
     const int sg = lane / SUB, sl = lane % SUB;
