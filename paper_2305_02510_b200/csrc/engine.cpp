@@ -980,6 +980,25 @@ void Engine::plan_launches() {
         // 1.27-2.7 ms on cfg4 against 0.56 ms for k_sparse_pull
         sparse_tma_ = !exact_ && !stdp_on_ && dict_.size() == 2 && nl_ > 0 && sk && std::string(sk) == "tma";
         if (sparse_tma_) sparse_tma_ = build_sparse_tma_plan(sms);
+        // k_sparse_count reads lists in any order: deal them bank-aware
+        const bool count_path = !exact_ && !stdp_on_ && dict_.size() == 2 && hbits_ != 64 && sub_ != 0 &&
+                                !sparse_tma_ && nl_ > 0 && sparse_elems_ > 0;
+        const char* bo = std::getenv("SNB_SPARSE_BANK_ORDER");  // A/B knob: 0 keeps pre order
+        if (count_path && !(bo && std::string(bo) == "0")) {
+            size_t free_b = 0, total_b = 0;
+            cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+            const size_t bytes = static_cast<size_t>(sparse_elems_) * 4;
+            if (bytes + (256u << 20) < free_b) {
+                DevBuf ordered;
+                ordered.alloc(bytes);
+                launch_sparse_bank_order(d_meta_.as<uint32_t>(), ordered.as<uint32_t>(), d_off_.as<int64_t>(),
+                                         static_cast<int64_t>(nblocks_) * nl_, nl_, sub_, hbits_, stream_);
+                cuda_check(cudaStreamSynchronize(stream_), "bank order");
+                std::swap(d_meta_.p, ordered.p);
+                std::swap(d_meta_.bytes, ordered.bytes);
+                bank_ordered_ = true;
+            }
+        }
     }
 }
 
@@ -1800,6 +1819,7 @@ void Engine::get_synapse_weights(double* out, int64_t count) {
     }
     for (size_t s = 0; s < pre_.size(); ++s) {
         if (slot_[s] < 0) { out[s] = 0.0; continue; }
+        if (bank_ordered_) { out[s] = dict_[0]; continue; }  // lists reordered; one weight
         if (!meta.empty()) out[s] = dict_[meta[slot_[s]] >> 23];
         else if (esz == 8) out[s] = reinterpret_cast<const double*>(host.data())[slot_[s]];
         else out[s] = static_cast<double>(reinterpret_cast<const float*>(host.data())[slot_[s]]);

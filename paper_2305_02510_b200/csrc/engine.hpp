@@ -183,6 +183,7 @@ private:
     DevBuf d_wdict_;
     void upload_dict();
     bool sparse_tma_ = false;  // k_sparse_tma stage plan (static uniform-weight lists)
+    bool bank_ordered_ = false;  // one-weight lists dealt bank-aware for k_sparse_count
     DevBuf d_sp_stages_, d_sp_first_, d_sp_block_, d_sp_bnd_;
     int32_t sp_ctas_ = 0;
     bool build_sparse_tma_plan(int ctas);

@@ -184,6 +184,9 @@ void launch_prologue(double* u_exact, const double* v, const double* leak, const
                      int nl, bool abm, cudaStream_t s);
 void launch_step_bump(int32_t* d_step, cudaStream_t s);
 int sparse_block_pres(int hbits);
+// setup: reorder one-weight lists for conflict-light history reads in k_sparse_count
+void launch_sparse_bank_order(const uint32_t* in, uint32_t* out, const int64_t* off, int64_t lists, int nl,
+                              int sub, int hbits, cudaStream_t s);
 // TMA-fed stream for static uniform-weight lists (dictionary {w, 0}), no exact order
 size_t sparse_tma_smem(const SparseArgs& a, int hbits);
 int sparse_tma_stage_entries();
