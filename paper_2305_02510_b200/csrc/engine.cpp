@@ -317,6 +317,7 @@ bool Engine::build_tiny() {
     probe.window = window_;
     probe.dp = dp_;
     if (tiny_smem_bytes(probe) + 4096 > static_cast<size_t>(tiny_max_smem())) return false;
+    if (stdp_on_ && static_cast<int64_t>(n_) * dp_ >= 0xffff) return false;  // pidx is 16-bit, 0xffff reserved
 
     std::vector<uint32_t> off(static_cast<size_t>(n_) + 1, 0);
     for (size_t s = 0; s < pre_.size(); ++s) ++off[post_[s] + 1];
@@ -326,8 +327,8 @@ bool Engine::build_tiny() {
     std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
         return post_[a] != post_[b] ? post_[a] < post_[b] : pre_[a] < pre_[b];
     });
-    // meta: (32-bit history word index << 5 | bit) with the word of delay bit
-    // d-1 of pre at (d-1)/32 * np + pre; plastic flag in bit 31
+    // meta: byte offset of the 32-bit history word of delay bit d-1 of pre
+    // (word (d-1)/32 * np + pre) << 5 | bit; pidx 0xffff marks non-plastic
     const uint32_t np = static_cast<uint32_t>(round_up(n_, 32));
     std::vector<uint32_t> meta(pre_.size());
     std::vector<uint16_t> pidx(stdp_on_ ? pre_.size() : 0);
@@ -341,8 +342,8 @@ bool Engine::build_tiny() {
         const uint32_t d1 = static_cast<uint32_t>(delay_[s] + axonal_[pre_[s]] - 1);
         const uint32_t pre = static_cast<uint32_t>(pre_[s]);
         const bool pl = stdp_on_ && plastic_[s];
-        meta[q] = (((d1 >> 5) * np + pre) << 5) | (d1 & 31u) | (pl ? (1u << 31) : 0u);
-        if (stdp_on_) pidx[q] = static_cast<uint16_t>(pre * static_cast<uint32_t>(dp_) + d1);
+        meta[q] = ((((d1 >> 5) * np + pre) * 4u) << 5) | (d1 & 31u);
+        if (stdp_on_) pidx[q] = pl ? static_cast<uint16_t>(pre * static_cast<uint32_t>(dp_) + d1) : uint16_t(0xffff);
         if (f64_) wd[q] = weight_[s];
         else wf[q] = static_cast<float>(weight_[s]);
         slot_[s] = static_cast<int64_t>(q);

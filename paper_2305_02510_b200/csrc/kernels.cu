@@ -975,7 +975,9 @@ __host__ __device__ inline TinyLayout tiny_layout(const TinyArgs& a) {
     L.off = o; o = tiny_align(o + (static_cast<size_t>(a.n) + 1) * 4);
     L.meta = o; o = tiny_align(o + static_cast<size_t>(a.m) * 4);
     L.pidx = o; o = tiny_align(o + (a.stdp ? static_cast<size_t>(a.m) * 2 : 0));
-    L.w = o; o = tiny_align(o + static_cast<size_t>(a.m) * (a.f64 ? 8 : 4));
+    // weights in smem: as stored for STDP nets (the update runs in WT), as
+    // double otherwise (no per-synapse conversion on the integration path)
+    L.w = o; o = tiny_align(o + static_cast<size_t>(a.m) * ((a.f64 || !a.stdp) ? 8 : 4));
     L.st_off = o; o = tiny_align(o + (static_cast<size_t>(a.steps) + 1) * 4);
     L.st_neuron = o; o = tiny_align(o + static_cast<size_t>(a.st_count) * 4);
     L.st_amp = o; o = tiny_align(o + static_cast<size_t>(a.st_count) * 8);
@@ -986,9 +988,9 @@ __host__ __device__ inline TinyLayout tiny_layout(const TinyArgs& a) {
 }
 
 // Bit test of one incoming synapse: meta = byte offset of the 32-bit history
-// word within a buffer << 3 | bit (plastic flag in bit 31, masked off here).
+// word within a buffer << 5 | bit; the funnel shift uses the low 5 bits.
 __device__ __forceinline__ bool tiny_bit(const uint8_t* buf, uint32_t mq) {
-    const uint32_t word = *reinterpret_cast<const uint32_t*>(buf + ((mq >> 3) & 0x3fffcu));
+    const uint32_t word = *reinterpret_cast<const uint32_t*>(buf + (mq >> 5));
     return __funnelshift_r(word, word, mq) & 1u;
 }
 
@@ -1007,7 +1009,8 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
     uint32_t* off = reinterpret_cast<uint32_t*>(sm + L.off);
     uint32_t* meta = reinterpret_cast<uint32_t*>(sm + L.meta);
     uint16_t* pidx = reinterpret_cast<uint16_t*>(sm + L.pidx);
-    WT* w = reinterpret_cast<WT*>(sm + L.w);
+    using WS = typename std::conditional<STDP, WT, double>::type;  // smem weight type
+    WS* w = reinterpret_cast<WS*>(sm + L.w);
     int32_t* st_off = reinterpret_cast<int32_t*>(sm + L.st_off);
     int32_t* st_neuron = reinterpret_cast<int32_t*>(sm + L.st_neuron);
     double* st_amp = reinterpret_cast<double*>(sm + L.st_amp);
@@ -1033,7 +1036,7 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
     for (int i = tid; i <= n; i += nt) off[i] = a.off[i];
     for (int q = tid; q < a.m; q += nt) {
         meta[q] = a.meta[q];
-        w[q] = static_cast<const WT*>(a.w)[q];
+        w[q] = static_cast<WS>(static_cast<const WT*>(a.w)[q]);
         if (STDP) pidx[q] = a.pidx[q];
     }
     const int64_t sbase = a.st_rows > 0 ? a.st_off[0] : 0;
@@ -1067,7 +1070,7 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
 #pragma unroll 4
             for (uint32_t q = q0; q < q1; ++q) {
                 const uint32_t mq = meta[q];
-                if (tiny_bit(hc, mq)) u += static_cast<double>(w[q]);
+                if (tiny_bit(hc, mq)) u += static_cast<double>(w[q]);  // WS = double unless STDP
             }
             int lo = st_off[s], hi = st_off[s + 1];
             if (hi > lo) {
@@ -1134,10 +1137,11 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
             const double* potn = pot + (cur ^ 1) * np * a.dp;
             const double depj = dep[(cur ^ 1) * np + j];
             for (uint32_t q = q0; q < q1; ++q) {
+                const uint16_t pq = pidx[q];
+                if (pq == 0xffffu) continue;  // not plastic
                 const uint32_t mq = meta[q];
-                if (!(mq >> 31)) continue;
                 WT dw = WT(0);
-                if (fired) dw += static_cast<WT>(potn[pidx[q]]);
+                if (fired) dw += static_cast<WT>(potn[pq]);
                 if (tiny_bit(hnb, mq)) dw -= static_cast<WT>(depj);
                 w[q] = clamp_ref<WT>(w[q] + dw, wmin, wmax);
             }
@@ -1154,7 +1158,7 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
     }
     if (STDP) {
         __syncthreads();  // every owner's last-step weight update is done
-        for (int q = tid; q < a.m; q += nt) static_cast<WT*>(a.w)[q] = w[q];
+        for (int q = tid; q < a.m; q += nt) static_cast<WT*>(a.w)[q] = static_cast<WT>(w[q]);
     }
     if (spikes) atomicAdd(a.spike_count, spikes);
     if (tid == 0) *a.d_step = t0 + a.steps;

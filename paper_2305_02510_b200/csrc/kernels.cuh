@@ -219,8 +219,8 @@ struct TinyArgs {
     const int32_t* refr;
     // incoming lists, post-major, pre ascending
     const uint32_t* off;       // [n+1]
-    const uint32_t* meta;      // history word byte offset << 3 | (d-1) & 31, plastic << 31
-    const uint16_t* pidx;      // STDP: pre * dp + (d-1), the pot^(d) trace of the pre
+    const uint32_t* meta;      // history word byte offset << 5 | (d-1) & 31
+    const uint16_t* pidx;      // STDP: pre * dp + (d-1), the pot^(d) trace of the pre; 0xffff = not plastic
     void* w;                   // float or double [m]
     int32_t m;
     // stimulus of this launch: rows of the per-step CSR (neuron ascending).
