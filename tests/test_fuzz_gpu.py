@@ -1,0 +1,101 @@
+"""Randomised cross-check of every engine plan against the C oracles: random
+nets (delays, axonal delays, refractory periods, infinite leaks, plastic
+subsets, STDP windows past 64 steps), random stimulus and random engine
+options (storage, precision, exact order, graphs, persistent loop, stream
+I/O, simulate() chunking, MAT or agent-based mode).  Rasters must be
+identical; fp64 + exact order (or the one-CTA loop) bit-exact; fp64 weights
+bit-exact in every plan; fp32 storage within its rounding."""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import cases as CS
+from support import close_rel, random_net, random_stim
+
+pytestmark = pytest.mark.gpu
+
+
+def _stdp(rng):
+    from paper_2305_02510_b200.model import StdpConfig
+    w = int(rng.choice([1, 3, 20, 40, 70]))
+    return StdpConfig(window=w, a_plus=list(0.03 * rng.random(w)), a_minus=list(0.03 * rng.random(w)),
+                      w_min=float(rng.choice([0.0, -1.0])), w_max=float(rng.choice([1.0, 3.0])))
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SNB_FUZZ_CASES", "240"))))
+def test_random_plans_match_oracle(seed):
+    from oracle import bridge as B
+    from paper_2305_02510_b200.engine import MatEngine
+    rng = np.random.default_rng(9000 + seed)
+    abm = seed % 4 == 3
+    net = random_net(9000 + seed, min_neurons=2, max_neurons=int(rng.choice([12, 40, 90])),
+                     edge_prob=float(rng.choice([0.05, 0.2, 0.5])), max_delay=int(rng.choice([1, 3, 9])),
+                     max_axonal=int(rng.choice([0, 2])), max_refractory=int(rng.choice([0, 3])))
+    n = net.neuron_count()
+    stdp = None
+    if not abm and rng.random() < 0.5:
+        stdp = _stdp(rng)
+        for s in net.synapses:
+            s.stdp_enabled = bool(rng.random() < 0.7)
+    steps = int(rng.choice([30, 120]))
+    stim = random_stim(9000 + seed, n, steps, int(rng.integers(5, 4 * n + 6)))
+    c = CS.Case(f"fuzz_{seed}", net, steps, stim, stdp=stdp, record=bool(rng.random() < 0.3))
+    a = c.arrays()
+    fire_p = None
+    if abm and rng.random() < 0.7:
+        fire_p = np.where(rng.random(n) < 0.5, rng.choice([0.0, 0.3, 0.5, 0.9], n), 1.0)
+    run_seed = int(rng.integers(0, 1 << 40))
+    if abm:
+        o = B.run_abm_oracle(a, steps, c.stim_arrays(), seed=run_seed, fire_p=fire_p, record_membrane=c.record)
+    else:
+        o = B.run_oracle(a, steps, c.stim_arrays(), c.stdp_tuple(), c.record)
+    opts = dict(storage=int(rng.integers(0, 3)), precision=str(rng.choice(["f32", "f64"])),
+                exact_order=bool(rng.random() < 0.5), use_graphs=bool(rng.random() < 0.7),
+                persistent=bool(rng.random() < 0.7), stream_io=bool(rng.random() < 0.3))
+    chunks = [steps] if rng.random() < 0.5 else [1, steps // 3, steps - 1 - steps // 3]
+    eng = MatEngine(record_membrane=c.record, mode="abm" if abm else "mat", **opts)
+    try:
+        eng.add_neurons(a["threshold"], a["leak"], a["reset"], a["refractory"], a["axonal"])
+        if len(a["pre"]):
+            eng.add_synapses(a["pre"], a["post"], a["weight"], a["delay"], None if abm else a["stdp"])
+        if stdp is not None:
+            eng.set_stdp(stdp.window, stdp.a_plus, stdp.a_minus, stdp.w_min, stdp.w_max)
+        if abm:
+            eng.set_seed(run_seed)
+            if fire_p is not None:
+                eng.set_fire_probability(fire_p)
+        eng.setup()
+        st = c.stim_arrays()
+        if len(st[0]):
+            eng.add_stimulus(*st)
+        for k in chunks:
+            eng.simulate(k)
+        s, q = eng.raster()
+        mem = eng.membrane()
+        w = eng.synapse_weights() if len(a["pre"]) else None
+        tr = eng.membrane_trace() if c.record else None
+        kernel = eng.stats()["sweep_kernel"]
+    finally:
+        eng.close()
+    tag = (seed, opts, chunks, abm, kernel)
+    assert np.array_equal(s, o["steps"]) and np.array_equal(q, o["neurons"]), tag
+    exact = opts["precision"] == "f64" and (opts["exact_order"] or kernel == 9)
+    if exact:
+        assert np.array_equal(mem, o["membrane"]), tag
+        if w is not None and stdp is not None:
+            assert np.array_equal(w, o["weights"]), tag
+        if tr is not None:
+            assert np.array_equal(tr, o["membrane_trace"]), tag
+    elif opts["precision"] == "f64":
+        assert close_rel(mem, o["membrane"]), tag
+        if w is not None and stdp is not None:
+            assert np.array_equal(w, o["weights"]), tag  # the per-synapse update is elementwise
+    else:
+        # fp32 weight storage: membranes integrate up to tens of weights of
+        # magnitude <= 3 that each carry a 2^-24 relative rounding
+        assert np.allclose(mem, o["membrane"], rtol=1e-5, atol=1e-4), tag
+        if w is not None and stdp is not None:  # fp32 updates of weights up to |3| over 120 steps
+            assert np.allclose(w, o["weights"], rtol=1e-5, atol=2e-5), tag
