@@ -477,3 +477,87 @@ def test_sparse_tma_stream_opt_in(monkeypatch):
         eng.close()
         assert st["sweep_kernel"] == 10, tag
         assert _digest(s, n) == e["digest"], tag
+
+
+@pytest.mark.parametrize("n,p,dmax,weights", [
+    (20000, 0.002, 20, "one"),      # 32-bit histories: 8192 pres per block -> 3 blocks
+    (20000, 0.002, 40, "one"),      # 64-bit histories: 4096 pres per block -> 5 blocks
+    (40000, 0.0005, 1, "one"),      # spike bits: 32768 pres per block -> 2 blocks
+    (20000, 0.002, 12, "three"),    # dictionary of 3 weights (k_sparse_pull<dict>)
+    (20000, 0.002, 12, "float"),    # weights streamed per synapse (k_sparse_pull)
+])
+def test_sparse_multiple_pre_blocks(n, p, dmax, weights):
+    """Sparse storage with several pre blocks per partition (history staged per
+    block, partials combined over blocks) against the oracle, for the
+    one-weight count kernel (bank-ordered lists), the dictionary pull and the
+    streamed-weight pull."""
+    from oracle import bridge as B
+    from paper_2305_02510_b200.engine import MatEngine
+    from paper_2305_02510_b200.netgen import RandomStream, erdos_renyi_arrays, scenario_stimulus
+    seed, steps = 5, 40
+    pre, post = erdos_renyi_arrays(n, p, seed)
+    m = len(pre)
+    rs = RandomStream(seed, 77)
+    k = np.arange(m, dtype=np.uint64)
+    delay = (1 + rs.below_np(k, dmax)).astype(np.int32)
+    if weights == "one":
+        w = np.ones(m)
+    elif weights == "three":
+        w = np.array([1.0, 2.0, -1.0])[rs.below_np(k + np.uint64(m), 3)]
+    else:
+        w = 0.25 + rs.unit_np(k + np.uint64(2 * m))
+    thr = np.full(n, 1.0 if weights != "float" else 1.3)
+    arrays = {"threshold": thr, "leak": np.zeros(n), "reset": np.zeros(n), "refractory": np.zeros(n, np.int32),
+              "axonal": np.zeros(n, np.int32), "pre": pre, "post": post, "weight": w, "delay": delay,
+              "stdp": np.zeros(m, np.uint8)}
+    stim = scenario_stimulus(n, steps, seed, count=200, period=2, amplitude=2.0).to_arrays()
+    o = B.run_oracle(arrays, steps, stim)
+    assert len(o["steps"]) > 1000
+    eng = MatEngine(storage=2, precision="f64")
+    eng.add_neurons(thr, arrays["leak"], arrays["reset"], arrays["refractory"], arrays["axonal"])
+    eng.add_synapses(pre, post, w, delay, None)
+    eng.setup()
+    eng.add_stimulus(*stim)
+    eng.simulate(steps)
+    s, q = eng.raster()
+    mem = eng.membrane()
+    st = eng.stats()
+    eng.close()
+    assert np.array_equal(s, o["steps"]) and np.array_equal(q, o["neurons"])
+    assert close_rel(mem, o["membrane"])
+    expect = {"one": 11 if dmax <= 32 else 6, "three": 6, "float": 5}[weights]
+    assert st["sweep_kernel"] == expect
+
+
+def test_dense_tma_sweep_8192_all_plastic():
+    """cfg3's plan at N = 8192 (many TMA work items, claimed dynamically):
+    ER(8192, p=1) all plastic with StdpConfig::defaults, paper stimulus,
+    15 steps, against the oracle (raster identical, fp32 weights 1e-5)."""
+    from oracle import bridge as B
+    from paper_2305_02510_b200.engine import MatEngine
+    from paper_2305_02510_b200.model import StdpConfig
+    from paper_2305_02510_b200.netgen import erdos_renyi_arrays, scenario_stimulus
+    n, steps = 8192, 15
+    pre, post = erdos_renyi_arrays(n, 1.0, 0)
+    m = len(pre)
+    arrays = {"threshold": np.ones(n), "leak": np.zeros(n), "reset": np.zeros(n),
+              "refractory": np.zeros(n, np.int32), "axonal": np.zeros(n, np.int32), "pre": pre, "post": post,
+              "weight": np.ones(m), "delay": np.ones(m, np.int32), "stdp": np.ones(m, np.uint8)}
+    d = StdpConfig.defaults()
+    sd = (d.window, np.array(d.a_plus), np.array(d.a_minus), d.w_min, d.w_max)
+    stim = scenario_stimulus(n, steps, 0).to_arrays()
+    o = B.run_oracle(arrays, steps, stim, sd)
+    eng = MatEngine(storage=1, persistent=False)
+    eng.generate_erdos_renyi(n, 1.0, 0, stdp=True)
+    eng.set_stdp(*sd)
+    eng.setup()
+    eng.add_stimulus(*stim)
+    eng.simulate(steps)
+    s, q = eng.raster()
+    W = eng.weight_matrix(n)
+    st = eng.stats()
+    eng.close()
+    assert st["sweep_kernel"] == 2  # k_dense_tma
+    assert np.array_equal(s, o["steps"]) and np.array_equal(q, o["neurons"])
+    w = W[pre, post]   # erdos_renyi list order (i, j ascending) = the oracle's synapse order
+    assert close_rel(w, o["weights"])
