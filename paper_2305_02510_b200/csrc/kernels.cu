@@ -101,7 +101,26 @@ __device__ __forceinline__ bool hist_update(const HistArgs& h, int i, bool s, in
     if (h.hist_lo) h.hist_lo[i] = static_cast<uint32_t>(words[0]);
     const uint64_t dmask = h.dmax >= 64 ? ~0ull : ((1ull << h.dmax) - 1ull);
     bool act = (words[0] & dmask) != 0;
-    if (h.stdp) {
+    if (h.stdp && h.hw == 1) {
+        // one history word (window + delay span <= 64): walk the set bits in
+        // ascending k, the order of the reference's sums (mat_engine.cpp:226-240)
+        const uint64_t w0 = words[0];
+        const uint64_t wmask = h.window >= 63 ? ~0ull : ((1ull << (h.window + 1)) - 1ull);
+        double dep = 0.0;
+        for (uint64_t m = w0 & wmask & ~1ull; m; m &= m - 1) dep += h.a_minus[__ffsll(static_cast<long long>(m)) - 2];
+        h.dep64[i] = dep;
+        h.dep32[i] = static_cast<float>(dep);
+        bool any_pot = false;
+        for (int d = 1; d <= h.dp; ++d) {
+            const uint64_t sh = w0 >> (d - 1);  // bit k of sh = s[t - k - d + 1]
+            double pot = 0.0;
+            for (uint64_t m = sh & wmask & ~1ull; m; m &= m - 1) pot += h.a_plus[__ffsll(static_cast<long long>(m)) - 2];
+            h.pot64[static_cast<int64_t>(i) * h.dp + (d - 1)] = pot;
+            h.pot32[static_cast<int64_t>(i) * h.dp + (d - 1)] = static_cast<float>(pot);
+            any_pot |= (pot != 0.0);
+        }
+        if (h.row_plastic[i] && (any_pot || t == 0)) act = true;
+    } else if (h.stdp) {
         // dep: bits 1..W
         double dep = 0.0;
         for (int k = 1; k <= h.window; ++k) {
@@ -144,14 +163,25 @@ __device__ __forceinline__ void neuron_step(const NeuronArgs& a, const HistArgs&
         if (EXACT) {
             u = a.u_exact[j];  // (leak(v) +) sum in ascending pre order, from the sweep
         } else {
-            // chunk partials: 8 independent loads in flight, fixed-order combine
+            // chunk partials: acc[k] sums chunks k, k+8, k+16, ... in order, then a
+            // fixed tree; 16 loads are issued before any add so a step's partials
+            // arrive in a few memory round trips
             double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             int c = 0;
+            for (; c + 16 <= a.nchunks; c += 16) {
+                double t[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) t[k] = __ldcg(a.partial + static_cast<int64_t>(c + k) * a.nl + j);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) acc[k & 7] += t[k];
+            }
             for (; c + 8 <= a.nchunks; c += 8) {
 #pragma unroll
                 for (int k = 0; k < 8; ++k) acc[k] += __ldcg(a.partial + static_cast<int64_t>(c + k) * a.nl + j);
             }
-            for (int k = 0; c < a.nchunks; ++c, ++k) acc[k] += __ldcg(a.partial + static_cast<int64_t>(c) * a.nl + j);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)  // remainder; unrolled so acc stays in registers
+                if (c + k < a.nchunks) acc[k] += __ldcg(a.partial + static_cast<int64_t>(c + k) * a.nl + j);
             const double in = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
             u = a.abm ? in : leak_toward(v, a.leak[j], reset) + in;
         }
