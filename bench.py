@@ -237,7 +237,7 @@ def run_ours(args):
     # (every 8th step's kernels carry CUDA event nodes), the persistent kernel
     # covers all K steps in one launch
     kname = sn._capi.Stats.KERNEL_NAMES.get(st["sweep_kernel"], "?")
-    persistent = kname in ("k_persistent_dense", "k_tiny")
+    persistent = kname in ("k_persistent_dense", "k_persistent_cols", "k_tiny")
     sweep_avg_ms = st["sweep_ms"] / (K if persistent else max(1, st["sweep_launches"]))
     bytes_per_sweep = st["sweep_bytes_total"] / K
     peak, peak_src = load_peaks()

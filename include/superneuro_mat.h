@@ -149,8 +149,10 @@ typedef enum sn_sweep_kernel {
                                    (single partition, N <= 1024, lists fit in smem) */
     SN_SWEEP_SPARSE_TMA = 10,   /* k_sparse_tma: cp.async.bulk-fed stream of uniform-weight
                                    lists (opt-in, SNB_SPARSE_KERNEL=tma) */
-    SN_SWEEP_SPARSE_COUNT = 11  /* k_sparse_count: k_sparse_pull specialised for one-weight
+    SN_SWEEP_SPARSE_COUNT = 11, /* k_sparse_count: k_sparse_pull specialised for one-weight
                                    static lists (counts the delivering pres) */
+    SN_SWEEP_PERSISTENT_COLS = 12 /* k_persistent_cols: whole step loop in one launch, CTAs own
+                                     32-post column groups, one grid barrier per step */
 } sn_sweep_kernel;
 
 /* ---- lifecycle ---------------------------------------------------------- */

@@ -901,6 +901,31 @@ void Engine::plan_launches() {
         dense_grid_ = std::min(items, sms * 8);
         d_partial_.alloc(static_cast<size_t>(nchunks_) * std::max(nl_, 1) * 8);
         cuda_check(cudaMemsetAsync(d_partial_.p, 0, d_partial_.bytes, stream_), "memset");
+        // column owners (one grid barrier per step) when the history is one word
+        // and there are enough 32-post column groups to spread the sweep
+        const char* pk = std::getenv("SNB_PERSIST_KERNEL");  // A/B knob: rows | cols
+        cols_ = hw_ == 1 && !tiny && nl_ >= 64 && !(pk && std::string(pk) == "rows");
+        if (pk && std::string(pk) == "cols" && hw_ == 1) cols_ = true;
+        if (cols_) {  // 8-post column groups, all co-resident (wider groups lose to the row chunks)
+            cols_ = false;
+            for (int w : {8}) {
+                const int groups = (nl_ + w - 1) / w;
+                if (groups <= persistent_cols_max_ctas(f64_, stdp_on_, has_delay_, w)) {
+                    cols_ = true;
+                    col_width_ = w;
+                    persist_grid_ = groups;
+                    break;
+                }
+            }
+        }
+        if (cols_) {
+            const size_t esz2 = f64_ ? 8 : 4;
+            d_hist2_.alloc(static_cast<size_t>(2) * n_ * 8);
+            d_pot2_.alloc(static_cast<size_t>(2) * n_ * std::max(dp_, 1) * esz2);
+            d_act2_.alloc(static_cast<size_t>(3) * ((n_ + 31) / 32) * 4);
+            for (DevBuf* b : {&d_hist2_, &d_pot2_, &d_act2_})
+                cuda_check(cudaMemsetAsync(b->p, 0, b->bytes, stream_), "memset");
+        }
     } else if (dense_) {
         const int vec = dense_vec(f64_);
         const int span = dense_threads() * vec;
@@ -1509,8 +1534,26 @@ void Engine::simulate(int32_t steps) {
         if (persistent_) {
             cudaEvent_t p0{}, p1{};
             if (opt_.profile) { p0 = get_event(); cuda_check(cudaEventRecord(p0, stream_), "rec"); }
-            launch_persistent_dense(na, hist_args(), dense_args(), f64_, stdp_on_, has_delay_, persist_grid_, steps,
-                                    stream_);
+            if (cols_) {
+                ColArgs ca{};
+                ca.hist2 = d_hist2_.as<uint64_t>();
+                ca.pot2 = d_pot2_.p;
+                ca.act3 = d_act2_.as<uint32_t>();
+                ca.row_plastic = d_row_plastic_.as<uint8_t>();
+                ca.a_plus = d_ap_.as<double>();
+                ca.a_minus = d_am_.as<double>();
+                ca.window = window_;
+                ca.dmax = dmax_;
+                // activity and raster words are OR-ed by 8-post groups: start from zero
+                cuda_check(cudaMemsetAsync(d_act2_.p, 0, d_act2_.bytes, stream_), "memset");
+                if (raster && nl_words_ > 0)
+                    cuda_check(cudaMemsetAsync(raster, 0, static_cast<size_t>(steps) * nl_words_ * 4, stream_), "memset");
+                launch_persistent_cols(na, dense_args(), ca, f64_, stdp_on_, has_delay_, col_width_, persist_grid_,
+                                       steps, stream_);
+            } else {
+                launch_persistent_dense(na, hist_args(), dense_args(), f64_, stdp_on_, has_delay_, persist_grid_,
+                                        steps, stream_);
+            }
             stats_.kernel_launches += 1;
             if (opt_.profile) {
                 p1 = get_event();
@@ -1876,7 +1919,7 @@ void Engine::get_stats(sn_stats* out) {
             stats_.sweep_kernel = SN_SWEEP_TINY;
             stats_.sweep_ctas = 1;
         } else if (dense_) {
-            stats_.sweep_kernel = persistent_ ? SN_SWEEP_PERSISTENT
+            stats_.sweep_kernel = persistent_ ? (cols_ ? SN_SWEEP_PERSISTENT_COLS : SN_SWEEP_PERSISTENT)
                                   : exact_    ? SN_SWEEP_DENSE_EXACT
                                   : tma_      ? SN_SWEEP_DENSE_TMA
                                               : SN_SWEEP_DENSE_STREAM;

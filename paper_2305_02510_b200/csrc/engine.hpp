@@ -191,6 +191,9 @@ private:
     // dense plan
     int32_t tile_w_ = 0, rows_per_chunk_ = 0, nchunks_ = 1, dense_grid_ = 1;
     bool persistent_ = false;     // small dense nets: one cooperative launch per simulate
+    bool cols_ = false;           // ... as column owners (k_persistent_cols, one barrier per step)
+    int32_t col_width_ = 8;       // posts per column group
+    DevBuf d_hist2_, d_pot2_, d_act2_;
     bool dynamic_sched_ = false;  // dense sweep items claimed through an atomic counter
     bool tma_ = false;            // k_dense_tma (cp.async.bulk ring) instead of k_dense_stream
     // tiny nets: the whole call in one CTA with shared-memory state (k_tiny)

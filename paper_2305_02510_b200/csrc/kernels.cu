@@ -1216,6 +1216,202 @@ __global__ void __launch_bounds__(kThreads, 2) k_persistent_dense(NeuronArgs na,
 }
 
 // ---------------------------------------------------------------------------
+// Column-owner persistent loop: CTA c owns posts [W c, W c + W), W = 8 (the
+// net must be small enough for every group to be co-resident).  Per step
+// (1) warp 0 updates its 8 posts from the input its own sweep produced (LIF as
+// neuron_step, history word, STDP traces, row activity) into the step's
+// parity buffers; (2) one grid barrier; (3) 1024 threads sweep every active row
+// of the CTA's 8 columns -- STDP of step t, then the delivery of step t + 1 --
+// and reduce the row-lane partials in a fixed tree.  Groups share 32-bit
+// words, so activity and raster words are OR-ed in (activity words
+// triple-buffered: the buffer of step t + 2 is cleared during step t's sweep,
+// after every reader of its previous use passed the barrier).  Used when the
+// history fits one word.
+constexpr int kColThreads = 1024;
+
+template <typename WT, bool STDP, bool DELAY, int kColW>
+__global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, DenseArgs da, ColArgs ca, int steps) {
+    cg::grid_group grid = cg::this_grid();
+    using VT = VecT<WT>;
+    using V = typename VT::V;
+    constexpr int VEC = VT::N;
+    constexpr int CV = kColW / VEC;          // column vectors per CTA
+    constexpr int RL = kColThreads / CV;     // row lanes
+    __shared__ double s_red[RL][kColW + 1];
+    __shared__ WT s_dep[kColW];
+    __shared__ uint32_t s_spk;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = blockIdx.x;
+    const int j = c * kColW + lane;          // warp 0, lanes < 8: this lane's post
+    const bool own = warp == 0 && lane < kColW && j < na.nl;
+    const int cv = tid % CV, rl = tid / CV;
+    const int j0 = c * kColW + cv * VEC;
+    const int n = da.n;
+    const int words = (n + 31) >> 5;
+    const int64_t pitch = da.pitch, mpitch = pitch >> 5;
+    const WT wmin = static_cast<WT>(da.w_min), wmax = static_cast<WT>(da.w_max);
+    WT* W = static_cast<WT*>(da.w);
+    WT* pot2 = static_cast<WT*>(ca.pot2);
+    const uint64_t dmask = ca.dmax >= 64 ? ~0ull : ((1ull << ca.dmax) - 1ull);
+    const uint64_t wmask = ca.window >= 63 ? ~0ull : ((1ull << (ca.window + 1)) - 1ull);
+    double in = own ? na.partial[j] : 0.0;   // input of the call's first step
+    int t = *na.d_step;
+    for (int s = 0; s < steps; ++s, ++t) {
+        const int cur = t & 1, prv = cur ^ 1;
+        uint32_t* act_now = ca.act3 + (t % 3) * words;
+        if (warp == 0) {
+            bool fired = false, act = false;
+            if (own) {
+                double v = na.v[j];
+                const double rst = na.reset[j];
+                double u = na.abm ? in : leak_toward(v, na.leak[j], rst) + in;
+                const int row = t - na.st_base;
+                if (row >= 0 && row < na.st_steps) {
+                    int64_t lo = na.st_off[row], hi = na.st_off[row + 1];
+                    if (hi > lo) {
+                        double ext = 0.0;
+                        while (lo < hi) {
+                            const int64_t mid = (lo + hi) >> 1;
+                            const int nid = na.st_neuron[mid];
+                            if (nid == j) { ext = na.st_amp[mid]; break; }
+                            if (nid < j) lo = mid + 1; else hi = mid;
+                        }
+                        u += ext;
+                    }
+                }
+                if (na.abm) u = leak_toward(v, na.leak[j], rst) + u;
+                fired = u > na.thr[j];
+                if (fired && na.fire_p) {
+                    const double p = na.fire_p[j];
+                    if (p < 1.0) fired = agent_fires(na.agent_key[j], t, p);
+                }
+                const int cnt = na.cnt[j];
+                if (cnt > 0) {
+                    fired = false;
+                    na.cnt[j] = cnt - 1;
+                    u = rst;
+                }
+                if (fired) {
+                    v = rst;
+                    na.cnt[j] = na.refr[j];
+                } else {
+                    v = u;
+                }
+                na.v[j] = v;
+                if (na.trace && (t - na.t_base) < na.raster_rows)
+                    na.trace[static_cast<int64_t>(t - na.t_base) * na.nl + j] = v;
+                const uint64_t hn = (__ldcg(ca.hist2 + static_cast<int64_t>(prv) * n + j) << 1) | (fired ? 1ull : 0ull);
+                ca.hist2[static_cast<int64_t>(cur) * n + j] = hn;
+                act = (hn & dmask) != 0;
+                if (STDP) {
+                    // set bits in ascending k: the reference's order (mat_engine.cpp:226-240)
+                    double dep = 0.0;
+                    for (uint64_t m = hn & wmask & ~1ull; m; m &= m - 1) dep += ca.a_minus[__ffsll(static_cast<long long>(m)) - 2];
+                    s_dep[lane] = static_cast<WT>(dep);
+                    bool any_pot = false;
+                    for (int d = 1; d <= da.dp; ++d) {
+                        double pot = 0.0;
+                        for (uint64_t m = (hn >> (d - 1)) & wmask & ~1ull; m; m &= m - 1)
+                            pot += ca.a_plus[__ffsll(static_cast<long long>(m)) - 2];
+                        pot2[(static_cast<int64_t>(cur) * n + j) * da.dp + (d - 1)] = static_cast<WT>(pot);
+                        any_pot |= pot != 0.0;
+                    }
+                    if (ca.row_plastic[j] && (any_pot || t == 0)) act = true;
+                }
+            }
+            const uint32_t word = __ballot_sync(0xffffffffu, fired);  // bits 0..W-1
+            const uint32_t aw = __ballot_sync(0xffffffffu, act);
+            if (lane == 0) {
+                const int wi = (c * kColW) >> 5, sh = (c * kColW) & 31;
+                if (aw) atomicOr(act_now + wi, aw << sh);
+                if (word) {
+                    if (na.raster && (t - na.t_base) < na.raster_rows)
+                        atomicOr(na.raster + static_cast<int64_t>(t - na.t_base) * na.nl_words + wi, word << sh);
+                    atomicAdd(na.spike_count, static_cast<unsigned long long>(__popc(word)));
+                }
+                s_spk = word;
+            }
+        }
+        grid.sync();
+        if (c == 0)  // clear the activity words of step t + 2 (last read by the sweep of step t - 1)
+            for (int k = tid; k < words; k += kColThreads) ca.act3[((t + 2) % 3) * words + k] = 0u;
+        // sweep of the CTA's columns: STDP of step t, delivery of step t + 1
+        const uint32_t spk = s_spk;
+        bool okc[VEC];
+        WT sj[VEC], dj[VEC];
+        double acc[VEC];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+            okc[k] = j0 + k < na.nl;
+            sj[k] = (STDP && okc[k] && ((spk >> (cv * VEC + k)) & 1u)) ? WT(1) : WT(0);
+            dj[k] = STDP ? s_dep[cv * VEC + k] : WT(0);
+            acc[k] = 0.0;
+        }
+        const uint64_t* hist = ca.hist2 + static_cast<int64_t>(cur) * n;
+        const WT* potc = pot2 + static_cast<int64_t>(cur) * n * da.dp;
+        for (int i = rl; i < n; i += RL) {
+            if (!((__ldcg(act_now + (i >> 5)) >> (i & 31)) & 1u)) continue;
+            const uint64_t eb = __ldcg(hist + i);
+            WT* wrow = W + static_cast<int64_t>(i) * pitch + j0;
+            V wv = VT::load(wrow);
+            uint32_t dv = 0;
+            if (DELAY) {
+                const uint8_t* dp8 = da.delay + static_cast<int64_t>(i) * pitch + j0;
+                dv = VEC == 4 ? *reinterpret_cast<const uint32_t*>(dp8) : *reinterpret_cast<const uint16_t*>(dp8);
+            }
+            uint8_t kind = kRowNone;
+            uint32_t mw = 0;
+            if (STDP) {
+                kind = da.kind[i];
+                if (kind == kRowMixed) mw = da.mask[static_cast<int64_t>(i) * mpitch + (j0 >> 5)];
+            }
+            bool changed = false;
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) {
+                if (!okc[k]) continue;
+                WT w = VT::get(wv, k);
+                const int d1 = DELAY ? static_cast<int>((dv >> (8 * k)) & 0xffu) - 1 : 0;
+                const bool e = (eb >> d1) & 1ull;
+                if (STDP && kind != kRowNone) {
+                    const bool pl = kind == kRowAll || (kind == kRowAllButSelf && j0 + k != i) ||
+                                    (kind == kRowMixed && ((mw >> ((j0 & 31) + k)) & 1u));
+                    if (pl) {
+                        const WT p = __ldcg(potc + static_cast<int64_t>(i) * da.dp + d1);
+                        WT dw = WT(0);  // dw = 0; if s_post dw += pot; if s_pre dw -= dep (mat_engine.cpp:243-246)
+                        if (sj[k] != WT(0)) dw += p;
+                        if (e) dw -= dj[k];
+                        const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
+                        changed |= nw != w;
+                        w = nw;
+                        VT::set(wv, k, nw);
+                    }
+                }
+                if (e) acc[k] += static_cast<double>(w);
+            }
+            if (STDP && changed) VT::store(wrow, wv);
+        }
+        // fixed tree: 8-row groups, then 8 groups of 8, then the rest in order
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) s_red[rl][cv * VEC + k] = acc[k];
+        __syncthreads();
+        for (int stride = 1; stride < RL; stride *= 8) {
+            const int col = tid % kColW, g = tid / kColW;  // RL / 8 groups per level
+            const int base = g * 8 * stride;
+            if (base < RL) {
+                double sum = 0.0;
+                for (int r = 0; r < 8 && base + r * stride < RL; ++r) sum += s_red[base + r * stride][col];
+                s_red[base][col] = sum;
+            }
+            __syncthreads();
+        }
+        if (warp == 0 && lane < kColW) in = s_red[0][lane];
+        __syncthreads();
+    }
+    if (own) da.partial[j] = in;  // (same buffer as na.partial) input of the next call's first step
+    if (blockIdx.x == 0 && tid == 0) *na.d_step = t;
+}
+
+// ---------------------------------------------------------------------------
 // Sparse pull: blocked CSC.  CTA (post group, pre block b) stages the spike
 // history of the block's pres in shared memory, then SUB lanes per post walk
 // the post's incoming list (pre ascending, padded to 4) with 128-bit loads:
@@ -2123,6 +2319,52 @@ int dense_stream_max_ctas(bool f64, bool stdp, bool delay) {
     }
     if (stdp) return delay ? stream_occ<float, true, true>() : stream_occ<float, true, false>();
     return delay ? stream_occ<float, false, true>() : stream_occ<float, false, false>();
+}
+
+template <typename WT, bool STDP, bool DELAY>
+static int cols_go(const NeuronArgs& na, const DenseArgs& da, const ColArgs& ca, int width, int grid, int steps,
+                   cudaStream_t s) {
+    // 16- and 32-post groups were slower than the row-chunk loop (2048-neuron
+    // STDP net: 29k vs 41k steps/s): only 8-post groups are instantiated
+    if (width != 8) throw std::runtime_error("k_persistent_cols: column groups of 8 posts only");
+    auto kern = k_persistent_cols<WT, STDP, DELAY, 8>;
+    if (grid <= 0) {
+        int dev = 0, sms = 0, occ = 0;
+        check(cudaGetDevice(&dev), "cudaGetDevice");
+        check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+        check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kColThreads, 0), "occupancy");
+        return occ * sms;
+    }
+    NeuronArgs a = na;
+    DenseArgs d = da;
+    ColArgs c = ca;
+    void* args[] = {&a, &d, &c, &steps};
+    check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kColThreads), args, 0, s),
+          "k_persistent_cols");
+    return grid;
+}
+
+static int cols_dispatch(const NeuronArgs& na, const DenseArgs& da, const ColArgs& ca, bool f64, bool stdp,
+                         bool delay, int width, int grid, int steps, cudaStream_t s) {
+#define SNB_C(WT)                                                                                 \
+    do {                                                                                          \
+        if (stdp) return delay ? cols_go<WT, true, true>(na, da, ca, width, grid, steps, s)       \
+                               : cols_go<WT, true, false>(na, da, ca, width, grid, steps, s);     \
+        return delay ? cols_go<WT, false, true>(na, da, ca, width, grid, steps, s)                \
+                     : cols_go<WT, false, false>(na, da, ca, width, grid, steps, s);              \
+    } while (0)
+    if (f64) SNB_C(double);
+    SNB_C(float);
+#undef SNB_C
+}
+
+int persistent_cols_max_ctas(bool f64, bool stdp, bool delay, int width) {
+    return cols_dispatch(NeuronArgs{}, DenseArgs{}, ColArgs{}, f64, stdp, delay, width, 0, 0, nullptr);
+}
+
+void launch_persistent_cols(const NeuronArgs& na, const DenseArgs& da, const ColArgs& ca, bool f64, bool stdp,
+                            bool delay, int width, int grid, int steps, cudaStream_t s) {
+    cols_dispatch(na, da, ca, f64, stdp, delay, width, grid, steps, s);
 }
 
 int persistent_max_ctas(bool f64, bool stdp, bool delay) {

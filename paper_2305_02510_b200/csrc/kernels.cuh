@@ -197,6 +197,25 @@ int persistent_max_ctas(bool f64, bool stdp, bool delay);
 void launch_persistent_dense(const NeuronArgs& na, const HistArgs& h, const DenseArgs& da, bool f64,
                              bool stdp, bool delay, int grid, int steps, cudaStream_t s);
 
+// ---- column-owner persistent loop (small dense nets, one history word) ----
+// CTA c owns posts [w c, w c + w), w in {8, 16, 32}: it sweeps all rows for those columns and
+// updates those neurons itself, so only one grid barrier per step is needed;
+// the per-step state other CTAs read (history word, pot traces, row activity)
+// is multi-buffered by step.
+struct ColArgs {
+    uint64_t* hist2;            // [2][n]   history word after step t in buffer t & 1
+    void* pot2;                 // WT [2][n * dp]
+    uint32_t* act3;             // [3][words] rows the sweep must visit (step t in t % 3; OR-ed)
+    const uint8_t* row_plastic; // [n]
+    const double* a_plus;
+    const double* a_minus;
+    int32_t window;
+    int32_t dmax;
+};
+int persistent_cols_max_ctas(bool f64, bool stdp, bool delay, int width);
+void launch_persistent_cols(const NeuronArgs& na, const DenseArgs& da, const ColArgs& ca, bool f64, bool stdp,
+                            bool delay, int width, int grid, int steps, cudaStream_t s);
+
 // ---- tiny nets: the whole T-step loop in one CTA, all state in shared memory ----
 // Eligible when N <= 1024 and the incoming lists, the per-neuron state and the
 // call's stimulus fit in shared memory.  Thread j owns post j: it sums its
