@@ -1256,51 +1256,71 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
     const uint64_t wmask = ca.window >= 63 ? ~0ull : ((1ull << (ca.window + 1)) - 1ull);
     double in = own ? na.partial[j] : 0.0;   // input of the call's first step
     int t = *na.d_step;
+    // the owned neurons' state and parameters stay in warp 0's registers for
+    // the whole call; only what other CTAs read goes through global memory
+    double v = 0.0, thr = 0.0, leak = 0.0, rst = 0.0, fire_p = 1.0;
+    int32_t cnt = 0, refr = 0;
+    uint64_t hprev = 0, akey = 0;
+    if (own) {
+        v = na.v[j];
+        thr = na.thr[j];
+        leak = na.leak[j];
+        rst = na.reset[j];
+        cnt = na.cnt[j];
+        refr = na.refr[j];
+        hprev = ca.hist2[static_cast<int64_t>((t & 1) ^ 1) * n + j];
+        if (na.fire_p) {
+            fire_p = na.fire_p[j];
+            akey = na.agent_key[j];
+        }
+    }
+    // stimulus rows of the next step, fetched one step ahead
+    auto stim_bounds = [&](int tt, int64_t& lo, int64_t& hi) {
+        lo = hi = 0;
+        const int row = tt - na.st_base;
+        if (warp == 0 && row >= 0 && row < na.st_steps) {
+            lo = __ldg(na.st_off + row);
+            hi = __ldg(na.st_off + row + 1);
+        }
+    };
+    int64_t slo, shi;
+    stim_bounds(t, slo, shi);
     for (int s = 0; s < steps; ++s, ++t) {
-        const int cur = t & 1, prv = cur ^ 1;
+        const int cur = t & 1;
         uint32_t* act_now = ca.act3 + (t % 3) * words;
         if (warp == 0) {
             bool fired = false, act = false;
             if (own) {
-                double v = na.v[j];
-                const double rst = na.reset[j];
-                double u = na.abm ? in : leak_toward(v, na.leak[j], rst) + in;
-                const int row = t - na.st_base;
-                if (row >= 0 && row < na.st_steps) {
-                    int64_t lo = na.st_off[row], hi = na.st_off[row + 1];
-                    if (hi > lo) {
-                        double ext = 0.0;
-                        while (lo < hi) {
-                            const int64_t mid = (lo + hi) >> 1;
-                            const int nid = na.st_neuron[mid];
-                            if (nid == j) { ext = na.st_amp[mid]; break; }
-                            if (nid < j) lo = mid + 1; else hi = mid;
-                        }
-                        u += ext;
+                double u = na.abm ? in : leak_toward(v, leak, rst) + in;
+                if (shi > slo) {
+                    int64_t lo = slo, hi = shi;
+                    double ext = 0.0;
+                    while (lo < hi) {
+                        const int64_t mid = (lo + hi) >> 1;
+                        const int nid = __ldg(na.st_neuron + mid);
+                        if (nid == j) { ext = __ldg(na.st_amp + mid); break; }
+                        if (nid < j) lo = mid + 1; else hi = mid;
                     }
+                    u += ext;
                 }
-                if (na.abm) u = leak_toward(v, na.leak[j], rst) + u;
-                fired = u > na.thr[j];
-                if (fired && na.fire_p) {
-                    const double p = na.fire_p[j];
-                    if (p < 1.0) fired = agent_fires(na.agent_key[j], t, p);
-                }
-                const int cnt = na.cnt[j];
+                if (na.abm) u = leak_toward(v, leak, rst) + u;
+                fired = u > thr;
+                if (fired && fire_p < 1.0) fired = agent_fires(akey, t, fire_p);
                 if (cnt > 0) {
                     fired = false;
-                    na.cnt[j] = cnt - 1;
+                    cnt -= 1;
                     u = rst;
                 }
                 if (fired) {
                     v = rst;
-                    na.cnt[j] = na.refr[j];
+                    cnt = refr;
                 } else {
                     v = u;
                 }
-                na.v[j] = v;
                 if (na.trace && (t - na.t_base) < na.raster_rows)
                     na.trace[static_cast<int64_t>(t - na.t_base) * na.nl + j] = v;
-                const uint64_t hn = (__ldcg(ca.hist2 + static_cast<int64_t>(prv) * n + j) << 1) | (fired ? 1ull : 0ull);
+                const uint64_t hn = (hprev << 1) | (fired ? 1ull : 0ull);
+                hprev = hn;
                 ca.hist2[static_cast<int64_t>(cur) * n + j] = hn;
                 act = (hn & dmask) != 0;
                 if (STDP) {
@@ -1333,6 +1353,7 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
             }
         }
         grid.sync();
+        stim_bounds(t + 1, slo, shi);  // in flight during the sweep
         if (c == 0)  // clear the activity words of step t + 2 (last read by the sweep of step t - 1)
             for (int k = tid; k < words; k += kColThreads) ca.act3[((t + 2) % 3) * words + k] = 0u;
         // sweep of the CTA's columns: STDP of step t, delivery of step t + 1
@@ -1407,7 +1428,11 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
         if (warp == 0 && lane < kColW) in = s_red[0][lane];
         __syncthreads();
     }
-    if (own) da.partial[j] = in;  // (same buffer as na.partial) input of the next call's first step
+    if (own) {
+        da.partial[j] = in;  // (same buffer as na.partial) input of the next call's first step
+        na.v[j] = v;
+        na.cnt[j] = cnt;
+    }
     if (blockIdx.x == 0 && tid == 0) *na.d_step = t;
 }
 
