@@ -1370,8 +1370,12 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
         }
         const uint64_t* hist = ca.hist2 + static_cast<int64_t>(cur) * n;
         const WT* potc = pot2 + static_cast<int64_t>(cur) * n * da.dp;
+        // every load of a row is issued before its activity bit is tested: the
+        // rows of a small net sit in L2 and one round trip per row pair is the
+        // cost that matters here
+#pragma unroll 2
         for (int i = rl; i < n; i += RL) {
-            if (!((__ldcg(act_now + (i >> 5)) >> (i & 31)) & 1u)) continue;
+            const uint32_t aword = __ldcg(act_now + (i >> 5));
             const uint64_t eb = __ldcg(hist + i);
             WT* wrow = W + static_cast<int64_t>(i) * pitch + j0;
             V wv = VT::load(wrow);
@@ -1386,6 +1390,7 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
                 kind = da.kind[i];
                 if (kind == kRowMixed) mw = da.mask[static_cast<int64_t>(i) * mpitch + (j0 >> 5)];
             }
+            if (!((aword >> (i & 31)) & 1u)) continue;
             bool changed = false;
 #pragma unroll
             for (int k = 0; k < VEC; ++k) {
