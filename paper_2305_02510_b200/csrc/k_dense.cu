@@ -1,0 +1,478 @@
+// Dense sweeps over W[pre][post]: exact-order k_dense_sweep, streaming
+// k_dense_stream and the TMA-staged k_dense_tma (the cfg3 hot kernel).
+#include "kernels_common.cuh"
+
+namespace snb {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Dense sweep: W[pre][post] row-major (pre-major like mat_engine.cpp:34-38),
+// column tiles x row chunks.  For each active row i (ascending) and each of the
+// thread's VEC local columns j:
+//   plastic: w' = clamp(w + s_j[t] pot_i^(d) - e_ij dep_j, w_min, w_max)
+//   e_ij = s_i[t+1-d_ij] (history bit d-1): input to post j at step t+1
+//   acc_j += e_ij * w'
+// Non-exact: per-thread fp32 group sums of U rows promoted to fp64, partials
+// per row chunk summed by k_neuron in chunk order (deterministic; exact for
+// integer nets).  Exact: one chunk, fp64 accumulator seeded with leak(v_j)
+// and rows added in ascending order exactly as mat_step does.
+template <typename WT, bool STDP, bool DELAY, bool EXACT>
+__global__ void __launch_bounds__(kThreads) k_dense_sweep(DenseArgs a) {
+    using VT = VecT<WT>;
+    using V = typename VT::V;
+    constexpr int VEC = VT::N;
+    constexpr int U = 8;  // rows in flight per thread
+
+    __shared__ int32_t s_rows[kSubRows];
+    __shared__ uint64_t s_e[kSubRows];
+    __shared__ WT s_pot[STDP && !DELAY ? kSubRows : 1];
+    __shared__ uint8_t s_kind[kSubRows];
+    __shared__ uint32_t s_word[32];
+    __shared__ int32_t s_wpref[33];
+
+    const int tid = threadIdx.x;
+    const int ntiles = (a.nl + a.tile_w - 1) / a.tile_w;
+    const int items = ntiles * a.nchunks;
+    const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
+    const WT* pot = static_cast<const WT*>(a.pot);
+    const WT* dep = static_cast<const WT*>(a.dep);
+    WT* W = static_cast<WT*>(a.w);
+    const uint64_t dmask = DELAY ? ~0ull : 1ull;
+
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int chunk = item / ntiles;
+        const int tile = item - chunk * ntiles;
+        const int tcol = tid * VEC;
+        const int c0 = tile * a.tile_w + tcol;
+        const bool in_tile = tcol < a.tile_w && c0 < a.nl;
+        const int r0 = chunk * a.rows_per_chunk;
+        const int r1 = min(a.n, r0 + a.rows_per_chunk);
+
+        bool sj[VEC];
+        WT depj[VEC];
+        int gc[VEC];
+        double acc[VEC];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+            gc[k] = a.first + c0 + k;
+            const bool ok = in_tile && (c0 + k) < a.nl;
+            sj[k] = ok && STDP ? bit_of(a.bits, gc[k]) : false;
+            depj[k] = ok && STDP ? dep[gc[k]] : WT(0);
+            acc[k] = (EXACT && ok && !a.abm) ? leak_toward(a.v[c0 + k], a.leak[c0 + k], a.reset[c0 + k]) : 0.0;
+        }
+
+        for (int sa = r0; sa < r1; sa += kSubRows) {
+            const int sb = min(r1, sa + kSubRows);
+            const int nwords = (sb - sa + 31) >> 5;
+            __syncthreads();  // previous sub-chunk fully consumed
+            if (tid < 32) {
+                uint32_t wd = 0;
+                if (tid < nwords) {
+                    wd = __ldcg(a.active + (sa >> 5) + tid);
+                    const int rem = sb - (sa + tid * 32);
+                    if (rem < 32) wd &= (rem <= 0) ? 0u : ((1u << rem) - 1u);
+                }
+                const int c = __popc(wd);
+                int incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int x = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (tid >= o) incl += x;
+                }
+                s_word[tid] = wd;
+                s_wpref[tid] = incl - c;
+                if (tid == 31) s_wpref[32] = incl;
+            }
+            __syncthreads();
+            for (int r = sa + tid; r < sb; r += kThreads) {
+                const int l = (r - sa) >> 5, b = (r - sa) & 31;
+                const uint32_t wd = s_word[l];
+                if ((wd >> b) & 1u) {
+                    const int pos = s_wpref[l] + __popc(wd & ((1u << b) - 1u));
+                    s_rows[pos] = r;
+                    s_e[pos] = __ldg(a.hist + r) & dmask;
+                    if (STDP) s_kind[pos] = __ldg(a.kind + r);
+                    if (STDP && !DELAY) s_pot[pos] = pot[r];
+                }
+            }
+            __syncthreads();
+            const int cnt = s_wpref[32];
+
+            for (int gb = 0; gb < cnt; gb += U) {
+                V wv[U];
+                uint32_t dv[U];
+                uint32_t mv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int idx = gb + u;
+                    dv[u] = 0x01010101u;
+                    mv[u] = 0;
+                    if (idx < cnt && in_tile) {
+                        const int row = s_rows[idx];
+                        const int64_t off = static_cast<int64_t>(row) * a.pitch + c0;
+                        wv[u] = VT::load(W + off);
+                        if (DELAY) {
+                            if (VEC == 4) dv[u] = __ldg(reinterpret_cast<const uint32_t*>(a.delay + off));
+                            else dv[u] = __ldg(reinterpret_cast<const uint16_t*>(a.delay + off));
+                        }
+                        if (STDP && s_kind[idx] == kRowMixed)
+                            mv[u] = __ldg(a.mask + static_cast<int64_t>(row) * (a.pitch >> 5) + (c0 >> 5)) >> (c0 & 31);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < VEC; ++k) VT::set(wv[u], k, WT(0));
+                    }
+                }
+                WT grp[VEC];
+#pragma unroll
+                for (int k = 0; k < VEC; ++k) grp[k] = WT(0);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int idx = gb + u;
+                    if (idx >= cnt || !in_tile) continue;
+                    const int row = s_rows[idx];
+                    const uint64_t ebits = s_e[idx];
+                    bool changed = false;
+                    uint8_t kind = STDP ? s_kind[idx] : uint8_t(kRowNone);
+#pragma unroll
+                    for (int k = 0; k < VEC; ++k) {
+                        WT w = VT::get(wv[u], k);
+                        const int d1 = DELAY ? static_cast<int>((dv[u] >> (8 * k)) & 0xffu) - 1 : 0;
+                        const bool e = (ebits >> d1) & 1ull;
+                        if (STDP && kind != kRowNone) {
+                            const bool pl = kind == kRowAll || (kind == kRowAllButSelf && gc[k] != row) ||
+                                            (kind == kRowMixed && ((mv[u] >> k) & 1u));
+                            if (pl) {
+                                const WT p = DELAY ? pot[static_cast<int64_t>(row) * a.dp + d1] : s_pot[idx];
+                                // dw = 0; if s_post: dw += pot; if s_pre: dw -= dep (243-246)
+                                WT dw = WT(0);
+                                if (sj[k]) dw += p;
+                                if (e) dw -= depj[k];
+                                const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
+                                changed |= (nw != w);
+                                w = nw;
+                                VT::set(wv[u], k, nw);
+                            }
+                        }
+                        if (e) {
+                            if (EXACT) acc[k] += static_cast<double>(w);
+                            else grp[k] += w;
+                        }
+                    }
+                    if (STDP && changed) {
+                        VT::store(W + static_cast<int64_t>(row) * a.pitch + c0, wv[u]);
+                    }
+                }
+                if (!EXACT) {
+#pragma unroll
+                    for (int k = 0; k < VEC; ++k) acc[k] += static_cast<double>(grp[k]);
+                }
+            }
+        }
+        if (in_tile) {
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) {
+                if (c0 + k < a.nl) {
+                    if (EXACT) a.u_exact[c0 + k] = acc[k];
+                    else a.partial[static_cast<int64_t>(chunk) * a.nl + c0 + k] = acc[k];
+                }
+            }
+        }
+    }
+    if (blockIdx.x == 0 && tid == 0) *a.d_step += 1;  // no other CTA reads it
+}
+
+template <typename WT, bool STDP, bool DELAY>
+__global__ void __launch_bounds__(kThreads, 2) k_dense_stream(DenseArgs a) {
+    dense_stream_body<WT, STDP, DELAY>(a, blockIdx.x, gridDim.x);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.d_step += 1;  // no other CTA reads it
+}
+
+// ---------------------------------------------------------------------------
+// TMA-staged dense sweep (fp32, unit delays): one CTA per SM, a producer warp
+// streams the active rows' tile segments into a kTmaStages-deep shared-memory
+// ring with cp.async.bulk (completion on mbarriers), 8 consumer warps apply
+// the same per-element update as k_dense_stream from shared memory and write
+// the new weights with 128-bit streaming stores.  Loads never occupy
+// registers, so the in-flight window per SM is the whole ring.
+constexpr int kTmaRows = 4;        // rows per stage
+constexpr int kTmaStages = 8;      // ring depth
+constexpr int kTmaListMax = 2048;  // rows per item (one list build per item)
+constexpr int kTmaThreads = 288;   // 8 consumer warps + 1 producer warp
+
+template <bool STDP>
+__global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const bool producer = warp == 8;
+    const int ntiles = (a.nl + a.tile_w - 1) / a.tile_w;
+    const int items = ntiles * a.nchunks;
+    const uint32_t row_bytes = static_cast<uint32_t>(a.tile_w) * 4u;
+    const size_t stage_bytes = static_cast<size_t>(kTmaRows) * row_bytes;
+    float* ring = reinterpret_cast<float*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * stage_bytes);
+    uint64_t* empty = full + kTmaStages;
+    RowRec<float>* s_rec = reinterpret_cast<RowRec<float>*>(empty + kTmaStages);
+    __shared__ uint32_t s_word[32];
+    __shared__ int32_t s_wpref[33];
+    __shared__ int32_t s_cnt;
+    __shared__ int s_item;
+
+    const float wmin = static_cast<float>(a.w_min), wmax = static_cast<float>(a.w_max);
+    const float* dep = static_cast<const float*>(a.dep);
+    const float* pot = static_cast<const float*>(a.pot);
+    float* W = static_cast<float*>(a.w);
+
+    if (tid == 0) {
+        for (int s = 0; s < kTmaStages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    uint32_t it = 0;  // ring position, advanced identically by producer and consumers
+    int item = blockIdx.x;
+    if (a.work) {
+        if (tid == 0) s_item = atomicAdd(a.work, 1);
+        __syncthreads();
+        item = s_item;
+    }
+    while (item < items) {
+        const int chunk = item / ntiles;
+        const int tile = item - chunk * ntiles;
+        const int col0 = tile * a.tile_w;
+        const int width = static_cast<int>(min(static_cast<int64_t>(a.tile_w), a.pitch - col0));
+        const uint32_t copy_bytes = static_cast<uint32_t>(width) * 4u;
+        const int r0 = chunk * a.rows_per_chunk;
+        const int r1 = min(a.n, r0 + a.rows_per_chunk);
+
+        // active-row list of [r0, r1) in <= 1024-row pieces (32-aligned bases)
+        if (tid == 0) s_cnt = 0;
+        __syncthreads();
+        for (int sa = r0, sb_next = r0; sa < r1; sa = sb_next) {
+            const int base = sa & ~31;
+            const int sb = min(r1, base + kSubRows);
+            sb_next = sb;
+            const int nwords = (sb - base + 31) >> 5;
+            const int cnt0 = s_cnt;
+            if (tid < 32) {
+                uint32_t wd = 0;
+                if (tid < nwords) {
+                    wd = __ldcg(a.active + (base >> 5) + tid);
+                    const int lo = sa - (base + tid * 32);
+                    if (lo > 0) wd &= (lo >= 32) ? 0u : ~((1u << lo) - 1u);
+                    const int rem = sb - (base + tid * 32);
+                    if (rem < 32) wd &= (rem <= 0) ? 0u : ((1u << rem) - 1u);
+                }
+                const int c = __popc(wd);
+                int incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int x = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (tid >= o) incl += x;
+                }
+                s_word[tid] = wd;
+                s_wpref[tid] = cnt0 + incl - c;
+                if (tid == 31) s_wpref[32] = cnt0 + incl;
+            }
+            __syncthreads();
+            for (int r = sa + tid; r < sb; r += kTmaThreads) {
+                const int l = (r - base) >> 5, b = (r - base) & 31;
+                const uint32_t wd = s_word[l];
+                if ((wd >> b) & 1u) {
+                    const int pos = s_wpref[l] + __popc(wd & ((1u << b) - 1u));
+                    const uint64_t h = __ldcg(a.hist + r);
+                    RowRec<float> rec;
+                    const int kind = STDP ? static_cast<int>(__ldg(a.kind + r)) : 0;
+                    rec.rowk = r | (kind << 28);
+                    rec.e_lo = static_cast<uint32_t>(h);
+                    rec.e_hi = static_cast<uint32_t>(h >> 32);
+                    rec.pot = STDP ? __ldcg(pot + r) : 0.f;
+                    s_rec[pos] = rec;
+                }
+            }
+            __syncthreads();
+            if (tid == 0) s_cnt = s_wpref[32];
+            __syncthreads();
+        }
+        const int cnt = s_cnt;
+        const int ngroups = (cnt + kTmaRows - 1) / kTmaRows;
+
+        if (producer) {
+            if (lane == 0) {
+                for (int g = 0; g < ngroups; ++g, ++it) {
+                    const int s = it % kTmaStages;
+                    const uint32_t ph = (it / kTmaStages) & 1u;
+                    mbar_wait(empty + s, ph ^ 1u);
+                    const int nr = min(kTmaRows, cnt - g * kTmaRows);
+                    mbar_arrive_expect_tx(full + s, static_cast<uint32_t>(nr) * copy_bytes);
+                    for (int r = 0; r < nr; ++r) {
+                        const int row = s_rec[g * kTmaRows + r].rowk & 0x0fffffff;
+                        bulk_g2s(reinterpret_cast<uint8_t*>(ring) + s * stage_bytes + static_cast<size_t>(r) * row_bytes,
+                                 W + static_cast<int64_t>(row) * a.pitch + col0, copy_bytes, full + s);
+                    }
+                }
+            } else {
+                it += ngroups;
+            }
+        } else {
+            const int tcol = tid * 4;
+            const int c0 = col0 + tcol;
+            const bool in_tile = tcol < width && c0 < a.nl;
+            const int gc0 = a.first + c0;
+            float sjf[4], depj[4];
+            double acc[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const bool ok = in_tile && (c0 + k) < a.nl;
+                sjf[k] = (ok && STDP && bit_of(a.bits, gc0 + k)) ? 1.f : 0.f;
+                depj[k] = (ok && STDP) ? __ldcg(dep + gc0 + k) : 0.f;
+                acc[k] = 0.0;
+            }
+            for (int g = 0; g < ngroups; ++g, ++it) {
+                const int s = it % kTmaStages;
+                const uint32_t ph = (it / kTmaStages) & 1u;
+                mbar_wait(full + s, ph);
+                const int nr = min(kTmaRows, cnt - g * kTmaRows);
+                float grp[4] = {0.f, 0.f, 0.f, 0.f};
+                if (in_tile) {
+#pragma unroll
+                    for (int r = 0; r < kTmaRows; ++r) {
+                        if (r >= nr) break;
+                        const RowRec<float> rec = s_rec[g * kTmaRows + r];
+                        const int row = rec.rowk & 0x0fffffff;
+                        const int kind = rec.rowk >> 28;
+                        const float4 wv = *reinterpret_cast<const float4*>(
+                            reinterpret_cast<const uint8_t*>(ring) + s * stage_bytes + static_cast<size_t>(r) * row_bytes + tcol * 4);
+                        float w[4] = {wv.x, wv.y, wv.z, wv.w};
+                        const float ef = (rec.e_lo & 1u) ? 1.f : 0.f;
+                        if (STDP && kind != kRowNone) {
+                            float nw[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const float dw = fmaf(sjf[k], rec.pot, -(ef * depj[k]));
+                                nw[k] = clamp_ref<float>(w[k] + dw, wmin, wmax);
+                            }
+                            if (kind == kRowAllButSelf) {
+                                const int selfk = row - gc0;
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) nw[k] = (selfk == k) ? w[k] : nw[k];
+                            } else if (kind == kRowMixed) {
+                                const uint32_t mv =
+                                    __ldg(a.mask + static_cast<int64_t>(row) * (a.pitch >> 5) + (c0 >> 5)) >> (c0 & 31);
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) nw[k] = ((mv >> k) & 1u) ? nw[k] : w[k];
+                            }
+                            __stcs(reinterpret_cast<float4*>(W + static_cast<int64_t>(row) * a.pitch + c0),
+                                   make_float4(nw[0], nw[1], nw[2], nw[3]));
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) w[k] = nw[k];
+                        }
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) grp[k] = fmaf(ef, w[k], grp[k]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + s);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc[k] += static_cast<double>(grp[k]);
+            }
+            if (in_tile) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (c0 + k < a.nl) a.partial[static_cast<int64_t>(chunk) * a.nl + c0 + k] = acc[k];
+            }
+        }
+        __syncthreads();  // ring drained for this item's rows; list may be rebuilt
+        if (a.work) {
+            if (tid == 0) s_item = atomicAdd(a.work, 1);
+            __syncthreads();
+            item = s_item;
+        } else {
+            item += gridDim.x;
+        }
+    }
+    if (blockIdx.x == 0 && tid == 0) *a.d_step += 1;
+}
+
+size_t dense_tma_smem(int tile_w) {
+    return static_cast<size_t>(kTmaStages) * kTmaRows * tile_w * 4 + 2 * kTmaStages * 8 +
+           static_cast<size_t>(kTmaListMax + kTmaRows) * sizeof(RowRec<float>);
+}
+
+}  // namespace
+
+int dense_vec(bool f64) { return f64 ? 2 : 4; }
+
+int dense_tma_max_rows() { return kTmaListMax; }
+
+void launch_dense_tma(const DenseArgs& a, bool stdp, int grid, cudaStream_t s) {
+    const size_t smem = dense_tma_smem(a.tile_w);
+    static size_t configured[2] = {0, 0};
+    auto kern = stdp ? k_dense_tma<true> : k_dense_tma<false>;
+    if (configured[stdp ? 1 : 0] < smem) {
+        check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+              "k_dense_tma smem attribute");
+        configured[stdp ? 1 : 0] = smem;
+    }
+    kern<<<grid, kTmaThreads, smem, s>>>(a);
+    check(cudaGetLastError(), "k_dense_tma");
+}
+int dense_threads() { return kThreads; }
+template <typename WT, bool STDP, bool DELAY, bool EXACT>
+static void dense_go(const DenseArgs& a, int grid, cudaStream_t s) {
+    if (EXACT) k_dense_sweep<WT, STDP, DELAY, true><<<grid, kThreads, 0, s>>>(a);
+    else k_dense_stream<WT, STDP, DELAY><<<grid, kThreads, 0, s>>>(a);
+}
+
+template <typename WT, bool STDP, bool DELAY>
+static int stream_occ() {
+    int dev = 0, sms = 0, occ = 0;
+    check(cudaGetDevice(&dev), "cudaGetDevice");
+    check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dense_stream<WT, STDP, DELAY>, kThreads, 0),
+          "occupancy");
+    return occ * sms;
+}
+
+int dense_stream_max_ctas(bool f64, bool stdp, bool delay) {
+    if (f64) {
+        if (stdp) return delay ? stream_occ<double, true, true>() : stream_occ<double, true, false>();
+        return delay ? stream_occ<double, false, true>() : stream_occ<double, false, false>();
+    }
+    if (stdp) return delay ? stream_occ<float, true, true>() : stream_occ<float, true, false>();
+    return delay ? stream_occ<float, false, true>() : stream_occ<float, false, false>();
+}
+
+void launch_dense(const DenseArgs& a, bool f64, bool stdp, bool delay, bool exact, int grid,
+                  cudaStream_t s) {
+#define SNB_DENSE(WT)                                                            \
+    do {                                                                         \
+        if (stdp) {                                                              \
+            if (delay) {                                                         \
+                if (exact) dense_go<WT, true, true, true>(a, grid, s);           \
+                else dense_go<WT, true, true, false>(a, grid, s);                \
+            } else {                                                             \
+                if (exact) dense_go<WT, true, false, true>(a, grid, s);          \
+                else dense_go<WT, true, false, false>(a, grid, s);               \
+            }                                                                    \
+        } else {                                                                 \
+            if (delay) {                                                         \
+                if (exact) dense_go<WT, false, true, true>(a, grid, s);          \
+                else dense_go<WT, false, true, false>(a, grid, s);               \
+            } else {                                                             \
+                if (exact) dense_go<WT, false, false, true>(a, grid, s);         \
+                else dense_go<WT, false, false, false>(a, grid, s);              \
+            }                                                                    \
+        }                                                                        \
+    } while (0)
+    if (f64) SNB_DENSE(double);
+    else SNB_DENSE(float);
+#undef SNB_DENSE
+    check(cudaGetLastError(), "k_dense_sweep");
+}
+
+}  // namespace snb

@@ -1,0 +1,103 @@
+// Neuron phase: LIF update + spike words + history/traces (k_neuron), the
+// history kernel of partitioned runs (k_hist), and two helpers.
+#include "kernels_common.cuh"
+
+namespace snb {
+
+namespace {
+
+template <bool EXACT, bool FUSED>
+__global__ void __launch_bounds__(kThreads) k_neuron(NeuronArgs a, HistArgs h) {
+    const int t = *a.d_step;
+    neuron_step<EXACT, FUSED>(a, h, blockIdx.x * kThreads + threadIdx.x, t);
+    if (a.peer_bits) {
+        // publish step t to every rank once all CTAs' words are out: each CTA
+        // fences its peer stores system-wide and counts itself; the last CTA
+        // releases flag[rank] = t + 1 in every rank's flag array
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t prev = atomicAdd(a.done, 1u);
+            if (prev == gridDim.x - 1) {
+                __threadfence_system();
+                for (int q = 0; q < a.world; ++q) st_release_sys(a.peer_flags[q] + a.rank, t + 1);
+                *a.done = 0;
+            }
+        }
+    }
+}
+
+// Partitioned runs: history/traces for all N from the all-gathered bitmask.
+__global__ void __launch_bounds__(kThreads) k_hist(HistArgs h) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    const int t = *h.d_step;
+    if (h.flags) {  // peer-to-peer exchange: wait for every rank's words of step t
+        if (threadIdx.x == 0) {
+            const uint64_t t0 = globaltimer_ns();
+            for (int q = 0; q < h.world; ++q) {
+                while (ld_acquire_sys(h.flags + q) <= t) {
+                    if (globaltimer_ns() - t0 > 30ull * 1000000000ull) {  // 30 s: a peer died
+                        atomicExch(h.error, 1);
+                        break;
+                    }
+                    __nanosleep(200);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    bool act = false;
+    if (i < h.n) {
+        const bool s = (h.bits[i >> 5] >> (i & 31)) & 1u;
+        act = hist_update(h, i, s, t);
+    }
+    const uint32_t aw = __ballot_sync(0xffffffffu, act);
+    if ((threadIdx.x & 31) == 0 && (i >> 5) < ((h.n + 31) >> 5)) {
+        h.active[i >> 5] = aw;
+        if (aw) atomicAdd(h.active_count, static_cast<unsigned long long>(__popc(aw)));
+    }
+}
+
+__global__ void k_prologue(double* u, const double* v, const double* leak, const double* reset,
+                           int nl, int abm) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < nl) u[j] = abm ? 0.0 : leak_toward(v[j], leak[j], reset[j]);
+}
+
+__global__ void k_step_bump(int32_t* d_step) { *d_step += 1; }
+
+}  // namespace
+
+void launch_neuron(const NeuronArgs& a, bool exact, bool fused, const HistArgs& h, cudaStream_t s) {
+    int grid = (a.nl + kThreads - 1) / kThreads;
+    if (a.peer_bits && grid == 0) grid = 1;  // an empty partition still publishes its step
+    if (grid == 0) return;
+    if (exact) {
+        if (fused) k_neuron<true, true><<<grid, kThreads, 0, s>>>(a, h);
+        else k_neuron<true, false><<<grid, kThreads, 0, s>>>(a, h);
+    } else {
+        if (fused) k_neuron<false, true><<<grid, kThreads, 0, s>>>(a, h);
+        else k_neuron<false, false><<<grid, kThreads, 0, s>>>(a, h);
+    }
+    check(cudaGetLastError(), "k_neuron");
+}
+
+void launch_hist(const HistArgs& h, cudaStream_t s) {
+    const int grid = (h.n + kThreads - 1) / kThreads;
+    k_hist<<<grid, kThreads, 0, s>>>(h);
+    check(cudaGetLastError(), "k_hist");
+}
+
+void launch_prologue(double* u, const double* v, const double* leak, const double* reset, int nl,
+                     bool abm, cudaStream_t s) {
+    if (nl <= 0) return;
+    k_prologue<<<(nl + 255) / 256, 256, 0, s>>>(u, v, leak, reset, nl, abm ? 1 : 0);
+    check(cudaGetLastError(), "k_prologue");
+}
+
+void launch_step_bump(int32_t* d_step, cudaStream_t s) {
+    k_step_bump<<<1, 1, 0, s>>>(d_step);
+    check(cudaGetLastError(), "k_step_bump");
+}
+
+}  // namespace snb

@@ -1,0 +1,593 @@
+// Whole-call step loops: k_tiny (one CTA, shared-memory state),
+// k_persistent_dense (row chunks) and k_persistent_cols (column owners).
+#include "kernels_common.cuh"
+
+namespace snb {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Tiny nets: one CTA runs the whole call with every array in shared memory.
+// Per step: (1) thread j integrates post j -- leak, its incoming list in
+// ascending pre order (history bit d-1 of the pre = s_pre[t-d]), the step's
+// stimulus, threshold/refractory/reset; (2) history shift, raster word (warp
+// ballot), STDP traces; (3) thread j applies STDP to its own plastic synapses
+// (mat_engine.cpp:242-249, every plastic synapse every step).  One CTA barrier
+// per step (double-buffered history), no global memory on the critical path.
+struct TinyLayout {
+    size_t hist, pot, dep, off, meta, pidx, w, st_off, st_neuron, st_amp, ap, am, total;
+};
+
+__host__ __device__ inline size_t tiny_align(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
+
+// Shared memory: history as 32-bit words, double-buffered (buffer b, word k,
+// neuron j at [(b * 2hw + k) * np + j]) so one barrier per step separates the
+// readers of step t from the writers of step t+1; STDP traces double-buffered
+// the same way.  Per-neuron LIF state lives in the owning thread's registers.
+__host__ __device__ inline TinyLayout tiny_layout(const TinyArgs& a) {
+    TinyLayout L{};
+    const size_t np = static_cast<size_t>((a.n + 31) / 32 * 32);
+    size_t o = 0;
+    L.hist = o; o = tiny_align(o + 2 * np * 8 * a.hw);
+    L.pot = o; o = tiny_align(o + (a.stdp ? 2 * np * 8 * a.dp : 0));
+    L.dep = o; o = tiny_align(o + (a.stdp ? 2 * np * 8 : 0));
+    L.off = o; o = tiny_align(o + (static_cast<size_t>(a.n) + 1) * 4);
+    L.meta = o; o = tiny_align(o + static_cast<size_t>(a.m) * 4);
+    L.pidx = o; o = tiny_align(o + (a.stdp ? static_cast<size_t>(a.m) * 2 : 0));
+    // weights in smem: as stored for STDP nets (the update runs in WT), as
+    // double otherwise (no per-synapse conversion on the integration path)
+    L.w = o; o = tiny_align(o + static_cast<size_t>(a.m) * ((a.f64 || !a.stdp) ? 8 : 4));
+    L.st_off = o; o = tiny_align(o + (static_cast<size_t>(a.steps) + 1) * 4);
+    L.st_neuron = o; o = tiny_align(o + static_cast<size_t>(a.st_count) * 4);
+    L.st_amp = o; o = tiny_align(o + static_cast<size_t>(a.st_count) * 8);
+    L.ap = o; o = tiny_align(o + (a.stdp ? static_cast<size_t>(a.window) * 8 : 0));
+    L.am = o; o = tiny_align(o + (a.stdp ? static_cast<size_t>(a.window) * 8 : 0));
+    L.total = o;
+    return L;
+}
+
+// Bit test of one incoming synapse: meta = byte offset of the 32-bit history
+// word within a buffer << 5 | bit; the funnel shift uses the low 5 bits.
+__device__ __forceinline__ bool tiny_bit(const uint8_t* buf, uint32_t mq) {
+    const uint32_t word = *reinterpret_cast<const uint32_t*>(buf + (mq >> 5));
+    return __funnelshift_r(word, word, mq) & 1u;
+}
+
+template <typename WT, bool STDP>
+__global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    const TinyLayout L = tiny_layout(a);
+    const int tid = threadIdx.x;
+    const int n = a.n;
+    const int np = (n + 31) / 32 * 32;
+    const int hw2 = 2 * a.hw;
+    const size_t hbuf = static_cast<size_t>(hw2) * np * 4;  // bytes per history buffer
+    uint32_t* hist = reinterpret_cast<uint32_t*>(sm + L.hist);
+    double* pot = reinterpret_cast<double*>(sm + L.pot);
+    double* dep = reinterpret_cast<double*>(sm + L.dep);
+    uint32_t* off = reinterpret_cast<uint32_t*>(sm + L.off);
+    uint32_t* meta = reinterpret_cast<uint32_t*>(sm + L.meta);
+    uint16_t* pidx = reinterpret_cast<uint16_t*>(sm + L.pidx);
+    using WS = typename std::conditional<STDP, WT, double>::type;  // smem weight type
+    WS* w = reinterpret_cast<WS*>(sm + L.w);
+    int32_t* st_off = reinterpret_cast<int32_t*>(sm + L.st_off);
+    int32_t* st_neuron = reinterpret_cast<int32_t*>(sm + L.st_neuron);
+    double* st_amp = reinterpret_cast<double*>(sm + L.st_amp);
+    double* ap = reinterpret_cast<double*>(sm + L.ap);
+    double* am = reinterpret_cast<double*>(sm + L.am);
+    // ---- load: owned neuron state into registers, shared arrays ----
+    const int j = tid;
+    const bool own = j < n;
+    double v = own ? a.v[j] : 0.0;
+    const double thr = own ? a.thr[j] : 0.0;
+    const double leak = own ? a.leak[j] : 0.0;
+    const double rst = own ? a.reset[j] : 0.0;
+    const int32_t refr = own ? a.refr[j] : 0;
+    int32_t cnt = own ? a.cnt[j] : 0;
+    const double fire_p = (own && a.fire_p) ? a.fire_p[j] : 1.0;
+    const uint64_t akey = fire_p < 1.0 ? a.agent_key[j] : 0ull;
+    for (int k = 0; k < a.hw; ++k) {
+        const uint64_t x = own ? a.hist[static_cast<int64_t>(k) * n + j] : 0ull;
+        hist[(2 * k) * np + j] = static_cast<uint32_t>(x);
+        hist[(2 * k + 1) * np + j] = static_cast<uint32_t>(x >> 32);
+    }
+    const int nt = blockDim.x;
+    for (int i = tid; i <= n; i += nt) off[i] = a.off[i];
+    for (int q = tid; q < a.m; q += nt) {
+        meta[q] = a.meta[q];
+        w[q] = static_cast<WS>(static_cast<const WT*>(a.w)[q]);
+        if (STDP) pidx[q] = a.pidx[q];
+    }
+    const int64_t sbase = a.st_rows > 0 ? a.st_off[0] : 0;
+    for (int s = tid; s <= a.steps; s += nt)
+        st_off[s] = a.st_rows > 0 ? static_cast<int32_t>(a.st_off[min(s, a.st_rows)] - sbase) : 0;
+    for (int e = tid; e < a.st_count; e += nt) {
+        st_neuron[e] = a.st_neuron[sbase + e];
+        st_amp[e] = a.st_amp[sbase + e];
+    }
+    if (STDP)
+        for (int k = tid; k < a.window; k += nt) {
+            ap[k] = a.a_plus[k];
+            am[k] = a.a_minus[k];
+        }
+    __syncthreads();
+    const int t0 = *a.d_step;
+    const int words = (n + 31) / 32;
+    const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
+    const uint32_t q0 = own ? off[j] : 0u, q1 = own ? off[j + 1] : 0u;
+    unsigned long long spikes = 0;
+    for (int s = 0; s < a.steps; ++s) {
+        const int cur = s & 1;
+        const uint8_t* hc = sm + L.hist + cur * hbuf;        // history through t-1
+        uint32_t* hn = reinterpret_cast<uint32_t*>(sm + L.hist + (cur ^ 1) * hbuf);  // through t
+        bool fired = false;
+        if (own) {
+            // (1) leak, incoming list in ascending pre order (bit d-1 = s_pre[t-d]),
+            // the step's stimulus, threshold, refractory (mat_engine.cpp:160-198)
+            // MAT: u = leak(v) + w...; ABM: pending = 0.0 + w..., u = leak(v) + (pending + ext)
+            double u = a.abm ? 0.0 : leak_toward(v, leak, rst);
+#pragma unroll 4
+            for (uint32_t q = q0; q < q1; ++q) {
+                const uint32_t mq = meta[q];
+                if (tiny_bit(hc, mq)) u += static_cast<double>(w[q]);  // WS = double unless STDP
+            }
+            int lo = st_off[s], hi = st_off[s + 1];
+            if (hi > lo) {
+                double ext = 0.0;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    const int nm = st_neuron[mid];
+                    if (nm == j) { ext = st_amp[mid]; break; }
+                    if (nm < j) lo = mid + 1; else hi = mid;
+                }
+                u += ext;
+            }
+            if (a.abm) u = leak_toward(v, leak, rst) + u;
+            fired = u > thr;
+            if (fired && fire_p < 1.0) fired = agent_fires(akey, t0 + s, fire_p);
+            if (cnt > 0) {
+                fired = false;
+                cnt -= 1;
+                u = rst;
+            }
+            if (fired) {
+                v = rst;
+                cnt = refr;
+            } else {
+                v = u;
+            }
+            if (a.trace) a.trace[static_cast<int64_t>(s) * n + j] = v;
+        }
+        const uint32_t word = __ballot_sync(0xffffffffu, fired);
+        if ((tid & 31) == 0 && (tid >> 5) < words) {
+            a.raster[static_cast<int64_t>(s) * words + (tid >> 5)] = word;
+            spikes += __popc(word);
+        }
+        // (2) own history row into the other buffer (+ own STDP traces)
+        if (j < np) {
+            const uint32_t* hcw = reinterpret_cast<const uint32_t*>(hc);
+            uint32_t carry = fired ? 1u : 0u;
+            for (int k = 0; k < hw2; ++k) {
+                const uint32_t x = hcw[k * np + j];
+                hn[k * np + j] = (x << 1) | carry;
+                carry = x >> 31;
+            }
+            if (STDP && own) {
+                double* potn = pot + (cur ^ 1) * np * a.dp;
+                double dsum = 0.0;
+                for (int k = 1; k <= a.window; ++k)
+                    if ((hn[(k >> 5) * np + j] >> (k & 31)) & 1u) dsum += am[k - 1];
+                dep[(cur ^ 1) * np + j] = dsum;
+                for (int d = 1; d <= a.dp; ++d) {
+                    double psum = 0.0;
+                    for (int k = 1; k <= a.window; ++k) {
+                        const int b = k + d - 1;
+                        if ((hn[(b >> 5) * np + j] >> (b & 31)) & 1u) psum += ap[k - 1];
+                    }
+                    potn[j * a.dp + (d - 1)] = psum;
+                }
+            }
+        }
+        __syncthreads();  // the new history (and traces) of step t are complete
+        if (STDP && own) {
+            // (3) STDP on post j's plastic synapses: dw = 0; if s_post dw += pot^(d)_pre;
+            // if s_pre[t-d+1] dw -= dep_post; clamp (mat_engine.cpp:242-249)
+            const uint8_t* hnb = reinterpret_cast<const uint8_t*>(hn);
+            const double* potn = pot + (cur ^ 1) * np * a.dp;
+            const double depj = dep[(cur ^ 1) * np + j];
+            for (uint32_t q = q0; q < q1; ++q) {
+                const uint16_t pq = pidx[q];
+                if (pq == 0xffffu) continue;  // not plastic
+                const uint32_t mq = meta[q];
+                WT dw = WT(0);
+                if (fired) dw += static_cast<WT>(potn[pq]);
+                if (tiny_bit(hnb, mq)) dw -= static_cast<WT>(depj);
+                w[q] = clamp_ref<WT>(w[q] + dw, wmin, wmax);
+            }
+        }
+    }
+    // ---- write back (the last step's history is in buffer steps & 1) ----
+    const uint32_t* hl = reinterpret_cast<const uint32_t*>(sm + L.hist + (a.steps & 1) * hbuf);
+    if (own) {
+        a.v[j] = v;
+        a.cnt[j] = cnt;
+        for (int k = 0; k < a.hw; ++k)
+            a.hist[static_cast<int64_t>(k) * n + j] =
+                static_cast<uint64_t>(hl[(2 * k) * np + j]) | (static_cast<uint64_t>(hl[(2 * k + 1) * np + j]) << 32);
+    }
+    if (STDP) {
+        __syncthreads();  // every owner's last-step weight update is done
+        for (int q = tid; q < a.m; q += nt) static_cast<WT*>(a.w)[q] = static_cast<WT>(w[q]);
+    }
+    if (spikes) atomicAdd(a.spike_count, spikes);
+    if (tid == 0) *a.d_step = t0 + a.steps;
+}
+
+// Persistent single-GPU step loop for small dense nets (launch-latency bound
+// otherwise): one cooperative launch runs `steps` steps; neuron phase and
+// sweep phase are separated by grid-wide barriers (cooperative groups).
+template <typename WT, bool STDP, bool DELAY>
+__global__ void __launch_bounds__(kThreads, 2) k_persistent_dense(NeuronArgs na, HistArgs h, DenseArgs da,
+                                                                 int steps) {
+    cg::grid_group grid = cg::this_grid();
+    const bool single = gridDim.x == 1;
+    int t = *na.d_step;
+    const int span = ((na.nl + 31) / 32) * 32;
+    for (int s = 0; s < steps; ++s, ++t) {
+        for (int j = blockIdx.x * kThreads + threadIdx.x; j - static_cast<int>(threadIdx.x & 31) < span;
+             j += gridDim.x * kThreads)
+            neuron_step<false, true>(na, h, j, t);
+        if (single) __syncthreads(); else grid.sync();
+        dense_stream_body<WT, STDP, DELAY>(da, blockIdx.x, gridDim.x);
+        if (single) __syncthreads(); else grid.sync();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *na.d_step = t;
+}
+
+// ---------------------------------------------------------------------------
+// Column-owner persistent loop: CTA c owns posts [W c, W c + W), W = 8 (the
+// net must be small enough for every group to be co-resident).  Per step
+// (1) warp 0 updates its 8 posts from the input its own sweep produced (LIF as
+// neuron_step, history word, STDP traces, row activity) into the step's
+// parity buffers; (2) one grid barrier; (3) 1024 threads sweep every active row
+// of the CTA's 8 columns -- STDP of step t, then the delivery of step t + 1 --
+// and reduce the row-lane partials in a fixed tree.  Groups share 32-bit
+// words, so activity and raster words are OR-ed in (activity words
+// triple-buffered: the buffer of step t + 2 is cleared during step t's sweep,
+// after every reader of its previous use passed the barrier).  Used when the
+// history fits one word.
+constexpr int kColThreads = 1024;
+
+template <typename WT, bool STDP, bool DELAY, int kColW>
+__global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, DenseArgs da, ColArgs ca, int steps) {
+    cg::grid_group grid = cg::this_grid();
+    using VT = VecT<WT>;
+    using V = typename VT::V;
+    constexpr int VEC = VT::N;
+    constexpr int CV = kColW / VEC;          // column vectors per CTA
+    constexpr int RL = kColThreads / CV;     // row lanes
+    __shared__ double s_red[RL][kColW + 1];
+    __shared__ WT s_dep[kColW];
+    __shared__ uint32_t s_spk;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = blockIdx.x;
+    const int j = c * kColW + lane;          // warp 0, lanes < 8: this lane's post
+    const bool own = warp == 0 && lane < kColW && j < na.nl;
+    const int cv = tid % CV, rl = tid / CV;
+    const int j0 = c * kColW + cv * VEC;
+    const int n = da.n;
+    const int words = (n + 31) >> 5;
+    const int64_t pitch = da.pitch, mpitch = pitch >> 5;
+    const WT wmin = static_cast<WT>(da.w_min), wmax = static_cast<WT>(da.w_max);
+    WT* W = static_cast<WT*>(da.w);
+    WT* pot2 = static_cast<WT*>(ca.pot2);
+    const uint64_t dmask = ca.dmax >= 64 ? ~0ull : ((1ull << ca.dmax) - 1ull);
+    const uint64_t wmask = ca.window >= 63 ? ~0ull : ((1ull << (ca.window + 1)) - 1ull);
+    double in = own ? na.partial[j] : 0.0;   // input of the call's first step
+    int t = *na.d_step;
+    // the owned neurons' state and parameters stay in warp 0's registers for
+    // the whole call; only what other CTAs read goes through global memory
+    double v = 0.0, thr = 0.0, leak = 0.0, rst = 0.0, fire_p = 1.0;
+    int32_t cnt = 0, refr = 0;
+    uint64_t hprev = 0, akey = 0;
+    if (own) {
+        v = na.v[j];
+        thr = na.thr[j];
+        leak = na.leak[j];
+        rst = na.reset[j];
+        cnt = na.cnt[j];
+        refr = na.refr[j];
+        hprev = ca.hist2[static_cast<int64_t>((t & 1) ^ 1) * n + j];
+        if (na.fire_p) {
+            fire_p = na.fire_p[j];
+            akey = na.agent_key[j];
+        }
+    }
+    // stimulus rows of the next step, fetched one step ahead
+    auto stim_bounds = [&](int tt, int64_t& lo, int64_t& hi) {
+        lo = hi = 0;
+        const int row = tt - na.st_base;
+        if (warp == 0 && row >= 0 && row < na.st_steps) {
+            lo = __ldg(na.st_off + row);
+            hi = __ldg(na.st_off + row + 1);
+        }
+    };
+    int64_t slo, shi;
+    stim_bounds(t, slo, shi);
+    for (int s = 0; s < steps; ++s, ++t) {
+        const int cur = t & 1;
+        uint32_t* act_now = ca.act3 + (t % 3) * words;
+        if (warp == 0) {
+            bool fired = false, act = false;
+            if (own) {
+                double u = na.abm ? in : leak_toward(v, leak, rst) + in;
+                if (shi > slo) {
+                    int64_t lo = slo, hi = shi;
+                    double ext = 0.0;
+                    while (lo < hi) {
+                        const int64_t mid = (lo + hi) >> 1;
+                        const int nid = __ldg(na.st_neuron + mid);
+                        if (nid == j) { ext = __ldg(na.st_amp + mid); break; }
+                        if (nid < j) lo = mid + 1; else hi = mid;
+                    }
+                    u += ext;
+                }
+                if (na.abm) u = leak_toward(v, leak, rst) + u;
+                fired = u > thr;
+                if (fired && fire_p < 1.0) fired = agent_fires(akey, t, fire_p);
+                if (cnt > 0) {
+                    fired = false;
+                    cnt -= 1;
+                    u = rst;
+                }
+                if (fired) {
+                    v = rst;
+                    cnt = refr;
+                } else {
+                    v = u;
+                }
+                if (na.trace && (t - na.t_base) < na.raster_rows)
+                    na.trace[static_cast<int64_t>(t - na.t_base) * na.nl + j] = v;
+                const uint64_t hn = (hprev << 1) | (fired ? 1ull : 0ull);
+                hprev = hn;
+                ca.hist2[static_cast<int64_t>(cur) * n + j] = hn;
+                act = (hn & dmask) != 0;
+                if (STDP) {
+                    // set bits in ascending k: the reference's order (mat_engine.cpp:226-240)
+                    double dep = 0.0;
+                    for (uint64_t m = hn & wmask & ~1ull; m; m &= m - 1) dep += ca.a_minus[__ffsll(static_cast<long long>(m)) - 2];
+                    s_dep[lane] = static_cast<WT>(dep);
+                    bool any_pot = false;
+                    for (int d = 1; d <= da.dp; ++d) {
+                        double pot = 0.0;
+                        for (uint64_t m = (hn >> (d - 1)) & wmask & ~1ull; m; m &= m - 1)
+                            pot += ca.a_plus[__ffsll(static_cast<long long>(m)) - 2];
+                        pot2[(static_cast<int64_t>(cur) * n + j) * da.dp + (d - 1)] = static_cast<WT>(pot);
+                        any_pot |= pot != 0.0;
+                    }
+                    if (ca.row_plastic[j] && (any_pot || t == 0)) act = true;
+                }
+            }
+            const uint32_t word = __ballot_sync(0xffffffffu, fired);  // bits 0..W-1
+            const uint32_t aw = __ballot_sync(0xffffffffu, act);
+            if (lane == 0) {
+                const int wi = (c * kColW) >> 5, sh = (c * kColW) & 31;
+                if (aw) atomicOr(act_now + wi, aw << sh);
+                if (word) {
+                    if (na.raster && (t - na.t_base) < na.raster_rows)
+                        atomicOr(na.raster + static_cast<int64_t>(t - na.t_base) * na.nl_words + wi, word << sh);
+                    atomicAdd(na.spike_count, static_cast<unsigned long long>(__popc(word)));
+                }
+                s_spk = word;
+            }
+        }
+        grid.sync();
+        stim_bounds(t + 1, slo, shi);  // in flight during the sweep
+        if (c == 0)  // clear the activity words of step t + 2 (last read by the sweep of step t - 1)
+            for (int k = tid; k < words; k += kColThreads) ca.act3[((t + 2) % 3) * words + k] = 0u;
+        // sweep of the CTA's columns: STDP of step t, delivery of step t + 1
+        const uint32_t spk = s_spk;
+        bool okc[VEC];
+        WT sj[VEC], dj[VEC];
+        double acc[VEC];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+            okc[k] = j0 + k < na.nl;
+            sj[k] = (STDP && okc[k] && ((spk >> (cv * VEC + k)) & 1u)) ? WT(1) : WT(0);
+            dj[k] = STDP ? s_dep[cv * VEC + k] : WT(0);
+            acc[k] = 0.0;
+        }
+        const uint64_t* hist = ca.hist2 + static_cast<int64_t>(cur) * n;
+        const WT* potc = pot2 + static_cast<int64_t>(cur) * n * da.dp;
+        // every load of a row is issued before its activity bit is tested: the
+        // rows of a small net sit in L2 and one round trip per row pair is the
+        // cost that matters here
+#pragma unroll 2
+        for (int i = rl; i < n; i += RL) {
+            const uint32_t aword = __ldcg(act_now + (i >> 5));
+            const uint64_t eb = __ldcg(hist + i);
+            WT* wrow = W + static_cast<int64_t>(i) * pitch + j0;
+            V wv = VT::load(wrow);
+            uint32_t dv = 0;
+            if (DELAY) {
+                const uint8_t* dp8 = da.delay + static_cast<int64_t>(i) * pitch + j0;
+                dv = VEC == 4 ? *reinterpret_cast<const uint32_t*>(dp8) : *reinterpret_cast<const uint16_t*>(dp8);
+            }
+            uint8_t kind = kRowNone;
+            uint32_t mw = 0;
+            if (STDP) {
+                kind = da.kind[i];
+                if (kind == kRowMixed) mw = da.mask[static_cast<int64_t>(i) * mpitch + (j0 >> 5)];
+            }
+            if (!((aword >> (i & 31)) & 1u)) continue;
+            bool changed = false;
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) {
+                if (!okc[k]) continue;
+                WT w = VT::get(wv, k);
+                const int d1 = DELAY ? static_cast<int>((dv >> (8 * k)) & 0xffu) - 1 : 0;
+                const bool e = (eb >> d1) & 1ull;
+                if (STDP && kind != kRowNone) {
+                    const bool pl = kind == kRowAll || (kind == kRowAllButSelf && j0 + k != i) ||
+                                    (kind == kRowMixed && ((mw >> ((j0 & 31) + k)) & 1u));
+                    if (pl) {
+                        const WT p = __ldcg(potc + static_cast<int64_t>(i) * da.dp + d1);
+                        WT dw = WT(0);  // dw = 0; if s_post dw += pot; if s_pre dw -= dep (mat_engine.cpp:243-246)
+                        if (sj[k] != WT(0)) dw += p;
+                        if (e) dw -= dj[k];
+                        const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
+                        changed |= nw != w;
+                        w = nw;
+                        VT::set(wv, k, nw);
+                    }
+                }
+                if (e) acc[k] += static_cast<double>(w);
+            }
+            if (STDP && changed) VT::store(wrow, wv);
+        }
+        // fixed tree: 8-row groups, then 8 groups of 8, then the rest in order
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) s_red[rl][cv * VEC + k] = acc[k];
+        __syncthreads();
+        for (int stride = 1; stride < RL; stride *= 8) {
+            const int col = tid % kColW, g = tid / kColW;  // RL / 8 groups per level
+            const int base = g * 8 * stride;
+            if (base < RL) {
+                double sum = 0.0;
+                for (int r = 0; r < 8 && base + r * stride < RL; ++r) sum += s_red[base + r * stride][col];
+                s_red[base][col] = sum;
+            }
+            __syncthreads();
+        }
+        if (warp == 0 && lane < kColW) in = s_red[0][lane];
+        __syncthreads();
+    }
+    if (own) {
+        da.partial[j] = in;  // (same buffer as na.partial) input of the next call's first step
+        na.v[j] = v;
+        na.cnt[j] = cnt;
+    }
+    if (blockIdx.x == 0 && tid == 0) *na.d_step = t;
+}
+
+}  // namespace
+
+size_t tiny_smem_bytes(const TinyArgs& a) { return tiny_layout(a).total; }
+
+int tiny_max_smem() {
+    int dev = 0, v = 0;
+    check(cudaGetDevice(&dev), "cudaGetDevice");
+    check(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
+    return v;
+}
+
+void launch_tiny(const TinyArgs& a, cudaStream_t s) {
+    const size_t smem = tiny_smem_bytes(a);
+    const int threads = (a.n + 31) / 32 * 32;
+    auto go = [&](auto kern) {
+        check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+              "k_tiny smem attribute");
+        kern<<<1, threads, smem, s>>>(a);
+    };
+    if (a.f64) {
+        if (a.stdp) go(k_tiny<double, true>);
+        else go(k_tiny<double, false>);
+    } else {
+        if (a.stdp) go(k_tiny<float, true>);
+        else go(k_tiny<float, false>);
+    }
+    check(cudaGetLastError(), "k_tiny");
+}
+
+template <typename WT, bool STDP, bool DELAY>
+static void persistent_go(NeuronArgs na, HistArgs h, DenseArgs da, int grid, int steps, cudaStream_t s,
+                          int* max_ctas) {
+    auto kern = k_persistent_dense<WT, STDP, DELAY>;
+    if (max_ctas) {
+        int dev = 0, sms = 0, occ = 0;
+        check(cudaGetDevice(&dev), "cudaGetDevice");
+        check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+        check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0), "occupancy");
+        *max_ctas = occ * sms;
+        return;
+    }
+    void* args[] = {&na, &h, &da, &steps};
+    check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kThreads), args, 0, s),
+          "k_persistent_dense");
+}
+
+static void persistent_dispatch(const NeuronArgs& na, const HistArgs& h, const DenseArgs& da, bool f64,
+                                bool stdp, bool delay, int grid, int steps, cudaStream_t s, int* max_ctas) {
+#define SNB_P(WT)                                                                         \
+    do {                                                                                  \
+        if (stdp) {                                                                       \
+            if (delay) persistent_go<WT, true, true>(na, h, da, grid, steps, s, max_ctas);   \
+            else persistent_go<WT, true, false>(na, h, da, grid, steps, s, max_ctas);        \
+        } else {                                                                          \
+            if (delay) persistent_go<WT, false, true>(na, h, da, grid, steps, s, max_ctas);  \
+            else persistent_go<WT, false, false>(na, h, da, grid, steps, s, max_ctas);       \
+        }                                                                                 \
+    } while (0)
+    if (f64) SNB_P(double);
+    else SNB_P(float);
+#undef SNB_P
+}
+
+template <typename WT, bool STDP, bool DELAY>
+static int cols_go(const NeuronArgs& na, const DenseArgs& da, const ColArgs& ca, int width, int grid, int steps,
+                   cudaStream_t s) {
+    // 16- and 32-post groups were slower than the row-chunk loop (2048-neuron
+    // STDP net: 29k vs 41k steps/s): only 8-post groups are instantiated
+    if (width != 8) throw std::runtime_error("k_persistent_cols: column groups of 8 posts only");
+    auto kern = k_persistent_cols<WT, STDP, DELAY, 8>;
+    if (grid <= 0) {
+        int dev = 0, sms = 0, occ = 0;
+        check(cudaGetDevice(&dev), "cudaGetDevice");
+        check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+        check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kColThreads, 0), "occupancy");
+        return occ * sms;
+    }
+    NeuronArgs a = na;
+    DenseArgs d = da;
+    ColArgs c = ca;
+    void* args[] = {&a, &d, &c, &steps};
+    check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kColThreads), args, 0, s),
+          "k_persistent_cols");
+    return grid;
+}
+
+static int cols_dispatch(const NeuronArgs& na, const DenseArgs& da, const ColArgs& ca, bool f64, bool stdp,
+                         bool delay, int width, int grid, int steps, cudaStream_t s) {
+#define SNB_C(WT)                                                                                 \
+    do {                                                                                          \
+        if (stdp) return delay ? cols_go<WT, true, true>(na, da, ca, width, grid, steps, s)       \
+                               : cols_go<WT, true, false>(na, da, ca, width, grid, steps, s);     \
+        return delay ? cols_go<WT, false, true>(na, da, ca, width, grid, steps, s)                \
+                     : cols_go<WT, false, false>(na, da, ca, width, grid, steps, s);              \
+    } while (0)
+    if (f64) SNB_C(double);
+    SNB_C(float);
+#undef SNB_C
+}
+
+int persistent_cols_max_ctas(bool f64, bool stdp, bool delay, int width) {
+    return cols_dispatch(NeuronArgs{}, DenseArgs{}, ColArgs{}, f64, stdp, delay, width, 0, 0, nullptr);
+}
+
+void launch_persistent_cols(const NeuronArgs& na, const DenseArgs& da, const ColArgs& ca, bool f64, bool stdp,
+                            bool delay, int width, int grid, int steps, cudaStream_t s) {
+    cols_dispatch(na, da, ca, f64, stdp, delay, width, grid, steps, s);
+}
+
+int persistent_max_ctas(bool f64, bool stdp, bool delay) {
+    int m = 0;
+    persistent_dispatch(NeuronArgs{}, HistArgs{}, DenseArgs{}, f64, stdp, delay, 0, 0, nullptr, &m);
+    return m;
+}
+
+void launch_persistent_dense(const NeuronArgs& na, const HistArgs& h, const DenseArgs& da, bool f64,
+                             bool stdp, bool delay, int grid, int steps, cudaStream_t s) {
+    persistent_dispatch(na, h, da, f64, stdp, delay, grid, steps, s, nullptr);
+}
+
+}  // namespace snb

@@ -1,0 +1,817 @@
+// Sparse (blocked CSC) sweeps: k_sparse_pull, k_sparse_count (+ its setup-time
+// bank-aware list order), k_sparse_exact, k_sparse_stream and the opt-in k_sparse_tma.
+#include "kernels_common.cuh"
+
+namespace snb {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Sparse pull: blocked CSC.  CTA (post group, pre block b) stages the spike
+// history of the block's pres in shared memory, then SUB lanes per post walk
+// the post's incoming list (pre ascending, padded to 4) with 128-bit loads:
+//   e = s_pre[t+1-d]  (history bit d-1)    acc += e * w'
+// Replaces the CSR branch of WeightMatrix::propagate (mat_engine.cpp:88-92)
+// and the oracle's delivery queue (oracle.cpp:91-95) without atomics.
+template <int HB> struct HistT { using T = uint64_t; };
+template <> struct HistT<16> { using T = uint16_t; };
+template <> struct HistT<32> { using T = uint32_t; };
+
+__host__ __device__ inline size_t sp_hist_bytes(int pb, int hbits) {
+    return hbits == 1 ? ((static_cast<size_t>(pb) / 32 + 1) * 4 + 15) & ~static_cast<size_t>(15)
+                      : ((static_cast<size_t>(pb) + 1) * (hbits / 8) + 15) & ~static_cast<size_t>(15);
+}
+
+// Shared-memory image of a pre block's spike history: pcount entries from
+// global memory, then zeros up to and including slot pb (the inert padding
+// pre of dictionary-encoded lists).  Returns the 16-aligned byte size.
+template <int HB>
+__device__ __forceinline__ size_t stage_history(const SparseArgs& a, int pre0, int pcount, uint8_t* smem) {
+    using HT = typename HistT<HB>::T;
+    const int tid = threadIdx.x;
+    if (HB == 1) {
+        uint32_t* sb = reinterpret_cast<uint32_t*>(smem);
+        const int nw = (pcount + 31) >> 5;
+        const int nw_all = a.pb / 32 + 1;
+        for (int k = tid; k < nw_all; k += blockDim.x) sb[k] = k < nw ? __ldcg(a.bits + (pre0 >> 5) + k) : 0u;
+        return (static_cast<size_t>(nw_all) * 4 + 15) & ~static_cast<size_t>(15);
+    }
+    HT* sh = reinterpret_cast<HT*>(smem);
+    for (int k = tid; k <= a.pb; k += blockDim.x) {
+        HT v = 0;
+        if (k < pcount) v = static_cast<HT>(HB == 64 ? __ldcg(a.hist + pre0 + k) : __ldcg(a.hist_lo + pre0 + k));
+        sh[k] = v;
+    }
+    return (static_cast<size_t>(a.pb + 1) * sizeof(HT) + 15) & ~static_cast<size_t>(15);
+}
+
+template <typename WT, bool STDP, int HB, int SUB, bool DICT>
+#ifndef SNB_SPARSE_MINB
+#define SNB_SPARSE_MINB 4  // <= 64 regs: 4 CTAs/SM (5 spills; cfg4 0.562 ms vs 0.652 unbounded)
+#endif
+__global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(SparseArgs a) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    using HT = typename HistT<HB>::T;
+    const int b = blockIdx.y;
+    const int pre0 = b * a.pb;
+    const int pcount = min(a.pb, a.n - pre0);
+    const int tid = threadIdx.x;
+    const size_t hbytes = stage_history<HB>(a, pre0, pcount, smem_raw);
+    // weight dictionary (non-plastic nets with <= 511 distinct weights): the
+    // meta word carries the index, so the weight stream disappears (4 B/synapse)
+    WT* s_wd = reinterpret_cast<WT*>(smem_raw + hbytes);
+    if (DICT)
+        for (int k = tid; k < a.dict_size; k += kThreads) s_wd[k] = static_cast<const WT*>(a.wdict)[k];
+    __syncthreads();
+    const uint32_t* sbits = reinterpret_cast<const uint32_t*>(smem_raw);
+    const HT* shist = reinterpret_cast<const HT*>(smem_raw);
+    const bool uniform = DICT && a.dict_size == 2;  // {w, 0.0 padding}: every synapse carries w
+
+    const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
+    const WT* pot = static_cast<const WT*>(a.pot);
+    const WT* dep = static_cast<const WT*>(a.dep);
+    WT* W = static_cast<WT*>(a.w);
+
+    const int p0 = blockIdx.x * a.posts_per_cta;
+    const int p1 = min(a.nl, p0 + a.posts_per_cta);
+    constexpr int PER_WARP = 32 / SUB;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int sg = lane / SUB, sl = lane % SUB;
+    // Software pipeline: the next post's list bounds are loaded while the
+    // current post streams, and each post's chunks are fetched UL at a time
+    // (all loads issued before any use) -- one memory round trip per post.
+    // chunk loads per lane per batch: cover a typical list in one round trip
+#ifndef SNB_SPARSE_UL
+#define SNB_SPARSE_UL 8
+#endif
+    constexpr int UL = DICT ? (SUB <= 8 ? SNB_SPARSE_UL : 4) : 2;
+    const int stride = (kThreads / 32) * PER_WARP;
+    const int64_t* offb = a.off + static_cast<int64_t>(b) * a.nl;
+    int p = p0 + warp * PER_WARP + sg;
+    int64_t beg = 0, end = 0;
+    if (p < p1) {
+        beg = __ldg(offb + p);
+        end = __ldg(offb + p + 1);
+    }
+    for (int pbase = p0 + warp * PER_WARP; pbase < p1; pbase += stride) {  // warp-uniform trip count
+        const bool valid = p < p1;
+        const int pn = p + stride;
+        int64_t nbeg = 0, nend = 0;
+        if (pn < p1) {
+            nbeg = __ldg(offb + pn);
+            nend = __ldg(offb + pn + 1);
+        }
+        WT sum = WT(0);
+        int cnt = 0;
+        if (valid) {
+            const int gp = a.first + p;
+            bool sp = false;
+            WT depp = WT(0);
+            if (STDP) {
+                sp = bit_of(a.bits, gp);
+                depp = dep[gp];
+            }
+            for (int64_t q0 = beg + sl * 4; q0 < end; q0 += SUB * 4 * UL) {
+                uint4 m4[UL];
+                WT wv[UL][4];
+#pragma unroll
+                for (int u = 0; u < UL; ++u) {
+                    const int64_t q = q0 + static_cast<int64_t>(u) * SUB * 4;
+                    if (q < end) {
+                        m4[u] = __ldcs(reinterpret_cast<const uint4*>(a.meta + q));
+                        if (!DICT) {
+                            if (sizeof(WT) == 4) {
+                                const float4 f = __ldcs(reinterpret_cast<const float4*>(W + q));
+                                wv[u][0] = f.x; wv[u][1] = f.y; wv[u][2] = f.z; wv[u][3] = f.w;
+                            } else {
+                                const double2 f0 = __ldcs(reinterpret_cast<const double2*>(W + q));
+                                const double2 f1 = __ldcs(reinterpret_cast<const double2*>(W + q + 2));
+                                wv[u][0] = f0.x; wv[u][1] = f0.y; wv[u][2] = f1.x; wv[u][3] = f1.y;
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < UL; ++u) {
+                    const int64_t q = q0 + static_cast<int64_t>(u) * SUB * 4;
+                    if (q >= end) continue;
+                    if (DICT && uniform) {
+                        // one weight for every synapse: count the delivering pres
+                        // (padding points at the zero-history slot pb)
+                        const uint32_t ms[4] = {m4[u].x, m4[u].y, m4[u].z, m4[u].w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const int pl = static_cast<int>(ms[k] & 0xffffu);
+                            if (HB == 1) cnt += static_cast<int>((sbits[pl >> 5] >> (pl & 31)) & 1u);
+                            else cnt += static_cast<int>((shist[pl] >> ((ms[k] >> 16) & 63u)) & 1u);
+                        }
+                        continue;
+                    }
+                    if (DICT) {
+                        wv[u][0] = s_wd[m4[u].x >> 23]; wv[u][1] = s_wd[m4[u].y >> 23];
+                        wv[u][2] = s_wd[m4[u].z >> 23]; wv[u][3] = s_wd[m4[u].w >> 23];
+                    }
+                    const uint32_t ms[4] = {m4[u].x, m4[u].y, m4[u].z, m4[u].w};
+                    bool changed = false;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t m = ms[k];
+                        const int pl = static_cast<int>(m & 0xffffu);
+                        const int d1 = static_cast<int>((m >> 16) & 63u);
+                        uint32_t e;
+                        if (HB == 1) e = (sbits[pl >> 5] >> (pl & 31)) & 1u;
+                        else e = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
+                        WT w = wv[u][k];
+                        if (!DICT && STDP && ((m >> 22) & 1u)) {
+                            const WT pt = pot[static_cast<int64_t>(pre0 + pl) * a.dp + d1];
+                            WT dw = WT(0);
+                            if (sp) dw += pt;
+                            if (e) dw -= depp;
+                            const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
+                            changed |= (nw != w);
+                            w = nw;
+                            wv[u][k] = nw;
+                        }
+                        if (e) sum += w;
+                    }
+                    if (!DICT && STDP && changed) {
+                        if (sizeof(WT) == 4) {
+                            __stcs(reinterpret_cast<float4*>(W + q),
+                                   make_float4(float(wv[u][0]), float(wv[u][1]), float(wv[u][2]), float(wv[u][3])));
+                        } else {
+                            __stcs(reinterpret_cast<double2*>(W + q), make_double2(double(wv[u][0]), double(wv[u][1])));
+                            __stcs(reinterpret_cast<double2*>(W + q + 2), make_double2(double(wv[u][2]), double(wv[u][3])));
+                        }
+                    }
+                }
+            }
+        }
+        if (DICT && uniform) {
+#pragma unroll
+            for (int o = SUB / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            sum = static_cast<WT>(cnt) * s_wd[0];
+        } else {
+#pragma unroll
+            for (int o = SUB / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        }
+        if (valid && sl == 0) a.partial[static_cast<int64_t>(b) * a.nl + p] = static_cast<double>(sum);
+        p = pn;
+        beg = nbeg;
+        end = nend;
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *a.d_step += 1;
+}
+
+// Sparse count: k_sparse_pull specialised for static lists that carry one
+// weight w (dictionary {w, 0}: the ER generator's nets, cfg4).  Same CTA
+// tiling and pipelining; per post the lanes count the delivering entries and
+// one lane writes count * w.  Loads are predicated on the 32-bit number of
+// remaining entries and the bit test is one funnel shift, so an entry costs
+// address + LDS + SHF.W + AND (padding entries point at the zero-history slot pb).
+template <typename WT, int HB, int SUB>
+__global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_count(SparseArgs a) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    using HT = typename HistT<HB>::T;
+    static_assert(HB != 64, "64-step histories use k_sparse_pull");
+    const int b = blockIdx.y;
+    const int pre0 = b * a.pb;
+    const int pcount = min(a.pb, a.n - pre0);
+    const int tid = threadIdx.x;
+    stage_history<HB>(a, pre0, pcount, smem_raw);
+    __syncthreads();
+    const uint32_t* sbits = reinterpret_cast<const uint32_t*>(smem_raw);
+    const HT* shist = reinterpret_cast<const HT*>(smem_raw);
+    const WT w0 = static_cast<const WT*>(a.wdict)[0];
+    const int p0 = blockIdx.x * a.posts_per_cta;
+    const int p1 = min(a.nl, p0 + a.posts_per_cta);
+    constexpr int PER_WARP = 32 / SUB;
+#ifndef SNB_SPARSE_COUNT_UL
+#define SNB_SPARSE_COUNT_UL 6  // cfg4 (tools/ab_sparse.sh): UL 4 0.579, 5 0.561, 6 0.514, 7 0.532, 8 0.541, 12 0.689 ms at SUB 8
+#endif
+    constexpr int UL = SUB <= 8 ? SNB_SPARSE_COUNT_UL : 4;
+    constexpr int STEP = SUB * 4 * UL;  // entries one lane group covers per batch
+    const int warp = tid >> 5, lane = tid & 31;
+    const int sg = lane / SUB, sl = lane % SUB;
+    const int stride = (kThreads / 32) * PER_WARP;
+    const int64_t* offb = a.off + static_cast<int64_t>(b) * a.nl;
+    int p = p0 + warp * PER_WARP + sg;
+    int64_t beg = 0, end = 0;
+    if (p < p1) {
+        beg = __ldg(offb + p);
+        end = __ldg(offb + p + 1);
+    }
+    for (int pbase = p0 + warp * PER_WARP; pbase < p1; pbase += stride) {  // warp-uniform trip count
+        const bool valid = p < p1;
+        const int pn = p + stride;
+        int64_t nbeg = 0, nend = 0;
+        if (pn < p1) {
+            nbeg = __ldg(offb + pn);
+            nend = __ldg(offb + pn + 1);
+        }
+        int cnt = 0;
+        if (valid) {
+            for (int64_t q0 = beg + sl * 4; q0 < end; q0 += STEP) {
+                const int rem = static_cast<int>(min(end - q0, static_cast<int64_t>(STEP)));
+                const uint4* src = reinterpret_cast<const uint4*>(a.meta + q0);
+                uint4 m4[UL];
+#pragma unroll
+                for (int u = 0; u < UL; ++u)
+                    if (u * SUB * 4 < rem) m4[u] = __ldcs(src + u * SUB);
+#pragma unroll
+                for (int u = 0; u < UL; ++u) {
+                    if (u * SUB * 4 < rem) {
+                        const uint32_t ms[4] = {m4[u].x, m4[u].y, m4[u].z, m4[u].w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint32_t mk = ms[k];
+                            if (HB == 1) {
+                                const uint32_t h = sbits[(mk & 0xffffu) >> 5];
+                                cnt += static_cast<int>(__funnelshift_r(h, h, mk) & 1u);  // bit pl & 31
+                            } else {
+                                const uint32_t h = static_cast<uint32_t>(shist[mk & 0xffffu]);
+                                cnt += static_cast<int>(__funnelshift_r(h, h, mk >> 16) & 1u);  // bit d-1 < 32
+                            }
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int o = SUB / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (valid && sl == 0)
+            a.partial[static_cast<int64_t>(b) * a.nl + p] = static_cast<double>(static_cast<WT>(cnt) * w0);
+        p = pn;
+        beg = nbeg;
+        end = nend;
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *a.d_step += 1;
+}
+
+// ---------------------------------------------------------------------------
+// Bank-aware order of one-weight lists (setup, k_sparse_count only: a count
+// does not depend on the order of a list).  In k_sparse_count one warp-wide
+// LDS of the staged history serves 32/SUB posts x SUB lanes, lane sl of a post
+// reading entry 4*SUB*r + 4*sl + k of its list.  Each list is bucket-sorted by
+// the shared-memory bank of its history word, rotated by the post's slot in
+// the warp (p mod 32/SUB), and dealt lane-major: the SUB entries one LDS
+// touches come from evenly spaced buckets, so the warp's 32 reads spread over
+// the banks instead of colliding at random (3.9 wavefronts per LDS before).
+__device__ __forceinline__ int sp_bank(uint32_t m, int hbits) {
+    const int pl = static_cast<int>(m & 0xffffu);
+    return hbits == 1 ? (pl >> 5) & 31 : hbits == 16 ? (pl >> 1) & 31 : pl & 31;
+}
+
+__global__ void k_sparse_bank_order(const uint32_t* in, uint32_t* out, const int64_t* off, int64_t lists,
+                                    int nl, int sub, int hbits) {
+    const int64_t L = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (L >= lists) return;
+    const int64_t beg = off[L];
+    const int len = static_cast<int>(off[L + 1] - beg);
+    if (len == 0) return;
+    const int per_warp = 32 / sub;
+    const int phase = static_cast<int>((L % nl) % per_warp);
+    int start[32];
+#pragma unroll
+    for (int b = 0; b < 32; ++b) start[b] = 0;
+    for (int j = 0; j < len; ++j) start[(sp_bank(in[beg + j], hbits) - phase) & 31] += 1;
+    int acc = 0;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+        const int c = start[b];
+        start[b] = acc;
+        acc += c;
+    }
+    // dealing order: lane-major over the (row, k) slots of the list's rows of
+    // 4*sub entries; only the last row can be partial, and there whole lanes
+    // drop out (len is a multiple of 4)
+    const int row = 4 * sub;
+    const int rows = (len + row - 1) / row;
+    const int last = (len - row * (rows - 1)) / 4;  // lanes with a full last row
+    const int full = 4 * rows, part = 4 * (rows - 1);
+    for (int j = 0; j < len; ++j) {
+        const uint32_t m = in[beg + j];
+        const int si = start[(sp_bank(m, hbits) - phase) & 31]++;
+        int sl, g;
+        if (si < full * last) {
+            sl = si / full;
+            g = si - sl * full;
+        } else {
+            const int t = si - full * last;
+            sl = last + t / part;  // part > 0 here: si < len = full * last + part * (sub - last)
+            g = t - (sl - last) * part;
+        }
+        out[beg + (g >> 2) * row + 4 * sl + (g & 3)] = m;
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// Sparse TMA stream (static nets whose lists carry one weight w: the ER
+// generator's networks, cfg4).  The blocked-CSC meta array is one contiguous
+// stream in (block, post) order.  The host cuts it into stages of whole posts
+// (<= kSpE entries, one pre block, <= kSpNbMax posts) and gives each CTA a
+// contiguous run of stages inside one pre block (CTAs per block in proportion
+// to its entries).  A producer warp
+// streams every stage's meta words plus the stage-relative end position of each
+// of its posts (uint16) into a kSpStages-deep ring with cp.async.bulk; each
+// consumer warp takes whole stages (warp w: stages w, w + kSpConsumers, ...) and
+// counts, 4 lanes per post, the entries whose pre delivers (e = s_pre[t+1-d])
+// -> partial[b][p] = count * w, the value k_sparse_pull's uniform path writes.
+// The loads never occupy registers; no CTA barrier per stage.
+constexpr int kSpE = 2048;        // entries per stage (8 KB of meta)
+constexpr int kSpStages = 20;     // ring depth: ~12 stages in flight beyond the ones being counted
+constexpr int kSpNbMax = 256;     // posts per stage
+constexpr int kSpConsumers = 8;   // consumer warps
+constexpr int kSpThreads = 32 * (kSpConsumers + 1);
+
+template <int HB>
+__device__ __forceinline__ void sp_stage_history(const SparseArgs& a, int b, uint8_t* smem, int tid, int nt) {
+    using HT = typename HistT<HB>::T;
+    const int pre0 = b * a.pb;
+    const int pcount = max(0, min(a.pb, a.n - pre0));
+    if (HB == 1) {
+        uint32_t* sb = reinterpret_cast<uint32_t*>(smem);
+        const int nw = (pcount + 31) >> 5;
+        const int nw_all = a.pb / 32 + 1;
+        for (int k = tid; k < nw_all; k += nt) sb[k] = k < nw ? __ldcg(a.bits + (pre0 >> 5) + k) : 0u;
+        return;
+    }
+    HT* sh = reinterpret_cast<HT*>(smem);
+    for (int k = tid; k <= a.pb; k += nt) {
+        HT v = 0;
+        if (k < pcount) v = static_cast<HT>(HB == 64 ? __ldcg(a.hist + pre0 + k) : __ldcg(a.hist_lo + pre0 + k));
+        sh[k] = v;
+    }
+}
+
+template <int HB>
+__device__ __forceinline__ uint32_t sp_hit(const uint8_t* hist, uint32_t m) {
+    using HT = typename HistT<HB>::T;
+    const int pl = static_cast<int>(m & 0xffffu);
+    if (HB == 1) return (reinterpret_cast<const uint32_t*>(hist)[pl >> 5] >> (pl & 31)) & 1u;
+    return static_cast<uint32_t>((reinterpret_cast<const HT*>(hist)[pl] >> ((m >> 16) & 63u)) & 1u);
+}
+
+template <typename WT, int HB>
+__global__ void __launch_bounds__(kSpThreads, 1) k_sparse_tma(SparseArgs a, SpStagePlan plan) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    uint32_t* r_meta = reinterpret_cast<uint32_t*>(smem);
+    uint16_t* r_bnd = reinterpret_cast<uint16_t*>(smem + kSpStages * kSpE * 4);
+    uint8_t* s_hist = smem + kSpStages * (kSpE * 4 + kSpNbMax * 2);
+    const size_t hist_bytes = sp_hist_bytes(a.pb, HB);
+    int4* s_hdr = reinterpret_cast<int4*>(s_hist + hist_bytes);  // [stages] {entries, k0, nb, block}
+    uint64_t* full = reinterpret_cast<uint64_t*>(s_hdr + kSpStages);
+    uint64_t* empty = full + kSpStages;
+    const int s0 = plan.cta_first[blockIdx.x], s1 = plan.cta_first[blockIdx.x + 1];
+    const int blk0 = plan.cta_block[blockIdx.x];
+    if (tid == 0) {
+        for (int s = 0; s < kSpStages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // the one pre block of this CTA's stages
+    if (warp < kSpConsumers) sp_stage_history<HB>(a, blk0, s_hist, tid, 32 * kSpConsumers);
+    __syncthreads();
+    if (warp == kSpConsumers) {
+        // ---- producer: stage records read 32 at a time (one per lane) ----
+        SpStage cur{}, nxt{};
+        if (s0 + lane < s1) cur = plan.stages[s0 + lane];
+        if (s0 + 32 + lane < s1) nxt = plan.stages[s0 + 32 + lane];
+        for (int s = s0, i = 0; s < s1; ++s, ++i) {
+            const int w = (s - s0) & 31;
+            if (w == 0 && s != s0) {
+                cur = nxt;
+                if (s + 32 + lane < s1) nxt = plan.stages[s + 32 + lane];
+            }
+            const int64_t q = __shfl_sync(0xffffffffu, cur.q, w);
+            const int64_t bo = __shfl_sync(0xffffffffu, cur.bnd_off, w);
+            const int entries = __shfl_sync(0xffffffffu, cur.entries, w);
+            const int k0 = __shfl_sync(0xffffffffu, cur.k0, w);
+            const int nb = __shfl_sync(0xffffffffu, cur.nb, w);
+            const int blk = __shfl_sync(0xffffffffu, cur.block, w);
+            const int slot = i % kSpStages;
+            if (lane == 0) {
+                mbar_wait(empty + slot, ((i / kSpStages) & 1u) ^ 1u);
+                s_hdr[slot] = make_int4(entries, k0, nb, blk);
+                const uint32_t mbytes = static_cast<uint32_t>(entries) * 4u;
+                const uint32_t bbytes = static_cast<uint32_t>((nb * 2 + 15) & ~15);
+                mbar_arrive_expect_tx(full + slot, mbytes + bbytes);
+                if (mbytes) bulk_g2s(r_meta + slot * kSpE, a.meta + q, mbytes, full + slot);
+                if (bbytes) bulk_g2s(r_bnd + slot * kSpNbMax, plan.bnd + bo, bbytes, full + slot);
+            }
+            __syncwarp();
+        }
+        return;
+    }
+    // ---- consumer warp: stages warp, warp + kSpConsumers, ... of the CTA's run;
+    // 4 lanes per post count the delivering entries of its list (16 B per lane-step) ----
+    const WT w0 = static_cast<const WT*>(a.wdict)[0];
+    const int sg = lane >> 2, sl = lane & 3;
+    for (int i = warp; s0 + i < s1; i += kSpConsumers) {
+        const int slot = i % kSpStages;
+        mbar_wait(full + slot, (i / kSpStages) & 1u);
+        const int4 hdr = s_hdr[slot];
+        const int k0 = hdr.y, nb = hdr.z;
+        const uint8_t* hist = s_hist;
+        const uint32_t* m = r_meta + slot * kSpE;
+        const uint16_t* bp = r_bnd + slot * kSpNbMax;
+        for (int j0 = 0; j0 < nb; j0 += 8) {
+            const int j = j0 + sg;
+            int beg = 0, end = 0;
+            if (j < nb) {
+                end = bp[j];
+                beg = j > 0 ? bp[j - 1] : 0;
+            }
+            int cnt = 0;
+#pragma unroll 4
+            for (int q = beg + sl * 4; q < end; q += 16) {
+                const uint4 mm = *reinterpret_cast<const uint4*>(m + q);
+                cnt += static_cast<int>(sp_hit<HB>(hist, mm.x) + sp_hit<HB>(hist, mm.y) + sp_hit<HB>(hist, mm.z) +
+                                        sp_hit<HB>(hist, mm.w));
+            }
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+            if (sl == 0 && j < nb) a.partial[k0 + j - 1] = static_cast<double>(static_cast<WT>(cnt) * w0);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + slot);
+    }
+    if (blockIdx.x == 0 && tid == 0) *a.d_step += 1;
+}
+
+// Sparse stream: the same blocked-CSC pull, but each warp streams a contiguous
+// run of its CTA's posts as one flat array of 4-entry chunks (lists are padded
+// to 4, so a chunk never straddles two posts): every lane issues U 128-bit
+// meta + weight loads back to back (no per-post tail waste), a fixed
+// segmented suffix-reduction over lanes folds chunks into per-post sums, and
+// the last segment's sum is carried into the next iteration.  The order of
+// additions is fixed by the data layout, so results are deterministic.
+template <typename WT, bool STDP, int HB, bool DICT>
+__global__ void __launch_bounds__(kThreads) k_sparse_stream(SparseArgs a) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    using HT = typename HistT<HB>::T;
+    constexpr int U = DICT ? 8 : 4;
+    const int b = blockIdx.y;
+    const int pre0 = b * a.pb;
+    const int pcount = min(a.pb, a.n - pre0);
+    const int tid = threadIdx.x;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *a.d_step += 1;  // nobody reads it here
+    const size_t hbytes = stage_history<HB>(a, pre0, pcount, smem_raw);
+    WT* s_wd = reinterpret_cast<WT*>(smem_raw + hbytes);
+    if (DICT)
+        for (int k = tid; k < a.dict_size; k += kThreads) s_wd[k] = static_cast<const WT*>(a.wdict)[k];
+    __syncthreads();
+    const uint32_t* sbits = reinterpret_cast<const uint32_t*>(smem_raw);
+    const HT* shist = reinterpret_cast<const HT*>(smem_raw);
+    const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
+    const WT* pot = static_cast<const WT*>(a.pot);
+    const WT* dep = static_cast<const WT*>(a.dep);
+    WT* W = static_cast<WT*>(a.w);
+    const int64_t* off = a.off + static_cast<int64_t>(b) * a.nl;  // off[p], p in [0, nl]
+    double* part = a.partial + static_cast<int64_t>(b) * a.nl;
+
+    const int warp = tid >> 5, lane = tid & 31;
+    const int p0 = blockIdx.x * a.posts_per_cta;
+    const int p1 = min(a.nl, p0 + a.posts_per_cta);
+    if (p0 >= p1) return;
+    // split [p0, p1) among the 8 warps by entry count (boundaries at post starts)
+    const int64_t e0 = __ldg(off + p0), e1 = __ldg(off + p1);
+    auto lower_post = [&](int64_t target) {  // first p in [p0, p1] with off[p] >= target
+        int lo = p0, hi = p1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(off + mid) < target) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+    };
+    const int nwarps = kThreads / 32;
+    const int pa = lower_post(e0 + (e1 - e0) * warp / nwarps);
+    const int pb = warp == nwarps - 1 ? p1 : lower_post(e0 + (e1 - e0) * (warp + 1) / nwarps);
+    if (pa >= pb) return;
+    // empty lists never appear in the stream: their partial is 0
+    for (int q = pa + lane; q < pb; q += 32)
+        if (__ldg(off + q) == __ldg(off + q + 1)) part[q] = 0.0;
+
+    int64_t e = __ldg(off + pa);
+    const int64_t end = __ldg(off + pb);
+    int carry_post = pa;
+    WT carry = WT(0);
+    int lp = pa;  // this lane's current post (monotone)
+    while (e < end) {
+        uint4 m4[U];
+        WT wv[U][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t q = e + static_cast<int64_t>(u * 32 + lane) * 4;
+            if (q < end) {
+                m4[u] = __ldcs(reinterpret_cast<const uint4*>(a.meta + q));
+                if (DICT) {
+                    // resolved after the loads (smem), see below
+                } else if (sizeof(WT) == 4) {
+                    const float4 f = __ldcs(reinterpret_cast<const float4*>(W + q));
+                    wv[u][0] = f.x; wv[u][1] = f.y; wv[u][2] = f.z; wv[u][3] = f.w;
+                } else {
+                    const double2 f0 = __ldcs(reinterpret_cast<const double2*>(W + q));
+                    const double2 f1 = __ldcs(reinterpret_cast<const double2*>(W + q + 2));
+                    wv[u][0] = f0.x; wv[u][1] = f0.y; wv[u][2] = f1.x; wv[u][3] = f1.y;
+                }
+            } else {
+                m4[u] = make_uint4(0, 0, 0, 0);
+                wv[u][0] = wv[u][1] = wv[u][2] = wv[u][3] = WT(0);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t q = e + static_cast<int64_t>(u * 32 + lane) * 4;
+            const bool valid = q < end;
+            if (DICT) {
+                wv[u][0] = s_wd[m4[u].x >> 23]; wv[u][1] = s_wd[m4[u].y >> 23];
+                wv[u][2] = s_wd[m4[u].z >> 23]; wv[u][3] = s_wd[m4[u].w >> 23];
+                if (!valid) wv[u][0] = wv[u][1] = wv[u][2] = wv[u][3] = WT(0);
+            }
+            int p = pb;  // sentinel for lanes past the end
+            if (valid) {
+                while (__ldg(off + lp + 1) <= q) ++lp;
+                p = lp;
+            }
+            WT csum = WT(0);
+            if (valid) {
+                const uint32_t ms[4] = {m4[u].x, m4[u].y, m4[u].z, m4[u].w};
+                bool sp = false;
+                WT depp = WT(0);
+                if (STDP) {
+                    sp = bit_of(a.bits, a.first + p);
+                    depp = __ldcg(dep + a.first + p);
+                }
+                bool changed = false;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t m = ms[k];
+                    const int pl = static_cast<int>(m & 0xffffu);
+                    const int d1 = static_cast<int>((m >> 16) & 63u);
+                    uint32_t ev;
+                    if (HB == 1) ev = (sbits[pl >> 5] >> (pl & 31)) & 1u;
+                    else ev = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
+                    WT w = wv[u][k];
+                    if (STDP && ((m >> 22) & 1u)) {
+                        const WT pt = __ldcg(pot + static_cast<int64_t>(pre0 + pl) * a.dp + d1);
+                        const WT dw = fma(sp ? WT(1) : WT(0), pt, -((ev ? WT(1) : WT(0)) * depp));
+                        const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
+                        changed |= (nw != w);
+                        w = nw;
+                        wv[u][k] = nw;
+                    }
+                    csum = fma(ev ? WT(1) : WT(0), w, csum);
+                }
+                if (STDP && changed) {
+                    if (sizeof(WT) == 4) {
+                        __stcs(reinterpret_cast<float4*>(W + q),
+                               make_float4(float(wv[u][0]), float(wv[u][1]), float(wv[u][2]), float(wv[u][3])));
+                    } else {
+                        __stcs(reinterpret_cast<double2*>(W + q), make_double2(double(wv[u][0]), double(wv[u][1])));
+                        __stcs(reinterpret_cast<double2*>(W + q + 2), make_double2(double(wv[u][2]), double(wv[u][3])));
+                    }
+                }
+            }
+            // segmented suffix sum over lanes (posts are non-decreasing in lane)
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const WT x = __shfl_down_sync(0xffffffffu, csum, o);
+                const int px = __shfl_down_sync(0xffffffffu, p, o);
+                if (lane + o < 32 && px == p) csum += x;
+            }
+            const int pprev = __shfl_up_sync(0xffffffffu, p, 1);
+            const bool head = lane == 0 || pprev != p;
+            const int plast = __shfl_sync(0xffffffffu, p, 31);
+            const int first_post = __shfl_sync(0xffffffffu, p, 0);
+            if (first_post != carry_post && lane == 0 && carry_post < pb) part[carry_post] = static_cast<double>(carry);
+            WT total = csum;
+            if (head && lane == 0 && p == carry_post) total += carry;
+            if (head && p != plast && p < pb) part[p] = static_cast<double>(total);
+            // the segment holding lane 31 continues into the next iteration;
+            // its head total already includes the old carry when it began at lane 0
+            const int head_last = __ffs(__ballot_sync(0xffffffffu, p == plast)) - 1;
+            carry = __shfl_sync(0xffffffffu, total, head_last);
+            carry_post = plast;
+        }
+        e += static_cast<int64_t>(U * 32) * 4;
+    }
+    if (lane == 0 && carry_post < pb) part[carry_post] = static_cast<double>(carry);
+}
+
+// Sparse exact: one thread per post, ascending pre, fp64 seeded with leak(v).
+template <typename WT, bool STDP>
+__global__ void __launch_bounds__(kThreads) k_sparse_exact(SparseArgs a) {
+    const int p = blockIdx.x * kThreads + threadIdx.x;
+    if (p < a.nl) {
+        const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
+        const WT* pot = static_cast<const WT*>(a.pot);
+        const WT* dep = static_cast<const WT*>(a.dep);
+        WT* W = static_cast<WT*>(a.w);
+        const int gp = a.first + p;
+        const bool sp = STDP ? bit_of(a.bits, gp) : false;
+        const WT depp = STDP ? dep[gp] : WT(0);
+        double acc = a.abm ? 0.0 : leak_toward(a.v[p], a.leak[p], a.reset[p]);
+        for (int b = 0; b < a.nblocks; ++b) {
+            const int64_t beg = a.off[static_cast<int64_t>(b) * a.nl + p];
+            const int64_t end = a.off[static_cast<int64_t>(b) * a.nl + p + 1];
+            for (int64_t q = beg; q < end; ++q) {
+                const uint32_t m = a.meta[q];
+                const int pre = b * a.pb + static_cast<int>(m & 0xffffu);
+                const int d1 = static_cast<int>((m >> 16) & 63u);
+                const bool e = (a.hist[pre] >> d1) & 1ull;
+                WT w = W[q];
+                if (STDP && ((m >> 22) & 1u)) {
+                    const WT pt = pot[static_cast<int64_t>(pre) * a.dp + d1];
+                    WT dw = WT(0);
+                    if (sp) dw += pt;
+                    if (e) dw -= depp;
+                    w = clamp_ref<WT>(w + dw, wmin, wmax);
+                    W[q] = w;
+                }
+                if (e) acc += static_cast<double>(w);
+            }
+        }
+        a.u_exact[p] = acc;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.d_step += 1;
+}
+
+}  // namespace
+
+int sparse_block_pres(int hbits) {
+    // 32 KB of staged history per CTA (pre ids are 16-bit block-local)
+    switch (hbits) {
+        case 1: return 32768;   // pre_local == pb is the inert padding slot (16-bit field)
+        case 16: return 16384;
+        case 32: return 8192;
+        default: return 4096;
+    }
+}
+
+template <typename WT, bool STDP, int HB>
+static void sparse_go_sub(const SparseArgs& a, int sub, int gx, size_t smem, cudaStream_t s) {
+    dim3 grid(gx, a.nblocks);
+    if (a.dict_size > 0) smem = ((smem + 15) & ~static_cast<size_t>(15)) + static_cast<size_t>(a.dict_size) * sizeof(WT);
+    if (a.dict_size == 2 && !STDP && sub != 0 && HB != 64) {  // one weight: count the delivering pres
+        constexpr int HC = HB == 64 ? 32 : HB;  // (64 never reaches the launch)
+        switch (sub) {
+            case 1: k_sparse_count<WT, HC, 1><<<grid, kThreads, smem, s>>>(a); break;
+            case 2: k_sparse_count<WT, HC, 2><<<grid, kThreads, smem, s>>>(a); break;
+            case 4: k_sparse_count<WT, HC, 4><<<grid, kThreads, smem, s>>>(a); break;
+            case 8: k_sparse_count<WT, HC, 8><<<grid, kThreads, smem, s>>>(a); break;
+            case 16: k_sparse_count<WT, HC, 16><<<grid, kThreads, smem, s>>>(a); break;
+            default: k_sparse_count<WT, HC, 32><<<grid, kThreads, smem, s>>>(a); break;
+        }
+        return;
+    }
+    if (a.dict_size > 0 && !STDP) {
+        switch (sub) {
+            case 0: k_sparse_stream<WT, false, HB, true><<<grid, kThreads, smem, s>>>(a); break;
+            case 1: k_sparse_pull<WT, false, HB, 1, true><<<grid, kThreads, smem, s>>>(a); break;
+            case 2: k_sparse_pull<WT, false, HB, 2, true><<<grid, kThreads, smem, s>>>(a); break;
+            case 4: k_sparse_pull<WT, false, HB, 4, true><<<grid, kThreads, smem, s>>>(a); break;
+            case 8: k_sparse_pull<WT, false, HB, 8, true><<<grid, kThreads, smem, s>>>(a); break;
+            case 16: k_sparse_pull<WT, false, HB, 16, true><<<grid, kThreads, smem, s>>>(a); break;
+            default: k_sparse_pull<WT, false, HB, 32, true><<<grid, kThreads, smem, s>>>(a); break;
+        }
+        return;
+    }
+    switch (sub) {
+        case 0: k_sparse_stream<WT, STDP, HB, false><<<grid, kThreads, smem, s>>>(a); break;
+        case 4: k_sparse_pull<WT, STDP, HB, 4, false><<<grid, kThreads, smem, s>>>(a); break;
+        case 8: k_sparse_pull<WT, STDP, HB, 8, false><<<grid, kThreads, smem, s>>>(a); break;
+        case 16: k_sparse_pull<WT, STDP, HB, 16, false><<<grid, kThreads, smem, s>>>(a); break;
+        default: k_sparse_pull<WT, STDP, HB, 32, false><<<grid, kThreads, smem, s>>>(a); break;
+    }
+}
+
+static size_t hist_smem_bytes(int pb, int hbits) {
+    if (hbits == 1) return (static_cast<size_t>(pb / 32 + 1) * 4 + 15) & ~static_cast<size_t>(15);
+    return (static_cast<size_t>(pb + 1) * (hbits / 8) + 15) & ~static_cast<size_t>(15);
+}
+
+template <typename WT, bool STDP>
+static void sparse_go(const SparseArgs& a, int hbits, int sub, int gx, cudaStream_t s) {
+    const size_t smem = hist_smem_bytes(a.pb, hbits);
+    switch (hbits) {
+        case 1: sparse_go_sub<WT, STDP, 1>(a, sub, gx, smem, s); break;
+        case 16: sparse_go_sub<WT, STDP, 16>(a, sub, gx, smem, s); break;
+        case 32: sparse_go_sub<WT, STDP, 32>(a, sub, gx, smem, s); break;
+        default: sparse_go_sub<WT, STDP, 64>(a, sub, gx, smem, s); break;
+    }
+}
+
+void launch_sparse(const SparseArgs& a, bool f64, bool stdp, int hbits, int sub, bool exact, int gx,
+                   cudaStream_t s) {
+    if (exact) {
+        const int grid = (a.nl + kThreads - 1) / kThreads;
+        if (grid == 0) {
+            launch_step_bump(a.d_step, s);
+            return;
+        }
+        if (f64) {
+            if (stdp) k_sparse_exact<double, true><<<grid, kThreads, 0, s>>>(a);
+            else k_sparse_exact<double, false><<<grid, kThreads, 0, s>>>(a);
+        } else {
+            if (stdp) k_sparse_exact<float, true><<<grid, kThreads, 0, s>>>(a);
+            else k_sparse_exact<float, false><<<grid, kThreads, 0, s>>>(a);
+        }
+    } else {
+        if (f64) {
+            if (stdp) sparse_go<double, true>(a, hbits, sub, gx, s);
+            else sparse_go<double, false>(a, hbits, sub, gx, s);
+        } else {
+            if (stdp) sparse_go<float, true>(a, hbits, sub, gx, s);
+            else sparse_go<float, false>(a, hbits, sub, gx, s);
+        }
+    }
+    check(cudaGetLastError(), "k_sparse");
+}
+
+void launch_sparse_bank_order(const uint32_t* in, uint32_t* out, const int64_t* off, int64_t lists, int nl,
+                              int sub, int hbits, cudaStream_t s) {
+    if (lists <= 0) return;
+    k_sparse_bank_order<<<static_cast<unsigned>((lists + 127) / 128), 128, 0, s>>>(in, out, off, lists, nl, sub,
+                                                                                  hbits);
+    check(cudaGetLastError(), "k_sparse_bank_order");
+}
+
+size_t sparse_tma_smem(const SparseArgs& a, int hbits) {
+    return static_cast<size_t>(kSpStages) * (kSpE * 4 + kSpNbMax * 2) + sp_hist_bytes(a.pb, hbits) +
+           kSpStages * 16 + 2 * kSpStages * 8;
+}
+
+int sparse_tma_stage_entries() { return kSpE; }
+int sparse_tma_max_boundaries() { return kSpNbMax; }
+
+void launch_sparse_tma(const SparseArgs& a, const SpStagePlan& plan, int ctas, bool f64, int hbits, cudaStream_t s) {
+    const size_t smem = sparse_tma_smem(a, hbits);
+    auto go = [&](auto kern) {
+        check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+              "k_sparse_tma smem attribute");
+        kern<<<ctas, kSpThreads, smem, s>>>(a, plan);
+    };
+    if (f64) {
+        switch (hbits) {
+            case 1: go(k_sparse_tma<double, 1>); break;
+            case 16: go(k_sparse_tma<double, 16>); break;
+            case 32: go(k_sparse_tma<double, 32>); break;
+            default: go(k_sparse_tma<double, 64>); break;
+        }
+    } else {
+        switch (hbits) {
+            case 1: go(k_sparse_tma<float, 1>); break;
+            case 16: go(k_sparse_tma<float, 16>); break;
+            case 32: go(k_sparse_tma<float, 32>); break;
+            default: go(k_sparse_tma<float, 64>); break;
+        }
+    }
+    check(cudaGetLastError(), "k_sparse_tma");
+}
+
+}  // namespace snb

@@ -1,5 +1,6 @@
 // Device-side parameter blocks and launcher declarations for the MAT step.
-// Reference semantics: see DESIGN.md and the per-kernel comments in kernels.cu.
+// Reference semantics: see DESIGN.md and the per-kernel comments in k_*.cu
+// (shared device helpers in kernels_common.cuh).
 #pragma once
 
 #include <cstdint>
@@ -166,7 +167,7 @@ struct SpStagePlan {
     const uint16_t* bnd;       // end position of each post of a stage, stage-relative
 };
 
-// ---- launchers (kernels.cu) ----
+// ---- launchers (k_neuron.cu, k_dense.cu, k_persistent.cu, k_sparse.cu, k_netgen.cu) ----
 void launch_neuron(const NeuronArgs& a, bool exact, bool fused_hist, const HistArgs& h,
                    cudaStream_t s);
 void launch_hist(const HistArgs& h, cudaStream_t s);
