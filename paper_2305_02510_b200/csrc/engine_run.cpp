@@ -1,0 +1,604 @@
+// The per-step launch sequence: kernel argument blocks, graph-captured
+// step chunks, persistent / tiny loops, stream I/O and the host-driven
+// partition steps (sn_step_local / sn_step_finish).
+#include "engine.hpp"
+#include "engine_util.hpp"
+#include "nccl_dl.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <thread>
+#include <unordered_map>
+#include <unordered_set>
+
+namespace snb {
+
+// One k_tiny launch per chunk of steps whose stimulus fits next to the state.
+void Engine::run_tiny(int t0, int steps, uint32_t* raster, double* trace, bool host_io) {
+    TinyArgs a{};
+    a.n = n_;
+    a.hw = hw_;
+    a.dmax = dmax_;
+    a.f64 = f64_ ? 1 : 0;
+    a.v = d_v_.as<double>();
+    a.cnt = d_cnt_.as<int32_t>();
+    a.hist = d_hist_.as<uint64_t>();
+    a.thr = d_thr_.as<double>();
+    a.leak = d_leak_.as<double>();
+    a.reset = d_reset_.as<double>();
+    a.refr = d_refr_.as<int32_t>();
+    a.off = d_toff_.as<uint32_t>();
+    a.meta = d_meta_.as<uint32_t>();
+    a.pidx = d_tpidx_.as<uint16_t>();
+    a.w = d_w_.p;
+    a.m = static_cast<int32_t>(pre_.size());
+    a.stdp = stdp_on_ ? 1 : 0;
+    a.window = window_;
+    a.dp = dp_;
+    a.a_plus = d_ap_.as<double>();
+    a.a_minus = d_am_.as<double>();
+    a.w_min = w_min_;
+    a.w_max = w_max_;
+    a.spike_count = d_spikes_.as<unsigned long long>();
+    a.d_step = d_step_.as<int32_t>();
+    a.abm = abm_ ? 1 : 0;
+    a.fire_p = any_stochastic_ ? d_firep_.as<double>() : nullptr;
+    a.agent_key = any_stochastic_ ? d_akey_.as<uint64_t>() : nullptr;
+    const size_t limit = static_cast<size_t>(tiny_max_smem());
+    const int words = std::max(nl_words_, 1);
+    const int table = static_cast<int>(hs_off_.size()) - 1;  // steps covered by the stimulus CSR
+    for (int done = 0; done < steps;) {
+        const int tt = t0 + done;
+        int k = steps - done, rows = 0;
+        int64_t lo = 0, hi = 0;
+        for (;;) {  // shrink the launch until its stimulus fits next to the state
+            rows = std::max(0, std::min(table - tt, k));
+            lo = rows > 0 ? hs_off_[tt] : 0;
+            hi = rows > 0 ? hs_off_[tt + rows] : 0;
+            a.steps = k;
+            a.st_rows = rows;
+            a.st_count = static_cast<int32_t>(hi - lo);
+            if (tiny_smem_bytes(a) <= limit || k == 1) break;
+            k = std::max(1, k / 2);
+        }
+        if (rows == 0) {
+            a.st_off = nullptr;
+            a.st_neuron = nullptr;
+            a.st_amp = nullptr;
+        } else if (host_io) {
+            // the kernel reads this launch's rows straight from pinned host memory
+            const size_t cnt = static_cast<size_t>(hi - lo);
+            const size_t ob = round_up((static_cast<int64_t>(rows) + 1) * 8, 16);
+            h_stage_.reserve(ob + cnt * 12 + 16);
+            uint8_t* base = h_stage_.as<uint8_t>();
+            int64_t* soff = reinterpret_cast<int64_t*>(base);
+            double* samp = reinterpret_cast<double*>(base + ob);
+            int32_t* sneu = reinterpret_cast<int32_t*>(base + ob + cnt * 8);
+            for (int s = 0; s <= rows; ++s) soff[s] = hs_off_[tt + s] - lo;
+            std::memcpy(samp, hs_amp_.data() + lo, cnt * 8);
+            std::memcpy(sneu, hs_neuron_.data() + lo, cnt * 4);
+            a.st_off = soff;
+            a.st_amp = samp;
+            a.st_neuron = sneu;
+            stats_.h2d_bytes_last += static_cast<double>(ob + cnt * 12);
+        } else {  // device-resident table from build_stimulus_table
+            a.st_off = d_st_off_.as<int64_t>() + tt;
+            a.st_neuron = d_st_neuron_.as<int32_t>();
+            a.st_amp = d_st_amp_.as<double>();
+        }
+        a.raster = raster + static_cast<size_t>(done) * words;
+        a.trace = trace ? trace + static_cast<size_t>(done) * n_ : nullptr;
+        launch_tiny(a, stream_);
+        stats_.kernel_launches += 1;
+        done += k;
+        if (host_io && rows > 0 && done < steps)
+            cuda_check(cudaStreamSynchronize(stream_), "tiny sync");  // staging is reused
+    }
+}
+
+// ---- per-step launch sequence ----------------------------------------------
+NeuronArgs Engine::neuron_args(int t_base, int rows, uint32_t* raster, double* trace, const int64_t* st_off,
+                               const int32_t* st_neuron, const double* st_amp, int32_t st_steps,
+                               int32_t st_base) {
+    NeuronArgs a{};
+    a.n = n_;
+    a.first = first_;
+    a.nl = nl_;
+    a.v = d_v_.as<double>();
+    a.thr = d_thr_.as<double>();
+    a.leak = d_leak_.as<double>();
+    a.reset = d_reset_.as<double>();
+    a.refr = d_refr_.as<int32_t>();
+    a.cnt = d_cnt_.as<int32_t>();
+    a.partial = d_partial_.as<double>();
+    a.nchunks = nchunks_;
+    a.u_exact = d_uexact_.as<double>();
+    a.st_off = st_off;
+    a.st_neuron = st_neuron;
+    a.st_amp = st_amp;
+    a.st_steps = st_steps;
+    a.st_base = st_base;
+    a.d_step = d_step_.as<int32_t>();
+    a.work = (dense_ && !exact_) ? d_work_.as<int32_t>() : nullptr;
+    a.t_base = t_base;
+    a.bits = d_bits_.as<uint32_t>();
+    a.raster = raster;
+    a.nl_words = nl_words_;
+    a.raster_rows = rows;
+    a.trace = trace;
+    a.spike_count = d_spikes_.as<unsigned long long>();
+    a.abm = abm_ ? 1 : 0;
+    a.fire_p = any_stochastic_ ? d_firep_.as<double>() : nullptr;
+    a.agent_key = any_stochastic_ ? d_akey_.as<uint64_t>() : nullptr;
+    if (p2p_) {
+        a.peer_bits = d_peer_bits_.as<uint32_t* const>();
+        a.peer_flags = d_peer_flags_.as<int32_t* const>();
+        a.done = d_done_.as<uint32_t>();
+        a.rank = opt_.rank;
+        a.world = opt_.world;
+    }
+    return a;
+}
+
+HistArgs Engine::hist_args() {
+    HistArgs h{};
+    h.n = n_;
+    h.bits = d_bits_.as<uint32_t>();
+    h.hist = d_hist_.as<uint64_t>();
+    h.hw = hw_;
+    h.dmax = dmax_;
+    h.stdp = stdp_on_ ? 1 : 0;
+    h.window = window_;
+    h.dp = stdp_on_ ? dp_ : 1;
+    h.a_plus = d_ap_.as<double>();
+    h.a_minus = d_am_.as<double>();
+    h.pot64 = d_pot64_.as<double>();
+    h.pot32 = d_pot32_.as<float>();
+    h.dep64 = d_dep64_.as<double>();
+    h.dep32 = d_dep32_.as<float>();
+    h.row_plastic = d_row_plastic_.as<uint8_t>();
+    h.active = d_active_.as<uint32_t>();
+    h.d_step = d_step_.as<int32_t>();
+    h.hist_lo = (!dense_ && (hbits_ == 16 || hbits_ == 32)) ? d_hist_lo_.as<uint32_t>() : nullptr;
+    h.active_count = d_spikes_.as<unsigned long long>() + 1;
+    if (p2p_) {
+        h.flags = d_flags_.as<int32_t>();
+        h.world = opt_.world;
+        h.error = d_err_.as<int32_t>();
+    }
+    return h;
+}
+
+DenseArgs Engine::dense_args() {
+    DenseArgs a{};
+    a.n = n_;
+    a.first = first_;
+    a.nl = nl_;
+    a.pitch = pitch_;
+    a.w = d_w_.p;
+    a.delay = has_delay_ ? d_delay_.as<uint8_t>() : nullptr;
+    a.mask = any_mixed_ ? d_mask_.as<uint32_t>() : nullptr;
+    a.kind = d_kind_.as<uint8_t>();
+    a.active = d_active_.as<uint32_t>();
+    a.hist = d_hist_.as<uint64_t>();
+    a.bits = d_bits_.as<uint32_t>();
+    a.pot = f64_ ? static_cast<const void*>(d_pot64_.p) : static_cast<const void*>(d_pot32_.p);
+    a.dep = f64_ ? static_cast<const void*>(d_dep64_.p) : static_cast<const void*>(d_dep32_.p);
+    a.dp = stdp_on_ ? dp_ : 1;
+    a.w_min = w_min_;
+    a.w_max = w_max_;
+    a.tile_w = tile_w_;
+    a.rows_per_chunk = rows_per_chunk_;
+    a.nchunks = nchunks_;
+    a.partial = d_partial_.as<double>();
+    a.v = d_v_.as<double>();
+    a.leak = d_leak_.as<double>();
+    a.reset = d_reset_.as<double>();
+    a.u_exact = d_uexact_.as<double>();
+    a.d_step = d_step_.as<int32_t>();
+    a.work = ((dynamic_sched_ || tma_) && !exact_ && !persistent_) ? d_work_.as<int32_t>() : nullptr;
+    a.abm = abm_ ? 1 : 0;
+    return a;
+}
+
+void Engine::launch_sweep_only() {
+    if (dense_) {
+        DenseArgs a = dense_args();
+        if (tma_) launch_dense_tma(a, stdp_on_, dense_grid_, stream_);
+        else launch_dense(a, f64_, stdp_on_, has_delay_, exact_, dense_grid_, stream_);
+    } else {
+        SparseArgs a{};
+        a.n = n_;
+        a.first = first_;
+        a.nl = nl_;
+        a.pb = pb_;
+        a.nblocks = nblocks_;
+        a.off = d_off_.as<int64_t>();
+        a.meta = d_meta_.as<uint32_t>();
+        a.w = d_w_.p;
+        a.bits = d_bits_.as<uint32_t>();
+        a.hist_lo = d_hist_lo_.as<uint32_t>();
+        a.hist = d_hist_.as<uint64_t>();
+        a.pot = f64_ ? static_cast<const void*>(d_pot64_.p) : static_cast<const void*>(d_pot32_.p);
+        a.dep = f64_ ? static_cast<const void*>(d_dep64_.p) : static_cast<const void*>(d_dep32_.p);
+        a.dp = stdp_on_ ? dp_ : 1;
+        a.w_min = w_min_;
+        a.w_max = w_max_;
+        a.posts_per_cta = posts_per_cta_;
+        a.wdict = dict_.empty() ? nullptr : d_wdict_.p;
+        a.dict_size = static_cast<int32_t>(dict_.size());
+        a.partial = d_partial_.as<double>();
+        a.v = d_v_.as<double>();
+        a.leak = d_leak_.as<double>();
+        a.reset = d_reset_.as<double>();
+        a.u_exact = d_uexact_.as<double>();
+        a.d_step = d_step_.as<int32_t>();
+        a.abm = abm_ ? 1 : 0;
+        if (nl_ == 0) {
+            launch_step_bump(a.d_step, stream_);
+        } else if (sparse_tma_) {
+            SpStagePlan plan{d_sp_stages_.as<SpStage>(), d_sp_first_.as<int32_t>(), d_sp_block_.as<int32_t>(),
+                             d_sp_bnd_.as<uint16_t>()};
+            launch_sparse_tma(a, plan, sp_ctas_, f64_, hbits_, stream_);
+        } else {
+            launch_sparse(a, f64_, stdp_on_, hbits_, sub_, exact_, sparse_gx_, stream_);
+        }
+    }
+}
+
+void Engine::launch_sweep() {
+    launch_sweep_only();
+    stats_.kernel_launches += 1;
+}
+
+cudaEvent_t Engine::get_event() {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+}
+
+void Engine::enqueue_step(const NeuronArgs& na, bool exchange) {
+    const bool prof = opt_.profile != 0;
+    const bool fused = opt_.world == 1;
+    const HistArgs h = hist_args();
+    cudaEvent_t e0{}, e1{}, e2{}, e3{};
+    if (prof) { e0 = get_event(); cuda_check(cudaEventRecord(e0, stream_), "rec"); }
+    launch_neuron(na, exact_, fused, h, stream_);
+    stats_.kernel_launches += 1;
+    if (prof) { e1 = get_event(); cuda_check(cudaEventRecord(e1, stream_), "rec"); pending_.push_back({e0, e1, 0, 0.0}); }
+    if (!fused && exchange) {
+        if (prof) { e0 = get_event(); cuda_check(cudaEventRecord(e0, stream_), "rec"); }
+        if (comm_ && !p2p_) comm_->all_gather_inplace(d_bits_.as<uint32_t>(), static_cast<size_t>(part_ / 32), stream_);
+        launch_hist(h, stream_);
+        stats_.kernel_launches += 1;
+        if (prof) { e1 = get_event(); cuda_check(cudaEventRecord(e1, stream_), "rec"); pending_.push_back({e0, e1, 2, 0.0}); }
+    }
+    if (prof) { e2 = get_event(); cuda_check(cudaEventRecord(e2, stream_), "rec"); }
+    launch_sweep();
+    if (prof) { e3 = get_event(); cuda_check(cudaEventRecord(e3, stream_), "rec"); pending_.push_back({e2, e3, 1, 0.0}); }
+}
+
+// The step loop as CUDA graphs of up to 64 steps (kernels read the step from
+// d_step, so one graph serves every chunk of a simulate call).  With
+// profiling, per-kernel CUDA events are captured into the graph (event record
+// nodes) and read after each replay, so the timed loop keeps graph launch
+// costs while reporting per-kernel device time.  Returns the summed device
+// time of the chunks.
+double Engine::run_graph_chunks(const NeuronArgs& na, int steps) {
+    const int chunk = std::min(steps, 64);
+    const bool prof = opt_.profile != 0;
+    const bool fused = opt_.world == 1;
+    const int per = 6;
+    std::vector<cudaEvent_t> ev(prof ? static_cast<size_t>(chunk) * per : 0);
+    for (auto& e : ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    const HistArgs h = hist_args();
+    auto capture = [&](int k) {
+        cudaGraph_t g;
+        cudaGraphExec_t ge;
+        cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
+        for (int s = 0; s < k; ++s) {
+            // per-kernel events on every kProfStride-th step only: event nodes cost
+            // ~1% of a 1.3 ms step when placed around every kernel
+            cudaEvent_t* e = (prof && s % kProfStride == 0) ? &ev[static_cast<size_t>(s) * per] : nullptr;
+            if (e) cuda_check(cudaEventRecordWithFlags(e[0], stream_, cudaEventRecordExternal), "rec");
+            launch_neuron(na, exact_, fused, h, stream_);
+            if (e) cuda_check(cudaEventRecordWithFlags(e[1], stream_, cudaEventRecordExternal), "rec");
+            if (!fused) {
+                if (e) cuda_check(cudaEventRecordWithFlags(e[2], stream_, cudaEventRecordExternal), "rec");
+                if (comm_ && !p2p_) comm_->all_gather_inplace(d_bits_.as<uint32_t>(), static_cast<size_t>(part_ / 32), stream_);
+                launch_hist(h, stream_);
+                if (e) cuda_check(cudaEventRecordWithFlags(e[3], stream_, cudaEventRecordExternal), "rec");
+            }
+            if (e) cuda_check(cudaEventRecordWithFlags(e[4], stream_, cudaEventRecordExternal), "rec");
+            launch_sweep_only();
+            if (e) cuda_check(cudaEventRecordWithFlags(e[5], stream_, cudaEventRecordExternal), "rec");
+        }
+        cuda_check(cudaStreamEndCapture(stream_, &g), "end capture");
+        cuda_check(cudaGraphInstantiate(&ge, g, 0), "instantiate");
+        cudaGraphDestroy(g);
+        return ge;
+    };
+    cudaGraphExec_t full = capture(chunk);
+    cudaGraphExec_t tail = (steps % chunk) ? capture(steps % chunk) : nullptr;
+    const int per_step_kernels = fused ? 2 : 3;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spans;
+    double total = 0.0;
+    for (int done = 0; done < steps;) {
+        const int k = std::min(chunk, steps - done);
+        cudaEvent_t c0 = get_event(), c1 = get_event();
+        cuda_check(cudaEventRecord(c0, stream_), "rec");
+        cuda_check(cudaGraphLaunch(k == chunk ? full : tail, stream_), "graph launch");
+        cuda_check(cudaEventRecord(c1, stream_), "rec");
+        spans.emplace_back(c0, c1);
+        stats_.kernel_launches += static_cast<int64_t>(per_step_kernels) * k;
+        if (prof) {
+            cuda_check(cudaStreamSynchronize(stream_), "profile sync");
+            for (int s = 0; s < k; s += kProfStride) {
+                const cudaEvent_t* e = &ev[static_cast<size_t>(s) * per];
+                float a = 0.f, b = 0.f, c = 0.f;
+                cuda_check(cudaEventElapsedTime(&a, e[0], e[1]), "elapsed");
+                cuda_check(cudaEventElapsedTime(&c, e[4], e[5]), "elapsed");
+                if (!fused) cuda_check(cudaEventElapsedTime(&b, e[2], e[3]), "elapsed");
+                stats_.neuron_ms += a;
+                stats_.neuron_launches += 1;
+                stats_.exchange_ms += b;
+                stats_.sweep_ms += c;
+                stats_.sweep_launches += 1;
+            }
+        }
+        done += k;
+    }
+    cuda_check(cudaStreamSynchronize(stream_), "simulate sync");
+    for (auto& sp : spans) {
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, sp.first, sp.second), "elapsed");
+        total += ms;
+        cudaEventDestroy(sp.first);
+        cudaEventDestroy(sp.second);
+    }
+    cudaGraphExecDestroy(full);
+    if (tail) cudaGraphExecDestroy(tail);
+    for (auto& e : ev) cudaEventDestroy(e);
+    return total;
+}
+
+void Engine::flush_pending() {
+    if (pending_.empty()) return;
+    cuda_check(cudaStreamSynchronize(stream_), "profile sync");
+    for (auto& p : pending_) {
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, p.a, p.b), "elapsed");
+        if (p.kind == 0) { stats_.neuron_ms += ms; stats_.neuron_launches += 1; }
+        else if (p.kind == 1) { stats_.sweep_ms += ms; stats_.sweep_launches += 1; }
+        else if (p.kind == 2) { stats_.exchange_ms += ms; }
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    pending_.clear();
+}
+
+void Engine::simulate(int32_t steps) {
+    require_setup("sn_simulate");
+    if (steps < 1) throw InvalidArgument(run_name() + ": steps must be >= 1");
+    if (opt_.world > 1 && !comm_ && !p2p_)
+        throw LogicError("sn_simulate: partitioned engine needs sn_comm_init or sn_p2p_open "
+                         "(or use sn_step_local/sn_step_finish)");
+    cuda_check(cudaSetDevice(opt_.device), "cudaSetDevice");
+    build_stimulus_table();
+    const int t0 = t_;
+    double* trace = nullptr;
+    if (opt_.record_membrane) {
+        d_trace_.alloc(static_cast<size_t>(steps) * std::max(nl_, 1) * 8);
+        trace = d_trace_.as<double>();
+    }
+    cudaEvent_t eb = get_event(), ee = get_event();
+    double graph_ms = -1.0;  // device time summed over graph chunks (excludes host syncs)
+    if (tiny_) {
+        // one CTA runs the call; stream_io: stimulus read from and raster
+        // written to pinned host memory by the kernel itself
+        const size_t rwords = static_cast<size_t>(steps) * std::max(nl_words_, 1);
+        uint32_t* raster;
+        stats_.h2d_bytes_last = 0.0;
+        if (opt_.stream_io) {
+            h_raster_.reserve(rwords * 4);
+            raster = h_raster_.as<uint32_t>();
+        } else {
+            if (d_raster_.bytes < rwords * 4) d_raster_.alloc(rwords * 4);
+            raster = d_raster_.as<uint32_t>();
+        }
+        cuda_check(cudaEventRecord(eb, stream_), "rec");
+        cudaEvent_t p0{}, p1{};
+        if (opt_.profile) { p0 = get_event(); cuda_check(cudaEventRecord(p0, stream_), "rec"); }
+        run_tiny(t0, steps, raster, trace, opt_.stream_io != 0);
+        if (opt_.profile) {  // the call is one fused launch: accounted as the sweep
+            p1 = get_event();
+            cuda_check(cudaEventRecord(p1, stream_), "rec");
+            pending_.push_back({p0, p1, 1, 0.0});
+        }
+        cuda_check(cudaEventRecord(ee, stream_), "rec");
+        RasterChunk ch;
+        ch.t0 = t0;
+        ch.rows = steps;
+        ch.words.resize(static_cast<size_t>(steps) * nl_words_);
+        if (!opt_.stream_io && !ch.words.empty())
+            cuda_check(cudaMemcpyAsync(ch.words.data(), raster, ch.words.size() * 4, cudaMemcpyDeviceToHost, stream_),
+                       "raster D2H");
+        cuda_check(cudaStreamSynchronize(stream_), "simulate sync");
+        if (opt_.stream_io && !ch.words.empty()) std::memcpy(ch.words.data(), raster, ch.words.size() * 4);
+        if (opt_.stream_io) stats_.d2h_bytes_last = static_cast<double>(ch.words.size()) * 4;
+        raster_.push_back(std::move(ch));
+    } else {
+        // stream_io (the end-to-end path): this call's stimulus rows go H2D from
+        // pinned memory in one copy inside the timed region, and the kernels
+        // store every step's spike words straight into pinned host memory
+        // (mapped), so each step's result crosses to the host as it is made.
+        const size_t rwords = static_cast<size_t>(steps) * std::max(nl_words_, 1);
+        uint32_t* raster = nullptr;
+        const int64_t* st_off = d_st_off_.as<int64_t>();
+        const int32_t* st_neuron = d_st_neuron_.as<int32_t>();
+        const double* st_amp = d_st_amp_.as<double>();
+        int32_t st_rows = st_steps_dev_, st_base = 0;
+        cuda_check(cudaEventRecord(eb, stream_), "rec");
+        if (opt_.stream_io) {
+            h_raster_.reserve(rwords * 4);
+            raster = h_raster_.as<uint32_t>();
+            const int table = static_cast<int>(hs_off_.size()) - 1;
+            st_rows = std::max(0, std::min(table - t0, steps));
+            st_base = t0;
+            const int64_t lo = st_rows > 0 ? hs_off_[t0] : 0, hi = st_rows > 0 ? hs_off_[t0 + st_rows] : 0;
+            const size_t cnt = static_cast<size_t>(hi - lo);
+            const size_t ob = round_up((static_cast<int64_t>(st_rows) + 1) * 8, 16);
+            const size_t bytes = ob + cnt * 12 + 16;
+            h_stage_.reserve(bytes);
+            uint8_t* hb = h_stage_.as<uint8_t>();
+            int64_t* soff = reinterpret_cast<int64_t*>(hb);
+            for (int r = 0; r <= st_rows; ++r) soff[r] = (st_rows > 0 ? hs_off_[t0 + r] : 0) - lo;
+            if (cnt) {
+                std::memcpy(hb + ob, hs_amp_.data() + lo, cnt * 8);
+                std::memcpy(hb + ob + cnt * 8, hs_neuron_.data() + lo, cnt * 4);
+            }
+            if (d_stage_.bytes < bytes) d_stage_.alloc(std::max(bytes, 2 * d_stage_.bytes));
+            cuda_check(cudaMemcpyAsync(d_stage_.p, hb, bytes, cudaMemcpyHostToDevice, stream_), "stim H2D");
+            uint8_t* db = d_stage_.as<uint8_t>();
+            st_off = reinterpret_cast<const int64_t*>(db);
+            st_amp = reinterpret_cast<const double*>(db + ob);
+            st_neuron = reinterpret_cast<const int32_t*>(db + ob + cnt * 8);
+            stats_.h2d_bytes_last = static_cast<double>(bytes);
+        } else {
+            if (d_raster_.bytes < rwords * 4) d_raster_.alloc(rwords * 4);
+            raster = d_raster_.as<uint32_t>();
+        }
+        NeuronArgs na = neuron_args(t0, steps, raster, trace, st_off, st_neuron, st_amp, st_rows, st_base);
+        if (persistent_) {
+            cudaEvent_t p0{}, p1{};
+            if (opt_.profile) { p0 = get_event(); cuda_check(cudaEventRecord(p0, stream_), "rec"); }
+            if (cols_) {
+                ColArgs ca{};
+                ca.hist2 = d_hist2_.as<uint64_t>();
+                ca.pot2 = d_pot2_.p;
+                ca.act3 = d_act2_.as<uint32_t>();
+                ca.row_plastic = d_row_plastic_.as<uint8_t>();
+                ca.a_plus = d_ap_.as<double>();
+                ca.a_minus = d_am_.as<double>();
+                ca.window = window_;
+                ca.dmax = dmax_;
+                // activity and raster words are OR-ed by 8-post groups: start from zero
+                cuda_check(cudaMemsetAsync(d_act2_.p, 0, d_act2_.bytes, stream_), "memset");
+                if (raster && nl_words_ > 0)
+                    cuda_check(cudaMemsetAsync(raster, 0, static_cast<size_t>(steps) * nl_words_ * 4, stream_), "memset");
+                launch_persistent_cols(na, dense_args(), ca, f64_, stdp_on_, has_delay_, col_width_, persist_grid_,
+                                       steps, stream_);
+            } else {
+                launch_persistent_dense(na, hist_args(), dense_args(), f64_, stdp_on_, has_delay_, persist_grid_,
+                                        steps, stream_);
+            }
+            stats_.kernel_launches += 1;
+            if (opt_.profile) {
+                p1 = get_event();
+                cuda_check(cudaEventRecord(p1, stream_), "rec");
+                pending_.push_back({p0, p1, 1, 0.0});
+            }
+            cuda_check(cudaEventRecord(ee, stream_), "rec");
+        } else if (opt_.use_graphs) {
+            graph_ms = run_graph_chunks(na, steps);
+            cuda_check(cudaEventRecord(ee, stream_), "rec");
+        } else {
+            for (int s = 0; s < steps; ++s) enqueue_step(na, true);
+            cuda_check(cudaEventRecord(ee, stream_), "rec");
+        }
+        RasterChunk ch;
+        ch.t0 = t0;
+        ch.rows = steps;
+        ch.words.resize(static_cast<size_t>(steps) * nl_words_);
+        if (!opt_.stream_io && !ch.words.empty())
+            cuda_check(cudaMemcpyAsync(ch.words.data(), d_raster_.p, ch.words.size() * 4, cudaMemcpyDeviceToHost, stream_), "raster D2H");
+        cuda_check(cudaStreamSynchronize(stream_), "simulate sync");
+        if (opt_.stream_io && !ch.words.empty()) std::memcpy(ch.words.data(), raster, ch.words.size() * 4);
+        if (opt_.stream_io) stats_.d2h_bytes_last = static_cast<double>(ch.words.size()) * 4;
+        raster_.push_back(std::move(ch));
+    }
+    float ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&ms, eb, ee), "elapsed");
+    cudaEventDestroy(eb);
+    cudaEventDestroy(ee);
+    stats_.last_simulate_ms = graph_ms >= 0.0 ? graph_ms : ms;
+    flush_pending();
+    check_exchange_error();
+    if (opt_.record_membrane) {
+        const size_t cnt = static_cast<size_t>(steps) * nl_;
+        const size_t old = trace_.size();
+        trace_.resize(old + cnt);
+        if (cnt) cuda_check(cudaMemcpy(trace_.data() + old, d_trace_.p, cnt * 8, cudaMemcpyDeviceToHost), "trace D2H");
+        trace_rows_ += steps;
+    }
+    t_ += steps;
+    stats_.steps_done = t_;
+    events_valid_ = false;
+}
+
+void Engine::synchronize() { cuda_check(cudaStreamSynchronize(stream_), "sn_synchronize"); }
+
+// ---- host-driven exchange (partition emulation / custom transports) ---------
+void Engine::step_local() {
+    require_setup("sn_step_local");
+    if (tiny_) throw LogicError("sn_step_local: single-partition engines run through sn_simulate");
+    host_exchange_ = true;
+    build_stimulus_table();
+    if (d_raster_.bytes < static_cast<size_t>(std::max(nl_words_, 1)) * 4)
+        d_raster_.alloc(static_cast<size_t>(std::max(nl_words_, 1)) * 4);
+    double* trace = nullptr;
+    if (opt_.record_membrane) {
+        d_trace_.alloc(static_cast<size_t>(std::max(nl_, 1)) * 8);
+        trace = d_trace_.as<double>();
+    }
+    if (opt_.stream_io) throw Unsupported("sn_step_local: stream_io engines use sn_simulate");
+    NeuronArgs na = neuron_args(t_, 1, d_raster_.as<uint32_t>(), trace, d_st_off_.as<int64_t>(),
+                                d_st_neuron_.as<int32_t>(), d_st_amp_.as<double>(), st_steps_dev_, 0);
+    launch_neuron(na, exact_, opt_.world == 1, hist_args(), stream_);
+    stats_.kernel_launches += 1;
+    cuda_check(cudaStreamSynchronize(stream_), "step_local sync");
+}
+
+void Engine::get_spike_words(uint32_t* out, int64_t words) {
+    require_setup("sn_get_spike_words");
+    if (words > words_) throw InvalidArgument("sn_get_spike_words: more words than the bitmask holds");
+    cuda_check(cudaMemcpy(out, d_bits_.p, static_cast<size_t>(words) * 4, cudaMemcpyDeviceToHost), "bits D2H");
+}
+
+void Engine::put_spike_words(int32_t first_word, const uint32_t* w, int64_t count) {
+    require_setup("sn_put_spike_words");
+    if (first_word < 0 || first_word + count > words_) throw InvalidArgument("sn_put_spike_words: range outside the bitmask");
+    cuda_check(cudaMemcpy(d_bits_.as<uint32_t>() + first_word, w, static_cast<size_t>(count) * 4, cudaMemcpyHostToDevice), "bits H2D");
+}
+
+void Engine::step_finish() {
+    require_setup("sn_step_finish");
+    if (tiny_) throw LogicError("sn_step_finish: single-partition engines run through sn_simulate");
+    if (opt_.world > 1) {
+        launch_hist(hist_args(), stream_);
+        stats_.kernel_launches += 1;
+    }
+    launch_sweep();
+    RasterChunk ch;
+    ch.t0 = t_;
+    ch.rows = 1;
+    ch.words.resize(static_cast<size_t>(nl_words_));
+    if (nl_words_) cuda_check(cudaMemcpyAsync(ch.words.data(), d_raster_.p, ch.words.size() * 4, cudaMemcpyDeviceToHost, stream_), "raster D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "step_finish sync");
+    check_exchange_error();
+    raster_.push_back(std::move(ch));
+    if (opt_.record_membrane) {
+        const size_t old = trace_.size();
+        trace_.resize(old + nl_);
+        if (nl_) cuda_check(cudaMemcpy(trace_.data() + old, d_trace_.p, static_cast<size_t>(nl_) * 8, cudaMemcpyDeviceToHost), "trace D2H");
+        trace_rows_ += 1;
+    }
+    t_ += 1;
+    stats_.steps_done = t_;
+    events_valid_ = false;
+}
+
+}  // namespace snb

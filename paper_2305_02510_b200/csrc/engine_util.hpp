@@ -1,0 +1,45 @@
+// Small host helpers shared by the engine translation units.
+#pragma once
+
+#include "engine.hpp"
+
+#include <cstdint>
+#include <cstdio>
+#include <sstream>
+#include <string>
+#include <vector>
+
+namespace snb {
+namespace {
+
+
+inline std::string fmt_double(double v) {  // model.cpp:26-30
+    std::ostringstream os;
+    os << v;
+    return os.str();
+}
+
+inline void throw_first(const char* where, const std::vector<std::string>& v) {  // mat_engine.cpp:15-21
+    if (v.empty()) return;
+    std::string msg = std::string(where) + ": " + v.front();
+    if (v.size() > 1) msg += " (+" + std::to_string(v.size() - 1) + " more)";
+    throw InvalidArgument(msg);
+}
+
+template <typename T>
+inline void upload(DevBuf& d, const std::vector<T>& h) {
+    d.alloc(h.size() * sizeof(T));
+    if (!h.empty()) cuda_check(cudaMemcpy(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+}
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+inline uint64_t host_mix64(uint64_t z) {  // rng.hpp:8-12
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+
+}  // namespace
+}  // namespace snb
