@@ -131,3 +131,40 @@ def test_word_packing_roundtrip_and_merge():
     b = (np.array([0, 1], np.int32), np.array([40, 33], np.int32))
     st, nr = D.merge_rasters([a, b])
     assert list(zip(st.tolist(), nr.tolist())) == [(0, 1), (0, 5), (0, 40), (1, 33), (2, 3)]
+
+
+def _id_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [os.path.dirname(here), here]
+    import torch.distributed as dist
+    from paper_2305_02510_b200 import distributed as D
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        uid = D.broadcast_uid(bytes(range(128)) if rank == 0 else None)
+        handles = D.exchange_p2p_handles(bytes([rank]) * 128)
+        q.put((rank, uid, handles))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_communicator_id_and_p2p_handle_exchange(world):
+    """bench.py's connect(): rank 0's NCCL unique id reaches every rank, and
+    every rank receives all ranks' IPC handle blocks in rank order (the layout
+    sn_p2p_open expects)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    expect = b"".join(bytes([r]) * 128 for r in range(world))
+    for rank, uid, handles in got:
+        assert uid == bytes(range(128))
+        assert handles == expect
