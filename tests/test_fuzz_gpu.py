@@ -99,3 +99,62 @@ def test_random_plans_match_oracle(seed):
         assert np.allclose(mem, o["membrane"], rtol=1e-5, atol=1e-4), tag
         if w is not None and stdp is not None:  # fp32 updates of weights up to |3| over 120 steps
             assert np.allclose(w, o["weights"], rtol=1e-5, atol=2e-5), tag
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SNB_FUZZ_MEDIUM", "12"))))
+def test_random_medium_plans_match_oracle(seed):
+    """Medium nets (2k-20k neurons: several dense row chunks / TMA items,
+    several sparse pre blocks) with random weights, delays, plasticity and
+    options against the C oracle (rasters identical, fp64 weights exact)."""
+    from oracle import bridge as B
+    from paper_2305_02510_b200.engine import MatEngine
+    from paper_2305_02510_b200.model import StdpConfig
+    from paper_2305_02510_b200.netgen import RandomStream, erdos_renyi_arrays, scenario_stimulus
+    rng = np.random.default_rng(7700 + seed)
+    n = int(rng.choice([2048, 5000, 12000, 20000]))
+    p = float({2048: 0.05, 5000: 0.01, 12000: 0.003, 20000: 0.002}[n])
+    pre, post = erdos_renyi_arrays(n, p, 7700 + seed)
+    m = len(pre)
+    rs = RandomStream(7700 + seed, 5)
+    k = np.arange(m, dtype=np.uint64)
+    dmax = int(rng.choice([1, 4, 20, 40]))
+    delay = (1 + rs.below_np(k, dmax)).astype(np.int32)
+    kind = str(rng.choice(["one", "three", "float"]))
+    w = (np.ones(m) if kind == "one" else np.array([1.0, 2.0, -1.0])[rs.below_np(k + np.uint64(m), 3)]
+         if kind == "three" else 0.2 + rs.unit_np(k + np.uint64(2 * m)))
+    stdp = None
+    plastic = np.zeros(m, np.uint8)
+    if rng.random() < 0.4 and dmax <= 20:
+        stdp = StdpConfig.defaults()
+        plastic = (rs.unit_np(k + np.uint64(3 * m)) < 0.5).astype(np.uint8)
+    thr = np.full(n, 1.0 if kind != "float" else 1.3)
+    arrays = {"threshold": thr, "leak": np.full(n, 0.25), "reset": np.zeros(n), "refractory": np.full(n, 1, np.int32),
+              "axonal": np.zeros(n, np.int32), "pre": pre, "post": post, "weight": w, "delay": delay, "stdp": plastic}
+    steps = 30
+    stim = scenario_stimulus(n, steps, 7700 + seed, count=max(3, n // 50), period=3, amplitude=2.0).to_arrays()
+    sd = None if stdp is None else (stdp.window, np.array(stdp.a_plus), np.array(stdp.a_minus), stdp.w_min, stdp.w_max)
+    o = B.run_oracle(arrays, steps, stim, sd)
+    opts = dict(storage=int(rng.integers(1, 3)), precision="f64", exact_order=bool(rng.random() < 0.3),
+                use_graphs=bool(rng.random() < 0.7), persistent=bool(rng.random() < 0.5),
+                stream_io=bool(rng.random() < 0.3))
+    eng = MatEngine(**opts)
+    try:
+        eng.add_neurons(thr, arrays["leak"], arrays["reset"], arrays["refractory"], arrays["axonal"])
+        eng.add_synapses(pre, post, w, delay, plastic)
+        if stdp is not None:
+            eng.set_stdp(*sd)
+        eng.setup()
+        eng.add_stimulus(*stim)
+        eng.simulate(steps)
+        s, q = eng.raster()
+        mem = eng.membrane()
+        wt = eng.synapse_weights()
+        kernel = eng.stats()["sweep_kernel"]
+    finally:
+        eng.close()
+    tag = (seed, n, dmax, kind, stdp is not None, opts, kernel)
+    assert len(o["steps"]) > 0, tag
+    assert np.array_equal(s, o["steps"]) and np.array_equal(q, o["neurons"]), tag
+    assert close_rel(mem, o["membrane"]), tag
+    if stdp is not None:
+        assert np.array_equal(wt, o["weights"]), tag
