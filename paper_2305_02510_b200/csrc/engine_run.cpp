@@ -485,12 +485,23 @@ void Engine::simulate(int32_t steps) {
                 ca.a_minus = d_am_.as<double>();
                 ca.window = window_;
                 ca.dmax = dmax_;
-                // activity and raster words are OR-ed by 8-post groups: start from zero
+                ca.active_count = d_spikes_.as<unsigned long long>() + 1;
+                // activity and raster words are OR-ed by 8-post groups: start from
+                // zero, and keep the OR targets in device memory (atomics on mapped
+                // host memory would cross PCIe one by one); stream_io copies the
+                // raster out once after the kernel
                 cuda_check(cudaMemsetAsync(d_act2_.p, 0, d_act2_.bytes, stream_), "memset");
-                if (raster && nl_words_ > 0)
-                    cuda_check(cudaMemsetAsync(raster, 0, static_cast<size_t>(steps) * nl_words_ * 4, stream_), "memset");
-                launch_persistent_cols(na, dense_args(), ca, f64_, stdp_on_, has_delay_, col_width_, persist_grid_,
+                const size_t rbytes = static_cast<size_t>(steps) * nl_words_ * 4;
+                NeuronArgs nc = na;
+                if (opt_.stream_io && raster) {
+                    if (d_raster_.bytes < rbytes) d_raster_.alloc(rbytes);
+                    nc.raster = d_raster_.as<uint32_t>();
+                }
+                if (nc.raster && rbytes) cuda_check(cudaMemsetAsync(nc.raster, 0, rbytes, stream_), "memset");
+                launch_persistent_cols(nc, dense_args(), ca, f64_, stdp_on_, has_delay_, col_width_, persist_grid_,
                                        steps, stream_);
+                if (opt_.stream_io && raster && rbytes)
+                    cuda_check(cudaMemcpyAsync(raster, nc.raster, rbytes, cudaMemcpyDeviceToHost, stream_), "raster D2H");
             } else {
                 launch_persistent_dense(na, hist_args(), dense_args(), f64_, stdp_on_, has_delay_, persist_grid_,
                                         steps, stream_);

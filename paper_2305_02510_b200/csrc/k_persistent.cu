@@ -372,7 +372,10 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
             const uint32_t aw = __ballot_sync(0xffffffffu, act);
             if (lane == 0) {
                 const int wi = (c * kColW) >> 5, sh = (c * kColW) & 31;
-                if (aw) atomicOr(act_now + wi, aw << sh);
+                if (aw) {
+                    atomicOr(act_now + wi, aw << sh);
+                    if (ca.active_count) atomicAdd(ca.active_count, static_cast<unsigned long long>(__popc(aw)));
+                }
                 if (word) {
                     if (na.raster && (t - na.t_base) < na.raster_rows)
                         atomicOr(na.raster + static_cast<int64_t>(t - na.t_base) * na.nl_words + wi, word << sh);

@@ -212,6 +212,7 @@ struct ColArgs {
     const double* a_minus;
     int32_t window;
     int32_t dmax;
+    unsigned long long* active_count;  // running sum of active rows (algorithmic bytes)
 };
 int persistent_cols_max_ctas(bool f64, bool stdp, bool delay, int width);
 void launch_persistent_cols(const NeuronArgs& na, const DenseArgs& da, const ColArgs& ca, bool f64, bool stdp,
