@@ -207,7 +207,7 @@ DenseArgs Engine::dense_args() {
 void Engine::launch_sweep_only() {
     if (dense_) {
         DenseArgs a = dense_args();
-        if (tma_) launch_dense_tma(a, stdp_on_, dense_grid_, stream_);
+        if (tma_) launch_dense_tma(a, f64_, stdp_on_, has_delay_, dense_grid_, stream_);
         else launch_dense(a, f64_, stdp_on_, has_delay_, exact_, dense_grid_, stream_);
     } else {
         SparseArgs a{};

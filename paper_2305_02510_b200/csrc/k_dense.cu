@@ -189,7 +189,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_dense_stream(DenseArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// TMA-staged dense sweep (fp32, unit delays): one CTA per SM, a producer warp
+// TMA-staged dense sweep (fp32 or fp64 weights; with synaptic delays the
+// rows' delay bytes ride in the same stages): one CTA per SM, a producer warp
 // streams the active rows' tile segments into a kTmaStages-deep shared-memory
 // ring with cp.async.bulk (completion on mbarriers), 8 consumer warps apply
 // the same per-element update as k_dense_stream from shared memory and write
@@ -200,29 +201,33 @@ constexpr int kTmaStages = 8;      // ring depth
 constexpr int kTmaListMax = 2048;  // rows per item (one list build per item)
 constexpr int kTmaThreads = 288;   // 8 consumer warps + 1 producer warp
 
-template <bool STDP>
+template <typename WT, bool STDP, bool DELAY>
 __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
+    using VT = VecT<WT>;
+    using V = typename VT::V;
+    constexpr int VEC = VT::N;
     extern __shared__ __align__(128) uint8_t smem[];
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const bool producer = warp == 8;
     const int ntiles = (a.nl + a.tile_w - 1) / a.tile_w;
     const int items = ntiles * a.nchunks;
-    const uint32_t row_bytes = static_cast<uint32_t>(a.tile_w) * 4u;
-    const size_t stage_bytes = static_cast<size_t>(kTmaRows) * row_bytes;
-    float* ring = reinterpret_cast<float*>(smem);
+    const uint32_t row_bytes = static_cast<uint32_t>(a.tile_w) * static_cast<uint32_t>(sizeof(WT));
+    const uint32_t drow_bytes = DELAY ? static_cast<uint32_t>(a.tile_w) : 0u;  // delay bytes per row segment
+    const size_t stage_bytes = static_cast<size_t>(kTmaRows) * (row_bytes + drow_bytes);
+    uint8_t* ring = smem;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * stage_bytes);
     uint64_t* empty = full + kTmaStages;
-    RowRec<float>* s_rec = reinterpret_cast<RowRec<float>*>(empty + kTmaStages);
+    RowRec<WT>* s_rec = reinterpret_cast<RowRec<WT>*>(empty + kTmaStages);
     __shared__ uint32_t s_word[32];
     __shared__ int32_t s_wpref[33];
     __shared__ int32_t s_cnt;
     __shared__ int s_item;
 
-    const float wmin = static_cast<float>(a.w_min), wmax = static_cast<float>(a.w_max);
-    const float* dep = static_cast<const float*>(a.dep);
-    const float* pot = static_cast<const float*>(a.pot);
-    float* W = static_cast<float*>(a.w);
+    const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
+    const WT* dep = static_cast<const WT*>(a.dep);
+    const WT* pot = static_cast<const WT*>(a.pot);
+    WT* W = static_cast<WT*>(a.w);
 
     if (tid == 0) {
         for (int s = 0; s < kTmaStages; ++s) {
@@ -245,7 +250,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
         const int tile = item - chunk * ntiles;
         const int col0 = tile * a.tile_w;
         const int width = static_cast<int>(min(static_cast<int64_t>(a.tile_w), a.pitch - col0));
-        const uint32_t copy_bytes = static_cast<uint32_t>(width) * 4u;
+        const uint32_t copy_bytes = static_cast<uint32_t>(width) * static_cast<uint32_t>(sizeof(WT));
         const int r0 = chunk * a.rows_per_chunk;
         const int r1 = min(a.n, r0 + a.rows_per_chunk);
 
@@ -285,12 +290,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                 if ((wd >> b) & 1u) {
                     const int pos = s_wpref[l] + __popc(wd & ((1u << b) - 1u));
                     const uint64_t h = __ldcg(a.hist + r);
-                    RowRec<float> rec;
+                    RowRec<WT> rec;
                     const int kind = STDP ? static_cast<int>(__ldg(a.kind + r)) : 0;
                     rec.rowk = r | (kind << 28);
                     rec.e_lo = static_cast<uint32_t>(h);
                     rec.e_hi = static_cast<uint32_t>(h >> 32);
-                    rec.pot = STDP ? __ldcg(pot + r) : 0.f;
+                    rec.pot = (STDP && !DELAY) ? __ldcg(pot + r) : WT(0);
                     s_rec[pos] = rec;
                 }
             }
@@ -308,28 +313,33 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                     const uint32_t ph = (it / kTmaStages) & 1u;
                     mbar_wait(empty + s, ph ^ 1u);
                     const int nr = min(kTmaRows, cnt - g * kTmaRows);
-                    mbar_arrive_expect_tx(full + s, static_cast<uint32_t>(nr) * copy_bytes);
+                    mbar_arrive_expect_tx(full + s, static_cast<uint32_t>(nr) * (copy_bytes + (DELAY ? width : 0)));
+                    uint8_t* st = ring + s * stage_bytes;
                     for (int r = 0; r < nr; ++r) {
                         const int row = s_rec[g * kTmaRows + r].rowk & 0x0fffffff;
-                        bulk_g2s(reinterpret_cast<uint8_t*>(ring) + s * stage_bytes + static_cast<size_t>(r) * row_bytes,
-                                 W + static_cast<int64_t>(row) * a.pitch + col0, copy_bytes, full + s);
+                        bulk_g2s(st + static_cast<size_t>(r) * row_bytes, W + static_cast<int64_t>(row) * a.pitch + col0,
+                                 copy_bytes, full + s);
+                        if (DELAY)
+                            bulk_g2s(st + static_cast<size_t>(kTmaRows) * row_bytes + static_cast<size_t>(r) * drow_bytes,
+                                     a.delay + static_cast<int64_t>(row) * a.pitch + col0, static_cast<uint32_t>(width),
+                                     full + s);
                     }
                 }
             } else {
                 it += ngroups;
             }
         } else {
-            const int tcol = tid * 4;
+            const int tcol = tid * VEC;
             const int c0 = col0 + tcol;
             const bool in_tile = tcol < width && c0 < a.nl;
             const int gc0 = a.first + c0;
-            float sjf[4], depj[4];
-            double acc[4];
+            WT sjf[VEC], depj[VEC];
+            double acc[VEC];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < VEC; ++k) {
                 const bool ok = in_tile && (c0 + k) < a.nl;
-                sjf[k] = (ok && STDP && bit_of(a.bits, gc0 + k)) ? 1.f : 0.f;
-                depj[k] = (ok && STDP) ? __ldcg(dep + gc0 + k) : 0.f;
+                sjf[k] = (ok && STDP && bit_of(a.bits, gc0 + k)) ? WT(1) : WT(0);
+                depj[k] = (ok && STDP) ? __ldcg(dep + gc0 + k) : WT(0);
                 acc[k] = 0.0;
             }
             for (int g = 0; g < ngroups; ++g, ++it) {
@@ -337,52 +347,72 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                 const uint32_t ph = (it / kTmaStages) & 1u;
                 mbar_wait(full + s, ph);
                 const int nr = min(kTmaRows, cnt - g * kTmaRows);
-                float grp[4] = {0.f, 0.f, 0.f, 0.f};
+                const uint8_t* st = ring + s * stage_bytes;
+                WT grp[VEC];
+#pragma unroll
+                for (int k = 0; k < VEC; ++k) grp[k] = WT(0);
                 if (in_tile) {
 #pragma unroll
                     for (int r = 0; r < kTmaRows; ++r) {
                         if (r >= nr) break;
-                        const RowRec<float> rec = s_rec[g * kTmaRows + r];
+                        const RowRec<WT> rec = s_rec[g * kTmaRows + r];
                         const int row = rec.rowk & 0x0fffffff;
                         const int kind = rec.rowk >> 28;
-                        const float4 wv = *reinterpret_cast<const float4*>(
-                            reinterpret_cast<const uint8_t*>(ring) + s * stage_bytes + static_cast<size_t>(r) * row_bytes + tcol * 4);
-                        float w[4] = {wv.x, wv.y, wv.z, wv.w};
-                        const float ef = (rec.e_lo & 1u) ? 1.f : 0.f;
-                        if (STDP && kind != kRowNone) {
-                            float nw[4];
+                        const V wv = *reinterpret_cast<const V*>(st + static_cast<size_t>(r) * row_bytes + tcol * sizeof(WT));
+                        uint32_t dv = 0;
+                        if (DELAY) {
+                            const uint8_t* dp8 = st + static_cast<size_t>(kTmaRows) * row_bytes +
+                                                 static_cast<size_t>(r) * drow_bytes + tcol;
+                            dv = VEC == 4 ? *reinterpret_cast<const uint32_t*>(dp8) : *reinterpret_cast<const uint16_t*>(dp8);
+                        }
+                        const uint64_t h = (static_cast<uint64_t>(rec.e_hi) << 32) | rec.e_lo;
+                        WT w[VEC], ef[VEC];
+                        int d1[VEC];
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                const float dw = fmaf(sjf[k], rec.pot, -(ef * depj[k]));
-                                nw[k] = clamp_ref<float>(w[k] + dw, wmin, wmax);
+                        for (int k = 0; k < VEC; ++k) {
+                            w[k] = VT::get(wv, k);
+                            d1[k] = DELAY ? static_cast<int>((dv >> (8 * k)) & 0xffu) - 1 : 0;
+                            ef[k] = ((h >> d1[k]) & 1ull) ? WT(1) : WT(0);  // s_pre[t+1-d], exact 0/1 factor
+                        }
+                        if (STDP && kind != kRowNone) {
+                            WT nw[VEC];
+#pragma unroll
+                            for (int k = 0; k < VEC; ++k) {
+                                const WT p = DELAY ? __ldg(pot + static_cast<int64_t>(row) * a.dp + d1[k]) : rec.pot;
+                                // dw = 0; if s_post dw += pot; if s_pre dw -= dep (mat_engine.cpp:243-246)
+                                const WT dw = fma(sjf[k], p, -(ef[k] * depj[k]));
+                                nw[k] = clamp_ref<WT>(w[k] + dw, wmin, wmax);
                             }
                             if (kind == kRowAllButSelf) {
                                 const int selfk = row - gc0;
 #pragma unroll
-                                for (int k = 0; k < 4; ++k) nw[k] = (selfk == k) ? w[k] : nw[k];
+                                for (int k = 0; k < VEC; ++k) nw[k] = (selfk == k) ? w[k] : nw[k];
                             } else if (kind == kRowMixed) {
                                 const uint32_t mv =
                                     __ldg(a.mask + static_cast<int64_t>(row) * (a.pitch >> 5) + (c0 >> 5)) >> (c0 & 31);
 #pragma unroll
-                                for (int k = 0; k < 4; ++k) nw[k] = ((mv >> k) & 1u) ? nw[k] : w[k];
+                                for (int k = 0; k < VEC; ++k) nw[k] = ((mv >> k) & 1u) ? nw[k] : w[k];
                             }
-                            __stcs(reinterpret_cast<float4*>(W + static_cast<int64_t>(row) * a.pitch + c0),
-                                   make_float4(nw[0], nw[1], nw[2], nw[3]));
+                            V out = wv;
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) w[k] = nw[k];
+                            for (int k = 0; k < VEC; ++k) {
+                                VT::set(out, k, nw[k]);
+                                w[k] = nw[k];
+                            }
+                            VT::store(W + static_cast<int64_t>(row) * a.pitch + c0, out);
                         }
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) grp[k] = fmaf(ef, w[k], grp[k]);
+                        for (int k = 0; k < VEC; ++k) grp[k] = fma(ef[k], w[k], grp[k]);
                     }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(empty + s);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) acc[k] += static_cast<double>(grp[k]);
+                for (int k = 0; k < VEC; ++k) acc[k] += static_cast<double>(grp[k]);
             }
             if (in_tile) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
+                for (int k = 0; k < VEC; ++k)
                     if (c0 + k < a.nl) a.partial[static_cast<int64_t>(chunk) * a.nl + c0 + k] = acc[k];
             }
         }
@@ -398,9 +428,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
     if (blockIdx.x == 0 && tid == 0) *a.d_step += 1;
 }
 
-size_t dense_tma_smem(int tile_w) {
-    return static_cast<size_t>(kTmaStages) * kTmaRows * tile_w * 4 + 2 * kTmaStages * 8 +
-           static_cast<size_t>(kTmaListMax + kTmaRows) * sizeof(RowRec<float>);
+size_t dense_tma_smem(int tile_w, bool f64, bool delay) {
+    const size_t esz = f64 ? 8 : 4;
+    const size_t rec = f64 ? sizeof(RowRec<double>) : sizeof(RowRec<float>);
+    return static_cast<size_t>(kTmaStages) * kTmaRows * tile_w * (esz + (delay ? 1 : 0)) + 2 * kTmaStages * 8 +
+           static_cast<size_t>(kTmaListMax + kTmaRows) * rec;
 }
 
 }  // namespace
@@ -409,16 +441,33 @@ int dense_vec(bool f64) { return f64 ? 2 : 4; }
 
 int dense_tma_max_rows() { return kTmaListMax; }
 
-void launch_dense_tma(const DenseArgs& a, bool stdp, int grid, cudaStream_t s) {
-    const size_t smem = dense_tma_smem(a.tile_w);
-    static size_t configured[2] = {0, 0};
-    auto kern = stdp ? k_dense_tma<true> : k_dense_tma<false>;
-    if (configured[stdp ? 1 : 0] < smem) {
+template <typename WT, bool STDP, bool DELAY>
+static void dense_tma_go(const DenseArgs& a, int grid, cudaStream_t s) {
+    const size_t smem = dense_tma_smem(a.tile_w, sizeof(WT) == 8, DELAY);
+    static size_t configured = 0;
+    auto kern = k_dense_tma<WT, STDP, DELAY>;
+    if (configured < smem) {
         check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
               "k_dense_tma smem attribute");
-        configured[stdp ? 1 : 0] = smem;
+        configured = smem;
     }
     kern<<<grid, kTmaThreads, smem, s>>>(a);
+}
+
+void launch_dense_tma(const DenseArgs& a, bool f64, bool stdp, bool delay, int grid, cudaStream_t s) {
+#define SNB_T(WT)                                                                   \
+    do {                                                                            \
+        if (stdp) {                                                                 \
+            if (delay) dense_tma_go<WT, true, true>(a, grid, s);                    \
+            else dense_tma_go<WT, true, false>(a, grid, s);                         \
+        } else {                                                                    \
+            if (delay) dense_tma_go<WT, false, true>(a, grid, s);                   \
+            else dense_tma_go<WT, false, false>(a, grid, s);                        \
+        }                                                                           \
+    } while (0)
+    if (f64) SNB_T(double);
+    else SNB_T(float);
+#undef SNB_T
     check(cudaGetLastError(), "k_dense_tma");
 }
 int dense_threads() { return kThreads; }

@@ -176,9 +176,10 @@ void launch_dense(const DenseArgs& a, bool f64, bool stdp, bool delay, bool exac
 int dense_vec(bool f64);
 int dense_threads();
 int dense_stream_max_ctas(bool f64, bool stdp, bool delay);  // occupancy x SMs
-// TMA-staged fp32 unit-delay sweep: one CTA per SM, rows_per_chunk <= dense_tma_max_rows()
+// TMA-staged sweep (fp32/fp64, optional delays): one CTA per SM, rows_per_chunk <= dense_tma_max_rows();
+// with delays the tile width must be a multiple of 16 (the delay bytes are bulk-copied)
 int dense_tma_max_rows();
-void launch_dense_tma(const DenseArgs& a, bool stdp, int grid, cudaStream_t s);
+void launch_dense_tma(const DenseArgs& a, bool f64, bool stdp, bool delay, int grid, cudaStream_t s);
 void launch_sparse(const SparseArgs& a, bool f64, bool stdp, int hbits, int sub, bool exact,
                    int grid_x, cudaStream_t s);
 void launch_prologue(double* u_exact, const double* v, const double* leak, const double* reset,
