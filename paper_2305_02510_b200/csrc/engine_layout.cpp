@@ -393,14 +393,15 @@ void Engine::plan_launches() {
             // TMA-staged variant (fp32, unit delays): one CTA per SM claiming items
             const char* dk = std::getenv("SNB_DENSE_KERNEL");
             // default (tools/ab_tma.sh, cfg3: 1.284 ms vs 1.425 ms for k_dense_stream)
-            // fp64 weights: 2.601 ms vs 2.990 ms (k_dense_stream) on a 32k fp64 STDP net; with
-            // delays the per-element pot^(d) gathers make it slower (2.296 vs 2.095 ms, d <= 4),
-            // so delayed nets take it only on request (SNB_DENSE_KERNEL=tma)
-            tma_ = !(dk && std::string(dk) == "stream") && (!has_delay_ || (dk && std::string(dk) == "tma"));
+            // fp64 weights: 2.601 ms vs 2.990 ms (k_dense_stream) on a 32k fp64 STDP net; delays
+            // 1-4 with STDP (delay bytes in the stages, pot^(d) staged per row): 1.746 vs 2.095 ms
+            tma_ = !(dk && std::string(dk) == "stream");
+            if (tma_ && has_delay_ && stdp_on_ && dp_ > dense_tma_max_dp()) tma_ = false;
             if (tma_ && has_delay_) {  // the delay bytes are bulk-copied: 16-byte multiples
                 tile_w_ = static_cast<int32_t>(round_up(tile_w_, 16));
                 ntiles = std::max(1, (nl_ + tile_w_ - 1) / tile_w_);
             }
+            if (tma_ && !dense_tma_fits(tile_w_, f64_, has_delay_, stdp_on_)) tma_ = false;
             if (tma_) {
                 const char* tw = std::getenv("SNB_TMA_WAVES");
                 const double tw_waves = tw ? std::atof(tw) : 14.0;

@@ -200,6 +200,7 @@ constexpr int kTmaRows = 4;        // rows per stage
 constexpr int kTmaStages = 8;      // ring depth
 constexpr int kTmaListMax = 2048;  // rows per item (one list build per item)
 constexpr int kTmaThreads = 288;   // 8 consumer warps + 1 producer warp
+constexpr int kTmaDp = 4;          // delayed STDP: pot^(d) traces staged per listed row
 
 template <typename WT, bool STDP, bool DELAY>
 __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
@@ -219,6 +220,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * stage_bytes);
     uint64_t* empty = full + kTmaStages;
     RowRec<WT>* s_rec = reinterpret_cast<RowRec<WT>*>(empty + kTmaStages);
+    // delayed STDP: pot^(d) of each listed row for d = 1..kTmaDp (a.dp <= kTmaDp)
+    WT* s_potd = reinterpret_cast<WT*>(s_rec + kTmaListMax + kTmaRows);
     __shared__ uint32_t s_word[32];
     __shared__ int32_t s_wpref[33];
     __shared__ int32_t s_cnt;
@@ -297,6 +300,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                     rec.e_hi = static_cast<uint32_t>(h >> 32);
                     rec.pot = (STDP && !DELAY) ? __ldcg(pot + r) : WT(0);
                     s_rec[pos] = rec;
+                    if (STDP && DELAY)
+                        for (int d = 0; d < kTmaDp; ++d)
+                            s_potd[pos * kTmaDp + d] = d < a.dp ? __ldcg(pot + static_cast<int64_t>(r) * a.dp + d) : WT(0);
                 }
             }
             __syncthreads();
@@ -378,7 +384,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                             WT nw[VEC];
 #pragma unroll
                             for (int k = 0; k < VEC; ++k) {
-                                const WT p = DELAY ? __ldg(pot + static_cast<int64_t>(row) * a.dp + d1[k]) : rec.pot;
+                                const WT p = DELAY ? s_potd[(g * kTmaRows + r) * kTmaDp + d1[k]] : rec.pot;
                                 // dw = 0; if s_post dw += pot; if s_pre dw -= dep (mat_engine.cpp:243-246)
                                 const WT dw = fma(sjf[k], p, -(ef[k] * depj[k]));
                                 nw[k] = clamp_ref<WT>(w[k] + dw, wmin, wmax);
@@ -428,11 +434,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
     if (blockIdx.x == 0 && tid == 0) *a.d_step += 1;
 }
 
-size_t dense_tma_smem(int tile_w, bool f64, bool delay) {
+size_t dense_tma_smem(int tile_w, bool f64, bool delay, bool stdp) {
     const size_t esz = f64 ? 8 : 4;
     const size_t rec = f64 ? sizeof(RowRec<double>) : sizeof(RowRec<float>);
     return static_cast<size_t>(kTmaStages) * kTmaRows * tile_w * (esz + (delay ? 1 : 0)) + 2 * kTmaStages * 8 +
-           static_cast<size_t>(kTmaListMax + kTmaRows) * rec;
+           static_cast<size_t>(kTmaListMax + kTmaRows) * (rec + ((delay && stdp) ? kTmaDp * esz : 0));
 }
 
 }  // namespace
@@ -440,10 +446,18 @@ size_t dense_tma_smem(int tile_w, bool f64, bool delay) {
 int dense_vec(bool f64) { return f64 ? 2 : 4; }
 
 int dense_tma_max_rows() { return kTmaListMax; }
+int dense_tma_max_dp() { return kTmaDp; }
+
+bool dense_tma_fits(int tile_w, bool f64, bool delay, bool stdp) {
+    int dev = 0, optin = 0;
+    check(cudaGetDevice(&dev), "cudaGetDevice");
+    check(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
+    return dense_tma_smem(tile_w, f64, delay, stdp) + 1024 <= static_cast<size_t>(optin);  // + static smem
+}
 
 template <typename WT, bool STDP, bool DELAY>
 static void dense_tma_go(const DenseArgs& a, int grid, cudaStream_t s) {
-    const size_t smem = dense_tma_smem(a.tile_w, sizeof(WT) == 8, DELAY);
+    const size_t smem = dense_tma_smem(a.tile_w, sizeof(WT) == 8, DELAY, STDP);
     static size_t configured = 0;
     auto kern = k_dense_tma<WT, STDP, DELAY>;
     if (configured < smem) {

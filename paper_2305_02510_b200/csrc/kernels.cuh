@@ -179,6 +179,8 @@ int dense_stream_max_ctas(bool f64, bool stdp, bool delay);  // occupancy x SMs
 // TMA-staged sweep (fp32/fp64, optional delays): one CTA per SM, rows_per_chunk <= dense_tma_max_rows();
 // with delays the tile width must be a multiple of 16 (the delay bytes are bulk-copied)
 int dense_tma_max_rows();
+int dense_tma_max_dp();  // delayed STDP: plastic delay span the TMA sweep supports
+bool dense_tma_fits(int tile_w, bool f64, bool delay, bool stdp);  // ring + row lists within the smem opt-in
 void launch_dense_tma(const DenseArgs& a, bool f64, bool stdp, bool delay, int grid, cudaStream_t s);
 void launch_sparse(const SparseArgs& a, bool f64, bool stdp, int hbits, int sub, bool exact,
                    int grid_x, cudaStream_t s);
