@@ -182,6 +182,8 @@ private:
     std::vector<double> dict_;   // sparse weight dictionary (empty: weights stored per synapse)
     DevBuf d_wdict_;
     void upload_dict();
+    int32_t sparse_pres_per_block() const;
+    mutable bool pot_staged_ = false;  // STDP pull sweep stages the block's pot traces in smem
     bool sparse_tma_ = false;  // k_sparse_tma stage plan (static uniform-weight lists)
     bool bank_ordered_ = false;  // one-weight lists dealt bank-aware for k_sparse_count
     DevBuf d_sp_stages_, d_sp_first_, d_sp_block_, d_sp_bnd_;

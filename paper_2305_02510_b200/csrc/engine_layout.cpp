@@ -126,8 +126,27 @@ void Engine::build_dense_from_lists() {
     sweep_bytes_full_ = static_cast<double>(n_) * nl_ * ((stdp_on_ ? 2.0 : 1.0) * (f64_ ? 8 : 4) + (has_delay_ ? 1 : 0));
 }
 
+// Pres per block: the history-width limit, and for STDP pull sweeps small
+// enough that the block's pot^(d) traces fit the shared-memory stage.
+int32_t Engine::sparse_pres_per_block() const {
+    int pb = sparse_block_pres(hbits_);
+    pot_staged_ = false;
+    if (stdp_on_ && !exact_) {
+        const int esz = f64_ ? 8 : 4;
+        // 100k-neuron ER(p=0.01) STDP sweep: staged 0.314 ms vs 0.413 gathered at dp = 1;
+        // at dp = 8 the 768-pre blocks lost (0.672 vs 0.591 ms), so only blocks of
+        // >= 2048 pres are staged
+        const int fit = sparse_pot_stage_bytes() / (std::max(dp_, 1) * esz) / 32 * 32;
+        if (fit >= 2048) {
+            pb = std::min(pb, fit);
+            pot_staged_ = true;
+        }
+    }
+    return pb;
+}
+
 void Engine::build_sparse_from_lists() {
-    pb_ = sparse_block_pres(hbits_);
+    pb_ = sparse_pres_per_block();
     nblocks_ = (n_ + pb_ - 1) / pb_;
     const int64_t nseg = static_cast<int64_t>(nblocks_) * nl_;
     std::vector<int64_t> cnt(static_cast<size_t>(nseg) + 1, 0);
@@ -268,7 +287,7 @@ void Engine::build_generated() {
         }
         sweep_bytes_full_ = static_cast<double>(n_) * nl_ * ((stdp_on_ ? 2.0 : 1.0) * esz + (has_delay_ ? 1 : 0));
     } else {
-        pb_ = sparse_block_pres(hbits_);
+        pb_ = sparse_pres_per_block();
         nblocks_ = (n_ + pb_ - 1) / pb_;
         const int64_t nseg = static_cast<int64_t>(nblocks_) * nl_;
         DevBuf d_counts;

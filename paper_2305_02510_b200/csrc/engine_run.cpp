@@ -230,6 +230,7 @@ void Engine::launch_sweep_only() {
         a.posts_per_cta = posts_per_cta_;
         a.wdict = dict_.empty() ? nullptr : d_wdict_.p;
         a.dict_size = static_cast<int32_t>(dict_.size());
+        a.pot_staged = pot_staged_ ? 1 : 0;
         a.partial = d_partial_.as<double>();
         a.v = d_v_.as<double>();
         a.leak = d_leak_.as<double>();

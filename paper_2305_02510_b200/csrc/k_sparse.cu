@@ -62,13 +62,20 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(Spars
     WT* s_wd = reinterpret_cast<WT*>(smem_raw + hbytes);
     if (DICT)
         for (int k = tid; k < a.dict_size; k += kThreads) s_wd[k] = static_cast<const WT*>(a.wdict)[k];
+    // STDP: the block's pot^(d) traces, [pcount][dp], staged next to the history
+    // (the per-synapse lookup would otherwise be a random global gather)
+    WT* s_pot = reinterpret_cast<WT*>(smem_raw + hbytes);
+    if (STDP && a.pot_staged) {
+        const WT* src = static_cast<const WT*>(a.pot) + static_cast<int64_t>(pre0) * a.dp;
+        for (int k = tid; k < pcount * a.dp; k += kThreads) s_pot[k] = __ldcg(src + k);
+    }
     __syncthreads();
     const uint32_t* sbits = reinterpret_cast<const uint32_t*>(smem_raw);
     const HT* shist = reinterpret_cast<const HT*>(smem_raw);
     const bool uniform = DICT && a.dict_size == 2;  // {w, 0.0 padding}: every synapse carries w
 
     const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
-    const WT* pot = static_cast<const WT*>(a.pot);
+    const WT* pot = (STDP && a.pot_staged) ? s_pot : static_cast<const WT*>(a.pot) + static_cast<int64_t>(pre0) * a.dp;
     const WT* dep = static_cast<const WT*>(a.dep);
     WT* W = static_cast<WT*>(a.w);
 
@@ -163,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(Spars
                         else e = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
                         WT w = wv[u][k];
                         if (!DICT && STDP && ((m >> 22) & 1u)) {
-                            const WT pt = pot[static_cast<int64_t>(pre0 + pl) * a.dp + d1];
+                            const WT pt = pot[pl * a.dp + d1];
                             WT dw = WT(0);
                             if (sp) dw += pt;
                             if (e) dw -= depp;
@@ -683,6 +690,8 @@ __global__ void __launch_bounds__(kThreads) k_sparse_exact(SparseArgs a) {
 
 }  // namespace
 
+int sparse_pot_stage_bytes() { return 24 * 1024; }  // 4 CTAs/SM keep fitting
+
 int sparse_block_pres(int hbits) {
     // 32 KB of staged history per CTA (pre ids are 16-bit block-local)
     switch (hbits) {
@@ -697,6 +706,7 @@ template <typename WT, bool STDP, int HB>
 static void sparse_go_sub(const SparseArgs& a, int sub, int gx, size_t smem, cudaStream_t s) {
     dim3 grid(gx, a.nblocks);
     if (a.dict_size > 0) smem = ((smem + 15) & ~static_cast<size_t>(15)) + static_cast<size_t>(a.dict_size) * sizeof(WT);
+    if (STDP && a.pot_staged) smem += static_cast<size_t>(a.pb) * a.dp * sizeof(WT);
     if (a.dict_size == 2 && !STDP && sub != 0 && HB != 64) {  // one weight: count the delivering pres
         constexpr int HC = HB == 64 ? 32 : HB;  // (64 never reaches the launch)
         switch (sub) {

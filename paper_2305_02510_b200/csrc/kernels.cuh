@@ -140,6 +140,7 @@ struct SparseArgs {
     int32_t posts_per_cta;
     const void* wdict;         // WT[dict_size] weight dictionary (meta bits 23..31) or null
     int32_t dict_size;         // 0: weights stream from w[]
+    int32_t pot_staged;        // STDP: the block's pot^(d) traces are staged in shared memory
     double* partial;           // [nblocks][nl]
     const double* v;
     const double* leak;
@@ -188,6 +189,8 @@ void launch_prologue(double* u_exact, const double* v, const double* leak, const
                      int nl, bool abm, cudaStream_t s);
 void launch_step_bump(int32_t* d_step, cudaStream_t s);
 int sparse_block_pres(int hbits);
+// STDP pull sweeps stage the pre block's pot^(d) traces in shared memory up to this many bytes
+int sparse_pot_stage_bytes();
 // setup: reorder one-weight lists for conflict-light history reads in k_sparse_count
 void launch_sparse_bank_order(const uint32_t* in, uint32_t* out, const int64_t* off, int64_t lists, int nl,
                               int sub, int hbits, cudaStream_t s);
