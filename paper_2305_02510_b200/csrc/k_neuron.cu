@@ -2,14 +2,24 @@
 // history kernel of partitioned runs (k_hist), and two helpers.
 #include "kernels_common.cuh"
 
+#ifndef SNB_NEURON_MINB
+#define SNB_NEURON_MINB 4
+#endif
+
 namespace snb {
 
 namespace {
 
 template <bool EXACT, bool FUSED>
-__global__ void __launch_bounds__(kThreads) k_neuron(NeuronArgs a, HistArgs h) {
+__global__ void __launch_bounds__(kThreads, SNB_NEURON_MINB) k_neuron(NeuronArgs a, HistArgs h) {
     const int t = *a.d_step;
-    neuron_step<EXACT, FUSED>(a, h, blockIdx.x * kThreads + threadIdx.x, t);
+    const uint32_t f = neuron_step<EXACT, FUSED, false>(a, h, blockIdx.x * kThreads + threadIdx.x, t);
+    const int spikes = __syncthreads_count(f & 1u);
+    const int active = FUSED ? __syncthreads_count(f & 2u) : 0;
+    if (threadIdx.x == 0) {
+        if (spikes) atomicAdd(a.spike_count, static_cast<unsigned long long>(spikes));
+        if (active) atomicAdd(h.active_count, static_cast<unsigned long long>(active));
+    }
     if (a.peer_bits) {
         // publish step t to every rank once all CTAs' words are out: each CTA
         // fences its peer stores system-wide and counts itself; the last CTA
@@ -52,10 +62,9 @@ __global__ void __launch_bounds__(kThreads) k_hist(HistArgs h) {
         act = hist_update(h, i, s, t);
     }
     const uint32_t aw = __ballot_sync(0xffffffffu, act);
-    if ((threadIdx.x & 31) == 0 && (i >> 5) < ((h.n + 31) >> 5)) {
-        h.active[i >> 5] = aw;
-        if (aw) atomicAdd(h.active_count, static_cast<unsigned long long>(__popc(aw)));
-    }
+    if ((threadIdx.x & 31) == 0 && (i >> 5) < ((h.n + 31) >> 5)) h.active[i >> 5] = aw;
+    const int active = __syncthreads_count(act);
+    if (threadIdx.x == 0 && active) atomicAdd(h.active_count, static_cast<unsigned long long>(active));
 }
 
 __global__ void k_prologue(double* u, const double* v, const double* leak, const double* reset,

@@ -159,8 +159,12 @@ __device__ __forceinline__ bool hist_update(const HistArgs& h, int i, bool s, in
 // ---------------------------------------------------------------------------
 // K1: LIF update of the local posts for step t (mat_engine.cpp:168-198).
 // Called by full warps (j covers a multiple of 32); one neuron per thread.
-template <bool EXACT, bool FUSED>
-__device__ __forceinline__ void neuron_step(const NeuronArgs& a, const HistArgs& h, int j, int t) {
+// WARP_COUNT: lane 0 of each warp adds the warp's spike / active counts to the
+// global counters; otherwise the caller aggregates the returned per-thread
+// flags (bit 0 spiked, bit 1 active) per CTA - one same-address atomic per
+// warp serialises at L2 once a step has ~10^4 warps.
+template <bool EXACT, bool FUSED, bool WARP_COUNT = true>
+__device__ __forceinline__ uint32_t neuron_step(const NeuronArgs& a, const HistArgs& h, int j, int t) {
     const bool valid = j < a.nl;
     if (a.work && j == 0) *a.work = 0;  // the previous sweep has finished (stream / grid order)
     bool s = false;
@@ -243,17 +247,18 @@ __device__ __forceinline__ void neuron_step(const NeuronArgs& a, const HistArgs&
                 if (q != a.rank) a.peer_bits[q][(a.first >> 5) + wi] = word;
         if (a.raster && (t - a.t_base) < a.raster_rows)
             a.raster[static_cast<int64_t>(t - a.t_base) * a.nl_words + wi] = word;
-        if (word) atomicAdd(a.spike_count, static_cast<unsigned long long>(__popc(word)));
+        if (WARP_COUNT && word) atomicAdd(a.spike_count, static_cast<unsigned long long>(__popc(word)));
     }
+    bool act = false;
     if (FUSED) {
-        bool act = false;
         if (valid) act = hist_update(h, j, s, t);
         const uint32_t aw = __ballot_sync(0xffffffffu, act);
         if (lane == 0 && wi < a.nl_words) {
             h.active[wi] = aw;
-            if (aw) atomicAdd(h.active_count, static_cast<unsigned long long>(__popc(aw)));
+            if (WARP_COUNT && aw) atomicAdd(h.active_count, static_cast<unsigned long long>(__popc(aw)));
         }
     }
+    return (s ? 1u : 0u) | (act ? 2u : 0u);
 }
 
 __device__ __forceinline__ void st_release_sys(int32_t* p, int32_t v) {
