@@ -134,9 +134,13 @@ int32_t Engine::sparse_pres_per_block() const {
     if (stdp_on_ && !exact_) {
         const int esz = f64_ ? 8 : 4;
         // 100k-neuron ER(p=0.01) STDP sweep: staged 0.314 ms vs 0.413 gathered at dp = 1;
-        // at dp = 8 the 768-pre blocks lost (0.672 vs 0.591 ms), so only blocks of
-        // >= 2048 pres are staged
-        const int fit = sparse_pot_stage_bytes() / (std::max(dp_, 1) * esz) / 32 * 32;
+        // at dp = 8 the 768-pre blocks of a 24 KB stage lost (0.672 vs 0.591 ms) while
+        // 2048-pre blocks in 64 KB (3 CTAs/SM) won (0.532); blocks below 2048 pres
+        // are never staged (list overhead), and dp = 1 keeps 24 KB (4 CTAs/SM:
+        // 0.328 ms vs 0.347 at 48 KB, 0.408 at 64 KB)
+        int budget = sparse_pot_stage_bytes(dp_);
+        if (const char* kb = std::getenv("SNB_SPARSE_POT_KB")) budget = std::atoi(kb) * 1024;  // A/B knob
+        const int fit = budget / (std::max(dp_, 1) * esz) / 32 * 32;
         if (fit >= 2048) {
             pb = std::min(pb, fit);
             pot_staged_ = true;

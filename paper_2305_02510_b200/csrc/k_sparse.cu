@@ -170,9 +170,8 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(Spars
                         else e = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
                         WT w = wv[u][k];
                         if (!DICT && STDP && ((m >> 22) & 1u)) {
-                            const WT pt = pot[pl * a.dp + d1];
                             WT dw = WT(0);
-                            if (sp) dw += pt;
+                            if (sp) dw += pot[pl * a.dp + d1];  // only spiking posts read pot^(d)
                             if (e) dw -= depp;
                             const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
                             changed |= (nw != w);
@@ -673,12 +672,12 @@ __global__ void __launch_bounds__(kThreads) k_sparse_exact(SparseArgs a) {
                 const bool e = (a.hist[pre] >> d1) & 1ull;
                 WT w = W[q];
                 if (STDP && ((m >> 22) & 1u)) {
-                    const WT pt = pot[static_cast<int64_t>(pre) * a.dp + d1];
                     WT dw = WT(0);
-                    if (sp) dw += pt;
+                    if (sp) dw += pot[static_cast<int64_t>(pre) * a.dp + d1];
                     if (e) dw -= depp;
-                    w = clamp_ref<WT>(w + dw, wmin, wmax);
-                    W[q] = w;
+                    const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
+                    if (nw != w) W[q] = nw;
+                    w = nw;
                 }
                 if (e) acc += static_cast<double>(w);
             }
@@ -690,7 +689,7 @@ __global__ void __launch_bounds__(kThreads) k_sparse_exact(SparseArgs a) {
 
 }  // namespace
 
-int sparse_pot_stage_bytes() { return 24 * 1024; }  // 4 CTAs/SM keep fitting
+int sparse_pot_stage_bytes(int dp) { return (dp > 1 ? 64 : 24) * 1024; }
 
 int sparse_block_pres(int hbits) {
     // 32 KB of staged history per CTA (pre ids are 16-bit block-local)
@@ -707,36 +706,42 @@ static void sparse_go_sub(const SparseArgs& a, int sub, int gx, size_t smem, cud
     dim3 grid(gx, a.nblocks);
     if (a.dict_size > 0) smem = ((smem + 15) & ~static_cast<size_t>(15)) + static_cast<size_t>(a.dict_size) * sizeof(WT);
     if (STDP && a.pot_staged) smem += static_cast<size_t>(a.pb) * a.dp * sizeof(WT);
+    auto go = [&](auto kern) {
+        if (smem > 48 * 1024)
+            check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+                  "k_sparse smem attribute");
+        kern<<<grid, kThreads, smem, s>>>(a);
+    };
     if (a.dict_size == 2 && !STDP && sub != 0 && HB != 64) {  // one weight: count the delivering pres
         constexpr int HC = HB == 64 ? 32 : HB;  // (64 never reaches the launch)
         switch (sub) {
-            case 1: k_sparse_count<WT, HC, 1><<<grid, kThreads, smem, s>>>(a); break;
-            case 2: k_sparse_count<WT, HC, 2><<<grid, kThreads, smem, s>>>(a); break;
-            case 4: k_sparse_count<WT, HC, 4><<<grid, kThreads, smem, s>>>(a); break;
-            case 8: k_sparse_count<WT, HC, 8><<<grid, kThreads, smem, s>>>(a); break;
-            case 16: k_sparse_count<WT, HC, 16><<<grid, kThreads, smem, s>>>(a); break;
-            default: k_sparse_count<WT, HC, 32><<<grid, kThreads, smem, s>>>(a); break;
+            case 1: go(k_sparse_count<WT, HC, 1>); break;
+            case 2: go(k_sparse_count<WT, HC, 2>); break;
+            case 4: go(k_sparse_count<WT, HC, 4>); break;
+            case 8: go(k_sparse_count<WT, HC, 8>); break;
+            case 16: go(k_sparse_count<WT, HC, 16>); break;
+            default: go(k_sparse_count<WT, HC, 32>); break;
         }
         return;
     }
     if (a.dict_size > 0 && !STDP) {
         switch (sub) {
-            case 0: k_sparse_stream<WT, false, HB, true><<<grid, kThreads, smem, s>>>(a); break;
-            case 1: k_sparse_pull<WT, false, HB, 1, true><<<grid, kThreads, smem, s>>>(a); break;
-            case 2: k_sparse_pull<WT, false, HB, 2, true><<<grid, kThreads, smem, s>>>(a); break;
-            case 4: k_sparse_pull<WT, false, HB, 4, true><<<grid, kThreads, smem, s>>>(a); break;
-            case 8: k_sparse_pull<WT, false, HB, 8, true><<<grid, kThreads, smem, s>>>(a); break;
-            case 16: k_sparse_pull<WT, false, HB, 16, true><<<grid, kThreads, smem, s>>>(a); break;
-            default: k_sparse_pull<WT, false, HB, 32, true><<<grid, kThreads, smem, s>>>(a); break;
+            case 0: go(k_sparse_stream<WT, false, HB, true>); break;
+            case 1: go(k_sparse_pull<WT, false, HB, 1, true>); break;
+            case 2: go(k_sparse_pull<WT, false, HB, 2, true>); break;
+            case 4: go(k_sparse_pull<WT, false, HB, 4, true>); break;
+            case 8: go(k_sparse_pull<WT, false, HB, 8, true>); break;
+            case 16: go(k_sparse_pull<WT, false, HB, 16, true>); break;
+            default: go(k_sparse_pull<WT, false, HB, 32, true>); break;
         }
         return;
     }
     switch (sub) {
-        case 0: k_sparse_stream<WT, STDP, HB, false><<<grid, kThreads, smem, s>>>(a); break;
-        case 4: k_sparse_pull<WT, STDP, HB, 4, false><<<grid, kThreads, smem, s>>>(a); break;
-        case 8: k_sparse_pull<WT, STDP, HB, 8, false><<<grid, kThreads, smem, s>>>(a); break;
-        case 16: k_sparse_pull<WT, STDP, HB, 16, false><<<grid, kThreads, smem, s>>>(a); break;
-        default: k_sparse_pull<WT, STDP, HB, 32, false><<<grid, kThreads, smem, s>>>(a); break;
+        case 0: go(k_sparse_stream<WT, STDP, HB, false>); break;
+        case 4: go(k_sparse_pull<WT, STDP, HB, 4, false>); break;
+        case 8: go(k_sparse_pull<WT, STDP, HB, 8, false>); break;
+        case 16: go(k_sparse_pull<WT, STDP, HB, 16, false>); break;
+        default: go(k_sparse_pull<WT, STDP, HB, 32, false>); break;
     }
 }
 

@@ -190,7 +190,7 @@ void launch_prologue(double* u_exact, const double* v, const double* leak, const
 void launch_step_bump(int32_t* d_step, cudaStream_t s);
 int sparse_block_pres(int hbits);
 // STDP pull sweeps stage the pre block's pot^(d) traces in shared memory up to this many bytes
-int sparse_pot_stage_bytes();
+int sparse_pot_stage_bytes(int dp);
 // setup: reorder one-weight lists for conflict-light history reads in k_sparse_count
 void launch_sparse_bank_order(const uint32_t* in, uint32_t* out, const int64_t* off, int64_t lists, int nl,
                               int sub, int hbits, cudaStream_t s);
