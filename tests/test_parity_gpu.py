@@ -529,6 +529,60 @@ def test_sparse_multiple_pre_blocks(n, p, dmax, weights):
     assert st["sweep_kernel"] == expect
 
 
+@pytest.mark.parametrize("precision,dmax", [
+    ("f32", 1),   # 24 KB pot stage: 6144-pre blocks
+    ("f32", 8),   # 64 KB pot stage (opt-in smem attribute): 2048-pre blocks
+    ("f64", 4),   # 64 KB pot stage: 2048-pre blocks
+    ("f64", 8),   # stage would leave 1024-pre blocks: per-synapse global pot gather
+])
+def test_sparse_stdp_multiple_pre_blocks(precision, dmax):
+    """Sparse STDP (k_sparse_pull, streamed weights) over several pre blocks,
+    with the pre block's pot^(d) traces staged in shared memory or gathered,
+    against the oracle: rasters identical, fp64 weights exact, fp32 weights
+    within their rounding."""
+    from oracle import bridge as B
+    from paper_2305_02510_b200.engine import MatEngine
+    from paper_2305_02510_b200.model import StdpConfig
+    from paper_2305_02510_b200.netgen import RandomStream, erdos_renyi_arrays, scenario_stimulus
+    n, p, seed, steps = 10000, 0.003, 11, 30
+    pre, post = erdos_renyi_arrays(n, p, seed)
+    m = len(pre)
+    rs = RandomStream(seed, 78)
+    k = np.arange(m, dtype=np.uint64)
+    delay = (1 + rs.below_np(k, dmax)).astype(np.int32)
+    w = 0.25 + rs.unit_np(k + np.uint64(m))
+    plastic = (rs.unit_np(k + np.uint64(2 * m)) < 0.6).astype(np.uint8)
+    thr = np.full(n, 1.3)
+    arrays = {"threshold": thr, "leak": np.full(n, 0.5), "reset": np.zeros(n), "refractory": np.zeros(n, np.int32),
+              "axonal": np.zeros(n, np.int32), "pre": pre, "post": post, "weight": w, "delay": delay,
+              "stdp": plastic}
+    d = StdpConfig.defaults()
+    sd = (d.window, np.array(d.a_plus), np.array(d.a_minus), d.w_min, d.w_max)
+    stim = scenario_stimulus(n, steps, seed, count=300, period=2, amplitude=2.0).to_arrays()
+    o = B.run_oracle(arrays, steps, stim, sd)
+    assert len(o["steps"]) > 1000
+    eng = MatEngine(storage=2, precision=precision)
+    eng.add_neurons(thr, arrays["leak"], arrays["reset"], arrays["refractory"], arrays["axonal"])
+    eng.add_synapses(pre, post, w, delay, plastic)
+    eng.set_stdp(*sd)
+    eng.setup()
+    eng.add_stimulus(*stim)
+    eng.simulate(steps)
+    s, q = eng.raster()
+    mem = eng.membrane()
+    wt = eng.synapse_weights()
+    st = eng.stats()
+    eng.close()
+    assert st["sweep_kernel"] == 5  # k_sparse_pull
+    assert np.array_equal(s, o["steps"]) and np.array_equal(q, o["neurons"])
+    if precision == "f64":
+        assert close_rel(mem, o["membrane"])
+        assert np.array_equal(wt, o["weights"])
+    else:
+        assert np.allclose(mem, o["membrane"], rtol=1e-5, atol=1e-4)
+        assert np.allclose(wt, o["weights"], rtol=1e-5, atol=2e-5)
+
+
 def test_dense_tma_sweep_8192_all_plastic():
     """cfg3's plan at N = 8192 (many TMA work items, claimed dynamically):
     ER(8192, p=1) all plastic with StdpConfig::defaults, paper stimulus,
