@@ -483,11 +483,17 @@ void Engine::plan_launches() {
             if (bytes + (256u << 20) < free_b) {
                 DevBuf ordered;
                 ordered.alloc(bytes);
-                launch_sparse_bank_order(d_meta_.as<uint32_t>(), ordered.as<uint32_t>(), d_off_.as<int64_t>(),
-                                         static_cast<int64_t>(nblocks_) * nl_, nl_, sub_, hbits_, stream_);
+                const char* bj = std::getenv("SNB_SPARSE_BANK_JOINT");  // A/B knob: 0 = per-list order
+                const bool joint = !(bj && std::string(bj) == "0") &&
+                                   launch_sparse_bank_joint(d_meta_.as<uint32_t>(), ordered.as<uint32_t>(),
+                                                            d_off_.as<int64_t>(), nblocks_, nl_, sub_, hbits_, stream_);
+                if (!joint) {
+                    launch_sparse_bank_order(d_meta_.as<uint32_t>(), ordered.as<uint32_t>(), d_off_.as<int64_t>(),
+                                             static_cast<int64_t>(nblocks_) * nl_, nl_, sub_, hbits_, stream_);
+                    std::swap(d_meta_.p, ordered.p);
+                    std::swap(d_meta_.bytes, ordered.bytes);
+                }
                 cuda_check(cudaStreamSynchronize(stream_), "bank order");
-                std::swap(d_meta_.p, ordered.p);
-                std::swap(d_meta_.bytes, ordered.bytes);
                 bank_ordered_ = true;
             }
         }

@@ -351,6 +351,75 @@ __global__ void k_sparse_bank_order(const uint32_t* in, uint32_t* out, const int
 }
 
 
+// Joint bank schedule of the 32/SUB lists one warp of k_sparse_count reads
+// together (posts P*k .. P*k+P-1 of one pre block; SUB = 4, 8, 16).  The lists
+// are scheduled LDS by LDS: for slot g (row g/4, word g%4) every active lane of
+// every post (posts in rotating order) takes an entry of its own list from the
+// bank with the lowest load in this LDS so far, ties broken by the bank's
+// remaining entries over the whole group (drain the heavy banks early).  The
+// per-list bank-sorted deal above leaves the 32/SUB posts of a warp colliding
+// with each other (cfg4: 2.59 wavefronts per LDS, measured and simulated);
+// the joint schedule simulates to 1.60 against a lower bound of ~1.5 set by
+// the group's bank histogram.  In place: meta -> tmp (bucketed) -> meta.
+template <int SUB>
+__global__ void k_sparse_bank_joint(uint32_t* meta, uint32_t* tmp, const int64_t* off, int nblocks, int nl,
+                                    int hbits) {
+    constexpr int P = 32 / SUB, ROW = 4 * SUB;
+    const int groups = (nl + P - 1) / P;
+    const int64_t G = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (G >= static_cast<int64_t>(groups) * nblocks) return;
+    const int b = static_cast<int>(G / groups), k = static_cast<int>(G % groups);
+    const int np = min(P, nl - P * k);
+    const int64_t* o = off + static_cast<int64_t>(b) * nl + P * k;
+    int cnt[P][32], cur[P][32], tot[32], len[P], rows[P], last[P];
+    for (int j = 0; j < 32; ++j) tot[j] = 0;
+    int gmax = 0;
+    for (int i = 0; i < P; ++i) {
+        for (int j = 0; j < 32; ++j) cnt[i][j] = 0;
+        len[i] = i < np ? static_cast<int>(o[i + 1] - o[i]) : 0;
+        rows[i] = (len[i] + ROW - 1) / ROW;
+        last[i] = len[i] > 0 ? (len[i] - ROW * (rows[i] - 1)) / 4 : 0;  // lanes with a full last row
+        gmax = max(gmax, 4 * rows[i]);
+        if (i >= np) continue;
+        for (int64_t q = o[i]; q < o[i + 1]; ++q) cnt[i][sp_bank(meta[q], hbits)] += 1;
+        int acc = 0;
+        for (int j = 0; j < 32; ++j) {
+            cur[i][j] = acc;
+            acc += cnt[i][j];
+            tot[j] += cnt[i][j];
+        }
+        for (int64_t q = o[i]; q < o[i + 1]; ++q) {  // bucket by bank into tmp
+            const uint32_t m = meta[q];
+            tmp[o[i] + cur[i][sp_bank(m, hbits)]++] = m;
+        }
+        for (int j = 0; j < 32; ++j) cur[i][j] -= cnt[i][j];  // back to the bucket starts
+    }
+    for (int g = 0; g < gmax; ++g) {
+        int load[32];
+        for (int j = 0; j < 32; ++j) load[j] = 0;
+        for (int r = 0; r < P; ++r) {
+            const int i = (g + r) % P;
+            if (i >= np) continue;
+            const int slots_full = 4 * rows[i], slots_part = 4 * (rows[i] - 1);
+            for (int sl = 0; sl < SUB; ++sl) {
+                if (g >= (sl < last[i] ? slots_full : slots_part)) continue;
+                int best = -1;
+                for (int j = 0; j < 32; ++j) {
+                    if (cnt[i][j] == 0) continue;
+                    if (best < 0 || load[j] < load[best] || (load[j] == load[best] &&
+                        (tot[j] > tot[best] || (tot[j] == tot[best] && cnt[i][j] > cnt[i][best]))))
+                        best = j;
+                }
+                const uint32_t m = tmp[o[i] + cur[i][best]++];
+                cnt[i][best] -= 1;
+                tot[best] -= 1;
+                load[best] += 1;
+                meta[o[i] + (g >> 2) * ROW + 4 * sl + (g & 3)] = m;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Sparse TMA stream (static nets whose lists carry one weight w: the ER
 // generator's networks, cfg4).  The blocked-CSC meta array is one contiguous
@@ -786,6 +855,23 @@ void launch_sparse(const SparseArgs& a, bool f64, bool stdp, int hbits, int sub,
         }
     }
     check(cudaGetLastError(), "k_sparse");
+}
+
+bool launch_sparse_bank_joint(uint32_t* meta, uint32_t* tmp, const int64_t* off, int nblocks, int nl, int sub,
+                              int hbits, cudaStream_t s) {
+    if (sub != 4 && sub != 8 && sub != 16) return false;
+    const int P = 32 / sub;
+    const int64_t groups = static_cast<int64_t>(nblocks) * ((nl + P - 1) / P);
+    if (groups <= 0) return true;
+    const unsigned grid = static_cast<unsigned>((groups + 63) / 64);
+    switch (sub) {
+        case 4: k_sparse_bank_joint<4><<<grid, 64, 0, s>>>(meta, tmp, off, nblocks, nl, hbits); break;
+        case 8: k_sparse_bank_joint<8><<<grid, 64, 0, s>>>(meta, tmp, off, nblocks, nl, hbits); break;
+        case 16: k_sparse_bank_joint<16><<<grid, 64, 0, s>>>(meta, tmp, off, nblocks, nl, hbits); break;
+        default: return false;
+    }
+    check(cudaGetLastError(), "k_sparse_bank_joint");
+    return true;
 }
 
 void launch_sparse_bank_order(const uint32_t* in, uint32_t* out, const int64_t* off, int64_t lists, int nl,

@@ -192,6 +192,10 @@ int sparse_block_pres(int hbits);
 // STDP pull sweeps stage the pre block's pot^(d) traces in shared memory up to this many bytes
 int sparse_pot_stage_bytes(int dp);
 // setup: reorder one-weight lists for conflict-light history reads in k_sparse_count
+// Joint per-warp bank schedule of one-weight lists, in place (tmp: scratch of
+// the same size); false when SUB has no joint form (the per-list order applies).
+bool launch_sparse_bank_joint(uint32_t* meta, uint32_t* tmp, const int64_t* off, int nblocks, int nl, int sub,
+                              int hbits, cudaStream_t s);
 void launch_sparse_bank_order(const uint32_t* in, uint32_t* out, const int64_t* off, int64_t lists, int nl,
                               int sub, int hbits, cudaStream_t s);
 // TMA-fed stream for static uniform-weight lists (dictionary {w, 0}), no exact order
