@@ -109,12 +109,21 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def mark(self):
+        """Start of the timed region: only samples from here on count (the
+        sampler itself is started before the warm-up, so NVML's start-up and
+        an idle gap do not fall on the first timed launch)."""
+        self.mark_at = len(self.samples)
+
     def stop(self):
         if self.nvml is not None:
             self.stop_flag.set()
             self.thread.join(timeout=2)
-            sm = [s for s, _ in self.samples]
-            reasons = sorted({r for _, rs in self.samples for r in rs})
+            m = getattr(self, "mark_at", 0)
+            # a region shorter than the 2 ms poll keeps the sample taken just before it
+            samples = self.samples[m:] or self.samples[max(0, m - 1):m]
+            sm = [s for s, _ in samples]
+            reasons = sorted({r for _, rs in samples for r in rs})
             return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.smax,
                     "reasons": reasons, "samples": len(sm), "source": "nvml"}
         if self.proc is None:
@@ -198,13 +207,14 @@ def run_ours(args):
     eng.setup()
     connect(sn, eng, rank, world, args.transport)
     stim = add_protocol_stimulus(sn, eng, n, horizon)
+    clocks = ClockSampler(device)
+    clocks.start()
     eng.simulate(W)                       # warm-up
     eng.synchronize()
     eng.reset_stats()
     if torch_dist:
         torch_dist.barrier()
-    clocks = ClockSampler(device)
-    clocks.start()
+    clocks.mark()
     t0 = time.perf_counter()
     eng.simulate(K)                       # timed: device events inside the engine
     eng.synchronize()
