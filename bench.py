@@ -271,8 +271,8 @@ def run_ours(args):
         eng2.setup()
         connect(sn, eng2, rank, world, args.transport)
         add_protocol_stimulus(sn, eng2, n, horizon)
-        eng2.simulate(W)
-        eng2.synchronize()
+        eng2.simulate(W)                  # warm-up, including one raster fetch
+        eng2.raster()
         eng2.clear_raster()
         if torch_dist:
             torch_dist.barrier()
