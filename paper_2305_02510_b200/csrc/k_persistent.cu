@@ -48,6 +48,17 @@ __host__ __device__ inline TinyLayout tiny_layout(const TinyArgs& a) {
 
 // Bit test of one incoming synapse: meta = byte offset of the 32-bit history
 // word within a buffer << 5 | bit; the funnel shift uses the low 5 bits.
+#ifndef SNB_TINY_HREGS
+#define SNB_TINY_HREGS 4
+#endif
+// own history words kept in registers (hw <= 2): cfg1 1.15e6 -> 1.24e6 steps/s.
+// Caching the first 4 / 8 incoming entries (meta + weight) in registers as
+// well lost (1.15e6 / 0.69e6: the 64-register cap of a 1024-thread CTA
+// spills), and so did batching the list walk 4 entries at a time (metas,
+// weights, history words issued together): 0.91e6 with branches, 0.97e6
+// with selects (every fp64 add executed)
+constexpr int kTinyHistRegs = SNB_TINY_HREGS;
+
 __device__ __forceinline__ bool tiny_bit(const uint8_t* buf, uint32_t mq) {
     const uint32_t word = *reinterpret_cast<const uint32_t*>(buf + (mq >> 5));
     return __funnelshift_r(word, word, mq) & 1u;
@@ -115,6 +126,11 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
     const int words = (n + 31) / 32;
     const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
     const uint32_t q0 = own ? off[j] : 0u, q1 = own ? off[j + 1] : 0u;
+    // own history words in registers (<= kTinyHistRegs 32-bit words)
+    const bool hreg = kTinyHistRegs > 0 && hw2 <= kTinyHistRegs;
+    uint32_t hr[kTinyHistRegs > 0 ? kTinyHistRegs : 1];
+#pragma unroll
+    for (int k = 0; k < kTinyHistRegs; ++k) hr[k] = (hreg && k < hw2 && j < np) ? hist[k * np + j] : 0u;
     unsigned long long spikes = 0;
     for (int s = 0; s < a.steps; ++s) {
         const int cur = s & 1;
@@ -165,12 +181,24 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
         }
         // (2) own history row into the other buffer (+ own STDP traces)
         if (j < np) {
-            const uint32_t* hcw = reinterpret_cast<const uint32_t*>(hc);
             uint32_t carry = fired ? 1u : 0u;
-            for (int k = 0; k < hw2; ++k) {
-                const uint32_t x = hcw[k * np + j];
-                hn[k * np + j] = (x << 1) | carry;
-                carry = x >> 31;
+            if (hreg) {
+#pragma unroll
+                for (int k = 0; k < kTinyHistRegs; ++k) {
+                    if (k < hw2) {
+                        const uint32_t x = hr[k];
+                        hr[k] = (x << 1) | carry;
+                        hn[k * np + j] = hr[k];
+                        carry = x >> 31;
+                    }
+                }
+            } else {
+                const uint32_t* hcw = reinterpret_cast<const uint32_t*>(hc);
+                for (int k = 0; k < hw2; ++k) {
+                    const uint32_t x = hcw[k * np + j];
+                    hn[k * np + j] = (x << 1) | carry;
+                    carry = x >> 31;
+                }
             }
             if (STDP && own) {
                 double* potn = pot + (cur ^ 1) * np * a.dp;
