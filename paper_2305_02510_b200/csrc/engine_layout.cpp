@@ -427,7 +427,11 @@ void Engine::plan_launches() {
             if (tma_ && !dense_tma_fits(tile_w_, f64_, has_delay_, stdp_on_)) tma_ = false;
             if (tma_) {
                 const char* tw = std::getenv("SNB_TMA_WAVES");
-                const double tw_waves = tw ? std::atof(tw) : 14.0;
+                // items per SM per step: with the planner warp building the next
+                // item's list in the background, finer items only shorten the
+                // step's tail (cfg3 sweep: 14 -> 1.288 ms, 30 -> 1.271, 60 -> 1.270
+                // but more partials for the neuron phase; fp64 32k 2.606 -> 2.538)
+                const double tw_waves = tw ? std::atof(tw) : 30.0;
                 int tn = std::max(1, static_cast<int>(std::lround(tw_waves * sms / ntiles)));
                 int trpc = static_cast<int>(round_up(std::max(32, (n_ + tn - 1) / tn), 32));
                 trpc = std::min(trpc, dense_tma_max_rows());

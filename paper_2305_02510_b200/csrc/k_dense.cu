@@ -198,10 +198,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_dense_stream(DenseArgs a) {
 // registers, so the in-flight window per SM is the whole ring.
 constexpr int kTmaRows = 4;        // rows per stage
 constexpr int kTmaStages = 8;      // ring depth
-constexpr int kTmaListMax = 2048;  // rows per item (one list build per item)
-constexpr int kTmaThreads = 288;   // 8 consumer warps + 1 producer warp
+constexpr int kTmaListMax = 1024;  // rows per item (one list per item, double-buffered)
+constexpr int kTmaThreads = 320;   // 8 consumer warps + 1 producer warp + 1 planner warp
 constexpr int kTmaDp = 4;          // delayed STDP: pot^(d) traces staged per listed row
+constexpr int kTmaRec = kTmaListMax + kTmaRows;
 
+// Roles: warp 9 (planner) claims the next item and builds its active-row list
+// into the other of two list buffers while warp 8 (producer) streams the
+// current item's rows and warps 0-7 (consumers) process them, so an item's
+// list build (two dependent global round trips + a scan) no longer stalls the
+// ring between items.  Buffers hand over on mbarriers: ready[b] (planner ->
+// producer + consumers), freeb[b] (producer + 8 consumer warps -> planner) and
+// issued (producer -> planner: claim the next item now).
 template <typename WT, bool STDP, bool DELAY>
 __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
     using VT = VecT<WT>;
@@ -210,7 +218,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const bool producer = warp == 8;
     const int ntiles = (a.nl + a.tile_w - 1) / a.tile_w;
     const int items = ntiles * a.nchunks;
     const uint32_t row_bytes = static_cast<uint32_t>(a.tile_w) * static_cast<uint32_t>(sizeof(WT));
@@ -219,13 +226,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
     uint8_t* ring = smem;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * stage_bytes);
     uint64_t* empty = full + kTmaStages;
-    RowRec<WT>* s_rec = reinterpret_cast<RowRec<WT>*>(empty + kTmaStages);
+    uint64_t* ready = empty + kTmaStages;
+    uint64_t* freeb = ready + 2;
+    uint64_t* issued = freeb + 2;  // producer -> planner: the current item's last stage is issued
+    RowRec<WT>* s_recs = reinterpret_cast<RowRec<WT>*>(issued + 2);
     // delayed STDP: pot^(d) of each listed row for d = 1..kTmaDp (a.dp <= kTmaDp)
-    WT* s_potd = reinterpret_cast<WT*>(s_rec + kTmaListMax + kTmaRows);
-    __shared__ uint32_t s_word[32];
-    __shared__ int32_t s_wpref[33];
-    __shared__ int32_t s_cnt;
-    __shared__ int s_item;
+    WT* s_potds = reinterpret_cast<WT*>(s_recs + 2 * kTmaRec);
+    __shared__ int s_item[2];
+    __shared__ int s_cnt[2];
 
     const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
     const WT* dep = static_cast<const WT*>(a.dep);
@@ -237,82 +245,121 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, 8);
         }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(ready + b, 1);
+            mbar_init(freeb + b, 9);
+        }
+        mbar_init(issued, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    uint32_t it = 0;  // ring position, advanced identically by producer and consumers
-    int item = blockIdx.x;
-    if (a.work) {
-        if (tid == 0) s_item = atomicAdd(a.work, 1);
-        __syncthreads();
-        item = s_item;
-    }
-    while (item < items) {
-        const int chunk = item / ntiles;
-        const int tile = item - chunk * ntiles;
-        const int col0 = tile * a.tile_w;
-        const int width = static_cast<int>(min(static_cast<int64_t>(a.tile_w), a.pitch - col0));
-        const uint32_t copy_bytes = static_cast<uint32_t>(width) * static_cast<uint32_t>(sizeof(WT));
-        const int r0 = chunk * a.rows_per_chunk;
-        const int r1 = min(a.n, r0 + a.rows_per_chunk);
-
-        // active-row list of [r0, r1) in <= 1024-row pieces (32-aligned bases)
-        if (tid == 0) s_cnt = 0;
-        __syncthreads();
-        for (int sa = r0, sb_next = r0; sa < r1; sa = sb_next) {
-            const int base = sa & ~31;
-            const int sb = min(r1, base + kSubRows);
-            sb_next = sb;
-            const int nwords = (sb - base + 31) >> 5;
-            const int cnt0 = s_cnt;
-            if (tid < 32) {
-                uint32_t wd = 0;
-                if (tid < nwords) {
-                    wd = __ldcg(a.active + (base >> 5) + tid);
-                    const int lo = sa - (base + tid * 32);
-                    if (lo > 0) wd &= (lo >= 32) ? 0u : ~((1u << lo) - 1u);
-                    const int rem = sb - (base + tid * 32);
-                    if (rem < 32) wd &= (rem <= 0) ? 0u : ((1u << rem) - 1u);
-                }
-                const int c = __popc(wd);
-                int incl = c;
+    if (warp == 9) {
+        // ---- planner ----
+        for (int ki = 0;; ++ki) {
+            const int b = ki & 1;
+            // claim the next item only once the current one is fully issued: a
+            // claim made earlier would hold work back from CTAs that finish
+            // first (the step's tail); the list build then overlaps the ring's
+            // last kTmaStages stages
+            if (ki >= 1) mbar_wait(issued, static_cast<uint32_t>((ki - 1) & 1));
+            if (ki >= 2) mbar_wait(freeb + b, static_cast<uint32_t>(((ki >> 1) - 1) & 1));
+            int item = blockIdx.x + ki * static_cast<int>(gridDim.x);
+            if (a.work) {
+                int got = 0;
+                if (lane == 0) got = atomicAdd(a.work, 1);
+                item = __shfl_sync(0xffffffffu, got, 0);
+            }
+            RowRec<WT>* rec = s_recs + b * kTmaRec;
+            WT* potd = s_potds + b * kTmaRec * kTmaDp;
+            int cnt = 0;
+            if (item < items) {
+                const int chunk = item / ntiles;
+                const int r0 = chunk * a.rows_per_chunk;
+                const int r1 = min(a.n, r0 + a.rows_per_chunk);
+                // (1) row ids of the active rows of [r0, r1), ascending, one word per lane
+                for (int wb = r0 & ~31; wb < r1; wb += 32 * 32) {
+                    const int wr = wb + lane * 32;
+                    uint32_t wd = 0;
+                    if (wr < r1) {
+                        wd = __ldcg(a.active + (wr >> 5));
+                        const int lo = r0 - wr;
+                        if (lo > 0) wd &= (lo >= 32) ? 0u : ~((1u << lo) - 1u);
+                        const int rem = r1 - wr;
+                        if (rem < 32) wd &= (rem <= 0) ? 0u : ((1u << rem) - 1u);
+                    }
+                    const int c = __popc(wd);
+                    int incl = c;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int x = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (tid >= o) incl += x;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int x = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += x;
+                    }
+                    int pos = cnt + incl - c;
+                    for (uint32_t m = wd; m; m &= m - 1) rec[pos++].rowk = wr + __ffs(static_cast<int>(m)) - 1;
+                    cnt += __shfl_sync(0xffffffffu, incl, 31);
                 }
-                s_word[tid] = wd;
-                s_wpref[tid] = cnt0 + incl - c;
-                if (tid == 31) s_wpref[32] = cnt0 + incl;
-            }
-            __syncthreads();
-            for (int r = sa + tid; r < sb; r += kTmaThreads) {
-                const int l = (r - base) >> 5, b = (r - base) & 31;
-                const uint32_t wd = s_word[l];
-                if ((wd >> b) & 1u) {
-                    const int pos = s_wpref[l] + __popc(wd & ((1u << b) - 1u));
-                    const uint64_t h = __ldcg(a.hist + r);
-                    RowRec<WT> rec;
-                    const int kind = STDP ? static_cast<int>(__ldg(a.kind + r)) : 0;
-                    rec.rowk = r | (kind << 28);
-                    rec.e_lo = static_cast<uint32_t>(h);
-                    rec.e_hi = static_cast<uint32_t>(h >> 32);
-                    rec.pot = (STDP && !DELAY) ? __ldcg(pot + r) : WT(0);
-                    s_rec[pos] = rec;
-                    if (STDP && DELAY)
-                        for (int d = 0; d < kTmaDp; ++d)
-                            s_potd[pos * kTmaDp + d] = d < a.dp ? __ldcg(pot + static_cast<int64_t>(r) * a.dp + d) : WT(0);
+                __syncwarp();
+                // (2) the rows' history words, kinds and traces, 4 rows per lane in flight
+                for (int p0 = 0; p0 < cnt; p0 += 4 * 32) {
+                    uint64_t h[4];
+                    int kd[4];
+                    WT pt[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int p = p0 + u * 32 + lane;
+                        h[u] = 0;
+                        kd[u] = 0;
+                        pt[u] = WT(0);
+                        if (p < cnt) {
+                            const int r = rec[p].rowk;
+                            h[u] = __ldcg(a.hist + r);
+                            kd[u] = STDP ? static_cast<int>(__ldg(a.kind + r)) : 0;
+                            pt[u] = (STDP && !DELAY) ? __ldcg(pot + r) : WT(0);
+                            if (STDP && DELAY)
+                                for (int d = 0; d < kTmaDp; ++d)
+                                    potd[p * kTmaDp + d] =
+                                        d < a.dp ? __ldcg(pot + static_cast<int64_t>(r) * a.dp + d) : WT(0);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int p = p0 + u * 32 + lane;
+                        if (p < cnt) {
+                            RowRec<WT> x;
+                            x.rowk = rec[p].rowk | (kd[u] << 28);
+                            x.e_lo = static_cast<uint32_t>(h[u]);
+                            x.e_hi = static_cast<uint32_t>(h[u] >> 32);
+                            x.pot = pt[u];
+                            rec[p] = x;
+                        }
+                    }
                 }
             }
-            __syncthreads();
-            if (tid == 0) s_cnt = s_wpref[32];
-            __syncthreads();
+            __syncwarp();
+            if (lane == 0) {
+                s_item[b] = item < items ? item : -1;
+                s_cnt[b] = cnt;
+                mbar_arrive(ready + b);  // release: the list and its count
+            }
+            if (item >= items) break;
         }
-        const int cnt = s_cnt;
-        const int ngroups = (cnt + kTmaRows - 1) / kTmaRows;
-
-        if (producer) {
+    } else if (warp == 8) {
+        // ---- producer ----
+        uint32_t it = 0;  // ring position, advanced identically by producer and consumers
+        for (int ki = 0;; ++ki) {
+            const int b = ki & 1;
+            mbar_wait(ready + b, static_cast<uint32_t>((ki >> 1) & 1));
+            const int item = s_item[b];
+            if (item < 0) break;
+            const int cnt = s_cnt[b];
+            const RowRec<WT>* rec = s_recs + b * kTmaRec;
+            const int chunk = item / ntiles;
+            const int tile = item - chunk * ntiles;
+            const int col0 = tile * a.tile_w;
+            const int width = static_cast<int>(min(static_cast<int64_t>(a.tile_w), a.pitch - col0));
+            const uint32_t copy_bytes = static_cast<uint32_t>(width) * static_cast<uint32_t>(sizeof(WT));
+            const int ngroups = (cnt + kTmaRows - 1) / kTmaRows;
             if (lane == 0) {
                 for (int g = 0; g < ngroups; ++g, ++it) {
                     const int s = it % kTmaStages;
@@ -322,7 +369,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                     mbar_arrive_expect_tx(full + s, static_cast<uint32_t>(nr) * (copy_bytes + (DELAY ? width : 0)));
                     uint8_t* st = ring + s * stage_bytes;
                     for (int r = 0; r < nr; ++r) {
-                        const int row = s_rec[g * kTmaRows + r].rowk & 0x0fffffff;
+                        const int row = rec[g * kTmaRows + r].rowk & 0x0fffffff;
                         bulk_g2s(st + static_cast<size_t>(r) * row_bytes, W + static_cast<int64_t>(row) * a.pitch + col0,
                                  copy_bytes, full + s);
                         if (DELAY)
@@ -331,10 +378,28 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                                      full + s);
                     }
                 }
+                mbar_arrive(issued);
+                mbar_arrive(freeb + b);
             } else {
                 it += ngroups;
             }
-        } else {
+        }
+    } else {
+        // ---- consumers ----
+        uint32_t it = 0;
+        for (int ki = 0;; ++ki) {
+            const int b = ki & 1;
+            mbar_wait(ready + b, static_cast<uint32_t>((ki >> 1) & 1));
+            const int item = s_item[b];
+            if (item < 0) break;
+            const int cnt = s_cnt[b];
+            const RowRec<WT>* s_rec = s_recs + b * kTmaRec;
+            const WT* s_potd = s_potds + b * kTmaRec * kTmaDp;
+            const int chunk = item / ntiles;
+            const int tile = item - chunk * ntiles;
+            const int col0 = tile * a.tile_w;
+            const int width = static_cast<int>(min(static_cast<int64_t>(a.tile_w), a.pitch - col0));
+            const int ngroups = (cnt + kTmaRows - 1) / kTmaRows;
             const int tcol = tid * VEC;
             const int c0 = col0 + tcol;
             const bool in_tile = tcol < width && c0 < a.nl;
@@ -421,14 +486,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                 for (int k = 0; k < VEC; ++k)
                     if (c0 + k < a.nl) a.partial[static_cast<int64_t>(chunk) * a.nl + c0 + k] = acc[k];
             }
-        }
-        __syncthreads();  // ring drained for this item's rows; list may be rebuilt
-        if (a.work) {
-            if (tid == 0) s_item = atomicAdd(a.work, 1);
-            __syncthreads();
-            item = s_item;
-        } else {
-            item += gridDim.x;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(freeb + b);
         }
     }
     if (blockIdx.x == 0 && tid == 0) *a.d_step += 1;
@@ -437,8 +496,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
 size_t dense_tma_smem(int tile_w, bool f64, bool delay, bool stdp) {
     const size_t esz = f64 ? 8 : 4;
     const size_t rec = f64 ? sizeof(RowRec<double>) : sizeof(RowRec<float>);
-    return static_cast<size_t>(kTmaStages) * kTmaRows * tile_w * (esz + (delay ? 1 : 0)) + 2 * kTmaStages * 8 +
-           static_cast<size_t>(kTmaListMax + kTmaRows) * (rec + ((delay && stdp) ? kTmaDp * esz : 0));
+    return static_cast<size_t>(kTmaStages) * kTmaRows * tile_w * (esz + (delay ? 1 : 0)) + (2 * kTmaStages + 6) * 8 +
+           2 * static_cast<size_t>(kTmaRec) * (rec + ((delay && stdp) ? kTmaDp * esz : 0));
 }
 
 }  // namespace
