@@ -151,8 +151,10 @@ typedef enum sn_sweep_kernel {
                                    lists (opt-in, SNB_SPARSE_KERNEL=tma) */
     SN_SWEEP_SPARSE_COUNT = 11, /* k_sparse_count: k_sparse_pull specialised for one-weight
                                    static lists (counts the delivering pres) */
-    SN_SWEEP_PERSISTENT_COLS = 12 /* k_persistent_cols: whole step loop in one launch, CTAs own
+    SN_SWEEP_PERSISTENT_COLS = 12, /* k_persistent_cols: whole step loop in one launch, CTAs own
                                      32-post column groups, one grid barrier per step */
+    SN_SWEEP_SPARSE_COUNT16 = 13  /* k_sparse_count16: one-weight lists as 16-bit entries in
+                                     4095-pre segments (2 B/synapse), delays <= 16 */
 } sn_sweep_kernel;
 
 /* ---- lifecycle ---------------------------------------------------------- */

@@ -183,9 +183,13 @@ private:
     DevBuf d_wdict_;
     void upload_dict();
     int32_t sparse_pres_per_block() const;
+    static bool c16_allowed();
     mutable bool pot_staged_ = false;  // STDP pull sweep stages the block's pot traces in smem
     bool sparse_tma_ = false;  // k_sparse_tma stage plan (static uniform-weight lists)
     bool bank_ordered_ = false;  // one-weight lists dealt bank-aware for k_sparse_count
+    bool c16_ = false;           // 16-bit segmented one-weight lists (k_sparse_count16)
+    DevBuf d_c16desc_, d_c16ent_;
+    bool build_c16();
     DevBuf d_sp_stages_, d_sp_first_, d_sp_block_, d_sp_bnd_;
     int32_t sp_ctas_ = 0;
     bool build_sparse_tma_plan(int ctas);

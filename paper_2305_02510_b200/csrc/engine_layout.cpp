@@ -131,6 +131,9 @@ void Engine::build_dense_from_lists() {
 int32_t Engine::sparse_pres_per_block() const {
     int pb = sparse_block_pres(hbits_);
     pot_staged_ = false;
+    // static nets with delays <= 16: 4 x 4095-pre blocks, the layout k_sparse_count16's
+    // 16-bit entries need (the other sparse kernels take any block size)
+    if (hbits_ == 16 && !stdp_on_ && !exact_ && c16_allowed()) pb = c16_block_pres();
     if (stdp_on_ && !exact_) {
         const int esz = f64_ ? 8 : 4;
         // 100k-neuron ER(p=0.01) STDP sweep: staged 0.314 ms vs 0.413 gathered at dp = 1;
@@ -454,6 +457,10 @@ void Engine::plan_launches() {
         // lines (4 posts per warp-wide LDG.128); cfg4, 160 entries per list:
         // SUB 8 0.514 ms vs SUB 4 0.529 ms, 16 0.678
         if (dict_.size() == 2 && !stdp_on_) sub_ = avg >= 1024 ? 16 : avg >= 96 ? 8 : 4;
+        // 16-bit segmented lists (k_sparse_count16): 4 lanes per post, 6 chunk loads each
+        // (cfg4, ~180 entries per list: SUB 4 0.452 ms, 8 0.486, 2 0.568)
+        if (dict_.size() == 2 && !stdp_on_ && !exact_ && hbits_ == 16 && pb_ == c16_block_pres() && c16_allowed())
+            sub_ = avg >= 768 ? 8 : 4;
         if (const char* sv = std::getenv("SNB_SPARSE_SUB")) {  // A/B knob: lanes per post
             const int v = std::atoi(sv);
             if (v == 4 || v == 8 || v == 16 || v == 32 || (!dict_.empty() && (v == 1 || v == 2))) sub_ = v;
@@ -480,7 +487,9 @@ void Engine::plan_launches() {
         const bool count_path = !exact_ && !stdp_on_ && dict_.size() == 2 && hbits_ != 64 && sub_ != 0 &&
                                 !sparse_tma_ && nl_ > 0 && sparse_elems_ > 0;
         const char* bo = std::getenv("SNB_SPARSE_BANK_ORDER");  // A/B knob: 0 keeps pre order
-        if (count_path && !(bo && std::string(bo) == "0")) {
+        if (count_path && build_c16()) {
+            bank_ordered_ = true;  // lists regrouped; every synapse carries dict_[0]
+        } else if (count_path && !(bo && std::string(bo) == "0")) {
             size_t free_b = 0, total_b = 0;
             cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
             const size_t bytes = static_cast<size_t>(sparse_elems_) * 4;
@@ -502,6 +511,62 @@ void Engine::plan_launches() {
             }
         }
     }
+}
+
+bool Engine::c16_allowed() {
+    const char* e = std::getenv("SNB_SPARSE_COUNT16");  // A/B knob: 0 keeps the 32-bit lists
+    return !(e && std::string(e) == "0");
+}
+
+// 16-bit segmented copy of the one-weight lists for k_sparse_count16 (layout
+// in k_sparse.cu): per-segment counts on the device, chunk offsets and the
+// list descriptors here, then the bank-scheduled fill.  False (the 32-bit count
+// path stays) when the block layout does not match or a list needs more than
+// 255 chunks of 8 entries.
+bool Engine::build_c16() {
+    if (!c16_allowed() || pb_ != c16_block_pres() || hbits_ != 16 || (sub_ != 2 && sub_ != 4 && sub_ != 8 && sub_ != 16))
+        return false;
+    const int64_t lists = static_cast<int64_t>(nblocks_) * nl_;
+    DevBuf d_cnt;
+    d_cnt.alloc(static_cast<size_t>(lists) * 8);
+    launch_c16_count(d_meta_.as<uint32_t>(), d_off_.as<int64_t>(), lists, pb_, d_cnt.as<uint2>(), stream_);
+    std::vector<uint32_t> cnt(static_cast<size_t>(lists) * 2);
+    cuda_check(cudaMemcpyAsync(cnt.data(), d_cnt.p, cnt.size() * 4, cudaMemcpyDeviceToHost, stream_), "c16 counts D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "c16 counts");
+    std::vector<uint32_t> desc(static_cast<size_t>(lists) * 2);
+    uint64_t chunks = 0;
+    for (int64_t L = 0; L < lists; ++L) {
+        const uint32_t x = cnt[2 * L], y = cnt[2 * L + 1];
+        const uint32_t n[4] = {x & 0xffffu, x >> 16, y & 0xffffu, y >> 16};
+        uint32_t e[4], acc = 0;
+        for (int s = 0; s < 4; ++s) {
+            acc += (n[s] + 7) / 8;
+            e[s] = acc;
+        }
+        if (acc > 255) return false;
+        desc[2 * L] = static_cast<uint32_t>(chunks);
+        desc[2 * L + 1] = e[0] | (e[1] << 8) | (e[2] << 16) | (e[3] << 24);
+        chunks += acc;
+    }
+    if (chunks >= (1ull << 32)) return false;
+    size_t free_b = 0, total_b = 0;
+    cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    const size_t need = static_cast<size_t>(chunks) * 16 + static_cast<size_t>(sparse_elems_) * 4 + (256u << 20);
+    if (need > free_b) return false;
+    upload(d_c16desc_, desc);
+    d_c16ent_.alloc(std::max<size_t>(static_cast<size_t>(chunks), 1) * 16);
+    DevBuf tmp;
+    tmp.alloc(std::max<size_t>(static_cast<size_t>(sparse_elems_), 1) * 4);
+    if (!launch_c16_fill(d_meta_.as<uint32_t>(), tmp.as<uint32_t>(), d_off_.as<int64_t>(), d_c16desc_.as<uint2>(),
+                         nblocks_, nl_, pb_, sub_, d_c16ent_.as<uint16_t>(), stream_)) {
+        d_c16desc_.release();
+        d_c16ent_.release();
+        return false;
+    }
+    cuda_check(cudaStreamSynchronize(stream_), "c16 fill");
+    c16_ = true;
+    sweep_bytes_full_ = static_cast<double>(syn_local_) * 2.0;  // 2 B per synapse entry
+    return true;
 }
 
 // Stage plan of k_sparse_tma: the (block, post) lists are cut into stages of

@@ -421,6 +421,261 @@ __global__ void k_sparse_bank_joint(uint32_t* meta, uint32_t* tmp, const int64_t
 }
 
 // ---------------------------------------------------------------------------
+// 16-bit one-weight lists (k_sparse_count16).  A pre block of kC16Pres = 4 x
+// 4095 pres is cut into 4 segments; each (block, post) list is regrouped by
+// segment, every segment padded to whole 16-byte chunks of 8 entries.  The
+// staged history image (uint16 per pre) puts segment s at slots [4096 s,
+// 4096 s + 4095) with slot 4096 s + 4095 zero.  An entry addresses the 32-bit
+// PAIR of slots holding its pre and the bit inside that pair:
+//   entry = (low >> 1) << 5 | (low & 1) << 4 | (d - 1),   low < 4096, d <= 16
+// so the test is one wrap-mode funnel shift by the entry itself (the shift
+// unit keeps its low 5 bits) -- no masking of the delay field -- and the
+// padding entry 0xfff0 reads the zero slot 4095.  A list descriptor {first
+// chunk, E1 | E2 << 8 | E3 << 16 | C << 24} carries the cumulative chunk
+// counts of the segments (C <= 255 chunks); a chunk's segment is (c >= E1) +
+// (c >= E2) + (c >= E3).  Half the bytes of the 32-bit meta words the other
+// count kernel streams; same counts.
+constexpr int kC16SegPres = 4095;
+constexpr int kC16Pres = 4 * kC16SegPres;
+
+__device__ __forceinline__ void c16_stage(const SparseArgs& a, int pre0, int pcount, uint16_t* sh) {
+    for (int k = threadIdx.x; k < 4 * 4096; k += blockDim.x) {
+        const int s = k >> 12, low = k & 4095;
+        const int pre = s * kC16SegPres + low;
+        sh[k] = (low < kC16SegPres && pre < pcount) ? static_cast<uint16_t>(__ldcg(a.hist_lo + pre0 + pre)) : 0;
+    }
+}
+
+#ifndef SNB_C16_MINB
+#define SNB_C16_MINB 4
+#endif
+// chunk loads per lane per batch; cfg4 (tools/ab_c16.sh): SUB 8: UL 2 0.527 ms, 3 0.499,
+// 4 0.486, 5 0.504; SUB 4: UL 5 0.474, 6 0.452, 7 0.458, 8 0.474; SUB 2: UL 6 0.568
+#ifdef SNB_C16_UL
+#define SNB_C16_UL_OF(SUB) SNB_C16_UL
+#else
+#define SNB_C16_UL_OF(SUB) ((SUB) <= 4 ? 6 : 4)
+#endif
+#ifndef SNB_C16_PIPE
+#define SNB_C16_PIPE 0
+#endif
+
+// Count the delivering entries of one loaded batch (UL chunks of lane sl).
+template <int SUB, int UL>
+__device__ __forceinline__ int c16_count_batch(const uint4 (&m4)[UL], int c0, int C, int E1, int E2, int E3,
+                                               const uint16_t* shist) {
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < UL; ++u) {
+        const int c = c0 + u * SUB;
+        if (c < C) {
+            const uint16_t* sh = shist + (((c >= E1) + (c >= E2) + (c >= E3)) << 12);
+            const uint32_t* sw = reinterpret_cast<const uint32_t*>(sh);
+            const uint32_t ws[4] = {m4[u].x, m4[u].y, m4[u].z, m4[u].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t x = ws[k];
+                const uint32_t h0 = sw[(x >> 5) & 0x7ffu];
+                const uint32_t h1 = sw[x >> 21];
+                cnt += static_cast<int>(__funnelshift_r(h0, h0, x) & 1u);
+                cnt += static_cast<int>(__funnelshift_r(h1, h1, x >> 16) & 1u);
+            }
+        }
+    }
+    return cnt;
+}
+
+template <int SUB, int UL>
+__device__ __forceinline__ void c16_load_batch(uint4 (&m4)[UL], const uint4* src, int c0, int C) {
+#pragma unroll
+    for (int u = 0; u < UL; ++u)
+        if (c0 + u * SUB < C) m4[u] = __ldcs(src + c0 + u * SUB);
+}
+
+template <typename WT, int SUB>
+__global__ void __launch_bounds__(kThreads, SNB_C16_MINB) k_sparse_count16(SparseArgs a, const uint2* desc,
+                                                                            const uint4* ent) {
+    __shared__ __align__(16) uint16_t shist[4 * 4096];
+    const int b = blockIdx.y;
+    const int pre0 = b * kC16Pres;
+    const int pcount = min(kC16Pres, a.n - pre0);
+    const int tid = threadIdx.x;
+    c16_stage(a, pre0, pcount, shist);
+    __syncthreads();
+    const WT w0 = static_cast<const WT*>(a.wdict)[0];
+    const int p0 = blockIdx.x * a.posts_per_cta;
+    const int p1 = min(a.nl, p0 + a.posts_per_cta);
+    constexpr int PER_WARP = 32 / SUB;
+    constexpr int UL = SNB_C16_UL_OF(SUB);
+    constexpr int STEP = SUB * UL;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int sg = lane / SUB, sl = lane % SUB;
+    const int stride = (kThreads / 32) * PER_WARP;
+    const uint2* db = desc + static_cast<int64_t>(b) * a.nl;
+    int p = p0 + warp * PER_WARP + sg;
+    uint2 d = make_uint2(0u, 0u);
+    if (p < p1) d = __ldg(db + p);
+#if SNB_C16_PIPE
+    // software pipeline across posts: the next post's first batch is in flight
+    // while the current one is counted
+    uint4 mc[UL];
+    c16_load_batch<SUB, UL>(mc, ent + d.x, sl, static_cast<int>(d.y >> 24));
+    uint2 dn = make_uint2(0u, 0u);
+    if (p + stride < p1) dn = __ldg(db + p + stride);
+#endif
+    for (int pbase = p0 + warp * PER_WARP; pbase < p1; pbase += stride) {  // warp-uniform trip count
+        const bool valid = p < p1;
+        const int pn = p + stride;
+#if SNB_C16_PIPE
+        uint4 mn[UL];
+        c16_load_batch<SUB, UL>(mn, ent + dn.x, sl, static_cast<int>(dn.y >> 24));
+        uint2 dnn = make_uint2(0u, 0u);
+        if (pn + stride < p1) dnn = __ldg(db + pn + stride);
+#else
+        uint2 dn = make_uint2(0u, 0u);
+        if (pn < p1) dn = __ldg(db + pn);
+#endif
+        int cnt = 0;
+        if (valid) {
+            const int C = static_cast<int>(d.y >> 24);
+            const int E1 = static_cast<int>(d.y & 255u), E2 = static_cast<int>((d.y >> 8) & 255u),
+                      E3 = static_cast<int>((d.y >> 16) & 255u);
+            const uint4* src = ent + d.x;
+#if SNB_C16_PIPE
+            cnt = c16_count_batch<SUB, UL>(mc, sl, C, E1, E2, E3, shist);
+            for (int c0 = sl + STEP; c0 < C; c0 += STEP) {
+#else
+            for (int c0 = sl; c0 < C; c0 += STEP) {
+#endif
+                uint4 m4[UL];
+                c16_load_batch<SUB, UL>(m4, src, c0, C);
+                cnt += c16_count_batch<SUB, UL>(m4, c0, C, E1, E2, E3, shist);
+            }
+        }
+#pragma unroll
+        for (int o = SUB / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (valid && sl == 0)
+            a.partial[static_cast<int64_t>(b) * a.nl + p] = static_cast<double>(static_cast<WT>(cnt) * w0);
+        p = pn;
+        d = dn;
+#if SNB_C16_PIPE
+        dn = dnn;
+#pragma unroll
+        for (int u = 0; u < UL; ++u) mc[u] = mn[u];
+#endif
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *a.d_step += 1;
+}
+
+// Setup: entries per segment of every 32-bit one-weight list (padding, pre slot
+// pb, skipped) -> cnt[list] = n0 | n1 << 16 (x) and n2 | n3 << 16 (y).
+__global__ void k_c16_count(const uint32_t* meta, const int64_t* off, int64_t lists, int pb, uint2* cnt) {
+    const int64_t L = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (L >= lists) return;
+    uint32_t n[4] = {0, 0, 0, 0};
+    for (int64_t q = off[L]; q < off[L + 1]; ++q) {
+        const uint32_t pl = meta[q] & 0xffffu;
+        if (static_cast<int>(pl) == pb) continue;
+        n[pl / kC16SegPres] += 1;
+    }
+    cnt[L] = make_uint2(n[0] | (n[1] << 16), n[2] | (n[3] << 16));
+}
+
+// Setup: the joint per-warp bank schedule of k_sparse_bank_joint, per segment:
+// the P = 32/SUB lists one warp reads together are filled LDS by LDS (slot g =
+// chunk row g/8, entry g%8); a lane takes, from its chunk's segment, an entry
+// in the bank with the lowest load in this LDS so far (ties: most entries left
+// in the group, then in the list), padding 0xfff0 once the segment is empty.
+template <int SUB>
+__global__ void k_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* off, const uint2* desc, int nblocks,
+                           int nl, int pb, uint16_t* out) {
+    constexpr int P = 32 / SUB;
+    const int groups = (nl + P - 1) / P;
+    const int64_t G = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (G >= static_cast<int64_t>(groups) * nblocks) return;
+    const int b = static_cast<int>(G / groups), k = static_cast<int>(G % groups);
+    const int np = min(P, nl - P * k);
+    const int64_t L0 = static_cast<int64_t>(b) * nl + P * k;
+    uint16_t cnt[P][4][32], cur[P][4][32];
+    int tot[32], C[P], E[P][3];
+    for (int j = 0; j < 32; ++j) tot[j] = 0;
+    int gmax = 0;
+    for (int i = 0; i < P; ++i) {
+        for (int s = 0; s < 4; ++s)
+            for (int j = 0; j < 32; ++j) cnt[i][s][j] = 0;
+        C[i] = 0;
+        E[i][0] = E[i][1] = E[i][2] = 0;
+        if (i >= np) continue;
+        const uint2 d = desc[L0 + i];
+        C[i] = static_cast<int>(d.y >> 24);
+        E[i][0] = static_cast<int>(d.y & 255u);
+        E[i][1] = static_cast<int>((d.y >> 8) & 255u);
+        E[i][2] = static_cast<int>((d.y >> 16) & 255u);
+        gmax = max(gmax, 8 * ((C[i] + SUB - 1) / SUB));
+        const int64_t o0 = off[L0 + i], o1 = off[L0 + i + 1];
+        for (int64_t q = o0; q < o1; ++q) {
+            const int pl = static_cast<int>(meta[q] & 0xffffu);
+            if (pl == pb) continue;
+            const int s = pl / kC16SegPres;
+            cnt[i][s][((pl - s * kC16SegPres) >> 1) & 31] += 1;
+        }
+        int acc = 0;
+        for (int s = 0; s < 4; ++s)
+            for (int j = 0; j < 32; ++j) {
+                cur[i][s][j] = static_cast<uint16_t>(acc);
+                acc += cnt[i][s][j];
+                tot[j] += cnt[i][s][j];
+            }
+        for (int64_t q = o0; q < o1; ++q) {  // bucket by (segment, bank) into tmp
+            const uint32_t m = meta[q];
+            const int pl = static_cast<int>(m & 0xffffu);
+            if (pl == pb) continue;
+            const int s = pl / kC16SegPres;
+            const int low = pl - s * kC16SegPres;
+            tmp[o0 + cur[i][s][(low >> 1) & 31]++] =
+                static_cast<uint32_t>((low >> 1) << 5 | (low & 1) << 4) | ((m >> 16) & 15u);
+        }
+        for (int s = 0; s < 4; ++s)
+            for (int j = 0; j < 32; ++j) cur[i][s][j] = static_cast<uint16_t>(cur[i][s][j] - cnt[i][s][j]);
+    }
+    for (int g = 0; g < gmax; ++g) {
+        int load[32];
+        for (int j = 0; j < 32; ++j) load[j] = 0;
+        const int row = g >> 3, e = g & 7;
+        for (int r = 0; r < P; ++r) {
+            const int i = (g + r) % P;
+            if (i >= np) continue;
+            const int64_t base = static_cast<int64_t>(desc[L0 + i].x) * 8;
+            const int64_t o0 = off[L0 + i];
+            for (int sl = 0; sl < SUB; ++sl) {
+                const int c = row * SUB + sl;
+                if (c >= C[i]) continue;
+                const int s = (c >= E[i][0]) + (c >= E[i][1]) + (c >= E[i][2]);
+                int best = -1;
+                for (int j = 0; j < 32; ++j) {
+                    if (cnt[i][s][j] == 0) continue;
+                    if (best < 0 || load[j] < load[best] ||
+                        (load[j] == load[best] && (tot[j] > tot[best] ||
+                                                   (tot[j] == tot[best] && cnt[i][s][j] > cnt[i][s][best]))))
+                        best = j;
+                }
+                uint16_t v = 0xfff0u;  // padding: the segment's zero slot 4095
+                if (best >= 0) {
+                    v = static_cast<uint16_t>(tmp[o0 + cur[i][s][best]]);
+                    cur[i][s][best] += 1;
+                    cnt[i][s][best] -= 1;
+                    tot[best] -= 1;
+                    load[best] += 1;
+                } else {
+                    load[31] += 1;
+                }
+                out[base + static_cast<int64_t>(c) * 8 + e] = v;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Sparse TMA stream (static nets whose lists carry one weight w: the ER
 // generator's networks, cfg4).  The blocked-CSC meta array is one contiguous
 // stream in (block, post) order.  The host cuts it into stages of whole posts
@@ -880,6 +1135,61 @@ void launch_sparse_bank_order(const uint32_t* in, uint32_t* out, const int64_t* 
     k_sparse_bank_order<<<static_cast<unsigned>((lists + 127) / 128), 128, 0, s>>>(in, out, off, lists, nl, sub,
                                                                                   hbits);
     check(cudaGetLastError(), "k_sparse_bank_order");
+}
+
+int c16_block_pres() { return kC16Pres; }
+
+void launch_c16_count(const uint32_t* meta, const int64_t* off, int64_t lists, int pb, uint2* cnt, cudaStream_t s) {
+    if (lists <= 0) return;
+    k_c16_count<<<static_cast<unsigned>((lists + 255) / 256), 256, 0, s>>>(meta, off, lists, pb, cnt);
+    check(cudaGetLastError(), "k_c16_count");
+}
+
+bool launch_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* off, const uint2* desc, int nblocks, int nl,
+                     int pb, int sub, uint16_t* out, cudaStream_t s) {
+    const int P = 32 / sub;
+    const int64_t groups = static_cast<int64_t>(nblocks) * ((nl + P - 1) / P);
+    if (groups <= 0) return true;
+    const unsigned grid = static_cast<unsigned>((groups + 63) / 64);
+    switch (sub) {
+        case 2: k_c16_fill<2><<<grid, 64, 0, s>>>(meta, tmp, off, desc, nblocks, nl, pb, out); break;
+        case 4: k_c16_fill<4><<<grid, 64, 0, s>>>(meta, tmp, off, desc, nblocks, nl, pb, out); break;
+        case 8: k_c16_fill<8><<<grid, 64, 0, s>>>(meta, tmp, off, desc, nblocks, nl, pb, out); break;
+        case 16: k_c16_fill<16><<<grid, 64, 0, s>>>(meta, tmp, off, desc, nblocks, nl, pb, out); break;
+        default: return false;
+    }
+    check(cudaGetLastError(), "k_c16_fill");
+    return true;
+}
+
+void launch_sparse_count16(const SparseArgs& a, const uint2* desc, const void* ent, bool f64, int sub, int gx,
+                           cudaStream_t s) {
+    dim3 grid(gx, a.nblocks);
+    const uint4* e = static_cast<const uint4*>(ent);
+    static bool carveout = false;  // 33 KB of history per CTA: let the occupancy limit be registers
+    if (!carveout) {
+        for (auto k : {k_sparse_count16<float, 2>, k_sparse_count16<float, 4>, k_sparse_count16<float, 8>, k_sparse_count16<float, 16>})
+            check(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
+        for (auto k : {k_sparse_count16<double, 2>, k_sparse_count16<double, 4>, k_sparse_count16<double, 8>, k_sparse_count16<double, 16>})
+            check(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
+        carveout = true;
+    }
+    if (f64) {
+        switch (sub) {
+            case 2: k_sparse_count16<double, 2><<<grid, kThreads, 0, s>>>(a, desc, e); break;
+            case 4: k_sparse_count16<double, 4><<<grid, kThreads, 0, s>>>(a, desc, e); break;
+            case 16: k_sparse_count16<double, 16><<<grid, kThreads, 0, s>>>(a, desc, e); break;
+            default: k_sparse_count16<double, 8><<<grid, kThreads, 0, s>>>(a, desc, e); break;
+        }
+    } else {
+        switch (sub) {
+            case 2: k_sparse_count16<float, 2><<<grid, kThreads, 0, s>>>(a, desc, e); break;
+            case 4: k_sparse_count16<float, 4><<<grid, kThreads, 0, s>>>(a, desc, e); break;
+            case 16: k_sparse_count16<float, 16><<<grid, kThreads, 0, s>>>(a, desc, e); break;
+            default: k_sparse_count16<float, 8><<<grid, kThreads, 0, s>>>(a, desc, e); break;
+        }
+    }
+    check(cudaGetLastError(), "k_sparse_count16");
 }
 
 size_t sparse_tma_smem(const SparseArgs& a, int hbits) {

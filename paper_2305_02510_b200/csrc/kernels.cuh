@@ -198,6 +198,14 @@ bool launch_sparse_bank_joint(uint32_t* meta, uint32_t* tmp, const int64_t* off,
                               int hbits, cudaStream_t s);
 void launch_sparse_bank_order(const uint32_t* in, uint32_t* out, const int64_t* off, int64_t lists, int nl,
                               int sub, int hbits, cudaStream_t s);
+// 16-bit one-weight lists (k_sparse_count16): pres per block (4 segments of
+// 4095), setup kernels (per-segment counts; joint bank-scheduled fill) and the sweep
+int c16_block_pres();
+void launch_c16_count(const uint32_t* meta, const int64_t* off, int64_t lists, int pb, uint2* cnt, cudaStream_t s);
+bool launch_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* off, const uint2* desc, int nblocks, int nl,
+                     int pb, int sub, uint16_t* out, cudaStream_t s);
+void launch_sparse_count16(const SparseArgs& a, const uint2* desc, const void* ent, bool f64, int sub, int gx,
+                           cudaStream_t s);
 // TMA-fed stream for static uniform-weight lists (dictionary {w, 0}), no exact order
 size_t sparse_tma_smem(const SparseArgs& a, int hbits);
 int sparse_tma_stage_entries();

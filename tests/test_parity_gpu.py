@@ -483,6 +483,8 @@ def test_sparse_tma_stream_opt_in(monkeypatch):
     (20000, 0.002, 20, "one"),      # 32-bit histories: 8192 pres per block -> 3 blocks
     (20000, 0.002, 40, "one"),      # 64-bit histories: 4096 pres per block -> 5 blocks
     (40000, 0.0005, 1, "one"),      # spike bits: 32768 pres per block -> 2 blocks
+    (40000, 0.002, 16, "one"),      # 16-bit segmented lists: 4 x 4095 pres per block -> 3 blocks
+    (6000, 0.5, 16, "one"),         # ~3000-entry lists overflow the 255-chunk descriptor: 32-bit count
     (20000, 0.002, 12, "three"),    # dictionary of 3 weights (k_sparse_pull<dict>)
     (20000, 0.002, 12, "float"),    # weights streamed per synapse (k_sparse_pull)
 ])
@@ -525,8 +527,52 @@ def test_sparse_multiple_pre_blocks(n, p, dmax, weights):
     eng.close()
     assert np.array_equal(s, o["steps"]) and np.array_equal(q, o["neurons"])
     assert close_rel(mem, o["membrane"])
-    expect = {"one": 11 if dmax <= 32 else 6, "three": 6, "float": 5}[weights]
+    c16 = 1 < dmax <= 16 and p < 0.1
+    expect = {"one": 13 if c16 else 11 if dmax <= 32 else 6, "three": 6, "float": 5}[weights]
     assert st["sweep_kernel"] == expect
+
+
+@pytest.mark.parametrize("storage", [2, 1])
+def test_count16_matches_count32(monkeypatch, storage):
+    """k_sparse_count16 (16-bit segmented lists, the cfg4 default) against the
+    32-bit count kernel (SNB_SPARSE_COUNT16=0) and the oracle on a 1% ER net with
+    delays 1..16 over 3 pre blocks: host-built lists (storage 2) and on-device
+    generation; rasters and membranes identical."""
+    from oracle import bridge as B
+    from paper_2305_02510_b200.engine import MatEngine
+    from paper_2305_02510_b200.netgen import DELAY_STREAM, RandomStream, erdos_renyi_arrays, scenario_stimulus
+    n, p, seed, steps, dmax = 36000, 0.01, 11, 30, 16
+    stim = scenario_stimulus(n, steps, seed, count=300, period=2, amplitude=4.0).to_arrays()
+    pre, post = erdos_renyi_arrays(n, p, seed)
+    keys = pre.astype(np.uint64) * np.uint64(n) + post.astype(np.uint64)
+    delay = (1 + RandomStream(seed, DELAY_STREAM).below_np(keys, dmax)).astype(np.int32)
+    arrays = {"threshold": np.full(n, 3.0), "leak": np.full(n, 0.5), "reset": np.zeros(n),
+              "refractory": np.full(n, 1, np.int32), "axonal": np.zeros(n, np.int32), "pre": pre, "post": post,
+              "weight": np.ones(len(pre)), "delay": delay, "stdp": np.zeros(len(pre), np.uint8)}
+    o = B.run_oracle(arrays, steps, stim) if storage == 2 else None
+    runs = {}
+    for c16 in ("1", "0"):
+        monkeypatch.setenv("SNB_SPARSE_COUNT16", c16)
+        eng = MatEngine(storage=2, precision="f64")
+        if storage == 2:
+            eng.add_neurons(arrays["threshold"], arrays["leak"], arrays["reset"], arrays["refractory"],
+                            arrays["axonal"])
+            eng.add_synapses(pre, post, arrays["weight"], delay, None)
+        else:
+            eng.generate_erdos_renyi(n, p, seed, delay_max=dmax)
+        eng.setup()
+        eng.add_stimulus(*stim)
+        eng.simulate(steps)
+        s, q = eng.raster()
+        runs[c16] = (s, q, eng.membrane(), eng.stats()["sweep_kernel"])
+        eng.close()
+    assert runs["1"][3] == 13 and runs["0"][3] == 11
+    assert len(runs["1"][0]) > 5000
+    assert np.array_equal(runs["1"][0], runs["0"][0]) and np.array_equal(runs["1"][1], runs["0"][1])
+    assert np.array_equal(runs["1"][2], runs["0"][2])
+    if o is not None:
+        assert np.array_equal(runs["1"][0], o["steps"]) and np.array_equal(runs["1"][1], o["neurons"])
+        assert close_rel(runs["1"][2], o["membrane"])
 
 
 @pytest.mark.parametrize("precision,dmax", [
