@@ -565,7 +565,9 @@ bool Engine::build_c16() {
     }
     cuda_check(cudaStreamSynchronize(stream_), "c16 fill");
     c16_ = true;
-    sweep_bytes_full_ = static_cast<double>(syn_local_) * 2.0;  // 2 B per synapse entry
+    // bytes the sweep moves in this format: 2 B per stored entry (padding included),
+    // the 8-byte descriptor and the 8-byte partial of every (block, post) list
+    sweep_bytes_full_ = static_cast<double>(chunks) * 16.0 + static_cast<double>(lists) * 16.0;
     return true;
 }
 

@@ -426,11 +426,15 @@ __global__ void k_sparse_bank_joint(uint32_t* meta, uint32_t* tmp, const int64_t
 // segment, every segment padded to whole 16-byte chunks of 8 entries.  The
 // staged history image (uint16 per pre) puts segment s at slots [4096 s,
 // 4096 s + 4095) with slot 4096 s + 4095 zero.  An entry addresses the 32-bit
-// PAIR of slots holding its pre and the bit inside that pair:
-//   entry = (low >> 1) << 5 | (low & 1) << 4 | (d - 1),   low < 4096, d <= 16
+// PAIR of slots holding its pre and a rotation that brings the pre's bit d-1
+// (bit j = 16 (low & 1) + d - 1 of the pair) to bit 31:
+//   entry = (low >> 1) << 5 | (j + 1) & 31,   low < 4096, d <= 16
 // so the test is one wrap-mode funnel shift by the entry itself (the shift
-// unit keeps its low 5 bits) -- no masking of the delay field -- and the
-// padding entry 0xfff0 reads the zero slot 4095.  A list descriptor {first
+// unit keeps its low 5 bits; no masking of the delay field) and one shift by
+// 31 (the ALU pipe is the limit: 77% busy; moving the address arithmetic and
+// the accumulation onto the FMA pipe as IMAD.HI with run-time multipliers
+// measured 0.420 / 0.452 ms against 0.421).  The padding entry 0xfff1 reads
+// the zero slot 4095.  A list descriptor {first
 // chunk, E1 | E2 << 8 | E3 << 16 | C << 24} carries the cumulative chunk
 // counts of the segments (C <= 255 chunks); a chunk's segment is (c >= E1) +
 // (c >= E2) + (c >= E3).  Half the bytes of the 32-bit meta words the other
@@ -461,24 +465,29 @@ __device__ __forceinline__ void c16_stage(const SparseArgs& a, int pre0, int pco
 #endif
 
 // Count the delivering entries of one loaded batch (UL chunks of lane sl).
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
 template <int SUB, int UL>
-__device__ __forceinline__ int c16_count_batch(const uint4 (&m4)[UL], int c0, int C, int E1, int E2, int E3,
-                                               const uint16_t* shist) {
-    int cnt = 0;
+__device__ __forceinline__ uint32_t c16_count_batch(const uint4 (&m4)[UL], int c0, int C, int E1, int E2, int E3,
+                                                    const uint16_t* shist) {
+    uint32_t cnt = 0;
 #pragma unroll
     for (int u = 0; u < UL; ++u) {
         const int c = c0 + u * SUB;
         if (c < C) {
             const uint16_t* sh = shist + (((c >= E1) + (c >= E2) + (c >= E3)) << 12);
-            const uint32_t* sw = reinterpret_cast<const uint32_t*>(sh);
+            const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sh));
             const uint32_t ws[4] = {m4[u].x, m4[u].y, m4[u].z, m4[u].w};
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const uint32_t x = ws[k];
-                const uint32_t h0 = sw[(x >> 5) & 0x7ffu];
-                const uint32_t h1 = sw[x >> 21];
-                cnt += static_cast<int>(__funnelshift_r(h0, h0, x) & 1u);
-                cnt += static_cast<int>(__funnelshift_r(h1, h1, x >> 16) & 1u);
+                const uint32_t h0 = lds_u32(base + ((x >> 3) & 0x1ffcu));   // pair (x >> 5) & 0x7ff
+                const uint32_t h1 = lds_u32(base + ((x >> 19) & 0x1ffcu));  // pair x >> 21
+                cnt += (__funnelshift_r(h0, h0, x) >> 31) + (__funnelshift_r(h1, h1, x >> 16) >> 31);
             }
         }
     }
@@ -542,14 +551,14 @@ __global__ void __launch_bounds__(kThreads, SNB_C16_MINB) k_sparse_count16(Spars
                       E3 = static_cast<int>((d.y >> 16) & 255u);
             const uint4* src = ent + d.x;
 #if SNB_C16_PIPE
-            cnt = c16_count_batch<SUB, UL>(mc, sl, C, E1, E2, E3, shist);
+            cnt = static_cast<int>(c16_count_batch<SUB, UL>(mc, sl, C, E1, E2, E3, shist));
             for (int c0 = sl + STEP; c0 < C; c0 += STEP) {
 #else
             for (int c0 = sl; c0 < C; c0 += STEP) {
 #endif
                 uint4 m4[UL];
                 c16_load_batch<SUB, UL>(m4, src, c0, C);
-                cnt += c16_count_batch<SUB, UL>(m4, c0, C, E1, E2, E3, shist);
+                cnt += static_cast<int>(c16_count_batch<SUB, UL>(m4, c0, C, E1, E2, E3, shist));
             }
         }
 #pragma unroll
@@ -585,7 +594,7 @@ __global__ void k_c16_count(const uint32_t* meta, const int64_t* off, int64_t li
 // the P = 32/SUB lists one warp reads together are filled LDS by LDS (slot g =
 // chunk row g/8, entry g%8); a lane takes, from its chunk's segment, an entry
 // in the bank with the lowest load in this LDS so far (ties: most entries left
-// in the group, then in the list), padding 0xfff0 once the segment is empty.
+// in the group, then in the list), padding 0xfff1 once the segment is empty.
 template <int SUB>
 __global__ void k_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* off, const uint2* desc, int nblocks,
                            int nl, int pb, uint16_t* out) {
@@ -632,8 +641,8 @@ __global__ void k_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* o
             if (pl == pb) continue;
             const int s = pl / kC16SegPres;
             const int low = pl - s * kC16SegPres;
-            tmp[o0 + cur[i][s][(low >> 1) & 31]++] =
-                static_cast<uint32_t>((low >> 1) << 5 | (low & 1) << 4) | ((m >> 16) & 15u);
+            const uint32_t j = static_cast<uint32_t>(low & 1) * 16u + ((m >> 16) & 15u);  // bit of the pair
+            tmp[o0 + cur[i][s][(low >> 1) & 31]++] = static_cast<uint32_t>(low >> 1) << 5 | ((j + 1u) & 31u);
         }
         for (int s = 0; s < 4; ++s)
             for (int j = 0; j < 32; ++j) cur[i][s][j] = static_cast<uint16_t>(cur[i][s][j] - cnt[i][s][j]);
@@ -659,7 +668,7 @@ __global__ void k_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* o
                                                    (tot[j] == tot[best] && cnt[i][s][j] > cnt[i][s][best]))))
                         best = j;
                 }
-                uint16_t v = 0xfff0u;  // padding: the segment's zero slot 4095
+                uint16_t v = 0xfff1u;  // padding: the segment's zero slot 4095 (pair 2047, bit 16)
                 if (best >= 0) {
                     v = static_cast<uint16_t>(tmp[o0 + cur[i][s][best]]);
                     cur[i][s][best] += 1;
