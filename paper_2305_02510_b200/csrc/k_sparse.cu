@@ -425,16 +425,16 @@ __global__ void k_sparse_bank_joint(uint32_t* meta, uint32_t* tmp, const int64_t
 // 4095 pres is cut into 4 segments; each (block, post) list is regrouped by
 // segment, every segment padded to whole 16-byte chunks of 8 entries.  The
 // staged history image (uint16 per pre) puts segment s at slots [4096 s,
-// 4096 s + 4095) with slot 4096 s + 4095 zero.  An entry addresses the 32-bit
+// 4096 s + 4096) with one zero slot (c16_zero_slot).  An entry addresses the 32-bit
 // PAIR of slots holding its pre and a rotation that brings the pre's bit d-1
-// (bit j = 16 (low & 1) + d - 1 of the pair) to bit 31:
-//   entry = (low >> 1) << 5 | (j + 1) & 31,   low < 4096, d <= 16
+// (bit j of the pair) to bit 31:
+//   entry = (slot >> 1) << 5 | (j + 1) & 31,   j = 16 (slot & 1) + d - 1, d <= 16
 // so the test is one wrap-mode funnel shift by the entry itself (the shift
 // unit keeps its low 5 bits; no masking of the delay field) and one shift by
 // 31 (the ALU pipe is the limit: 77% busy; moving the address arithmetic and
 // the accumulation onto the FMA pipe as IMAD.HI with run-time multipliers
-// measured 0.420 / 0.452 ms against 0.421).  The padding entry 0xfff1 reads
-// the zero slot 4095.  A list descriptor {first
+// measured 0.420 / 0.452 ms against 0.421).  Padding entries read the segment's
+// zero slot.  A list descriptor {first
 // chunk, E1 | E2 << 8 | E3 << 16 | C << 24} carries the cumulative chunk
 // counts of the segments (C <= 255 chunks); a chunk's segment is (c >= E1) +
 // (c >= E2) + (c >= E3).  Half the bytes of the 32-bit meta words the other
@@ -442,11 +442,16 @@ __global__ void k_sparse_bank_joint(uint32_t* meta, uint32_t* tmp, const int64_t
 constexpr int kC16SegPres = 4095;
 constexpr int kC16Pres = 4 * kC16SegPres;
 
+// Zero slot of segment s: 4095 - 16 s, so the padding of the 4 segments reads
+// 4 different banks (31, 23, 15, 7); pre offset j of the segment sits in slot
+// j + (j >= zero slot).
+__host__ __device__ constexpr int c16_zero_slot(int s) { return 4095 - 16 * s; }
+
 __device__ __forceinline__ void c16_stage(const SparseArgs& a, int pre0, int pcount, uint16_t* sh) {
     for (int k = threadIdx.x; k < 4 * 4096; k += blockDim.x) {
-        const int s = k >> 12, low = k & 4095;
-        const int pre = s * kC16SegPres + low;
-        sh[k] = (low < kC16SegPres && pre < pcount) ? static_cast<uint16_t>(__ldcg(a.hist_lo + pre0 + pre)) : 0;
+        const int s = k >> 12, slot = k & 4095, z = c16_zero_slot(s);
+        const int pre = s * kC16SegPres + slot - (slot > z);
+        sh[k] = (slot != z && pre < pcount) ? static_cast<uint16_t>(__ldcg(a.hist_lo + pre0 + pre)) : 0;
     }
 }
 
@@ -594,7 +599,7 @@ __global__ void k_c16_count(const uint32_t* meta, const int64_t* off, int64_t li
 // the P = 32/SUB lists one warp reads together are filled LDS by LDS (slot g =
 // chunk row g/8, entry g%8); a lane takes, from its chunk's segment, an entry
 // in the bank with the lowest load in this LDS so far (ties: most entries left
-// in the group, then in the list), padding 0xfff1 once the segment is empty.
+// in the group, then in the list), padding (the zero slot) once the segment is empty.
 template <int SUB>
 __global__ void k_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* off, const uint2* desc, int nblocks,
                            int nl, int pb, uint16_t* out) {
@@ -626,7 +631,8 @@ __global__ void k_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* o
             const int pl = static_cast<int>(meta[q] & 0xffffu);
             if (pl == pb) continue;
             const int s = pl / kC16SegPres;
-            cnt[i][s][((pl - s * kC16SegPres) >> 1) & 31] += 1;
+            const int low = pl - s * kC16SegPres;
+            cnt[i][s][((low + (low >= c16_zero_slot(s))) >> 1) & 31] += 1;
         }
         int acc = 0;
         for (int s = 0; s < 4; ++s)
@@ -640,9 +646,9 @@ __global__ void k_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* o
             const int pl = static_cast<int>(m & 0xffffu);
             if (pl == pb) continue;
             const int s = pl / kC16SegPres;
-            const int low = pl - s * kC16SegPres;
-            const uint32_t j = static_cast<uint32_t>(low & 1) * 16u + ((m >> 16) & 15u);  // bit of the pair
-            tmp[o0 + cur[i][s][(low >> 1) & 31]++] = static_cast<uint32_t>(low >> 1) << 5 | ((j + 1u) & 31u);
+            const int slot = pl - s * kC16SegPres + (pl - s * kC16SegPres >= c16_zero_slot(s));
+            const uint32_t j = static_cast<uint32_t>(slot & 1) * 16u + ((m >> 16) & 15u);  // bit of the pair
+            tmp[o0 + cur[i][s][(slot >> 1) & 31]++] = static_cast<uint32_t>(slot >> 1) << 5 | ((j + 1u) & 31u);
         }
         for (int s = 0; s < 4; ++s)
             for (int j = 0; j < 32; ++j) cur[i][s][j] = static_cast<uint16_t>(cur[i][s][j] - cnt[i][s][j]);
@@ -668,7 +674,9 @@ __global__ void k_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* o
                                                    (tot[j] == tot[best] && cnt[i][s][j] > cnt[i][s][best]))))
                         best = j;
                 }
-                uint16_t v = 0xfff1u;  // padding: the segment's zero slot 4095 (pair 2047, bit 16)
+                // padding: the segment's zero slot (odd: upper half of its pair, bit 16)
+                const int z = c16_zero_slot(s);
+                uint16_t v = static_cast<uint16_t>((z >> 1) << 5 | 17);
                 if (best >= 0) {
                     v = static_cast<uint16_t>(tmp[o0 + cur[i][s][best]]);
                     cur[i][s][best] += 1;
@@ -676,7 +684,7 @@ __global__ void k_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* o
                     tot[best] -= 1;
                     load[best] += 1;
                 } else {
-                    load[31] += 1;
+                    load[(z >> 1) & 31] += 1;
                 }
                 out[base + static_cast<int64_t>(c) * 8 + e] = v;
             }
