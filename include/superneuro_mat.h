@@ -153,8 +153,11 @@ typedef enum sn_sweep_kernel {
                                    static lists (counts the delivering pres) */
     SN_SWEEP_PERSISTENT_COLS = 12, /* k_persistent_cols: whole step loop in one launch, CTAs own
                                      32-post column groups, one grid barrier per step */
-    SN_SWEEP_SPARSE_COUNT16 = 13  /* k_sparse_count16: one-weight lists as 16-bit entries in
+    SN_SWEEP_SPARSE_COUNT16 = 13, /* k_sparse_count16: one-weight lists as 16-bit entries in
                                      4095-pre segments (2 B/synapse), delays <= 16 */
+    SN_SWEEP_CLUSTER = 14         /* k_cluster_count: whole step loop in ONE thread-block cluster,
+                                     history exchanged through distributed shared memory
+                                     (small static one-weight nets, delays <= 31) */
 } sn_sweep_kernel;
 
 /* ---- lifecycle ---------------------------------------------------------- */

@@ -199,6 +199,11 @@ private:
     bool persistent_ = false;     // small dense nets: one cooperative launch per simulate
     bool cols_ = false;           // ... as column owners (k_persistent_cols, one barrier per step)
     int32_t col_width_ = 8;       // posts per column group
+    bool cluster_ = false;        // ... as one thread-block cluster (k_cluster_count: static one-weight nets)
+    int32_t cl_cs_ = 0, cl_P_ = 0;
+    double cl_w0_ = 0.0;
+    DevBuf d_clcodes_;
+    bool uniform_weight(double* w0) const;
     DevBuf d_hist2_, d_pot2_, d_act2_;
     bool dynamic_sched_ = false;  // dense sweep items claimed through an atomic counter
     bool tma_ = false;            // k_dense_tma (cp.async.bulk ring) instead of k_dense_stream

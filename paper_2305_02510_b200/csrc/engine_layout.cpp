@@ -379,6 +379,27 @@ void Engine::plan_launches() {
                 }
             }
         }
+        // one thread-block cluster with distributed shared memory instead of a
+        // grid barrier: static one-weight nets without plasticity (cfg2)
+        cluster_ = false;
+        double w0 = 0.0;
+        if (!stdp_on_ && !tiny && dmax_ <= 31 && hw_ == 1 && !(pk && std::string(pk) != "cluster") &&
+            uniform_weight(&w0) && w0 != 0.0) {
+            int P = 0;
+            const int cs = cluster_plan(n_, nl_, f64_, &P);
+            if (cs > 0) {
+                cluster_ = true;
+                cols_ = false;
+                cl_cs_ = cs;
+                cl_P_ = P;
+                cl_w0_ = w0;
+                d_clcodes_.alloc(static_cast<size_t>(cs) * n_ * P);
+                launch_cluster_codes(dense_args(), nl_, P, cs, d_clcodes_.as<uint8_t>(), f64_, stream_);
+                d_hist2_.alloc(static_cast<size_t>(2) * n_ * 8);
+                cuda_check(cudaMemsetAsync(d_hist2_.p, 0, d_hist2_.bytes, stream_), "memset");
+                persist_grid_ = cs;
+            }
+        }
         if (cols_) {
             const size_t esz2 = f64_ ? 8 : 4;
             d_hist2_.alloc(static_cast<size_t>(2) * n_ * 8);
@@ -511,6 +532,20 @@ void Engine::plan_launches() {
             }
         }
     }
+}
+
+// One weight for every synapse (ER-generated nets, or host lists whose weights
+// are all equal): the cluster loop counts delivering pres instead of summing.
+bool Engine::uniform_weight(double* w0) const {
+    if (generated_) {
+        *w0 = f64_ ? er_.weight_d : static_cast<double>(er_.weight_f);
+        return true;
+    }
+    if (weight_.empty()) return false;
+    for (double w : weight_)
+        if (w != weight_[0]) return false;
+    *w0 = weight_[0];
+    return true;
 }
 
 bool Engine::c16_allowed() {

@@ -187,7 +187,7 @@ void Engine::get_stats(sn_stats* out) {
             stats_.sweep_kernel = SN_SWEEP_TINY;
             stats_.sweep_ctas = 1;
         } else if (dense_) {
-            stats_.sweep_kernel = persistent_ ? (cols_ ? SN_SWEEP_PERSISTENT_COLS : SN_SWEEP_PERSISTENT)
+            stats_.sweep_kernel = persistent_ ? (cluster_ ? SN_SWEEP_CLUSTER : cols_ ? SN_SWEEP_PERSISTENT_COLS : SN_SWEEP_PERSISTENT)
                                   : exact_    ? SN_SWEEP_DENSE_EXACT
                                   : tma_      ? SN_SWEEP_DENSE_TMA
                                               : SN_SWEEP_DENSE_STREAM;

@@ -478,7 +478,18 @@ void Engine::simulate(int32_t steps) {
         if (persistent_) {
             cudaEvent_t p0{}, p1{};
             if (opt_.profile) { p0 = get_event(); cuda_check(cudaEventRecord(p0, stream_), "rec"); }
-            if (cols_) {
+            if (cluster_) {
+                ClusterArgs ka{};
+                ka.codes = d_clcodes_.as<uint8_t>();
+                ka.P = cl_P_;
+                ka.cs = cl_cs_;
+                ka.w0 = cl_w0_;
+                ka.hist2 = d_hist2_.as<uint64_t>();
+                ka.partial = d_partial_.as<double>();
+                ka.active_count = d_spikes_.as<unsigned long long>() + 1;
+                ka.dmask = dmax_ >= 64 ? ~0ull : ((1ull << dmax_) - 1ull);
+                launch_cluster_count(na, ka, f64_, steps, stream_);
+            } else if (cols_) {
                 ColArgs ca{};
                 ca.hist2 = d_hist2_.as<uint64_t>();
                 ca.pot2 = d_pot2_.p;

@@ -501,6 +501,196 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
     if (blockIdx.x == 0 && tid == 0) *na.d_step = t;
 }
 
+// ---------------------------------------------------------------------------
+// Cluster loop for small static one-weight nets without plasticity (cfg2: 1000
+// neurons all-to-all, delays 1..8): ONE thread-block cluster of cs CTAs (16,
+// non-portable, or 8) runs the whole call.  CTA r owns posts [r P, r P + P)
+// (P a multiple of 32) and keeps, in its shared memory, one rotation code per
+// (pre, owned post) -- (d + 1) & 31 for a synapse of delay d, 1 for none -- and
+// a copy of every pre's history word h << 1 (double-buffered by step parity).
+// Per step: (1) the owner threads run the LIF update of their posts (as
+// k_persistent_cols) and store their new history word into EVERY CTA's copy
+// with distributed-shared-memory stores; (2) one cluster barrier
+// (barrier.cluster arrive.release / wait.acquire) -- instead of a grid barrier
+// plus L2 round trips; (3) each CTA counts, for its posts, the pres whose bit
+// d - 1 is set: rot_r(h << 1, code) >> 31 per (pre, post), integer counts
+// reduced in shared memory, input = count * w.  No global memory on the step
+// path except the raster words and the stimulus table.
+constexpr int kClThreads = 1024;
+
+template <typename WT>
+__global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, ClusterArgs ca, int steps) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int r = static_cast<int>(cluster.block_rank());
+    const int cs = ca.cs, P = ca.P, n = na.n;
+    const int npad = (n + 3) & ~3;
+    uint8_t* s_code = smem;                                                       // [n][P]
+    uint32_t* s_h2 = reinterpret_cast<uint32_t*>(smem + static_cast<size_t>(n) * P);  // [2][npad]
+    int* s_red = reinterpret_cast<int*>(s_h2 + 2 * npad);                            // [1024 / (P/4)][P]
+    double* s_in = reinterpret_cast<double*>(s_red + kClThreads * 4);               // [P]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    {   // this CTA's code block, once per call
+        const uint4* src = reinterpret_cast<const uint4*>(ca.codes + static_cast<size_t>(r) * n * P);
+        uint4* dst = reinterpret_cast<uint4*>(s_code);
+        for (int k = tid; k < n * P / 16; k += kClThreads) dst[k] = __ldg(src + k);
+    }
+    const int p = tid;                       // owner thread of post j (tid < P)
+    const int j = r * P + p;
+    const bool own = tid < P && j < na.nl;
+    int t = *na.d_step;
+    double v = 0.0, thr = 0.0, leak = 0.0, rst = 0.0, fire_p = 1.0, in = 0.0;
+    int32_t cnt = 0, refr = 0;
+    uint64_t hprev = 0, akey = 0;
+    unsigned long long spikes = 0, active = 0;
+    if (own) {
+        v = na.v[j];
+        thr = na.thr[j];
+        leak = na.leak[j];
+        rst = na.reset[j];
+        cnt = na.cnt[j];
+        refr = na.refr[j];
+        in = na.partial[j];
+        hprev = ca.hist2[static_cast<int64_t>((t & 1) ^ 1) * n + j];
+        if (na.fire_p) {
+            fire_p = na.fire_p[j];
+            akey = na.agent_key[j];
+        }
+    }
+    int64_t slo = 0, shi = 0;                // stimulus rows of the step, fetched a step ahead
+    auto stim_bounds = [&](int tt) {
+        slo = shi = 0;
+        const int row = tt - na.st_base;
+        if (own && row >= 0 && row < na.st_steps) {
+            slo = __ldg(na.st_off + row);
+            shi = __ldg(na.st_off + row + 1);
+        }
+    };
+    stim_bounds(t);
+    const int CG = P / 4, RL = kClThreads / CG;  // threads tid >= RL * CG idle in the sweep
+    const int cg4 = tid % CG, rl = tid / CG;
+    int per = 32;                                  // reduction threads per post: a power of two
+    while (per * P > kClThreads) per >>= 1;
+    const WT w0 = static_cast<WT>(ca.w0);
+    for (int s = 0; s < steps; ++s, ++t) {
+        const int cur = t & 1;
+        if (tid < P) {  // (1) LIF update of the owned posts (k_persistent_cols' neuron phase)
+            bool fired = false;
+            if (own) {
+                double u = na.abm ? in : leak_toward(v, leak, rst) + in;
+                if (shi > slo) {
+                    int64_t lo = slo, hi = shi;
+                    double ext = 0.0;
+                    while (lo < hi) {
+                        const int64_t mid = (lo + hi) >> 1;
+                        const int nid = __ldg(na.st_neuron + mid);
+                        if (nid == j) { ext = __ldg(na.st_amp + mid); break; }
+                        if (nid < j) lo = mid + 1; else hi = mid;
+                    }
+                    u += ext;
+                }
+                if (na.abm) u = leak_toward(v, leak, rst) + u;
+                fired = u > thr;
+                if (fired && fire_p < 1.0) fired = agent_fires(akey, t, fire_p);
+                if (cnt > 0) {
+                    fired = false;
+                    cnt -= 1;
+                    u = rst;
+                }
+                if (fired) {
+                    v = rst;
+                    cnt = refr;
+                } else {
+                    v = u;
+                }
+                if (na.trace && (t - na.t_base) < na.raster_rows)
+                    na.trace[static_cast<int64_t>(t - na.t_base) * na.nl + j] = v;
+                const uint64_t hn = (hprev << 1) | (fired ? 1ull : 0ull);
+                hprev = hn;
+                spikes += fired ? 1 : 0;
+                active += (hn & ca.dmask) != 0 ? 1 : 0;
+                const uint32_t h2 = static_cast<uint32_t>(hn << 1);
+                uint32_t* mine = s_h2 + cur * npad + j;
+                for (int q = 0; q < cs; ++q) *cluster.map_shared_rank(mine, q) = h2;  // DSMEM store
+            }
+            const uint32_t word = __ballot_sync(0xffffffffu, fired);
+            if (lane == 0 && na.raster && (t - na.t_base) < na.raster_rows && (r * P + warp * 32) < na.nl)
+                na.raster[static_cast<int64_t>(t - na.t_base) * na.nl_words + ((r * P) >> 5) + warp] = word;
+        }
+        cluster.sync();  // (2) every CTA's copy of the step's history words is complete
+        stim_bounds(t + 1);
+        // (3) counts of the delivering pres for this CTA's posts
+        const uint32_t* h2c = s_h2 + cur * npad;
+        int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll 4
+        for (int i = rl < RL ? rl : n; i < n; i += RL) {
+            const uint32_t code = *reinterpret_cast<const uint32_t*>(s_code + static_cast<size_t>(i) * P + cg4 * 4);
+            const uint32_t h = h2c[i];
+            c0 += static_cast<int>(__funnelshift_r(h, h, code) >> 31);
+            c1 += static_cast<int>(__funnelshift_r(h, h, code >> 8) >> 31);
+            c2 += static_cast<int>(__funnelshift_r(h, h, code >> 16) >> 31);
+            c3 += static_cast<int>(__funnelshift_r(h, h, code >> 24) >> 31);
+        }
+        if (rl < RL) {
+            int* red = s_red + rl * P + cg4 * 4;
+            red[0] = c0;
+            red[1] = c1;
+            red[2] = c2;
+            red[3] = c3;
+        }
+        __syncthreads();
+        if (tid < per * P) {  // integer partials: any order is exact; then shuffles over `per` lanes
+            const int pp = tid / per, q = tid % per;
+            int sum = 0;
+            for (int k = q; k < RL; k += per) sum += s_red[k * P + pp];
+            for (int o = per / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            if (q == 0) s_in[pp] = static_cast<double>(static_cast<WT>(sum) * w0);
+        }
+        __syncthreads();
+        if (tid < P) in = s_in[p];
+    }
+    if (own) {
+        ca.partial[j] = in;  // (same buffer as na.partial) input of the next call's first step
+        na.v[j] = v;
+        na.cnt[j] = cnt;
+        ca.hist2[static_cast<int64_t>((t & 1) ^ 1) * n + j] = hprev;
+    }
+    if (tid < P) {
+        for (int o = 16; o > 0; o >>= 1) {
+            spikes += __shfl_xor_sync(0xffffffffu, spikes, o);
+            active += __shfl_xor_sync(0xffffffffu, active, o);
+        }
+        if (lane == 0) {
+            if (spikes) atomicAdd(na.spike_count, spikes);
+            if (active && ca.active_count) atomicAdd(ca.active_count, active);
+        }
+    }
+    if (r == 0 && tid == 0) *na.d_step = t;
+}
+
+// Setup: rotation codes of the cluster loop, [cs][n][P]; a synapse is a
+// non-zero weight (one-weight nets), its delay d from the dense delay bytes.
+template <typename WT>
+__global__ void k_cluster_codes(DenseArgs da, int nl, int P, int cs, uint8_t* codes) {
+    const int64_t total = static_cast<int64_t>(cs) * da.n * P;
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int p = static_cast<int>(k % P);
+        const int64_t ri = k / P;
+        const int i = static_cast<int>(ri % da.n), r = static_cast<int>(ri / da.n);
+        const int j = r * P + p;
+        uint8_t c = 1;
+        if (j < nl) {
+            const int64_t e = static_cast<int64_t>(i) * da.pitch + j;
+            if (static_cast<const WT*>(da.w)[e] != WT(0)) {
+                const int d = da.delay ? da.delay[e] : 1;
+                c = static_cast<uint8_t>((d + 1) & 31);
+            }
+        }
+        codes[k] = c;
+    }
+}
+
 }  // namespace
 
 size_t tiny_smem_bytes(const TinyArgs& a) { return tiny_layout(a).total; }
@@ -619,6 +809,81 @@ int persistent_max_ctas(bool f64, bool stdp, bool delay) {
 void launch_persistent_dense(const NeuronArgs& na, const HistArgs& h, const DenseArgs& da, bool f64,
                              bool stdp, bool delay, int grid, int steps, cudaStream_t s) {
     persistent_dispatch(na, h, da, f64, stdp, delay, grid, steps, s, nullptr);
+}
+
+
+size_t cluster_smem_bytes(int n, int P) {
+    const int npad = (n + 3) & ~3;
+    return static_cast<size_t>(n) * P + static_cast<size_t>(2) * npad * 4 + static_cast<size_t>(kClThreads) * 4 * 4 +
+           static_cast<size_t>(P) * 8;
+}
+
+// Cluster size for a net of n posts: 16 CTAs (non-portable) when the device
+// runs such a cluster, else 8; 0 when the codes do not fit shared memory.
+int cluster_plan(int n, int nl, bool f64, int* P_out) {
+    int dev = 0, optin = 0;
+    check(cudaGetDevice(&dev), "cudaGetDevice");
+    check(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
+    for (int cs : {16, 8}) {
+        const int P = ((nl + cs - 1) / cs + 31) / 32 * 32;
+        if (P > 256) continue;  // 1024 threads: >= 16 row lanes of 4 posts, >= 4 reduction threads per post
+        const size_t smem = cluster_smem_bytes(n, P);
+        if (smem > static_cast<size_t>(optin)) continue;
+        auto kern = f64 ? reinterpret_cast<const void*>(k_cluster_count<double>)
+                        : reinterpret_cast<const void*>(k_cluster_count<float>);
+        if (cs > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+              "k_cluster_count smem attribute");
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(cs);
+        cfg.blockDim = dim3(kClThreads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at{};
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = cs;
+        at.val.clusterDim.y = 1;
+        at.val.clusterDim.z = 1;
+        cfg.attrs = &at;
+        cfg.numAttrs = 1;
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        if (clusters < 1) continue;
+        *P_out = P;
+        return cs;
+    }
+    return 0;
+}
+
+void launch_cluster_codes(const DenseArgs& da, int nl, int P, int cs, uint8_t* codes, bool f64, cudaStream_t s) {
+    const int64_t total = static_cast<int64_t>(cs) * da.n * P;
+    const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+    if (f64) k_cluster_codes<double><<<grid, 256, 0, s>>>(da, nl, P, cs, codes);
+    else k_cluster_codes<float><<<grid, 256, 0, s>>>(da, nl, P, cs, codes);
+    check(cudaGetLastError(), "k_cluster_codes");
+}
+
+void launch_cluster_count(const NeuronArgs& na, const ClusterArgs& ca, bool f64, int steps, cudaStream_t s) {
+    const size_t smem = cluster_smem_bytes(na.n, ca.P);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ca.cs);
+    cfg.blockDim = dim3(kClThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at{};
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = ca.cs;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    if (f64) check(cudaLaunchKernelEx(&cfg, k_cluster_count<double>, na, ca, steps), "k_cluster_count");
+    else check(cudaLaunchKernelEx(&cfg, k_cluster_count<float>, na, ca, steps), "k_cluster_count");
 }
 
 }  // namespace snb

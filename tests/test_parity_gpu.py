@@ -210,6 +210,85 @@ def test_cfg2_delays_match_reference(storage):
     assert _digest(s, n) == e["digest"]
 
 
+def test_cfg2_cluster_loop_selected_and_exact():
+    """cfg2 runs as one thread-block cluster (k_cluster_count) and reproduces the
+    reference raster; so does the column-owner loop it replaced."""
+    import os
+    e = _scale()["cfg2_seed0"]
+    eng = _generated(e, 1, by_syn=True)
+    st = eng.stats()
+    s, n = eng.raster()
+    eng.close()
+    assert st["sweep_kernel"] == 14
+    assert _digest(s, n) == e["digest"]
+    os.environ["SNB_PERSIST_KERNEL"] = "cols"
+    try:
+        eng = _generated(e, 1, by_syn=True)
+        st = eng.stats()
+        s, n = eng.raster()
+        eng.close()
+    finally:
+        del os.environ["SNB_PERSIST_KERNEL"]
+    assert st["sweep_kernel"] == 12
+    assert _digest(s, n) == e["digest"]
+
+
+@pytest.mark.parametrize("n,dmax,precision,abm,chunks", [
+    (300, 31, "f64", False, (40, 1, 19)),   # 32-post CTAs, longest delay, chunked calls
+    (1000, 8, "f32", True, (60,)),          # stochastic agents (ABM) in the cluster
+    (1500, 4, "f32", False, (25, 25)),      # 96-post CTAs (row lanes and reduction threads not powers of two)
+    (777, 12, "f64", False, (30,)),         # ragged last CTA
+])
+def test_cluster_loop_matches_oracle(n, dmax, precision, abm, chunks):
+    """k_cluster_count on host-built one-weight nets (leak, refractory,
+    thresholds, stimulus, delays, membranes traced) against the C oracles, over
+    several simulate() calls."""
+    from oracle import bridge as B
+    from paper_2305_02510_b200.engine import MatEngine
+    from paper_2305_02510_b200.netgen import RandomStream, erdos_renyi_arrays, scenario_stimulus
+    seed = 17
+    steps = sum(chunks)
+    pre, post = erdos_renyi_arrays(n, 0.3, seed)
+    m = len(pre)
+    rs = RandomStream(seed, 5)
+    k = np.arange(m, dtype=np.uint64)
+    delay = (1 + rs.below_np(k, dmax)).astype(np.int32)
+    ki = np.arange(n, dtype=np.uint64)
+    thr = 20.0 + 10.0 * rs.unit_np(ki + np.uint64(m))
+    leak = np.where(ki % 5 == 0, np.inf, 0.75 * rs.unit_np(ki + np.uint64(m + n)))
+    reset = np.zeros(n)
+    refr = (ki % 3).astype(np.int32)
+    w = np.full(m, 0.5)
+    arrays = {"threshold": thr, "leak": leak, "reset": reset, "refractory": refr,
+              "axonal": np.zeros(n, np.int32), "pre": pre, "post": post, "weight": w, "delay": delay,
+              "stdp": np.zeros(m, np.uint8)}
+    stim = scenario_stimulus(n, steps, seed, count=max(3, n // 20), period=3, amplitude=30.0).to_arrays()
+    fire_p = None
+    if abm:
+        fire_p = np.where(ki % 2 == 0, 1.0, 0.5)
+        o = B.run_abm_oracle(arrays, steps, stim, seed=seed, fire_p=fire_p)
+    else:
+        o = B.run_oracle(arrays, steps, stim)
+    eng = MatEngine(storage=1, precision=precision, mode="abm" if abm else "mat")
+    eng.add_neurons(thr, leak, reset, refr, arrays["axonal"])
+    if abm:
+        eng.set_seed(seed)
+        eng.set_fire_probability(fire_p)
+    eng.add_synapses(pre, post, w, delay, None)
+    eng.setup()
+    eng.add_stimulus(*stim)
+    for c in chunks:
+        eng.simulate(c)
+    s, q = eng.raster()
+    st = eng.stats()
+    mem = eng.membrane()
+    eng.close()
+    assert st["sweep_kernel"] == 14
+    assert len(o["steps"]) > 200
+    assert np.array_equal(s, o["steps"]) and np.array_equal(q, o["neurons"])
+    assert close_rel(mem, o["membrane"])
+
+
 @pytest.mark.parametrize("storage", [0, 1, 2])
 def test_long_stdp_window_multiword_history(storage):
     """StdpConfig windows are arbitrary (model.cpp:104-117): window 70 with
