@@ -200,7 +200,7 @@ private:
     bool cols_ = false;           // ... as column owners (k_persistent_cols, one barrier per step)
     int32_t col_width_ = 8;       // posts per column group
     bool cluster_ = false;        // ... as one thread-block cluster (k_cluster_count: static one-weight nets)
-    int32_t cl_cs_ = 0, cl_P_ = 0;
+    int32_t cl_cs_ = 0, cl_P_ = 0, cl_D_ = 0;
     double cl_w0_ = 0.0;
     DevBuf d_clcodes_;
     bool uniform_weight(double* w0) const;

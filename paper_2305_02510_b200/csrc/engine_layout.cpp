@@ -385,16 +385,17 @@ void Engine::plan_launches() {
         double w0 = 0.0;
         if (!stdp_on_ && !tiny && dmax_ <= 31 && hw_ == 1 && !(pk && std::string(pk) != "cluster") &&
             uniform_weight(&w0) && w0 != 0.0) {
-            int P = 0;
-            const int cs = cluster_plan(n_, nl_, f64_, &P);
+            int P = 0, D = 0;
+            const int cs = cluster_plan(n_, nl_, f64_, dmax_, &P, &D);
             if (cs > 0) {
                 cluster_ = true;
                 cols_ = false;
                 cl_cs_ = cs;
                 cl_P_ = P;
+                cl_D_ = D;
                 cl_w0_ = w0;
-                d_clcodes_.alloc(static_cast<size_t>(cs) * n_ * P);
-                launch_cluster_codes(dense_args(), nl_, P, cs, d_clcodes_.as<uint8_t>(), f64_, stream_);
+                d_clcodes_.alloc(cluster_table_bytes(n_, P, D, cs));
+                launch_cluster_table(dense_args(), nl_, P, D, cs, d_clcodes_.p, f64_, stream_);
                 d_hist2_.alloc(static_cast<size_t>(2) * n_ * 8);
                 cuda_check(cudaMemsetAsync(d_hist2_.p, 0, d_hist2_.bytes, stream_), "memset");
                 persist_grid_ = cs;

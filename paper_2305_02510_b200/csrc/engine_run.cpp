@@ -482,6 +482,7 @@ void Engine::simulate(int32_t steps) {
                 ClusterArgs ka{};
                 ka.codes = d_clcodes_.as<uint8_t>();
                 ka.P = cl_P_;
+                ka.D = cl_D_;
                 ka.cs = cl_cs_;
                 ka.w0 = cl_w0_;
                 ka.hist2 = d_hist2_.as<uint64_t>();

@@ -518,23 +518,88 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
 // path except the raster words and the stimulus table.
 constexpr int kClThreads = 1024;
 
-template <typename WT>
+// DSMEM store that completes 4 transaction bytes on the target CTA's mbarrier
+__device__ __forceinline__ void st_async_u32(uint32_t remote_addr, uint32_t v, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(remote_addr),
+                 "r"(v), "r"(remote_bar)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, int rank) {
+    uint32_t d;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(addr), "r"(rank));
+    return d;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAITC_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Shared-memory layout of k_cluster_count (D = 0: rotation codes; D = 8 / 16:
+// delay bit-planes).
+struct ClLayout {
+    size_t code, ex, red, in, bar, total;
+};
+__host__ __device__ inline ClLayout cl_layout(int n, int P, int D) {
+    ClLayout L{};
+    const int npad = (n + 3) & ~3;
+    const int wn4 = ((n + 31) / 32 + 15) & ~15;
+    size_t o = 0;
+    L.code = o;
+    o += D == 0 ? static_cast<size_t>(n) * P : static_cast<size_t>(P) * D * wn4 * 4;
+    L.ex = o;
+    o += D == 0 ? static_cast<size_t>(2) * npad * 4 : static_cast<size_t>(2) * D * wn4 * 4;
+    L.red = o;
+    o += D == 0 ? static_cast<size_t>(kClThreads) * 4 * 4 : 0;
+    L.in = o;
+    o += static_cast<size_t>(P) * 8;
+    L.bar = o;
+    o += 16;
+    L.total = o;
+    return L;
+}
+
+template <typename WT, int P, int D>
 __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, ClusterArgs ca, int steps) {
     extern __shared__ __align__(16) uint8_t smem[];
     cg::cluster_group cluster = cg::this_cluster();
     const int r = static_cast<int>(cluster.block_rank());
-    const int cs = ca.cs, P = ca.P, n = na.n;
+    const int cs = ca.cs, n = na.n;
     const int npad = (n + 3) & ~3;
-    uint8_t* s_code = smem;                                                       // [n][P]
-    uint32_t* s_h2 = reinterpret_cast<uint32_t*>(smem + static_cast<size_t>(n) * P);  // [2][npad]
-    int* s_red = reinterpret_cast<int*>(s_h2 + 2 * npad);                            // [1024 / (P/4)][P]
-    double* s_in = reinterpret_cast<double*>(s_red + kClThreads * 4);               // [P]
+    const int wn4 = ((n + 31) / 32 + 15) & ~15;  // history words per delay plane (padded)
+    const ClLayout L = cl_layout(n, P, D);
+    uint8_t* s_code = smem + L.code;                                  // D = 0: [n][P] rotation codes
+    const uint32_t* s_mask = reinterpret_cast<const uint32_t*>(smem + L.code);  // D > 0: [P][D][wn4]
+    uint32_t* s_ex = reinterpret_cast<uint32_t*>(smem + L.ex);        // [2][npad] h << 1, or [2][D][wn4] planes
+    int* s_red = reinterpret_cast<int*>(smem + L.red);                // D = 0: [1024 / (P/4)][P]
+    double* s_in = reinterpret_cast<double*>(smem + L.in);            // [P]
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L.bar);      // [2] exchange buffer full
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    {   // this CTA's code block, once per call
-        const uint4* src = reinterpret_cast<const uint4*>(ca.codes + static_cast<size_t>(r) * n * P);
-        uint4* dst = reinterpret_cast<uint4*>(s_code);
-        for (int k = tid; k < n * P / 16; k += kClThreads) dst[k] = __ldg(src + k);
+    {   // this CTA's code / mask block, once per call; zero the exchange buffers (plane padding)
+        const size_t bytes = L.ex - L.code;
+        const uint4* src = reinterpret_cast<const uint4*>(ca.codes + static_cast<size_t>(r) * bytes);
+        uint4* dst = reinterpret_cast<uint4*>(smem + L.code);
+        for (size_t k = tid; k < bytes / 16; k += kClThreads) dst[k] = __ldg(src + k);
+        for (size_t k = tid; k < (L.red - L.ex) / 4; k += kClThreads) s_ex[k] = 0u;
     }
+    // exchange by st.async into every CTA's buffer, each store completing its
+    // bytes on that CTA's mbarrier of the buffer: no cluster barrier and no
+    // fence on the step path; double buffering keeps writers one step behind
+    // readers (a CTA writes buffer t+1 only after every CTA's step-t words
+    // reached it, i.e. after every CTA finished reading buffer t-1)
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster.sync();
+    uint32_t ph0 = 0, ph1 = 0;
+    const uint32_t tx_bytes = D == 0 ? 4u * static_cast<uint32_t>(na.nl)
+                                     : 4u * D * static_cast<uint32_t>((na.nl + 31) / 32);
     const int p = tid;                       // owner thread of post j (tid < P)
     const int j = r * P + p;
     const bool own = tid < P && j < na.nl;
@@ -567,15 +632,13 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
         }
     };
     stim_bounds(t);
-    const int CG = P / 4, RL = kClThreads / CG;  // threads tid >= RL * CG idle in the sweep
-    const int cg4 = tid % CG, rl = tid / CG;
-    int per = 32;                                  // reduction threads per post: a power of two
-    while (per * P > kClThreads) per >>= 1;
     const WT w0 = static_cast<WT>(ca.w0);
     for (int s = 0; s < steps; ++s, ++t) {
         const int cur = t & 1;
+        if (tid == 0) mbar_arrive_expect_tx(&s_bar[cur], tx_bytes);
         if (tid < P) {  // (1) LIF update of the owned posts (k_persistent_cols' neuron phase)
             bool fired = false;
+            uint64_t hn = 0;
             if (own) {
                 double u = na.abm ? in : leak_toward(v, leak, rst) + in;
                 if (shi > slo) {
@@ -605,48 +668,94 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
                 }
                 if (na.trace && (t - na.t_base) < na.raster_rows)
                     na.trace[static_cast<int64_t>(t - na.t_base) * na.nl + j] = v;
-                const uint64_t hn = (hprev << 1) | (fired ? 1ull : 0ull);
+                hn = (hprev << 1) | (fired ? 1ull : 0ull);
                 hprev = hn;
                 spikes += fired ? 1 : 0;
                 active += (hn & ca.dmask) != 0 ? 1 : 0;
-                const uint32_t h2 = static_cast<uint32_t>(hn << 1);
-                uint32_t* mine = s_h2 + cur * npad + j;
-                for (int q = 0; q < cs; ++q) *cluster.map_shared_rank(mine, q) = h2;  // DSMEM store
+                if (D == 0) {  // this pre's word h << 1 into every CTA's copy
+                    const uint32_t la = smem_u32(s_ex + cur * npad + j), lb = smem_u32(&s_bar[cur]);
+                    const uint32_t h2 = static_cast<uint32_t>(hn << 1);
+                    for (int q = 0; q < cs; ++q) st_async_u32(mapa_u32(la, q), h2, mapa_u32(lb, q));
+                }
+            }
+            const bool live = (r * P + warp * 32) < na.nl;  // warp-uniform
+            if (D > 0) {  // delay planes: lane d holds the word of bit d of the warp's 32 pres
+                uint32_t mine = 0;
+#pragma unroll
+                for (int d = 0; d < D; ++d) {
+                    const uint32_t b = __ballot_sync(0xffffffffu, (hn >> d) & 1ull);
+                    if (lane == d) mine = b;
+                }
+                if (live && lane < D) {
+                    const int w = (r * P) / 32 + warp;
+                    const uint32_t la = smem_u32(s_ex + (cur * D + lane) * wn4 + w), lb = smem_u32(&s_bar[cur]);
+                    for (int q = 0; q < cs; ++q) st_async_u32(mapa_u32(la, q), mine, mapa_u32(lb, q));
+                }
             }
             const uint32_t word = __ballot_sync(0xffffffffu, fired);
-            if (lane == 0 && na.raster && (t - na.t_base) < na.raster_rows && (r * P + warp * 32) < na.nl)
+            if (lane == 0 && na.raster && (t - na.t_base) < na.raster_rows && live)
                 na.raster[static_cast<int64_t>(t - na.t_base) * na.nl_words + ((r * P) >> 5) + warp] = word;
         }
-        cluster.sync();  // (2) every CTA's copy of the step's history words is complete
+        // (2) every owner's words of the step have landed in this CTA's buffer
+        if (cur) { mbar_wait_cluster(&s_bar[1], ph1); ph1 ^= 1u; }
+        else { mbar_wait_cluster(&s_bar[0], ph0); ph0 ^= 1u; }
         stim_bounds(t + 1);
-        // (3) counts of the delivering pres for this CTA's posts
-        const uint32_t* h2c = s_h2 + cur * npad;
-        int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
-#pragma unroll 4
-        for (int i = rl < RL ? rl : n; i < n; i += RL) {
-            const uint32_t code = *reinterpret_cast<const uint32_t*>(s_code + static_cast<size_t>(i) * P + cg4 * 4);
-            const uint32_t h = h2c[i];
-            c0 += static_cast<int>(__funnelshift_r(h, h, code) >> 31);
-            c1 += static_cast<int>(__funnelshift_r(h, h, code >> 8) >> 31);
-            c2 += static_cast<int>(__funnelshift_r(h, h, code >> 16) >> 31);
-            c3 += static_cast<int>(__funnelshift_r(h, h, code >> 24) >> 31);
-        }
-        if (rl < RL) {
-            int* red = s_red + rl * P + cg4 * 4;
-            red[0] = c0;
-            red[1] = c1;
-            red[2] = c2;
-            red[3] = c3;
-        }
-        __syncthreads();
-        if (tid < per * P) {  // integer partials: any order is exact; then shuffles over `per` lanes
-            const int pp = tid / per, q = tid % per;
+        // (3) counts of the delivering pres for this CTA's posts (integers: any order is exact)
+        if (D > 0) {
+            // thread (post, delay d, part): popc(mask[post][d] & plane[d]) over its words
+            constexpr int PAIRS = P * (D > 0 ? D : 1);
+            constexpr int T = kClThreads / PAIRS >= 4 ? 4 : kClThreads / PAIRS >= 2 ? 2 : 1;
+            static_assert(D == 0 || (PAIRS <= kClThreads && D * T <= 32), "cluster plane tiling");
             int sum = 0;
-            for (int k = q; k < RL; k += per) sum += s_red[k * P + pp];
-            for (int o = per / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-            if (q == 0) s_in[pp] = static_cast<double>(static_cast<WT>(sum) * w0);
+            if (tid < PAIRS * T) {
+                const int pi = tid / T, part = tid % T;
+                const int pp = pi / (D > 0 ? D : 1), d = pi % (D > 0 ? D : 1);
+                const int per_part = wn4 / T;  // multiple of 4
+                const uint4* m4 = reinterpret_cast<const uint4*>(s_mask + (pp * D + d) * wn4 + part * per_part);
+                const uint4* e4 = reinterpret_cast<const uint4*>(s_ex + (cur * D + d) * wn4 + part * per_part);
+                for (int k = 0; k < per_part / 4; ++k) {
+                    const uint4 m = m4[k], e = e4[k];
+                    sum += __popc(m.x & e.x) + __popc(m.y & e.y) + __popc(m.z & e.z) + __popc(m.w & e.w);
+                }
+#pragma unroll
+                for (int o = (D * T) / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                if (d == 0 && part == 0) s_in[pp] = static_cast<double>(static_cast<WT>(sum) * w0);
+            }
+            __syncthreads();
+        } else {
+            constexpr int CG = P / 4, RL = kClThreads / CG;  // threads tid >= RL * CG idle in the sweep
+            constexpr int per = kClThreads / P >= 32 ? 32 : kClThreads / P >= 16 ? 16 : kClThreads / P >= 8 ? 8 : 4;
+            const int cg4 = tid % CG, rl = tid / CG;
+            const uint32_t* h2c = s_ex + cur * npad;
+            int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll 4
+            for (int i = rl < RL ? rl : n; i < n; i += RL) {
+                const uint32_t code = *reinterpret_cast<const uint32_t*>(s_code + static_cast<size_t>(i) * P + cg4 * 4);
+                const uint32_t h = h2c[i];
+                c0 += static_cast<int>(__funnelshift_r(h, h, code) >> 31);
+                c1 += static_cast<int>(__funnelshift_r(h, h, code >> 8) >> 31);
+                c2 += static_cast<int>(__funnelshift_r(h, h, code >> 16) >> 31);
+                c3 += static_cast<int>(__funnelshift_r(h, h, code >> 24) >> 31);
+            }
+            if (rl < RL) {
+                int* red = s_red + rl * P + cg4 * 4;
+                red[0] = c0;
+                red[1] = c1;
+                red[2] = c2;
+                red[3] = c3;
+            }
+            __syncthreads();
+            if (tid < per * P) {  // RL / per partials per thread, then shuffles over `per` lanes
+                const int pp = tid / per, q = tid % per;
+                int sum = 0;
+#pragma unroll
+                for (int k = q; k < RL; k += per) sum += s_red[k * P + pp];
+#pragma unroll
+                for (int o = per / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                if (q == 0) s_in[pp] = static_cast<double>(static_cast<WT>(sum) * w0);
+            }
+            __syncthreads();
         }
-        __syncthreads();
         if (tid < P) in = s_in[p];
     }
     if (own) {
@@ -666,6 +775,34 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
         }
     }
     if (r == 0 && tid == 0) *na.d_step = t;
+    cluster.sync();  // no CTA leaves while a peer's last stores may target it
+}
+
+// Setup: delay bit-planes of the cluster loop, [cs][P][D][wn4]: bit b of word w
+// of plane d is set when pre 32 w + b has a synapse of delay d + 1 onto post
+// r P + p (one-weight nets: a synapse is a non-zero weight).
+template <typename WT>
+__global__ void k_cluster_masks(DenseArgs da, int nl, int P, int cs, int D, uint32_t* masks) {
+    const int wn4 = ((da.n + 31) / 32 + 15) & ~15;
+    const int64_t total = static_cast<int64_t>(cs) * P * D * wn4;
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int w = static_cast<int>(k % wn4);
+        const int64_t rest = k / wn4;
+        const int d = static_cast<int>(rest % D);
+        const int64_t rp = rest / D;
+        const int pp = static_cast<int>(rp % P), r = static_cast<int>(rp / P);
+        const int j = r * P + pp;
+        uint32_t bits = 0;
+        if (j < nl)
+            for (int b = 0; b < 32; ++b) {
+                const int i = 32 * w + b;
+                if (i >= da.n) break;
+                const int64_t e = static_cast<int64_t>(i) * da.pitch + j;
+                if (static_cast<const WT*>(da.w)[e] != WT(0) && (da.delay ? da.delay[e] : 1) == d + 1) bits |= 1u << b;
+            }
+        masks[k] = bits;
+    }
 }
 
 // Setup: rotation codes of the cluster loop, [cs][n][P]; a synapse is a
@@ -812,64 +949,100 @@ void launch_persistent_dense(const NeuronArgs& na, const HistArgs& h, const Dens
 }
 
 
-size_t cluster_smem_bytes(int n, int P) {
-    const int npad = (n + 3) & ~3;
-    return static_cast<size_t>(n) * P + static_cast<size_t>(2) * npad * 4 + static_cast<size_t>(kClThreads) * 4 * 4 +
-           static_cast<size_t>(P) * 8;
+static const void* cluster_kernel(bool f64, int P, int D) {
+#define SNB_CLK(WT, DD)                                                                  \
+    switch (P) {                                                                         \
+        case 32: return reinterpret_cast<const void*>(k_cluster_count<WT, 32, DD>);      \
+        case 64: return reinterpret_cast<const void*>(k_cluster_count<WT, 64, DD>);      \
+        case 96: return reinterpret_cast<const void*>(k_cluster_count<WT, 96, DD>);      \
+        default: return reinterpret_cast<const void*>(k_cluster_count<WT, 128, DD>);     \
+    }
+    if (D == 16 && P > 64) return nullptr;  // P * D > 1024: not planned
+    if (f64) {
+        if (D == 8) SNB_CLK(double, 8)
+        if (D == 16) return P == 32 ? reinterpret_cast<const void*>(k_cluster_count<double, 32, 16>)
+                                    : reinterpret_cast<const void*>(k_cluster_count<double, 64, 16>);
+        SNB_CLK(double, 0)
+    }
+    if (D == 8) SNB_CLK(float, 8)
+    if (D == 16) return P == 32 ? reinterpret_cast<const void*>(k_cluster_count<float, 32, 16>)
+                                : reinterpret_cast<const void*>(k_cluster_count<float, 64, 16>);
+    SNB_CLK(float, 0)
+#undef SNB_CLK
 }
 
-// Cluster size for a net of n posts: 16 CTAs (non-portable) when the device
-// runs such a cluster, else 8; 0 when the codes do not fit shared memory.
-int cluster_plan(int n, int nl, bool f64, int* P_out) {
+// Cluster shape for a net of n posts: 16 CTAs (non-portable) when the device
+// runs such a cluster, else 8; delay bit-planes (D = 8 / 16) when the delays
+// and the planes fit, else rotation codes (D = 0, delays <= 31).  0: no fit.
+int cluster_plan(int n, int nl, bool f64, int dmax, int* P_out, int* D_out) {
     int dev = 0, optin = 0;
     check(cudaGetDevice(&dev), "cudaGetDevice");
     check(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
+    const char* ck = std::getenv("SNB_CLUSTER_CODES");  // A/B knob: 1 = rotation codes only
     for (int cs : {16, 8}) {
         const int P = ((nl + cs - 1) / cs + 31) / 32 * 32;
-        if (P > 256) continue;  // 1024 threads: >= 16 row lanes of 4 posts, >= 4 reduction threads per post
-        const size_t smem = cluster_smem_bytes(n, P);
-        if (smem > static_cast<size_t>(optin)) continue;
-        auto kern = f64 ? reinterpret_cast<const void*>(k_cluster_count<double>)
-                        : reinterpret_cast<const void*>(k_cluster_count<float>);
-        if (cs > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
-            cudaGetLastError();
-            continue;
+        if (P != 32 && P != 64 && P != 96 && P != 128) continue;  // instantiated widths
+        int cands[3] = {dmax <= 8 ? 8 : 16, 0, -1};
+        if (dmax > 16 || (ck && std::string(ck) == "1")) cands[0] = 0, cands[1] = -1;
+        for (int D : cands) {
+            if (D < 0) break;
+            if (D > 0 && P * D > kClThreads) continue;
+            const size_t smem = cl_layout(n, P, D).total;
+            if (smem > static_cast<size_t>(optin)) continue;
+            const void* kern = cluster_kernel(f64, P, D);
+            if (cs > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+                  "k_cluster_count smem attribute");
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(cs);
+            cfg.blockDim = dim3(kClThreads);
+            cfg.dynamicSmemBytes = smem;
+            cudaLaunchAttribute at{};
+            at.id = cudaLaunchAttributeClusterDimension;
+            at.val.clusterDim.x = cs;
+            at.val.clusterDim.y = 1;
+            at.val.clusterDim.z = 1;
+            cfg.attrs = &at;
+            cfg.numAttrs = 1;
+            int clusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            if (clusters < 1) continue;
+            *P_out = P;
+            *D_out = D;
+            return cs;
         }
-        check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-              "k_cluster_count smem attribute");
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(cs);
-        cfg.blockDim = dim3(kClThreads);
-        cfg.dynamicSmemBytes = smem;
-        cudaLaunchAttribute at{};
-        at.id = cudaLaunchAttributeClusterDimension;
-        at.val.clusterDim.x = cs;
-        at.val.clusterDim.y = 1;
-        at.val.clusterDim.z = 1;
-        cfg.attrs = &at;
-        cfg.numAttrs = 1;
-        int clusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess) {
-            cudaGetLastError();
-            continue;
-        }
-        if (clusters < 1) continue;
-        *P_out = P;
-        return cs;
     }
     return 0;
 }
 
-void launch_cluster_codes(const DenseArgs& da, int nl, int P, int cs, uint8_t* codes, bool f64, cudaStream_t s) {
-    const int64_t total = static_cast<int64_t>(cs) * da.n * P;
+size_t cluster_table_bytes(int n, int P, int D, int cs) {
+    const ClLayout L = cl_layout(n, P, D);
+    return (L.ex - L.code) * cs;
+}
+
+void launch_cluster_table(const DenseArgs& da, int nl, int P, int D, int cs, void* table, bool f64, cudaStream_t s) {
+    const int64_t total = D == 0 ? static_cast<int64_t>(cs) * da.n * P
+                                 : static_cast<int64_t>(cs) * P * D * ((((da.n + 31) / 32) + 15) & ~15);
     const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-    if (f64) k_cluster_codes<double><<<grid, 256, 0, s>>>(da, nl, P, cs, codes);
-    else k_cluster_codes<float><<<grid, 256, 0, s>>>(da, nl, P, cs, codes);
-    check(cudaGetLastError(), "k_cluster_codes");
+    if (D == 0) {
+        if (f64) k_cluster_codes<double><<<grid, 256, 0, s>>>(da, nl, P, cs, static_cast<uint8_t*>(table));
+        else k_cluster_codes<float><<<grid, 256, 0, s>>>(da, nl, P, cs, static_cast<uint8_t*>(table));
+    } else {
+        if (f64) k_cluster_masks<double><<<grid, 256, 0, s>>>(da, nl, P, cs, D, static_cast<uint32_t*>(table));
+        else k_cluster_masks<float><<<grid, 256, 0, s>>>(da, nl, P, cs, D, static_cast<uint32_t*>(table));
+    }
+    check(cudaGetLastError(), "cluster table");
 }
 
 void launch_cluster_count(const NeuronArgs& na, const ClusterArgs& ca, bool f64, int steps, cudaStream_t s) {
-    const size_t smem = cluster_smem_bytes(na.n, ca.P);
+    const void* kern = cluster_kernel(f64, ca.P, ca.D);
+    const size_t smem = cl_layout(na.n, ca.P, ca.D).total;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ca.cs);
     cfg.blockDim = dim3(kClThreads);
@@ -882,8 +1055,11 @@ void launch_cluster_count(const NeuronArgs& na, const ClusterArgs& ca, bool f64,
     at.val.clusterDim.z = 1;
     cfg.attrs = &at;
     cfg.numAttrs = 1;
-    if (f64) check(cudaLaunchKernelEx(&cfg, k_cluster_count<double>, na, ca, steps), "k_cluster_count");
-    else check(cudaLaunchKernelEx(&cfg, k_cluster_count<float>, na, ca, steps), "k_cluster_count");
+    NeuronArgs a0 = na;
+    ClusterArgs a1 = ca;
+    int a2 = steps;
+    void* args[] = {&a0, &a1, &a2};
+    check(cudaLaunchKernelExC(&cfg, kern, args), "k_cluster_count");
 }
 
 }  // namespace snb

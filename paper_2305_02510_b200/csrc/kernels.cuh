@@ -234,8 +234,9 @@ struct ColArgs {
 };
 // Cluster loop (k_cluster_count): static one-weight nets without STDP, delays <= 31
 struct ClusterArgs {
-    const uint8_t* codes;          // [cs][n][P] rotation codes
-    int32_t P;                     // posts per CTA (32, 64 or 128)
+    const uint8_t* codes;          // per-CTA table: [n][P] rotation codes (D = 0) or [P][D][wn4] delay planes
+    int32_t P;                     // posts per CTA (32, 64, 96 or 128)
+    int32_t D;                     // delay planes (8 / 16), 0 = rotation codes
     int32_t cs;                    // CTAs in the cluster
     double w0;                     // the one weight
     uint64_t* hist2;               // [2][n], ColArgs layout
@@ -243,8 +244,9 @@ struct ClusterArgs {
     unsigned long long* active_count;
     uint64_t dmask;
 };
-int cluster_plan(int n, int nl, bool f64, int* P_out);
-void launch_cluster_codes(const DenseArgs& da, int nl, int P, int cs, uint8_t* codes, bool f64, cudaStream_t s);
+int cluster_plan(int n, int nl, bool f64, int dmax, int* P_out, int* D_out);
+size_t cluster_table_bytes(int n, int P, int D, int cs);
+void launch_cluster_table(const DenseArgs& da, int nl, int P, int D, int cs, void* table, bool f64, cudaStream_t s);
 void launch_cluster_count(const NeuronArgs& na, const ClusterArgs& ca, bool f64, int steps, cudaStream_t s);
 int persistent_cols_max_ctas(bool f64, bool stdp, bool delay, int width);
 void launch_persistent_cols(const NeuronArgs& na, const DenseArgs& da, const ColArgs& ca, bool f64, bool stdp,

@@ -221,6 +221,16 @@ def test_cfg2_cluster_loop_selected_and_exact():
     eng.close()
     assert st["sweep_kernel"] == 14
     assert _digest(s, n) == e["digest"]
+    os.environ["SNB_CLUSTER_CODES"] = "1"  # rotation codes instead of delay bit-planes
+    try:
+        eng = _generated(e, 1, by_syn=True)
+        st = eng.stats()
+        s, n = eng.raster()
+        eng.close()
+    finally:
+        del os.environ["SNB_CLUSTER_CODES"]
+    assert st["sweep_kernel"] == 14
+    assert _digest(s, n) == e["digest"]
     os.environ["SNB_PERSIST_KERNEL"] = "cols"
     try:
         eng = _generated(e, 1, by_syn=True)
@@ -234,10 +244,10 @@ def test_cfg2_cluster_loop_selected_and_exact():
 
 
 @pytest.mark.parametrize("n,dmax,precision,abm,chunks", [
-    (300, 31, "f64", False, (40, 1, 19)),   # 32-post CTAs, longest delay, chunked calls
-    (1000, 8, "f32", True, (60,)),          # stochastic agents (ABM) in the cluster
-    (1500, 4, "f32", False, (25, 25)),      # 96-post CTAs (row lanes and reduction threads not powers of two)
-    (777, 12, "f64", False, (30,)),         # ragged last CTA
+    (300, 31, "f64", False, (40, 1, 19)),   # 32-post CTAs, delays > 16: rotation codes, chunked calls
+    (1000, 8, "f32", True, (60,)),          # 8 delay bit-planes, stochastic agents (ABM)
+    (1500, 4, "f32", False, (25, 25)),      # 96-post CTAs: 768 (post, plane) pairs
+    (777, 12, "f64", False, (30,)),         # 16 delay bit-planes, ragged last CTA
 ])
 def test_cluster_loop_matches_oracle(n, dmax, precision, abm, chunks):
     """k_cluster_count on host-built one-weight nets (leak, refractory,
