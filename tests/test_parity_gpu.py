@@ -299,6 +299,45 @@ def test_cluster_loop_matches_oracle(n, dmax, precision, abm, chunks):
     assert close_rel(mem, o["membrane"])
 
 
+@pytest.mark.parametrize("stream_io", [False, True])
+def test_cluster_loop_trace_and_stream_io(stream_io):
+    """k_cluster_count with the membrane trace recorded and with stream I/O (the
+    raster words stored into pinned host memory): trace rows, raster and final
+    membranes equal the oracle's, over two simulate() calls."""
+    from oracle import bridge as B
+    from paper_2305_02510_b200.engine import MatEngine
+    from paper_2305_02510_b200.netgen import RandomStream, erdos_renyi_arrays, scenario_stimulus
+    n, seed, steps = 640, 23, 48
+    pre, post = erdos_renyi_arrays(n, 0.2, seed)
+    m = len(pre)
+    rs = RandomStream(seed, 9)
+    delay = (1 + rs.below_np(np.arange(m, dtype=np.uint64), 6)).astype(np.int32)
+    ki = np.arange(n, dtype=np.uint64)
+    thr = 8.0 + 4.0 * rs.unit_np(ki + np.uint64(m))
+    leak = 0.5 * rs.unit_np(ki + np.uint64(m + n))
+    arrays = {"threshold": thr, "leak": leak, "reset": np.zeros(n), "refractory": (ki % 2).astype(np.int32),
+              "axonal": np.zeros(n, np.int32), "pre": pre, "post": post, "weight": np.full(m, 0.25),
+              "delay": delay, "stdp": np.zeros(m, np.uint8)}
+    stim = scenario_stimulus(n, steps, seed, count=30, period=2, amplitude=12.0).to_arrays()
+    o = B.run_oracle(arrays, steps, stim, None, True)
+    eng = MatEngine(storage=1, precision="f64", record_membrane=True, stream_io=stream_io)
+    eng.add_neurons(thr, leak, arrays["reset"], arrays["refractory"], arrays["axonal"])
+    eng.add_synapses(pre, post, arrays["weight"], delay, None)
+    eng.setup()
+    eng.add_stimulus(*stim)
+    eng.simulate(20)
+    eng.simulate(steps - 20)
+    s, q = eng.raster()
+    st = eng.stats()
+    tr = eng.membrane_trace()
+    mem = eng.membrane()
+    eng.close()
+    assert st["sweep_kernel"] == 14
+    assert len(o["steps"]) > 500
+    assert np.array_equal(s, o["steps"]) and np.array_equal(q, o["neurons"])
+    assert close_rel(tr, o["membrane_trace"]) and close_rel(mem, o["membrane"])
+
+
 @pytest.mark.parametrize("storage", [0, 1, 2])
 def test_long_stdp_window_multiword_history(storage):
     """StdpConfig windows are arbitrary (model.cpp:104-117): window 70 with
