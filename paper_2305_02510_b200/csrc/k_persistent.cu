@@ -555,6 +555,11 @@ __host__ __device__ inline ClLayout cl_layout(int n, int P, int D) {
     return L;
 }
 
+#ifndef SNB_CL_MREG
+#define SNB_CL_MREG 1
+#endif
+constexpr int kClMregs = 4;  // uint4 mask registers per thread (16 words)
+
 template <typename WT, int P, int D>
 __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, ClusterArgs ca, int steps) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -625,6 +630,22 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
     };
     stim_bounds(t);
     const WT w0 = static_cast<WT>(ca.w0);
+    // delay planes: when a thread's slice is exactly kClMregs uint4 (cfg2: 1000 pres,
+    // 2 threads per (post, plane)), it stays in registers for the whole call
+    uint4 mreg[kClMregs];
+#pragma unroll
+    for (int k = 0; k < kClMregs; ++k) mreg[k] = make_uint4(0u, 0u, 0u, 0u);
+    if (D > 0 && SNB_CL_MREG) {
+        constexpr int PAIRS = P * (D > 0 ? D : 1);
+        constexpr int T = kClThreads / PAIRS >= 4 ? 4 : kClThreads / PAIRS >= 2 ? 2 : 1;
+        if (tid < PAIRS * T && wn4 / T == 4 * kClMregs) {
+            const int pi = tid / T, part = tid % T;
+            const int pp = pi / (D > 0 ? D : 1), d = pi % (D > 0 ? D : 1);
+            const uint4* m4 = reinterpret_cast<const uint4*>(s_mask + (pp * D + d) * wn4 + part * (wn4 / T));
+#pragma unroll
+            for (int k = 0; k < kClMregs; ++k) mreg[k] = m4[k];
+        }
+    }
     for (int s = 0; s < steps; ++s, ++t) {
         const int cur = t & 1;
         if (tid == 0) mbar_arrive_expect_tx(&s_bar[cur], tx_bytes);
@@ -706,11 +727,19 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
                 const int pi = tid / T, part = tid % T;
                 const int pp = pi / (D > 0 ? D : 1), d = pi % (D > 0 ? D : 1);
                 const int per_part = wn4 / T;  // multiple of 4
-                const uint4* m4 = reinterpret_cast<const uint4*>(s_mask + (pp * D + d) * wn4 + part * per_part);
                 const uint4* e4 = reinterpret_cast<const uint4*>(s_ex + (cur * D + d) * wn4 + part * per_part);
-                for (int k = 0; k < per_part / 4; ++k) {
-                    const uint4 m = m4[k], e = e4[k];
-                    sum += __popc(m.x & e.x) + __popc(m.y & e.y) + __popc(m.z & e.z) + __popc(m.w & e.w);
+                if (SNB_CL_MREG && per_part == 4 * kClMregs) {  // mask words in registers for the call
+#pragma unroll
+                    for (int k = 0; k < kClMregs; ++k) {
+                        const uint4 m = mreg[k], e = e4[k];
+                        sum += __popc(m.x & e.x) + __popc(m.y & e.y) + __popc(m.z & e.z) + __popc(m.w & e.w);
+                    }
+                } else {
+                    const uint4* m4 = reinterpret_cast<const uint4*>(s_mask + (pp * D + d) * wn4 + part * per_part);
+                    for (int k = 0; k < per_part / 4; ++k) {
+                        const uint4 m = m4[k], e = e4[k];
+                        sum += __popc(m.x & e.x) + __popc(m.y & e.y) + __popc(m.z & e.z) + __popc(m.w & e.w);
+                    }
                 }
 #pragma unroll
                 for (int o = (D * T) / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
