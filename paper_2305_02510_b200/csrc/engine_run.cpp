@@ -16,6 +16,8 @@
 
 namespace snb {
 
+static int words_of(int n) { return (n + 31) / 32; }
+
 // One k_tiny launch per chunk of steps whose stimulus fits next to the state.
 void Engine::run_tiny(int t0, int steps, uint32_t* raster, double* trace, bool host_io) {
     TinyArgs a{};
@@ -47,6 +49,15 @@ void Engine::run_tiny(int t0, int steps, uint32_t* raster, double* trace, bool h
     a.abm = abm_ ? 1 : 0;
     a.fire_p = any_stochastic_ ? d_firep_.as<double>() : nullptr;
     a.agent_key = any_stochastic_ ? d_akey_.as<uint64_t>() : nullptr;
+    {   // count mode: one weight, unit delays, no plasticity, <= 256 neurons
+        double w0 = 0.0;
+        const char* tc = std::getenv("SNB_TINY_COUNT");  // A/B knob: 0 walks the in-lists
+        if (!stdp_on_ && dmax_ == 1 && words_of(n_) <= tiny_count_words_max() && !(tc && std::string(tc) == "0") &&
+            uniform_weight(&w0)) {
+            a.count_words = words_of(n_);
+            a.w0 = f64_ ? w0 : static_cast<double>(static_cast<float>(w0));
+        }
+    }
     const size_t limit = static_cast<size_t>(tiny_max_smem());
     const int words = std::max(nl_words_, 1);
     const int table = static_cast<int>(hs_off_.size()) - 1;  // steps covered by the stimulus CSR

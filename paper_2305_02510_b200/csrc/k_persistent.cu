@@ -58,6 +58,7 @@ __host__ __device__ inline TinyLayout tiny_layout(const TinyArgs& a) {
 // weights, history words issued together): 0.91e6 with branches, 0.97e6
 // with selects (every fp64 add executed)
 constexpr int kTinyHistRegs = SNB_TINY_HREGS;
+constexpr int kTinyCountWords = 8;  // count mode: nets of <= 256 neurons
 
 __device__ __forceinline__ bool tiny_bit(const uint8_t* buf, uint32_t mq) {
     const uint32_t word = *reinterpret_cast<const uint32_t*>(buf + (mq >> 5));
@@ -132,6 +133,25 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
 #pragma unroll
     for (int k = 0; k < kTinyHistRegs; ++k) hr[k] = (hreg && k < hw2 && j < np) ? hist[k * np + j] : 0u;
     unsigned long long spikes = 0;
+    // count mode: this post's in-list as a pre bitmask in registers, the previous
+    // step's spike words double-buffered in shared memory
+    __shared__ uint32_t s_spk[2][kTinyCountWords];
+    const bool cmode = !STDP && a.count_words > 0;
+    uint32_t cm[kTinyCountWords];
+#pragma unroll
+    for (int k = 0; k < kTinyCountWords; ++k) cm[k] = 0u;
+    if (cmode) {
+        if (own)
+            for (uint32_t q = q0; q < q1; ++q) {
+                const uint32_t i = (meta[q] >> 5) >> 2;  // byte offset of pre i's word 0 (delay 1: bit 0)
+#pragma unroll
+                for (int k = 0; k < kTinyCountWords; ++k)
+                    if (static_cast<uint32_t>(k) == (i >> 5)) cm[k] |= 1u << (i & 31);
+            }
+        const uint32_t w0 = __ballot_sync(0xffffffffu, own && (hist[j] & 1u));  // spikes of step t0 - 1
+        if ((tid & 31) == 0 && (tid >> 5) < kTinyCountWords) s_spk[0][tid >> 5] = w0;
+        __syncthreads();
+    }
     for (int s = 0; s < a.steps; ++s) {
         const int cur = s & 1;
         const uint8_t* hc = sm + L.hist + cur * hbuf;        // history through t-1
@@ -142,10 +162,19 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
             // the step's stimulus, threshold, refractory (mat_engine.cpp:160-198)
             // MAT: u = leak(v) + w...; ABM: pending = 0.0 + w..., u = leak(v) + (pending + ext)
             double u = a.abm ? 0.0 : leak_toward(v, leak, rst);
+            if (cmode) {
+                int k = 0;
+#pragma unroll
+                for (int wd = 0; wd < kTinyCountWords; ++wd)
+                    if (wd < a.count_words) k += __popc(cm[wd] & s_spk[cur][wd]);
+                const double w0 = a.w0;
+                for (int c = 0; c < k; ++c) u += w0;  // ascending-pre sum of equal weights
+            } else {
 #pragma unroll 4
-            for (uint32_t q = q0; q < q1; ++q) {
-                const uint32_t mq = meta[q];
-                if (tiny_bit(hc, mq)) u += static_cast<double>(w[q]);  // WS = double unless STDP
+                for (uint32_t q = q0; q < q1; ++q) {
+                    const uint32_t mq = meta[q];
+                    if (tiny_bit(hc, mq)) u += static_cast<double>(w[q]);  // WS = double unless STDP
+                }
             }
             int lo = st_off[s], hi = st_off[s + 1];
             if (hi > lo) {
@@ -178,6 +207,7 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
         if ((tid & 31) == 0 && (tid >> 5) < words) {
             a.raster[static_cast<int64_t>(s) * words + (tid >> 5)] = word;
             spikes += __popc(word);
+            if (cmode) s_spk[cur ^ 1][tid >> 5] = word;  // read after the step's __syncthreads
         }
         // (2) own history row into the other buffer (+ own STDP traces)
         if (j < np) {
@@ -855,6 +885,8 @@ __global__ void k_cluster_codes(DenseArgs da, int nl, int P, int cs, uint8_t* co
 }  // namespace
 
 size_t tiny_smem_bytes(const TinyArgs& a) { return tiny_layout(a).total; }
+
+int tiny_count_words_max() { return kTinyCountWords; }
 
 int tiny_max_smem() {
     int dev = 0, v = 0;

@@ -302,9 +302,16 @@ struct TinyArgs {
     int32_t abm;
     const double* fire_p;      // [n] or null
     const uint64_t* agent_key; // [n]
+    // one-weight unit-delay nets without STDP: each post's in-list as a bitmask
+    // over the pres (count_words words, <= kTinyCountWords), the input as
+    // popc(mask & previous spike words) sequential additions of w0 (the
+    // reference's ascending-pre sum of equal weights, bit for bit); 0 = off
+    int32_t count_words;
+    double w0;
 };
 size_t tiny_smem_bytes(const TinyArgs& a);
 int tiny_max_smem();
+int tiny_count_words_max();
 void launch_tiny(const TinyArgs& a, cudaStream_t s);
 
 // ---- on-device Erdos-Renyi generation (netgen.cpp:36-51 semantics) ----
