@@ -91,3 +91,12 @@ def test_stdp_defaults_match_reference_defaults():
         rlo, rhi = C.c_double(), C.c_double()
         lib.ref_stdp_defaults(C.byref(rw), rap, ram, C.byref(rlo), C.byref(rhi))
         assert list(rap) == list(ap) and list(ram) == list(am)
+
+
+def test_missing_engine_library_fails_loudly(tmp_path):
+    """No CPU fallback: without libsnmat.so the package refuses to import."""
+    env = dict(os.environ, SNB_LIB=str(tmp_path / "absent" / "libsnmat.so"))
+    r = subprocess.run(["python", "-c", "import paper_2305_02510_b200"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "is missing" in r.stderr and "ImportError" in r.stderr
