@@ -43,8 +43,8 @@ void Engine::p2p_get_handles(uint8_t* out, int64_t cap) {
 void Engine::set_peer_tables(const std::vector<uint32_t*>& bits, const std::vector<int32_t*>& flags) {
     d_peer_bits_.alloc(bits.size() * sizeof(uint32_t*));
     d_peer_flags_.alloc(flags.size() * sizeof(int32_t*));
-    cuda_check(cudaMemcpy(d_peer_bits_.p, bits.data(), bits.size() * sizeof(uint32_t*), cudaMemcpyHostToDevice), "peer table");
-    cuda_check(cudaMemcpy(d_peer_flags_.p, flags.data(), flags.size() * sizeof(int32_t*), cudaMemcpyHostToDevice), "peer table");
+    h2d_sync(d_peer_bits_.p, bits.data(), bits.size() * sizeof(uint32_t*), "peer table");
+    h2d_sync(d_peer_flags_.p, flags.data(), flags.size() * sizeof(int32_t*), "peer table");
     p2p_ = true;
 }
 

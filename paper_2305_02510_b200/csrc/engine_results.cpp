@@ -212,7 +212,7 @@ void Engine::reset_stats() {
     stats_.kernel_launches = 0;
     stats_.sweep_bytes_total = 0.0;
     steps_at_reset_ = t_;
-    if (setup_done_) cuda_check(cudaMemset(d_spikes_.as<unsigned long long>() + 1, 0, 8), "reset");
+    if (setup_done_) cuda_check(cudaMemsetAsync(d_spikes_.as<unsigned long long>() + 1, 0, 8, stream_), "reset");
 }
 
 }  // namespace snb

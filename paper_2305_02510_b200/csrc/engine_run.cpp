@@ -608,7 +608,7 @@ void Engine::get_spike_words(uint32_t* out, int64_t words) {
 void Engine::put_spike_words(int32_t first_word, const uint32_t* w, int64_t count) {
     require_setup("sn_put_spike_words");
     if (first_word < 0 || first_word + count > words_) throw InvalidArgument("sn_put_spike_words: range outside the bitmask");
-    cuda_check(cudaMemcpy(d_bits_.as<uint32_t>() + first_word, w, static_cast<size_t>(count) * 4, cudaMemcpyHostToDevice), "bits H2D");
+    h2d_sync(d_bits_.as<uint32_t>() + first_word, w, static_cast<size_t>(count) * 4, "bits H2D");
 }
 
 void Engine::step_finish() {
