@@ -31,6 +31,11 @@ void cuda_check(cudaError_t err, const char* what) {
     throw CudaError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(err));
 }
 
+void Engine::d2h(void* dst, const void* src, size_t bytes, const char* what) const {
+    cuda_check(cudaStreamSynchronize(stream_), what);
+    cuda_check(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), what);
+}
+
 void DevBuf::alloc(size_t b) {
     release();
     if (b == 0) b = 16;

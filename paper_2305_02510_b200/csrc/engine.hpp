@@ -140,6 +140,10 @@ private:
 
     sn_options opt_;
     cudaStream_t stream_ = nullptr;
+    // Device-to-host read ordered after all work queued on stream_ (a plain
+    // cudaMemcpy runs on the legacy stream, which a non-blocking stream_ does
+    // not synchronise with).
+    void d2h(void* dst, const void* src, size_t bytes, const char* what) const;
     bool setup_done_ = false;
 
     // ---- model (host, as given) ----

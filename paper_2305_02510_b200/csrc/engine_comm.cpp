@@ -97,7 +97,7 @@ void Engine::p2p_connect_local(Engine* const* engines, int32_t world) {
 void Engine::check_exchange_error() {
     if (!p2p_) return;
     int32_t err = 0;
-    cuda_check(cudaMemcpy(&err, d_err_.p, 4, cudaMemcpyDeviceToHost), "exchange error D2H");
+    d2h(&err, d_err_.p, 4, "exchange error D2H");
     if (err) throw NcclError("peer-to-peer spike exchange timed out (a peer rank stopped publishing)");
 }
 

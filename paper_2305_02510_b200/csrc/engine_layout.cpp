@@ -615,7 +615,7 @@ bool Engine::build_c16() {
 bool Engine::build_sparse_tma_plan(int ctas) {
     const int64_t P = static_cast<int64_t>(nblocks_) * nl_;
     std::vector<int64_t> off(static_cast<size_t>(P) + 1);
-    cuda_check(cudaMemcpy(off.data(), d_off_.p, off.size() * 8, cudaMemcpyDeviceToHost), "offsets D2H");
+    d2h(off.data(), d_off_.p, off.size() * 8, "offsets D2H");
     const int64_t Q = off[P];
     const int64_t E = sparse_tma_stage_entries();
     const int NB = sparse_tma_max_boundaries();

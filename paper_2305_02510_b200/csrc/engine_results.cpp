@@ -106,7 +106,7 @@ void Engine::clear_raster() {
 void Engine::get_membrane(double* out, int64_t count) {
     require_setup("sn_get_membrane");
     if (count < nl_) throw InvalidArgument("sn_get_membrane: buffer smaller than the local neuron count");
-    if (nl_) cuda_check(cudaMemcpy(out, d_v_.p, static_cast<size_t>(nl_) * 8, cudaMemcpyDeviceToHost), "membrane D2H");
+    if (nl_) d2h(out, d_v_.p, static_cast<size_t>(nl_) * 8, "membrane D2H");
 }
 
 int64_t Engine::trace_rows() { return trace_rows_; }
@@ -123,11 +123,11 @@ void Engine::get_synapse_weights(double* out, int64_t count) {
     cuda_check(cudaStreamSynchronize(stream_), "sync");
     const size_t esz = f64_ ? 8 : 4;
     std::vector<uint8_t> host(d_w_.bytes);
-    cuda_check(cudaMemcpy(host.data(), d_w_.p, d_w_.bytes, cudaMemcpyDeviceToHost), "weights D2H");
+    d2h(host.data(), d_w_.p, d_w_.bytes, "weights D2H");
     std::vector<uint32_t> meta;
     if (!dense_ && !dict_.empty()) {
         meta.resize(static_cast<size_t>(sparse_elems_));
-        if (!meta.empty()) cuda_check(cudaMemcpy(meta.data(), d_meta_.p, meta.size() * 4, cudaMemcpyDeviceToHost), "meta D2H");
+        if (!meta.empty()) d2h(meta.data(), d_meta_.p, meta.size() * 4, "meta D2H");
     }
     for (size_t s = 0; s < pre_.size(); ++s) {
         if (slot_[s] < 0) { out[s] = 0.0; continue; }
@@ -145,7 +145,7 @@ void Engine::get_weight_matrix(double* out, int64_t count) {
     std::fill(out, out + static_cast<int64_t>(n_) * nl_, 0.0);
     const size_t esz = f64_ ? 8 : 4;
     std::vector<uint8_t> host(d_w_.bytes);
-    cuda_check(cudaMemcpy(host.data(), d_w_.p, d_w_.bytes, cudaMemcpyDeviceToHost), "weights D2H");
+    d2h(host.data(), d_w_.p, d_w_.bytes, "weights D2H");
     auto get = [&](int64_t q) {
         return esz == 8 ? reinterpret_cast<const double*>(host.data())[q]
                         : static_cast<double>(reinterpret_cast<const float*>(host.data())[q]);
@@ -158,8 +158,8 @@ void Engine::get_weight_matrix(double* out, int64_t count) {
     } else {
         std::vector<int64_t> off(static_cast<size_t>(nblocks_) * nl_ + 1);
         std::vector<uint32_t> meta(static_cast<size_t>(sparse_elems_));
-        cuda_check(cudaMemcpy(off.data(), d_off_.p, off.size() * 8, cudaMemcpyDeviceToHost), "off D2H");
-        if (!meta.empty()) cuda_check(cudaMemcpy(meta.data(), d_meta_.p, meta.size() * 4, cudaMemcpyDeviceToHost), "meta D2H");
+        d2h(off.data(), d_off_.p, off.size() * 8, "off D2H");
+        if (!meta.empty()) d2h(meta.data(), d_meta_.p, meta.size() * 4, "meta D2H");
         for (int b = 0; b < nblocks_; ++b)
             for (int p = 0; p < nl_; ++p)
                 for (int64_t q = off[static_cast<size_t>(b) * nl_ + p]; q < off[static_cast<size_t>(b) * nl_ + p + 1]; ++q) {
@@ -173,7 +173,7 @@ void Engine::get_weight_matrix(double* out, int64_t count) {
 void Engine::get_stats(sn_stats* out) {
     if (setup_done_) {
         unsigned long long c[2] = {0, 0};
-        cuda_check(cudaMemcpy(c, d_spikes_.p, 16, cudaMemcpyDeviceToHost), "stats D2H");
+        d2h(c, d_spikes_.p, 16, "stats D2H");
         stats_.spike_count = static_cast<int64_t>(c[0]);
         // algorithmic bytes: every visited row (dense) or every stored synapse (sparse pull)
         if (dense_) {

@@ -568,7 +568,7 @@ void Engine::simulate(int32_t steps) {
         const size_t cnt = static_cast<size_t>(steps) * nl_;
         const size_t old = trace_.size();
         trace_.resize(old + cnt);
-        if (cnt) cuda_check(cudaMemcpy(trace_.data() + old, d_trace_.p, cnt * 8, cudaMemcpyDeviceToHost), "trace D2H");
+        if (cnt) d2h(trace_.data() + old, d_trace_.p, cnt * 8, "trace D2H");
         trace_rows_ += steps;
     }
     t_ += steps;
@@ -602,7 +602,7 @@ void Engine::step_local() {
 void Engine::get_spike_words(uint32_t* out, int64_t words) {
     require_setup("sn_get_spike_words");
     if (words > words_) throw InvalidArgument("sn_get_spike_words: more words than the bitmask holds");
-    cuda_check(cudaMemcpy(out, d_bits_.p, static_cast<size_t>(words) * 4, cudaMemcpyDeviceToHost), "bits D2H");
+    d2h(out, d_bits_.p, static_cast<size_t>(words) * 4, "bits D2H");
 }
 
 void Engine::put_spike_words(int32_t first_word, const uint32_t* w, int64_t count) {
@@ -630,7 +630,7 @@ void Engine::step_finish() {
     if (opt_.record_membrane) {
         const size_t old = trace_.size();
         trace_.resize(old + nl_);
-        if (nl_) cuda_check(cudaMemcpy(trace_.data() + old, d_trace_.p, static_cast<size_t>(nl_) * 8, cudaMemcpyDeviceToHost), "trace D2H");
+        if (nl_) d2h(trace_.data() + old, d_trace_.p, static_cast<size_t>(nl_) * 8, "trace D2H");
         trace_rows_ += 1;
     }
     t_ += 1;
