@@ -213,12 +213,15 @@ def _collect(lib, r: Result, steps: int, with_state: bool = True) -> dict:
     return out
 
 
-def run_oracle(arrays, steps, stim=None, stdp=None, record_membrane=False) -> dict:
-    """mat_oracle.c: the plain-C restatement."""
+def run_oracle(arrays, steps, stim=None, stdp=None, record_membrane=False, f32_weights=False) -> dict:
+    """mat_oracle.c: the plain-C restatement.  f32_weights: the fp32 weight
+    storage model (every stored weight rounded to float once; all arithmetic
+    fp64) -- the engine's default precision must reproduce its weights bit
+    for bit."""
     lib = oracle_lib()
     p, keep = make_problem(arrays, steps, stim, stdp, record_membrane)
     r = Result()
-    lib.mat_oracle_run(C.byref(p), C.byref(r))
+    (lib.mat_oracle_run_f32w if f32_weights else lib.mat_oracle_run)(C.byref(p), C.byref(r))
     return _collect(lib, r, steps)
 
 
@@ -342,6 +345,28 @@ def ref_serialize_stdp(stdp) -> str:
 def ref_roundtrip_network(text: str) -> str:
     ref_lib().ref_roundtrip_network.argtypes = [C.c_char_p]
     return _ref_str("ref_roundtrip_network", text.encode())
+
+
+def ref_bench_run(n, p, seed, horizon, warmup, steps, stdp_on, storage=0, delay_max=1, by_index=False,
+                  delay_stream=0) -> dict:
+    """Reference CPU path at the given size (oracle/ref_shim.cpp ref_bench_run):
+    setup untimed, `warmup` untimed steps, `steps` timed steps (mat_step +
+    apply_stdp, or AbmWorld::step for delayed nets)."""
+    lib = ref_lib()
+    info = np.zeros(6)
+    step_s = np.zeros(max(1, steps))
+    r = Result()
+    dp = C.POINTER(C.c_double)
+    lib.ref_bench_run.argtypes = [C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                  C.c_int, C.c_int, C.c_uint64, dp, dp, C.POINTER(Result)]
+    lib.ref_bench_run(n, p, seed, horizon, warmup, steps, 1 if stdp_on else 0, storage, delay_max,
+                      1 if by_index else 0, delay_stream, info.ctypes.data_as(dp), step_s.ctypes.data_as(dp),
+                      C.byref(r))
+    out = _collect(lib, r, steps, with_state=False)
+    out.update({"setup_s": float(info[0]), "warmup_s": float(info[1]), "timed_s": float(info[2]),
+                "storage": {1: "dense", 0: "csr", -1: "abm"}[int(info[3])], "synapses": int(info[4]),
+                "peak_rss_gb": float(info[5]), "step_s": step_s[:steps].tolist()})
+    return out
 
 
 def ref_bench_scenario(n, p, seed, steps, stdp_on, storage=0) -> dict:

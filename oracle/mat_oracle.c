@@ -77,7 +77,20 @@ static void fail(orc_result* out, int status, const char* msg) {
 /* History lookup: s_i[tau], 0 for tau < 0 (nothing spiked before step 0). */
 #define HIST(tau, i) ((tau) < 0 ? 0 : hist[((tau) % H) * (int64_t)n + (i)])
 
-int mat_oracle_run(const orc_problem* p, orc_result* out) {
+/* f32w = 1: the engine's default fp32 weight storage as a model of the same
+ * algorithm -- every stored weight (initial and after each update) rounded to
+ * float once, everything else (traces, dw, w + dw, clamp, input sums) in fp64
+ * exactly as above.  Rounding is monotone, so RN(clamp(x)) = clamp(RN(x),
+ * RN(lo), RN(hi)): the engine's fp32 clamp gives the same stored value. */
+static int mat_oracle_impl(const orc_problem* p, orc_result* out, int f32w);
+
+int mat_oracle_run(const orc_problem* p, orc_result* out) { return mat_oracle_impl(p, out, 0); }
+
+int mat_oracle_run_f32w(const orc_problem* p, orc_result* out) { return mat_oracle_impl(p, out, 1); }
+
+#define STORE_W(x) (f32w ? (double)(float)(x) : (x))
+
+static int mat_oracle_impl(const orc_problem* p, orc_result* out, int f32w) {
     memset(out, 0, sizeof(*out));
     const int n = p->n;
     const int64_t m = p->m;
@@ -134,7 +147,7 @@ int mat_oracle_run(const orc_problem* p, orc_result* out) {
     double* dep = (double*)calloc((size_t)n, sizeof(double));
     double* potd = (double*)calloc((size_t)n * (size_t)dmax, sizeof(double));
     for (int i = 0; i < n; ++i) v[i] = p->reset[i];
-    for (int64_t s = 0; s < m; ++s) w[s] = p->weight[s];
+    for (int64_t s = 0; s < m; ++s) w[s] = STORE_W(p->weight[s]);
     if (p->record_membrane)
         out->membrane_trace = (double*)malloc(sizeof(double) * (size_t)T * (size_t)n);
 
@@ -210,7 +223,7 @@ int mat_oracle_run(const orc_problem* p, orc_result* out) {
                 double nw = w[s] + dw;
                 /* std::clamp(v, lo, hi): v < lo ? lo : hi < v ? hi : v */
                 nw = nw < p->w_min ? p->w_min : (p->w_max < nw ? p->w_max : nw);
-                w[s] = nw;
+                w[s] = STORE_W(nw);
             }
         }
     }

@@ -39,6 +39,17 @@ using namespace spikeforge;
 
 namespace {
 
+double peak_rss_gb() {  // VmHWM of this process
+    FILE* f = std::fopen("/proc/self/status", "r");
+    if (!f) return -1.0;
+    char line[256];
+    double kb = -1.0;
+    while (std::fgets(line, sizeof line, f))
+        if (std::strncmp(line, "VmHWM:", 6) == 0) kb = std::atof(line + 6);
+    std::fclose(f);
+    return kb / (1024.0 * 1024.0);
+}
+
 NetworkDef to_net(const orc_problem* p) {
     NetworkDef net;
     net.neurons.resize(static_cast<std::size_t>(p->n));
@@ -412,6 +423,92 @@ int ref_bench_scenario(int n, double p, uint64_t seed, int steps, int stdp_on, i
         }
         out->seconds =
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        out->spike_count = spikes;
+    });
+}
+
+// CPU reference arm at the full workload size: build_scenario(n, p, seed)
+// with a `horizon`-step protocol, mat_init with the reference's own storage
+// choice (storage 0 = Auto: CSR above 12,000 neurons, mat_engine.cpp:13,
+// 29-30) outside the clock; then `warmup` untimed steps (step 0 has no
+// propagation) and `steps` timed steps of mat_step (+ apply_stdp), each timed
+// with steady_clock (bench.cpp:24-50).  delay_max > 1 (delays
+// 1 + below_at(key, delay_max) on stream delay_stream, key = i*n + j or the
+// synapse index when by_index) runs the reference's native-delay path
+// instead: AbmWorld built outside the clock, AbmWorld::step timed
+// (abm_engine.cpp:146-206).  info[0..5] = {setup s, warm-up s, timed s,
+// dense storage (1/0, -1 for abm), synapses, peak RSS GB}; step_s[k] = time
+// of timed step k.
+int ref_bench_run(int n, double p, uint64_t seed, int horizon, int warmup, int steps, int stdp_on,
+                  int storage, int delay_max, int by_index, uint64_t delay_stream, double* info,
+                  double* step_s, orc_result* out) {
+    return guarded(out, [&] {
+        using clk = std::chrono::steady_clock;
+        const auto s0 = clk::now();
+        BenchScenario sc;
+        sc.neuron_count = n;
+        sc.connection_probability = p;
+        sc.steps = horizon;
+        sc.seed = seed;
+        ScenarioBundle b = build_scenario(sc);
+        const int64_t m = static_cast<int64_t>(b.net.synapses.size());
+        if (delay_max > 1) {
+            const RandomStream ds(seed, delay_stream);
+            for (std::size_t s = 0; s < b.net.synapses.size(); ++s) {
+                SynapseDef& y = b.net.synapses[s];
+                const uint64_t key = by_index ? static_cast<uint64_t>(s)
+                                              : static_cast<uint64_t>(y.pre) * static_cast<uint64_t>(n) + y.post;
+                y.delay = 1 + static_cast<int>(ds.below_at(key, static_cast<uint64_t>(delay_max)));
+            }
+        }
+        if (stdp_on) {
+            for (SynapseDef& s : b.net.synapses) s.stdp_enabled = true;
+            b.cfg.stdp = StdpConfig::defaults();
+        }
+        std::vector<std::vector<std::pair<int, double>>> per_step(static_cast<std::size_t>(horizon));
+        for (const StimulusEntry& e : b.stim.entries) per_step[e.step].emplace_back(e.neuron, e.amplitude);
+        std::vector<double> ext(static_cast<std::size_t>(n), 0.0);
+        long long spikes = 0;
+        auto run = [&](auto&& step_fn) {
+            info[0] = std::chrono::duration<double>(clk::now() - s0).count();
+            auto one = [&](int t) {
+                bool any = false;
+                for (const auto& [j, a] : per_step[t]) { ext[j] += a; any = true; }
+                const long long k = static_cast<long long>(step_fn(any).size());
+                for (const auto& [j, a] : per_step[t]) ext[j] = 0.0;
+                return k;
+            };
+            const auto w0 = clk::now();
+            for (int t = 0; t < warmup; ++t) one(t);
+            info[1] = std::chrono::duration<double>(clk::now() - w0).count();
+            const auto t0 = clk::now();
+            for (int k = 0; k < steps; ++k) {
+                const auto a = clk::now();
+                spikes += one(warmup + k);
+                step_s[k] = std::chrono::duration<double>(clk::now() - a).count();
+            }
+            info[2] = std::chrono::duration<double>(clk::now() - t0).count();
+        };
+        if (delay_max > 1) {
+            AbmWorld world(b.net, b.cfg);
+            b.net = NetworkDef{};
+            info[3] = -1;
+            run([&](bool any) -> const std::vector<int>& {
+                return world.step(any ? std::span<const double>(ext) : std::span<const double>());
+            });
+        } else {
+            MatState st = mat_init(b.net, b.cfg, to_storage(storage));
+            b.net = NetworkDef{};  // release the synapse list before timing
+            info[3] = st.weights.dense() ? 1 : 0;
+            run([&](bool) -> const std::vector<int>& {
+                const std::vector<int>& spiked = mat_step(st, ext);
+                if (b.cfg.stdp) apply_stdp(st, *b.cfg.stdp);
+                return spiked;
+            });
+        }
+        info[4] = static_cast<double>(m);
+        info[5] = peak_rss_gb();
+        out->seconds = info[2];
         out->spike_count = spikes;
     });
 }

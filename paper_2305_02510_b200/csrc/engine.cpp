@@ -351,7 +351,7 @@ void Engine::setup() {
     {
         int32_t f0, c0;
         partition(n_, 0, opt_.world, &f0, &c0);
-        part_ = std::max(c0, 32);
+        part_ = static_cast<int32_t>(round_up(std::max(c0, 1), 32));  // words_ covers the whole bitmask
     }
     nl_words_ = (nl_ + 31) / 32;
     words_ = opt_.world * (part_ / 32);
@@ -424,11 +424,11 @@ void Engine::setup() {
 
 void Engine::alloc_state() {
     std::vector<double> v(reset_.begin() + first_, reset_.begin() + first_ + nl_);
-    upload(d_v_, v);  // membrane = reset (mat_engine.cpp:143)
-    upload(d_thr_, std::vector<double>(thr_.begin() + first_, thr_.begin() + first_ + nl_));
-    upload(d_leak_, std::vector<double>(leak_.begin() + first_, leak_.begin() + first_ + nl_));
-    upload(d_reset_, std::vector<double>(reset_.begin() + first_, reset_.begin() + first_ + nl_));
-    upload(d_refr_, std::vector<int32_t>(refr_.begin() + first_, refr_.begin() + first_ + nl_));
+    upload(stream_, d_v_, v);  // membrane = reset (mat_engine.cpp:143)
+    upload(stream_, d_thr_, std::vector<double>(thr_.begin() + first_, thr_.begin() + first_ + nl_));
+    upload(stream_, d_leak_, std::vector<double>(leak_.begin() + first_, leak_.begin() + first_ + nl_));
+    upload(stream_, d_reset_, std::vector<double>(reset_.begin() + first_, reset_.begin() + first_ + nl_));
+    upload(stream_, d_refr_, std::vector<int32_t>(refr_.begin() + first_, refr_.begin() + first_ + nl_));
     d_cnt_.alloc(static_cast<size_t>(std::max(nl_, 1)) * 4);
     cuda_check(cudaMemsetAsync(d_cnt_.p, 0, d_cnt_.bytes, stream_), "memset");
     const size_t wbytes = static_cast<size_t>(std::max(words_, (n_ + 31) / 32)) * 4;
@@ -436,6 +436,10 @@ void Engine::alloc_state() {
     d_active_.alloc(wbytes);
     cuda_check(cudaMemsetAsync(d_bits_.p, 0, wbytes, stream_), "memset");
     cuda_check(cudaMemsetAsync(d_active_.p, 0, wbytes, stream_), "memset");
+    if (opt_.world > 1) {  // p2p exchange buffers: step t lands in buffer t & 1
+        d_xbits_.alloc(2 * wbytes);
+        cuda_check(cudaMemsetAsync(d_xbits_.p, 0, 2 * wbytes, stream_), "memset");
+    }
     d_hist_.alloc(static_cast<size_t>(hw_) * n_ * 8);
     cuda_check(cudaMemsetAsync(d_hist_.p, 0, d_hist_.bytes, stream_), "memset");
     d_hist_lo_.alloc(static_cast<size_t>(n_) * 4);
@@ -448,8 +452,8 @@ void Engine::alloc_state() {
     for (DevBuf* b : {&d_pot64_, &d_pot32_, &d_dep64_, &d_dep32_})
         cuda_check(cudaMemsetAsync(b->p, 0, b->bytes, stream_), "memset");
     if (stdp_on_) {
-        upload(d_ap_, a_plus_);
-        upload(d_am_, a_minus_);
+        upload(stream_, d_ap_, a_plus_);
+        upload(stream_, d_am_, a_minus_);
     } else {
         d_ap_.alloc(8);
         d_am_.alloc(8);
@@ -472,8 +476,8 @@ void Engine::alloc_state() {
         std::vector<double> fp(fire_p_.begin() + first_, fire_p_.begin() + first_ + nl_);
         std::vector<uint64_t> key(static_cast<size_t>(nl_));
         for (int j = 0; j < nl_; ++j) key[j] = agent_stream_key(seed_, static_cast<uint64_t>(first_ + j));
-        upload(d_firep_, fp);
-        upload(d_akey_, key);
+        upload(stream_, d_firep_, fp);
+        upload(stream_, d_akey_, key);
     }
 }
 
@@ -510,9 +514,9 @@ void Engine::build_stimulus_table() {
         hs_off_[t + 1] = static_cast<int64_t>(hs_neuron_.size());
     }
     if (!opt_.stream_io) {
-        upload(d_st_off_, hs_off_);
-        upload(d_st_neuron_, hs_neuron_);
-        upload(d_st_amp_, hs_amp_);
+        upload(stream_, d_st_off_, hs_off_);
+        upload(stream_, d_st_neuron_, hs_neuron_);
+        upload(stream_, d_st_amp_, hs_amp_);
         st_steps_dev_ = steps;
     }
     stim_dirty_ = false;

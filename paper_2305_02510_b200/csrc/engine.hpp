@@ -264,7 +264,7 @@ private:
 
     NcclComm* comm_ = nullptr;
     bool p2p_ = false;
-    DevBuf d_flags_, d_done_, d_err_, d_peer_bits_, d_peer_flags_;
+    DevBuf d_flags_, d_done_, d_err_, d_peer_bits_, d_peer_flags_, d_xbits_;
     std::vector<void*> ipc_opened_;  // peer allocations mapped with cudaIpcOpenMemHandle
     void set_peer_tables(const std::vector<uint32_t*>& bits, const std::vector<int32_t*>& flags);
     void check_exchange_error();

@@ -25,16 +25,20 @@ void Engine::comm_init(const uint8_t* id, int32_t rank, int32_t world) {
 }
 
 // ---- peer-to-peer exchange ---------------------------------------------------
-// Each rank exports (cudaIpcGetMemHandle) its full spike bitmask and its
-// flag array; after opening every peer's pair, the neuron kernel stores its
-// spike words straight into all peers' bitmasks over NVLink and releases
-// flag[rank] = t + 1 in each of them; k_hist acquires all flags before
-// reading the bitmask.  No NCCL call remains on the step path.
+// Each rank exports (cudaIpcGetMemHandle) its exchange bitmask (two
+// step-parity buffers) and its flag array; after opening every peer's pair,
+// the neuron kernel stores its spike words of step t straight into buffer
+// t & 1 of every rank over NVLink and releases flag[rank] = t + 1 in each of
+// them; k_hist acquires all flags before reading buffer t & 1 into the local
+// bitmask.  Double buffering is what makes free-running ranks safe: a rank
+// can be at most one step ahead of its slowest peer (its k_hist(t + 1) waits
+// for every flag t + 2), so its step t + 2 stores never hit a buffer a peer
+// is still reading for step t.  No NCCL call remains on the step path.
 void Engine::p2p_get_handles(uint8_t* out, int64_t cap) {
     require_setup("sn_p2p_get_handles");
     if (cap < 2 * kIpcHandleBytes) throw InvalidArgument("sn_p2p_get_handles: buffer smaller than 128 bytes");
     cudaIpcMemHandle_t hb, hf;
-    cuda_check(cudaIpcGetMemHandle(&hb, d_bits_.p), "cudaIpcGetMemHandle(bits)");
+    cuda_check(cudaIpcGetMemHandle(&hb, d_xbits_.p), "cudaIpcGetMemHandle(bits)");
     cuda_check(cudaIpcGetMemHandle(&hf, d_flags_.p), "cudaIpcGetMemHandle(flags)");
     std::memcpy(out, &hb, kIpcHandleBytes);
     std::memcpy(out + kIpcHandleBytes, &hf, kIpcHandleBytes);
@@ -43,8 +47,8 @@ void Engine::p2p_get_handles(uint8_t* out, int64_t cap) {
 void Engine::set_peer_tables(const std::vector<uint32_t*>& bits, const std::vector<int32_t*>& flags) {
     d_peer_bits_.alloc(bits.size() * sizeof(uint32_t*));
     d_peer_flags_.alloc(flags.size() * sizeof(int32_t*));
-    h2d_sync(d_peer_bits_.p, bits.data(), bits.size() * sizeof(uint32_t*), "peer table");
-    h2d_sync(d_peer_flags_.p, flags.data(), flags.size() * sizeof(int32_t*), "peer table");
+    h2d_sync(stream_, d_peer_bits_.p, bits.data(), bits.size() * sizeof(uint32_t*), "peer table");
+    h2d_sync(stream_, d_peer_flags_.p, flags.data(), flags.size() * sizeof(int32_t*), "peer table");
     p2p_ = true;
 }
 
@@ -56,7 +60,7 @@ void Engine::p2p_open(const uint8_t* all, int32_t world) {
     std::vector<int32_t*> flags(world);
     for (int q = 0; q < world; ++q) {
         if (q == opt_.rank) {
-            bits[q] = d_bits_.as<uint32_t>();
+            bits[q] = d_xbits_.as<uint32_t>();
             flags[q] = d_flags_.as<int32_t>();
             continue;
         }
@@ -85,7 +89,7 @@ void Engine::p2p_connect_local(Engine* const* engines, int32_t world) {
             throw InvalidArgument("sn_p2p_connect_local: engines must be ranks 0..world-1 in order");
         if (e->opt_.device != engines[0]->opt_.device)
             throw InvalidArgument("sn_p2p_connect_local: engines must share one device (use sn_p2p_open across GPUs)");
-        bits[q] = e->d_bits_.as<uint32_t>();
+        bits[q] = e->d_xbits_.as<uint32_t>();
         flags[q] = e->d_flags_.as<int32_t>();
     }
     for (int q = 0; q < world; ++q) {

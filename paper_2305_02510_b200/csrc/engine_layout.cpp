@@ -62,11 +62,11 @@ bool Engine::build_tiny() {
         else wf[q] = static_cast<float>(weight_[s]);
         slot_[s] = static_cast<int64_t>(q);
     }
-    upload(d_toff_, off);
-    upload(d_meta_, meta);
-    upload(d_tpidx_, pidx);
-    if (f64_) upload(d_w_, wd);
-    else upload(d_w_, wf);
+    upload(stream_, d_toff_, off);
+    upload(stream_, d_meta_, meta);
+    upload(stream_, d_tpidx_, pidx);
+    if (f64_) upload(stream_, d_w_, wd);
+    else upload(stream_, d_w_, wf);
     syn_local_ = static_cast<int64_t>(pre_.size());
     sweep_bytes_full_ = static_cast<double>(pre_.size()) * ((stdp_on_ ? 2.0 : 1.0) * (f64_ ? 8 : 4) + 4.0);
     return true;
@@ -108,9 +108,9 @@ void Engine::build_dense_from_lists() {
         else { kind[i] = kRowMixed; any_mixed_ = true; }
         row_pl[i] = kind[i] != kRowNone;
     }
-    if (f64_) upload(d_w_, wd);
-    else upload(d_w_, wf);
-    if (has_delay_) upload(d_delay_, dl);
+    if (f64_) upload(stream_, d_w_, wd);
+    else upload(stream_, d_w_, wf);
+    if (has_delay_) upload(stream_, d_delay_, dl);
     if (any_mixed_) {
         std::vector<uint32_t> mask(static_cast<size_t>(n_) * (pitch_ / 32), 0u);
         for (size_t s = 0; s < pre_.size(); ++s) {
@@ -119,10 +119,10 @@ void Engine::build_dense_from_lists() {
             const int64_t row = off / pitch_, c = off % pitch_;
             mask[row * (pitch_ / 32) + c / 32] |= 1u << (c % 32);
         }
-        upload(d_mask_, mask);
+        upload(stream_, d_mask_, mask);
     }
-    upload(d_kind_, kind);
-    upload(d_row_plastic_, row_pl);
+    upload(stream_, d_kind_, kind);
+    upload(stream_, d_row_plastic_, row_pl);
     sweep_bytes_full_ = static_cast<double>(n_) * nl_ * ((stdp_on_ ? 2.0 : 1.0) * (f64_ ? 8 : 4) + (has_delay_ ? 1 : 0));
 }
 
@@ -135,7 +135,7 @@ int32_t Engine::sparse_pres_per_block() const {
     // 16-bit entries need (the other sparse kernels take any block size)
     if (hbits_ == 16 && !stdp_on_ && !exact_ && c16_allowed()) pb = c16_block_pres();
     if (stdp_on_ && !exact_) {
-        const int esz = f64_ ? 8 : 4;
+        const int esz = 8;  // fp64 traces for every weight type
         // 100k-neuron ER(p=0.01) STDP sweep: staged 0.314 ms vs 0.413 gathered at dp = 1;
         // at dp = 8 the 768-pre blocks of a 24 KB stage lost (0.672 vs 0.591 ms) while
         // 2048-pre blocks in 64 KB (3 CTAs/SM) won (0.532); blocks below 2048 pres
@@ -231,13 +231,13 @@ void Engine::build_sparse_from_lists() {
         slot_[s] = q;
         if (pl) row_pl[i] = 1;
     }
-    upload(d_off_, off);
-    upload(d_meta_, meta);
+    upload(stream_, d_off_, off);
+    upload(stream_, d_meta_, meta);
     if (dict) d_w_.alloc(16);
-    else if (f64_) upload(d_w_, wd);
-    else upload(d_w_, wf);
+    else if (f64_) upload(stream_, d_w_, wd);
+    else upload(stream_, d_w_, wf);
     upload_dict();
-    upload(d_row_plastic_, row_pl);
+    upload(stream_, d_row_plastic_, row_pl);
     sweep_bytes_full_ = static_cast<double>(syn_local_) *
                         (dict ? 4.0 : (stdp_on_ ? 2.0 : 1.0) * (f64_ ? 8 : 4) + 4.0);
 }
@@ -248,10 +248,10 @@ void Engine::upload_dict() {
         return;
     }
     if (f64_) {
-        upload(d_wdict_, dict_);
+        upload(stream_, d_wdict_, dict_);
     } else {
         std::vector<float> f(dict_.begin(), dict_.end());
-        upload(d_wdict_, f);
+        upload(stream_, d_wdict_, f);
     }
 }
 
@@ -285,7 +285,7 @@ void Engine::build_generated() {
         launch_er_dense(er_, d_w_.p, f64_, has_delay_ ? d_delay_.as<uint8_t>() : nullptr,
                         any_mixed_ ? d_mask_.as<uint32_t>() : nullptr, first_, nl_, pitch_, stream_);
         stats_.kernel_launches += 1;
-        upload(d_kind_, kind);
+        upload(stream_, d_kind_, kind);
         if (er_.p >= 1.0) {
             const int64_t self_local = std::max(0, std::min(nl_, n_ - first_));
             syn_local_ = static_cast<int64_t>(n_) * nl_ - self_local;
@@ -310,7 +310,7 @@ void Engine::build_generated() {
             syn_local_ += cnt[g];
         }
         sparse_elems_ = off[nseg];
-        upload(d_off_, off);
+        upload(stream_, d_off_, off);
         d_meta_.alloc(static_cast<size_t>(sparse_elems_) * 4);
         // static nets use the weight dictionary {weight, 0.0 (padding)}: 4 B/synapse
         dict_.clear();
@@ -324,7 +324,7 @@ void Engine::build_generated() {
         if (er_.stdp) std::fill(row_pl.begin(), row_pl.end(), 1);
         sweep_bytes_full_ = static_cast<double>(syn_local_) * (dict ? 4.0 : (stdp_on_ ? 2.0 : 1.0) * esz + 4.0);
     }
-    upload(d_row_plastic_, row_pl);
+    upload(stream_, d_row_plastic_, row_pl);
     if (er_.stdp && !stdp_on_)
         throw InvalidArgument("mat_init: plastic synapses were generated but no STDP config was set (sn_set_stdp)");
 }
@@ -402,9 +402,8 @@ void Engine::plan_launches() {
             }
         }
         if (cols_) {
-            const size_t esz2 = f64_ ? 8 : 4;
             d_hist2_.alloc(static_cast<size_t>(2) * n_ * 8);
-            d_pot2_.alloc(static_cast<size_t>(2) * n_ * std::max(dp_, 1) * esz2);
+            d_pot2_.alloc(static_cast<size_t>(2) * n_ * std::max(dp_, 1) * 8);  // fp64 traces
             d_act2_.alloc(static_cast<size_t>(3) * ((n_ + 31) / 32) * 4);
             for (DevBuf* b : {&d_hist2_, &d_pot2_, &d_act2_})
                 cuda_check(cudaMemsetAsync(b->p, 0, b->bytes, stream_), "memset");
@@ -449,7 +448,8 @@ void Engine::plan_launches() {
                 tile_w_ = static_cast<int32_t>(round_up(tile_w_, 16));
                 ntiles = std::max(1, (nl_ + tile_w_ - 1) / tile_w_);
             }
-            if (tma_ && !dense_tma_fits(tile_w_, f64_, has_delay_, stdp_on_)) tma_ = false;
+            const int tma_rows = tma_ ? dense_tma_max_rows(tile_w_, f64_, has_delay_, stdp_on_) : 0;
+            if (tma_rows < 64) tma_ = false;
             if (tma_) {
                 const char* tw = std::getenv("SNB_TMA_WAVES");
                 // items per SM per step: with the planner warp building the next
@@ -459,7 +459,7 @@ void Engine::plan_launches() {
                 const double tw_waves = tw ? std::atof(tw) : 30.0;
                 int tn = std::max(1, static_cast<int>(std::lround(tw_waves * sms / ntiles)));
                 int trpc = static_cast<int>(round_up(std::max(32, (n_ + tn - 1) / tn), 32));
-                trpc = std::min(trpc, dense_tma_max_rows());
+                trpc = std::min(trpc, tma_rows);
                 rows_per_chunk_ = trpc;
                 nchunks_ = (n_ + trpc - 1) / trpc;
                 dense_grid_ = std::min(sms, ntiles * nchunks_);
@@ -467,7 +467,8 @@ void Engine::plan_launches() {
         }
         const int items = ntiles * nchunks_;
         if (exact_) dense_grid_ = std::min(items, sms * 8);
-        d_partial_.alloc(static_cast<size_t>(nchunks_) * std::max(nl_, 1) * 8);
+        const int prows = nchunks_ * (tma_ ? dense_tma_partials_per_chunk() : 1);
+        d_partial_.alloc(static_cast<size_t>(prows) * std::max(nl_, 1) * 8);
         cuda_check(cudaMemsetAsync(d_partial_.p, 0, d_partial_.bytes, stream_), "memset");
     } else {
         const double avg = nl_ > 0 ? static_cast<double>(sparse_elems_) / (static_cast<double>(nblocks_) * nl_) : 0.0;
@@ -589,7 +590,7 @@ bool Engine::build_c16() {
     cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
     const size_t need = static_cast<size_t>(chunks) * 16 + static_cast<size_t>(sparse_elems_) * 4 + (256u << 20);
     if (need > free_b) return false;
-    upload(d_c16desc_, desc);
+    upload(stream_, d_c16desc_, desc);
     d_c16ent_.alloc(std::max<size_t>(static_cast<size_t>(chunks), 1) * 16);
     DevBuf tmp;
     tmp.alloc(std::max<size_t>(static_cast<size_t>(sparse_elems_), 1) * 4);
@@ -688,10 +689,10 @@ bool Engine::build_sparse_tma_plan(int ctas) {
     first.push_back(static_cast<int32_t>(stages.size()));
     if (bnd.empty()) bnd.assign(8, 0);
     if (stages.empty()) stages.resize(1);
-    upload(d_sp_stages_, stages);
-    upload(d_sp_first_, first);
-    upload(d_sp_block_, cblock);
-    upload(d_sp_bnd_, bnd);
+    upload(stream_, d_sp_stages_, stages);
+    upload(stream_, d_sp_first_, first);
+    upload(stream_, d_sp_block_, cblock);
+    upload(stream_, d_sp_bnd_, bnd);
     sp_ctas_ = static_cast<int32_t>(cblock.size());
     return sp_ctas_ > 0;
 }

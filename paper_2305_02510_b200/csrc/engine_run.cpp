@@ -125,7 +125,7 @@ NeuronArgs Engine::neuron_args(int t_base, int rows, uint32_t* raster, double* t
     a.refr = d_refr_.as<int32_t>();
     a.cnt = d_cnt_.as<int32_t>();
     a.partial = d_partial_.as<double>();
-    a.nchunks = nchunks_;
+    a.nchunks = nchunks_ * ((dense_ && tma_) ? dense_tma_partials_per_chunk() : 1);  // partial rows to sum
     a.u_exact = d_uexact_.as<double>();
     a.st_off = st_off;
     a.st_neuron = st_neuron;
@@ -146,6 +146,7 @@ NeuronArgs Engine::neuron_args(int t_base, int rows, uint32_t* raster, double* t
     a.agent_key = any_stochastic_ ? d_akey_.as<uint64_t>() : nullptr;
     if (p2p_) {
         a.peer_bits = d_peer_bits_.as<uint32_t* const>();
+        a.xstride = static_cast<int32_t>(d_xbits_.bytes / 8);
         a.peer_flags = d_peer_flags_.as<int32_t* const>();
         a.done = d_done_.as<uint32_t>();
         a.rank = opt_.rank;
@@ -177,6 +178,8 @@ HistArgs Engine::hist_args() {
     h.active_count = d_spikes_.as<unsigned long long>() + 1;
     if (p2p_) {
         h.flags = d_flags_.as<int32_t>();
+        h.xbits = d_xbits_.as<uint32_t>();
+        h.xstride = static_cast<int32_t>(d_xbits_.bytes / 8);
         h.world = opt_.world;
         h.error = d_err_.as<int32_t>();
     }
@@ -196,8 +199,8 @@ DenseArgs Engine::dense_args() {
     a.active = d_active_.as<uint32_t>();
     a.hist = d_hist_.as<uint64_t>();
     a.bits = d_bits_.as<uint32_t>();
-    a.pot = f64_ ? static_cast<const void*>(d_pot64_.p) : static_cast<const void*>(d_pot32_.p);
-    a.dep = f64_ ? static_cast<const void*>(d_dep64_.p) : static_cast<const void*>(d_dep32_.p);
+    a.pot = d_pot64_.as<double>();
+    a.dep = d_dep64_.as<double>();
     a.dp = stdp_on_ ? dp_ : 1;
     a.w_min = w_min_;
     a.w_max = w_max_;
@@ -233,8 +236,8 @@ void Engine::launch_sweep_only() {
         a.bits = d_bits_.as<uint32_t>();
         a.hist_lo = d_hist_lo_.as<uint32_t>();
         a.hist = d_hist_.as<uint64_t>();
-        a.pot = f64_ ? static_cast<const void*>(d_pot64_.p) : static_cast<const void*>(d_pot32_.p);
-        a.dep = f64_ ? static_cast<const void*>(d_dep64_.p) : static_cast<const void*>(d_dep32_.p);
+        a.pot = d_pot64_.as<double>();
+        a.dep = d_dep64_.as<double>();
         a.dp = stdp_on_ ? dp_ : 1;
         a.w_min = w_min_;
         a.w_max = w_max_;
@@ -608,7 +611,7 @@ void Engine::get_spike_words(uint32_t* out, int64_t words) {
 void Engine::put_spike_words(int32_t first_word, const uint32_t* w, int64_t count) {
     require_setup("sn_put_spike_words");
     if (first_word < 0 || first_word + count > words_) throw InvalidArgument("sn_put_spike_words: range outside the bitmask");
-    h2d_sync(d_bits_.as<uint32_t>() + first_word, w, static_cast<size_t>(count) * 4, "bits H2D");
+    h2d_sync(stream_, d_bits_.as<uint32_t>() + first_word, w, static_cast<size_t>(count) * 4, "bits H2D");
 }
 
 void Engine::step_finish() {

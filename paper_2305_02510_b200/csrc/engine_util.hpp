@@ -26,19 +26,20 @@ inline void throw_first(const char* where, const std::vector<std::string>& v) { 
     throw InvalidArgument(msg);
 }
 
-// Host-to-device copy that is complete on return.  A pageable cudaMemcpy H2D
-// may return while its DMA is still in flight on the legacy default stream,
-// which the engine's non-blocking stream does not wait for: kernels launched
-// right after could read the old contents.
-inline void h2d_sync(void* dst, const void* src, size_t bytes, const char* what) {
-    cuda_check(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), what);
-    cuda_check(cudaStreamSynchronize(cudaStreamLegacy), what);
+// Host-to-device copy that is complete on return, ordered on the engine's
+// stream: after every engine kernel queued before it, before every kernel
+// queued after it, and independent of the legacy default stream (a plain
+// pageable cudaMemcpy may return with its DMA still queued there, and the
+// engine's non-blocking stream does not wait for it).
+inline void h2d_sync(cudaStream_t s, void* dst, const void* src, size_t bytes, const char* what) {
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), what);
+    cuda_check(cudaStreamSynchronize(s), what);
 }
 
 template <typename T>
-inline void upload(DevBuf& d, const std::vector<T>& h) {
+inline void upload(cudaStream_t s, DevBuf& d, const std::vector<T>& h) {
     d.alloc(h.size() * sizeof(T));
-    if (!h.empty()) h2d_sync(d.p, h.data(), h.size() * sizeof(T), "upload");
+    if (!h.empty()) h2d_sync(s, d.p, h.data(), h.size() * sizeof(T), "upload");
 }
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }

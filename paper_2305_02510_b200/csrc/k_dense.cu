@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(kThreads) k_dense_sweep(DenseArgs a) {
 
     __shared__ int32_t s_rows[kSubRows];
     __shared__ uint64_t s_e[kSubRows];
-    __shared__ WT s_pot[STDP && !DELAY ? kSubRows : 1];
+    __shared__ double s_pot[STDP && !DELAY ? kSubRows : 1];
     __shared__ uint8_t s_kind[kSubRows];
     __shared__ uint32_t s_word[32];
     __shared__ int32_t s_wpref[33];
@@ -35,8 +35,8 @@ __global__ void __launch_bounds__(kThreads) k_dense_sweep(DenseArgs a) {
     const int ntiles = (a.nl + a.tile_w - 1) / a.tile_w;
     const int items = ntiles * a.nchunks;
     const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
-    const WT* pot = static_cast<const WT*>(a.pot);
-    const WT* dep = static_cast<const WT*>(a.dep);
+    const double* pot = a.pot;
+    const double* dep = a.dep;
     WT* W = static_cast<WT*>(a.w);
     const uint64_t dmask = DELAY ? ~0ull : 1ull;
 
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(kThreads) k_dense_sweep(DenseArgs a) {
         const int r1 = min(a.n, r0 + a.rows_per_chunk);
 
         bool sj[VEC];
-        WT depj[VEC];
+        double depj[VEC];
         int gc[VEC];
         double acc[VEC];
 #pragma unroll
@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(kThreads) k_dense_sweep(DenseArgs a) {
             gc[k] = a.first + c0 + k;
             const bool ok = in_tile && (c0 + k) < a.nl;
             sj[k] = ok && STDP ? bit_of(a.bits, gc[k]) : false;
-            depj[k] = ok && STDP ? dep[gc[k]] : WT(0);
+            depj[k] = ok && STDP ? dep[gc[k]] : 0.0;
             acc[k] = (EXACT && ok && !a.abm) ? leak_toward(a.v[c0 + k], a.leak[c0 + k], a.reset[c0 + k]) : 0.0;
         }
 
@@ -143,12 +143,8 @@ __global__ void __launch_bounds__(kThreads) k_dense_sweep(DenseArgs a) {
                             const bool pl = kind == kRowAll || (kind == kRowAllButSelf && gc[k] != row) ||
                                             (kind == kRowMixed && ((mv[u] >> k) & 1u));
                             if (pl) {
-                                const WT p = DELAY ? pot[static_cast<int64_t>(row) * a.dp + d1] : s_pot[idx];
-                                // dw = 0; if s_post: dw += pot; if s_pre: dw -= dep (243-246)
-                                WT dw = WT(0);
-                                if (sj[k]) dw += p;
-                                if (e) dw -= depj[k];
-                                const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
+                                const double p = DELAY ? pot[static_cast<int64_t>(row) * a.dp + d1] : s_pot[idx];
+                                const WT nw = stdp_apply<WT>(w, stdp_dw(sj[k], p, e, depj[k]), wmin, wmax);
                                 changed |= (nw != w);
                                 w = nw;
                                 VT::set(wv[u], k, nw);
@@ -192,23 +188,35 @@ __global__ void __launch_bounds__(kThreads, 2) k_dense_stream(DenseArgs a) {
 // TMA-staged dense sweep (fp32 or fp64 weights; with synaptic delays the
 // rows' delay bytes ride in the same stages): one CTA per SM, a producer warp
 // streams the active rows' tile segments into a kTmaStages-deep shared-memory
-// ring with cp.async.bulk (completion on mbarriers), 8 consumer warps apply
-// the same per-element update as k_dense_stream from shared memory and write
-// the new weights with 128-bit streaming stores.  Loads never occupy
-// registers, so the in-flight window per SM is the whole ring.
+// ring with cp.async.bulk (completion on mbarriers), 8 x kTmaHalves consumer
+// warps apply the same per-element update as k_dense_stream from shared
+// memory and write the new weights with 128-bit streaming stores.  Loads
+// never occupy registers, so the in-flight window per SM is the whole ring.
+// Consumer warp w owns column slot w & 7 of every row r = w >> 3 (mod
+// kTmaHalves) of a stage: two halves give each scheduler 4 consumer warps to
+// hide the fp64 STDP arithmetic's dependent latency (cfg3 sweep 1.47 ms with
+// one half), and each half writes its own partial row.
+#ifndef SNB_TMA_HALVES
+#define SNB_TMA_HALVES 2
+#endif
 constexpr int kTmaRows = 4;        // rows per stage
 constexpr int kTmaStages = 8;      // ring depth
-constexpr int kTmaListMax = 1024;  // rows per item (one list per item, double-buffered)
-constexpr int kTmaThreads = 320;   // 8 consumer warps + 1 producer warp + 1 planner warp
+constexpr int kTmaListMax = 1024;  // rows per item at most (one list per item, double-buffered)
+constexpr int kTmaHalves = SNB_TMA_HALVES;
+constexpr int kTmaConsumers = 8 * kTmaHalves;               // consumer warps
+constexpr int kTmaThreads = 32 * (kTmaConsumers + 2);       // + 1 producer warp + 1 planner warp
 constexpr int kTmaDp = 4;          // delayed STDP: pot^(d) traces staged per listed row
-constexpr int kTmaRec = kTmaListMax + kTmaRows;
+// Row records of both weight types carry the fp64 trace (RowRec<double>):
+// the STDP update is computed in fp64 for fp32 storage too.
+using TmaRec = RowRec<double>;
 
-// Roles: warp 9 (planner) claims the next item and builds its active-row list
-// into the other of two list buffers while warp 8 (producer) streams the
-// current item's rows and warps 0-7 (consumers) process them, so an item's
+// Roles: warp kTmaConsumers + 1 (planner) claims the next item and builds its
+// active-row list into the other of two list buffers while warp kTmaConsumers
+// (producer) streams the current item's rows and the consumer warps process
+// them, so an item's
 // list build (two dependent global round trips + a scan) no longer stalls the
 // ring between items.  Buffers hand over on mbarriers: ready[b] (planner ->
-// producer + consumers), freeb[b] (producer + 8 consumer warps -> planner) and
+// producer + consumers), freeb[b] (producer + consumer warps -> planner) and
 // issued (producer -> planner: claim the next item now).
 template <typename WT, bool STDP, bool DELAY>
 __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
@@ -229,32 +237,34 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
     uint64_t* ready = empty + kTmaStages;
     uint64_t* freeb = ready + 2;
     uint64_t* issued = freeb + 2;  // producer -> planner: the current item's last stage is issued
-    RowRec<WT>* s_recs = reinterpret_cast<RowRec<WT>*>(issued + 2);
-    // delayed STDP: pot^(d) of each listed row for d = 1..kTmaDp (a.dp <= kTmaDp)
-    WT* s_potds = reinterpret_cast<WT*>(s_recs + 2 * kTmaRec);
+    // list buffers sized for this launch's items (rows_per_chunk rows + one stage of padding)
+    const int rec_cap = a.rows_per_chunk + kTmaRows;
+    TmaRec* s_recs = reinterpret_cast<TmaRec*>(issued + 2);
+    // delayed STDP: fp64 pot^(d) of each listed row for d = 1..kTmaDp (a.dp <= kTmaDp)
+    double* s_potds = reinterpret_cast<double*>(s_recs + 2 * rec_cap);
     __shared__ int s_item[2];
     __shared__ int s_cnt[2];
 
     const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
-    const WT* dep = static_cast<const WT*>(a.dep);
-    const WT* pot = static_cast<const WT*>(a.pot);
+    const double* dep = a.dep;
+    const double* pot = a.pot;
     WT* W = static_cast<WT*>(a.w);
 
     if (tid == 0) {
         for (int s = 0; s < kTmaStages; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, 8);
+            mbar_init(empty + s, kTmaConsumers);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(ready + b, 1);
-            mbar_init(freeb + b, 9);
+            mbar_init(freeb + b, kTmaConsumers + 1);
         }
         mbar_init(issued, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    if (warp == 9) {
+    if (warp == kTmaConsumers + 1) {
         // ---- planner ----
         for (int ki = 0;; ++ki) {
             const int b = ki & 1;
@@ -270,8 +280,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                 if (lane == 0) got = atomicAdd(a.work, 1);
                 item = __shfl_sync(0xffffffffu, got, 0);
             }
-            RowRec<WT>* rec = s_recs + b * kTmaRec;
-            WT* potd = s_potds + b * kTmaRec * kTmaDp;
+            TmaRec* rec = s_recs + b * rec_cap;
+            double* potd = s_potds + b * rec_cap * kTmaDp;
             int cnt = 0;
             if (item < items) {
                 const int chunk = item / ntiles;
@@ -304,29 +314,29 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                 for (int p0 = 0; p0 < cnt; p0 += 4 * 32) {
                     uint64_t h[4];
                     int kd[4];
-                    WT pt[4];
+                    double pt[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int p = p0 + u * 32 + lane;
                         h[u] = 0;
                         kd[u] = 0;
-                        pt[u] = WT(0);
+                        pt[u] = 0.0;
                         if (p < cnt) {
                             const int r = rec[p].rowk;
                             h[u] = __ldcg(a.hist + r);
                             kd[u] = STDP ? static_cast<int>(__ldg(a.kind + r)) : 0;
-                            pt[u] = (STDP && !DELAY) ? __ldcg(pot + r) : WT(0);
+                            pt[u] = (STDP && !DELAY) ? __ldcg(pot + r) : 0.0;
                             if (STDP && DELAY)
                                 for (int d = 0; d < kTmaDp; ++d)
                                     potd[p * kTmaDp + d] =
-                                        d < a.dp ? __ldcg(pot + static_cast<int64_t>(r) * a.dp + d) : WT(0);
+                                        d < a.dp ? __ldcg(pot + static_cast<int64_t>(r) * a.dp + d) : 0.0;
                         }
                     }
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int p = p0 + u * 32 + lane;
                         if (p < cnt) {
-                            RowRec<WT> x;
+                            TmaRec x;
                             x.rowk = rec[p].rowk | (kd[u] << 28);
                             x.e_lo = static_cast<uint32_t>(h[u]);
                             x.e_hi = static_cast<uint32_t>(h[u] >> 32);
@@ -344,7 +354,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
             }
             if (item >= items) break;
         }
-    } else if (warp == 8) {
+    } else if (warp == kTmaConsumers) {
         // ---- producer ----
         uint32_t it = 0;  // ring position, advanced identically by producer and consumers
         for (int ki = 0;; ++ki) {
@@ -353,7 +363,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
             const int item = s_item[b];
             if (item < 0) break;
             const int cnt = s_cnt[b];
-            const RowRec<WT>* rec = s_recs + b * kTmaRec;
+            const TmaRec* rec = s_recs + b * rec_cap;
             const int chunk = item / ntiles;
             const int tile = item - chunk * ntiles;
             const int col0 = tile * a.tile_w;
@@ -393,24 +403,28 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
             const int item = s_item[b];
             if (item < 0) break;
             const int cnt = s_cnt[b];
-            const RowRec<WT>* s_rec = s_recs + b * kTmaRec;
-            const WT* s_potd = s_potds + b * kTmaRec * kTmaDp;
+            const TmaRec* s_rec = s_recs + b * rec_cap;
+            const double* s_potd = s_potds + b * rec_cap * kTmaDp;
             const int chunk = item / ntiles;
             const int tile = item - chunk * ntiles;
             const int col0 = tile * a.tile_w;
             const int width = static_cast<int>(min(static_cast<int64_t>(a.tile_w), a.pitch - col0));
             const int ngroups = (cnt + kTmaRows - 1) / kTmaRows;
-            const int tcol = tid * VEC;
+            const int rh = warp >> 3;                 // row half
+            const int tcol = ((warp & 7) * 32 + lane) * VEC;
             const int c0 = col0 + tcol;
             const bool in_tile = tcol < width && c0 < a.nl;
             const int gc0 = a.first + c0;
-            WT sjf[VEC], depj[VEC];
+            bool sj[VEC];
+            double depj[VEC], sjd[VEC], ndep[VEC];
             double acc[VEC];
 #pragma unroll
             for (int k = 0; k < VEC; ++k) {
                 const bool ok = in_tile && (c0 + k) < a.nl;
-                sjf[k] = (ok && STDP && bit_of(a.bits, gc0 + k)) ? WT(1) : WT(0);
-                depj[k] = (ok && STDP) ? __ldcg(dep + gc0 + k) : WT(0);
+                sj[k] = ok && STDP && bit_of(a.bits, gc0 + k);
+                depj[k] = (ok && STDP) ? __ldcg(dep + gc0 + k) : 0.0;
+                sjd[k] = sj[k] ? 1.0 : 0.0;  // exact 0/1 factors for the unit-delay fma form
+                ndep[k] = -depj[k];
                 acc[k] = 0.0;
             }
             for (int g = 0; g < ngroups; ++g, ++it) {
@@ -424,9 +438,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                 for (int k = 0; k < VEC; ++k) grp[k] = WT(0);
                 if (in_tile) {
 #pragma unroll
-                    for (int r = 0; r < kTmaRows; ++r) {
+                    for (int r = rh; r < kTmaRows; r += kTmaHalves) {
                         if (r >= nr) break;
-                        const RowRec<WT> rec = s_rec[g * kTmaRows + r];
+                        const TmaRec rec = s_rec[g * kTmaRows + r];
                         const int row = rec.rowk & 0x0fffffff;
                         const int kind = rec.rowk >> 28;
                         const V wv = *reinterpret_cast<const V*>(st + static_cast<size_t>(r) * row_bytes + tcol * sizeof(WT));
@@ -447,12 +461,22 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                         }
                         if (STDP && kind != kRowNone) {
                             WT nw[VEC];
+                            if (DELAY) {
 #pragma unroll
-                            for (int k = 0; k < VEC; ++k) {
-                                const WT p = DELAY ? s_potd[(g * kTmaRows + r) * kTmaDp + d1[k]] : rec.pot;
-                                // dw = 0; if s_post dw += pot; if s_pre dw -= dep (mat_engine.cpp:243-246)
-                                const WT dw = fma(sjf[k], p, -(ef[k] * depj[k]));
-                                nw[k] = clamp_ref<WT>(w[k] + dw, wmin, wmax);
+                                for (int k = 0; k < VEC; ++k) {
+                                    const double p = s_potd[(g * kTmaRows + r) * kTmaDp + d1[k]];
+                                    nw[k] = stdp_apply<WT>(w[k], stdp_dw(sj[k], p, ef[k] != WT(0), depj[k]), wmin, wmax);
+                                }
+                            } else if (h & 1ull) {
+                                // unit delay: s_pre is the row's bit (warp-uniform branch);
+                                // dw = fma(s_post, pot, -dep) rounds pot - dep once like the
+                                // reference's dw -= dep, and is exactly -dep when s_post = 0
+#pragma unroll
+                                for (int k = 0; k < VEC; ++k)
+                                    nw[k] = stdp_apply<WT>(w[k], fma(sjd[k], rec.pot, ndep[k]), wmin, wmax);
+                            } else {
+#pragma unroll
+                                for (int k = 0; k < VEC; ++k) nw[k] = stdp_apply<WT>(w[k], sjd[k] * rec.pot, wmin, wmax);
                             }
                             if (kind == kRowAllButSelf) {
                                 const int selfk = row - gc0;
@@ -484,7 +508,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
             if (in_tile) {
 #pragma unroll
                 for (int k = 0; k < VEC; ++k)
-                    if (c0 + k < a.nl) a.partial[static_cast<int64_t>(chunk) * a.nl + c0 + k] = acc[k];
+                    if (c0 + k < a.nl) a.partial[static_cast<int64_t>(chunk * kTmaHalves + rh) * a.nl + c0 + k] = acc[k];
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(freeb + b);
@@ -493,30 +517,39 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
     if (blockIdx.x == 0 && tid == 0) *a.d_step += 1;
 }
 
-size_t dense_tma_smem(int tile_w, bool f64, bool delay, bool stdp) {
+size_t dense_tma_smem(int tile_w, bool f64, bool delay, bool stdp, int rows) {
     const size_t esz = f64 ? 8 : 4;
-    const size_t rec = f64 ? sizeof(RowRec<double>) : sizeof(RowRec<float>);
     return static_cast<size_t>(kTmaStages) * kTmaRows * tile_w * (esz + (delay ? 1 : 0)) + (2 * kTmaStages + 6) * 8 +
-           2 * static_cast<size_t>(kTmaRec) * (rec + ((delay && stdp) ? kTmaDp * esz : 0));
+           2 * static_cast<size_t>(rows + kTmaRows) * (sizeof(TmaRec) + ((delay && stdp) ? kTmaDp * 8 : 0));
+}
+
+int smem_optin() {
+    int dev = 0, optin = 0;
+    check(cudaGetDevice(&dev), "cudaGetDevice");
+    check(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
+    return optin;
 }
 
 }  // namespace
 
 int dense_vec(bool f64) { return f64 ? 2 : 4; }
 
-int dense_tma_max_rows() { return kTmaListMax; }
 int dense_tma_max_dp() { return kTmaDp; }
+int dense_tma_partials_per_chunk() { return kTmaHalves; }
 
-bool dense_tma_fits(int tile_w, bool f64, bool delay, bool stdp) {
-    int dev = 0, optin = 0;
-    check(cudaGetDevice(&dev), "cudaGetDevice");
-    check(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
-    return dense_tma_smem(tile_w, f64, delay, stdp) + 1024 <= static_cast<size_t>(optin);  // + static smem
+// Longest item row list (a multiple of 32, <= kTmaListMax) whose two list
+// buffers fit next to the ring in the opt-in shared memory; 0 if even 32 rows
+// do not fit.
+int dense_tma_max_rows(int tile_w, bool f64, bool delay, bool stdp) {
+    const size_t optin = static_cast<size_t>(smem_optin());
+    for (int rows = kTmaListMax; rows >= 32; rows -= 32)
+        if (dense_tma_smem(tile_w, f64, delay, stdp, rows) + 1024 <= optin) return rows;  // + static smem
+    return 0;
 }
 
 template <typename WT, bool STDP, bool DELAY>
 static void dense_tma_go(const DenseArgs& a, int grid, cudaStream_t s) {
-    const size_t smem = dense_tma_smem(a.tile_w, sizeof(WT) == 8, DELAY, STDP);
+    const size_t smem = dense_tma_smem(a.tile_w, sizeof(WT) == 8, DELAY, STDP, a.rows_per_chunk);
     static size_t configured = 0;
     auto kern = k_dense_tma<WT, STDP, DELAY>;
     if (configured < smem) {

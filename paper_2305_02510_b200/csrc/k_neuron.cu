@@ -57,10 +57,19 @@ __global__ void __launch_bounds__(kThreads) k_hist(HistArgs h) {
         __syncthreads();
     }
     bool act = false;
-    if (i < h.n) {
-        const bool s = (h.bits[i >> 5] >> (i & 31)) & 1u;
-        act = hist_update(h, i, s, t);
+    bool s = false;
+    if (h.xbits) {
+        // step t arrived in exchange buffer t & 1; a peer writes step t + 2 into
+        // the same buffer only after its k_hist(t + 1) saw our flag t + 2, i.e.
+        // after this kernel (and the sweep of step t) finished on this rank
+        const uint32_t* src = h.xbits + static_cast<int64_t>(t & 1) * h.xstride;
+        if (i < h.n) s = (src[i >> 5] >> (i & 31)) & 1u;
+        const uint32_t word = __ballot_sync(0xffffffffu, s);
+        if ((threadIdx.x & 31) == 0 && (i >> 5) < ((h.n + 31) >> 5)) h.bits[i >> 5] = word;
+    } else if (i < h.n) {
+        s = (h.bits[i >> 5] >> (i & 31)) & 1u;
     }
+    if (i < h.n) act = hist_update(h, i, s, t);
     const uint32_t aw = __ballot_sync(0xffffffffu, act);
     if ((threadIdx.x & 31) == 0 && (i >> 5) < ((h.n + 31) >> 5)) h.active[i >> 5] = aw;
     const int active = __syncthreads_count(act);

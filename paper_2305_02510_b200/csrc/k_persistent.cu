@@ -257,10 +257,8 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
                 const uint16_t pq = pidx[q];
                 if (pq == 0xffffu) continue;  // not plastic
                 const uint32_t mq = meta[q];
-                WT dw = WT(0);
-                if (fired) dw += static_cast<WT>(potn[pq]);
-                if (tiny_bit(hnb, mq)) dw -= static_cast<WT>(depj);
-                w[q] = clamp_ref<WT>(w[q] + dw, wmin, wmax);
+                w[q] = stdp_apply<WT>(w[q], stdp_dw(fired, fired ? potn[pq] : 0.0, tiny_bit(hnb, mq), depj), wmin,
+                                      wmax);
             }
         }
     }
@@ -325,7 +323,7 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
     constexpr int CV = kColW / VEC;          // column vectors per CTA
     constexpr int RL = kColThreads / CV;     // row lanes
     __shared__ double s_red[RL][kColW + 1];
-    __shared__ WT s_dep[kColW];
+    __shared__ double s_dep[kColW];
     __shared__ uint32_t s_spk;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int c = blockIdx.x;
@@ -338,7 +336,7 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
     const int64_t pitch = da.pitch, mpitch = pitch >> 5;
     const WT wmin = static_cast<WT>(da.w_min), wmax = static_cast<WT>(da.w_max);
     WT* W = static_cast<WT*>(da.w);
-    WT* pot2 = static_cast<WT*>(ca.pot2);
+    double* pot2 = static_cast<double*>(ca.pot2);  // fp64 traces (fp64 STDP math)
     const uint64_t dmask = ca.dmax >= 64 ? ~0ull : ((1ull << ca.dmax) - 1ull);
     const uint64_t wmask = ca.window >= 63 ? ~0ull : ((1ull << (ca.window + 1)) - 1ull);
     double in = own ? na.partial[j] : 0.0;   // input of the call's first step
@@ -414,13 +412,13 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
                     // set bits in ascending k: the reference's order (mat_engine.cpp:226-240)
                     double dep = 0.0;
                     for (uint64_t m = hn & wmask & ~1ull; m; m &= m - 1) dep += ca.a_minus[__ffsll(static_cast<long long>(m)) - 2];
-                    s_dep[lane] = static_cast<WT>(dep);
+                    s_dep[lane] = dep;
                     bool any_pot = false;
                     for (int d = 1; d <= da.dp; ++d) {
                         double pot = 0.0;
                         for (uint64_t m = (hn >> (d - 1)) & wmask & ~1ull; m; m &= m - 1)
                             pot += ca.a_plus[__ffsll(static_cast<long long>(m)) - 2];
-                        pot2[(static_cast<int64_t>(cur) * n + j) * da.dp + (d - 1)] = static_cast<WT>(pot);
+                        pot2[(static_cast<int64_t>(cur) * n + j) * da.dp + (d - 1)] = pot;
                         any_pot |= pot != 0.0;
                     }
                     if (ca.row_plastic[j] && (any_pot || t == 0)) act = true;
@@ -449,17 +447,18 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
         // sweep of the CTA's columns: STDP of step t, delivery of step t + 1
         const uint32_t spk = s_spk;
         bool okc[VEC];
-        WT sj[VEC], dj[VEC];
+        bool sj[VEC];
+        double dj[VEC];
         double acc[VEC];
 #pragma unroll
         for (int k = 0; k < VEC; ++k) {
             okc[k] = j0 + k < na.nl;
-            sj[k] = (STDP && okc[k] && ((spk >> (cv * VEC + k)) & 1u)) ? WT(1) : WT(0);
-            dj[k] = STDP ? s_dep[cv * VEC + k] : WT(0);
+            sj[k] = STDP && okc[k] && ((spk >> (cv * VEC + k)) & 1u);
+            dj[k] = STDP ? s_dep[cv * VEC + k] : 0.0;
             acc[k] = 0.0;
         }
         const uint64_t* hist = ca.hist2 + static_cast<int64_t>(cur) * n;
-        const WT* potc = pot2 + static_cast<int64_t>(cur) * n * da.dp;
+        const double* potc = pot2 + static_cast<int64_t>(cur) * n * da.dp;
         // every load of a row is issued before its activity bit is tested: the
         // rows of a small net sit in L2 and one round trip per row pair is the
         // cost that matters here
@@ -492,11 +491,8 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
                     const bool pl = kind == kRowAll || (kind == kRowAllButSelf && j0 + k != i) ||
                                     (kind == kRowMixed && ((mw >> ((j0 & 31) + k)) & 1u));
                     if (pl) {
-                        const WT p = __ldcg(potc + static_cast<int64_t>(i) * da.dp + d1);
-                        WT dw = WT(0);  // dw = 0; if s_post dw += pot; if s_pre dw -= dep (mat_engine.cpp:243-246)
-                        if (sj[k] != WT(0)) dw += p;
-                        if (e) dw -= dj[k];
-                        const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
+                        const double p = __ldcg(potc + static_cast<int64_t>(i) * da.dp + d1);
+                        const WT nw = stdp_apply<WT>(w, stdp_dw(sj[k], p, e, dj[k]), wmin, wmax);
                         changed |= nw != w;
                         w = nw;
                         VT::set(wv, k, nw);

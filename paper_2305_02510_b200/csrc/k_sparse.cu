@@ -64,9 +64,9 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(Spars
         for (int k = tid; k < a.dict_size; k += kThreads) s_wd[k] = static_cast<const WT*>(a.wdict)[k];
     // STDP: the block's pot^(d) traces, [pcount][dp], staged next to the history
     // (the per-synapse lookup would otherwise be a random global gather)
-    WT* s_pot = reinterpret_cast<WT*>(smem_raw + hbytes);
+    double* s_pot = reinterpret_cast<double*>(smem_raw + hbytes);
     if (STDP && a.pot_staged) {
-        const WT* src = static_cast<const WT*>(a.pot) + static_cast<int64_t>(pre0) * a.dp;
+        const double* src = a.pot + static_cast<int64_t>(pre0) * a.dp;
         for (int k = tid; k < pcount * a.dp; k += kThreads) s_pot[k] = __ldcg(src + k);
     }
     __syncthreads();
@@ -75,8 +75,8 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(Spars
     const bool uniform = DICT && a.dict_size == 2;  // {w, 0.0 padding}: every synapse carries w
 
     const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
-    const WT* pot = (STDP && a.pot_staged) ? s_pot : static_cast<const WT*>(a.pot) + static_cast<int64_t>(pre0) * a.dp;
-    const WT* dep = static_cast<const WT*>(a.dep);
+    const double* pot = (STDP && a.pot_staged) ? s_pot : a.pot + static_cast<int64_t>(pre0) * a.dp;
+    const double* dep = a.dep;
     WT* W = static_cast<WT*>(a.w);
 
     const int p0 = blockIdx.x * a.posts_per_cta;
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(Spars
         if (valid) {
             const int gp = a.first + p;
             bool sp = false;
-            WT depp = WT(0);
+            double depp = 0.0;
             if (STDP) {
                 sp = bit_of(a.bits, gp);
                 depp = dep[gp];
@@ -170,10 +170,8 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(Spars
                         else e = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
                         WT w = wv[u][k];
                         if (!DICT && STDP && ((m >> 22) & 1u)) {
-                            WT dw = WT(0);
-                            if (sp) dw += pot[pl * a.dp + d1];  // only spiking posts read pot^(d)
-                            if (e) dw -= depp;
-                            const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
+                            const double pt = sp ? pot[pl * a.dp + d1] : 0.0;  // only spiking posts read pot^(d)
+                            const WT nw = stdp_apply<WT>(w, stdp_dw(sp, pt, e != 0u, depp), wmin, wmax);
                             changed |= (nw != w);
                             w = nw;
                             wv[u][k] = nw;
@@ -855,8 +853,8 @@ __global__ void __launch_bounds__(kThreads) k_sparse_stream(SparseArgs a) {
     const uint32_t* sbits = reinterpret_cast<const uint32_t*>(smem_raw);
     const HT* shist = reinterpret_cast<const HT*>(smem_raw);
     const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
-    const WT* pot = static_cast<const WT*>(a.pot);
-    const WT* dep = static_cast<const WT*>(a.dep);
+    const double* pot = a.pot;
+    const double* dep = a.dep;
     WT* W = static_cast<WT*>(a.w);
     const int64_t* off = a.off + static_cast<int64_t>(b) * a.nl;  // off[p], p in [0, nl]
     double* part = a.partial + static_cast<int64_t>(b) * a.nl;
@@ -929,7 +927,7 @@ __global__ void __launch_bounds__(kThreads) k_sparse_stream(SparseArgs a) {
             if (valid) {
                 const uint32_t ms[4] = {m4[u].x, m4[u].y, m4[u].z, m4[u].w};
                 bool sp = false;
-                WT depp = WT(0);
+                double depp = 0.0;
                 if (STDP) {
                     sp = bit_of(a.bits, a.first + p);
                     depp = __ldcg(dep + a.first + p);
@@ -945,9 +943,8 @@ __global__ void __launch_bounds__(kThreads) k_sparse_stream(SparseArgs a) {
                     else ev = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
                     WT w = wv[u][k];
                     if (STDP && ((m >> 22) & 1u)) {
-                        const WT pt = __ldcg(pot + static_cast<int64_t>(pre0 + pl) * a.dp + d1);
-                        const WT dw = fma(sp ? WT(1) : WT(0), pt, -((ev ? WT(1) : WT(0)) * depp));
-                        const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
+                        const double pt = __ldcg(pot + static_cast<int64_t>(pre0 + pl) * a.dp + d1);
+                        const WT nw = stdp_apply<WT>(w, stdp_dw(sp, pt, ev != 0u, depp), wmin, wmax);
                         changed |= (nw != w);
                         w = nw;
                         wv[u][k] = nw;
@@ -996,12 +993,12 @@ __global__ void __launch_bounds__(kThreads) k_sparse_exact(SparseArgs a) {
     const int p = blockIdx.x * kThreads + threadIdx.x;
     if (p < a.nl) {
         const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
-        const WT* pot = static_cast<const WT*>(a.pot);
-        const WT* dep = static_cast<const WT*>(a.dep);
+        const double* pot = a.pot;
+        const double* dep = a.dep;
         WT* W = static_cast<WT*>(a.w);
         const int gp = a.first + p;
         const bool sp = STDP ? bit_of(a.bits, gp) : false;
-        const WT depp = STDP ? dep[gp] : WT(0);
+        const double depp = STDP ? dep[gp] : 0.0;
         double acc = a.abm ? 0.0 : leak_toward(a.v[p], a.leak[p], a.reset[p]);
         for (int b = 0; b < a.nblocks; ++b) {
             const int64_t beg = a.off[static_cast<int64_t>(b) * a.nl + p];
@@ -1013,10 +1010,8 @@ __global__ void __launch_bounds__(kThreads) k_sparse_exact(SparseArgs a) {
                 const bool e = (a.hist[pre] >> d1) & 1ull;
                 WT w = W[q];
                 if (STDP && ((m >> 22) & 1u)) {
-                    WT dw = WT(0);
-                    if (sp) dw += pot[static_cast<int64_t>(pre) * a.dp + d1];
-                    if (e) dw -= depp;
-                    const WT nw = clamp_ref<WT>(w + dw, wmin, wmax);
+                    const double pt = sp ? pot[static_cast<int64_t>(pre) * a.dp + d1] : 0.0;
+                    const WT nw = stdp_apply<WT>(w, stdp_dw(sp, pt, e, depp), wmin, wmax);
                     if (nw != w) W[q] = nw;
                     w = nw;
                 }
@@ -1046,7 +1041,7 @@ template <typename WT, bool STDP, int HB>
 static void sparse_go_sub(const SparseArgs& a, int sub, int gx, size_t smem, cudaStream_t s) {
     dim3 grid(gx, a.nblocks);
     if (a.dict_size > 0) smem = ((smem + 15) & ~static_cast<size_t>(15)) + static_cast<size_t>(a.dict_size) * sizeof(WT);
-    if (STDP && a.pot_staged) smem += static_cast<size_t>(a.pb) * a.dp * sizeof(WT);
+    if (STDP && a.pot_staged) smem += static_cast<size_t>(a.pb) * a.dp * sizeof(double);
     auto go = [&](auto kern) {
         if (smem > 48 * 1024)
             check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),

@@ -50,8 +50,10 @@ struct NeuronArgs {
     double* trace;             // [rows][nl] or null
     unsigned long long* spike_count;
     // peer-to-peer spike exchange (fused into this kernel; null when unused):
-    // every rank's full bitmask and flag array, reachable over NVLink
+    // every rank's exchange bitmask (two step-parity buffers of xstride
+    // words: step t goes to buffer t & 1) and flag array, over NVLink
     uint32_t* const* peer_bits;   // [world] device pointers (peer or local)
+    int32_t xstride;              // words per parity buffer
     int32_t* const* peer_flags;   // [world] -> int32[world]; flag[src] = last step src published
     uint32_t* done;               // CTA completion counter of this launch
     int32_t rank;
@@ -66,7 +68,7 @@ struct NeuronArgs {
 
 struct HistArgs {
     int32_t n;
-    const uint32_t* bits;      // full spike bitmask of step t
+    uint32_t* bits;            // full spike bitmask of step t (k_hist rebuilds it from xbits in p2p mode)
     uint64_t* hist;            // [hw][n]; bit k of the concatenation = s[t-k]
     int32_t hw;
     int32_t dmax;              // propagation delay span (bits 0..dmax-1)
@@ -87,6 +89,8 @@ struct HistArgs {
     unsigned long long* active_count;  // running sum of active rows (algorithmic bytes)
     // peer-to-peer exchange: wait until every rank published step t (flags[q] > t)
     const int32_t* flags;              // this rank's int32[world] (written by peers) or null
+    const uint32_t* xbits;             // this rank's exchange bitmask [2][xstride] (peers store step t into t & 1)
+    int32_t xstride;
     int32_t world;
     int32_t* error;                    // set to 1 when the wait times out
 };
@@ -103,8 +107,8 @@ struct DenseArgs {
     const uint32_t* active;    // [words]
     const uint64_t* hist;      // word 0 of the history
     const uint32_t* bits;      // spike bitmask (column spikes s_j[t])
-    const void* pot;           // WT [n][dp]
-    const void* dep;           // WT [n]
+    const double* pot;         // [n][dp] fp64 traces (the STDP math is fp64 for every weight type)
+    const double* dep;         // [n]
     int32_t dp;
     double w_min, w_max;
     int32_t tile_w;            // columns per CTA tile (multiple of VEC)
@@ -133,8 +137,8 @@ struct SparseArgs {
     const uint32_t* bits;
     const uint32_t* hist_lo;
     const uint64_t* hist;
-    const void* pot;
-    const void* dep;
+    const double* pot;         // [n][dp] fp64
+    const double* dep;         // [n]
     int32_t dp;
     double w_min, w_max;
     int32_t posts_per_cta;
@@ -177,11 +181,11 @@ void launch_dense(const DenseArgs& a, bool f64, bool stdp, bool delay, bool exac
 int dense_vec(bool f64);
 int dense_threads();
 int dense_stream_max_ctas(bool f64, bool stdp, bool delay);  // occupancy x SMs
-// TMA-staged sweep (fp32/fp64, optional delays): one CTA per SM, rows_per_chunk <= dense_tma_max_rows();
+// TMA-staged sweep (fp32/fp64, optional delays): one CTA per SM, rows_per_chunk <= dense_tma_max_rows(...);
 // with delays the tile width must be a multiple of 16 (the delay bytes are bulk-copied)
-int dense_tma_max_rows();
 int dense_tma_max_dp();  // delayed STDP: plastic delay span the TMA sweep supports
-bool dense_tma_fits(int tile_w, bool f64, bool delay, bool stdp);  // ring + row lists within the smem opt-in
+int dense_tma_partials_per_chunk();  // partial rows the TMA sweep writes per row chunk
+int dense_tma_max_rows(int tile_w, bool f64, bool delay, bool stdp);  // longest row list whose buffers fit (0: none)
 void launch_dense_tma(const DenseArgs& a, bool f64, bool stdp, bool delay, int grid, cudaStream_t s);
 void launch_sparse(const SparseArgs& a, bool f64, bool stdp, int hbits, int sub, bool exact,
                    int grid_x, cudaStream_t s);

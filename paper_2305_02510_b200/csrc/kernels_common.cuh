@@ -80,6 +80,29 @@ __device__ __forceinline__ T clamp_ref(T v, T lo, T hi) {
     return v < lo ? lo : (hi < v ? hi : v);
 }
 
+// One plastic synapse (mat_engine.cpp:243-248): dw = 0; if s_post dw += pot_pre;
+// if s_pre dw -= dep_post; w = clamp(w + dw, w_min, w_max), with the traces,
+// dw and w + dw in fp64 like the reference.  dw: one subtraction of selected
+// operands gives the reference's value in every case (0 + pot = pot,
+// pot - dep rounded once, 0 - dep, +0).  fp32 storage rounds w + dw once;
+// rounding is monotone, so RN(clamp(x, lo, hi)) == clamp(RN(x), RN(lo),
+// RN(hi)) and the clamp runs in fp32 on bounds rounded the same way (min/max:
+// identical to clamp_ref for the NaN-free values here, up to the sign of a
+// zero weight).
+__device__ __forceinline__ double stdp_dw(bool s_post, double pot, bool s_pre, double dep) {
+    return (s_post ? pot : 0.0) - (s_pre ? dep : 0.0);
+}
+template <typename WT>
+__device__ __forceinline__ WT stdp_apply(WT w, double dw, WT lo, WT hi);
+template <>
+__device__ __forceinline__ double stdp_apply<double>(double w, double dw, double lo, double hi) {
+    return clamp_ref<double>(w + dw, lo, hi);
+}
+template <>
+__device__ __forceinline__ float stdp_apply<float>(float w, double dw, float lo, float hi) {
+    return fminf(fmaxf(__double2float_rn(static_cast<double>(w) + dw), lo), hi);
+}
+
 __device__ __forceinline__ uint32_t bit_of(const uint32_t* bits, int i) {
     return (__ldcg(bits + (i >> 5)) >> (i & 31)) & 1u;
 }
@@ -242,9 +265,10 @@ __device__ __forceinline__ uint32_t neuron_step(const NeuronArgs& a, const HistA
     const int wi = j >> 5;
     if (lane == 0 && wi < a.nl_words) {
         a.bits[(a.first >> 5) + wi] = word;
-        if (a.peer_bits)  // fused all-gather: store the word into every peer's bitmask (NVLink)
-            for (int q = 0; q < a.world; ++q)
-                if (q != a.rank) a.peer_bits[q][(a.first >> 5) + wi] = word;
+        if (a.peer_bits) {  // fused all-gather: store the word into every rank's exchange buffer t & 1 (NVLink)
+            const int64_t o = static_cast<int64_t>(t & 1) * a.xstride + (a.first >> 5) + wi;
+            for (int q = 0; q < a.world; ++q) a.peer_bits[q][o] = word;
+        }
         if (a.raster && (t - a.t_base) < a.raster_rows)
             a.raster[static_cast<int64_t>(t - a.t_base) * a.nl_words + wi] = word;
         if (WARP_COUNT && word) atomicAdd(a.spike_count, static_cast<unsigned long long>(__popc(word)));
@@ -324,7 +348,8 @@ __device__ __forceinline__ void dense_stream_body(const DenseArgs& a, int cta, i
     using V = typename VT::V;
     constexpr int VEC = VT::N;
     constexpr int U = 8;
-    __shared__ RowRec<WT> s_rec[kSubRows + U];
+    using Rec = RowRec<double>;  // fp64 trace for both weight types (fp64 STDP math)
+    __shared__ Rec s_rec[kSubRows + U];
     __shared__ uint32_t s_word[32];
     __shared__ int32_t s_wpref[33];
 
@@ -332,8 +357,8 @@ __device__ __forceinline__ void dense_stream_body(const DenseArgs& a, int cta, i
     const int ntiles = (a.nl + a.tile_w - 1) / a.tile_w;
     const int items = ntiles * a.nchunks;
     const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
-    const WT* pot = static_cast<const WT*>(a.pot);
-    const WT* dep = static_cast<const WT*>(a.dep);
+    const double* pot = a.pot;
+    const double* dep = a.dep;
     WT* W = static_cast<WT*>(a.w);
     const int64_t mpitch = a.pitch >> 5;
 
@@ -357,13 +382,14 @@ __device__ __forceinline__ void dense_stream_body(const DenseArgs& a, int cta, i
         const int r0 = chunk * a.rows_per_chunk;
         const int r1 = min(a.n, r0 + a.rows_per_chunk);
 
-        WT sjf[VEC], depj[VEC];
+        bool sj[VEC];
+        double depj[VEC];
         double acc[VEC];
 #pragma unroll
         for (int k = 0; k < VEC; ++k) {
             const bool ok = in_tile && (c0 + k) < a.nl;
-            sjf[k] = (ok && STDP && bit_of(a.bits, gc0 + k)) ? WT(1) : WT(0);
-            depj[k] = (ok && STDP) ? __ldcg(dep + gc0 + k) : WT(0);
+            sj[k] = ok && STDP && bit_of(a.bits, gc0 + k);
+            depj[k] = (ok && STDP) ? __ldcg(dep + gc0 + k) : 0.0;
             acc[k] = 0.0;
         }
 
@@ -401,21 +427,21 @@ __device__ __forceinline__ void dense_stream_body(const DenseArgs& a, int cta, i
                 if ((wd >> b) & 1u) {
                     const int pos = s_wpref[l] + __popc(wd & ((1u << b) - 1u));
                     const uint64_t h = __ldcg(a.hist + r);
-                    RowRec<WT> rec;
+                    Rec rec;
                     const int kind = STDP ? static_cast<int>(__ldg(a.kind + r)) : 0;
                     rec.rowk = r | (kind << 28);
                     rec.e_lo = static_cast<uint32_t>(h);
                     rec.e_hi = static_cast<uint32_t>(h >> 32);
-                    rec.pot = (STDP && !DELAY) ? __ldcg(pot + r) : WT(0);
+                    rec.pot = (STDP && !DELAY) ? __ldcg(pot + r) : 0.0;
                     s_rec[pos] = rec;
                 }
             }
             const int cnt = s_wpref[32];
             if (tid < U && cnt > 0) {  // inert padding: re-reads row sa, no spike, no store
-                RowRec<WT> rec;
+                Rec rec;
                 rec.rowk = sa;
                 rec.e_lo = rec.e_hi = 0;
-                rec.pot = WT(0);
+                rec.pot = 0.0;
                 s_rec[cnt + tid] = rec;
             }
             __syncthreads();
@@ -439,7 +465,7 @@ __device__ __forceinline__ void dense_stream_body(const DenseArgs& a, int cta, i
                 for (int k = 0; k < VEC; ++k) grp[k] = WT(0);
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const RowRec<WT> rec = s_rec[gb + u];
+                    const Rec rec = s_rec[gb + u];
                     const int row = rec.rowk & 0x0fffffff;
                     const int kind = rec.rowk >> 28;
                     const uint64_t ebits = (static_cast<uint64_t>(rec.e_hi) << 32) | rec.e_lo;
@@ -454,16 +480,14 @@ __device__ __forceinline__ void dense_stream_body(const DenseArgs& a, int cta, i
                         WT nw[VEC];
 #pragma unroll
                         for (int k = 0; k < VEC; ++k) {
-                            WT p;
+                            double p;
                             if (DELAY) {
                                 const int d1 = static_cast<int>((dv[u] >> (8 * k)) & 0xffu) - 1;
                                 p = __ldcg(pot + static_cast<int64_t>(row) * a.dp + d1);
                             } else {
                                 p = rec.pot;
                             }
-                            // dw = s_post*pot - s_pre*dep (mat_engine.cpp:243-246); 0/1 factors are exact
-                            const WT dw = fma(sjf[k], p, -(ef[k] * depj[k]));
-                            nw[k] = clamp_ref<WT>(w[k] + dw, wmin, wmax);
+                            nw[k] = stdp_apply<WT>(w[k], stdp_dw(sj[k], p, ef[k] != WT(0), depj[k]), wmin, wmax);
                         }
                         if (kind == kRowAllButSelf) {
                             const int selfk = row - gc0;   // (i, i) is absent: keep it exactly

@@ -15,6 +15,7 @@ from __future__ import annotations
 import json
 import math
 from dataclasses import dataclass
+from decimal import Decimal
 from typing import List, Optional
 
 import numpy as np
@@ -40,17 +41,30 @@ def _num(v: float) -> str:
 
 
 def _shortest(v: float) -> str:
-    """std::to_chars(double) shortest form (io.cpp:17-21): 2 not 2.0, 1e-05 style."""
+    """std::to_chars(double) with no format (io.cpp:17-21): the shortest
+    round-trip digits (those of repr), written in fixed or scientific notation,
+    whichever has fewer characters, fixed on a tie -- so 2 (not 2.0), 0.001,
+    1e-04, 1e+05, 1.5e-07, 123456; a fixed integral value prints all its exact
+    digits (531527556293501632, not ...630)."""
     f = float(v)
-    if f == int(f) and abs(f) < 1e16:
-        return str(int(f))
-    r = repr(f)
-    if "e" in r:
-        mant, exp = r.split("e")
-        sign = "-" if exp.startswith("-") else "+"
-        digits = exp.lstrip("+-").lstrip("0") or "0"
-        return f"{mant}e{sign}{digits.zfill(2)}"
-    return r
+    if not math.isfinite(f):
+        raise FormatError("non-finite number")
+    if f == 0.0:
+        return "-0" if math.copysign(1.0, f) < 0 else "0"
+    sign, digs, exp = Decimal(repr(f)).as_tuple()
+    full = "".join(map(str, digs))
+    d = full.rstrip("0")            # value = d * 10**e, d without trailing zeros
+    e = exp + len(full) - len(d)
+    k = len(d)
+    if e >= 0:   # integral: printf("%.0f")'s exact digits, same width as d + "0" * e
+        fixed = str(int(abs(f)))
+    else:
+        point = k + e
+        fixed = d[:point] + "." + d[point:] if point > 0 else "0." + "0" * (-point) + d
+    x = k - 1 + e
+    sci = d[0] + ("." + d[1:] if k > 1 else "") + "e" + ("-" if x < 0 else "+") + str(abs(x)).zfill(2)
+    out = fixed if len(fixed) <= len(sci) else sci
+    return ("-" if sign else "") + out
 
 
 def serialize_network(net: NetworkDef) -> str:

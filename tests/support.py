@@ -98,6 +98,16 @@ def stim_arrays(stim: StimulusSchedule):
     return stim.to_arrays()
 
 
+def fp32_weight_floor(steps, *weights) -> float:
+    """Rigorous bound on how far an fp32-stored weight can drift from the
+    reference's fp64 weight over `steps` STDP updates when every update is
+    computed in fp64 and rounded to float once: each rounding adds at most
+    half an ulp <= 2^-24 |w| and the clamp is 1-Lipschitz, so after the
+    initial rounding and T updates |w32 - w64| <= (T + 1) 2^-24 max|w|."""
+    m = max(float(np.max(np.abs(np.asarray(w, float)))) if np.size(w) else 0.0 for w in weights)
+    return (steps + 1) * 2.0 ** -24 * m
+
+
 def close_rel(a, b, rel=1e-5, abs_floor=1e-6):
     """|a-b| <= rel*|b| + abs_floor elementwise (north star: 1e-5 relative,
     absolute floor near 0 where weights clip to w_min)."""

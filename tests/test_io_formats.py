@@ -84,3 +84,25 @@ def test_committed_fixture_bytes():
     with open(os.path.join(GOLD, "io_raster.csv")) as f:
         rt = f.read()
     assert fio.write_raster(fio.parse_raster(rt)) == rt
+
+
+def test_shortest_matches_std_to_chars():
+    """io.cpp:17-21 renders numbers with std::to_chars(double): shortest
+    round-trip digits, fixed or scientific, whichever is shorter (fixed on a
+    tie).  tests/golden/to_chars.txt holds 4,000+ values rendered by libstdc++
+    (generator: tests/golden/to_chars_gen.cpp)."""
+    with open(os.path.join(GOLD, "to_chars.txt")) as f:
+        rows = [ln.split() for ln in f if ln.strip()]
+    assert len(rows) > 4000
+    bad = [(h, ref, fio._shortest(float.fromhex(h))) for h, ref in rows if fio._shortest(float.fromhex(h)) != ref]
+    assert not bad, bad[:5]
+    for v, s in ((1e-4, "1e-04"), (2e-4, "2e-04"), (1e5, "1e+05"), (1e6, "1e+06"), (1e15, "1e+15"),
+                 (0.001, "0.001"), (2.0, "2"), (123456.0, "123456")):
+        assert fio._shortest(v) == s
+
+
+@needs_ref_io
+def test_stimulus_small_and_large_amplitudes_byte_identical():
+    amps = [1e-4, 2e-4, 1e5, 1e6, 1e15, 0.001, 2.0, -3.5e-9, 531527556293501632.0]
+    stim = StimulusSchedule([StimulusEntry(i, i % 3, a) for i, a in enumerate(amps)])
+    assert fio.write_stimulus(stim) == B.ref_write_stimulus(stim.to_arrays())
