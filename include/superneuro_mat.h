@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SN_ABI_VERSION 1
+#define SN_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define SN_API __attribute__((visibility("default")))
@@ -232,6 +232,22 @@ SN_API sn_status sn_setup(sn_engine* e);
 SN_API sn_status sn_simulate(sn_engine* e, int32_t steps);
 /* Blocks until all queued device work of the engine is done. */
 SN_API sn_status sn_synchronize(sn_engine* e);
+/* One step of mat_step (mat_engine.cpp:168-208; the borrowed spike list of
+ * mat_engine.hpp:92-94): the step's external input is exactly `ext` -- n
+ * amplitudes, or ext_len = 0 for none (the stimulus schedule is not consulted
+ * for this step) -- followed by apply_stdp when STDP is configured and
+ * plasticity is on.  Writes the step's spiking ids ascending into `spikes`
+ * (capacity `cap`; spikes = NULL only reports *count).  ext_len other than 0
+ * or n: SN_ERR_INVALID_ARGUMENT "mat_step: ext must have one amplitude per
+ * neuron" (mat_engine.cpp:170-171).  Single-partition engines. */
+SN_API sn_status sn_step(sn_engine* e, const double* ext, int64_t ext_len, int32_t* spikes,
+                         int64_t cap, int64_t* count);
+/* Whether the following steps apply STDP (default on): off = mat_step
+ * without apply_stdp (mat_engine.hpp:92-98 exposes them separately).  The
+ * history and traces keep advancing, so re-enabling resumes exactly as the
+ * reference's apply_stdp would, including its first-call clamp of every
+ * plastic weight (mat_engine.cpp:243-249) on the first plastic step. */
+SN_API sn_status sn_set_plasticity(sn_engine* e, int32_t enabled);
 
 /* ---- results ------------------------------------------------------------ */
 /* Spike events of this partition since setup, (step, neuron) ascending. */
@@ -251,6 +267,11 @@ SN_API sn_status sn_get_synapse_weights(sn_engine* e, double* out, int64_t count
 /* Dense export of this partition's weight block W[pre][post_local]
  * (n x n_local doubles) -- absent synapses read 0 (test/debug helper). */
 SN_API sn_status sn_get_weight_matrix(sn_engine* e, double* out, int64_t count);
+/* Weight census on the device (dense storage; cfg5's 36.9 GB matrix cannot be
+ * read back): counts[k] = stored weights of the n x n_local block equal to
+ * values[k] rounded to the storage precision (k < count <= 8, first match),
+ * counts[count] = every other cell, absent synapses (stored 0) included. */
+SN_API sn_status sn_weight_value_counts(sn_engine* e, const double* values, int32_t count, int64_t* counts);
 SN_API sn_status sn_get_stats(sn_engine* e, sn_stats* out);
 SN_API sn_status sn_reset_stats(sn_engine* e);
 

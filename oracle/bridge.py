@@ -235,6 +235,20 @@ def run_ref_mat(arrays, steps, stim=None, stdp=None, record_membrane=False, stor
     return _collect(lib, r, steps)
 
 
+def run_ref_mat_masked(arrays, steps, stim, stdp, plastic_steps, storage=0, lower=False) -> dict:
+    """The reference's mat_step loop with apply_stdp only on steps whose
+    plastic_steps byte is non-zero (oracle/ref_shim.cpp mat_loop)."""
+    lib = ref_lib()
+    p, keep = make_problem(arrays, steps, stim, stdp)
+    mask = np.ascontiguousarray(plastic_steps, np.uint8)
+    assert len(mask) == steps
+    r = Result()
+    lib.ref_mat_run_masked.argtypes = [C.POINTER(Problem), C.c_int, C.c_int, C.POINTER(C.c_uint8), C.POINTER(Result)]
+    lib.ref_mat_run_masked(C.byref(p), storage, 1 if lower else 0, mask.ctypes.data_as(C.POINTER(C.c_uint8)),
+                           C.byref(r))
+    return _collect(lib, r, steps)
+
+
 def run_ref_mat_raster(arrays, steps, stim=None, stdp=None, storage=0) -> dict:
     lib = ref_lib()
     p, keep = make_problem(arrays, steps, stim, stdp)
@@ -366,6 +380,23 @@ def ref_bench_run(n, p, seed, horizon, warmup, steps, stdp_on, storage=0, delay_
     out.update({"setup_s": float(info[0]), "warmup_s": float(info[1]), "timed_s": float(info[2]),
                 "storage": {1: "dense", 0: "csr", -1: "abm"}[int(info[3])], "synapses": int(info[4]),
                 "peak_rss_gb": float(info[5]), "step_s": step_s[:steps].tolist()})
+    return out
+
+
+def ref_scenario_abm_raster(n, p, seed, steps, delay_max=1, by_index=False, delay_stream=0x64656C6179) -> dict:
+    """Raster of the reference's abm_run on a generated scenario (ref_shim.cpp
+    ref_scenario_abm_raster); also synapse count, build / run seconds, RSS."""
+    lib = ref_lib()
+    info = np.zeros(4)
+    r = Result()
+    dp = C.POINTER(C.c_double)
+    lib.ref_scenario_abm_raster.argtypes = [C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_int, C.c_int,
+                                            C.c_uint64, dp, C.POINTER(Result)]
+    lib.ref_scenario_abm_raster(n, p, seed, steps, delay_max, 1 if by_index else 0, delay_stream,
+                                info.ctypes.data_as(dp), C.byref(r))
+    out = _collect(lib, r, steps, with_state=False)
+    out.update({"synapses": int(info[0]), "build_s": float(info[1]), "run_s": float(info[2]),
+                "peak_rss_gb": float(info[3])})
     return out
 
 

@@ -145,8 +145,12 @@ struct MatOutcome {
     MatState st;
 };
 
+// plastic_steps (optional, one byte per step): apply_stdp only after the
+// mat_step of steps with a non-zero byte -- the reference's public API driven
+// like an engine whose plasticity is switched off for some steps.
 MatOutcome mat_loop(const NetworkDef& net, const SimulationConfig& cfg,
-                    const StimulusSchedule& stim, WeightStorage storage) {
+                    const StimulusSchedule& stim, WeightStorage storage,
+                    const uint8_t* plastic_steps = nullptr) {
     if (cfg.steps < 1) throw std::invalid_argument("mat_run: steps must be >= 1");
     MatOutcome o;
     o.st = mat_init(net, cfg, storage);
@@ -171,7 +175,7 @@ MatOutcome mat_loop(const NetworkDef& net, const SimulationConfig& cfg,
         }
         const std::vector<int>& spiked =
             mat_step(o.st, any_ext ? std::span<const double>(ext) : std::span<const double>());
-        if (cfg.stdp) apply_stdp(o.st, *cfg.stdp);
+        if (cfg.stdp && (!plastic_steps || plastic_steps[t])) apply_stdp(o.st, *cfg.stdp);
         for (int j : spiked) o.raster.events.push_back({t, j});
         if (cfg.record_membrane) o.trace.push_back(o.st.membrane);
         for (std::size_t k = first; k < cursor; ++k) ext[sorted[k].neuron] = 0.0;
@@ -220,13 +224,14 @@ void orc_result_free(orc_result* r) {
 // With lower != 0 the reference MAT path for delayed nets is used:
 // lower_delays -> mat_run -> restrict_raster (spikeforge_main.cpp:44-64);
 // final weights are read from each original synapse's last hop.
-int ref_mat_run(const orc_problem* p, int storage, int lower, orc_result* out) {
+int ref_mat_run_masked(const orc_problem* p, int storage, int lower, const uint8_t* plastic_steps,
+                       orc_result* out) {
     return guarded(out, [&] {
         const NetworkDef net = to_net(p);
         const SimulationConfig cfg = to_cfg(p);
         const StimulusSchedule stim = to_stim(p);
         if (!lower) {
-            MatOutcome o = mat_loop(net, cfg, stim, to_storage(storage));
+            MatOutcome o = mat_loop(net, cfg, stim, to_storage(storage), plastic_steps);
             put_raster(o.raster, out);
             std::vector<int64_t> slot_of(net.synapses.size());
             for (std::size_t s = 0; s < slot_of.size(); ++s) slot_of[s] = static_cast<int64_t>(s);
@@ -234,7 +239,7 @@ int ref_mat_run(const orc_problem* p, int storage, int lower, orc_result* out) {
             return;
         }
         const LoweredNetwork lw = lower_delays(net);
-        MatOutcome o = mat_loop(lw.net, cfg, stim, to_storage(storage));
+        MatOutcome o = mat_loop(lw.net, cfg, stim, to_storage(storage), plastic_steps);
         put_raster(restrict_raster(o.raster, lw.original_count), out);
         // lower_delays emits, per original synapse in order, 1 synapse when the
         // effective delay is 1, else d (the last one carries weight + stdp).
@@ -247,6 +252,10 @@ int ref_mat_run(const orc_problem* p, int storage, int lower, orc_result* out) {
         }
         put_state(o, lw.original_count, slot_of, out);
     });
+}
+
+int ref_mat_run(const orc_problem* p, int storage, int lower, orc_result* out) {
+    return ref_mat_run_masked(p, storage, lower, nullptr, out);
 }
 
 // mat_run itself (raster only), to pin mat_loop above against the real thing.
@@ -266,6 +275,41 @@ int ref_abm_run(const orc_problem* p, orc_result* out) {
         SimulationConfig cfg = to_cfg(p);
         cfg.stdp.reset();
         put_raster(abm_run(to_net(p), cfg, to_stim(p)).raster, out);
+    });
+}
+
+// Scale golden of a generated scenario: build_scenario(n, p, seed) with a
+// `steps`-step protocol, delays 1 + below_at(key, delay_max) on stream
+// delay_stream (key = pair index i*n + j, or the synapse index when by_index),
+// then the reference's native-delay path abm_run (== mat_run(lower_delays),
+// pinned by the small goldens).  The network is built in place (no orc_problem
+// copy): at N = 256,000, p = 0.01 it is 655 M synapses (~16 GB NetworkDef).
+int ref_scenario_abm_raster(int n, double p, uint64_t seed, int steps, int delay_max, int by_index,
+                            uint64_t delay_stream, double* info, orc_result* out) {
+    return guarded(out, [&] {
+        const auto s0 = std::chrono::steady_clock::now();
+        BenchScenario sc;
+        sc.neuron_count = n;
+        sc.connection_probability = p;
+        sc.steps = steps;
+        sc.seed = seed;
+        ScenarioBundle b = build_scenario(sc);
+        if (delay_max > 1) {
+            const RandomStream ds(seed, delay_stream);
+            for (std::size_t s = 0; s < b.net.synapses.size(); ++s) {
+                SynapseDef& y = b.net.synapses[s];
+                const uint64_t key = by_index ? static_cast<uint64_t>(s)
+                                              : static_cast<uint64_t>(y.pre) * static_cast<uint64_t>(n) + y.post;
+                y.delay = 1 + static_cast<int>(ds.below_at(key, static_cast<uint64_t>(delay_max)));
+            }
+        }
+        info[0] = static_cast<double>(b.net.synapses.size());
+        const auto s1 = std::chrono::steady_clock::now();
+        const RunResult r = abm_run(b.net, b.cfg, b.stim);
+        info[1] = std::chrono::duration<double>(s1 - s0).count();
+        info[2] = std::chrono::duration<double>(std::chrono::steady_clock::now() - s1).count();
+        info[3] = peak_rss_gb();
+        put_raster(r.raster, out);
     });
 }
 

@@ -23,7 +23,7 @@ SN_ERR_UNSUPPORTED = 6
 SN_STORAGE_AUTO, SN_STORAGE_DENSE, SN_STORAGE_SPARSE = 0, 1, 2
 SN_WEIGHTS_F32, SN_WEIGHTS_F64 = 0, 1
 SN_MODE_MAT, SN_MODE_ABM = 0, 1
-SN_ABI_VERSION = 1
+SN_ABI_VERSION = 2
 
 
 class Options(C.Structure):
@@ -114,6 +114,8 @@ SIGNATURES = {
     "sn_setup": (_i32, [_P]),
     "sn_simulate": (_i32, [_P, _i32]),
     "sn_synchronize": (_i32, [_P]),
+    "sn_step": (_i32, [_P, _pdbl, _i64, _pi32, _i64, _pi64]),
+    "sn_set_plasticity": (_i32, [_P, _i32]),
     "sn_raster_size": (_i32, [_P, _pi64]),
     "sn_get_raster": (_i32, [_P, _pi32, _pi32, _i64]),
     "sn_clear_raster": (_i32, [_P]),
@@ -122,6 +124,7 @@ SIGNATURES = {
     "sn_get_membrane_trace": (_i32, [_P, _pdbl, _i64]),
     "sn_get_synapse_weights": (_i32, [_P, _pdbl, _i64]),
     "sn_get_weight_matrix": (_i32, [_P, _pdbl, _i64]),
+    "sn_weight_value_counts": (_i32, [_P, _pdbl, _i32, _pi64]),
     "sn_get_stats": (_i32, [_P, C.POINTER(Stats)]),
     "sn_reset_stats": (_i32, [_P]),
     "sn_comm_id_size": (_i32, []),

@@ -295,6 +295,28 @@ sn_status sn_partition_range(int32_t n, int32_t rank, int32_t world, int32_t* fi
     });
 }
 
+sn_status sn_weight_value_counts(sn_engine* e, const double* values, int32_t count, int64_t* counts) {
+    return guard([&] {
+        SN_NEED(e);
+        e->impl.weight_value_counts(values, count, counts);
+    });
+}
+
+sn_status sn_step(sn_engine* e, const double* ext, int64_t ext_len, int32_t* spikes, int64_t cap,
+                  int64_t* count) {
+    return guard([&] {
+        SN_NEED(e);
+        e->impl.step(ext, ext_len, spikes, cap, count);
+    });
+}
+
+sn_status sn_set_plasticity(sn_engine* e, int32_t enabled) {
+    return guard([&] {
+        SN_NEED(e);
+        e->impl.set_plasticity(enabled != 0);
+    });
+}
+
 sn_status sn_step_local(sn_engine* e) {
     return guard([&] {
         SN_NEED(e);

@@ -13,6 +13,7 @@
 #include "nccl_dl.hpp"
 
 #include <algorithm>
+#include <limits>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -184,9 +185,9 @@ void Engine::add_stimulus(int64_t count, const int32_t* step, const int32_t* neu
         if (step[i] < 0)
             throw InvalidArgument(run_name() + ": " + who + ": step " + std::to_string(step[i]) + " is negative");
         if (!std::isfinite(amp[i])) throw InvalidArgument(run_name() + ": " + who + ": amplitude must be finite");
-        if (setup_done_ && (neuron[i] < 0 || neuron[i] >= n_))
+        if (setup_done_ && (neuron[i] < 0 || neuron[i] >= n_user_))
             throw InvalidArgument(run_name() + ": " + who + ": neuron id " + std::to_string(neuron[i]) +
-                                  " out of range (" + std::to_string(n_) + " neurons)");
+                                  " out of range (" + std::to_string(n_user_) + " neurons)");
     }
     st_step_.insert(st_step_.end(), step, step + count);
     st_neuron_.insert(st_neuron_.end(), neuron, neuron + count);
@@ -338,13 +339,98 @@ void Engine::validate() const {
                                   " neurons)");
 }
 
+// ---- delay relays ---------------------------------------------------------------
+// The sweeps read one 64-bit history word per pre, so effective delays (delay
+// + axonal of the pre) up to 64 are native.  A longer synapse i -> j (d > 64;
+// the reference accepts any delay, lowering.cpp:39-57) is rerouted through a
+// chain of relay neurons of i: relay k fires exactly 64 k steps after i
+// (threshold 0, infinite leak, reset 0, no refractory period, one weight-1
+// input: u = 1 > 0 iff its upstream spiked 64 steps earlier), and the synapse
+// leaves relay q = (d - 1) / 64 with delay d - 64 q in [1, 64].  Arrival times
+// are unchanged, and so is STDP: the engine pairs the pre train shifted by
+// d' - 1 through a synapse of delay d' (the lowered net's last proxy), and
+// relay q's train shifted by d - 64 q - 1 is i's train shifted by d - 1.
+// Relays live after the caller's neurons; their hops are appended after the
+// caller's synapses, which keep their list order.  Single partition only.
+void Engine::add_delay_relays() {
+    const int n = static_cast<int>(thr_.size());
+    const size_t m = pre_.size();
+    std::vector<int32_t> chain(static_cast<size_t>(n), 0);
+    bool any = false;
+    for (size_t s = 0; s < m; ++s) {
+        const int64_t d = static_cast<int64_t>(delay_[s]) + axonal_[pre_[s]];
+        if (d <= kMaxNativeDelay) continue;
+        if (axonal_[pre_[s]] >= kMaxNativeDelay)
+            throw Unsupported("mat_init: neurons[" + std::to_string(pre_[s]) + "] has axonal_delay " +
+                              std::to_string(axonal_[pre_[s]]) + "; axonal delays of 64 steps or more are unsupported");
+        chain[pre_[s]] = std::max<int32_t>(chain[pre_[s]], static_cast<int32_t>((d - 1) / kMaxNativeDelay));
+        any = true;
+    }
+    if (!any) return;
+    if (opt_.world > 1)
+        throw Unsupported("mat_init: delays over 64 steps are supported on single-partition engines only");
+    pre_user_ = pre_;
+    std::vector<int64_t> first_relay(static_cast<size_t>(n), -1);
+    for (int i = 0; i < n; ++i) {
+        if (!chain[i]) continue;
+        first_relay[i] = static_cast<int64_t>(thr_.size());
+        for (int k = 1; k <= chain[i]; ++k) {
+            const int32_t r = static_cast<int32_t>(thr_.size());
+            thr_.push_back(0.0);
+            leak_.push_back(std::numeric_limits<double>::infinity());
+            reset_.push_back(0.0);
+            refr_.push_back(0);
+            axonal_.push_back(0);
+            if (!fire_p_.empty()) fire_p_.push_back(1.0);
+            // hop into relay k: from i (its axonal delay counts) or from relay k - 1
+            pre_.push_back(k == 1 ? i : r - 1);
+            post_.push_back(r);
+            weight_.push_back(1.0);
+            delay_.push_back(k == 1 ? kMaxNativeDelay - axonal_[i] : kMaxNativeDelay);
+            plastic_.push_back(0);
+        }
+    }
+    if (thr_.size() > static_cast<size_t>(INT32_MAX)) throw InvalidArgument("mat_init: too many neurons with delay relays");
+    for (size_t s = 0; s < m; ++s) {
+        const int64_t d = static_cast<int64_t>(delay_[s]) + axonal_[pre_[s]];
+        if (d <= kMaxNativeDelay) continue;
+        const int64_t q = (d - 1) / kMaxNativeDelay;
+        delay_[s] = static_cast<int32_t>(d - q * kMaxNativeDelay);
+        pre_[s] = static_cast<int32_t>(first_relay[pre_[s]] + q - 1);
+    }
+    relays_ = true;
+}
+
+// Clears the relay neurons' bits of every raster row not yet stripped (ids
+// >= n_user_; single partition, so local ids are global ids).
+void Engine::strip_relays() {
+    if (!relays_) return;
+    for (RasterChunk& ch : raster_) {
+        if (ch.stripped) continue;
+        for (int r = 0; r < ch.rows; ++r) {
+            uint32_t* row = ch.words.data() + static_cast<size_t>(r) * nl_words_;
+            for (int w = n_user_ >> 5; w < nl_words_; ++w) {
+                const int lo = n_user_ - w * 32;  // bits below lo are user neurons
+                const uint32_t keep = lo >= 32 ? ~0u : lo <= 0 ? 0u : ((1u << lo) - 1u);
+                relay_spikes_ += __builtin_popcount(row[w] & ~keep);
+                row[w] &= keep;
+            }
+        }
+        ch.stripped = true;
+    }
+}
+
 // ---- setup -------------------------------------------------------------------
 void Engine::setup() {
+    NvtxRange nv("sn_setup");
     require_not_setup("sn_setup");
     cuda_check(cudaSetDevice(opt_.device), "cudaSetDevice");
     validate();
+    if (thr_.empty()) throw InvalidArgument(std::string(abm_ ? "abm world" : "mat_init") + ": the network has no neurons");
+    n_user_ = static_cast<int32_t>(thr_.size());
+    m_user_ = static_cast<int64_t>(pre_.size());
+    if (!generated_) add_delay_relays();
     n_ = static_cast<int32_t>(thr_.size());
-    if (n_ < 1) throw InvalidArgument(std::string(abm_ ? "abm world" : "mat_init") + ": the network has no neurons");
     if (!fire_p_.empty()) fire_p_.resize(static_cast<size_t>(n_), 1.0);
     any_stochastic_ = abm_ && std::any_of(fire_p_.begin(), fire_p_.end(), [](double p) { return p < 1.0; });
     partition(n_, opt_.rank, opt_.world, &first_, &nl_);
@@ -364,10 +450,7 @@ void Engine::setup() {
         if (er_.stdp) dp_ = er_delay_max_;
     } else {
         for (size_t s = 0; s < pre_.size(); ++s) {
-            const int64_t d = static_cast<int64_t>(delay_[s]) + axonal_[pre_[s]];
-            if (d > 64)
-                throw Unsupported("mat_init: synapses[" + std::to_string(s) + "] has effective delay " +
-                                  std::to_string(d) + "; this engine supports delays up to 64 steps");
+            const int64_t d = static_cast<int64_t>(delay_[s]) + axonal_[pre_[s]];  // <= 64 after the relays
             dmax_ = std::max<int32_t>(dmax_, static_cast<int32_t>(d));
             if (stdp_on_ && plastic_[s]) dp_ = std::max<int32_t>(dp_, static_cast<int32_t>(d));
         }
@@ -375,8 +458,6 @@ void Engine::setup() {
     has_delay_ = dmax_ > 1;
     hw_ = stdp_on_ ? static_cast<int32_t>((window_ + dp_ + 63) / 64) : 1;
     hw_ = std::max(hw_, 1);
-    if (hw_ > 8)
-        throw Unsupported("mat_init: STDP window + delay span exceeds the 512-step history of this engine");
     hbits_ = dmax_ == 1 ? 1 : dmax_ <= 16 ? 16 : dmax_ <= 32 ? 32 : 64;
 
     // storage choice (mat_engine.cpp:27-30 switches at n > 12000; here the
@@ -417,7 +498,7 @@ void Engine::setup() {
     setup_done_ = true;
     stats_.synapses_local = syn_local_;
     stats_.dense = dense_ ? 1 : 0;
-    stats_.n_local = nl_;
+    stats_.n_local = relays_ ? n_user_ : nl_;
     stats_.first_local = first_;
     stats_.max_delay = dmax_;
 }
@@ -446,10 +527,8 @@ void Engine::alloc_state() {
     cuda_check(cudaMemsetAsync(d_hist_lo_.p, 0, d_hist_lo_.bytes, stream_), "memset");
     const size_t np = static_cast<size_t>(n_) * (stdp_on_ ? dp_ : 1);
     d_pot64_.alloc(np * 8);
-    d_pot32_.alloc(np * 4);
     d_dep64_.alloc(static_cast<size_t>(n_) * 8);
-    d_dep32_.alloc(static_cast<size_t>(n_) * 4);
-    for (DevBuf* b : {&d_pot64_, &d_pot32_, &d_dep64_, &d_dep32_})
+    for (DevBuf* b : {&d_pot64_, &d_dep64_})
         cuda_check(cudaMemsetAsync(b->p, 0, b->bytes, stream_), "memset");
     if (stdp_on_) {
         upload(stream_, d_ap_, a_plus_);

@@ -66,6 +66,7 @@ struct RasterChunk {
     int32_t t0 = 0;
     int32_t rows = 0;
     std::vector<uint32_t> words;  // rows x nl_words
+    bool stripped = false;        // relay neurons' bits cleared (Engine::strip_relays)
 };
 
 struct NcclComm;  // nccl_dl.cpp
@@ -98,6 +99,7 @@ public:
     void get_trace(double* out, int64_t count);
     void get_synapse_weights(double* out, int64_t count);
     void get_weight_matrix(double* out, int64_t count);
+    void weight_value_counts(const double* values, int32_t count, int64_t* counts);
     void get_stats(sn_stats* out);
     void reset_stats();
 
@@ -107,6 +109,12 @@ public:
     void p2p_get_handles(uint8_t* out, int64_t cap);
     void p2p_open(const uint8_t* all_handles, int32_t world);
     static void p2p_connect_local(Engine* const* engines, int32_t world);
+    // mat_step (mat_engine.cpp:168-208): one step whose external input is
+    // exactly `ext` (n amplitudes, or none), returning its spikes ascending;
+    // apply_stdp follows when plasticity is on (mat_run:277-279)
+    void step(const double* ext, int64_t ext_len, int32_t* spikes, int64_t cap, int64_t* count);
+    // whether steps apply STDP (mat_run with / without apply_stdp after mat_step)
+    void set_plasticity(bool on);
     void step_local();
     void get_spike_words(uint32_t* out, int64_t words);
     void put_spike_words(int32_t first_word, const uint32_t* w, int64_t count);
@@ -226,7 +234,7 @@ private:
     DevBuf d_off_, d_meta_;
     DevBuf d_v_, d_thr_, d_leak_, d_reset_, d_refr_, d_cnt_;
     DevBuf d_bits_, d_hist_, d_hist_lo_, d_active_;
-    DevBuf d_pot64_, d_pot32_, d_dep64_, d_dep32_, d_ap_, d_am_;
+    DevBuf d_pot64_, d_dep64_, d_ap_, d_am_;
     DevBuf d_partial_, d_uexact_;
     DevBuf d_step_, d_spikes_, d_work_;
     DevBuf d_st_off_, d_st_neuron_, d_st_amp_;
@@ -269,6 +277,21 @@ private:
     void set_peer_tables(const std::vector<uint32_t*>& bits, const std::vector<int32_t*>& flags);
     void check_exchange_error();
     bool host_exchange_ = false;
+    // delay relays (effective delays > kMaxNativeDelay): relay neurons appended
+    // after the user's, raster bits of ids >= n_user_ stripped on the host
+    static constexpr int kMaxNativeDelay = 64;
+    void add_delay_relays();
+    void strip_relays();
+    bool relays_ = false;
+    int32_t n_user_ = 0;          // neurons the caller added (== n_ without relays)
+    int64_t m_user_ = 0;          // synapses the caller added
+    std::vector<int32_t> pre_user_;
+    int64_t relay_spikes_ = 0;    // relay spikes seen in stripped raster rows
+    bool plasticity_ = true;      // sn_set_plasticity
+    int32_t clamp_step_ = -1;     // first step that applied STDP (HistArgs::clamp_step), -1 = none yet
+    void note_first_plastic_step() {
+        if (stdp_on_ && plasticity_ && clamp_step_ < 0) clamp_step_ = t_;
+    }
 };
 
 }  // namespace snb

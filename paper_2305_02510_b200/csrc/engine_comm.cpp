@@ -19,9 +19,15 @@ void Engine::comm_init(const uint8_t* id, int32_t rank, int32_t world) {
     if (world != opt_.world || rank != opt_.rank)
         throw InvalidArgument("sn_comm_init: rank/world differ from the engine options");
     cuda_check(cudaSetDevice(opt_.device), "cudaSetDevice");
+    if (world == 1 && (tiny_ || persistent_))
+        throw LogicError("sn_comm_init: this single-partition engine runs whole simulate calls in one kernel "
+                         "(create it with persistent = 0 and a dense or sparse storage)");
     delete comm_;
     comm_ = nullptr;
-    if (world > 1) comm_ = new NcclComm(id, rank, world);
+    // world 1: a one-rank communicator switches the engine to the partitioned
+    // step sequence (k_neuron -> in-graph ncclAllGather -> k_hist -> sweep),
+    // the exact launch sequence of every rank of an N-GPU run
+    comm_ = new NcclComm(id, rank, world);
 }
 
 // ---- peer-to-peer exchange ---------------------------------------------------

@@ -19,6 +19,8 @@ namespace snb {
 // prefix sum, then rows decoded in parallel straight into the two arrays.
 void Engine::decode_raster() {
     if (events_valid_) return;
+    NvtxRange nv("raster decode");
+    strip_relays();
     std::vector<std::pair<const uint32_t*, int32_t>> rows;  // (words, step)
     for (const RasterChunk& ch : raster_)
         for (int r = 0; r < ch.rows; ++r)
@@ -97,6 +99,7 @@ void Engine::get_raster(int32_t* steps, int32_t* neurons, int64_t cap) {
 }
 
 void Engine::clear_raster() {
+    strip_relays();  // count the relay spikes of the dropped rows first (stats)
     raster_.clear();
     dec_rows_.clear();
     dec_start_.clear();
@@ -105,21 +108,28 @@ void Engine::clear_raster() {
 
 void Engine::get_membrane(double* out, int64_t count) {
     require_setup("sn_get_membrane");
-    if (count < nl_) throw InvalidArgument("sn_get_membrane: buffer smaller than the local neuron count");
-    if (nl_) d2h(out, d_v_.p, static_cast<size_t>(nl_) * 8, "membrane D2H");
+    const int32_t nv = relays_ ? n_user_ : nl_;  // relay neurons are internal
+    if (count < nv) throw InvalidArgument("sn_get_membrane: buffer smaller than the local neuron count");
+    if (nv) d2h(out, d_v_.p, static_cast<size_t>(nv) * 8, "membrane D2H");
 }
 
 int64_t Engine::trace_rows() { return trace_rows_; }
 
 void Engine::get_trace(double* out, int64_t count) {
-    if (count < static_cast<int64_t>(trace_.size())) throw InvalidArgument("sn_get_membrane_trace: buffer too small");
-    std::memcpy(out, trace_.data(), trace_.size() * 8);
+    const int64_t nv = relays_ ? n_user_ : nl_;
+    if (count < trace_rows_ * nv) throw InvalidArgument("sn_get_membrane_trace: buffer too small");
+    if (nv == nl_) {
+        std::memcpy(out, trace_.data(), trace_.size() * 8);
+        return;
+    }
+    for (int64_t r = 0; r < trace_rows_; ++r)  // drop the relay columns
+        std::memcpy(out + r * nv, trace_.data() + r * nl_, static_cast<size_t>(nv) * 8);
 }
 
 void Engine::get_synapse_weights(double* out, int64_t count) {
     require_setup("sn_get_synapse_weights");
     if (generated_) throw Unsupported("sn_get_synapse_weights: generated networks have no synapse list; use sn_get_weight_matrix");
-    if (count < static_cast<int64_t>(pre_.size())) throw InvalidArgument("sn_get_synapse_weights: buffer too small");
+    if (count < m_user_) throw InvalidArgument("sn_get_synapse_weights: buffer too small");
     cuda_check(cudaStreamSynchronize(stream_), "sync");
     const size_t esz = f64_ ? 8 : 4;
     std::vector<uint8_t> host(d_w_.bytes);
@@ -129,7 +139,7 @@ void Engine::get_synapse_weights(double* out, int64_t count) {
         meta.resize(static_cast<size_t>(sparse_elems_));
         if (!meta.empty()) d2h(meta.data(), d_meta_.p, meta.size() * 4, "meta D2H");
     }
-    for (size_t s = 0; s < pre_.size(); ++s) {
+    for (size_t s = 0; s < static_cast<size_t>(m_user_); ++s) {  // relay hops follow the caller's synapses
         if (slot_[s] < 0) { out[s] = 0.0; continue; }
         if (bank_ordered_) { out[s] = dict_[0]; continue; }  // lists reordered; one weight
         if (!meta.empty()) out[s] = dict_[meta[slot_[s]] >> 23];
@@ -138,8 +148,43 @@ void Engine::get_synapse_weights(double* out, int64_t count) {
     }
 }
 
+// Census of the dense weight block W[0:n][0:n_local] on the device: how many
+// stored weights equal each of `values` (rounded to the storage precision);
+// counts[count] = every other cell, absent synapses (stored 0) included.
+void Engine::weight_value_counts(const double* values, int32_t count, int64_t* counts) {
+    require_setup("sn_weight_value_counts");
+    if (!dense_ || tiny_ || relays_) throw Unsupported("sn_weight_value_counts: dense weight storage (no delay relays) only");
+    if (count < 0 || count > census_max_values())
+        throw InvalidArgument("sn_weight_value_counts: 0.." + std::to_string(census_max_values()) + " values");
+    if ((count && !values) || !counts) throw InvalidArgument("sn_weight_value_counts: null parameter array");
+    DevBuf dv, dc;
+    if (f64_) {
+        upload(stream_, dv, std::vector<double>(values, values + count));
+    } else {
+        std::vector<float> f(static_cast<size_t>(count));
+        for (int k = 0; k < count; ++k) f[k] = static_cast<float>(values[k]);
+        upload(stream_, dv, f);
+    }
+    dc.alloc(static_cast<size_t>(count + 1) * 8);
+    cuda_check(cudaMemsetAsync(dc.p, 0, dc.bytes, stream_), "memset");
+    int dev = 0, sms = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    launch_value_counts(d_w_.p, f64_, pitch_, n_, nl_, dv.p, count, dc.as<unsigned long long>(),
+                        std::min(n_, sms * 8), stream_);
+    d2h(counts, dc.p, dc.bytes, "counts D2H");
+}
+
 void Engine::get_weight_matrix(double* out, int64_t count) {
     require_setup("sn_get_weight_matrix");
+    if (relays_) {  // the caller's n x n matrix: each synapse at its own (pre, post), relays hidden
+        if (count < static_cast<int64_t>(n_user_) * n_user_) throw InvalidArgument("sn_get_weight_matrix: buffer too small");
+        std::vector<double> w(static_cast<size_t>(m_user_));
+        get_synapse_weights(w.data(), m_user_);
+        std::fill(out, out + static_cast<int64_t>(n_user_) * n_user_, 0.0);
+        for (int64_t s = 0; s < m_user_; ++s) out[static_cast<int64_t>(pre_user_[s]) * n_user_ + post_[s]] = w[s];
+        return;
+    }
     if (count < static_cast<int64_t>(n_) * nl_) throw InvalidArgument("sn_get_weight_matrix: buffer too small");
     cuda_check(cudaStreamSynchronize(stream_), "sync");
     std::fill(out, out + static_cast<int64_t>(n_) * nl_, 0.0);
@@ -174,7 +219,8 @@ void Engine::get_stats(sn_stats* out) {
     if (setup_done_) {
         unsigned long long c[2] = {0, 0};
         d2h(c, d_spikes_.p, 16, "stats D2H");
-        stats_.spike_count = static_cast<int64_t>(c[0]);
+        strip_relays();
+        stats_.spike_count = static_cast<int64_t>(c[0]) - relay_spikes_;  // the caller's neurons only
         // algorithmic bytes: every visited row (dense) or every stored synapse (sparse pull)
         if (dense_) {
             const double per_row = static_cast<double>(nl_) * ((stdp_on_ ? 2.0 : 1.0) * (f64_ ? 8 : 4) + (has_delay_ ? 1 : 0));

@@ -44,6 +44,7 @@ void Engine::run_tiny(int t0, int steps, uint32_t* raster, double* trace, bool h
     a.a_minus = d_am_.as<double>();
     a.w_min = w_min_;
     a.w_max = w_max_;
+    a.plastic_on = plasticity_ ? 1 : 0;
     a.spike_count = d_spikes_.as<unsigned long long>();
     a.d_step = d_step_.as<int32_t>();
     a.abm = abm_ ? 1 : 0;
@@ -168,14 +169,13 @@ HistArgs Engine::hist_args() {
     h.a_plus = d_ap_.as<double>();
     h.a_minus = d_am_.as<double>();
     h.pot64 = d_pot64_.as<double>();
-    h.pot32 = d_pot32_.as<float>();
     h.dep64 = d_dep64_.as<double>();
-    h.dep32 = d_dep32_.as<float>();
     h.row_plastic = d_row_plastic_.as<uint8_t>();
     h.active = d_active_.as<uint32_t>();
     h.d_step = d_step_.as<int32_t>();
     h.hist_lo = (!dense_ && (hbits_ == 16 || hbits_ == 32)) ? d_hist_lo_.as<uint32_t>() : nullptr;
     h.active_count = d_spikes_.as<unsigned long long>() + 1;
+    h.clamp_step = clamp_step_;
     if (p2p_) {
         h.flags = d_flags_.as<int32_t>();
         h.xbits = d_xbits_.as<uint32_t>();
@@ -215,6 +215,7 @@ DenseArgs Engine::dense_args() {
     a.d_step = d_step_.as<int32_t>();
     a.work = ((dynamic_sched_ || tma_) && !exact_ && !persistent_) ? d_work_.as<int32_t>() : nullptr;
     a.abm = abm_ ? 1 : 0;
+    a.plastic_on = plasticity_ ? 1 : 0;
     return a;
 }
 
@@ -252,6 +253,7 @@ void Engine::launch_sweep_only() {
         a.u_exact = d_uexact_.as<double>();
         a.d_step = d_step_.as<int32_t>();
         a.abm = abm_ ? 1 : 0;
+        a.plastic_on = plasticity_ ? 1 : 0;
         if (nl_ == 0) {
             launch_step_bump(a.d_step, stream_);
         } else if (sparse_tma_) {
@@ -279,14 +281,18 @@ cudaEvent_t Engine::get_event() {
 
 void Engine::enqueue_step(const NeuronArgs& na, bool exchange) {
     const bool prof = opt_.profile != 0;
-    const bool fused = opt_.world == 1;
+    const bool fused = opt_.world == 1 && !comm_;  // a 1-rank communicator runs the partitioned sequence
     const HistArgs h = hist_args();
     cudaEvent_t e0{}, e1{}, e2{}, e3{};
     if (prof) { e0 = get_event(); cuda_check(cudaEventRecord(e0, stream_), "rec"); }
-    launch_neuron(na, exact_, fused, h, stream_);
+    {
+        NvtxRange nv("neuron phase");
+        launch_neuron(na, exact_, fused, h, stream_);
+    }
     stats_.kernel_launches += 1;
     if (prof) { e1 = get_event(); cuda_check(cudaEventRecord(e1, stream_), "rec"); pending_.push_back({e0, e1, 0, 0.0}); }
     if (!fused && exchange) {
+        NvtxRange nv("spike exchange + history");
         if (prof) { e0 = get_event(); cuda_check(cudaEventRecord(e0, stream_), "rec"); }
         if (comm_ && !p2p_) comm_->all_gather_inplace(d_bits_.as<uint32_t>(), static_cast<size_t>(part_ / 32), stream_);
         launch_hist(h, stream_);
@@ -294,7 +300,10 @@ void Engine::enqueue_step(const NeuronArgs& na, bool exchange) {
         if (prof) { e1 = get_event(); cuda_check(cudaEventRecord(e1, stream_), "rec"); pending_.push_back({e0, e1, 2, 0.0}); }
     }
     if (prof) { e2 = get_event(); cuda_check(cudaEventRecord(e2, stream_), "rec"); }
-    launch_sweep();
+    {
+        NvtxRange nv("sweep");
+        launch_sweep();
+    }
     if (prof) { e3 = get_event(); cuda_check(cudaEventRecord(e3, stream_), "rec"); pending_.push_back({e2, e3, 1, 0.0}); }
 }
 
@@ -307,12 +316,13 @@ void Engine::enqueue_step(const NeuronArgs& na, bool exchange) {
 double Engine::run_graph_chunks(const NeuronArgs& na, int steps) {
     const int chunk = std::min(steps, 64);
     const bool prof = opt_.profile != 0;
-    const bool fused = opt_.world == 1;
+    const bool fused = opt_.world == 1 && !comm_;  // a 1-rank communicator runs the partitioned sequence
     const int per = 6;
     std::vector<cudaEvent_t> ev(prof ? static_cast<size_t>(chunk) * per : 0);
     for (auto& e : ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
     const HistArgs h = hist_args();
     auto capture = [&](int k) {
+        NvtxRange nv("step graph capture");
         cudaGraph_t g;
         cudaGraphExec_t ge;
         cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
@@ -343,6 +353,7 @@ double Engine::run_graph_chunks(const NeuronArgs& na, int steps) {
     const int per_step_kernels = fused ? 2 : 3;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spans;
     double total = 0.0;
+    NvtxRange nv_replay("step graph replay");
     for (int done = 0; done < steps;) {
         const int k = std::min(chunk, steps - done);
         cudaEvent_t c0 = get_event(), c1 = get_event();
@@ -398,12 +409,14 @@ void Engine::flush_pending() {
 }
 
 void Engine::simulate(int32_t steps) {
+    NvtxRange nv("sn_simulate");
     require_setup("sn_simulate");
     if (steps < 1) throw InvalidArgument(run_name() + ": steps must be >= 1");
     if (opt_.world > 1 && !comm_ && !p2p_)
         throw LogicError("sn_simulate: partitioned engine needs sn_comm_init or sn_p2p_open "
                          "(or use sn_step_local/sn_step_finish)");
     cuda_check(cudaSetDevice(opt_.device), "cudaSetDevice");
+    note_first_plastic_step();
     build_stimulus_table();
     const int t0 = t_;
     double* trace = nullptr;
@@ -515,6 +528,7 @@ void Engine::simulate(int32_t steps) {
                 ca.window = window_;
                 ca.dmax = dmax_;
                 ca.active_count = d_spikes_.as<unsigned long long>() + 1;
+                ca.clamp_step = clamp_step_;
                 // activity and raster words are OR-ed by 8-post groups: start from
                 // zero, and keep the OR targets in device memory (atomics on mapped
                 // host memory would cross PCIe one by one); stream_io copies the
@@ -582,10 +596,78 @@ void Engine::simulate(int32_t steps) {
 void Engine::synchronize() { cuda_check(cudaStreamSynchronize(stream_), "sn_synchronize"); }
 
 // ---- host-driven exchange (partition emulation / custom transports) ---------
+void Engine::set_plasticity(bool on) {
+    if (!stdp_on_ && on) {
+        plasticity_ = true;  // nothing to apply; a no-op like calling mat_run without an StdpConfig
+        return;
+    }
+    plasticity_ = on;
+}
+
+void Engine::step(const double* ext, int64_t ext_len, int32_t* spikes, int64_t cap, int64_t* count) {
+    require_setup("sn_step");
+    if (opt_.world > 1) throw LogicError("sn_step: partitioned engines step through sn_step_local / sn_step_finish");
+    if (ext_len != 0 && ext_len != n_user_)  // mat_engine.cpp:170-171
+        throw InvalidArgument("mat_step: ext must have one amplitude per neuron");
+    if (ext_len && !ext) throw InvalidArgument("sn_step: null ext");
+    if (!count) throw InvalidArgument("sn_step: null count");
+    // the step's input is exactly ext: mat_step does not consult a schedule.
+    // The schedule is swapped for one row holding ext's non-zero entries
+    // (adding a zero amplitude leaves u unchanged) and restored afterwards.
+    std::vector<int32_t> ss, sn;
+    std::vector<double> sa;
+    ss.swap(st_step_);
+    sn.swap(st_neuron_);
+    sa.swap(st_amp_);
+    for (int64_t j = 0; j < ext_len; ++j) {
+        if (!std::isfinite(ext[j])) {
+            ss.swap(st_step_);
+            sn.swap(st_neuron_);
+            sa.swap(st_amp_);
+            throw InvalidArgument("mat_step: ext[" + std::to_string(j) + "] must be finite");
+        }
+        if (ext[j] != 0.0) {
+            st_step_.push_back(t_);
+            st_neuron_.push_back(static_cast<int32_t>(j));
+            st_amp_.push_back(ext[j]);
+        }
+    }
+    stim_dirty_ = true;
+    const int32_t t = t_;
+    try {
+        simulate(1);
+    } catch (...) {
+        st_step_.swap(ss);
+        st_neuron_.swap(sn);
+        st_amp_.swap(sa);
+        stim_dirty_ = true;
+        throw;
+    }
+    st_step_.swap(ss);
+    st_neuron_.swap(sn);
+    st_amp_.swap(sa);
+    stim_dirty_ = true;
+    // this step's spike words: the last row of the host raster
+    strip_relays();
+    const RasterChunk& ch = raster_.back();
+    if (ch.t0 + ch.rows - 1 != t) throw LogicError("sn_step: raster row of the step is missing");
+    const uint32_t* row = ch.words.data() + static_cast<size_t>(ch.rows - 1) * nl_words_;
+    int64_t c = 0;
+    for (int w = 0; w < nl_words_; ++w) c += __builtin_popcount(row[w]);
+    *count = c;
+    if (!spikes) return;  // size query
+    if (cap < c) throw InvalidArgument("sn_step: capacity " + std::to_string(cap) + " < " + std::to_string(c) + " spikes");
+    int64_t o = 0;
+    for (int w = 0; w < nl_words_; ++w)
+        for (uint32_t m = row[w]; m; m &= m - 1) spikes[o++] = first_ + w * 32 + __builtin_ctz(m);
+}
+
 void Engine::step_local() {
+    NvtxRange nv("sn_step_local");
     require_setup("sn_step_local");
     if (tiny_) throw LogicError("sn_step_local: single-partition engines run through sn_simulate");
     host_exchange_ = true;
+    note_first_plastic_step();
     build_stimulus_table();
     if (d_raster_.bytes < static_cast<size_t>(std::max(nl_words_, 1)) * 4)
         d_raster_.alloc(static_cast<size_t>(std::max(nl_words_, 1)) * 4);
@@ -615,6 +697,7 @@ void Engine::put_spike_words(int32_t first_word, const uint32_t* w, int64_t coun
 }
 
 void Engine::step_finish() {
+    NvtxRange nv("sn_step_finish");
     require_setup("sn_step_finish");
     if (tiny_) throw LogicError("sn_step_finish: single-partition engines run through sn_simulate");
     if (opt_.world > 1) {

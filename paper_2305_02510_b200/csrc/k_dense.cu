@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kThreads) k_dense_sweep(DenseArgs a) {
                         WT w = VT::get(wv[u], k);
                         const int d1 = DELAY ? static_cast<int>((dv[u] >> (8 * k)) & 0xffu) - 1 : 0;
                         const bool e = (ebits >> d1) & 1ull;
-                        if (STDP && kind != kRowNone) {
+                        if (STDP && a.plastic_on && kind != kRowNone) {
                             const bool pl = kind == kRowAll || (kind == kRowAllButSelf && gc[k] != row) ||
                                             (kind == kRowMixed && ((mv[u] >> k) & 1u));
                             if (pl) {
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                             d1[k] = DELAY ? static_cast<int>((dv >> (8 * k)) & 0xffu) - 1 : 0;
                             ef[k] = ((h >> d1[k]) & 1ull) ? WT(1) : WT(0);  // s_pre[t+1-d], exact 0/1 factor
                         }
-                        if (STDP && kind != kRowNone) {
+                        if (STDP && a.plastic_on && kind != kRowNone) {
                             WT nw[VEC];
                             if (DELAY) {
 #pragma unroll

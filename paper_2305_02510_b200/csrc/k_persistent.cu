@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
             }
         }
         __syncthreads();  // the new history (and traces) of step t are complete
-        if (STDP && own) {
+        if (STDP && a.plastic_on && own) {
             // (3) STDP on post j's plastic synapses: dw = 0; if s_post dw += pot^(d)_pre;
             // if s_pre[t-d+1] dw -= dep_post; clamp (mat_engine.cpp:242-249)
             const uint8_t* hnb = reinterpret_cast<const uint8_t*>(hn);
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
                         pot2[(static_cast<int64_t>(cur) * n + j) * da.dp + (d - 1)] = pot;
                         any_pot |= pot != 0.0;
                     }
-                    if (ca.row_plastic[j] && (any_pot || t == 0)) act = true;
+                    if (ca.row_plastic[j] && (any_pot || t == ca.clamp_step)) act = true;
                 }
             }
             const uint32_t word = __ballot_sync(0xffffffffu, fired);  // bits 0..W-1
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
                 WT w = VT::get(wv, k);
                 const int d1 = DELAY ? static_cast<int>((dv >> (8 * k)) & 0xffu) - 1 : 0;
                 const bool e = (eb >> d1) & 1ull;
-                if (STDP && kind != kRowNone) {
+                if (STDP && da.plastic_on && kind != kRowNone) {
                     const bool pl = kind == kRowAll || (kind == kRowAllButSelf && j0 + k != i) ||
                                     (kind == kRowMixed && ((mw >> ((j0 & 31) + k)) & 1u));
                     if (pl) {

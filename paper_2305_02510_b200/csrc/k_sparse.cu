@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(Spars
                         if (HB == 1) e = (sbits[pl >> 5] >> (pl & 31)) & 1u;
                         else e = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
                         WT w = wv[u][k];
-                        if (!DICT && STDP && ((m >> 22) & 1u)) {
+                        if (!DICT && STDP && a.plastic_on && ((m >> 22) & 1u)) {
                             const double pt = sp ? pot[pl * a.dp + d1] : 0.0;  // only spiking posts read pot^(d)
                             const WT nw = stdp_apply<WT>(w, stdp_dw(sp, pt, e != 0u, depp), wmin, wmax);
                             changed |= (nw != w);
@@ -942,7 +942,7 @@ __global__ void __launch_bounds__(kThreads) k_sparse_stream(SparseArgs a) {
                     if (HB == 1) ev = (sbits[pl >> 5] >> (pl & 31)) & 1u;
                     else ev = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
                     WT w = wv[u][k];
-                    if (STDP && ((m >> 22) & 1u)) {
+                    if (STDP && a.plastic_on && ((m >> 22) & 1u)) {
                         const double pt = __ldcg(pot + static_cast<int64_t>(pre0 + pl) * a.dp + d1);
                         const WT nw = stdp_apply<WT>(w, stdp_dw(sp, pt, ev != 0u, depp), wmin, wmax);
                         changed |= (nw != w);
@@ -1009,7 +1009,7 @@ __global__ void __launch_bounds__(kThreads) k_sparse_exact(SparseArgs a) {
                 const int d1 = static_cast<int>((m >> 16) & 63u);
                 const bool e = (a.hist[pre] >> d1) & 1ull;
                 WT w = W[q];
-                if (STDP && ((m >> 22) & 1u)) {
+                if (STDP && a.plastic_on && ((m >> 22) & 1u)) {
                     const double pt = sp ? pot[static_cast<int64_t>(pre) * a.dp + d1] : 0.0;
                     const WT nw = stdp_apply<WT>(w, stdp_dw(sp, pt, e, depp), wmin, wmax);
                     if (nw != w) W[q] = nw;

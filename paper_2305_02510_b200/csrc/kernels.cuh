@@ -79,9 +79,7 @@ struct HistArgs {
     const double* a_plus;
     const double* a_minus;
     double* pot64;             // [n][dp]
-    float* pot32;
     double* dep64;             // [n]
-    float* dep32;
     const uint8_t* row_plastic;  // [n]
     uint32_t* active;          // [words] rows that the sweep must visit
     int32_t* d_step;
@@ -93,6 +91,10 @@ struct HistArgs {
     int32_t xstride;
     int32_t world;
     int32_t* error;                    // set to 1 when the wait times out
+    // first step that applies STDP: apply_stdp clamps every plastic weight on
+    // its first call even when dw == 0 (mat_engine.cpp:243-249), so every
+    // plastic row is visited then (0 unless plasticity was switched off first)
+    int32_t clamp_step;
 };
 
 struct DenseArgs {
@@ -123,6 +125,7 @@ struct DenseArgs {
     int32_t* d_step;
     int32_t* work;             // dynamic item counter (null: static striding)
     int32_t abm;               // exact mode seeds the accumulator with 0.0 instead of leak(v)
+    int32_t plastic_on;        // 0: steps without apply_stdp (sn_set_plasticity); weights untouched
 };
 
 struct SparseArgs {
@@ -152,6 +155,7 @@ struct SparseArgs {
     double* u_exact;
     int32_t* d_step;
     int32_t abm;               // exact mode seeds the accumulator with 0.0 instead of leak(v)
+    int32_t plastic_on;        // 0: steps without apply_stdp (sn_set_plasticity)
 };
 
 // Stage plan of k_sparse_tma (built on the host at setup from the CSC offsets):
@@ -184,6 +188,10 @@ int dense_stream_max_ctas(bool f64, bool stdp, bool delay);  // occupancy x SMs
 // TMA-staged sweep (fp32/fp64, optional delays): one CTA per SM, rows_per_chunk <= dense_tma_max_rows(...);
 // with delays the tile width must be a multiple of 16 (the delay bytes are bulk-copied)
 int dense_tma_max_dp();  // delayed STDP: plastic delay span the TMA sweep supports
+// weight census of a dense block (k_inspect.cu): counts[k] = cells equal to vals[k], counts[nv] = others
+int census_max_values();
+void launch_value_counts(const void* W, bool f64, int64_t pitch, int n, int nl, const void* vals, int nv,
+                         unsigned long long* counts, int ctas, cudaStream_t s);
 int dense_tma_partials_per_chunk();  // partial rows the TMA sweep writes per row chunk
 int dense_tma_max_rows(int tile_w, bool f64, bool delay, bool stdp);  // longest row list whose buffers fit (0: none)
 void launch_dense_tma(const DenseArgs& a, bool f64, bool stdp, bool delay, int grid, cudaStream_t s);
@@ -235,6 +243,7 @@ struct ColArgs {
     int32_t window;
     int32_t dmax;
     unsigned long long* active_count;  // running sum of active rows (algorithmic bytes)
+    int32_t clamp_step;                // HistArgs::clamp_step
 };
 // Cluster loop (k_cluster_count): static one-weight nets without STDP, delays <= 31
 struct ClusterArgs {
@@ -297,6 +306,7 @@ struct TinyArgs {
     const double* a_plus;
     const double* a_minus;
     double w_min, w_max;
+    int32_t plastic_on;        // 0: steps without apply_stdp (sn_set_plasticity)
     // outputs (device or host-mapped pinned memory)
     uint32_t* raster;          // [steps][words]
     double* trace;             // [steps][n] or null

@@ -114,7 +114,44 @@ __device__ __forceinline__ uint32_t bit_of(const uint32_t* bits, int i) {
 //   dep_i      = sum_{k=1..W} a_minus[k-1] s_i[t-k]           (k ascending, fp64)
 //   pot_i^(d)  = sum_{k=1..W} a_plus[k-1]  s_i[t-k-d+1]       (lowered-net shift)
 // Returns whether row i must be visited by the sweep this step.
+//
+// Windows + delay spans beyond kHistWordsMax * 64 steps (any window >= 1 is
+// valid, model.cpp:104-117) take hist_update_long: the same sums with the
+// history words read back from global memory instead of registers.
+__device__ __noinline__ bool hist_update_long(const HistArgs& h, int i, bool s, int t) {
+    uint64_t carry = s ? 1ull : 0ull, w0 = 0;
+    for (int k = 0; k < h.hw; ++k) {
+        uint64_t* p = h.hist + static_cast<int64_t>(k) * h.n + i;
+        const uint64_t x = *p;
+        const uint64_t nx = (x << 1) | carry;
+        carry = x >> 63;
+        *p = nx;
+        if (k == 0) w0 = nx;
+    }
+    if (h.hist_lo) h.hist_lo[i] = static_cast<uint32_t>(w0);
+    const uint64_t dmask = h.dmax >= 64 ? ~0ull : ((1ull << h.dmax) - 1ull);
+    bool act = (w0 & dmask) != 0;
+    if (h.stdp) {
+        auto bit = [&](int b) { return (h.hist[static_cast<int64_t>(b >> 6) * h.n + i] >> (b & 63)) & 1ull; };
+        double dep = 0.0;
+        for (int k = 1; k <= h.window; ++k)
+            if (bit(k)) dep += h.a_minus[k - 1];
+        h.dep64[i] = dep;
+        bool any_pot = false;
+        for (int d = 1; d <= h.dp; ++d) {
+            double pot = 0.0;
+            for (int k = 1; k <= h.window; ++k)
+                if (bit(k + d - 1)) pot += h.a_plus[k - 1];
+            h.pot64[static_cast<int64_t>(i) * h.dp + (d - 1)] = pot;
+            any_pot |= (pot != 0.0);
+        }
+        if (h.row_plastic[i] && (any_pot || t == h.clamp_step)) act = true;
+    }
+    return act;
+}
+
 __device__ __forceinline__ bool hist_update(const HistArgs& h, int i, bool s, int t) {
+    if (h.hw > kHistWordsMax) return hist_update_long(h, i, s, t);
     uint64_t words[kHistWordsMax];
     uint64_t carry = s ? 1ull : 0ull;
 #pragma unroll
@@ -140,17 +177,15 @@ __device__ __forceinline__ bool hist_update(const HistArgs& h, int i, bool s, in
         double dep = 0.0;
         for (uint64_t m = w0 & wmask & ~1ull; m; m &= m - 1) dep += h.a_minus[__ffsll(static_cast<long long>(m)) - 2];
         h.dep64[i] = dep;
-        h.dep32[i] = static_cast<float>(dep);
         bool any_pot = false;
         for (int d = 1; d <= h.dp; ++d) {
             const uint64_t sh = w0 >> (d - 1);  // bit k of sh = s[t - k - d + 1]
             double pot = 0.0;
             for (uint64_t m = sh & wmask & ~1ull; m; m &= m - 1) pot += h.a_plus[__ffsll(static_cast<long long>(m)) - 2];
             h.pot64[static_cast<int64_t>(i) * h.dp + (d - 1)] = pot;
-            h.pot32[static_cast<int64_t>(i) * h.dp + (d - 1)] = static_cast<float>(pot);
             any_pot |= (pot != 0.0);
         }
-        if (h.row_plastic[i] && (any_pot || t == 0)) act = true;
+        if (h.row_plastic[i] && (any_pot || t == h.clamp_step)) act = true;
     } else if (h.stdp) {
         // dep: bits 1..W
         double dep = 0.0;
@@ -159,7 +194,6 @@ __device__ __forceinline__ bool hist_update(const HistArgs& h, int i, bool s, in
             if ((words[b >> 6] >> (b & 63)) & 1ull) dep += h.a_minus[k - 1];
         }
         h.dep64[i] = dep;
-        h.dep32[i] = static_cast<float>(dep);
         bool any_pot = false;
         for (int d = 1; d <= h.dp; ++d) {
             double pot = 0.0;
@@ -168,13 +202,12 @@ __device__ __forceinline__ bool hist_update(const HistArgs& h, int i, bool s, in
                 if ((words[b >> 6] >> (b & 63)) & 1ull) pot += h.a_plus[k - 1];
             }
             h.pot64[static_cast<int64_t>(i) * h.dp + (d - 1)] = pot;
-            h.pot32[static_cast<int64_t>(i) * h.dp + (d - 1)] = static_cast<float>(pot);
             any_pot |= (pot != 0.0);
         }
         // t == 0: apply_stdp clamps every plastic weight even when dw == 0
         // (mat_engine.cpp:243-249); afterwards weights stay inside the bounds,
         // so rows with no pairing and no delivery are provably unchanged.
-        if (h.row_plastic[i] && (any_pot || t == 0)) act = true;
+        if (h.row_plastic[i] && (any_pot || t == h.clamp_step)) act = true;
     }
     return act;
 }
@@ -476,7 +509,7 @@ __device__ __forceinline__ void dense_stream_body(const DenseArgs& a, int cta, i
                         const int d1 = DELAY ? static_cast<int>((dv[u] >> (8 * k)) & 0xffu) - 1 : 0;
                         ef[k] = ((ebits >> d1) & 1ull) ? WT(1) : WT(0);
                     }
-                    if (STDP && kind != kRowNone) {
+                    if (STDP && a.plastic_on && kind != kRowNone) {
                         WT nw[VEC];
 #pragma unroll
                         for (int k = 0; k < VEC; ++k) {

@@ -5,6 +5,7 @@
 #include "nccl_dl.hpp"
 
 #include <dlfcn.h>
+#include <cstdlib>
 
 #include <cstring>
 #include <mutex>
@@ -29,7 +30,13 @@ NcclApi& api() {
     static NcclApi a;
     static std::once_flag once;
     std::call_once(once, [] {
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        // SNB_NCCL_LIB first: a process that also uses torch must load torch's
+        // own libnccl.so.2 -- whichever copy is loaded first owns the soname,
+        // and torch's libtorch_cuda cannot bind to an older one loaded here
+        // (the Python layer points this at the nvidia-nccl wheel, engine.py)
+        void* h = nullptr;
+        if (const char* p = std::getenv("SNB_NCCL_LIB"); p && *p) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
         if (!h) {
             a.error = std::string("cannot load libnccl.so.2: ") + dlerror();

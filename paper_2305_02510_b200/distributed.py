@@ -25,7 +25,8 @@ def partition_ranges(n: int, world: int) -> List[Tuple[int, int]]:
 
 
 def words_per_rank(n: int, world: int) -> int:
-    return max(partition_ranges(n, world)[0][1], 32) // 32
+    """Spike words per rank slice: rank 0's range rounded up to whole words."""
+    return (max(partition_ranges(n, world)[0][1], 1) + 31) // 32
 
 
 def pack_words(spikes: np.ndarray, words: int) -> np.ndarray:

@@ -6,6 +6,7 @@ numpy buffers across the boundary.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import Optional
 
 import numpy as np
@@ -132,6 +133,23 @@ class MatEngine:
     def synchronize(self):
         check(lib.sn_synchronize(self._h))
 
+    def step(self, ext=None) -> np.ndarray:
+        """mat_step (mat_engine.cpp:168-208): one step with external input
+        exactly `ext` (n amplitudes, or None), then apply_stdp when plasticity
+        is on; returns the step's spiking ids ascending."""
+        e = None if ext is None else _c(ext, np.float64)
+        n = 0 if e is None else len(e)
+        cnt = C.c_int64()
+        cap = max(1, self.stats()["n_local"])
+        out = np.empty(cap, np.int32)
+        check(lib.sn_step(self._h, ptr(e, C.c_double) if e is not None else None, n,
+                          ptr(out, C.c_int32), cap, C.byref(cnt)))
+        return out[:cnt.value].copy()
+
+    def set_plasticity(self, enabled: bool):
+        """Whether following steps run apply_stdp after mat_step."""
+        check(lib.sn_set_plasticity(self._h, 1 if enabled else 0))
+
     # ---- results ----
     def raster(self):
         n = C.c_int64()
@@ -166,6 +184,14 @@ class MatEngine:
         check(lib.sn_get_membrane_trace(self._h, ptr(out, C.c_double), out.size))
         return out
 
+    def weight_value_counts(self, values) -> np.ndarray:
+        """Device census of the dense weight block: counts of each value
+        (storage precision), then all other cells."""
+        v = _c(values, np.float64)
+        out = np.zeros(len(v) + 1, np.int64)
+        check(lib.sn_weight_value_counts(self._h, ptr(v, C.c_double), len(v), ptr(out, C.c_int64)))
+        return out
+
     def synapse_weights(self) -> np.ndarray:
         out = np.empty(self.n_synapses, np.float64)
         check(lib.sn_get_synapse_weights(self._h, ptr(out, C.c_double), self.n_synapses))
@@ -179,6 +205,7 @@ class MatEngine:
 
     # ---- partitioned stepping ----
     def comm_init(self, uid: bytes, rank: int, world: int):
+        _point_at_torch_nccl()
         buf = (C.c_uint8 * len(uid)).from_buffer_copy(uid)
         check(lib.sn_comm_init(self._h, buf, rank, world))
 
@@ -216,7 +243,26 @@ def p2p_connect_local(engines) -> None:
     check(lib.sn_p2p_connect_local(arr, len(engines)))
 
 
+def _point_at_torch_nccl():
+    """NCCL is dlopen'ed by the engine; in a process that also imports torch
+    it must be the same libnccl.so.2 torch links (the nvidia-nccl wheel), since
+    the first copy loaded owns the soname.  Sets SNB_NCCL_LIB unless given."""
+    if os.environ.get("SNB_NCCL_LIB"):
+        return
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        spec = None
+    for d in (list(spec.submodule_search_locations) if spec and spec.submodule_search_locations else []):
+        path = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(path):
+            os.environ["SNB_NCCL_LIB"] = path
+            return
+
+
 def comm_unique_id() -> bytes:
+    _point_at_torch_nccl()
     size = lib.sn_comm_id_size()
     buf = (C.c_uint8 * size)()
     check(lib.sn_comm_create_id(buf))

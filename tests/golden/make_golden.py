@@ -171,7 +171,47 @@ def main():
         json.dump(scale, f, indent=1)
 
 
+def cfg4_entry(steps: int) -> dict:
+    """BASELINE cfg4 at full size, truncated T: build_scenario(256000, 0.01,
+    seed 0) with delays 1 + below_at(i*n + j, 16) on the "delay" stream (the
+    engine's sn_generate_erdos_renyi pair-keyed delays), run by the
+    reference's native-delay path abm_run (abm_engine.cpp:208-243; equal to
+    mat_run(lower_delays) and oracle_run on every small golden).  Needs ~45 GB
+    of host RAM and ~15 min: generated on the GPU box's host
+    (python tests/golden/make_golden.py --cfg4 OUT.json), merged into
+    scale.json by --merge-cfg4 OUT.json."""
+    n, p, seed, dmax = 256000, 0.01, 0, 16
+    t0 = time.time()
+    r = B.ref_scenario_abm_raster(n, p, seed, steps, dmax, False)
+    return {"n": n, "p": p, "seed": seed, "steps": steps, "delay_max": dmax, "delay_key": "pair",
+            "synapses": r["synapses"], "spikes": int(len(r["steps"])),
+            "digest": raster_digest(r["steps"], r["neurons"]),
+            "per_step": np.bincount(r["steps"], minlength=steps).astype(int).tolist(),
+            "ref_path": "abm_run (reference, oracle/_ref)", "ref_build_s": round(r["build_s"], 1),
+            "ref_run_s": round(r["run_s"], 1), "ref_peak_rss_gb": round(r["peak_rss_gb"], 1),
+            "ref_seconds": round(time.time() - t0, 1)}
+
+
 if __name__ == "__main__":
+    if "--cfg4" in sys.argv:     # full-size cfg4 golden (run on a host with >= 64 GB RAM)
+        out = sys.argv[sys.argv.index("--cfg4") + 1]
+        steps = int(os.environ.get("CFG4_STEPS", "24"))
+        B.build(ref=False)
+        e = cfg4_entry(steps)
+        with open(out, "w") as f:
+            json.dump(e, f, indent=1)
+        print(json.dumps({k: v for k, v in e.items() if k != "per_step"}))
+        sys.exit(0)
+    if "--merge-cfg4" in sys.argv:
+        with open(sys.argv[sys.argv.index("--merge-cfg4") + 1]) as f:
+            e = json.load(f)
+        path = os.path.join(HERE, "scale.json")
+        with open(path) as f:
+            scale = json.load(f)
+        scale[f"cfg4_seed0_T{e['steps']}"] = e
+        with open(path, "w") as f:
+            json.dump(scale, f, indent=1)
+        sys.exit(0)
     if "--abm" in sys.argv:   # agent-based fixtures only (abm.npz + scale.json abm entries)
         main_abm()
     else:

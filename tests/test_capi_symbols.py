@@ -61,7 +61,7 @@ def test_options_and_partition_math():
     from paper_2305_02510_b200 import _capi
     o = _capi.Options()
     assert _capi.lib.sn_options_init(C.byref(o)) == 0
-    assert o.abi_version == 1 and o.world == 1 and o.use_graphs == 1
+    assert o.abi_version == _capi.SN_ABI_VERSION and o.world == 1 and o.use_graphs == 1
     for n in (1, 31, 32, 100, 1000, 32000, 256000, 96000):
         for world in (1, 2, 3, 4, 8):
             parts = [sn.partition_range(n, r, world) for r in range(world)]
