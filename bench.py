@@ -40,7 +40,11 @@ WORKLOADS = {
     "cfg3": (32000, 1.0, True, 1, False, 100, "ER(32000, p=1) all synapses plastic, STDP defaults, fp32 weights"),
     "cfg4": (256000, 0.01, False, 16, False, 1000, "ER(256000, p=0.01) CSC, delays 1..16 (pair keyed), no STDP"),
     "cfg5": (96000, 1.0, True, 1, False, 100, "ER(96000, p=1) all plastic, STDP defaults, fp32 weights"),
+    # not BASELINE configs: the plastic sparse path (k_sparse_pull with streamed weights)
+    "sstdp1": (100000, 0.01, True, 1, False, 100, "ER(100000, p=0.01) all plastic, STDP defaults, unit delay (sparse STDP)"),
+    "sstdp8": (100000, 0.01, True, 8, False, 100, "ER(100000, p=0.01) all plastic, STDP defaults, delays 1..8 (sparse STDP)"),
 }
+BASELINE_CONFIGS = ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5")
 
 
 def load_peaks():
@@ -347,7 +351,7 @@ def run_ours(args):
     if not args.no_per_config:
         # the other BASELINE configs, each with its own clock and CPU sample;
         # partitioned runs (N > 1) repeat only the partitioned configs
-        others = [c for c in WORKLOADS if c != wl and (world == 1 or c in ("cfg4", "cfg5"))]
+        others = [c for c in BASELINE_CONFIGS if c != wl and (world == 1 or c in ("cfg4", "cfg5"))]
         for c in others:
             k2, w2 = PER_CONFIG_STEPS[c]
             rc = measure_ours(sn, c, k2, w2, rank, world, device, args.transport, torch_dist, not args.no_e2e)
@@ -423,6 +427,8 @@ def cpu_baseline(wl, cfg3_sample=None):
         return {"value": base["value"] / f, "unit": UNIT, "cores": 1, "kind": base["kind"], "extrapolated": True,
                 "sample": f"cfg3's sample ({base['sample']}) scaled by the synapse-count ratio x{f:.2f}; the "
                           f"full cfg5 NetworkDef (~221 GB) does not fit the host", "cpu": cpu_model()}
+    if wl not in CPU_SAMPLES:
+        return None
     ns, ps, warm, steps, note = CPU_SAMPLES[wl]
     factor = _synapses(n, p) / _synapses(ns, ps)
     try:

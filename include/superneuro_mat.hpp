@@ -156,7 +156,28 @@ public:
         return r;
     }
 
+    // mat_step (mat_engine.cpp:168-208): one step whose external input is
+    // exactly `ext` (one amplitude per neuron, or empty); returns the step's
+    // spiking neurons ascending -- the list mat_step lends (mat_engine.hpp:92-94).
+    // apply_stdp follows when STDP is set up and plasticity is on.
+    const std::vector<int>& step(const std::vector<double>& ext = {}) {
+        if (!e_) throw std::logic_error("step: call setup() first");
+        int64_t k = 0;
+        step_spikes_.resize(thr_.size());
+        static_assert(sizeof(int) == sizeof(int32_t), "int32 spike ids");
+        check(sn_step(e_, ext.empty() ? nullptr : ext.data(), static_cast<int64_t>(ext.size()),
+                      reinterpret_cast<int32_t*>(step_spikes_.data()), static_cast<int64_t>(step_spikes_.size()), &k));
+        step_spikes_.resize(static_cast<size_t>(k));
+        return step_spikes_;
+    }
+    // whether following steps run apply_stdp after mat_step (mat_engine.hpp:92-98)
+    void set_plasticity(bool on) {
+        if (!e_) throw std::logic_error("set_plasticity: call setup() first");
+        check(sn_set_plasticity(e_, on ? 1 : 0));
+    }
+
 private:
+    std::vector<int> step_spikes_;
     sn_options opts_{};
     sn_engine* e_ = nullptr;
     std::vector<double> thr_, leak_, reset_, w_, sa_, fire_p_;

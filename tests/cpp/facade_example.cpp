@@ -1,11 +1,13 @@
 // Drop-in use of the C++ facade: the two-neuron delay-3 chain of the
 // reference tests (test_oracle.cpp:47-51) -> {(0,0),(3,1)}; plus an STDP pair
 // (test_stdp.cpp:46-57) -> weight 0.5 + 0.1 within fp32 storage tolerance;
+// plus the mat_step KATs through Model::step (test_mat_engine.cpp:61-95);
 // plus a seeded stochastic agent-based run.
 #include "superneuro_mat.hpp"
 
 #include <cmath>
 #include <cstdio>
+#include <vector>
 
 int main() {
     try {
@@ -36,6 +38,27 @@ int main() {
         if (q.weights.size() != 1 || q.weights[0] != 0.5 + 0.1) {
             std::printf("FAIL stdp %.17g\n", q.weights.empty() ? -1.0 : q.weights[0]);
             return 1;
+        }
+        // per-step API, the mat_step KATs of test_mat_engine.cpp:61-95: chain with
+        // threshold 0.5 -> {0}, {1}, {}; refractory 3 -> {0}, {}, {}, {}, {0}
+        {
+            superneuro::Model c(0, SN_STORAGE_DENSE, SN_WEIGHTS_F64);
+            c.create_neuron(0.5);
+            c.create_neuron(0.5);
+            c.create_synapse(0, 1, 1.0, 1, false);
+            c.setup();
+            const bool ok = c.step({1.0, 0.0}) == std::vector<int>{0} && c.step({0.0, 0.0}) == std::vector<int>{1} &&
+                            c.step({0.0, 0.0}).empty();
+            superneuro::Model r;
+            r.create_neuron(1.0, 0.0, 0.0, 3);
+            r.setup();
+            std::vector<std::vector<int>> got;
+            for (int t = 0; t < 5; ++t) got.push_back(r.step({2.0}));
+            const std::vector<std::vector<int>> want{{0}, {}, {}, {}, {0}};
+            if (!ok || got != want) {
+                std::printf("FAIL step\n");
+                return 1;
+            }
         }
         // agent-based mode: stochastic_lif (p = 0.5) post, seeded -- deterministic
         // per seed, fires on some but not all of its above-threshold steps
