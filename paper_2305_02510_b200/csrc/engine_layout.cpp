@@ -493,7 +493,9 @@ void Engine::plan_launches() {
         // A/B runs with SNB_SPARSE_KERNEL=stream (tools/ab_sparse.sh)
         const char* sk = std::getenv("SNB_SPARSE_KERNEL");
         if (sk && std::string(sk) == "stream") sub_ = 0;
-        const int target = sms * 8;
+        int per_sm = 8;  // CTAs per SM the grid aims at (A/B knob SNB_SPARSE_CTAS_PER_SM)
+        if (const char* cp = std::getenv("SNB_SPARSE_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(cp));
+        const int target = sms * per_sm;
         int gx = std::max(1, target / std::max(1, nblocks_));
         const int unit = sub_ == 0 ? 8 : 8 * (32 / sub_);
         posts_per_cta_ = static_cast<int32_t>(round_up((nl_ + gx - 1) / gx, unit));

@@ -306,6 +306,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                         if (lane >= o) incl += x;
                     }
                     int pos = cnt + incl - c;
+                    SNB_DCHECK(pos + c <= rec_cap - kTmaRows);
                     for (uint32_t m = wd; m; m &= m - 1) rec[pos++].rowk = wr + __ffs(static_cast<int>(m)) - 1;
                     cnt += __shfl_sync(0xffffffffu, incl, 31);
                 }
@@ -380,6 +381,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                     uint8_t* st = ring + s * stage_bytes;
                     for (int r = 0; r < nr; ++r) {
                         const int row = rec[g * kTmaRows + r].rowk & 0x0fffffff;
+                        SNB_DCHECK(row < a.n && col0 + width <= a.pitch && g * kTmaRows + r < cnt);
                         bulk_g2s(st + static_cast<size_t>(r) * row_bytes, W + static_cast<int64_t>(row) * a.pitch + col0,
                                  copy_bytes, full + s);
                         if (DELAY)
@@ -443,6 +445,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                         const TmaRec rec = s_rec[g * kTmaRows + r];
                         const int row = rec.rowk & 0x0fffffff;
                         const int kind = rec.rowk >> 28;
+                        SNB_DCHECK(g * kTmaRows + r < cnt && row < a.n);
                         const V wv = *reinterpret_cast<const V*>(st + static_cast<size_t>(r) * row_bytes + tcol * sizeof(WT));
                         uint32_t dv = 0;
                         if (DELAY) {
@@ -464,6 +467,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
                             if (DELAY) {
 #pragma unroll
                                 for (int k = 0; k < VEC; ++k) {
+                                    SNB_DCHECK(d1[k] >= 0 && d1[k] < a.dp);
                                     const double p = s_potd[(g * kTmaRows + r) * kTmaDp + d1[k]];
                                     nw[k] = stdp_apply<WT>(w[k], stdp_dw(sj[k], p, ef[k] != WT(0), depj[k]), wmin, wmax);
                                 }

@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
     const int words = (n + 31) / 32;
     const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
     const uint32_t q0 = own ? off[j] : 0u, q1 = own ? off[j + 1] : 0u;
+    SNB_DCHECK(q0 <= q1 && q1 <= static_cast<uint32_t>(a.m));
     // own history words in registers (<= kTinyHistRegs 32-bit words)
     const bool hreg = kTinyHistRegs > 0 && hw2 <= kTinyHistRegs;
     uint32_t hr[kTinyHistRegs > 0 ? kTinyHistRegs : 1];

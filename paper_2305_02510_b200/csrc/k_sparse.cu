@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(Spars
                         const uint32_t m = ms[k];
                         const int pl = static_cast<int>(m & 0xffffu);
                         const int d1 = static_cast<int>((m >> 16) & 63u);
+                        SNB_DCHECK(pl <= a.pb && (!STDP || !((m >> 22) & 1u) || (pl < pcount && d1 < a.dp)));
                         uint32_t e;
                         if (HB == 1) e = (sbits[pl >> 5] >> (pl & 31)) & 1u;
                         else e = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
@@ -482,6 +483,7 @@ __device__ __forceinline__ uint32_t c16_count_batch(const uint4 (&m4)[UL], int c
     for (int u = 0; u < UL; ++u) {
         const int c = c0 + u * SUB;
         if (c < C) {
+            SNB_DCHECK(E1 <= E2 && E2 <= E3 && E3 <= C && C <= 255);
             const uint16_t* sh = shist + (((c >= E1) + (c >= E2) + (c >= E3)) << 12);
             const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sh));
             const uint32_t ws[4] = {m4[u].x, m4[u].y, m4[u].z, m4[u].w};

@@ -26,6 +26,27 @@
 #include <stdexcept>
 #include <string>
 
+// Checked builds (-DSNB_CHECKED, tools/build_variant.sh checked -DSNB_CHECKED):
+// device-side bounds checks on the hot kernels' shared-memory and list
+// indexing, and mbarrier waits that trap after ~2^31 polls instead of hanging
+// -- the substitute for compute-sanitizer, which this GPU pool refuses
+// (profiles/r02_compute_sanitizer_refused.txt).  Compiled out otherwise.
+#ifdef SNB_CHECKED
+#include <cstdio>
+#define SNB_DCHECK(cond)                                                                    \
+    do {                                                                                    \
+        if (!(cond)) {                                                                      \
+            printf("SNB_DCHECK failed %s:%d block (%d,%d) thread %d: %s\n", __FILE__, __LINE__, \
+                   blockIdx.x, blockIdx.y, threadIdx.x, #cond);                             \
+            __trap();                                                                       \
+        }                                                                                   \
+    } while (0)
+#else
+#define SNB_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 namespace snb {
 
 namespace cg = cooperative_groups;
@@ -577,6 +598,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef SNB_CHECKED
+    uint32_t ok = 0;
+    for (long long spins = 0; !ok; ++spins) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        SNB_DCHECK(spins < (1ll << 31));  // a lost arrival: trap instead of hanging the GPU
+    }
+#else
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
@@ -584,6 +618,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
