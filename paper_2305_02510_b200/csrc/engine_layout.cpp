@@ -493,7 +493,14 @@ void Engine::plan_launches() {
         // A/B runs with SNB_SPARSE_KERNEL=stream (tools/ab_sparse.sh)
         const char* sk = std::getenv("SNB_SPARSE_KERNEL");
         if (sk && std::string(sk) == "stream") sub_ = 0;
-        int per_sm = 8;  // CTAs per SM the grid aims at (A/B knob SNB_SPARSE_CTAS_PER_SM)
+        // CTAs per SM the grid aims at.  16-bit count lists (cfg4): 12 at full
+        // size (0.418 ms vs 0.431 at 8, 0.425 at 16; three waves of ~2,300 posts
+        // per CTA), 4 for post partitions (an eighth of cfg4: 70.5 us vs 76.9 at
+        // 8 -- every CTA stages a whole pre block, so fewer, fuller CTAs);
+        // A/B knob SNB_SPARSE_CTAS_PER_SM (tools/ab_env.sh)
+        const bool c16_plan = dict_.size() == 2 && !stdp_on_ && !exact_ && hbits_ == 16 &&
+                              pb_ == c16_block_pres() && c16_allowed();
+        int per_sm = c16_plan ? (nl_ >= 131072 ? 12 : 4) : 8;
         if (const char* cp = std::getenv("SNB_SPARSE_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(cp));
         const int target = sms * per_sm;
         int gx = std::max(1, target / std::max(1, nblocks_));
