@@ -257,3 +257,49 @@ def test_abm_oracle_matches_live_reference_random():
         r = B.run_ref_abm_full(net.to_arrays(), 160, st, seed=seed, fire_p=fp, record_membrane=True)
         assert np.array_equal(o["steps"], r["steps"]) and np.array_equal(o["neurons"], r["neurons"])
         assert np.array_equal(o["membrane_trace"], r["membrane_trace"])
+
+
+def test_fp32_storage_model_against_fp64_and_numpy():
+    """The oracle's fp32 weight-storage model (mat_oracle_run_f32w, the bit-exact
+    target of fp32 engines): with the fp64 run's spike train, its weights equal
+    an independent numpy replay of apply_stdp (mat_engine.cpp:210-250) with one
+    float rounding per update, and stay within the rigorous drift bound
+    (T + 1) 2^-24 max|w| of the fp64 reference weights."""
+    from paper_2305_02510_b200.model import StdpConfig
+    from paper_2305_02510_b200.netgen import RandomStream, erdos_renyi_arrays, scenario_stimulus
+    from support import fp32_weight_floor
+    n, p, seed, steps = 300, 0.05, 5, 120
+    pre, post = erdos_renyi_arrays(n, p, seed)
+    m = len(pre)
+    rs = RandomStream(seed, 3)
+    k = np.arange(m, dtype=np.uint64)
+    w = 0.1 + 0.8 * rs.unit_np(k)
+    plastic = (rs.unit_np(k + np.uint64(m)) < 0.7).astype(np.uint8)
+    arrays = {"threshold": np.full(n, 2.0), "leak": np.full(n, 0.5), "reset": np.zeros(n),
+              "refractory": np.ones(n, np.int32), "axonal": np.zeros(n, np.int32), "pre": pre, "post": post,
+              "weight": w, "delay": np.ones(m, np.int32), "stdp": plastic}
+    d = StdpConfig.defaults()
+    sd = (d.window, np.array(d.a_plus), np.array(d.a_minus), d.w_min, d.w_max)
+    stim = scenario_stimulus(n, steps, seed, count=40, period=1, amplitude=3.0).to_arrays()
+    o = B.run_oracle(arrays, steps, stim, sd)
+    o32 = B.run_oracle(arrays, steps, stim, sd, f32_weights=True)
+    assert len(o["steps"]) > 2000
+    assert np.array_equal(o32["steps"], o["steps"]) and np.array_equal(o32["neurons"], o["neurons"])
+    S = np.zeros((steps, n), bool)
+    S[o["steps"], o["neurons"]] = True
+    ap, am = np.array(d.a_plus), np.array(d.a_minus)
+    w32 = w.astype(np.float32)
+    for t in range(steps):
+        pot = np.zeros(n)
+        dep = np.zeros(n)
+        for kk in range(1, min(d.window, t) + 1):
+            pot += ap[kk - 1] * S[t - kk]
+            dep += am[kk - 1] * S[t - kk]
+        dw = np.where(S[t][post], pot[pre], 0.0)
+        dw = np.where(S[t][pre], dw - dep[post], dw)
+        upd = np.clip((w32.astype(np.float64) + dw).astype(np.float32), np.float32(d.w_min), np.float32(d.w_max))
+        w32 = np.where(plastic == 1, upd, w32)
+    assert np.array_equal(o32["weights"], w32.astype(np.float64))
+    floor = fp32_weight_floor(steps, w, d.w_min, d.w_max)
+    assert np.all(np.abs(o32["weights"] - o["weights"]) <= floor)
+    assert not np.array_equal(o32["weights"], o["weights"])   # the rounding is visible
