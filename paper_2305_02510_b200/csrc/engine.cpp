@@ -490,6 +490,12 @@ void Engine::setup() {
     stim_dirty_ = true;
     build_stimulus_table();
     if (!tiny_) plan_launches();
+    if (c16_) {  // folded-history buffers of partitioned runs (fold_hist())
+        d_hist16_.alloc(static_cast<size_t>(2) * n_ * 2);
+        cuda_check(cudaMemsetAsync(d_hist16_.p, 0, d_hist16_.bytes, stream_), "memset");
+        d_step_copy_.alloc(8);
+        cuda_check(cudaMemsetAsync(d_step_copy_.p, 0, 8, stream_), "memset");
+    }
     if (opt_.stream_io) {  // pinned staging sized up front (1024 steps of spike words)
         h_raster_.reserve(static_cast<size_t>(1024) * std::max(nl_words_, 1) * 4);
         h_stage_.reserve(64 * 1024);

@@ -22,6 +22,8 @@ void Engine::comm_init(const uint8_t* id, int32_t rank, int32_t world) {
     if (world == 1 && (tiny_ || persistent_))
         throw LogicError("sn_comm_init: this single-partition engine runs whole simulate calls in one kernel "
                          "(create it with persistent = 0 and a dense or sparse storage)");
+    if (world == 1 && t_ > 0)  // switches a 1-rank engine to the partitioned step sequence
+        throw LogicError("sn_comm_init: a single-partition engine joins a communicator before its first step");
     delete comm_;
     comm_ = nullptr;
     // world 1: a one-rank communicator switches the engine to the partitioned
@@ -51,6 +53,8 @@ void Engine::p2p_get_handles(uint8_t* out, int64_t cap) {
 }
 
 void Engine::set_peer_tables(const std::vector<uint32_t*>& bits, const std::vector<int32_t*>& flags) {
+    if (c16_ && t_ > 0)  // the p2p exchange keeps k_hist; the folded history would be lost
+        throw LogicError("sn_p2p_open: connect the peer-to-peer exchange before the first step");
     d_peer_bits_.alloc(bits.size() * sizeof(uint32_t*));
     d_peer_flags_.alloc(flags.size() * sizeof(int32_t*));
     h2d_sync(stream_, d_peer_bits_.p, bits.data(), bits.size() * sizeof(uint32_t*), "peer table");

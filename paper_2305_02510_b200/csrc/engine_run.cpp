@@ -135,6 +135,7 @@ NeuronArgs Engine::neuron_args(int t_base, int rows, uint32_t* raster, double* t
     a.st_base = st_base;
     a.d_step = d_step_.as<int32_t>();
     a.work = (dense_ && !exact_) ? d_work_.as<int32_t>() : nullptr;
+    a.step_out = fold_hist() ? d_step_copy_.as<int32_t>() : nullptr;
     a.t_base = t_base;
     a.bits = d_bits_.as<uint32_t>();
     a.raster = raster;
@@ -254,6 +255,10 @@ void Engine::launch_sweep_only() {
         a.d_step = d_step_.as<int32_t>();
         a.abm = abm_ ? 1 : 0;
         a.plastic_on = plasticity_ ? 1 : 0;
+        if (fold_hist()) {
+            a.step_in = d_step_copy_.as<int32_t>();
+            a.hist16 = d_hist16_.as<uint16_t>();
+        }
         if (nl_ == 0) {
             launch_step_bump(a.d_step, stream_);
         } else if (sparse_tma_) {
@@ -295,8 +300,10 @@ void Engine::enqueue_step(const NeuronArgs& na, bool exchange) {
         NvtxRange nv("spike exchange + history");
         if (prof) { e0 = get_event(); cuda_check(cudaEventRecord(e0, stream_), "rec"); }
         if (comm_ && !p2p_) comm_->all_gather_inplace(d_bits_.as<uint32_t>(), static_cast<size_t>(part_ / 32), stream_);
-        launch_hist(h, stream_);
-        stats_.kernel_launches += 1;
+        if (!fold_hist()) {
+            launch_hist(h, stream_);
+            stats_.kernel_launches += 1;
+        }
         if (prof) { e1 = get_event(); cuda_check(cudaEventRecord(e1, stream_), "rec"); pending_.push_back({e0, e1, 2, 0.0}); }
     }
     if (prof) { e2 = get_event(); cuda_check(cudaEventRecord(e2, stream_), "rec"); }
@@ -336,7 +343,7 @@ double Engine::run_graph_chunks(const NeuronArgs& na, int steps) {
             if (!fused) {
                 if (e) cuda_check(cudaEventRecordWithFlags(e[2], stream_, cudaEventRecordExternal), "rec");
                 if (comm_ && !p2p_) comm_->all_gather_inplace(d_bits_.as<uint32_t>(), static_cast<size_t>(part_ / 32), stream_);
-                launch_hist(h, stream_);
+                if (!fold_hist()) launch_hist(h, stream_);
                 if (e) cuda_check(cudaEventRecordWithFlags(e[3], stream_, cudaEventRecordExternal), "rec");
             }
             if (e) cuda_check(cudaEventRecordWithFlags(e[4], stream_, cudaEventRecordExternal), "rec");
@@ -350,7 +357,7 @@ double Engine::run_graph_chunks(const NeuronArgs& na, int steps) {
     };
     cudaGraphExec_t full = capture(chunk);
     cudaGraphExec_t tail = (steps % chunk) ? capture(steps % chunk) : nullptr;
-    const int per_step_kernels = fused ? 2 : 3;
+    const int per_step_kernels = (fused || fold_hist()) ? 2 : 3;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spans;
     double total = 0.0;
     NvtxRange nv_replay("step graph replay");
@@ -700,7 +707,7 @@ void Engine::step_finish() {
     NvtxRange nv("sn_step_finish");
     require_setup("sn_step_finish");
     if (tiny_) throw LogicError("sn_step_finish: single-partition engines run through sn_simulate");
-    if (opt_.world > 1) {
+    if (opt_.world > 1 && !fold_hist()) {
         launch_hist(hist_args(), stream_);
         stats_.kernel_launches += 1;
     }

@@ -13,6 +13,7 @@ namespace {
 template <bool EXACT, bool FUSED>
 __global__ void __launch_bounds__(kThreads, SNB_NEURON_MINB) k_neuron(NeuronArgs a, HistArgs h) {
     const int t = *a.d_step;
+    if (a.step_out && blockIdx.x == 0 && threadIdx.x == 0) *a.step_out = t;
     const uint32_t f = neuron_step<EXACT, FUSED, false>(a, h, blockIdx.x * kThreads + threadIdx.x, t);
     const int spikes = __syncthreads_count(f & 1u);
     const int active = FUSED ? __syncthreads_count(f & 2u) : 0;

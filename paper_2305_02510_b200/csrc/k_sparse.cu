@@ -447,10 +447,50 @@ constexpr int kC16Pres = 4 * kC16SegPres;
 __host__ __device__ constexpr int c16_zero_slot(int s) { return 4095 - 16 * s; }
 
 __device__ __forceinline__ void c16_stage(const SparseArgs& a, int pre0, int pcount, uint16_t* sh) {
-    for (int k = threadIdx.x; k < 4 * 4096; k += blockDim.x) {
-        const int s = k >> 12, slot = k & 4095, z = c16_zero_slot(s);
-        const int pre = s * kC16SegPres + slot - (slot > z);
-        sh[k] = (slot != z && pre < pcount) ? static_cast<uint16_t>(__ldcg(a.hist_lo + pre0 + pre)) : 0;
+    if (a.hist16) {
+        // folded history: h = (history after step t - 1) << 1 | s[t]; the first CTA
+        // of the pre block commits it to the other parity buffer for step t + 1
+        const int t = *a.step_in;
+        const uint16_t* hin = a.hist16 + static_cast<int64_t>(t & 1) * a.n;
+        uint16_t* hout = a.hist16 + static_cast<int64_t>((t + 1) & 1) * a.n;
+        const bool commit = blockIdx.x == 0;
+        // 8 slots per thread per pass, all loads issued before any use
+        constexpr int R = 8;
+        for (int k0 = threadIdx.x; k0 < 4 * 4096; k0 += R * blockDim.x) {
+            uint32_t hv[R], bw[R];
+            int gs[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int k = k0 + r * blockDim.x;
+                const int s = k >> 12, slot = k & 4095, z = c16_zero_slot(s);
+                const int pre = s * kC16SegPres + slot - (slot > z);
+                gs[r] = (k < 4 * 4096 && slot != z && pre < pcount) ? pre0 + pre : -1;
+                hv[r] = gs[r] >= 0 ? __ldcg(hin + gs[r]) : 0u;
+                bw[r] = gs[r] >= 0 ? __ldcg(a.bits + (gs[r] >> 5)) : 0u;
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int k = k0 + r * blockDim.x;
+                const uint16_t h = gs[r] >= 0 ? static_cast<uint16_t>((hv[r] << 1) | ((bw[r] >> (gs[r] & 31)) & 1u)) : 0;
+                if (k < 4 * 4096) sh[k] = h;
+                if (commit && gs[r] >= 0) hout[gs[r]] = h;
+            }
+        }
+        return;
+    }
+    constexpr int R = 8;  // slots per thread per pass, loads first (memory-level parallelism)
+    for (int k0 = threadIdx.x; k0 < 4 * 4096; k0 += R * blockDim.x) {
+        uint32_t hv[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int k = k0 + r * blockDim.x;
+            const int s = k >> 12, slot = k & 4095, z = c16_zero_slot(s);
+            const int pre = s * kC16SegPres + slot - (slot > z);
+            hv[r] = (k < 4 * 4096 && slot != z && pre < pcount) ? __ldcg(a.hist_lo + pre0 + pre) : 0u;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            if (k0 + r * blockDim.x < 4 * 4096) sh[k0 + r * blockDim.x] = static_cast<uint16_t>(hv[r]);
     }
 }
 

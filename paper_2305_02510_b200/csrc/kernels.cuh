@@ -40,6 +40,7 @@ struct NeuronArgs {
     int32_t st_base;           // step of table row 0 (row = t - st_base)
     // time
     int32_t* d_step;           // device step counter (read here; sweep increments)
+    int32_t* step_out;         // or null: block 0 stores the step here for the sweep (folded history)
     int32_t* work;             // sweep work counter, reset here (null: static schedule)
     int32_t t_base;            // raster/trace row = t - t_base
     // outputs
@@ -156,6 +157,12 @@ struct SparseArgs {
     int32_t* d_step;
     int32_t abm;               // exact mode seeds the accumulator with 0.0 instead of leak(v)
     int32_t plastic_on;        // 0: steps without apply_stdp (sn_set_plasticity)
+    // folded history (partitioned k_sparse_count16 runs, no k_hist): the sweep
+    // shifts step t's spike bits into hist16[t & 1] -> hist16[(t + 1) & 1]
+    // itself while staging; t comes from k_neuron via step_in (the sweep
+    // bumps d_step, so it cannot read d_step safely)
+    const int32_t* step_in;
+    uint16_t* hist16;          // [2][n] or null
 };
 
 // Stage plan of k_sparse_tma (built on the host at setup from the CSC offsets):

@@ -1153,3 +1153,71 @@ def test_nccl_one_rank_partitioned_sequence(storage, use_graphs):
         assert np.array_equal(w, o["weights"])
         assert st["kernel_launches"] == 3 * steps      # neuron + hist + sweep every step
         assert st["exchange_ms"] > 0.0                  # the all-gather + k_hist span was timed
+
+
+def _count16_problem():
+    """cfg4-shaped one-weight net small enough for the oracle: ER(36000, 0.01),
+    pair-keyed delays 1..16 (the 16-bit count lists, 3 pre blocks)."""
+    from paper_2305_02510_b200.netgen import DELAY_STREAM, RandomStream, erdos_renyi_arrays, scenario_stimulus
+    n, p, seed, steps, dmax = 36000, 0.01, 11, 30, 16
+    stim = scenario_stimulus(n, steps, seed, count=300, period=2, amplitude=4.0).to_arrays()
+    pre, post = erdos_renyi_arrays(n, p, seed)
+    keys = pre.astype(np.uint64) * np.uint64(n) + post.astype(np.uint64)
+    delay = (1 + RandomStream(seed, DELAY_STREAM).below_np(keys, dmax)).astype(np.int32)
+    arrays = {"threshold": np.full(n, 3.0), "leak": np.full(n, 0.5), "reset": np.zeros(n),
+              "refractory": np.full(n, 1, np.int32), "axonal": np.zeros(n, np.int32), "pre": pre, "post": post,
+              "weight": np.ones(len(pre)), "delay": delay, "stdp": np.zeros(len(pre), np.uint8)}
+    return arrays, stim, steps
+
+
+@pytest.mark.parametrize("mode", ["host2", "host4", "nccl1"])
+def test_count16_partitions_fold_history(mode):
+    """Partitioned k_sparse_count16 runs fold k_hist into the sweep's staging
+    (history double-buffered by step parity, the step handed over by k_neuron):
+    G = 2 / 4 partitions through the host exchange and the 1-rank NCCL
+    sequence (k_neuron -> in-graph ncclAllGather -> sweep, two kernels per
+    step) reproduce the oracle's raster on a cfg4-shaped net."""
+    import paper_2305_02510_b200 as sn
+    from oracle import bridge as B
+    from paper_2305_02510_b200.engine import MatEngine, partition_range
+    arrays, stim, steps = _count16_problem()
+    n = len(arrays["threshold"])
+    o = B.run_oracle(arrays, steps, stim)
+    assert len(o["steps"]) > 5000
+    world = {"host2": 2, "host4": 4, "nccl1": 1}[mode]
+    engines = []
+    for r in range(world):
+        e = MatEngine(storage=2, rank=r, world=world, persistent=False)
+        e.add_neurons(arrays["threshold"], arrays["leak"], arrays["reset"], arrays["refractory"], arrays["axonal"])
+        e.add_synapses(arrays["pre"], arrays["post"], arrays["weight"], arrays["delay"], None)
+        e.setup()
+        e.add_stimulus(*stim)
+        engines.append(e)
+    if mode == "nccl1":
+        e = engines[0]
+        e.comm_init(sn.comm_unique_id(), 0, 1)
+        e.simulate(13)
+        e.simulate(steps - 13)
+        assert e.stats()["kernel_launches"] == 2 * steps     # no k_hist
+    else:
+        wpr = (partition_range(n, 0, world)[1] + 31) // 32
+        for _ in range(steps):
+            for e in engines:
+                e.step_local()
+            words = [e.spike_words(wpr * world)[r * wpr:(r + 1) * wpr].copy() for r, e in enumerate(engines)]
+            for r, e in enumerate(engines):
+                for q in range(world):
+                    if q != r:
+                        e.put_spike_words(q * wpr, words[q])
+            for e in engines:
+                e.step_finish()
+    assert all(e.stats()["sweep_kernel"] == 13 for e in engines)   # k_sparse_count16
+    rasters = [e.raster() for e in engines]
+    s = np.concatenate([x[0] for x in rasters])
+    q = np.concatenate([x[1] for x in rasters])
+    order = np.lexsort((q, s))
+    assert np.array_equal(s[order], o["steps"]) and np.array_equal(q[order], o["neurons"])
+    mem = np.concatenate([e.membrane() for e in engines])
+    assert close_rel(mem, o["membrane"])
+    for e in engines:
+        e.close()
