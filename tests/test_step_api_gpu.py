@@ -137,3 +137,34 @@ def test_plasticity_switch_matches_reference(storage, dmax):
     assert np.array_equal(e.synapse_weights(), o["weights"])
     assert close_rel(e.membrane(), o["membrane"])
     e.close()
+
+
+def test_new_entry_points_error_contract():
+    """Error behaviour of the round-2 entry points: wrong ext length
+    (mat_step's message), plasticity toggles on a net without STDP (no-op),
+    the weight census on sparse storage and delay relays on a partitioned
+    engine (SN_ERR_UNSUPPORTED), and a 1-rank communicator after the first
+    step (SN_ERR_LOGIC)."""
+    import paper_2305_02510_b200 as sn
+    arrays, stim, sd, steps = _problem(n=64, steps=10)
+    e = _engine(arrays, None, 2)
+    e.set_plasticity(False)
+    e.set_plasticity(True)                        # no STDP configured: nothing to apply
+    with pytest.raises(ValueError, match="mat_step: ext must have one amplitude per neuron"):
+        e.step(np.zeros(65))
+    with pytest.raises(NotImplementedError, match="dense weight storage"):
+        e.weight_value_counts([1.0])
+    e.close()
+    e = _engine(arrays, None, 1, "f64")
+    e.simulate(1)
+    with pytest.raises(RuntimeError, match="before its first step"):
+        e.comm_init(sn.comm_unique_id(), 0, 1)
+    e.close()
+    from paper_2305_02510_b200.engine import MatEngine
+    a = dict(arrays, delay=np.full(len(arrays["pre"]), 90, np.int32))
+    e = MatEngine(storage=1, rank=0, world=2)
+    e.add_neurons(a["threshold"], a["leak"], a["reset"], a["refractory"], a["axonal"])
+    e.add_synapses(a["pre"], a["post"], a["weight"], a["delay"], a["stdp"])
+    with pytest.raises(NotImplementedError, match="single-partition engines only"):
+        e.setup()
+    e.close()
