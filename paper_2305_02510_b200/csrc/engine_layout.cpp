@@ -467,8 +467,7 @@ void Engine::plan_launches() {
         }
         const int items = ntiles * nchunks_;
         if (exact_) dense_grid_ = std::min(items, sms * 8);
-        const int prows = nchunks_ * (tma_ ? dense_tma_partials_per_chunk() : 1);
-        d_partial_.alloc(static_cast<size_t>(prows) * std::max(nl_, 1) * 8);
+        d_partial_.alloc(static_cast<size_t>(nchunks_) * std::max(nl_, 1) * 8);
         cuda_check(cudaMemsetAsync(d_partial_.p, 0, d_partial_.bytes, stream_), "memset");
     } else {
         const double avg = nl_ > 0 ? static_cast<double>(sparse_elems_) / (static_cast<double>(nblocks_) * nl_) : 0.0;

@@ -126,7 +126,7 @@ NeuronArgs Engine::neuron_args(int t_base, int rows, uint32_t* raster, double* t
     a.refr = d_refr_.as<int32_t>();
     a.cnt = d_cnt_.as<int32_t>();
     a.partial = d_partial_.as<double>();
-    a.nchunks = nchunks_ * ((dense_ && tma_) ? dense_tma_partials_per_chunk() : 1);  // partial rows to sum
+    a.nchunks = nchunks_;  // partial rows to sum
     a.u_exact = d_uexact_.as<double>();
     a.st_off = st_off;
     a.st_neuron = st_neuron;

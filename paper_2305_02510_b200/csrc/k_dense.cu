@@ -195,7 +195,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_dense_stream(DenseArgs a) {
 // Consumer warp w owns column slot w & 7 of every row r = w >> 3 (mod
 // kTmaHalves) of a stage: two halves give each scheduler 4 consumer warps to
 // hide the fp64 STDP arithmetic's dependent latency (cfg3 sweep 1.47 ms with
-// one half), and each half writes its own partial row.
+// one half); at the end of an item half 1 hands its column
+// sums to half 0 through shared memory (fixed order: half 0 + half 1), so
+// the neuron phase still adds one partial row per row chunk.
 #ifndef SNB_TMA_HALVES
 #define SNB_TMA_HALVES 2
 #endif
@@ -205,6 +207,12 @@ constexpr int kTmaListMax = 1024;  // rows per item at most (one list per item, 
 constexpr int kTmaHalves = SNB_TMA_HALVES;
 constexpr int kTmaConsumers = 8 * kTmaHalves;               // consumer warps
 constexpr int kTmaThreads = 32 * (kTmaConsumers + 2);       // + 1 producer warp + 1 planner warp
+static_assert(kTmaHalves == 1 || kTmaHalves == 2, "row halves");
+constexpr int kTmaXchDoubles = kTmaHalves > 1 ? 8 * 32 * 4 : 0;  // half-1 column sums (VEC <= 4)
+
+__device__ __forceinline__ void tma_consumer_bar() {  // the consumer warps only (named barrier 1)
+    asm volatile("bar.sync 1, %0;" ::"r"(kTmaConsumers * 32) : "memory");
+}
 constexpr int kTmaDp = 4;          // delayed STDP: pot^(d) traces staged per listed row
 // Row records of both weight types carry the fp64 trace (RowRec<double>):
 // the STDP update is computed in fp64 for fp32 storage too.
@@ -242,6 +250,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
     TmaRec* s_recs = reinterpret_cast<TmaRec*>(issued + 2);
     // delayed STDP: fp64 pot^(d) of each listed row for d = 1..kTmaDp (a.dp <= kTmaDp)
     double* s_potds = reinterpret_cast<double*>(s_recs + 2 * rec_cap);
+    double* s_xch = s_potds + ((DELAY && STDP) ? 2 * rec_cap * kTmaDp : 0);  // kTmaXchDoubles
     __shared__ int s_item[2];
     __shared__ int s_cnt[2];
 
@@ -509,10 +518,23 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
 #pragma unroll
                 for (int k = 0; k < VEC; ++k) acc[k] += static_cast<double>(grp[k]);
             }
-            if (in_tile) {
+            if (kTmaHalves > 1) {
+                double* x = s_xch + ((warp & 7) * 32 + lane) * VEC;
+                if (rh == 1) {
+#pragma unroll
+                    for (int k = 0; k < VEC; ++k) x[k] = acc[k];
+                }
+                tma_consumer_bar();
+                if (rh == 0 && in_tile) {
+#pragma unroll
+                    for (int k = 0; k < VEC; ++k)
+                        if (c0 + k < a.nl) a.partial[static_cast<int64_t>(chunk) * a.nl + c0 + k] = acc[k] + x[k];
+                }
+                tma_consumer_bar();  // x is rewritten by the next item
+            } else if (in_tile) {
 #pragma unroll
                 for (int k = 0; k < VEC; ++k)
-                    if (c0 + k < a.nl) a.partial[static_cast<int64_t>(chunk * kTmaHalves + rh) * a.nl + c0 + k] = acc[k];
+                    if (c0 + k < a.nl) a.partial[static_cast<int64_t>(chunk) * a.nl + c0 + k] = acc[k];
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(freeb + b);
@@ -524,7 +546,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_dense_tma(DenseArgs a) {
 size_t dense_tma_smem(int tile_w, bool f64, bool delay, bool stdp, int rows) {
     const size_t esz = f64 ? 8 : 4;
     return static_cast<size_t>(kTmaStages) * kTmaRows * tile_w * (esz + (delay ? 1 : 0)) + (2 * kTmaStages + 6) * 8 +
-           2 * static_cast<size_t>(rows + kTmaRows) * (sizeof(TmaRec) + ((delay && stdp) ? kTmaDp * 8 : 0));
+           2 * static_cast<size_t>(rows + kTmaRows) * (sizeof(TmaRec) + ((delay && stdp) ? kTmaDp * 8 : 0)) +
+           static_cast<size_t>(kTmaXchDoubles) * 8;
 }
 
 int smem_optin() {
@@ -539,7 +562,6 @@ int smem_optin() {
 int dense_vec(bool f64) { return f64 ? 2 : 4; }
 
 int dense_tma_max_dp() { return kTmaDp; }
-int dense_tma_partials_per_chunk() { return kTmaHalves; }
 
 // Longest item row list (a multiple of 32, <= kTmaListMax) whose two list
 // buffers fit next to the ring in the opt-in shared memory; 0 if even 32 rows

@@ -199,7 +199,6 @@ int dense_tma_max_dp();  // delayed STDP: plastic delay span the TMA sweep suppo
 int census_max_values();
 void launch_value_counts(const void* W, bool f64, int64_t pitch, int n, int nl, const void* vals, int nv,
                          unsigned long long* counts, int ctas, cudaStream_t s);
-int dense_tma_partials_per_chunk();  // partial rows the TMA sweep writes per row chunk
 int dense_tma_max_rows(int tile_w, bool f64, bool delay, bool stdp);  // longest row list whose buffers fit (0: none)
 void launch_dense_tma(const DenseArgs& a, bool f64, bool stdp, bool delay, int grid, cudaStream_t s);
 void launch_sparse(const SparseArgs& a, bool f64, bool stdp, int hbits, int sub, bool exact,
