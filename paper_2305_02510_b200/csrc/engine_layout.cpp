@@ -501,9 +501,11 @@ void Engine::plan_launches() {
                               pb_ == c16_block_pres() && c16_allowed();
         int per_sm = c16_plan ? (nl_ >= 131072 ? 12 : 4) : 8;
         if (const char* cp = std::getenv("SNB_SPARSE_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(cp));
+        const int warps = c16_plan ? c16_threads() / 32 : 8;  // per CTA
+        if (c16_plan) per_sm = std::max(1, per_sm * 8 / warps);  // same warps per SM for bigger CTAs
         const int target = sms * per_sm;
         int gx = std::max(1, target / std::max(1, nblocks_));
-        const int unit = sub_ == 0 ? 8 : 8 * (32 / sub_);
+        const int unit = sub_ == 0 ? 8 : warps * (32 / sub_);
         posts_per_cta_ = static_cast<int32_t>(round_up((nl_ + gx - 1) / gx, unit));
         posts_per_cta_ = std::max(posts_per_cta_, unit);
         sparse_gx_ = std::max(1, (nl_ + posts_per_cta_ - 1) / posts_per_cta_);

@@ -2,6 +2,8 @@
 // bank-aware list order), k_sparse_exact, k_sparse_stream and the opt-in k_sparse_tma.
 #include "kernels_common.cuh"
 
+#include <cstdlib>
+
 namespace snb {
 
 namespace {
@@ -546,9 +548,12 @@ __device__ __forceinline__ void c16_load_batch(uint4 (&m4)[UL], const uint4* src
         if (c0 + u * SUB < C) m4[u] = __ldcs(src + c0 + u * SUB);
 }
 
-template <typename WT, int SUB>
-__global__ void __launch_bounds__(kThreads, SNB_C16_MINB) k_sparse_count16(SparseArgs a, const uint2* desc,
-                                                                            const uint4* ent) {
+// NT threads per CTA: a CTA stages its pre block's 32 KB history once for
+// NT / SUB posts at a time; bigger CTAs amortise the stage over more posts
+// (what a post partition, with a G-th of the posts per block, needs).
+template <typename WT, int SUB, int NT = kThreads>
+__global__ void __launch_bounds__(NT, NT == kThreads ? SNB_C16_MINB : 1024 / NT)
+    k_sparse_count16(SparseArgs a, const uint2* desc, const uint4* ent) {
     __shared__ __align__(16) uint16_t shist[4 * 4096];
     const int b = blockIdx.y;
     const int pre0 = b * kC16Pres;
@@ -564,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, SNB_C16_MINB) k_sparse_count16(Spars
     constexpr int STEP = SUB * UL;
     const int warp = tid >> 5, lane = tid & 31;
     const int sg = lane / SUB, sl = lane % SUB;
-    const int stride = (kThreads / 32) * PER_WARP;
+    const int stride = (NT / 32) * PER_WARP;
     const uint2* db = desc + static_cast<int64_t>(b) * a.nl;
     int p = p0 + warp * PER_WARP + sg;
     uint2 d = make_uint2(0u, 0u);
@@ -1216,32 +1221,42 @@ bool launch_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* off, co
     return true;
 }
 
+template <typename WT, int NT>
+static void c16_go(const SparseArgs& a, const uint2* desc, const uint4* e, int sub, dim3 grid, cudaStream_t s) {
+    static bool carveout = false;  // 33 KB of history per CTA: let the occupancy limit be registers
+    if (!carveout) {
+        for (auto k : {k_sparse_count16<WT, 2, NT>, k_sparse_count16<WT, 4, NT>, k_sparse_count16<WT, 8, NT>,
+                       k_sparse_count16<WT, 16, NT>})
+            check(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
+        carveout = true;
+    }
+    switch (sub) {
+        case 2: k_sparse_count16<WT, 2, NT><<<grid, NT, 0, s>>>(a, desc, e); break;
+        case 4: k_sparse_count16<WT, 4, NT><<<grid, NT, 0, s>>>(a, desc, e); break;
+        case 16: k_sparse_count16<WT, 16, NT><<<grid, NT, 0, s>>>(a, desc, e); break;
+        default: k_sparse_count16<WT, 8, NT><<<grid, NT, 0, s>>>(a, desc, e); break;
+    }
+}
+
+int c16_threads() {
+    const char* t = std::getenv("SNB_C16_THREADS");  // A/B knob: threads per CTA (256, 512, 1024)
+    const int v = t ? std::atoi(t) : kThreads;
+    return (v == 512 || v == 1024) ? v : kThreads;
+}
+
 void launch_sparse_count16(const SparseArgs& a, const uint2* desc, const void* ent, bool f64, int sub, int gx,
                            cudaStream_t s) {
     dim3 grid(gx, a.nblocks);
     const uint4* e = static_cast<const uint4*>(ent);
-    static bool carveout = false;  // 33 KB of history per CTA: let the occupancy limit be registers
-    if (!carveout) {
-        for (auto k : {k_sparse_count16<float, 2>, k_sparse_count16<float, 4>, k_sparse_count16<float, 8>, k_sparse_count16<float, 16>})
-            check(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
-        for (auto k : {k_sparse_count16<double, 2>, k_sparse_count16<double, 4>, k_sparse_count16<double, 8>, k_sparse_count16<double, 16>})
-            check(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
-        carveout = true;
-    }
+    const int nt = c16_threads();
     if (f64) {
-        switch (sub) {
-            case 2: k_sparse_count16<double, 2><<<grid, kThreads, 0, s>>>(a, desc, e); break;
-            case 4: k_sparse_count16<double, 4><<<grid, kThreads, 0, s>>>(a, desc, e); break;
-            case 16: k_sparse_count16<double, 16><<<grid, kThreads, 0, s>>>(a, desc, e); break;
-            default: k_sparse_count16<double, 8><<<grid, kThreads, 0, s>>>(a, desc, e); break;
-        }
+        if (nt == 1024) c16_go<double, 1024>(a, desc, e, sub, grid, s);
+        else if (nt == 512) c16_go<double, 512>(a, desc, e, sub, grid, s);
+        else c16_go<double, kThreads>(a, desc, e, sub, grid, s);
     } else {
-        switch (sub) {
-            case 2: k_sparse_count16<float, 2><<<grid, kThreads, 0, s>>>(a, desc, e); break;
-            case 4: k_sparse_count16<float, 4><<<grid, kThreads, 0, s>>>(a, desc, e); break;
-            case 16: k_sparse_count16<float, 16><<<grid, kThreads, 0, s>>>(a, desc, e); break;
-            default: k_sparse_count16<float, 8><<<grid, kThreads, 0, s>>>(a, desc, e); break;
-        }
+        if (nt == 1024) c16_go<float, 1024>(a, desc, e, sub, grid, s);
+        else if (nt == 512) c16_go<float, 512>(a, desc, e, sub, grid, s);
+        else c16_go<float, kThreads>(a, desc, e, sub, grid, s);
     }
     check(cudaGetLastError(), "k_sparse_count16");
 }
