@@ -200,6 +200,7 @@ private:
     bool sparse_tma_ = false;  // k_sparse_tma stage plan (static uniform-weight lists)
     bool bank_ordered_ = false;  // one-weight lists dealt bank-aware for k_sparse_count
     bool c16_ = false;           // 16-bit segmented one-weight lists (k_sparse_count16)
+    int32_t c16_threads_ = 256;  // threads per k_sparse_count16 CTA (c16_threads)
     // partitioned k_sparse_count16 runs fold k_hist into the sweep's staging
     // (k_sparse.cu c16_stage): no history kernel on the step path
     bool fold_hist() const { return c16_ && !p2p_ && (opt_.world > 1 || comm_ != nullptr); }

@@ -501,7 +501,8 @@ void Engine::plan_launches() {
                               pb_ == c16_block_pres() && c16_allowed();
         int per_sm = c16_plan ? (nl_ >= 131072 ? 12 : 4) : 8;
         if (const char* cp = std::getenv("SNB_SPARSE_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(cp));
-        const int warps = c16_plan ? c16_threads() / 32 : 8;  // per CTA
+        c16_threads_ = c16_plan ? c16_threads(nl_) : 256;
+        const int warps = c16_threads_ / 32;  // per CTA
         if (c16_plan) per_sm = std::max(1, per_sm * 8 / warps);  // same warps per SM for bigger CTAs
         const int target = sms * per_sm;
         int gx = std::max(1, target / std::max(1, nblocks_));

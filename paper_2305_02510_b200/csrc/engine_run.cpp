@@ -266,7 +266,7 @@ void Engine::launch_sweep_only() {
                              d_sp_bnd_.as<uint16_t>()};
             launch_sparse_tma(a, plan, sp_ctas_, f64_, hbits_, stream_);
         } else if (c16_) {
-            launch_sparse_count16(a, d_c16desc_.as<uint2>(), d_c16ent_.p, f64_, sub_, sparse_gx_, stream_);
+            launch_sparse_count16(a, d_c16desc_.as<uint2>(), d_c16ent_.p, f64_, sub_, sparse_gx_, c16_threads_, stream_);
         } else {
             launch_sparse(a, f64_, stdp_on_, hbits_, sub_, exact_, sparse_gx_, stream_);
         }

@@ -1238,17 +1238,19 @@ static void c16_go(const SparseArgs& a, const uint2* desc, const uint4* e, int s
     }
 }
 
-int c16_threads() {
-    const char* t = std::getenv("SNB_C16_THREADS");  // A/B knob: threads per CTA (256, 512, 1024)
-    const int v = t ? std::atoi(t) : kThreads;
+int c16_threads(int nl) {
+    // full-size lists: 256-thread CTAs (cfg4 0.4127 ms; 512: 0.4165, 1024: 0.419); post
+    // partitions (an eighth of cfg4's posts per block): 1024 (65.8 us vs 70.4 at 512,
+    // 79.1 at 256) -- a CTA stages its pre block once for 4x the posts
+    int v = nl >= 131072 ? kThreads : 1024;
+    if (const char* t = std::getenv("SNB_C16_THREADS")) v = std::atoi(t);  // A/B knob: 256, 512, 1024
     return (v == 512 || v == 1024) ? v : kThreads;
 }
 
 void launch_sparse_count16(const SparseArgs& a, const uint2* desc, const void* ent, bool f64, int sub, int gx,
-                           cudaStream_t s) {
+                           int nt, cudaStream_t s) {
     dim3 grid(gx, a.nblocks);
     const uint4* e = static_cast<const uint4*>(ent);
-    const int nt = c16_threads();
     if (f64) {
         if (nt == 1024) c16_go<double, 1024>(a, desc, e, sub, grid, s);
         else if (nt == 512) c16_go<double, 512>(a, desc, e, sub, grid, s);

@@ -223,8 +223,8 @@ void launch_c16_count(const uint32_t* meta, const int64_t* off, int64_t lists, i
 bool launch_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* off, const uint2* desc, int nblocks, int nl,
                      int pb, int sub, uint16_t* out, cudaStream_t s);
 void launch_sparse_count16(const SparseArgs& a, const uint2* desc, const void* ent, bool f64, int sub, int gx,
-                           cudaStream_t s);
-int c16_threads();  // threads per k_sparse_count16 CTA
+                           int nt, cudaStream_t s);
+int c16_threads(int nl);  // threads per k_sparse_count16 CTA for nl local posts
 // TMA-fed stream for static uniform-weight lists (dictionary {w, 0}), no exact order
 size_t sparse_tma_smem(const SparseArgs& a, int hbits);
 int sparse_tma_stage_entries();
