@@ -559,7 +559,13 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, int rank) {
 
 
 // Shared-memory layout of k_cluster_count (D = 0: rotation codes; D = 8 / 16:
-// delay bit-planes).
+// delay bit-planes).  With planes, the exchange buffer is a ring of
+// cl_ring(D) = D + 2 spike-word rows: row t mod R holds s[t] of every pre, and
+// plane d of step t is row (t - d) mod R, so a step exchanges one word per 32
+// pres (not D) and only plane 0 waits for it.  D + 2 rows keep a writer's
+// step t + 1 off every row a peer can still be reading (planes 0..D-1 of its
+// step t - 1 or t).
+__host__ __device__ constexpr int cl_ring(int D) { return D > 0 ? D + 2 : 2; }
 struct ClLayout {
     size_t code, ex, red, in, bar, total;
 };
@@ -571,13 +577,13 @@ __host__ __device__ inline ClLayout cl_layout(int n, int P, int D) {
     L.code = o;
     o += D == 0 ? static_cast<size_t>(n) * P : static_cast<size_t>(P) * D * wn4 * 4;
     L.ex = o;
-    o += D == 0 ? static_cast<size_t>(2) * npad * 4 : static_cast<size_t>(2) * D * wn4 * 4;
+    o += D == 0 ? static_cast<size_t>(2) * npad * 4 : static_cast<size_t>(cl_ring(D)) * wn4 * 4;
     L.red = o;
     o += D == 0 ? static_cast<size_t>(kClThreads) * 4 * 4 : 0;
     L.in = o;
     o += static_cast<size_t>(P) * 8;
     L.bar = o;
-    o += 16;
+    o += static_cast<size_t>(cl_ring(D)) * 8;
     L.total = o;
     return L;
 }
@@ -601,7 +607,8 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
     uint32_t* s_ex = reinterpret_cast<uint32_t*>(smem + L.ex);        // [2][npad] h << 1, or [2][D][wn4] planes
     int* s_red = reinterpret_cast<int*>(smem + L.red);                // D = 0: [1024 / (P/4)][P]
     double* s_in = reinterpret_cast<double*>(smem + L.in);            // [P]
-    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L.bar);      // [2] exchange buffer full
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L.bar);      // [R] exchange buffer full
+    constexpr int R = cl_ring(D);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     {   // this CTA's code / mask block, once per call; zero the exchange buffers (plane padding)
         const size_t bytes = L.ex - L.code;
@@ -616,18 +623,31 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
     // readers (a CTA writes buffer t+1 only after every CTA's step-t words
     // reached it, i.e. after every CTA finished reading buffer t-1)
     if (tid == 0) {
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
+        for (int k = 0; k < R; ++k) mbar_init(&s_bar[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    int t = *na.d_step;
+    if (D > 0) {
+        __syncthreads();  // the zeroing above is complete
+        // ring rows of the D - 1 steps before the call, from the history words
+        // the previous call left in hist2 (bit k - 1 of pre i's word = s_i[t - k])
+        const uint64_t* hp = ca.hist2 + static_cast<int64_t>((t & 1) ^ 1) * n;
+        for (int i0 = warp * 32; i0 < n; i0 += kClThreads) {
+            const int i = i0 + lane;
+            const uint64_t h = i < n ? hp[i] : 0ull;
+            for (int k = 1; k < D; ++k) {
+                const uint32_t b = __ballot_sync(0xffffffffu, (h >> (k - 1)) & 1ull);
+                if (lane == 0) s_ex[(((t - k) % R + R) % R) * wn4 + (i0 >> 5)] = b;
+            }
+        }
+    }
     cluster.sync();
-    uint32_t ph0 = 0, ph1 = 0;
+    uint32_t ph0 = 0, ph1 = 0, phr = 0;      // phr: bit k = parity of ring row k's barrier
     const uint32_t tx_bytes = D == 0 ? 4u * static_cast<uint32_t>(na.nl)
-                                     : 4u * D * static_cast<uint32_t>((na.nl + 31) / 32);
+                                     : 4u * static_cast<uint32_t>((na.nl + 31) / 32);
     const int p = tid;                       // owner thread of post j (tid < P)
     const int j = r * P + p;
     const bool own = tid < P && j < na.nl;
-    int t = *na.d_step;
     double v = 0.0, thr = 0.0, leak = 0.0, rst = 0.0, fire_p = 1.0, in = 0.0;
     int32_t cnt = 0, refr = 0;
     uint64_t hprev = 0, akey = 0;
@@ -674,7 +694,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
         }
     }
     for (int s = 0; s < steps; ++s, ++t) {
-        const int cur = t & 1;
+        const int cur = D > 0 ? t % R : (t & 1);  // exchange row / buffer of this step
         if (tid == 0) mbar_arrive_expect_tx(&s_bar[cur], tx_bytes);
         if (tid < P) {  // (1) LIF update of the owned posts (k_persistent_cols' neuron phase)
             bool fired = false;
@@ -719,20 +739,12 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
                 }
             }
             const bool live = (r * P + warp * 32) < na.nl;  // warp-uniform
-            if (D > 0) {  // delay planes: lane d holds the word of bit d of the warp's 32 pres
-                uint32_t mine = 0;
-#pragma unroll
-                for (int d = 0; d < D; ++d) {
-                    const uint32_t b = __ballot_sync(0xffffffffu, (hn >> d) & 1ull);
-                    if (lane == d) mine = b;
-                }
-                if (live && lane < D) {
-                    const int w = (r * P) / 32 + warp;
-                    const uint32_t la = smem_u32(s_ex + (cur * D + lane) * wn4 + w), lb = smem_u32(&s_bar[cur]);
-                    for (int q = 0; q < cs; ++q) st_async_u32(mapa_u32(la, q), mine, mapa_u32(lb, q));
-                }
-            }
             const uint32_t word = __ballot_sync(0xffffffffu, fired);
+            if (D > 0 && live && lane < cs) {  // the warp's spike word of step t into ring row t of CTA `lane`
+                const int w = (r * P) / 32 + warp;
+                const uint32_t la = smem_u32(s_ex + cur * wn4 + w), lb = smem_u32(&s_bar[cur]);
+                st_async_u32(mapa_u32(la, lane), word, mapa_u32(lb, lane));
+            }
             if (lane == 0 && na.raster && (t - na.t_base) < na.raster_rows && live)
                 na.raster[static_cast<int64_t>(t - na.t_base) * na.nl_words + ((r * P) >> 5) + warp] = word;
         }
@@ -740,9 +752,11 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
         // (the async-proxy stores are tracked by complete_tx, so a CTA-scope wait
         // sees them, as for bulk copies; an acquire.cluster wait adds an L1
         // invalidation per step: 2.81e5 vs 2.86e5 steps/s on cfg2)
-        if (cur) { mbar_wait(&s_bar[1], ph1); ph1 ^= 1u; }
-        else { mbar_wait(&s_bar[0], ph0); ph0 ^= 1u; }
         stim_bounds(t + 1);
+        if (D == 0) {
+            if (cur) { mbar_wait(&s_bar[1], ph1); ph1 ^= 1u; }
+            else { mbar_wait(&s_bar[0], ph0); ph0 ^= 1u; }
+        }
         // (3) counts of the delivering pres for this CTA's posts (integers: any order is exact)
         if (D > 0) {
             // thread (post, delay d, part): popc(mask[post][d] & plane[d]) over its words
@@ -750,24 +764,36 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
             constexpr int T = kClThreads / PAIRS >= 4 ? 4 : kClThreads / PAIRS >= 2 ? 2 : 1;
             static_assert(D == 0 || (PAIRS <= kClThreads && D * T <= 32), "cluster plane tiling");
             int sum = 0;
-            if (tid < PAIRS * T) {
-                const int pi = tid / T, part = tid % T;
-                const int pp = pi / (D > 0 ? D : 1), d = pi % (D > 0 ? D : 1);
-                const int per_part = wn4 / T;  // multiple of 4
-                const uint4* e4 = reinterpret_cast<const uint4*>(s_ex + (cur * D + d) * wn4 + part * per_part);
+            const int pi = tid / T, part = tid % T;
+            const int pp = pi / (D > 0 ? D : 1), d = pi % (D > 0 ? D : 1);
+            const int per_part = wn4 / T;  // multiple of 4
+            const bool pair = tid < PAIRS * T;
+            auto plane_count = [&]() {
+                const int row = ((t - d) % R + R) % R;  // plane d of step t = s[t - d]
+                const uint4* e4 = reinterpret_cast<const uint4*>(s_ex + row * wn4 + part * per_part);
+                int c = 0;
                 if (SNB_CL_MREG && per_part == 4 * kClMregs) {  // mask words in registers for the call
 #pragma unroll
                     for (int k = 0; k < kClMregs; ++k) {
                         const uint4 m = mreg[k], e = e4[k];
-                        sum += __popc(m.x & e.x) + __popc(m.y & e.y) + __popc(m.z & e.z) + __popc(m.w & e.w);
+                        c += __popc(m.x & e.x) + __popc(m.y & e.y) + __popc(m.z & e.z) + __popc(m.w & e.w);
                     }
                 } else {
                     const uint4* m4 = reinterpret_cast<const uint4*>(s_mask + (pp * D + d) * wn4 + part * per_part);
                     for (int k = 0; k < per_part / 4; ++k) {
                         const uint4 m = m4[k], e = e4[k];
-                        sum += __popc(m.x & e.x) + __popc(m.y & e.y) + __popc(m.z & e.z) + __popc(m.w & e.w);
+                        c += __popc(m.x & e.x) + __popc(m.y & e.y) + __popc(m.z & e.z) + __popc(m.w & e.w);
                     }
                 }
+                return c;
+            };
+            // planes 1..D-1 are rows of earlier steps, already here: counted while
+            // this step's words are in flight; plane 0 after the row's barrier
+            if (pair && d > 0) sum = plane_count();
+            mbar_wait(&s_bar[cur], (phr >> cur) & 1u);
+            phr ^= 1u << cur;
+            if (pair && d == 0) sum = plane_count();
+            if (pair) {
 #pragma unroll
                 for (int o = (D * T) / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
                 if (d == 0 && part == 0) s_in[pp] = static_cast<double>(static_cast<WT>(sum) * w0);

@@ -155,12 +155,19 @@ def test_new_entry_points_error_contract():
     with pytest.raises(NotImplementedError, match="dense weight storage"):
         e.weight_value_counts([1.0])
     e.close()
-    e = _engine(arrays, None, 1, "f64")
+    from paper_2305_02510_b200.engine import MatEngine
+    e = MatEngine(storage=1, precision="f64", persistent=False)
+    e.add_neurons(arrays["threshold"], arrays["leak"], arrays["reset"], arrays["refractory"], arrays["axonal"])
+    e.add_synapses(arrays["pre"], arrays["post"], arrays["weight"], arrays["delay"], arrays["stdp"])
+    e.setup()
     e.simulate(1)
     with pytest.raises(RuntimeError, match="before its first step"):
         e.comm_init(sn.comm_unique_id(), 0, 1)
     e.close()
-    from paper_2305_02510_b200.engine import MatEngine
+    e = _engine(arrays, None, 0)                  # the one-CTA whole-call loop cannot join a communicator
+    with pytest.raises(RuntimeError, match="whole simulate calls in one kernel"):
+        e.comm_init(sn.comm_unique_id(), 0, 1)
+    e.close()
     a = dict(arrays, delay=np.full(len(arrays["pre"]), 90, np.int32))
     e = MatEngine(storage=1, rank=0, world=2)
     e.add_neurons(a["threshold"], a["leak"], a["reset"], a["refractory"], a["axonal"])
