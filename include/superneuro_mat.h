@@ -232,6 +232,15 @@ SN_API sn_status sn_setup(sn_engine* e);
 SN_API sn_status sn_simulate(sn_engine* e, int32_t steps);
 /* Blocks until all queued device work of the engine is done. */
 SN_API sn_status sn_synchronize(sn_engine* e);
+/* sn_simulate plus the raster of exactly these steps, (step, neuron)
+ * ascending, written into the caller's arrays -- the RunResult.raster of a
+ * mat_run over these steps (mat_engine.cpp:252-287).  capacity must cover the
+ * events (steps x neurons is always enough); *count receives their number.
+ * With stream_io and graphs, finished 16-step chunks are expanded on the host
+ * while later chunks run on the device.  The events also stay available to
+ * sn_get_raster. */
+SN_API sn_status sn_simulate_raster(sn_engine* e, int32_t steps, int32_t* out_steps, int32_t* out_neurons,
+                                    int64_t capacity, int64_t* count);
 /* One step of mat_step (mat_engine.cpp:168-208; the borrowed spike list of
  * mat_engine.hpp:92-94): the step's external input is exactly `ext` -- n
  * amplitudes, or ext_len = 0 for none (the stimulus schedule is not consulted

@@ -115,6 +115,7 @@ SIGNATURES = {
     "sn_simulate": (_i32, [_P, _i32]),
     "sn_synchronize": (_i32, [_P]),
     "sn_step": (_i32, [_P, _pdbl, _i64, _pi32, _i64, _pi64]),
+    "sn_simulate_raster": (_i32, [_P, _i32, _pi32, _pi32, _i64, _pi64]),
     "sn_set_plasticity": (_i32, [_P, _i32]),
     "sn_raster_size": (_i32, [_P, _pi64]),
     "sn_get_raster": (_i32, [_P, _pi32, _pi32, _i64]),

@@ -310,6 +310,14 @@ sn_status sn_step(sn_engine* e, const double* ext, int64_t ext_len, int32_t* spi
     });
 }
 
+sn_status sn_simulate_raster(sn_engine* e, int32_t steps, int32_t* out_steps, int32_t* out_neurons,
+                             int64_t capacity, int64_t* count) {
+    return guard([&] {
+        SN_NEED(e);
+        e->impl.simulate_raster(steps, out_steps, out_neurons, capacity, count);
+    });
+}
+
 sn_status sn_set_plasticity(sn_engine* e, int32_t enabled) {
     return guard([&] {
         SN_NEED(e);

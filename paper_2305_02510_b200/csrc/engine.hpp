@@ -89,6 +89,9 @@ public:
     void set_fire_probability(int64_t first, int64_t count, const double* p);
     void setup();
     void simulate(int32_t steps);
+    // simulate + the raster of exactly these steps into the caller's arrays;
+    // with stream_io and graphs, finished chunks are decoded while later ones run
+    void simulate_raster(int32_t steps, int32_t* out_steps, int32_t* out_neurons, int64_t cap, int64_t* count);
     void synchronize();
 
     int64_t raster_size();
@@ -139,6 +142,14 @@ private:
     void launch_sweep();
     void launch_sweep_only();  // no launch accounting (graph capture counts in bulk)
     double run_graph_chunks(const NeuronArgs& na, int steps);
+    struct RasterSink {
+        int32_t* steps = nullptr;
+        int32_t* neurons = nullptr;
+        int64_t cap = 0, count = 0;
+        int32_t rows_done = 0;    // rows of the call already decoded into the arrays
+    };
+    RasterSink* sink_ = nullptr;  // set by simulate_raster for one call
+    void sink_rows(const uint32_t* rows, int32_t nrows, int32_t t_first);
     static constexpr int kProfStride = 8;  // graph mode: time every 8th step's kernels
     int64_t steps_at_reset_ = 0;
     DenseArgs dense_args();

@@ -321,8 +321,11 @@ void Engine::enqueue_step(const NeuronArgs& na, bool exchange) {
 // costs while reporting per-kernel device time.  Returns the summed device
 // time of the chunks.
 double Engine::run_graph_chunks(const NeuronArgs& na, int steps) {
-    const int chunk = std::min(steps, 64);
     const bool prof = opt_.profile != 0;
+    // a raster sink with stream_io decodes each finished chunk while the next
+    // ones run: 16-step chunks leave only the last one's decode exposed
+    const bool overlap = sink_ && opt_.stream_io && na.raster && !prof;
+    const int chunk = std::min(steps, overlap ? 16 : 64);
     const bool fused = opt_.world == 1 && !comm_;  // a 1-rank communicator runs the partitioned sequence
     const int per = 6;
     std::vector<cudaEvent_t> ev(prof ? static_cast<size_t>(chunk) * per : 0);
@@ -385,6 +388,15 @@ double Engine::run_graph_chunks(const NeuronArgs& na, int steps) {
             }
         }
         done += k;
+    }
+    if (overlap) {  // every chunk is queued: decode each as its end event fires
+        int row = 0;
+        for (auto& sp : spans) {
+            cuda_check(cudaEventSynchronize(sp.second), "chunk sync");
+            const int k = std::min(chunk, steps - row);
+            sink_rows(na.raster + static_cast<size_t>(row) * nl_words_, k, na.t_base + row);
+            row += k;
+        }
     }
     cuda_check(cudaStreamSynchronize(stream_), "simulate sync");
     for (auto& sp : spans) {
@@ -601,6 +613,87 @@ void Engine::simulate(int32_t steps) {
 }
 
 void Engine::synchronize() { cuda_check(cudaStreamSynchronize(stream_), "sn_synchronize"); }
+
+// Rows of spike words -> (step, neuron) events appended to the sink, rows in
+// parallel (the same expansion as get_raster); relay neurons' bits skipped.
+void Engine::sink_rows(const uint32_t* rows, int32_t nrows, int32_t t_first) {
+    RasterSink& k = *sink_;
+    const int lim = relays_ ? n_user_ - first_ : nl_;  // local ids below lim are the caller's
+    auto word_of = [&](const uint32_t* row, int w) {
+        const int lo = lim - w * 32;
+        return lo >= 32 ? row[w] : lo <= 0 ? 0u : (row[w] & ((1u << lo) - 1u));
+    };
+    std::vector<int64_t> start(static_cast<size_t>(nrows) + 1, 0);
+    for (int r = 0; r < nrows; ++r) {
+        const uint32_t* row = rows + static_cast<size_t>(r) * nl_words_;
+        int64_t c = 0;
+        for (int w = 0; w < nl_words_; ++w) c += __builtin_popcount(word_of(row, w));
+        start[r + 1] = start[r] + c;
+    }
+    if (k.count + start[nrows] > k.cap)
+        throw InvalidArgument("sn_simulate_raster: capacity " + std::to_string(k.cap) + " < " +
+                              std::to_string(k.count + start[nrows]) + " events");
+    auto expand = [&](int a, int b) {
+        for (int r = a; r < b; ++r) {
+            const uint32_t* row = rows + static_cast<size_t>(r) * nl_words_;
+            int64_t o = k.count + start[r];
+            for (int w = 0; w < nl_words_; ++w)
+                for (uint32_t x = word_of(row, w); x; x &= x - 1) {
+                    k.steps[o] = t_first + r;
+                    k.neurons[o] = first_ + w * 32 + __builtin_ctz(x);
+                    ++o;
+                }
+        }
+    };
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const int nthreads = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({static_cast<int64_t>(hw),
+                                                                               start[nrows] / 65536, nrows})));
+    if (nthreads == 1) {
+        expand(0, nrows);
+    } else {
+        std::vector<std::thread> pool;
+        const int per = (nrows + nthreads - 1) / nthreads;
+        for (int i = 0; i < nthreads; ++i) {
+            const int a = i * per, b = std::min(nrows, a + per);
+            if (a < b) pool.emplace_back(expand, a, b);
+        }
+        for (auto& th : pool) th.join();
+    }
+    k.count += start[nrows];
+    k.rows_done += nrows;
+}
+
+void Engine::simulate_raster(int32_t steps, int32_t* out_steps, int32_t* out_neurons, int64_t cap, int64_t* count) {
+    require_setup("sn_simulate_raster");
+    if (!count || (cap > 0 && (!out_steps || !out_neurons))) throw InvalidArgument("sn_simulate_raster: null parameter");
+    RasterSink k;
+    k.steps = out_steps;
+    k.neurons = out_neurons;
+    k.cap = cap;
+    sink_ = &k;
+    const int32_t t0 = t_;
+    try {
+        simulate(steps);
+    } catch (...) {
+        sink_ = nullptr;
+        throw;
+    }
+    sink_ = nullptr;
+    if (k.rows_done < steps) {  // no overlap on this path: decode the call's rows now
+        const RasterChunk& ch = raster_.back();
+        if (ch.t0 != t0 || ch.rows != steps) throw LogicError("sn_simulate_raster: the call's raster rows are missing");
+        sink_ = &k;
+        try {
+            sink_rows(ch.words.data() + static_cast<size_t>(k.rows_done) * nl_words_, steps - k.rows_done,
+                      t0 + k.rows_done);
+        } catch (...) {
+            sink_ = nullptr;
+            throw;
+        }
+        sink_ = nullptr;
+    }
+    *count = k.count;
+}
 
 // ---- host-driven exchange (partition emulation / custom transports) ---------
 void Engine::set_plasticity(bool on) {

@@ -133,6 +133,17 @@ class MatEngine:
     def synchronize(self):
         check(lib.sn_synchronize(self._h))
 
+    def simulate_raster(self, steps: int):
+        """simulate(steps) and that call's raster as (steps, neurons) int32
+        arrays; with stream_io the host expands finished chunks while later
+        ones run (sn_simulate_raster)."""
+        cap = int(steps) * max(1, self.stats()["n_local"])
+        s = np.empty(cap, np.int32)
+        q = np.empty(cap, np.int32)
+        cnt = C.c_int64()
+        check(lib.sn_simulate_raster(self._h, int(steps), ptr(s, C.c_int32), ptr(q, C.c_int32), cap, C.byref(cnt)))
+        return s[:cnt.value], q[:cnt.value]
+
     def step(self, ext=None) -> np.ndarray:
         """mat_step (mat_engine.cpp:168-208): one step with external input
         exactly `ext` (n amplitudes, or None), then apply_stdp when plasticity

@@ -175,3 +175,39 @@ def test_new_entry_points_error_contract():
     with pytest.raises(NotImplementedError, match="single-partition engines only"):
         e.setup()
     e.close()
+
+
+@pytest.mark.parametrize("opts", [dict(storage=2, stream_io=True), dict(storage=1, stream_io=True, persistent=False),
+                                  dict(storage=1, stream_io=False, persistent=False), dict(storage=0, stream_io=True),
+                                  dict(storage=2, stream_io=True, use_graphs=False)],
+                         ids=["sparse_io", "dense_io", "dense_noio", "tiny_io", "sparse_io_nograph"])
+def test_simulate_raster_equals_simulate_then_raster(opts):
+    """sn_simulate_raster (the events of exactly the call's steps, expanded
+    chunk by chunk while later chunks run when stream_io is on) equals
+    simulate + raster on the same engine configuration, across calls."""
+    from paper_2305_02510_b200.engine import MatEngine
+    arrays, stim, sd, steps = _problem(n=300, steps=90)
+
+    def make():
+        e = MatEngine(precision="f64", **opts)
+        e.add_neurons(arrays["threshold"], arrays["leak"], arrays["reset"], arrays["refractory"], arrays["axonal"])
+        e.add_synapses(arrays["pre"], arrays["post"], arrays["weight"], arrays["delay"], arrays["stdp"])
+        e.set_stdp(*sd)
+        e.setup()
+        e.add_stimulus(*stim)
+        return e
+
+    a = make()
+    a.simulate(37)
+    a.simulate(steps - 37)
+    s_ref, q_ref = a.raster()
+    a.close()
+    b = make()
+    s1, q1 = b.simulate_raster(37)
+    s2, q2 = b.simulate_raster(steps - 37)
+    s_all, q_all = b.raster()
+    b.close()
+    assert len(s_ref) > 500
+    assert np.array_equal(np.concatenate([s1, s2]), s_ref) and np.array_equal(np.concatenate([q1, q2]), q_ref)
+    assert np.all(s1 < 37) and np.all(s2 >= 37)
+    assert np.array_equal(s_all, s_ref) and np.array_equal(q_all, q_ref)
