@@ -426,8 +426,16 @@ void Engine::setup() {
     require_not_setup("sn_setup");
     cuda_check(cudaSetDevice(opt_.device), "cudaSetDevice");
     validate();
-    if (thr_.empty()) throw InvalidArgument(std::string(abm_ ? "abm world" : "mat_init") + ": the network has no neurons");
     n_user_ = static_cast<int32_t>(thr_.size());
+    if (thr_.empty()) {
+        // mat_init / AbmWorld accept an empty network (mat_engine.cpp:109-166 has no
+        // minimum size): every step is empty; no device state is needed
+        n_ = nl_ = nl_words_ = 0;
+        m_user_ = 0;
+        setup_done_ = true;
+        stats_.n_local = 0;
+        return;
+    }
     m_user_ = static_cast<int64_t>(pre_.size());
     if (!generated_) add_delay_relays();
     n_ = static_cast<int32_t>(thr_.size());

@@ -130,6 +130,7 @@ void Engine::get_synapse_weights(double* out, int64_t count) {
     require_setup("sn_get_synapse_weights");
     if (generated_) throw Unsupported("sn_get_synapse_weights: generated networks have no synapse list; use sn_get_weight_matrix");
     if (count < m_user_) throw InvalidArgument("sn_get_synapse_weights: buffer too small");
+    if (m_user_ == 0) return;
     cuda_check(cudaStreamSynchronize(stream_), "sync");
     const size_t esz = f64_ ? 8 : 4;
     std::vector<uint8_t> host(d_w_.bytes);
@@ -177,6 +178,7 @@ void Engine::weight_value_counts(const double* values, int32_t count, int64_t* c
 
 void Engine::get_weight_matrix(double* out, int64_t count) {
     require_setup("sn_get_weight_matrix");
+    if (n_ == 0) return;
     if (relays_) {  // the caller's n x n matrix: each synapse at its own (pre, post), relays hidden
         if (count < static_cast<int64_t>(n_user_) * n_user_) throw InvalidArgument("sn_get_weight_matrix: buffer too small");
         std::vector<double> w(static_cast<size_t>(m_user_));
@@ -216,7 +218,7 @@ void Engine::get_weight_matrix(double* out, int64_t count) {
 }
 
 void Engine::get_stats(sn_stats* out) {
-    if (setup_done_) {
+    if (setup_done_ && n_ > 0) {
         unsigned long long c[2] = {0, 0};
         d2h(c, d_spikes_.p, 16, "stats D2H");
         strip_relays();
@@ -258,7 +260,7 @@ void Engine::reset_stats() {
     stats_.kernel_launches = 0;
     stats_.sweep_bytes_total = 0.0;
     steps_at_reset_ = t_;
-    if (setup_done_) cuda_check(cudaMemsetAsync(d_spikes_.as<unsigned long long>() + 1, 0, 8, stream_), "reset");
+    if (setup_done_ && n_ > 0) cuda_check(cudaMemsetAsync(d_spikes_.as<unsigned long long>() + 1, 0, 8, stream_), "reset");
 }
 
 }  // namespace snb

@@ -431,6 +431,18 @@ void Engine::simulate(int32_t steps) {
     NvtxRange nv("sn_simulate");
     require_setup("sn_simulate");
     if (steps < 1) throw InvalidArgument(run_name() + ": steps must be >= 1");
+    if (n_ == 0) {  // empty network: empty steps
+        RasterChunk ch;
+        ch.t0 = t_;
+        ch.rows = steps;
+        raster_.push_back(std::move(ch));
+        if (opt_.record_membrane) trace_rows_ += steps;
+        t_ += steps;
+        stats_.steps_done = t_;
+        stats_.last_simulate_ms = 0.0;
+        events_valid_ = false;
+        return;
+    }
     if (opt_.world > 1 && !comm_ && !p2p_)
         throw LogicError("sn_simulate: partitioned engine needs sn_comm_init or sn_p2p_open "
                          "(or use sn_step_local/sn_step_finish)");
@@ -765,6 +777,7 @@ void Engine::step(const double* ext, int64_t ext_len, int32_t* spikes, int64_t c
 void Engine::step_local() {
     NvtxRange nv("sn_step_local");
     require_setup("sn_step_local");
+    if (n_ == 0) throw LogicError("sn_step_local: the network has no neurons");
     if (tiny_) throw LogicError("sn_step_local: single-partition engines run through sn_simulate");
     host_exchange_ = true;
     note_first_plastic_step();
@@ -799,6 +812,7 @@ void Engine::put_spike_words(int32_t first_word, const uint32_t* w, int64_t coun
 void Engine::step_finish() {
     NvtxRange nv("sn_step_finish");
     require_setup("sn_step_finish");
+    if (n_ == 0) throw LogicError("sn_step_finish: the network has no neurons");
     if (tiny_) throw LogicError("sn_step_finish: single-partition engines run through sn_simulate");
     if (opt_.world > 1 && !fold_hist()) {
         launch_hist(hist_args(), stream_);

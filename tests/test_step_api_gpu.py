@@ -211,3 +211,33 @@ def test_simulate_raster_equals_simulate_then_raster(opts):
     assert np.array_equal(np.concatenate([s1, s2]), s_ref) and np.array_equal(np.concatenate([q1, q2]), q_ref)
     assert np.all(s1 < 37) and np.all(s2 >= 37)
     assert np.array_equal(s_all, s_ref) and np.array_equal(q_all, q_ref)
+
+
+def test_empty_network_runs_like_the_reference():
+    """mat_run / abm_run accept a network with no neurons (no minimum size in
+    mat_init, mat_engine.cpp:109-166): T empty steps, an empty raster; a
+    stimulus entry is then out of range with the reference's message."""
+    import paper_2305_02510_b200 as sn
+    from oracle import bridge as B
+    net = sn.NetworkDef()
+    r = sn.mat_run(net, sn.SimulationConfig(steps=7))
+    assert len(r.raster.events) == 0 and r.raster.step_count == 7 and r.raster.neuron_count == 0
+    if B.ref_available():
+        ref = B.run_ref_mat({"threshold": np.zeros(0), "leak": np.zeros(0), "reset": np.zeros(0),
+                             "refractory": np.zeros(0, np.int32), "pre": [], "post": [], "weight": []}, 7)
+        assert len(ref["steps"]) == 0
+    from paper_2305_02510_b200.engine import MatEngine
+    for mode in ("mat", "abm"):
+        e = MatEngine(mode=mode, record_membrane=True)
+        e.setup()
+        e.simulate(3)
+        assert len(e.step(None)) == 0
+        s, q = e.raster()
+        assert len(s) == 0 and len(e.membrane()) == 0 and e.membrane_trace().shape == (4, 0)
+        assert e.stats()["spike_count"] == 0 and e.stats()["steps_done"] == 4
+        with pytest.raises(ValueError, match="out of range"):
+            e.add_stimulus(np.array([0], np.int32), np.array([0], np.int32), np.array([1.0]))
+        e.close()
+    with pytest.raises(ValueError, match=r"stimulus\[0\]: neuron id 0 out of range \(0 neurons\)"):
+        sn.mat_run(net, sn.SimulationConfig(steps=3),
+                   sn.StimulusSchedule([sn.StimulusEntry(0, 0, 1.0)]))
