@@ -296,6 +296,7 @@ private:
     // delay relays (effective delays > kMaxNativeDelay): relay neurons appended
     // after the user's, raster bits of ids >= n_user_ stripped on the host
     static constexpr int kMaxNativeDelay = 64;
+    static constexpr int kMinGraphSteps = 4;  // shorter simulate calls launch without a graph
     void add_delay_relays();
     void strip_relays();
     bool relays_ = false;

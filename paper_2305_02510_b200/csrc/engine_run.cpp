@@ -587,7 +587,9 @@ void Engine::simulate(int32_t steps) {
                 pending_.push_back({p0, p1, 1, 0.0});
             }
             cuda_check(cudaEventRecord(ee, stream_), "rec");
-        } else if (opt_.use_graphs) {
+        } else if (opt_.use_graphs && steps >= kMinGraphSteps) {
+            // (a capture + instantiate costs ~1 ms: calls of a few steps, sn_step's
+            // in particular, launch their kernels directly)
             graph_ms = run_graph_chunks(na, steps);
             cuda_check(cudaEventRecord(ee, stream_), "rec");
         } else {
