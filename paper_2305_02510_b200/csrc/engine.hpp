@@ -214,7 +214,7 @@ private:
     int32_t c16_threads_ = 256;  // threads per k_sparse_count16 CTA (c16_threads)
     // partitioned k_sparse_count16 runs fold k_hist into the sweep's staging
     // (k_sparse.cu c16_stage): no history kernel on the step path
-    bool fold_hist() const { return c16_ && !p2p_ && (opt_.world > 1 || comm_ != nullptr); }
+    bool fold_hist() const { return c16_ && (opt_.world > 1 || comm_ != nullptr); }
     DevBuf d_hist16_, d_step_copy_;
     DevBuf d_c16desc_, d_c16ent_;
     bool build_c16();

@@ -258,6 +258,13 @@ void Engine::launch_sweep_only() {
         if (fold_hist()) {
             a.step_in = d_step_copy_.as<int32_t>();
             a.hist16 = d_hist16_.as<uint16_t>();
+            if (p2p_) {  // the sweep itself waits for the peers' words of the step (no k_hist)
+                a.flags = d_flags_.as<int32_t>();
+                a.world = opt_.world;
+                a.error = d_err_.as<int32_t>();
+                a.xbits = d_xbits_.as<uint32_t>();
+                a.xstride = static_cast<int32_t>(d_xbits_.bytes / 8);
+            }
         }
         if (nl_ == 0) {
             launch_step_bump(a.d_step, stream_);

@@ -453,6 +453,22 @@ __device__ __forceinline__ void c16_stage(const SparseArgs& a, int pre0, int pco
         // folded history: h = (history after step t - 1) << 1 | s[t]; the first CTA
         // of the pre block commits it to the other parity buffer for step t + 1
         const int t = *a.step_in;
+        const uint32_t* bits = a.bits;
+        if (a.flags) {  // p2p: every rank's step-t words have landed in exchange buffer t & 1
+            if (threadIdx.x == 0) {
+                const uint64_t g0 = globaltimer_ns();
+                for (int q = 0; q < a.world; ++q)
+                    while (ld_acquire_sys(a.flags + q) <= t) {
+                        if (globaltimer_ns() - g0 > 30ull * 1000000000ull) {  // 30 s: a peer died
+                            atomicExch(a.error, 1);
+                            break;
+                        }
+                        __nanosleep(200);
+                    }
+            }
+            __syncthreads();
+            bits = a.xbits + static_cast<int64_t>(t & 1) * a.xstride;
+        }
         const uint16_t* hin = a.hist16 + static_cast<int64_t>(t & 1) * a.n;
         uint16_t* hout = a.hist16 + static_cast<int64_t>((t + 1) & 1) * a.n;
         const bool commit = blockIdx.x == 0;
@@ -468,7 +484,7 @@ __device__ __forceinline__ void c16_stage(const SparseArgs& a, int pre0, int pco
                 const int pre = s * kC16SegPres + slot - (slot > z);
                 gs[r] = (k < 4 * 4096 && slot != z && pre < pcount) ? pre0 + pre : -1;
                 hv[r] = gs[r] >= 0 ? __ldcg(hin + gs[r]) : 0u;
-                bw[r] = gs[r] >= 0 ? __ldcg(a.bits + (gs[r] >> 5)) : 0u;
+                bw[r] = gs[r] >= 0 ? __ldcg(bits + (gs[r] >> 5)) : 0u;
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) {

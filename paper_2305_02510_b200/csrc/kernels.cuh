@@ -163,6 +163,13 @@ struct SparseArgs {
     // bumps d_step, so it cannot read d_step safely)
     const int32_t* step_in;
     uint16_t* hist16;          // [2][n] or null
+    // folded history over the p2p exchange: wait until every rank published
+    // step t (flags[q] > t), then read the spike bits from exchange buffer t & 1
+    const int32_t* flags;      // or null
+    int32_t world;
+    int32_t* error;            // set to 1 when the wait times out
+    const uint32_t* xbits;
+    int32_t xstride;
 };
 
 // Stage plan of k_sparse_tma (built on the host at setup from the CSC offsets):

@@ -1221,3 +1221,42 @@ def test_count16_partitions_fold_history(mode):
     assert close_rel(mem, o["membrane"])
     for e in engines:
         e.close()
+
+
+@pytest.mark.parametrize("skew", [False, True], ids=["lockstep", "rank0_ahead"])
+@pytest.mark.parametrize("world", [2, 4])
+def test_count16_p2p_fold_waits_in_the_sweep(world, skew):
+    """The p2p exchange with the folded history: two kernels per step --
+    k_neuron stores its words into every rank's exchange buffer t & 1 and
+    releases its flag; the k_sparse_count16 sweep waits for every flag and
+    stages from that buffer (no k_hist).  Emulated partitions driven so that
+    no kernel waits on one that has not run (lockstep and rank 0 a step
+    ahead), against the oracle."""
+    from oracle import bridge as B
+    from paper_2305_02510_b200.engine import MatEngine, p2p_connect_local
+    arrays, stim, steps = _count16_problem()
+    o = B.run_oracle(arrays, steps, stim)
+    engines = []
+    for r in range(world):
+        e = MatEngine(storage=2, rank=r, world=world, persistent=False)
+        e.add_neurons(arrays["threshold"], arrays["leak"], arrays["reset"], arrays["refractory"], arrays["axonal"])
+        e.add_synapses(arrays["pre"], arrays["post"], arrays["weight"], arrays["delay"], None)
+        e.setup()
+        e.add_stimulus(*stim)
+        engines.append(e)
+    p2p_connect_local(engines)
+    for r, what, _ in _p2p_schedule(world, steps, skew):
+        if what == "local":
+            engines[r].step_local()
+        else:
+            engines[r].step_finish()
+            engines[r].synchronize()
+    assert all(e.stats()["sweep_kernel"] == 13 for e in engines)
+    assert all(e.stats()["kernel_launches"] == 2 * steps for e in engines)   # k_neuron + sweep
+    rasters = [e.raster() for e in engines]
+    s = np.concatenate([x[0] for x in rasters])
+    q = np.concatenate([x[1] for x in rasters])
+    order = np.lexsort((q, s))
+    assert np.array_equal(s[order], o["steps"]) and np.array_equal(q[order], o["neurons"])
+    for e in engines:
+        e.close()
