@@ -155,9 +155,12 @@ typedef enum sn_sweep_kernel {
                                      32-post column groups, one grid barrier per step */
     SN_SWEEP_SPARSE_COUNT16 = 13, /* k_sparse_count16: one-weight lists as 16-bit entries in
                                      4095-pre segments (2 B/synapse), delays <= 16 */
-    SN_SWEEP_CLUSTER = 14         /* k_cluster_count: whole step loop in ONE thread-block cluster,
+    SN_SWEEP_CLUSTER = 14,        /* k_cluster_count: whole step loop in ONE thread-block cluster,
                                      history exchanged through distributed shared memory
                                      (small static one-weight nets, delays <= 31) */
+    SN_SWEEP_SPARSE_COUNT8 = 15   /* k_sparse_count8: the 16-bit segmented lists of
+                                     k_sparse_count16 over a byte-per-(pre, delay) shared
+                                     image (3 x 4095-pre segments), default for them */
 } sn_sweep_kernel;
 
 /* ---- lifecycle ---------------------------------------------------------- */

@@ -400,6 +400,20 @@ def ref_scenario_abm_raster(n, p, seed, steps, delay_max=1, by_index=False, dela
     return out
 
 
+def ref_scenario_stdp_raster(n, p, seed, steps) -> dict:
+    """Raster of the reference's mat_run on the all-plastic STDP scenario
+    (ref_shim.cpp ref_scenario_stdp_raster); also synapses, seconds, RSS."""
+    lib = ref_lib()
+    info = np.zeros(3)
+    r = Result()
+    dp = C.POINTER(C.c_double)
+    lib.ref_scenario_stdp_raster.argtypes = [C.c_int, C.c_double, C.c_uint64, C.c_int, dp, C.POINTER(Result)]
+    lib.ref_scenario_stdp_raster(n, p, seed, steps, info.ctypes.data_as(dp), C.byref(r))
+    out = _collect(lib, r, steps, with_state=False)
+    out.update({"synapses": int(info[0]), "seconds": float(info[1]), "peak_rss_gb": float(info[2])})
+    return out
+
+
 def ref_bench_scenario(n, p, seed, steps, stdp_on, storage=0) -> dict:
     """Reference CPU path timed like bench.cpp:24-50 (mat_init outside the clock)."""
     lib = ref_lib()

@@ -313,6 +313,28 @@ int ref_scenario_abm_raster(int n, double p, uint64_t seed, int steps, int delay
     });
 }
 
+// Scale golden of the STDP scenario: build_scenario(n, p, seed) with every
+// synapse plastic and StdpConfig::defaults(), mat_run for `steps` steps with
+// the reference's Auto storage (CSR above 12,000 neurons).
+int ref_scenario_stdp_raster(int n, double p, uint64_t seed, int steps, double* info, orc_result* out) {
+    return guarded(out, [&] {
+        const auto s0 = std::chrono::steady_clock::now();
+        BenchScenario sc;
+        sc.neuron_count = n;
+        sc.connection_probability = p;
+        sc.steps = steps;
+        sc.seed = seed;
+        ScenarioBundle b = build_scenario(sc);
+        for (SynapseDef& s : b.net.synapses) s.stdp_enabled = true;
+        b.cfg.stdp = StdpConfig::defaults();
+        info[0] = static_cast<double>(b.net.synapses.size());
+        const RunResult r = mat_run(b.net, b.cfg, b.stim);
+        info[1] = std::chrono::duration<double>(std::chrono::steady_clock::now() - s0).count();
+        info[2] = peak_rss_gb();
+        put_raster(r.raster, out);
+    });
+}
+
 // abm_run with heterogeneous behaviours: fire_p[i] < 1 runs neuron i under a
 // StochasticLifBehavior(fire_p[i]) registered through the reference's own
 // registry (the register_stochastic_lif binding, bindings.cpp:180-186);

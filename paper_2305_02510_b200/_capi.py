@@ -73,7 +73,7 @@ class Stats(C.Structure):
                     4: "k_persistent_dense", 5: "k_sparse_pull", 6: "k_sparse_pull<dict>",
                     7: "k_sparse_stream", 8: "k_sparse_exact", 9: "k_tiny",
                     10: "k_sparse_tma", 11: "k_sparse_count", 12: "k_persistent_cols",
-                    13: "k_sparse_count16", 14: "k_cluster_count"}
+                    13: "k_sparse_count16", 14: "k_cluster_count", 15: "k_sparse_count8"}
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

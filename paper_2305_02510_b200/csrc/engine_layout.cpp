@@ -2,6 +2,7 @@
 // with delays / plastic masks / row kinds, blocked CSC (with the weight
 // dictionary and bank-aware list order), on-device generated nets, and the
 // launch plans of every kernel family.
+#include <cstdio>
 #include "engine.hpp"
 #include "engine_util.hpp"
 #include "nccl_dl.hpp"
@@ -499,11 +500,12 @@ void Engine::plan_launches() {
         // A/B knob SNB_SPARSE_CTAS_PER_SM (tools/ab_env.sh)
         const bool c16_plan = dict_.size() == 2 && !stdp_on_ && !exact_ && hbits_ == 16 &&
                               pb_ == c16_block_pres() && c16_allowed();
-        int per_sm = c16_plan ? (nl_ >= 131072 ? 12 : 4) : 8;
-        if (const char* cp = std::getenv("SNB_SPARSE_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(cp));
+        const bool c8_plan = c16_plan && c16_bytes();  // byte image: one 1024-thread CTA per SM
+        int per_sm = c8_plan ? 1 : c16_plan ? (nl_ >= 131072 ? 12 : 4) : 8;
         c16_threads_ = c16_plan ? c16_threads(nl_) : 256;
         const int warps = c16_threads_ / 32;  // per CTA
-        if (c16_plan) per_sm = std::max(1, per_sm * 8 / warps);  // same warps per SM for bigger CTAs
+        if (c16_plan && !c8_plan) per_sm = std::max(1, per_sm * 8 / warps);  // same warps per SM for bigger CTAs
+        if (const char* cp = std::getenv("SNB_SPARSE_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(cp));
         const int target = sms * per_sm;
         int gx = std::max(1, target / std::max(1, nblocks_));
         const int unit = sub_ == 0 ? 8 : warps * (32 / sub_);
@@ -583,7 +585,13 @@ bool Engine::build_c16() {
     cuda_check(cudaStreamSynchronize(stream_), "c16 counts");
     std::vector<uint32_t> desc(static_cast<size_t>(lists) * 2);
     uint64_t chunks = 0;
+    // byte image (k_sparse_count8): the 32 / sub posts of a warp share one
+    // row-major chunk stream; every descriptor carries the group's first chunk
+    const bool grouped = c16_bytes();
+    const int P = 32 / sub_;
+    uint64_t group0 = 0;
     for (int64_t L = 0; L < lists; ++L) {
+        if (grouped && (L % nl_) % P == 0) group0 = chunks;
         const uint32_t x = cnt[2 * L], y = cnt[2 * L + 1];
         const uint32_t n[4] = {x & 0xffffu, x >> 16, y & 0xffffu, y >> 16};
         uint32_t e[4], acc = 0;
@@ -592,7 +600,7 @@ bool Engine::build_c16() {
             e[s] = acc;
         }
         if (acc > 255) return false;
-        desc[2 * L] = static_cast<uint32_t>(chunks);
+        desc[2 * L] = static_cast<uint32_t>(grouped ? group0 : chunks);
         desc[2 * L + 1] = e[0] | (e[1] << 8) | (e[2] << 16) | (e[3] << 24);
         chunks += acc;
     }
@@ -612,6 +620,17 @@ bool Engine::build_c16() {
         return false;
     }
     cuda_check(cudaStreamSynchronize(stream_), "c16 fill");
+    if (const char* dump = std::getenv("SNB_C16_DUMP")) {  // debugging aid: descriptors + entries
+        std::vector<uint16_t> ent(static_cast<size_t>(chunks) * 8);
+        d2h(ent.data(), d_c16ent_.p, ent.size() * 2, "c16 dump");
+        if (FILE* f = std::fopen(dump, "wb")) {
+            const int64_t hdr[4] = {lists, static_cast<int64_t>(chunks), sub_, nl_};
+            std::fwrite(hdr, 8, 4, f);
+            std::fwrite(desc.data(), 4, desc.size(), f);
+            std::fwrite(ent.data(), 2, ent.size(), f);
+            std::fclose(f);
+        }
+    }
     c16_ = true;
     // bytes the sweep moves in this format: 2 B per stored entry (padding included),
     // the 8-byte descriptor and the 8-byte partial of every (block, post) list

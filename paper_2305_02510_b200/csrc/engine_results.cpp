@@ -243,7 +243,7 @@ void Engine::get_stats(sn_stats* out) {
         } else {
             stats_.sweep_kernel = exact_ ? SN_SWEEP_SPARSE_EXACT
                                   : sparse_tma_ ? SN_SWEEP_SPARSE_TMA
-                                  : c16_ ? SN_SWEEP_SPARSE_COUNT16
+                                  : c16_ ? (c16_bytes() ? SN_SWEEP_SPARSE_COUNT8 : SN_SWEEP_SPARSE_COUNT16)
                                   : (dict_.size() == 2 && !stdp_on_ && sub_ != 0 && hbits_ != 64) ? SN_SWEEP_SPARSE_COUNT
                                   : sub_ == 0 ? SN_SWEEP_SPARSE_STREAM
                                   : !dict_.empty() ? SN_SWEEP_SPARSE_DICT

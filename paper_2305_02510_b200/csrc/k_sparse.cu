@@ -3,6 +3,7 @@
 #include "kernels_common.cuh"
 
 #include <cstdlib>
+#include <string>
 
 namespace snb {
 
@@ -448,7 +449,12 @@ constexpr int kC16Pres = 4 * kC16SegPres;
 // j + (j >= zero slot).
 __host__ __device__ constexpr int c16_zero_slot(int s) { return 4095 - 16 * s; }
 
-__device__ __forceinline__ void c16_stage(const SparseArgs& a, int pre0, int pcount, uint16_t* sh) {
+// Stage one pre block's history: put(k, h) for every slot k of NSEG segments
+// (h = the pre's 16-bit delay history, 0 for the zero slots and past the end).
+template <int NSEG, typename Put>
+__device__ __forceinline__ void c16_stage_slots(const SparseArgs& a, int pre0, int pcount, Put&& put) {
+    constexpr int K = NSEG * 4096;
+    constexpr int R = 8;  // slots per thread per pass, all loads issued before any use
     if (a.hist16) {
         // folded history: h = (history after step t - 1) << 1 | s[t]; the first CTA
         // of the pre block commits it to the other parity buffer for step t + 1
@@ -472,9 +478,7 @@ __device__ __forceinline__ void c16_stage(const SparseArgs& a, int pre0, int pco
         const uint16_t* hin = a.hist16 + static_cast<int64_t>(t & 1) * a.n;
         uint16_t* hout = a.hist16 + static_cast<int64_t>((t + 1) & 1) * a.n;
         const bool commit = blockIdx.x == 0;
-        // 8 slots per thread per pass, all loads issued before any use
-        constexpr int R = 8;
-        for (int k0 = threadIdx.x; k0 < 4 * 4096; k0 += R * blockDim.x) {
+        for (int k0 = threadIdx.x; k0 < K; k0 += R * blockDim.x) {
             uint32_t hv[R], bw[R];
             int gs[R];
 #pragma unroll
@@ -482,7 +486,7 @@ __device__ __forceinline__ void c16_stage(const SparseArgs& a, int pre0, int pco
                 const int k = k0 + r * blockDim.x;
                 const int s = k >> 12, slot = k & 4095, z = c16_zero_slot(s);
                 const int pre = s * kC16SegPres + slot - (slot > z);
-                gs[r] = (k < 4 * 4096 && slot != z && pre < pcount) ? pre0 + pre : -1;
+                gs[r] = (k < K && slot != z && pre < pcount) ? pre0 + pre : -1;
                 hv[r] = gs[r] >= 0 ? __ldcg(hin + gs[r]) : 0u;
                 bw[r] = gs[r] >= 0 ? __ldcg(bits + (gs[r] >> 5)) : 0u;
             }
@@ -490,26 +494,29 @@ __device__ __forceinline__ void c16_stage(const SparseArgs& a, int pre0, int pco
             for (int r = 0; r < R; ++r) {
                 const int k = k0 + r * blockDim.x;
                 const uint16_t h = gs[r] >= 0 ? static_cast<uint16_t>((hv[r] << 1) | ((bw[r] >> (gs[r] & 31)) & 1u)) : 0;
-                if (k < 4 * 4096) sh[k] = h;
+                if (k < K) put(k, h);
                 if (commit && gs[r] >= 0) hout[gs[r]] = h;
             }
         }
         return;
     }
-    constexpr int R = 8;  // slots per thread per pass, loads first (memory-level parallelism)
-    for (int k0 = threadIdx.x; k0 < 4 * 4096; k0 += R * blockDim.x) {
+    for (int k0 = threadIdx.x; k0 < K; k0 += R * blockDim.x) {
         uint32_t hv[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int k = k0 + r * blockDim.x;
             const int s = k >> 12, slot = k & 4095, z = c16_zero_slot(s);
             const int pre = s * kC16SegPres + slot - (slot > z);
-            hv[r] = (k < 4 * 4096 && slot != z && pre < pcount) ? __ldcg(a.hist_lo + pre0 + pre) : 0u;
+            hv[r] = (k < K && slot != z && pre < pcount) ? __ldcg(a.hist_lo + pre0 + pre) : 0u;
         }
 #pragma unroll
         for (int r = 0; r < R; ++r)
-            if (k0 + r * blockDim.x < 4 * 4096) sh[k0 + r * blockDim.x] = static_cast<uint16_t>(hv[r]);
+            if (k0 + r * blockDim.x < K) put(k0 + r * blockDim.x, static_cast<uint16_t>(hv[r]));
     }
+}
+
+__device__ __forceinline__ void c16_stage(const SparseArgs& a, int pre0, int pcount, uint16_t* sh) {
+    c16_stage_slots<4>(a, pre0, pcount, [&](int k, uint16_t h) { sh[k] = h; });
 }
 
 #ifndef SNB_C16_MINB
@@ -642,6 +649,101 @@ __global__ void __launch_bounds__(NT, NT == kThreads ? SNB_C16_MINB : 1024 / NT)
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *a.d_step += 1;
 }
 
+// Byte-image variant (k_sparse_count8): the same segmented lists over 3
+// segments (a pre block of kC8Pres = 3 x 4095 pres), but the staged image
+// holds one BYTE per (slot, delay) -- byte 16 slot + d - 1 of a segment's 64 KB
+// is bit d - 1 of the slot's history -- and an entry is that byte offset:
+//   entry = slot << 4 | (d - 1)
+// so the test is one LDS.U8 whose value is added as is: per 32-bit word of two
+// entries one mask, one shift-add (LEA.HI) and one 3-input add instead of the
+// two address extractions, two funnel shifts and two shift-adds of the pair
+// encoding.  192 KB of image: one CTA of 1024 threads per SM.
+constexpr int kC8Segs = 3;
+constexpr int kC8Pres = kC8Segs * kC16SegPres;
+constexpr int kC8ImageBytes = kC8Segs * 65536;
+
+// 4 history bits -> 4 bytes of 0/1 (bit i of n to byte i)
+__device__ __forceinline__ uint32_t c8_spread4(uint32_t n) { return (n * 0x00204081u) & 0x01010101u; }
+
+template <int SUB, int UL>
+__device__ __forceinline__ uint32_t c8_count_batch(const uint4 (&m4)[UL], int c0, int C, int E1, int E2,
+                                                   const uint8_t* img) {
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int u = 0; u < UL; ++u) {
+        const int c = c0 + u * SUB;
+        if (c < C) {
+            SNB_DCHECK(E1 <= E2 && E2 <= C && C <= 255);
+            const uint8_t* seg = img + (((c >= E1) + (c >= E2)) << 16);
+            const uint32_t ws[4] = {m4[u].x, m4[u].y, m4[u].z, m4[u].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cnt += seg[ws[k] & 0xffffu] + seg[ws[k] >> 16];
+        }
+    }
+    return cnt;
+}
+
+template <typename WT, int SUB, int NT>
+__global__ void __launch_bounds__(NT, 1) k_sparse_count8(SparseArgs a, const uint2* desc, const uint4* ent) {
+    extern __shared__ __align__(16) uint8_t c8img[];
+    const int b = blockIdx.y;
+    const int pre0 = b * kC8Pres;
+    const int pcount = min(kC8Pres, a.n - pre0);
+    const int tid = threadIdx.x;
+    c16_stage_slots<kC8Segs>(a, pre0, pcount, [&](int k, uint16_t h) {
+        const uint32_t x = h;
+        *reinterpret_cast<uint4*>(c8img + 16 * k) =
+            make_uint4(c8_spread4(x & 15u), c8_spread4((x >> 4) & 15u), c8_spread4((x >> 8) & 15u), c8_spread4(x >> 12));
+    });
+    __syncthreads();
+    const WT w0 = static_cast<const WT*>(a.wdict)[0];
+    const int p0 = blockIdx.x * a.posts_per_cta;
+    const int p1 = min(a.nl, p0 + a.posts_per_cta);
+    constexpr int PER_WARP = 32 / SUB;
+    constexpr int UL = SNB_C16_UL_OF(SUB);
+    const int warp = tid >> 5, lane = tid & 31;
+    const int sg = lane / SUB, sl = lane % SUB;
+    const int stride = (NT / 32) * PER_WARP;
+    const uint2* db = desc + static_cast<int64_t>(b) * a.nl;
+    const uint32_t lt = (1u << lane) - 1u;  // lanes below this one
+    int p = p0 + warp * PER_WARP + sg;
+    uint2 d = make_uint2(0u, 0u);
+    if (p < p1) d = __ldg(db + p);
+    for (int pbase = p0 + warp * PER_WARP; pbase < p1; pbase += stride) {  // warp-uniform trip count
+        const bool valid = p < p1;
+        const int pn = p + stride;
+        uint2 dn = make_uint2(0u, 0u);
+        if (pn < p1) dn = __ldg(db + pn);
+        // the warp's P posts share one chunk stream, row-major: row r holds chunks
+        // SUB r .. SUB r + SUB - 1 of every post that has them, in post order, so a
+        // row's loads are one contiguous run of up to 512 bytes
+        const int C = valid ? static_cast<int>(d.y >> 24) : 0;
+        const int E1 = static_cast<int>(d.y & 255u), E2 = static_cast<int>((d.y >> 8) & 255u);
+        const int rows = (static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(C))) + SUB - 1) / SUB;
+        uint32_t pos = __shfl_sync(0xffffffffu, d.x, 0);  // the group's first chunk
+        uint32_t cnt = 0;
+        for (int r0 = 0; r0 < rows; r0 += UL) {
+            const int c0 = r0 * SUB + sl;
+            uint4 m4[UL];
+#pragma unroll
+            for (int u = 0; u < UL; ++u) {
+                const bool act = c0 + u * SUB < C;
+                const uint32_t A = __ballot_sync(0xffffffffu, act);
+                if (act) m4[u] = __ldcs(ent + pos + __popc(A & lt));
+                pos += __popc(A);
+            }
+            cnt += c8_count_batch<SUB, UL>(m4, c0, C, E1, E2, c8img);
+        }
+#pragma unroll
+        for (int o = SUB / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (valid && sl == 0)
+            a.partial[static_cast<int64_t>(b) * a.nl + p] = static_cast<double>(static_cast<WT>(static_cast<int>(cnt)) * w0);
+        p = pn;
+        d = dn;
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *a.d_step += 1;
+}
+
 // Setup: entries per segment of every 32-bit one-weight list (padding, pre slot
 // pb, skipped) -> cnt[list] = n0 | n1 << 16 (x) and n2 | n3 << 16 (y).
 __global__ void k_c16_count(const uint32_t* meta, const int64_t* off, int64_t lists, int pb, uint2* cnt) {
@@ -661,15 +763,37 @@ __global__ void k_c16_count(const uint32_t* meta, const int64_t* off, int64_t li
 // chunk row g/8, entry g%8); a lane takes, from its chunk's segment, an entry
 // in the bank with the lowest load in this LDS so far (ties: most entries left
 // in the group, then in the list), padding (the zero slot) once the segment is empty.
-template <int SUB>
-__global__ void k_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* off, const uint2* desc, int nblocks,
-                           int nl, int pb, uint16_t* out) {
+// host/device helpers of the fill (the fill also runs on the host in tools/c16_fill_check)
+__host__ __device__ __forceinline__ int c16_popc(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return __popc(x);
+#else
+    return __builtin_popcount(x);
+#endif
+}
+__host__ __device__ __forceinline__ int c16_ffs(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return __ffs(static_cast<int>(x));
+#else
+    return __builtin_ffs(static_cast<int>(x));
+#endif
+}
+__host__ __device__ __forceinline__ int c16_min(int a, int b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int c16_max(int a, int b) { return a > b ? a : b; }
+
+// BYTES: the byte-image encoding of k_sparse_count8 (slot << 4 | d - 1, bank
+// (4 slot + (d - 1) / 4) mod 32) instead of the pair encoding.
+__host__ __device__ __forceinline__ int c16_bank(bool bytes, int slot, int dm1) {
+    return bytes ? ((slot << 2) + (dm1 >> 2)) & 31 : (slot >> 1) & 31;
+}
+
+template <int SUB, bool BYTES>
+__host__ __device__ void c16_fill_group(int64_t G, const uint32_t* meta, uint32_t* tmp, const int64_t* off,
+                                        const uint2* desc, int nl, int pb, uint16_t* out) {
     constexpr int P = 32 / SUB;
     const int groups = (nl + P - 1) / P;
-    const int64_t G = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (G >= static_cast<int64_t>(groups) * nblocks) return;
     const int b = static_cast<int>(G / groups), k = static_cast<int>(G % groups);
-    const int np = min(P, nl - P * k);
+    const int np = c16_min(P, nl - P * k);
     const int64_t L0 = static_cast<int64_t>(b) * nl + P * k;
     uint16_t cnt[P][4][32], cur[P][4][32];
     int tot[32], C[P], E[P][3];
@@ -686,14 +810,14 @@ __global__ void k_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* o
         E[i][0] = static_cast<int>(d.y & 255u);
         E[i][1] = static_cast<int>((d.y >> 8) & 255u);
         E[i][2] = static_cast<int>((d.y >> 16) & 255u);
-        gmax = max(gmax, 8 * ((C[i] + SUB - 1) / SUB));
+        gmax = c16_max(gmax, 8 * ((C[i] + SUB - 1) / SUB));
         const int64_t o0 = off[L0 + i], o1 = off[L0 + i + 1];
         for (int64_t q = o0; q < o1; ++q) {
             const int pl = static_cast<int>(meta[q] & 0xffffu);
             if (pl == pb) continue;
             const int s = pl / kC16SegPres;
             const int low = pl - s * kC16SegPres;
-            cnt[i][s][((low + (low >= c16_zero_slot(s))) >> 1) & 31] += 1;
+            cnt[i][s][c16_bank(BYTES, low + (low >= c16_zero_slot(s)), static_cast<int>((meta[q] >> 16) & 15u))] += 1;
         }
         int acc = 0;
         for (int s = 0; s < 4; ++s)
@@ -708,8 +832,10 @@ __global__ void k_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* o
             if (pl == pb) continue;
             const int s = pl / kC16SegPres;
             const int slot = pl - s * kC16SegPres + (pl - s * kC16SegPres >= c16_zero_slot(s));
-            const uint32_t j = static_cast<uint32_t>(slot & 1) * 16u + ((m >> 16) & 15u);  // bit of the pair
-            tmp[o0 + cur[i][s][(slot >> 1) & 31]++] = static_cast<uint32_t>(slot >> 1) << 5 | ((j + 1u) & 31u);
+            const uint32_t dm1 = (m >> 16) & 15u;
+            const uint32_t j = static_cast<uint32_t>(slot & 1) * 16u + dm1;  // bit of the pair
+            tmp[o0 + cur[i][s][c16_bank(BYTES, slot, static_cast<int>(dm1))]++] =
+                BYTES ? static_cast<uint32_t>(slot) << 4 | dm1 : static_cast<uint32_t>(slot >> 1) << 5 | ((j + 1u) & 31u);
         }
         for (int s = 0; s < 4; ++s)
             for (int j = 0; j < 32; ++j) cur[i][s][j] = static_cast<uint16_t>(cur[i][s][j] - cnt[i][s][j]);
@@ -718,39 +844,141 @@ __global__ void k_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* o
         int load[32];
         for (int j = 0; j < 32; ++j) load[j] = 0;
         const int row = g >> 3, e = g & 7;
+        // BYTES: chunks of row `row` start after the group's earlier rows, post i's
+        // after the row's chunks of posts < i (k_sparse_count8's stream order)
+        int64_t rbase = 0;
+        int before[P];
+        if (BYTES) {
+            const int64_t g0 = desc[L0].x;
+            int64_t prior = 0;
+            for (int rr = 0; rr < row; ++rr)
+                for (int i = 0; i < np; ++i) prior += c16_min(SUB, c16_max(0, C[i] - SUB * rr));
+            int acc = 0;
+            for (int i = 0; i < P; ++i) {
+                before[i] = acc;
+                if (i < np) acc += c16_min(SUB, c16_max(0, C[i] - SUB * row));
+            }
+            rbase = g0 + prior;
+        }
+        // BYTES: the LDS's lanes get pairwise different banks where their pools
+        // allow it -- a maximum bipartite matching of lanes to banks (augmenting
+        // paths, most constrained lanes first, abundant banks tried first), the
+        // banks of padding lanes excluded; unmatched lanes fall back to the
+        // least-loaded bank below
+        int asg[P][SUB];
+        if (BYTES) {
+            int li[32], ls[32], order[32], matchB[32];
+            uint32_t opt[32], fixed = 0;
+            int nlanes = 0;
+            for (int i = 0; i < P; ++i)
+                for (int sl = 0; sl < SUB; ++sl) {
+                    asg[i][sl] = -1;
+                    const int c = row * SUB + sl;
+                    if (i >= np || c >= C[i]) continue;
+                    const int s = (c >= E[i][0]) + (c >= E[i][1]) + (c >= E[i][2]);
+                    uint32_t m = 0;
+                    for (int j = 0; j < 32; ++j)
+                        if (cnt[i][s][j]) m |= 1u << j;
+                    if (!m) {
+                        fixed |= 1u << c16_bank(true, c16_zero_slot(s), 4 * s);
+                        continue;
+                    }
+                    li[nlanes] = i;
+                    ls[nlanes] = sl;
+                    opt[nlanes] = m;
+                    order[nlanes] = nlanes;
+                    ++nlanes;
+                }
+            for (int l = 0; l < nlanes; ++l) {
+                if (opt[l] & ~fixed) opt[l] &= ~fixed;
+                for (int k = l; k > 0 && c16_popc(opt[order[k]]) < c16_popc(opt[order[k - 1]]); --k) {
+                    const int t = order[k];
+                    order[k] = order[k - 1];
+                    order[k - 1] = t;
+                }
+            }
+            for (int j = 0; j < 32; ++j) matchB[j] = -1;
+            for (int q = 0; q < nlanes; ++q) {
+                int stk[33], via[33], sp = 1;
+                uint32_t rem[33], vis = 0;
+                stk[0] = order[q];
+                rem[0] = opt[order[q]];
+                while (sp > 0) {
+                    const uint32_t m = rem[sp - 1] & ~vis;
+                    if (!m) {
+                        --sp;
+                        continue;
+                    }
+                    int b = -1;
+                    for (uint32_t mm = m; mm; mm &= mm - 1) {
+                        const int j = c16_ffs(mm) - 1;
+                        if (b < 0 || tot[j] > tot[b]) b = j;
+                    }
+                    rem[sp - 1] = m & ~(1u << b);
+                    vis |= 1u << b;
+                    via[sp - 1] = b;
+                    if (matchB[b] < 0) {
+                        for (int k = 0; k < sp; ++k) matchB[via[k]] = stk[k];
+                        break;
+                    }
+                    stk[sp] = matchB[b];
+                    rem[sp] = opt[matchB[b]];
+                    ++sp;
+                }
+            }
+            for (int j = 0; j < 32; ++j) {
+                if (matchB[j] >= 0) asg[li[matchB[j]]][ls[matchB[j]]] = j;
+                load[j] += (matchB[j] >= 0) + static_cast<int>((fixed >> j) & 1u);
+            }
+        }
+        // matched lanes take their entries first (pass 0), then the rest
+        for (int pass = BYTES ? 0 : 1; pass < 2; ++pass)
         for (int r = 0; r < P; ++r) {
             const int i = (g + r) % P;
             if (i >= np) continue;
-            const int64_t base = static_cast<int64_t>(desc[L0 + i].x) * 8;
             const int64_t o0 = off[L0 + i];
             for (int sl = 0; sl < SUB; ++sl) {
                 const int c = row * SUB + sl;
                 if (c >= C[i]) continue;
+                if (BYTES && (pass == 0) != (asg[i][sl] >= 0)) continue;
+                const int64_t base = BYTES ? (rbase + before[i] + sl - c) * 8 : static_cast<int64_t>(desc[L0 + i].x) * 8;
                 const int s = (c >= E[i][0]) + (c >= E[i][1]) + (c >= E[i][2]);
-                int best = -1;
-                for (int j = 0; j < 32; ++j) {
+                int best = BYTES ? asg[i][sl] : -1;
+                const bool matched = best >= 0;
+                for (int j = 0; j < 32 && !matched; ++j) {
                     if (cnt[i][s][j] == 0) continue;
                     if (best < 0 || load[j] < load[best] ||
                         (load[j] == load[best] && (tot[j] > tot[best] ||
                                                    (tot[j] == tot[best] && cnt[i][s][j] > cnt[i][s][best]))))
                         best = j;
                 }
-                // padding: the segment's zero slot (odd: upper half of its pair, bit 16)
+                // padding: the segment's zero slot (pairs: upper half of its pair, bit 16;
+                // bytes: byte 4 s, bank 28 + s)
                 const int z = c16_zero_slot(s);
-                uint16_t v = static_cast<uint16_t>((z >> 1) << 5 | 17);
+                uint16_t v = BYTES ? static_cast<uint16_t>(z << 4 | (4 * s)) : static_cast<uint16_t>((z >> 1) << 5 | 17);
                 if (best >= 0) {
                     v = static_cast<uint16_t>(tmp[o0 + cur[i][s][best]]);
                     cur[i][s][best] += 1;
                     cnt[i][s][best] -= 1;
                     tot[best] -= 1;
-                    load[best] += 1;
-                } else {
-                    load[(z >> 1) & 31] += 1;
+                    if (!(BYTES && pass == 0)) load[best] += 1;
+                } else if (!BYTES) {
+                    load[c16_bank(BYTES, z, 4 * s)] += 1;
                 }
                 out[base + static_cast<int64_t>(c) * 8 + e] = v;
             }
         }
     }
+}
+
+template <int SUB, bool BYTES>
+__global__ void k_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* off, const uint2* desc, int nblocks,
+                           int nl, int pb, uint16_t* out) {
+    constexpr int P = 32 / SUB;
+    const int groups = (nl + P - 1) / P;
+    const int64_t G = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (G >= static_cast<int64_t>(groups) * nblocks) return;
+    c16_fill_group<SUB, BYTES>(G, meta, tmp, off, desc, nl, pb, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -1212,7 +1440,12 @@ void launch_sparse_bank_order(const uint32_t* in, uint32_t* out, const int64_t* 
     check(cudaGetLastError(), "k_sparse_bank_order");
 }
 
-int c16_block_pres() { return kC16Pres; }
+bool c16_bytes() {
+    const char* e = std::getenv("SNB_C16_IMAGE");  // A/B knob: "bits" = the pair-encoded 16-bit image
+    return !(e && std::string(e) == "bits");
+}
+
+int c16_block_pres() { return c16_bytes() ? kC8Pres : kC16Pres; }
 
 void launch_c16_count(const uint32_t* meta, const int64_t* off, int64_t lists, int pb, uint2* cnt, cudaStream_t s) {
     if (lists <= 0) return;
@@ -1226,11 +1459,15 @@ bool launch_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* off, co
     const int64_t groups = static_cast<int64_t>(nblocks) * ((nl + P - 1) / P);
     if (groups <= 0) return true;
     const unsigned grid = static_cast<unsigned>((groups + 63) / 64);
+    const bool bytes = c16_bytes();
+    auto go = [&](auto kb, auto kp) {
+        (bytes ? kb : kp)<<<grid, 64, 0, s>>>(meta, tmp, off, desc, nblocks, nl, pb, out);
+    };
     switch (sub) {
-        case 2: k_c16_fill<2><<<grid, 64, 0, s>>>(meta, tmp, off, desc, nblocks, nl, pb, out); break;
-        case 4: k_c16_fill<4><<<grid, 64, 0, s>>>(meta, tmp, off, desc, nblocks, nl, pb, out); break;
-        case 8: k_c16_fill<8><<<grid, 64, 0, s>>>(meta, tmp, off, desc, nblocks, nl, pb, out); break;
-        case 16: k_c16_fill<16><<<grid, 64, 0, s>>>(meta, tmp, off, desc, nblocks, nl, pb, out); break;
+        case 2: go(k_c16_fill<2, true>, k_c16_fill<2, false>); break;
+        case 4: go(k_c16_fill<4, true>, k_c16_fill<4, false>); break;
+        case 8: go(k_c16_fill<8, true>, k_c16_fill<8, false>); break;
+        case 16: go(k_c16_fill<16, true>, k_c16_fill<16, false>); break;
         default: return false;
     }
     check(cudaGetLastError(), "k_c16_fill");
@@ -1254,7 +1491,28 @@ static void c16_go(const SparseArgs& a, const uint2* desc, const uint4* e, int s
     }
 }
 
+template <typename WT, int NT>
+static void c8_go(const SparseArgs& a, const uint2* desc, const uint4* e, int sub, dim3 grid, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        for (auto k : {k_sparse_count8<WT, 2, NT>, k_sparse_count8<WT, 4, NT>, k_sparse_count8<WT, 8, NT>,
+                       k_sparse_count8<WT, 16, NT>})
+            check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kC8ImageBytes), "c8 smem");
+        attr = true;
+    }
+    switch (sub) {
+        case 2: k_sparse_count8<WT, 2, NT><<<grid, NT, kC8ImageBytes, s>>>(a, desc, e); break;
+        case 4: k_sparse_count8<WT, 4, NT><<<grid, NT, kC8ImageBytes, s>>>(a, desc, e); break;
+        case 16: k_sparse_count8<WT, 16, NT><<<grid, NT, kC8ImageBytes, s>>>(a, desc, e); break;
+        default: k_sparse_count8<WT, 8, NT><<<grid, NT, kC8ImageBytes, s>>>(a, desc, e); break;
+    }
+}
+
 int c16_threads(int nl) {
+    if (c16_bytes()) {  // one CTA per SM (192 KB image): 1024 threads, or 512 (A/B knob)
+        const char* t = std::getenv("SNB_C16_THREADS");
+        return t && std::atoi(t) == 512 ? 512 : 1024;
+    }
     // full-size lists: 256-thread CTAs (cfg4 0.4127 ms; 512: 0.4165, 1024: 0.419); post
     // partitions (an eighth of cfg4's posts per block): 1024 (65.8 us vs 70.4 at 512,
     // 79.1 at 256) -- a CTA stages its pre block once for 4x the posts
@@ -1267,6 +1525,17 @@ void launch_sparse_count16(const SparseArgs& a, const uint2* desc, const void* e
                            int nt, cudaStream_t s) {
     dim3 grid(gx, a.nblocks);
     const uint4* e = static_cast<const uint4*>(ent);
+    if (c16_bytes()) {
+        if (f64) {
+            if (nt == 512) c8_go<double, 512>(a, desc, e, sub, grid, s);
+            else c8_go<double, 1024>(a, desc, e, sub, grid, s);
+        } else {
+            if (nt == 512) c8_go<float, 512>(a, desc, e, sub, grid, s);
+            else c8_go<float, 1024>(a, desc, e, sub, grid, s);
+        }
+        check(cudaGetLastError(), "k_sparse_count8");
+        return;
+    }
     if (f64) {
         if (nt == 1024) c16_go<double, 1024>(a, desc, e, sub, grid, s);
         else if (nt == 512) c16_go<double, 512>(a, desc, e, sub, grid, s);

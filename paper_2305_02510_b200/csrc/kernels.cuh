@@ -226,6 +226,7 @@ void launch_sparse_bank_order(const uint32_t* in, uint32_t* out, const int64_t* 
 // 16-bit one-weight lists (k_sparse_count16): pres per block (4 segments of
 // 4095), setup kernels (per-segment counts; joint bank-scheduled fill) and the sweep
 int c16_block_pres();
+bool c16_bytes();  // k_sparse_count8 byte image (default) vs the pair-encoded k_sparse_count16
 void launch_c16_count(const uint32_t* meta, const int64_t* off, int64_t lists, int pb, uint2* cnt, cudaStream_t s);
 bool launch_c16_fill(const uint32_t* meta, uint32_t* tmp, const int64_t* off, const uint2* desc, int nblocks, int nl,
                      int pb, int sub, uint16_t* out, cudaStream_t s);

@@ -192,7 +192,39 @@ def cfg4_entry(steps: int) -> dict:
             "ref_seconds": round(time.time() - t0, 1)}
 
 
+def cfg3_entry(steps: int) -> dict:
+    """BASELINE cfg3 at full size, truncated T: the reference's own mat_run
+    on build_scenario(32000, 1.0, seed 0), all synapses plastic,
+    StdpConfig::defaults(), Auto storage (CSR).  ~70 GB of host RAM, ~4 min
+    plus ~4 s per step: generated on the GPU box's host
+    (python tests/golden/make_golden.py --cfg3 OUT.json)."""
+    t0 = time.time()
+    r = B.ref_scenario_stdp_raster(32000, 1.0, 0, steps)
+    return {"n": 32000, "p": 1.0, "seed": 0, "steps": steps, "stdp": "defaults", "synapses": r["synapses"],
+            "spikes": int(len(r["steps"])), "digest": raster_digest(r["steps"], r["neurons"]),
+            "per_step": np.bincount(r["steps"], minlength=steps).astype(int).tolist(),
+            "ref_path": "mat_run (reference, oracle/_ref, Auto storage)", "ref_seconds": round(time.time() - t0, 1),
+            "ref_peak_rss_gb": round(r["peak_rss_gb"], 1)}
+
+
 if __name__ == "__main__":
+    if "--cfg3" in sys.argv:     # full-size cfg3 golden (run on a host with >= 96 GB RAM)
+        out = sys.argv[sys.argv.index("--cfg3") + 1]
+        e = cfg3_entry(int(os.environ.get("CFG3_STEPS", "6")))
+        with open(out, "w") as f:
+            json.dump(e, f, indent=1)
+        print(json.dumps(e))
+        sys.exit(0)
+    if "--merge-cfg3" in sys.argv:
+        with open(sys.argv[sys.argv.index("--merge-cfg3") + 1]) as f:
+            e = json.load(f)
+        path = os.path.join(HERE, "scale.json")
+        with open(path) as f:
+            scale = json.load(f)
+        scale[f"cfg3_seed0_T{e['steps']}"] = e
+        with open(path, "w") as f:
+            json.dump(scale, f, indent=1)
+        sys.exit(0)
     if "--cfg4" in sys.argv:     # full-size cfg4 golden (run on a host with >= 64 GB RAM)
         out = sys.argv[sys.argv.index("--cfg4") + 1]
         steps = int(os.environ.get("CFG4_STEPS", "24"))

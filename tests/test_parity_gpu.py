@@ -797,7 +797,7 @@ def test_sparse_multiple_pre_blocks(n, p, dmax, weights):
     assert np.array_equal(s, o["steps"]) and np.array_equal(q, o["neurons"])
     assert close_rel(mem, o["membrane"])
     c16 = 1 < dmax <= 16 and p < 0.1
-    expect = {"one": 13 if c16 else 11 if dmax <= 32 else 6, "three": 6, "float": 5}[weights]
+    expect = {"one": 15 if c16 else 11 if dmax <= 32 else 6, "three": 6, "float": 5}[weights]
     assert st["sweep_kernel"] == expect
 
 
@@ -820,8 +820,9 @@ def test_count16_matches_count32(monkeypatch, storage):
               "weight": np.ones(len(pre)), "delay": delay, "stdp": np.zeros(len(pre), np.uint8)}
     o = B.run_oracle(arrays, steps, stim) if storage == 2 else None
     runs = {}
-    for c16 in ("1", "0"):
-        monkeypatch.setenv("SNB_SPARSE_COUNT16", c16)
+    for c16 in ("bytes", "bits", "0"):
+        monkeypatch.setenv("SNB_SPARSE_COUNT16", "0" if c16 == "0" else "1")
+        monkeypatch.setenv("SNB_C16_IMAGE", c16 if c16 != "0" else "bytes")
         eng = MatEngine(storage=2, precision="f64")
         if storage == 2:
             eng.add_neurons(arrays["threshold"], arrays["leak"], arrays["reset"], arrays["refractory"],
@@ -835,13 +836,14 @@ def test_count16_matches_count32(monkeypatch, storage):
         s, q = eng.raster()
         runs[c16] = (s, q, eng.membrane(), eng.stats()["sweep_kernel"])
         eng.close()
-    assert runs["1"][3] == 13 and runs["0"][3] == 11
-    assert len(runs["1"][0]) > 5000
-    assert np.array_equal(runs["1"][0], runs["0"][0]) and np.array_equal(runs["1"][1], runs["0"][1])
-    assert np.array_equal(runs["1"][2], runs["0"][2])
+    assert runs["bytes"][3] == 15 and runs["bits"][3] == 13 and runs["0"][3] == 11
+    assert len(runs["bytes"][0]) > 5000
+    for k in ("bits", "0"):
+        assert np.array_equal(runs["bytes"][0], runs[k][0]) and np.array_equal(runs["bytes"][1], runs[k][1])
+        assert np.array_equal(runs["bytes"][2], runs[k][2])
     if o is not None:
-        assert np.array_equal(runs["1"][0], o["steps"]) and np.array_equal(runs["1"][1], o["neurons"])
-        assert close_rel(runs["1"][2], o["membrane"])
+        assert np.array_equal(runs["bytes"][0], o["steps"]) and np.array_equal(runs["bytes"][1], o["neurons"])
+        assert close_rel(runs["bytes"][2], o["membrane"])
 
 
 @pytest.mark.parametrize("precision,dmax", [
@@ -1010,6 +1012,27 @@ def test_cfg3_full_size_invariants():
     assert census.tolist() == [sizes[k] for k in vals] + [n]   # + the N absent diagonal cells
 
 
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_cfg3_full_size_raster_matches_reference(precision):
+    """BASELINE cfg3 at its full size -- ER(32000, p=1), 1.02e9 synapses, all
+    plastic, StdpConfig::defaults(), paper stimulus -- generated on the
+    device, against the first T steps of the reference's own mat_run on the
+    same scenario (tests/golden/scale.json "cfg3_seed0_T*", made by
+    make_golden.py --cfg3 on the GPU box's host: 70 GB, ~4 min): raster
+    SHA-256 and per-step counts identical, with fp32 and fp64 weights."""
+    entries = [v for k, v in _scale().items() if k.startswith("cfg3_seed0_T")]
+    if not entries:
+        pytest.skip("no full-size cfg3 golden in scale.json")
+    e = max(entries, key=lambda v: v["steps"])
+    eng = _generated(e, 1, stdp=True, precision=precision)
+    s, q = eng.raster()
+    st = eng.stats()
+    eng.close()
+    assert st["synapses_local"] == e["synapses"]
+    assert np.bincount(s, minlength=e["steps"]).tolist() == e["per_step"]
+    assert _digest(s, q) == e["digest"]
+
+
 def test_cfg5_full_size_invariants():
     """BASELINE cfg5 at its full size on one GPU (ER(96000, p=1) all plastic,
     36.9 GB of fp32 weights): the 3 inputs alone fire at t = 0, the saturated
@@ -1099,7 +1122,7 @@ def test_float_stdp_300_steps_fp32_storage(storage, dmax):
     assert close_rel(wt, ow, abs_floor=fp32_weight_floor(steps, w, d.w_min, d.w_max))
 
 
-@pytest.mark.parametrize("count16", ["1", "0"], ids=["count16", "count32"])
+@pytest.mark.parametrize("count16", ["bytes", "bits", "0"], ids=["count8", "count16", "count32"])
 def test_cfg4_full_size_raster_matches_reference(monkeypatch, count16):
     """BASELINE cfg4 at its full size -- ER(256000, p=0.01), 655 M synapses,
     pair-keyed delays 1..16, paper stimulus -- generated on the device, for the
@@ -1111,12 +1134,13 @@ def test_cfg4_full_size_raster_matches_reference(monkeypatch, count16):
     if not entries:
         pytest.skip("no full-size cfg4 golden in scale.json")
     e = max(entries, key=lambda v: v["steps"])
-    monkeypatch.setenv("SNB_SPARSE_COUNT16", count16)
+    monkeypatch.setenv("SNB_SPARSE_COUNT16", "0" if count16 == "0" else "1")
+    monkeypatch.setenv("SNB_C16_IMAGE", "bits" if count16 == "bits" else "bytes")
     eng = _generated(dict(e, stdp=False), 2, precision="f32")
     s, q = eng.raster()
     st = eng.stats()
     eng.close()
-    assert st["sweep_kernel"] == (13 if count16 == "1" else 11)
+    assert st["sweep_kernel"] == {"bytes": 15, "bits": 13, "0": 11}[count16]
     assert st["synapses_local"] == e["synapses"]
     assert np.bincount(s, minlength=e["steps"]).tolist() == e["per_step"]
     assert _digest(s, q) == e["digest"]
@@ -1155,6 +1179,12 @@ def test_nccl_one_rank_partitioned_sequence(storage, use_graphs):
         assert st["exchange_ms"] > 0.0                  # the all-gather + k_hist span was timed
 
 
+# the two shared-memory images of the 16-bit segmented lists: one byte per
+# (pre, delay) -- k_sparse_count8, the default -- and the pair-encoded 16-bit
+# history of k_sparse_count16 (SNB_C16_IMAGE=bits)
+C16_IMAGES = {"bytes": 15, "bits": 13}
+
+
 def _count16_problem():
     """cfg4-shaped one-weight net small enough for the oracle: ER(36000, 0.01),
     pair-keyed delays 1..16 (the 16-bit count lists, 3 pre blocks)."""
@@ -1170,8 +1200,9 @@ def _count16_problem():
     return arrays, stim, steps
 
 
+@pytest.mark.parametrize("image", list(C16_IMAGES))
 @pytest.mark.parametrize("mode", ["host2", "host4", "nccl1"])
-def test_count16_partitions_fold_history(mode):
+def test_count16_partitions_fold_history(monkeypatch, mode, image):
     """Partitioned k_sparse_count16 runs fold k_hist into the sweep's staging
     (history double-buffered by step parity, the step handed over by k_neuron):
     G = 2 / 4 partitions through the host exchange and the 1-rank NCCL
@@ -1180,6 +1211,7 @@ def test_count16_partitions_fold_history(mode):
     import paper_2305_02510_b200 as sn
     from oracle import bridge as B
     from paper_2305_02510_b200.engine import MatEngine, partition_range
+    monkeypatch.setenv("SNB_C16_IMAGE", image)
     arrays, stim, steps = _count16_problem()
     n = len(arrays["threshold"])
     o = B.run_oracle(arrays, steps, stim)
@@ -1211,7 +1243,7 @@ def test_count16_partitions_fold_history(mode):
                         e.put_spike_words(q * wpr, words[q])
             for e in engines:
                 e.step_finish()
-    assert all(e.stats()["sweep_kernel"] == 13 for e in engines)   # k_sparse_count16
+    assert all(e.stats()["sweep_kernel"] == C16_IMAGES[image] for e in engines)
     rasters = [e.raster() for e in engines]
     s = np.concatenate([x[0] for x in rasters])
     q = np.concatenate([x[1] for x in rasters])
@@ -1223,9 +1255,10 @@ def test_count16_partitions_fold_history(mode):
         e.close()
 
 
+@pytest.mark.parametrize("image", list(C16_IMAGES))
 @pytest.mark.parametrize("skew", [False, True], ids=["lockstep", "rank0_ahead"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_count16_p2p_fold_waits_in_the_sweep(world, skew):
+def test_count16_p2p_fold_waits_in_the_sweep(monkeypatch, world, skew, image):
     """The p2p exchange with the folded history: two kernels per step --
     k_neuron stores its words into every rank's exchange buffer t & 1 and
     releases its flag; the k_sparse_count16 sweep waits for every flag and
@@ -1234,6 +1267,7 @@ def test_count16_p2p_fold_waits_in_the_sweep(world, skew):
     ahead), against the oracle."""
     from oracle import bridge as B
     from paper_2305_02510_b200.engine import MatEngine, p2p_connect_local
+    monkeypatch.setenv("SNB_C16_IMAGE", image)
     arrays, stim, steps = _count16_problem()
     o = B.run_oracle(arrays, steps, stim)
     engines = []
@@ -1251,7 +1285,7 @@ def test_count16_p2p_fold_waits_in_the_sweep(world, skew):
         else:
             engines[r].step_finish()
             engines[r].synchronize()
-    assert all(e.stats()["sweep_kernel"] == 13 for e in engines)
+    assert all(e.stats()["sweep_kernel"] == C16_IMAGES[image] for e in engines)
     assert all(e.stats()["kernel_launches"] == 2 * steps for e in engines)   # k_neuron + sweep
     rasters = [e.raster() for e in engines]
     s = np.concatenate([x[0] for x in rasters])

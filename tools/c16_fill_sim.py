@@ -1,0 +1,62 @@
+"""Shared-memory wavefronts per LDS of the k_sparse_count8 list layout, from
+the fill code itself run on the host (tools/c16_fill_check.cu): random
+cfg4-shaped lists (p = 0.01 over a 3 x 4095-pre block, delays 1..16, SUB = 4,
+8 posts per warp group), the kernel's LDS order (row-major chunk stream, entry
+e of every active lane's chunk per LDS), banks = 4-byte words mod 32 with
+same-word broadcast.  Usage: python tools/c16_fill_sim.py [groups]"""
+import os
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SEGP, SUB, P = 4095, 4, 8
+
+
+def zero(s):
+    return 4095 - 16 * s
+
+
+def main(groups):
+    rng = np.random.default_rng(7)
+    tmp = tempfile.mkdtemp()
+    exe = os.path.join(tmp, "c16_fill_check")
+    subprocess.run(["nvcc", "-std=c++17", "-O2", "-gencode", "arch=compute_100a,code=sm_100a",
+                    "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "paper_2305_02510_b200", "csrc"),
+                    "-I" + os.path.join(ROOT, "include"), "-o", exe,
+                    os.path.join(ROOT, "tools", "c16_fill_check.cu")], check=True, capture_output=True)
+    posts = []
+    buf = [np.int32(groups).tobytes()]
+    for _ in range(groups * P):
+        m = rng.binomial(3 * SEGP, 0.01)
+        pl = np.sort(rng.choice(3 * SEGP, m, replace=False))
+        dm1 = rng.integers(0, 16, m)
+        n = np.bincount(pl // SEGP, minlength=3)
+        e = np.cumsum((n + 7) // 8)
+        y = int(e[0]) | int(e[1]) << 8 | int(e[2]) << 16 | int(e[2]) << 24
+        posts.append((int(e[2]), int(e[0]), int(e[1])))
+        buf += [np.array([y, m], np.uint32).tobytes(), (pl | dm1 << 16).astype(np.uint32).tobytes()]
+    inp, outp = os.path.join(tmp, "in.bin"), os.path.join(tmp, "out.bin")
+    with open(inp, "wb") as f:
+        f.write(b"".join(buf))
+    subprocess.run([exe, inp, outp], check=True)
+    ent = np.fromfile(outp, np.uint16).reshape(-1, 8)
+    pos, wf, lds = 0, 0, 0
+    for g in range(groups):
+        grp = posts[g * P:(g + 1) * P]
+        rows = (max(c for c, _, _ in grp) + SUB - 1) // SUB
+        for r in range(rows):
+            lanes = [(i, r * SUB + sl) for i in range(P) for sl in range(SUB) if r * SUB + sl < grp[i][0]]
+            for e in range(8):
+                words = {((int(c >= grp[i][1]) + int(c >= grp[i][2])) << 16 | int(ent[pos + q, e])) >> 2
+                         for q, (i, c) in enumerate(lanes)}
+                wf += np.bincount([w & 31 for w in words], minlength=32).max()
+                lds += 1
+            pos += len(lanes)
+    print(f"{groups} warp groups, {lds} LDS: {wf / lds:.3f} shared-memory wavefronts per LDS (ideal 1)")
+
+
+if __name__ == "__main__":
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 200)

@@ -48,7 +48,7 @@ CASES = {  # name: (problem args, engine options, expected sweep kernel)
     "dense_tma_delay": (dict(n=2048, p=0.5, seed=2, steps=8, dmax=3, plastic=1.0), dict(storage=1, persistent=False), 2),
     "cluster": (dict(n=600, p=0.5, seed=3, steps=20, dmax=8, one_weight=True), dict(storage=1), 14),
     "tiny": (dict(n=200, p=0.1, seed=4, steps=30, dmax=3, plastic=0.7), dict(storage=0), 9),
-    "count16": (dict(n=20000, p=0.002, seed=5, steps=12, dmax=8, one_weight=True), dict(storage=2), 13),
+    "count16": (dict(n=20000, p=0.002, seed=5, steps=12, dmax=8, one_weight=True), dict(storage=2), 15),
     "sparse_pull": (dict(n=5000, p=0.01, seed=6, steps=10, dmax=2, plastic=0.6), dict(storage=2), 5),
 }
 
