@@ -633,8 +633,8 @@ bool Engine::build_c16() {
     }
     c16_ = true;
     // bytes the sweep moves in this format: 2 B per stored entry (padding included),
-    // the 8-byte descriptor and the 8-byte partial of every (block, post) list
-    sweep_bytes_full_ = static_cast<double>(chunks) * 16.0 + static_cast<double>(lists) * 16.0;
+    // the 8-byte descriptor and the 2-byte count of every (block, post) list
+    sweep_bytes_full_ = static_cast<double>(chunks) * 16.0 + static_cast<double>(lists) * 10.0;
     return true;
 }
 

@@ -127,6 +127,9 @@ NeuronArgs Engine::neuron_args(int t_base, int rows, uint32_t* raster, double* t
     a.cnt = d_cnt_.as<int32_t>();
     a.partial = d_partial_.as<double>();
     a.nchunks = nchunks_;  // partial rows to sum
+    a.partial16 = c16_ ? d_partial_.as<uint16_t>() : nullptr;
+    a.w0 = dict_.empty() ? 0.0 : dict_[0];
+    a.w0_f32 = f64_ ? 0 : 1;
     a.u_exact = d_uexact_.as<double>();
     a.st_off = st_off;
     a.st_neuron = st_neuron;
@@ -248,6 +251,7 @@ void Engine::launch_sweep_only() {
         a.dict_size = static_cast<int32_t>(dict_.size());
         a.pot_staged = pot_staged_ ? 1 : 0;
         a.partial = d_partial_.as<double>();
+        a.partial16 = c16_ ? d_partial_.as<uint16_t>() : nullptr;
         a.v = d_v_.as<double>();
         a.leak = d_leak_.as<double>();
         a.reset = d_reset_.as<double>();

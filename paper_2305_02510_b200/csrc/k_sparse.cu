@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(NT, NT == kThreads ? SNB_C16_MINB : 1024 / NT)
 #pragma unroll
         for (int o = SUB / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         if (valid && sl == 0)
-            a.partial[static_cast<int64_t>(b) * a.nl + p] = static_cast<double>(static_cast<WT>(cnt) * w0);
+            a.partial16[static_cast<int64_t>(b) * a.nl + p] = static_cast<uint16_t>(cnt);
         p = pn;
         d = dn;
 #if SNB_C16_PIPE
@@ -737,7 +737,7 @@ __global__ void __launch_bounds__(NT, 1) k_sparse_count8(SparseArgs a, const uin
 #pragma unroll
         for (int o = SUB / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         if (valid && sl == 0)
-            a.partial[static_cast<int64_t>(b) * a.nl + p] = static_cast<double>(static_cast<WT>(static_cast<int>(cnt)) * w0);
+            a.partial16[static_cast<int64_t>(b) * a.nl + p] = static_cast<uint16_t>(cnt);
         p = pn;
         d = dn;
     }

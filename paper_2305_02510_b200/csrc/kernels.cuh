@@ -31,6 +31,11 @@ struct NeuronArgs {
     // synaptic input
     const double* partial;     // [nchunks][nl] (non-exact)
     int32_t nchunks;
+    // or, from the 16-bit count-list sweeps: per-block delivery counts, a
+    // block's input being (double)((WT)count * w0) as those sweeps computed it
+    const uint16_t* partial16; // [nchunks][nl] or null
+    double w0;
+    int32_t w0_f32;            // WT = float
     const double* u_exact;     // [nl] (exact mode)
     // stimulus: per-step CSR over (neuron asc, amp)
     const int64_t* st_off;     // [st_steps + 1]
@@ -150,6 +155,7 @@ struct SparseArgs {
     int32_t dict_size;         // 0: weights stream from w[]
     int32_t pot_staged;        // STDP: the block's pot^(d) traces are staged in shared memory
     double* partial;           // [nblocks][nl]
+    uint16_t* partial16;       // [nblocks][nl] counts (k_sparse_count8 / count16)
     const double* v;
     const double* leak;
     const double* reset;

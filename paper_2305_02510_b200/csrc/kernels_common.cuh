@@ -136,10 +136,10 @@ __device__ __forceinline__ uint32_t bit_of(const uint32_t* bits, int i) {
 //   pot_i^(d)  = sum_{k=1..W} a_plus[k-1]  s_i[t-k-d+1]       (lowered-net shift)
 // Returns whether row i must be visited by the sweep this step.
 //
-// Windows + delay spans beyond kHistWordsMax * 64 steps (any window >= 1 is
-// valid, model.cpp:104-117) take hist_update_long: the same sums with the
-// history words read back from global memory instead of registers.
-__device__ __noinline__ bool hist_update_long(const HistArgs& h, int i, bool s, int t) {
+// Windows + delay spans beyond 64 steps (any window >= 1 is valid,
+// model.cpp:104-117) take hist_update_long: the same sums with the history
+// words read back from global memory instead of one register.
+__device__ __forceinline__ bool hist_update_long(const HistArgs& h, int i, bool s, int t) {
     uint64_t carry = s ? 1ull : 0ull, w0 = 0;
     for (int k = 0; k < h.hw; ++k) {
         uint64_t* p = h.hist + static_cast<int64_t>(k) * h.n + i;
@@ -172,28 +172,19 @@ __device__ __noinline__ bool hist_update_long(const HistArgs& h, int i, bool s, 
 }
 
 __device__ __forceinline__ bool hist_update(const HistArgs& h, int i, bool s, int t) {
-    if (h.hw > kHistWordsMax) return hist_update_long(h, i, s, t);
-    uint64_t words[kHistWordsMax];
-    uint64_t carry = s ? 1ull : 0ull;
-#pragma unroll
-    for (int k = 0; k < kHistWordsMax; ++k) {
-        if (k < h.hw) {
-            const uint64_t x = h.hist[static_cast<int64_t>(k) * h.n + i];
-            const uint64_t nx = (x << 1) | carry;
-            carry = x >> 63;
-            h.hist[static_cast<int64_t>(k) * h.n + i] = nx;
-            words[k] = nx;
-        } else {
-            words[k] = 0;
-        }
-    }
-    if (h.hist_lo) h.hist_lo[i] = static_cast<uint32_t>(words[0]);
+    // one history word (window + delay span <= 64) in registers; longer
+    // histories (several words) go through hist_update_long, whose dynamic
+    // bit indexing would otherwise put a word array in local memory on every path
+    if (h.hw != 1) return hist_update_long(h, i, s, t);
+    uint64_t* p = h.hist + i;
+    const uint64_t w0 = (*p << 1) | (s ? 1ull : 0ull);
+    *p = w0;
+    if (h.hist_lo) h.hist_lo[i] = static_cast<uint32_t>(w0);
     const uint64_t dmask = h.dmax >= 64 ? ~0ull : ((1ull << h.dmax) - 1ull);
-    bool act = (words[0] & dmask) != 0;
-    if (h.stdp && h.hw == 1) {
-        // one history word (window + delay span <= 64): walk the set bits in
-        // ascending k, the order of the reference's sums (mat_engine.cpp:226-240)
-        const uint64_t w0 = words[0];
+    bool act = (w0 & dmask) != 0;
+    if (h.stdp) {
+        // walk the set bits in ascending k, the order of the reference's sums
+        // (mat_engine.cpp:226-240)
         const uint64_t wmask = h.window >= 63 ? ~0ull : ((1ull << (h.window + 1)) - 1ull);
         double dep = 0.0;
         for (uint64_t m = w0 & wmask & ~1ull; m; m &= m - 1) dep += h.a_minus[__ffsll(static_cast<long long>(m)) - 2];
@@ -203,25 +194,6 @@ __device__ __forceinline__ bool hist_update(const HistArgs& h, int i, bool s, in
             const uint64_t sh = w0 >> (d - 1);  // bit k of sh = s[t - k - d + 1]
             double pot = 0.0;
             for (uint64_t m = sh & wmask & ~1ull; m; m &= m - 1) pot += h.a_plus[__ffsll(static_cast<long long>(m)) - 2];
-            h.pot64[static_cast<int64_t>(i) * h.dp + (d - 1)] = pot;
-            any_pot |= (pot != 0.0);
-        }
-        if (h.row_plastic[i] && (any_pot || t == h.clamp_step)) act = true;
-    } else if (h.stdp) {
-        // dep: bits 1..W
-        double dep = 0.0;
-        for (int k = 1; k <= h.window; ++k) {
-            const int b = k;
-            if ((words[b >> 6] >> (b & 63)) & 1ull) dep += h.a_minus[k - 1];
-        }
-        h.dep64[i] = dep;
-        bool any_pot = false;
-        for (int d = 1; d <= h.dp; ++d) {
-            double pot = 0.0;
-            for (int k = 1; k <= h.window; ++k) {
-                const int b = k + d - 1;
-                if ((words[b >> 6] >> (b & 63)) & 1ull) pot += h.a_plus[k - 1];
-            }
             h.pot64[static_cast<int64_t>(i) * h.dp + (d - 1)] = pot;
             any_pot |= (pot != 0.0);
         }
@@ -257,6 +229,28 @@ __device__ __forceinline__ uint32_t neuron_step(const NeuronArgs& a, const HistA
             // arrive in a few memory round trips
             double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             int c = 0;
+            if (a.partial16) {
+                // 16-bit block counts: 2 B per (block, post) instead of 8; the block's
+                // value and the summation tree are the ones of the fp64 partials
+                const float w0f = static_cast<float>(a.w0);
+                auto val = [&](uint32_t k) {
+                    return a.w0_f32 ? static_cast<double>(static_cast<float>(k) * w0f) : static_cast<double>(k) * a.w0;
+                };
+                for (; c + 16 <= a.nchunks; c += 16) {
+                    uint32_t t[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) t[k] = __ldcg(a.partial16 + static_cast<int64_t>(c + k) * a.nl + j);
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) acc[k & 7] += val(t[k]);
+                }
+                uint32_t t[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) t[k] = c + k < a.nchunks ? __ldcg(a.partial16 + static_cast<int64_t>(c + k) * a.nl + j) : 0u;
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                    if (c + k < a.nchunks) acc[k & 7] += val(t[k]);
+                c = a.nchunks;
+            }
             for (; c + 16 <= a.nchunks; c += 16) {
                 double t[16];
 #pragma unroll
