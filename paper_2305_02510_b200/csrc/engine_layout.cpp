@@ -586,12 +586,13 @@ bool Engine::build_c16() {
     std::vector<uint32_t> desc(static_cast<size_t>(lists) * 2);
     uint64_t chunks = 0;
     // byte image (k_sparse_count8): the 32 / sub posts of a warp share one
-    // row-major chunk stream; every descriptor carries the group's first chunk
+    // row-major chunk stream; every descriptor carries the group's first chunk,
+    // aligned to 128 bytes so the rows every post fills are 4 whole lines
     const bool grouped = c16_bytes();
     const int P = 32 / sub_;
-    uint64_t group0 = 0;
+    uint64_t group0 = 0, stored = 0;
     for (int64_t L = 0; L < lists; ++L) {
-        if (grouped && (L % nl_) % P == 0) group0 = chunks;
+        if (grouped && (L % nl_) % P == 0) group0 = chunks = (chunks + 7) / 8 * 8;
         const uint32_t x = cnt[2 * L], y = cnt[2 * L + 1];
         const uint32_t n[4] = {x & 0xffffu, x >> 16, y & 0xffffu, y >> 16};
         uint32_t e[4], acc = 0;
@@ -603,6 +604,7 @@ bool Engine::build_c16() {
         desc[2 * L] = static_cast<uint32_t>(grouped ? group0 : chunks);
         desc[2 * L + 1] = e[0] | (e[1] << 8) | (e[2] << 16) | (e[3] << 24);
         chunks += acc;
+        stored += acc;
     }
     if (chunks >= (1ull << 32)) return false;
     size_t free_b = 0, total_b = 0;
@@ -634,7 +636,7 @@ bool Engine::build_c16() {
     c16_ = true;
     // bytes the sweep moves in this format: 2 B per stored entry (padding included),
     // the 8-byte descriptor and the 2-byte count of every (block, post) list
-    sweep_bytes_full_ = static_cast<double>(chunks) * 16.0 + static_cast<double>(lists) * 10.0;
+    sweep_bytes_full_ = static_cast<double>(stored) * 16.0 + static_cast<double>(lists) * 10.0;
     return true;
 }
 
