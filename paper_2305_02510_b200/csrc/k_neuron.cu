@@ -2,6 +2,8 @@
 // history kernel of partitioned runs (k_hist), and two helpers.
 #include "kernels_common.cuh"
 
+#include <cstdlib>
+
 #ifndef SNB_NEURON_MINB
 #define SNB_NEURON_MINB 4
 #endif
@@ -32,6 +34,50 @@ __global__ void __launch_bounds__(kThreads, SNB_NEURON_MINB) k_neuron(NeuronArgs
             if (prev == gridDim.x - 1) {
                 __threadfence_system();
                 for (int q = 0; q < a.world; ++q) st_release_sys(a.peer_flags[q] + a.rank, t + 1);
+                *a.done = 0;
+            }
+        }
+    }
+}
+
+// Many partial rows (dense sweeps: 125 for cfg3, 334 per rank for an 8-way
+// cfg5 partition): a CTA of kThreads threads takes kSplitPosts posts, its four
+// thread quarters sum a quarter of the rows each (four times the loads in
+// flight per post), and its first kSplitPosts threads combine the quarters in
+// a fixed order and run the neuron step.
+constexpr int kSplitPosts = kThreads / 4;
+template <bool FUSED>
+__global__ void __launch_bounds__(kThreads, SNB_NEURON_MINB) k_neuron_split(NeuronArgs a, HistArgs h) {
+    __shared__ double quarter[4][kSplitPosts];
+    const int t = *a.d_step;
+    if (a.step_out && blockIdx.x == 0 && threadIdx.x == 0) *a.step_out = t;
+    const int q = threadIdx.x / kSplitPosts, jl = threadIdx.x % kSplitPosts;
+    const int j0 = blockIdx.x * kSplitPosts;
+    if (j0 + jl < a.nl) {
+        const int c0 = static_cast<int>((static_cast<int64_t>(a.nchunks) * q) / 4);
+        const int c1 = static_cast<int>((static_cast<int64_t>(a.nchunks) * (q + 1)) / 4);
+        quarter[q][jl] = partial_sum<false>(a, j0 + jl, c0, c1);
+    }
+    __syncthreads();
+    uint32_t f = 0;
+    if (threadIdx.x < kSplitPosts) {  // whole warps
+        const double in = (quarter[0][jl] + quarter[1][jl]) + (quarter[2][jl] + quarter[3][jl]);
+        f = neuron_step<false, FUSED, false, true>(a, h, j0 + jl, t, in);
+    }
+    const int spikes = __syncthreads_count(f & 1u);
+    const int active = FUSED ? __syncthreads_count(f & 2u) : 0;
+    if (threadIdx.x == 0) {
+        if (spikes) atomicAdd(a.spike_count, static_cast<unsigned long long>(spikes));
+        if (active) atomicAdd(h.active_count, static_cast<unsigned long long>(active));
+    }
+    if (a.peer_bits) {  // as k_neuron
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t prev = atomicAdd(a.done, 1u);
+            if (prev == gridDim.x - 1) {
+                __threadfence_system();
+                for (int r = 0; r < a.world; ++r) st_release_sys(a.peer_flags[r] + a.rank, t + 1);
                 *a.done = 0;
             }
         }
@@ -87,7 +133,25 @@ __global__ void k_step_bump(int32_t* d_step) { *d_step += 1; }
 
 }  // namespace
 
+int neuron_split_min_rows() {
+    static const int v = [] {
+        const char* e = std::getenv("SNB_NEURON_SPLIT_ROWS");  // A/B knob; 0 disables the split kernel
+        return e ? std::atoi(e) : 32;
+    }();
+    return v;
+}
+
 void launch_neuron(const NeuronArgs& a, bool exact, bool fused, const HistArgs& h, cudaStream_t s) {
+    const int split_rows = neuron_split_min_rows();
+    if (!exact && !a.partial16 && split_rows > 0 && a.nchunks >= split_rows) {
+        int grid = (a.nl + kSplitPosts - 1) / kSplitPosts;
+        if (a.peer_bits && grid == 0) grid = 1;
+        if (grid == 0) return;
+        if (fused) k_neuron_split<true><<<grid, kThreads, 0, s>>>(a, h);
+        else k_neuron_split<false><<<grid, kThreads, 0, s>>>(a, h);
+        check(cudaGetLastError(), "k_neuron_split");
+        return;
+    }
     int grid = (a.nl + kThreads - 1) / kThreads;
     if (a.peer_bits && grid == 0) grid = 1;  // an empty partition still publishes its step
     if (grid == 0) return;

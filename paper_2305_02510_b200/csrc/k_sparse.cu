@@ -48,7 +48,11 @@ __device__ __forceinline__ size_t stage_history(const SparseArgs& a, int pre0, i
     return (static_cast<size_t>(a.pb + 1) * sizeof(HT) + 15) & ~static_cast<size_t>(15);
 }
 
-template <typename WT, bool STDP, int HB, int SUB, bool DICT>
+// PS: the pre block's pot^(d) traces are staged in shared memory (a.pot_staged);
+// a compile-time flag so their loads are LDS, free to move past the weight
+// stores (through one generic pointer for both cases every pot load was an
+// LD.E.64 ordered after the previous chunk's weight store)
+template <typename WT, bool STDP, int HB, int SUB, bool DICT, bool PS = false>
 #ifndef SNB_SPARSE_MINB
 #define SNB_SPARSE_MINB 4  // <= 64 regs: 4 CTAs/SM (5 spills; cfg4 0.562 ms vs 0.652 unbounded)
 #endif
@@ -68,7 +72,7 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(Spars
     // STDP: the block's pot^(d) traces, [pcount][dp], staged next to the history
     // (the per-synapse lookup would otherwise be a random global gather)
     double* s_pot = reinterpret_cast<double*>(smem_raw + hbytes);
-    if (STDP && a.pot_staged) {
+    if (STDP && PS) {
         const double* src = a.pot + static_cast<int64_t>(pre0) * a.dp;
         for (int k = tid; k < pcount * a.dp; k += kThreads) s_pot[k] = __ldcg(src + k);
     }
@@ -78,7 +82,7 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(Spars
     const bool uniform = DICT && a.dict_size == 2;  // {w, 0.0 padding}: every synapse carries w
 
     const WT wmin = static_cast<WT>(a.w_min), wmax = static_cast<WT>(a.w_max);
-    const double* pot = (STDP && a.pot_staged) ? s_pot : a.pot + static_cast<int64_t>(pre0) * a.dp;
+    const double* pot = (STDP && PS) ? s_pot : a.pot + static_cast<int64_t>(pre0) * a.dp;
     const double* dep = a.dep;
     WT* W = static_cast<WT*>(a.w);
 
@@ -163,18 +167,27 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(Spars
                     }
                     const uint32_t ms[4] = {m4[u].x, m4[u].y, m4[u].z, m4[u].w};
                     bool changed = false;
+                    // the 4 history bits and pot^(d) traces first (all loads in flight together)
+                    uint32_t ev[4];
+                    double ptv[4];
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const uint32_t m = ms[k];
                         const int pl = static_cast<int>(m & 0xffffu);
                         const int d1 = static_cast<int>((m >> 16) & 63u);
                         SNB_DCHECK(pl <= a.pb && (!STDP || !((m >> 22) & 1u) || (pl < pcount && d1 < a.dp)));
-                        uint32_t e;
-                        if (HB == 1) e = (sbits[pl >> 5] >> (pl & 31)) & 1u;
-                        else e = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
+                        if (HB == 1) ev[k] = (sbits[pl >> 5] >> (pl & 31)) & 1u;
+                        else ev[k] = static_cast<uint32_t>((shist[pl] >> d1) & 1u);
+                        // only spiking posts read pot^(d), only plastic synapses index it
+                        ptv[k] = (!DICT && STDP && sp && ((m >> 22) & 1u)) ? pot[pl * a.dp + d1] : 0.0;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t m = ms[k];
+                        const uint32_t e = ev[k];
                         WT w = wv[u][k];
                         if (!DICT && STDP && a.plastic_on && ((m >> 22) & 1u)) {
-                            const double pt = sp ? pot[pl * a.dp + d1] : 0.0;  // only spiking posts read pot^(d)
+                            const double pt = ptv[k];
                             const WT nw = stdp_apply<WT>(w, stdp_dw(sp, pt, e != 0u, depp), wmin, wmax);
                             changed |= (nw != w);
                             w = nw;
@@ -1362,6 +1375,15 @@ static void sparse_go_sub(const SparseArgs& a, int sub, int gx, size_t smem, cud
             default: go(k_sparse_pull<WT, false, HB, 32, true>); break;
         }
         return;
+    }
+    if (STDP && a.pot_staged) {
+        switch (sub) {
+            case 4: go(k_sparse_pull<WT, STDP, HB, 4, false, true>); return;
+            case 8: go(k_sparse_pull<WT, STDP, HB, 8, false, true>); return;
+            case 16: go(k_sparse_pull<WT, STDP, HB, 16, false, true>); return;
+            case 32: go(k_sparse_pull<WT, STDP, HB, 32, false, true>); return;
+            default: break;  // sub 0: the stream kernel reads a.pot_staged itself
+        }
     }
     switch (sub) {
         case 0: go(k_sparse_stream<WT, STDP, HB, false>); break;

@@ -205,6 +205,53 @@ __device__ __forceinline__ bool hist_update(const HistArgs& h, int i, bool s, in
     return act;
 }
 
+// Sum of the synaptic input partials of local post j over chunk rows [c0, c1):
+// acc[k] sums rows k, k+8, k+16, ... in order, then a fixed tree.
+template <bool P16>  // rows are a.partial16 block counts (else fp64 a.partial)
+__device__ __forceinline__ double partial_sum(const NeuronArgs& a, int j, int c0, int c1) {
+    // 16 loads are issued before any add, so the rows arrive in a few memory
+    // round trips
+    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int c = c0;
+    if (P16) {
+        // 16-bit block counts: 2 B per (block, post) instead of 8; the block's
+        // value and the summation tree are the ones of the fp64 partials
+        const float w0f = static_cast<float>(a.w0);
+        auto val = [&](uint32_t k) {
+            return a.w0_f32 ? static_cast<double>(static_cast<float>(k) * w0f) : static_cast<double>(k) * a.w0;
+        };
+        for (; c + 16 <= c1; c += 16) {
+            uint32_t t[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) t[k] = __ldcg(a.partial16 + static_cast<int64_t>(c + k) * a.nl + j);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) acc[k & 7] += val(t[k]);
+        }
+        uint32_t t[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) t[k] = c + k < c1 ? __ldcg(a.partial16 + static_cast<int64_t>(c + k) * a.nl + j) : 0u;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (c + k < c1) acc[k & 7] += val(t[k]);
+        c = c1;
+    }
+    for (; c + 16 <= c1; c += 16) {
+        double t[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) t[k] = __ldcg(a.partial + static_cast<int64_t>(c + k) * a.nl + j);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k & 7] += t[k];
+    }
+    for (; c + 8 <= c1; c += 8) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += __ldcg(a.partial + static_cast<int64_t>(c + k) * a.nl + j);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)  // remainder; unrolled so acc stays in registers
+        if (c + k < c1) acc[k] += __ldcg(a.partial + static_cast<int64_t>(c + k) * a.nl + j);
+    return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+}
+
 // ---------------------------------------------------------------------------
 // K1: LIF update of the local posts for step t (mat_engine.cpp:168-198).
 // Called by full warps (j covers a multiple of 32); one neuron per thread.
@@ -212,8 +259,9 @@ __device__ __forceinline__ bool hist_update(const HistArgs& h, int i, bool s, in
 // global counters; otherwise the caller aggregates the returned per-thread
 // flags (bit 0 spiked, bit 1 active) per CTA - one same-address atomic per
 // warp serialises at L2 once a step has ~10^4 warps.
-template <bool EXACT, bool FUSED, bool WARP_COUNT = true>
-__device__ __forceinline__ uint32_t neuron_step(const NeuronArgs& a, const HistArgs& h, int j, int t) {
+template <bool EXACT, bool FUSED, bool WARP_COUNT = true, bool INPUT = false>
+__device__ __forceinline__ uint32_t neuron_step(const NeuronArgs& a, const HistArgs& h, int j, int t,
+                                                double given = 0.0) {
     const bool valid = j < a.nl;
     if (a.work && j == 0) *a.work = 0;  // the previous sweep has finished (stream / grid order)
     bool s = false;
@@ -225,47 +273,10 @@ __device__ __forceinline__ uint32_t neuron_step(const NeuronArgs& a, const HistA
             u = a.u_exact[j];  // (leak(v) +) sum in ascending pre order, from the sweep
         } else {
             // chunk partials: acc[k] sums chunks k, k+8, k+16, ... in order, then a
-            // fixed tree; 16 loads are issued before any add so a step's partials
-            // arrive in a few memory round trips
-            double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            int c = 0;
-            if (a.partial16) {
-                // 16-bit block counts: 2 B per (block, post) instead of 8; the block's
-                // value and the summation tree are the ones of the fp64 partials
-                const float w0f = static_cast<float>(a.w0);
-                auto val = [&](uint32_t k) {
-                    return a.w0_f32 ? static_cast<double>(static_cast<float>(k) * w0f) : static_cast<double>(k) * a.w0;
-                };
-                for (; c + 16 <= a.nchunks; c += 16) {
-                    uint32_t t[16];
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) t[k] = __ldcg(a.partial16 + static_cast<int64_t>(c + k) * a.nl + j);
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) acc[k & 7] += val(t[k]);
-                }
-                uint32_t t[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) t[k] = c + k < a.nchunks ? __ldcg(a.partial16 + static_cast<int64_t>(c + k) * a.nl + j) : 0u;
-#pragma unroll
-                for (int k = 0; k < 16; ++k)
-                    if (c + k < a.nchunks) acc[k & 7] += val(t[k]);
-                c = a.nchunks;
-            }
-            for (; c + 16 <= a.nchunks; c += 16) {
-                double t[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) t[k] = __ldcg(a.partial + static_cast<int64_t>(c + k) * a.nl + j);
-#pragma unroll
-                for (int k = 0; k < 16; ++k) acc[k & 7] += t[k];
-            }
-            for (; c + 8 <= a.nchunks; c += 8) {
-#pragma unroll
-                for (int k = 0; k < 8; ++k) acc[k] += __ldcg(a.partial + static_cast<int64_t>(c + k) * a.nl + j);
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k)  // remainder; unrolled so acc stays in registers
-                if (c + k < a.nchunks) acc[k] += __ldcg(a.partial + static_cast<int64_t>(c + k) * a.nl + j);
-            const double in = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+            // fixed tree (partial_sum); or the sum handed over by the split kernel
+            const double in = INPUT ? given
+                              : a.partial16 ? partial_sum<true>(a, j, 0, a.nchunks)
+                                            : partial_sum<false>(a, j, 0, a.nchunks);
             u = a.abm ? in : leak_toward(v, a.leak[j], reset) + in;
         }
         // external stimulus: the step's entries pre-summed in list order
