@@ -133,13 +133,21 @@ class MatEngine:
     def synchronize(self):
         check(lib.sn_synchronize(self._h))
 
-    def simulate_raster(self, steps: int):
+    def simulate_raster(self, steps: int, out=None):
         """simulate(steps) and that call's raster as (steps, neurons) int32
         arrays; with stream_io the host expands finished chunks while later
-        ones run (sn_simulate_raster)."""
+        ones run (sn_simulate_raster).  out=(s, q): caller-owned int32 buffers
+        of steps * n_local entries each, reused across calls (the returned
+        arrays are views of them)."""
         cap = int(steps) * max(1, self.stats()["n_local"])
-        s = np.empty(cap, np.int32)
-        q = np.empty(cap, np.int32)
+        if out is None:
+            s = np.empty(cap, np.int32)
+            q = np.empty(cap, np.int32)
+        else:
+            s, q = out
+            if s.dtype != np.int32 or q.dtype != np.int32 or not (s.flags.c_contiguous and q.flags.c_contiguous):
+                raise ValueError("simulate_raster: out must be two C-contiguous int32 arrays")
+            cap = min(len(s), len(q))
         cnt = C.c_int64()
         check(lib.sn_simulate_raster(self._h, int(steps), ptr(s, C.c_int32), ptr(q, C.c_int32), cap, C.byref(cnt)))
         return s[:cnt.value], q[:cnt.value]

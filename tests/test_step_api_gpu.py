@@ -211,6 +211,17 @@ def test_simulate_raster_equals_simulate_then_raster(opts):
     assert np.array_equal(np.concatenate([s1, s2]), s_ref) and np.array_equal(np.concatenate([q1, q2]), q_ref)
     assert np.all(s1 < 37) and np.all(s2 >= 37)
     assert np.array_equal(s_all, s_ref) and np.array_equal(q_all, q_ref)
+    # caller-owned output arrays, reused across calls (views of them come back)
+    c = make()
+    bufs = (np.full(300 * 60, -1, np.int32), np.full(300 * 60, -1, np.int32))
+    s1, q1 = c.simulate_raster(37, out=bufs)
+    s1, q1 = s1.copy(), q1.copy()
+    s2, q2 = c.simulate_raster(steps - 37, out=bufs)
+    c.close()
+    assert np.shares_memory(s2, bufs[0]) and np.shares_memory(q2, bufs[1])
+    assert np.array_equal(np.concatenate([s1, s2]), s_ref) and np.array_equal(np.concatenate([q1, q2]), q_ref)
+    with pytest.raises(ValueError, match="int32"):
+        make().simulate_raster(3, out=(np.zeros(900, np.int64), np.zeros(900, np.int64)))
 
 
 def test_empty_network_runs_like_the_reference():
