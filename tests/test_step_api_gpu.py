@@ -220,8 +220,10 @@ def test_simulate_raster_equals_simulate_then_raster(opts):
     c.close()
     assert np.shares_memory(s2, bufs[0]) and np.shares_memory(q2, bufs[1])
     assert np.array_equal(np.concatenate([s1, s2]), s_ref) and np.array_equal(np.concatenate([q1, q2]), q_ref)
+    d = make()
     with pytest.raises(ValueError, match="int32"):
-        make().simulate_raster(3, out=(np.zeros(900, np.int64), np.zeros(900, np.int64)))
+        d.simulate_raster(3, out=(np.zeros(900, np.int64), np.zeros(900, np.int64)))
+    d.close()
 
 
 def test_empty_network_runs_like_the_reference():
