@@ -142,8 +142,16 @@ int neuron_split_min_rows() {
 }
 
 void launch_neuron(const NeuronArgs& a, bool exact, bool fused, const HistArgs& h, cudaStream_t s) {
+    // the split grid is 4x the plain one: only while it fits one wave (cfg3 32k
+    // posts: 22.4 -> 19.2 us; cfg5 96k posts: 29.5 -> 40 us, so no)
+    static const int wave_posts = [] {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return sms * SNB_NEURON_MINB * kSplitPosts;
+    }();
     const int split_rows = neuron_split_min_rows();
-    if (!exact && !a.partial16 && split_rows > 0 && a.nchunks >= split_rows) {
+    if (!exact && !a.partial16 && split_rows > 0 && a.nchunks >= split_rows && a.nl <= wave_posts) {
         int grid = (a.nl + kSplitPosts - 1) / kSplitPosts;
         if (a.peer_bits && grid == 0) grid = 1;
         if (grid == 0) return;
