@@ -566,6 +566,11 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, int rank) {
 // step t + 1 off every row a peer can still be reading (planes 0..D-1 of its
 // step t - 1 or t).
 __host__ __device__ constexpr int cl_ring(int D) { return D > 0 ? D + 2 : 2; }
+// Words between ring rows: one 16-byte bank group more than a row, so the
+// rows the (post, delay) threads of a warp read together start in different
+// banks (with a 128-byte multiple every row began at bank 0: 8-way conflicts
+// on each LDS.128 of the plane counts)
+__host__ __device__ constexpr int cl_rstride(int wn4) { return wn4 + 4; }
 struct ClLayout {
     size_t code, ex, red, in, bar, total;
 };
@@ -577,7 +582,7 @@ __host__ __device__ inline ClLayout cl_layout(int n, int P, int D) {
     L.code = o;
     o += D == 0 ? static_cast<size_t>(n) * P : static_cast<size_t>(P) * D * wn4 * 4;
     L.ex = o;
-    o += D == 0 ? static_cast<size_t>(2) * npad * 4 : static_cast<size_t>(cl_ring(D)) * wn4 * 4;
+    o += D == 0 ? static_cast<size_t>(2) * npad * 4 : static_cast<size_t>(cl_ring(D)) * cl_rstride(wn4) * 4;
     L.red = o;
     o += D == 0 ? static_cast<size_t>(kClThreads) * 4 * 4 : 0;
     L.in = o;
@@ -591,16 +596,19 @@ __host__ __device__ inline ClLayout cl_layout(int n, int P, int D) {
 #ifndef SNB_CL_MREG
 #define SNB_CL_MREG 1
 #endif
-constexpr int kClMregs = 4;  // uint4 mask registers per thread (16 words)
 
-template <typename WT, int P, int D>
-__global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, ClusterArgs ca, int steps) {
+constexpr int kClMregs = 4;  // uint4 mask registers per thread of a 1024-thread CTA (16 words)
+
+template <typename WT, int P, int D, int NT>
+__global__ void __launch_bounds__(NT, 1) k_cluster_count(NeuronArgs na, ClusterArgs ca, int steps) {
     extern __shared__ __align__(16) uint8_t smem[];
+    constexpr int MR = kClMregs * (kClThreads / NT);  // uint4 mask registers per thread
     cg::cluster_group cluster = cg::this_cluster();
     const int r = static_cast<int>(cluster.block_rank());
     const int cs = ca.cs, n = na.n;
     const int npad = (n + 3) & ~3;
     const int wn4 = ((n + 31) / 32 + 15) & ~15;  // history words per delay plane (padded)
+    const int rs = cl_rstride(wn4);               // words between exchange ring rows
     const ClLayout L = cl_layout(n, P, D);
     uint8_t* s_code = smem + L.code;                                  // D = 0: [n][P] rotation codes
     const uint32_t* s_mask = reinterpret_cast<const uint32_t*>(smem + L.code);  // D > 0: [P][D][wn4]
@@ -614,8 +622,8 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
         const size_t bytes = L.ex - L.code;
         const uint4* src = reinterpret_cast<const uint4*>(ca.codes + static_cast<size_t>(r) * bytes);
         uint4* dst = reinterpret_cast<uint4*>(smem + L.code);
-        for (size_t k = tid; k < bytes / 16; k += kClThreads) dst[k] = __ldg(src + k);
-        for (size_t k = tid; k < (L.red - L.ex) / 4; k += kClThreads) s_ex[k] = 0u;
+        for (size_t k = tid; k < bytes / 16; k += NT) dst[k] = __ldg(src + k);
+        for (size_t k = tid; k < (L.red - L.ex) / 4; k += NT) s_ex[k] = 0u;
     }
     // exchange by st.async into every CTA's buffer, each store completing its
     // bytes on that CTA's mbarrier of the buffer: no cluster barrier and no
@@ -632,12 +640,12 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
         // ring rows of the D - 1 steps before the call, from the history words
         // the previous call left in hist2 (bit k - 1 of pre i's word = s_i[t - k])
         const uint64_t* hp = ca.hist2 + static_cast<int64_t>((t & 1) ^ 1) * n;
-        for (int i0 = warp * 32; i0 < n; i0 += kClThreads) {
+        for (int i0 = warp * 32; i0 < n; i0 += NT) {
             const int i = i0 + lane;
             const uint64_t h = i < n ? hp[i] : 0ull;
             for (int k = 1; k < D; ++k) {
                 const uint32_t b = __ballot_sync(0xffffffffu, (h >> (k - 1)) & 1ull);
-                if (lane == 0) s_ex[(((t - k) % R + R) % R) * wn4 + (i0 >> 5)] = b;
+                if (lane == 0) s_ex[(((t - k) % R + R) % R) * rs + (i0 >> 5)] = b;
             }
         }
     }
@@ -677,25 +685,39 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
     };
     stim_bounds(t);
     const WT w0 = static_cast<WT>(ca.w0);
-    // delay planes: when a thread's slice is exactly kClMregs uint4 (cfg2: 1000 pres,
+    // delay planes: when a thread's slice is exactly MR uint4 (cfg2: 1000 pres,
     // 2 threads per (post, plane)), it stays in registers for the whole call
-    uint4 mreg[kClMregs];
+    uint4 mreg[MR];
 #pragma unroll
-    for (int k = 0; k < kClMregs; ++k) mreg[k] = make_uint4(0u, 0u, 0u, 0u);
+    for (int k = 0; k < MR; ++k) mreg[k] = make_uint4(0u, 0u, 0u, 0u);
     if (D > 0 && SNB_CL_MREG) {
         constexpr int PAIRS = P * (D > 0 ? D : 1);
-        constexpr int T = kClThreads / PAIRS >= 4 ? 4 : kClThreads / PAIRS >= 2 ? 2 : 1;
-        if (tid < PAIRS * T && wn4 / T == 4 * kClMregs) {
+        constexpr int T = NT / PAIRS >= 4 ? 4 : NT / PAIRS >= 2 ? 2 : 1;
+        if (tid < PAIRS * T && wn4 / T == 4 * MR) {
             const int pi = tid / T, part = tid % T;
             const int pp = pi / (D > 0 ? D : 1), d = pi % (D > 0 ? D : 1);
             const uint4* m4 = reinterpret_cast<const uint4*>(s_mask + (pp * D + d) * wn4 + part * (wn4 / T));
 #pragma unroll
-            for (int k = 0; k < kClMregs; ++k) mreg[k] = m4[k];
+            for (int k = 0; k < MR; ++k) mreg[k] = m4[k];
         }
     }
+#ifdef SNB_CL_TRACE
+    // phase clocks of thread 0 (CTA 0): LIF + exchange issue, wait, count, barrier
+    long long tr_sum[7] = {0, 0, 0, 0, 0, 0, 0};
+    long long tr_prev = clock64();
+#define SNB_CL_MARK(k)                                       \
+    if (tid == 0) {                                          \
+        const long long now = clock64();                     \
+        tr_sum[k] += now - tr_prev;                          \
+        tr_prev = now;                                       \
+    }
+#else
+#define SNB_CL_MARK(k)
+#endif
     for (int s = 0; s < steps; ++s, ++t) {
         const int cur = D > 0 ? t % R : (t & 1);  // exchange row / buffer of this step
         if (tid == 0) mbar_arrive_expect_tx(&s_bar[cur], tx_bytes);
+        SNB_CL_MARK(4)
         if (tid < P) {  // (1) LIF update of the owned posts (k_persistent_cols' neuron phase)
             bool fired = false;
             uint64_t hn = 0;
@@ -738,20 +760,23 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
                     for (int q = 0; q < cs; ++q) st_async_u32(mapa_u32(la, q), h2, mapa_u32(lb, q));
                 }
             }
+            SNB_CL_MARK(5)
             const bool live = (r * P + warp * 32) < na.nl;  // warp-uniform
             const uint32_t word = __ballot_sync(0xffffffffu, fired);
             if (D > 0 && live && lane < cs) {  // the warp's spike word of step t into ring row t of CTA `lane`
                 const int w = (r * P) / 32 + warp;
-                const uint32_t la = smem_u32(s_ex + cur * wn4 + w), lb = smem_u32(&s_bar[cur]);
+                const uint32_t la = smem_u32(s_ex + cur * rs + w), lb = smem_u32(&s_bar[cur]);
                 st_async_u32(mapa_u32(la, lane), word, mapa_u32(lb, lane));
             }
             if (lane == 0 && na.raster && (t - na.t_base) < na.raster_rows && live)
                 na.raster[static_cast<int64_t>(t - na.t_base) * na.nl_words + ((r * P) >> 5) + warp] = word;
         }
+
         // (2) every owner's words of the step have landed in this CTA's buffer
         // (the async-proxy stores are tracked by complete_tx, so a CTA-scope wait
         // sees them, as for bulk copies; an acquire.cluster wait adds an L1
         // invalidation per step: 2.81e5 vs 2.86e5 steps/s on cfg2)
+        SNB_CL_MARK(6)
         stim_bounds(t + 1);
         if (D == 0) {
             if (cur) { mbar_wait(&s_bar[1], ph1); ph1 ^= 1u; }
@@ -761,8 +786,9 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
         if (D > 0) {
             // thread (post, delay d, part): popc(mask[post][d] & plane[d]) over its words
             constexpr int PAIRS = P * (D > 0 ? D : 1);
-            constexpr int T = kClThreads / PAIRS >= 4 ? 4 : kClThreads / PAIRS >= 2 ? 2 : 1;
-            static_assert(D == 0 || (PAIRS <= kClThreads && D * T <= 32), "cluster plane tiling");
+            constexpr int T = NT / PAIRS >= 4 ? 4 : NT / PAIRS >= 2 ? 2 : 1;
+            // (combinations with PAIRS > NT are compiled but never launched)
+            static_assert(D == 0 || PAIRS > NT || D * T <= 32, "cluster plane tiling");
             int sum = 0;
             const int pi = tid / T, part = tid % T;
             const int pp = pi / (D > 0 ? D : 1), d = pi % (D > 0 ? D : 1);
@@ -770,11 +796,11 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
             const bool pair = tid < PAIRS * T;
             auto plane_count = [&]() {
                 const int row = ((t - d) % R + R) % R;  // plane d of step t = s[t - d]
-                const uint4* e4 = reinterpret_cast<const uint4*>(s_ex + row * wn4 + part * per_part);
+                const uint4* e4 = reinterpret_cast<const uint4*>(s_ex + row * rs + part * per_part);
                 int c = 0;
-                if (SNB_CL_MREG && per_part == 4 * kClMregs) {  // mask words in registers for the call
+                if (SNB_CL_MREG && per_part == 4 * MR) {  // mask words in registers for the call
 #pragma unroll
-                    for (int k = 0; k < kClMregs; ++k) {
+                    for (int k = 0; k < MR; ++k) {
                         const uint4 m = mreg[k], e = e4[k];
                         c += __popc(m.x & e.x) + __popc(m.y & e.y) + __popc(m.z & e.z) + __popc(m.w & e.w);
                     }
@@ -789,19 +815,23 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
             };
             // planes 1..D-1 are rows of earlier steps, already here: counted while
             // this step's words are in flight; plane 0 after the row's barrier
+            SNB_CL_MARK(0)
             if (pair && d > 0) sum = plane_count();
             mbar_wait(&s_bar[cur], (phr >> cur) & 1u);
             phr ^= 1u << cur;
+            SNB_CL_MARK(1)
             if (pair && d == 0) sum = plane_count();
             if (pair) {
 #pragma unroll
                 for (int o = (D * T) / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
                 if (d == 0 && part == 0) s_in[pp] = static_cast<double>(static_cast<WT>(sum) * w0);
             }
+            SNB_CL_MARK(2)
             __syncthreads();
+            SNB_CL_MARK(3)
         } else {
-            constexpr int CG = P / 4, RL = kClThreads / CG;  // threads tid >= RL * CG idle in the sweep
-            constexpr int per = kClThreads / P >= 32 ? 32 : kClThreads / P >= 16 ? 16 : kClThreads / P >= 8 ? 8 : 4;
+            constexpr int CG = P / 4, RL = NT / CG;  // threads tid >= RL * CG idle in the sweep
+            constexpr int per = NT / P >= 32 ? 32 : NT / P >= 16 ? 16 : NT / P >= 8 ? 8 : 4;
             const int cg4 = tid % CG, rl = tid / CG;
             const uint32_t* h2c = s_ex + cur * npad;
             int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
@@ -852,6 +882,14 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_count(NeuronArgs na, 
         }
     }
     if (r == 0 && tid == 0) *na.d_step = t;
+#ifdef SNB_CL_TRACE
+    if (r == 0 && tid == 0 && steps > 0)
+        printf("cluster trace: %d steps, cycles per step: top %.0f, lif %.0f, exchange issue %.0f, stim bounds %.0f, "
+               "wait (planes 1..D-1 + barrier) %.0f, plane 0 + reduce %.0f, syncthreads %.0f\n",
+               steps, double(tr_sum[4]) / steps, double(tr_sum[5]) / steps, double(tr_sum[6]) / steps,
+               double(tr_sum[0]) / steps, double(tr_sum[1]) / steps, double(tr_sum[2]) / steps,
+               double(tr_sum[3]) / steps);
+#endif
     cluster.sync();  // no CTA leaves while a peer's last stores may target it
 }
 
@@ -1028,24 +1066,43 @@ void launch_persistent_dense(const NeuronArgs& na, const HistArgs& h, const Dens
 }
 
 
+// Threads per CTA of the cluster loop: 512 when the (post, delay) pairs fit
+// (cfg2, P = 64 x D = 8: 1.86 -> 1.69 us per step -- half the warps contend
+// for the schedulers after each exchange), else 1024.
+static int cl_threads(int P, int D) {
+    const char* e = std::getenv("SNB_CLUSTER_THREADS");  // A/B knob: 1024 keeps the wide CTAs
+    if (e && std::atoi(e) == 1024) return kClThreads;
+    return D > 0 && P * D <= 512 ? 512 : kClThreads;
+}
+
 static const void* cluster_kernel(bool f64, int P, int D) {
 #define SNB_CLK(WT, DD)                                                                  \
     switch (P) {                                                                         \
-        case 32: return reinterpret_cast<const void*>(k_cluster_count<WT, 32, DD>);      \
-        case 64: return reinterpret_cast<const void*>(k_cluster_count<WT, 64, DD>);      \
-        case 96: return reinterpret_cast<const void*>(k_cluster_count<WT, 96, DD>);      \
-        default: return reinterpret_cast<const void*>(k_cluster_count<WT, 128, DD>);     \
+        case 32: return reinterpret_cast<const void*>(k_cluster_count<WT, 32, DD, kClThreads>);      \
+        case 64: return reinterpret_cast<const void*>(k_cluster_count<WT, 64, DD, kClThreads>);      \
+        case 96: return reinterpret_cast<const void*>(k_cluster_count<WT, 96, DD, kClThreads>);      \
+        default: return reinterpret_cast<const void*>(k_cluster_count<WT, 128, DD, kClThreads>);     \
     }
     if (D == 16 && P > 64) return nullptr;  // P * D > 1024: not planned
+    // 512-thread CTAs where the (post, delay) pairs fit (cl_threads)
+    if (cl_threads(P, D) == 512) {
+#define SNB_CL5(WT)                                                                               \
+    if (D == 8) return P == 32 ? reinterpret_cast<const void*>(k_cluster_count<WT, 32, 8, 512>)   \
+                               : reinterpret_cast<const void*>(k_cluster_count<WT, 64, 8, 512>);  \
+    return reinterpret_cast<const void*>(k_cluster_count<WT, 32, 16, 512>);
+        if (f64) { SNB_CL5(double) }
+        SNB_CL5(float)
+#undef SNB_CL5
+    }
     if (f64) {
         if (D == 8) SNB_CLK(double, 8)
-        if (D == 16) return P == 32 ? reinterpret_cast<const void*>(k_cluster_count<double, 32, 16>)
-                                    : reinterpret_cast<const void*>(k_cluster_count<double, 64, 16>);
+        if (D == 16) return P == 32 ? reinterpret_cast<const void*>(k_cluster_count<double, 32, 16, kClThreads>)
+                                    : reinterpret_cast<const void*>(k_cluster_count<double, 64, 16, kClThreads>);
         SNB_CLK(double, 0)
     }
     if (D == 8) SNB_CLK(float, 8)
-    if (D == 16) return P == 32 ? reinterpret_cast<const void*>(k_cluster_count<float, 32, 16>)
-                                : reinterpret_cast<const void*>(k_cluster_count<float, 64, 16>);
+    if (D == 16) return P == 32 ? reinterpret_cast<const void*>(k_cluster_count<float, 32, 16, kClThreads>)
+                                : reinterpret_cast<const void*>(k_cluster_count<float, 64, 16, kClThreads>);
     SNB_CLK(float, 0)
 #undef SNB_CLK
 }
@@ -1077,7 +1134,7 @@ int cluster_plan(int n, int nl, bool f64, int dmax, int* P_out, int* D_out) {
                   "k_cluster_count smem attribute");
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(cs);
-            cfg.blockDim = dim3(kClThreads);
+            cfg.blockDim = dim3(cl_threads(P, D));
             cfg.dynamicSmemBytes = smem;
             cudaLaunchAttribute at{};
             at.id = cudaLaunchAttributeClusterDimension;
@@ -1124,7 +1181,7 @@ void launch_cluster_count(const NeuronArgs& na, const ClusterArgs& ca, bool f64,
     const size_t smem = cl_layout(na.n, ca.P, ca.D).total;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ca.cs);
-    cfg.blockDim = dim3(kClThreads);
+    cfg.blockDim = dim3(cl_threads(ca.P, ca.D));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute at{};
