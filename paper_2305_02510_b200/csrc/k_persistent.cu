@@ -701,6 +701,18 @@ __global__ void __launch_bounds__(NT, 1) k_cluster_count(NeuronArgs na, ClusterA
             for (int k = 0; k < MR; ++k) mreg[k] = m4[k];
         }
     }
+    // plane 0 split over a post's D lanes (one thread per (post, delay), 32-word
+    // planes): after the exchange every lane counts 4 words of plane 0 instead of
+    // the delay-0 lane counting all 32 -- the count that follows the wait is the
+    // step's critical path
+    constexpr bool SPLIT0 = D == 8 && NT / (P * (D > 0 ? D : 1)) == 1 && SNB_CL_MREG;
+    uint4 m0 = make_uint4(0u, 0u, 0u, 0u);
+    const bool split0 = SPLIT0 && wn4 == 32 && tid < P * D;
+    if (split0) {
+        constexpr int DD = D > 0 ? D : 1;
+        const int pp = tid / DD, d = tid % DD;
+        m0 = reinterpret_cast<const uint4*>(s_mask + (pp * DD + 0) * wn4)[d];
+    }
 #ifdef SNB_CL_TRACE
     // phase clocks of thread 0 (CTA 0): LIF + exchange issue, wait, count, barrier
     long long tr_sum[7] = {0, 0, 0, 0, 0, 0, 0};
@@ -820,7 +832,12 @@ __global__ void __launch_bounds__(NT, 1) k_cluster_count(NeuronArgs na, ClusterA
             mbar_wait(&s_bar[cur], (phr >> cur) & 1u);
             phr ^= 1u << cur;
             SNB_CL_MARK(1)
-            if (pair && d == 0) sum = plane_count();
+            if (split0) {
+                const uint4 e = reinterpret_cast<const uint4*>(s_ex + (t % R) * rs)[d];
+                sum += __popc(m0.x & e.x) + __popc(m0.y & e.y) + __popc(m0.z & e.z) + __popc(m0.w & e.w);
+            } else if (pair && d == 0) {
+                sum = plane_count();
+            }
             if (pair) {
 #pragma unroll
                 for (int o = (D * T) / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
