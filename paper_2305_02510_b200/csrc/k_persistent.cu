@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
 #pragma unroll
     for (int k = 0; k < kTinyHistRegs; ++k) hr[k] = (hreg && k < hw2 && j < np) ? hist[k * np + j] : 0u;
     unsigned long long spikes = 0;
+    double lv = leak_toward(v, leak, rst);  // leak(v) of the coming step
     // count mode: this post's in-list as a pre bitmask in registers, the previous
     // step's spike words double-buffered in shared memory
     __shared__ uint32_t s_spk[2][kTinyCountWords];
@@ -153,6 +154,18 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
         if ((tid & 31) == 0 && (tid >> 5) < kTinyCountWords) s_spk[0][tid >> 5] = w0;
         __syncthreads();
     }
+#ifdef SNB_TINY_TRACE
+    long long tt_sum[6] = {0, 0, 0, 0, 0, 0};
+    long long tt_prev = clock64();
+#define SNB_TT_MARK(k)                                   \
+    if (tid == 0) {                                      \
+        const long long now = clock64();                 \
+        tt_sum[k] += now - tt_prev;                      \
+        tt_prev = now;                                   \
+    }
+#else
+#define SNB_TT_MARK(k)
+#endif
     for (int s = 0; s < a.steps; ++s) {
         const int cur = s & 1;
         const uint8_t* hc = sm + L.hist + cur * hbuf;        // history through t-1
@@ -162,7 +175,7 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
             // (1) leak, incoming list in ascending pre order (bit d-1 = s_pre[t-d]),
             // the step's stimulus, threshold, refractory (mat_engine.cpp:160-198)
             // MAT: u = leak(v) + w...; ABM: pending = 0.0 + w..., u = leak(v) + (pending + ext)
-            double u = a.abm ? 0.0 : leak_toward(v, leak, rst);
+            double u = a.abm ? 0.0 : lv;
             if (cmode) {
                 int k = 0;
 #pragma unroll
@@ -177,6 +190,7 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
                     if (tiny_bit(hc, mq)) u += static_cast<double>(w[q]);  // WS = double unless STDP
                 }
             }
+            SNB_TT_MARK(3)
             int lo = st_off[s], hi = st_off[s + 1];
             if (hi > lo) {
                 double ext = 0.0;
@@ -188,7 +202,8 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
                 }
                 u += ext;
             }
-            if (a.abm) u = leak_toward(v, leak, rst) + u;
+            SNB_TT_MARK(4)
+            if (a.abm) u = lv + u;
             fired = u > thr;
             if (fired && fire_p < 1.0) fired = agent_fires(akey, t0 + s, fire_p);
             if (cnt > 0) {
@@ -202,8 +217,10 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
             } else {
                 v = u;
             }
+            lv = leak_toward(v, leak, rst);  // next step's leak, off its critical path
             if (a.trace) a.trace[static_cast<int64_t>(s) * n + j] = v;
         }
+        SNB_TT_MARK(0)
         const uint32_t word = __ballot_sync(0xffffffffu, fired);
         if ((tid & 31) == 0 && (tid >> 5) < words) {
             a.raster[static_cast<int64_t>(s) * words + (tid >> 5)] = word;
@@ -247,7 +264,9 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
                 }
             }
         }
+        SNB_TT_MARK(1)
         __syncthreads();  // the new history (and traces) of step t are complete
+        SNB_TT_MARK(2)
         if (STDP && a.plastic_on && own) {
             // (3) STDP on post j's plastic synapses: dw = 0; if s_post dw += pot^(d)_pre;
             // if s_pre[t-d+1] dw -= dep_post; clamp (mat_engine.cpp:242-249)
@@ -278,6 +297,12 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
     }
     if (spikes) atomicAdd(a.spike_count, spikes);
     if (tid == 0) *a.d_step = t0 + a.steps;
+#ifdef SNB_TINY_TRACE
+    if (tid == 0 && a.steps > 0)
+        printf("tiny trace: %d steps, cycles per step: inputs %.0f, stimulus %.0f, lif rest %.0f, raster+history %.0f, "
+               "syncthreads %.0f\n", a.steps, double(tt_sum[3]) / a.steps, double(tt_sum[4]) / a.steps,
+               double(tt_sum[0]) / a.steps, double(tt_sum[1]) / a.steps, double(tt_sum[2]) / a.steps);
+#endif
 }
 
 // Persistent single-GPU step loop for small dense nets (launch-latency bound
@@ -674,6 +699,7 @@ __global__ void __launch_bounds__(NT, 1) k_cluster_count(NeuronArgs na, ClusterA
             akey = na.agent_key[j];
         }
     }
+    double lv = leak_toward(v, leak, rst);  // leak(v) of the coming step
     int64_t slo = 0, shi = 0;                // stimulus rows of the step, fetched a step ahead
     auto stim_bounds = [&](int tt) {
         slo = shi = 0;
@@ -734,7 +760,7 @@ __global__ void __launch_bounds__(NT, 1) k_cluster_count(NeuronArgs na, ClusterA
             bool fired = false;
             uint64_t hn = 0;
             if (own) {
-                double u = na.abm ? in : leak_toward(v, leak, rst) + in;
+                double u = na.abm ? in : lv + in;
                 if (shi > slo) {
                     int64_t lo = slo, hi = shi;
                     double ext = 0.0;
@@ -746,7 +772,7 @@ __global__ void __launch_bounds__(NT, 1) k_cluster_count(NeuronArgs na, ClusterA
                     }
                     u += ext;
                 }
-                if (na.abm) u = leak_toward(v, leak, rst) + u;
+                if (na.abm) u = lv + u;
                 fired = u > thr;
                 if (fired && fire_p < 1.0) fired = agent_fires(akey, t, fire_p);
                 if (cnt > 0) {
@@ -760,6 +786,7 @@ __global__ void __launch_bounds__(NT, 1) k_cluster_count(NeuronArgs na, ClusterA
                 } else {
                     v = u;
                 }
+                lv = leak_toward(v, leak, rst);  // next step's leak, off its critical path
                 if (na.trace && (t - na.t_base) < na.raster_rows)
                     na.trace[static_cast<int64_t>(t - na.t_base) * na.nl + j] = v;
                 hn = (hprev << 1) | (fired ? 1ull : 0ull);
