@@ -403,17 +403,7 @@ __global__ void __launch_bounds__(kColThreads) k_persistent_cols(NeuronArgs na, 
             bool fired = false, act = false;
             if (own) {
                 double u = na.abm ? in : leak_toward(v, leak, rst) + in;
-                if (shi > slo) {
-                    int64_t lo = slo, hi = shi;
-                    double ext = 0.0;
-                    while (lo < hi) {
-                        const int64_t mid = (lo + hi) >> 1;
-                        const int nid = __ldg(na.st_neuron + mid);
-                        if (nid == j) { ext = __ldg(na.st_amp + mid); break; }
-                        if (nid < j) lo = mid + 1; else hi = mid;
-                    }
-                    u += ext;
-                }
+                if (shi > slo) u += stim_lookup(na.st_neuron, na.st_amp, slo, shi, j);
                 if (na.abm) u = leak_toward(v, leak, rst) + u;
                 fired = u > thr;
                 if (fired && fire_p < 1.0) fired = agent_fires(akey, t, fire_p);
@@ -761,17 +751,7 @@ __global__ void __launch_bounds__(NT, 1) k_cluster_count(NeuronArgs na, ClusterA
             uint64_t hn = 0;
             if (own) {
                 double u = na.abm ? in : lv + in;
-                if (shi > slo) {
-                    int64_t lo = slo, hi = shi;
-                    double ext = 0.0;
-                    while (lo < hi) {
-                        const int64_t mid = (lo + hi) >> 1;
-                        const int nid = __ldg(na.st_neuron + mid);
-                        if (nid == j) { ext = __ldg(na.st_amp + mid); break; }
-                        if (nid < j) lo = mid + 1; else hi = mid;
-                    }
-                    u += ext;
-                }
+                if (shi > slo) u += stim_lookup(na.st_neuron, na.st_amp, slo, shi, j);
                 if (na.abm) u = lv + u;
                 fired = u > thr;
                 if (fired && fire_p < 1.0) fired = agent_fires(akey, t, fire_p);

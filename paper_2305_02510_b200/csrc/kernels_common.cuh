@@ -128,6 +128,31 @@ __device__ __forceinline__ uint32_t bit_of(const uint32_t* bits, int i) {
     return (__ldcg(bits + (i >> 5)) >> (i & 31)) & 1u;
 }
 
+// Amplitude of neuron j in one step's stimulus row [lo, hi) (neuron ids
+// ascending, unique: the step's entries pre-summed in list order), 0 if absent.
+// Rows of up to 16 entries (the paper protocol's few driven inputs) are read
+// with all their loads in flight; longer rows are binary-searched.
+__device__ __forceinline__ double stim_lookup(const int32_t* st_neuron, const double* st_amp, int64_t lo, int64_t hi,
+                                              int j) {
+    if (hi - lo <= 16) {
+        int32_t nb[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) nb[k] = lo + k < hi ? __ldg(st_neuron + lo + k) : -1;
+        int hit = -1;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (nb[k] == j) hit = k;
+        return hit >= 0 ? __ldg(st_amp + lo + hit) : 0.0;
+    }
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        const int nid = __ldg(st_neuron + mid);
+        if (nid == j) return __ldg(st_amp + mid);
+        if (nid < j) lo = mid + 1; else hi = mid;
+    }
+    return 0.0;
+}
+
 // ---------------------------------------------------------------------------
 // History shift + windowed STDP traces for neuron i (mat_engine.cpp:200-240).
 // hist bit k (across words) = s_i[t-k]; history before step 0 is zero, so the
