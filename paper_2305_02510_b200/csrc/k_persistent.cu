@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
     for (int k = 0; k < kTinyHistRegs; ++k) hr[k] = (hreg && k < hw2 && j < np) ? hist[k * np + j] : 0u;
     unsigned long long spikes = 0;
     double lv = leak_toward(v, leak, rst);  // leak(v) of the coming step
+    const bool w0_int = a.w0 == trunc(a.w0) && fabs(a.w0) <= 1048576.0;  // integer weight below 2^20
     // count mode: this post's in-list as a pre bitmask in registers, the previous
     // step's spike words double-buffered in shared memory
     __shared__ uint32_t s_spk[2][kTinyCountWords];
@@ -182,7 +183,15 @@ __global__ void __launch_bounds__(1024, 1) k_tiny(TinyArgs a) {
                 for (int wd = 0; wd < kTinyCountWords; ++wd)
                     if (wd < a.count_words) k += __popc(cm[wd] & s_spk[cur][wd]);
                 const double w0 = a.w0;
-                for (int c = 0; c < k; ++c) u += w0;  // ascending-pre sum of equal weights
+                if (k > 0 && w0_int && u == trunc(u) && fabs(u) <= 1099511627776.0) {
+                    // integers below 2^40 plus at most 1024 integer weights below 2^20:
+                    // every partial sum of the reference's k adds is exact, so one
+                    // fma is the same double (the chain of dependent adds was the
+                    // step's longest latency)
+                    u = fma(static_cast<double>(k), w0, u);
+                } else {
+                    for (int c = 0; c < k; ++c) u += w0;  // ascending-pre sum of equal weights
+                }
             } else {
 #pragma unroll 4
                 for (uint32_t q = q0; q < q1; ++q) {
