@@ -482,6 +482,43 @@ def test_tiny_long_delays_and_edge_sizes():
             assert np.array_equal(r["weights"], o["weights"]), c.name
 
 
+@pytest.mark.parametrize("w0,leak,amp", [(2.0, 0.0, 2.0), (3.0, 0.5, 2.0), (1.0, 0.0, 2.5), (-1.0, 0.25, 3.0),
+                                          (0.5, 0.0, 2.0), (1048577.0, 0.0, 2.0)],
+                         ids=["int", "int_frac_leak", "int_frac_stim", "neg_int", "frac_w", "w_2p20"])
+def test_tiny_count_mode_exact(w0, leak, amp):
+    """k_tiny's count mode (one weight, <= 256 neurons) against the oracle,
+    bit for bit, on both sides of its exact fast path (one fma when the weight
+    is an integer below 2^20 and the running value an integer below 2^40;
+    otherwise the reference's chain of adds): integer and fractional weights,
+    leaks and stimulus amplitudes, a weight just past 2^20."""
+    from oracle import bridge as B
+    from paper_2305_02510_b200.engine import MatEngine
+    from paper_2305_02510_b200.netgen import erdos_renyi_arrays, scenario_stimulus
+    n, steps = 200, 120
+    pre, post = erdos_renyi_arrays(n, 0.08, 11)
+    thr = 2.5 if w0 < 1e6 else 3e6
+    arrays = {"threshold": np.full(n, thr), "leak": np.full(n, leak), "reset": np.zeros(n),
+              "refractory": np.full(n, 1, np.int32), "axonal": np.zeros(n, np.int32), "pre": pre, "post": post,
+              "weight": np.full(len(pre), w0), "delay": np.ones(len(pre), np.int32),
+              "stdp": np.zeros(len(pre), np.uint8)}
+    stim = scenario_stimulus(n, steps, 11, count=20, period=3, amplitude=amp if w0 < 1e6 else 3e6).to_arrays()
+    o = B.run_oracle(arrays, steps, stim)
+    e = MatEngine(storage=0, precision="f64")
+    e.add_neurons(arrays["threshold"], arrays["leak"], arrays["reset"], arrays["refractory"], arrays["axonal"])
+    e.add_synapses(pre, post, arrays["weight"], arrays["delay"], None)
+    e.setup()
+    e.add_stimulus(*stim)
+    e.simulate(steps)
+    s_, q_ = e.raster()
+    mem = e.membrane()
+    st = e.stats()
+    e.close()
+    assert st["sweep_kernel"] == TINY_KERNEL
+    assert len(o["steps"]) > 200
+    assert np.array_equal(s_, o["steps"]) and np.array_equal(q_, o["neurons"])
+    assert np.array_equal(mem.view(np.uint64), o["membrane"].view(np.uint64))
+
+
 @pytest.mark.parametrize("storage", [2, 1])
 def test_cfg4_shape_at_reduced_scale(storage):
     """cfg4's shape (1% ER, delays 1..16 keyed by pair index, unit weights) at
