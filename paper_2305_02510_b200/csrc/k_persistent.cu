@@ -699,6 +699,10 @@ __global__ void __launch_bounds__(NT, 1) k_cluster_count(NeuronArgs na, ClusterA
         }
     }
     double lv = leak_toward(v, leak, rst);  // leak(v) of the coming step
+    // exchange targets of this lane (owner warps, lane < cs): CTA `lane`'s ring
+    // and barriers, as cluster addresses
+    const uint32_t rem_ex = (D > 0 && lane < cs) ? mapa_u32(smem_u32(s_ex), lane) : 0u;
+    const uint32_t rem_bar = (D > 0 && lane < cs) ? mapa_u32(smem_u32(s_bar), lane) : 0u;
     int64_t slo = 0, shi = 0;                // stimulus rows of the step, fetched a step ahead
     auto stim_bounds = [&](int tt) {
         slo = shi = 0;
@@ -793,8 +797,9 @@ __global__ void __launch_bounds__(NT, 1) k_cluster_count(NeuronArgs na, ClusterA
             const uint32_t word = __ballot_sync(0xffffffffu, fired);
             if (D > 0 && live && lane < cs) {  // the warp's spike word of step t into ring row t of CTA `lane`
                 const int w = (r * P) / 32 + warp;
-                const uint32_t la = smem_u32(s_ex + cur * rs + w), lb = smem_u32(&s_bar[cur]);
-                st_async_u32(mapa_u32(la, lane), word, mapa_u32(lb, lane));
+                // CTA `lane`'s window, mapped once per call (offsets carry over)
+                st_async_u32(rem_ex + static_cast<uint32_t>((cur * rs + w) * 4), word,
+                             rem_bar + static_cast<uint32_t>(cur * 8));
             }
             if (lane == 0 && na.raster && (t - na.t_base) < na.raster_rows && live)
                 na.raster[static_cast<int64_t>(t - na.t_base) * na.nl_words + ((r * P) >> 5) + warp] = word;
