@@ -558,7 +558,32 @@ void Engine::simulate(int32_t steps) {
                 ka.partial = d_partial_.as<double>();
                 ka.active_count = d_spikes_.as<unsigned long long>() + 1;
                 ka.dmask = dmax_ >= 64 ? ~0ull : ((1ull << dmax_) - 1ull);
-                launch_cluster_count(na, ka, f64_, steps, stream_);
+                // a raster sink with stream_io: the call runs as 4 launches (each
+                // resumes from the state the previous one saved, like consecutive
+                // calls) and the host expands each launch's rows while the next
+                // runs (cfg2: 1M events per 1000 steps)
+                const bool overlap = sink_ && opt_.stream_io && raster && !opt_.profile && steps >= 256;
+                if (!overlap) {
+                    launch_cluster_count(na, ka, f64_, steps, stream_);
+                } else {
+                    const int chunk = (steps + 3) / 4;
+                    std::vector<std::pair<int, cudaEvent_t>> ends;
+                    for (int done = 0; done < steps; done += chunk) {
+                        const int k = std::min(chunk, steps - done);
+                        launch_cluster_count(na, ka, f64_, k, stream_);
+                        cudaEvent_t e = get_event();
+                        cuda_check(cudaEventRecord(e, stream_), "rec");
+                        ends.emplace_back(k, e);
+                    }
+                    stats_.kernel_launches += static_cast<int64_t>(ends.size()) - 1;
+                    int row = 0;
+                    for (auto& e : ends) {
+                        cuda_check(cudaEventSynchronize(e.second), "chunk sync");
+                        sink_rows(na.raster + static_cast<size_t>(row) * nl_words_, e.first, na.t_base + row);
+                        row += e.first;
+                        cudaEventDestroy(e.second);
+                    }
+                }
             } else if (cols_) {
                 ColArgs ca{};
                 ca.hist2 = d_hist2_.as<uint64_t>();

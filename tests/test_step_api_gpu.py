@@ -254,3 +254,34 @@ def test_empty_network_runs_like_the_reference():
     with pytest.raises(ValueError, match=r"stimulus\[0\]: neuron id 0 out of range \(0 neurons\)"):
         sn.mat_run(net, sn.SimulationConfig(steps=3),
                    sn.StimulusSchedule([sn.StimulusEntry(0, 0, 1.0)]))
+
+
+def test_cluster_loop_simulate_raster_in_launch_chunks():
+    """The cluster loop (cfg2's plan) under sn_simulate_raster with stream_io
+    runs a long call as 4 launches and expands each launch's rows while the
+    next runs; the events equal simulate + raster of an engine without
+    stream_io, across calls of different lengths."""
+    from paper_2305_02510_b200.engine import MatEngine
+    from paper_2305_02510_b200.netgen import scenario_stimulus
+
+    def make(io):
+        e = MatEngine(storage=1, stream_io=io)
+        e.generate_erdos_renyi(1000, 1.0, 0, delay_max=8, delay_by_synapse_index=True)
+        e.setup()
+        e.add_stimulus(*scenario_stimulus(1000, 1300, 0).to_arrays())
+        return e
+
+    a = make(False)
+    for k in (700, 300, 257):
+        a.simulate(k)
+    s_ref, q_ref = a.raster()
+    assert a.stats()["sweep_kernel"] == 14
+    a.close()
+    b = make(True)
+    parts = [b.simulate_raster(k) for k in (700, 300, 257)]
+    assert b.stats()["sweep_kernel"] == 14
+    b.close()
+    s = np.concatenate([p[0] for p in parts])
+    q = np.concatenate([p[1] for p in parts])
+    assert len(s_ref) > 100000
+    assert np.array_equal(s, s_ref) and np.array_equal(q, q_ref)
