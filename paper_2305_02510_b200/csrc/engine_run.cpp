@@ -2,6 +2,9 @@
 // step chunks, persistent / tiny loops, stream I/O and the host-driven
 // partition steps (sn_step_local / sn_step_finish).
 #include "engine.hpp"
+
+#include <chrono>
+#include <cstdio>
 #include "engine_util.hpp"
 #include "nccl_dl.hpp"
 
@@ -369,8 +372,16 @@ double Engine::run_graph_chunks(const NeuronArgs& na, int steps) {
         cudaGraphDestroy(g);
         return ge;
     };
+#ifdef SNB_TIME_CAPTURE
+    const auto c0 = std::chrono::steady_clock::now();
+#endif
     cudaGraphExec_t full = capture(chunk);
     cudaGraphExec_t tail = (steps % chunk) ? capture(steps % chunk) : nullptr;
+#ifdef SNB_TIME_CAPTURE
+    std::fprintf(stderr, "graph capture+instantiate: %.1f us for %d + %d steps\n",
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - c0).count(), chunk,
+                 steps % chunk);
+#endif
     const int per_step_kernels = (fused || fold_hist()) ? 2 : 3;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spans;
     double total = 0.0;
@@ -403,9 +414,20 @@ double Engine::run_graph_chunks(const NeuronArgs& na, int steps) {
     if (overlap) {  // every chunk is queued: decode each as its end event fires
         int row = 0;
         for (auto& sp : spans) {
+#ifdef SNB_TIME_CAPTURE
+            const auto w0 = std::chrono::steady_clock::now();
+#endif
             cuda_check(cudaEventSynchronize(sp.second), "chunk sync");
+#ifdef SNB_TIME_CAPTURE
+            const auto w1 = std::chrono::steady_clock::now();
+#endif
             const int k = std::min(chunk, steps - row);
             sink_rows(na.raster + static_cast<size_t>(row) * nl_words_, k, na.t_base + row);
+#ifdef SNB_TIME_CAPTURE
+            std::fprintf(stderr, "chunk %d rows: waited %.1f us, decoded in %.1f us\n", k,
+                         std::chrono::duration<double, std::micro>(w1 - w0).count(),
+                         std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w1).count());
+#endif
             row += k;
         }
     }
@@ -673,21 +695,31 @@ void Engine::sink_rows(const uint32_t* rows, int32_t nrows, int32_t t_first) {
         const int lo = lim - w * 32;
         return lo >= 32 ? row[w] : lo <= 0 ? 0u : (row[w] & ((1u << lo) - 1u));
     };
-    std::vector<int64_t> start(static_cast<size_t>(nrows) + 1, 0);
-    for (int r = 0; r < nrows; ++r) {
-        const uint32_t* row = rows + static_cast<size_t>(r) * nl_words_;
+    // work units: (row, word segment), enough of them for every thread even
+    // when a chunk has few rows (the last chunk of a call is on the critical path)
+    const unsigned hw = static_cast<unsigned>(host_threads());
+    const int segs = std::max(1, std::min<int>(std::max(1, nl_words_ / 256),
+                                                (static_cast<int>(hw) + nrows - 1) / std::max(1, nrows)));
+    const int seg_words = (nl_words_ + segs - 1) / segs;
+    const int units = nrows * segs;
+    std::vector<int64_t> start(static_cast<size_t>(units) + 1, 0);
+    for (int u = 0; u < units; ++u) {
+        const uint32_t* row = rows + static_cast<size_t>(u / segs) * nl_words_;
+        const int w0 = (u % segs) * seg_words, w1 = std::min(nl_words_, w0 + seg_words);
         int64_t c = 0;
-        for (int w = 0; w < nl_words_; ++w) c += __builtin_popcount(word_of(row, w));
-        start[r + 1] = start[r] + c;
+        for (int w = w0; w < w1; ++w) c += __builtin_popcount(word_of(row, w));
+        start[u + 1] = start[u] + c;
     }
-    if (k.count + start[nrows] > k.cap)
+    if (k.count + start[units] > k.cap)
         throw InvalidArgument("sn_simulate_raster: capacity " + std::to_string(k.cap) + " < " +
-                              std::to_string(k.count + start[nrows]) + " events");
+                              std::to_string(k.count + start[units]) + " events");
     auto expand = [&](int a, int b) {
-        for (int r = a; r < b; ++r) {
+        for (int u = a; u < b; ++u) {
+            const int r = u / segs;
             const uint32_t* row = rows + static_cast<size_t>(r) * nl_words_;
-            int64_t o = k.count + start[r];
-            for (int w = 0; w < nl_words_; ++w)
+            const int w0 = (u % segs) * seg_words, w1 = std::min(nl_words_, w0 + seg_words);
+            int64_t o = k.count + start[u];
+            for (int w = w0; w < w1; ++w)
                 for (uint32_t x = word_of(row, w); x; x &= x - 1) {
                     k.steps[o] = t_first + r;
                     k.neurons[o] = first_ + w * 32 + __builtin_ctz(x);
@@ -695,21 +727,23 @@ void Engine::sink_rows(const uint32_t* rows, int32_t nrows, int32_t t_first) {
                 }
         }
     };
-    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     const int nthreads = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({static_cast<int64_t>(hw),
-                                                                               start[nrows] / 65536, nrows})));
+                                                                               start[units] / 65536, units})));
     if (nthreads == 1) {
-        expand(0, nrows);
+        expand(0, units);
     } else {
-        std::vector<std::thread> pool;
-        const int per = (nrows + nthreads - 1) / nthreads;
-        for (int i = 0; i < nthreads; ++i) {
-            const int a = i * per, b = std::min(nrows, a + per);
-            if (a < b) pool.emplace_back(expand, a, b);
+        // contiguous unit ranges of about equal event counts, on the host pool
+        std::vector<int> cut(static_cast<size_t>(nthreads) + 1, units);
+        cut[0] = 0;
+        for (int i = 1; i < nthreads; ++i) {
+            const int64_t target = start[units] * i / nthreads;
+            int u1 = cut[i - 1];
+            while (u1 < units && start[u1] < target) ++u1;
+            cut[i] = u1;
         }
-        for (auto& th : pool) th.join();
+        host_parallel(nthreads, [&](int i) { expand(cut[i], cut[i + 1]); });
     }
-    k.count += start[nrows];
+    k.count += start[units];
     k.rows_done += nrows;
 }
 

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <functional>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -12,6 +13,11 @@
 #include <nvtx3/nvToolsExt.h>
 
 namespace snb {
+
+// host_pool.cpp: f(0..n-1) on a persistent pool of host threads (and the caller)
+int host_threads();
+void host_parallel(int n, const std::function<void(int)>& f);
+
 namespace {
 
 // NVTX range for the host phases of the engine (setup, simulate, graph
