@@ -476,6 +476,10 @@ void Engine::plan_launches() {
         // dictionary lists are half as long in bytes; more posts per warp hide
         // more latency (cfg4, 160 entries/list: SUB 16 0.720 ms, 8 0.682, 4 0.652)
         if (!dict_.empty()) sub_ = avg >= 1024 ? 16 : avg >= 384 ? 8 : 4;
+        // plastic lists with staged traces, ~30 synapses per (post, block): 2 lanes
+        // x 4 chunks per post, 16 posts per warp in flight (sstdp1 0.376 vs 0.379 ms,
+        // sstdp8 0.527 vs 0.550 at SUB 4)
+        if (stdp_on_ && pot_staged_ && dict_.empty() && !exact_ && avg < 40) sub_ = 2;
         // one-weight lists (k_sparse_count): 8 lanes per post read whole 128-byte
         // lines (4 posts per warp-wide LDG.128); cfg4, 160 entries per list:
         // SUB 8 0.514 ms vs SUB 4 0.529 ms, 16 0.678
@@ -486,7 +490,9 @@ void Engine::plan_launches() {
             sub_ = avg >= 768 ? 8 : 4;
         if (const char* sv = std::getenv("SNB_SPARSE_SUB")) {  // A/B knob: lanes per post
             const int v = std::atoi(sv);
-            if (v == 4 || v == 8 || v == 16 || v == 32 || (!dict_.empty() && (v == 1 || v == 2))) sub_ = v;
+            if (v == 4 || v == 8 || v == 16 || v == 32 || (!dict_.empty() && v == 1) ||
+                (v == 2 && (!dict_.empty() || (stdp_on_ && pot_staged_))))
+                sub_ = v;
         }
         // default: SUB lanes per post (k_sparse_pull, 1.058 ms on cfg4); the flat
         // per-warp chunk stream (k_sparse_stream, 1.115 ms) stays selectable for

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kThreads, SNB_SPARSE_MINB) k_sparse_pull(Spars
 #ifndef SNB_SPARSE_UL
 #define SNB_SPARSE_UL 8
 #endif
-    constexpr int UL = DICT ? (SUB <= 8 ? SNB_SPARSE_UL : 4) : 2;
+    constexpr int UL = DICT ? (SUB <= 8 ? SNB_SPARSE_UL : 4) : (SUB <= 2 ? 4 : 2);
     const int stride = (kThreads / 32) * PER_WARP;
     const int64_t* offb = a.off + static_cast<int64_t>(b) * a.nl;
     int p = p0 + warp * PER_WARP + sg;
@@ -1378,6 +1378,7 @@ static void sparse_go_sub(const SparseArgs& a, int sub, int gx, size_t smem, cud
     }
     if (STDP && a.pot_staged) {
         switch (sub) {
+            case 2: go(k_sparse_pull<WT, STDP, HB, 2, false, true>); return;
             case 4: go(k_sparse_pull<WT, STDP, HB, 4, false, true>); return;
             case 8: go(k_sparse_pull<WT, STDP, HB, 8, false, true>); return;
             case 16: go(k_sparse_pull<WT, STDP, HB, 16, false, true>); return;
